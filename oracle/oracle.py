@@ -1,0 +1,303 @@
+"""TEST INFRASTRUCTURE ONLY - Python driver for the plain C oracle.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs may import this module.  It sequences the C
+functions of ``tsat_oracle.c`` into one TurboSAT iteration in the paper's
+order (Fig. 3, §3.2, §4.1):
+
+  Eq. 5 normalise -> Eq. 2 binarise -> Eq. 1 R = PA -> §3.1.4 hard S / unsat
+  -> Eq. 4 SmoothMin, Eq. 3 loss -> STE backward (P^T) -> Eq. 5 Jacobian
+  -> AdamW with the §4.1 LR schedule.
+
+Selection and export (§4.2) are a stable sort here
+(numpy.lexsort), the plain definition.
+
+Sharding: every cross-candidate reduction (Q, I, gmax, thmax, S, best) goes
+through ``self.comm`` (``LocalComm``: identity).  tests/ substitute a
+torch.distributed (gloo) or thread-barrier communicator to prove that a
+candidate-sharded run equals the unsharded one.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import math
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "tsat_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (gcc -O2 -ffp-contract=off)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ct.CDLL(build())
+        P = ct.c_void_p
+        i32, i64, u64, f64, f32 = ct.c_int, ct.c_int64, ct.c_uint64, ct.c_double, ct.c_float
+        sig = {
+            "or_philox4x32_10": (None, [P, P, P]),
+            "or_init": (None, [i32, i64, i32, u64, P, P, P]),
+            "or_row_sums": (i32, [i32, i32, P, P]),
+            "or_row_finish": (None, [i32, i64, P, i32, f64, P, P, P, P]),
+            "or_binarize": (None, [i32, i32, P, P, P]),
+            "or_clause_eval": (None, [i32, P, P, i32, P, P]),
+            "or_histogram": (None, [i32, i32, i32, P, P]),
+            "or_smoothmin": (None, [i32, i32, P, P, f64, P, P, P]),
+            "or_smoothmin_direct": (f64, [i32, P, f64]),
+            "or_backward": (None, [i32, i32, P, P, i32, i32, P, P, P]),
+            "or_jacobian_partial": (None, [i32, i32, P, P, P, i64, f64, f32, P, P, P]),
+            "or_jacobian_finish": (None, [i32, i64, P, P, P, P, P, i32, P, P]),
+            "or_grad": (None, [i32, i32, P, P, P, P]),
+            "or_lr_at": (f64, [i64, f64, f64, i32, i32, f64]),
+            "or_adamw": (None, [i32, i64, i32, P, P, P, P, i64, f64, f64, f64, f64, f64, f64, u64]),
+            "or_abs_max": (f32, [ct.c_size_t, P]),
+            "or_gmax": (f64, [i32, i32, P, P]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(_lib, name)
+            fn.restype = res
+            fn.argtypes = args
+    return _lib
+
+
+def _p(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(ct.c_void_p)
+
+
+# ---------------------------------------------------------------- pieces
+def philox(ctr, key):
+    c = np.array(ctr, dtype=np.uint32)
+    k = np.array(key, dtype=np.uint32)
+    out = np.zeros(4, dtype=np.uint32)
+    lib().or_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def init_theta(V, N, seed, n0=0, Nl=None):
+    Nl = N if Nl is None else Nl
+    th = np.empty((V, Nl), np.float32)
+    m = np.empty((V, Nl), np.float32)
+    v = np.empty((V, Nl), np.float32)
+    lib().or_init(V, n0, Nl, seed, _p(th), _p(m), _p(v))
+    return th, m, v
+
+
+def lr_at(t, cfg):
+    return lib().or_lr_at(t, cfg.lr0, cfg.decay_factor, cfg.decay_every, cfg.restart_every, cfg.lr_min)
+
+
+def clause_eval(cnf, b):
+    Nl = b.shape[1]
+    R = np.empty((cnf.C, Nl), np.uint8)
+    lib().or_clause_eval(cnf.C, _p(cnf.clause_ptr), _p(cnf.lits), Nl, _p(np.ascontiguousarray(b, np.uint8)), _p(R))
+    return R
+
+
+def histogram(R, K):
+    C, Nl = R.shape
+    h = np.empty((Nl, K + 1), np.int32)
+    lib().or_histogram(C, Nl, K, _p(R), _p(h))
+    return h
+
+
+def exp_table(tau, K):
+    """E[d] = exp(-tau d), d = 0..K (host libm; R11)."""
+    return np.array([math.exp(-tau * d) for d in range(K + 1)], dtype=np.float64)
+
+
+def smoothmin(h, tau):
+    Nl, K1 = h.shape
+    K = K1 - 1
+    E = exp_table(tau, K)
+    S = np.empty(Nl, np.float64)
+    g = np.empty((Nl, K1), np.float64)
+    rmin = np.empty(Nl, np.int32)
+    lib().or_smoothmin(Nl, K, _p(np.ascontiguousarray(h, np.int32)), _p(E), tau, _p(S), _p(g), _p(rmin))
+    return S, g, rmin
+
+
+def smoothmin_direct(col, tau):
+    c = np.ascontiguousarray(col, np.int32)
+    return lib().or_smoothmin_direct(len(c), _p(c), tau)
+
+
+def backward(cnf, R, g):
+    Nl = R.shape[1]
+    K = g.shape[1] - 1
+    G = np.empty((cnf.V, Nl), np.float64)
+    lib().or_backward(cnf.V, cnf.C, _p(cnf.clause_ptr), _p(cnf.lits), Nl, K, _p(R), _p(np.ascontiguousarray(g)), _p(G))
+    return G
+
+
+def compute_k(V: int) -> int:
+    """k = 0.01% of V, at least 20, at most V (R13 ceil)."""
+    return min(V, max(-(-V // 10000), 20))
+
+
+def select_top(unsat: np.ndarray, M: int, n0: int = 0):
+    """Top-M candidates by (unsat asc, index asc) (R15)."""
+    idx = np.arange(len(unsat), dtype=np.int64) + n0
+    order = np.lexsort((idx, unsat))
+    return idx[order[:M]], unsat[order[:M]]
+
+
+def export_partial(absG_col: np.ndarray, bits_col: np.ndarray, k: int):
+    """k variables with smallest |G| (ties -> lower v), most confident first
+    (R14, R15).  Returns signed 1-based DIMACS literals."""
+    v = np.arange(len(absG_col), dtype=np.int64)
+    order = np.lexsort((v, absG_col))[:k]
+    lits = np.where(bits_col[order] == 1, order + 1, -(order + 1)).astype(np.int32)
+    return lits, absG_col[order]
+
+
+# ---------------------------------------------------------------- config
+@dataclass
+class Config:
+    tau: float = 1.0
+    normalize: int = 1
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 1e-2
+    lr0: float = 1e-1
+    lr_min: float = 1e-15
+    decay_factor: float = 10.0
+    decay_every: int = 30
+    restart_every: int = 360
+    noise_sigma: float = 0.0
+    eps_norm: float = 1e-8
+
+
+class LocalComm:
+    """Single-shard communicator: every reduction is the identity."""
+
+    def sum_i64(self, a):
+        return a
+
+    def max(self, x):
+        return x
+
+    def min_key(self, k):
+        return k
+
+    def gather_f64(self, a):
+        return a
+
+
+@dataclass
+class StepOut:
+    t: int
+    bits: np.ndarray          # evaluated state b_t (V x Nl, uint8)
+    R: np.ndarray             # C x Nl
+    h: np.ndarray             # Nl x (K+1)
+    unsat: np.ndarray         # Nl
+    S: np.ndarray             # Nl
+    g: np.ndarray             # Nl x (K+1)
+    loss: float               # -sum_n S_n over ALL candidates
+    G: np.ndarray             # V x Nl (pre-Jacobian variable gradient)
+    grad: np.ndarray          # V x Nl fp32 (post-Jacobian)
+    J: np.ndarray
+    d: np.ndarray
+    gmax: float
+    thmax: float
+    best_unsat: int
+    best_idx: int
+    lr: float
+    extra: dict = field(default_factory=dict)
+
+
+class Oracle:
+    """One TurboSAT batch on the CPU: state theta, m, v (fp32, V x Nl) for the
+    candidate shard [n0, n0 + Nl) of N global candidates."""
+
+    def __init__(self, cnf, N, seed, cfg: Config | None = None, n0=0, Nl=None, init=True):
+        self.cnf = cnf
+        self.N = int(N)
+        self.n0 = int(n0)
+        self.Nl = self.N if Nl is None else int(Nl)
+        self.seed = int(seed)
+        self.cfg = cfg or Config()
+        self.K = cnf.K
+        self.t = 0
+        lits = np.abs(cnf.lits.astype(np.int64)) - 1
+        self.occ = np.bincount(lits, minlength=cnf.V).astype(np.int32)
+        if init:
+            self.theta, self.m, self.v = init_theta(cnf.V, self.N, self.seed, self.n0, self.Nl)
+        self.comm = LocalComm()
+
+    def set_state(self, theta, m, v, t):
+        self.theta = np.ascontiguousarray(theta, np.float32).copy()
+        self.m = np.ascontiguousarray(m, np.float32).copy()
+        self.v = np.ascontiguousarray(v, np.float32).copy()
+        self.t = int(t)
+
+    def row_stats(self):
+        V = self.cnf.V
+        Q = np.empty(V, np.int64)
+        L = lib()
+        L.or_row_sums(V, self.Nl, _p(self.theta), _p(Q))
+        Q = self.comm.sum_i64(Q)
+        thmax_local = float(np.abs(self.theta).max()) if self.theta.size else 0.0
+        assert self.N * thmax_local < 2.0 ** 30, "row-sum fixed-point bound (R10)"
+        mu = np.empty(V); d = np.empty(V); rho = np.empty(V); guard = np.empty(V, np.uint8)
+        L.or_row_finish(V, self.N, _p(Q), self.cfg.normalize, self.cfg.eps_norm, _p(mu), _p(d), _p(rho), _p(guard))
+        return Q, mu, d, rho, guard
+
+    def step(self) -> StepOut:
+        cnf, cfg, L = self.cnf, self.cfg, lib()
+        V, Nl, K = cnf.V, self.Nl, self.K
+        t = self.t
+        # Eq. 5 normalisation statistics and Eq. 2 binarisation
+        Q, mu, d, rho, guard = self.row_stats()
+        b = np.empty((V, Nl), np.uint8)
+        L.or_binarize(V, Nl, _p(self.theta), _p(d), _p(b))
+        # Eq. 1 and §3.1.4
+        R = clause_eval(cnf, b)
+        h = histogram(R, K)
+        unsat = h[:, 0].copy()
+        # Eq. 4 / Eq. 3
+        S, g, rmin = smoothmin(h, cfg.tau)
+        Sall = self.comm.gather_f64(S)
+        loss = -float(sum(float(x) for x in Sall))
+        gmax = self.comm.max(L.or_gmax(Nl, K, _p(g), _p(rmin)))
+        thmax = self.comm.max(L.or_abs_max(self.theta.size, _p(self.theta)))
+        # STE backward and Eq. 5 Jacobian
+        G = backward(cnf, R, g)
+        I = np.empty(V, np.int64); s = np.empty(V, np.int32); valid = np.empty(V, np.uint8)
+        L.or_jacobian_partial(V, Nl, _p(G), _p(self.theta), _p(self.occ), self.N, gmax, thmax, _p(I), _p(s), _p(valid))
+        I = self.comm.sum_i64(I)
+        J = np.empty(V); cv = np.empty(V)
+        L.or_jacobian_finish(V, self.N, _p(I), _p(s), _p(valid), _p(rho), _p(guard), cfg.normalize, _p(J), _p(cv))
+        grad = np.empty((V, Nl), np.float32)
+        L.or_grad(V, Nl, _p(G), _p(rho), _p(cv), _p(grad))
+        # selection (§4.2): best = argmin (unsat, n)
+        j = int(np.lexsort((np.arange(Nl), unsat))[0]) if Nl else 0
+        key = (int(unsat[j]), self.n0 + j)
+        best_unsat, best_idx = self.comm.min_key(key)
+        # AdamW + LR schedule (§4.1)
+        lr = lr_at(t, cfg)
+        L.or_adamw(V, self.n0, Nl, _p(self.theta), _p(self.m), _p(self.v), _p(grad), t, lr,
+                   cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, cfg.noise_sigma, self.seed)
+        self.t = t + 1
+        return StepOut(t=t, bits=b, R=R, h=h, unsat=unsat, S=S, g=g, loss=loss, G=G, grad=grad,
+                       J=J, d=d, gmax=gmax, thmax=thmax, best_unsat=best_unsat, best_idx=best_idx,
+                       lr=lr, extra=dict(Q=Q, mu=mu, rho=rho, guard=guard, cv=cv, rmin=rmin, I=I, s=s))

@@ -1,0 +1,408 @@
+/*
+ * tsat_oracle.c - TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, single-threaded CPU oracle of TurboSAT's batched
+ * differentiable SAT step (arXiv 2511.07737, /root/reference/PAPER.md), used
+ * to prove the CUDA path (paper_2511_07737_b200/) correct.  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+ * may load it.  It shares NO code with the CUDA path (no headers, helpers or
+ * tables); the only common inputs come from tsat_synth/ (seeded instances).
+ *
+ * Build: gcc -O2 -ffp-contract=off -fPIC -shared -o liboracle.so tsat_oracle.c -lm
+ * (-ffp-contract=off: every floating operation below is a separate IEEE
+ *  round-to-nearest op; fused multiply-adds appear only as explicit fmaf()).
+ *
+ * Notation follows the paper: V variables, C clauses, N candidate
+ * assignments; theta = A_real (one parameter per variable and candidate,
+ * DESIGN.md reading R2); R = P A (Eq. 1); B = clip(sign, 0, 1) (Eq. 2);
+ * L = -sum S_i (Eq. 3); S_i = SmoothMin (Eq. 4); Eq. 5 per-variable
+ * normalisation; AdamW + step-decay LR with restarts (§4.1).
+ * Array layouts: theta/m/v/G/b are [V][N] row-major (candidate fastest);
+ * R is [C][N]; h and g are [N][K+1].
+ *
+ * Where the paper is silent the readings are DESIGN.md §"Readings" R1..R25.
+ * Parity pins: tests/test_oracle_pins.py.  "parity unpinned": none of the
+ * functions below; trajectory QUALITY (steps-to-SAT) is unpinned.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ */
+/* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11).  Counter-based RNG  */
+/* used for (a1) init (§4.1 l.250: "random values from the      */
+/* standard normal distribution") and the optional noise hook (R17).     */
+/* ------------------------------------------------------------------ */
+void or_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int round = 0; round < 10; ++round) {
+        uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* (a1) Init, §4.1 l.250-252.  theta_vn ~ N(0,1): Philox keyed by
+ * seed, counter (n>>2, v, 0, 0) over the GLOBAL candidate index n, then
+ * Box-Muller on the pairs (x0,x1), (x2,x3): u1 = (x+1) 2^-32 in (0,1],
+ * u2 = x 2^-32, z = sqrt(-2 ln u1) {cos,sin}(2 pi u2) in fp64 -> fp32.
+ * m = v = 0.  Candidates [n0, n0+Nl) are produced (a shard). */
+void or_init(int V, int64_t n0, int Nl, uint64_t seed, float* theta, float* m, float* vv)
+{
+    const double two_pi = 6.283185307179586;
+    const double two_m32 = 2.3283064365386963e-10; /* 2^-32 */
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    for (int v = 0; v < V; ++v) {
+        for (int j = 0; j < Nl; ++j) {
+            int64_t n = n0 + j;
+            uint32_t ctr[4] = {(uint32_t)(n >> 2), (uint32_t)v, 0u, 0u};
+            uint32_t x[4];
+            or_philox4x32_10(ctr, key, x);
+            int q = (int)(n & 3);
+            int pair = q >> 1;
+            double u1 = ((double)x[2 * pair] + 1.0) * two_m32;
+            double u2 = (double)x[2 * pair + 1] * two_m32;
+            double r = sqrt(-2.0 * log(u1));
+            double a = two_pi * u2;
+            double z = (q & 1) ? r * sin(a) : r * cos(a);
+            theta[(size_t)v * Nl + j] = (float)z;
+            m[(size_t)v * Nl + j] = 0.0f;
+            vv[(size_t)v * Nl + j] = 0.0f;
+        }
+    }
+}
+
+/* ------------------------------------------------------------------ */
+/* (a2) Eq. 5 row statistics (§4.1 l.262-269).                   */
+/* The row mean is taken over ALL N candidates (R20).  The sum is exact: */
+/* Q_v = sum_n round_half_even(theta_vn 2^32) in int64 (R10), so any     */
+/* partition of the candidates gives the same Q_v.                       */
+/* ------------------------------------------------------------------ */
+int or_row_sums(int V, int Nl, const float* theta, int64_t* Q)
+{
+    for (int v = 0; v < V; ++v) {
+        int64_t s = 0;
+        for (int j = 0; j < Nl; ++j) {
+            double x = (double)theta[(size_t)v * Nl + j] * 4294967296.0; /* exact */
+            s += (int64_t)llrint(x);
+        }
+        Q[v] = s;
+    }
+    return 0;
+}
+
+/* mu_v = (Q_v 2^-32)/N; d_v = sign(mu_v) max(|mu_v|, eps), sign(0)=+1;
+ * rho_v = 1/d_v (R3: x/mu computed as x * (1/mu)); guard_v = |mu_v| <= eps.
+ * normalize == 0 (variant, R20): d = rho = 1, guard = 1. */
+void or_row_finish(int V, int64_t N, const int64_t* Q, int normalize, double eps_norm,
+                   double* mu, double* d, double* rho, uint8_t* guard)
+{
+    for (int v = 0; v < V; ++v) {
+        if (!normalize) {
+            mu[v] = 0.0; d[v] = 1.0; rho[v] = 1.0; guard[v] = 1;
+            continue;
+        }
+        double m_ = ((double)Q[v] * 2.3283064365386963e-10) / (double)N;
+        double a = fabs(m_);
+        double mag = a > eps_norm ? a : eps_norm;
+        mu[v] = m_;
+        d[v] = (m_ >= 0.0) ? mag : -mag;
+        rho[v] = 1.0 / d[v];
+        guard[v] = (a <= eps_norm) ? 1 : 0;
+    }
+}
+
+/* (a3) Eq. 2, A = B(A_real^norm) = clip(sign(theta/d), 0, 1), evaluated by
+ * sign logic (no division): b = (theta>0 && d>0) || (theta<0 && d<0).
+ * theta = 0 gives 0 (R5). */
+void or_binarize(int V, int Nl, const float* theta, const double* d, uint8_t* b)
+{
+    for (int v = 0; v < V; ++v)
+        for (int j = 0; j < Nl; ++j) {
+            float x = theta[(size_t)v * Nl + j];
+            b[(size_t)v * Nl + j] = (uint8_t)((x > 0.0f && d[v] > 0.0) || (x < 0.0f && d[v] < 0.0));
+        }
+}
+
+/* (a4) Eq. 1, R = P A: R_cn = number of literals of clause c that candidate n
+ * sets true (§3.1.3 l.161-167).  Positive literal +v takes b_vn, negative -v
+ * takes 1 - b_vn (§3.1.2 l.155-158).  Literals are signed 1-based DIMACS. */
+void or_clause_eval(int C, const int64_t* cptr, const int32_t* lits, int Nl,
+                    const uint8_t* b, uint8_t* R)
+{
+    for (int c = 0; c < C; ++c) {
+        uint8_t* row = R + (size_t)c * Nl;
+        for (int j = 0; j < Nl; ++j) row[j] = 0;
+        for (int64_t l = cptr[c]; l < cptr[c + 1]; ++l) {
+            int32_t lit = lits[l];
+            int v = (lit > 0 ? lit : -lit) - 1;
+            const uint8_t* brow = b + (size_t)v * Nl;
+            for (int j = 0; j < Nl; ++j) {
+                uint8_t val = lit > 0 ? brow[j] : (uint8_t)(1 - brow[j]);
+                row[j] = (uint8_t)(row[j] + val);
+            }
+        }
+    }
+}
+
+/* (a5) §3.1.4: per candidate the number of clauses with R_cn = r, r=0..K.
+ * unsat_n = h_n[0]; the hard S_n (column minimum) is the least r with h>0. */
+void or_histogram(int C, int Nl, int K, const uint8_t* R, int32_t* h)
+{
+    for (int j = 0; j < Nl * (K + 1); ++j) h[j] = 0;
+    for (int c = 0; c < C; ++c)
+        for (int j = 0; j < Nl; ++j) h[(size_t)j * (K + 1) + R[(size_t)c * Nl + j]] += 1;
+}
+
+/* (a6) Eq. 4 SmoothMin and its derivative, per candidate.
+ * R takes only the integer values 0..K, so the C-term sums of Eq. 4 group
+ * exactly into K+1 terms (R11): with E[d] = exp(-tau d) (host libm) and the
+ * max-shift by rmin,
+ *   den = sum_{r>=rmin} h_r E[r-rmin],  num = sum_{r>=rmin} (r h_r) E[r-rmin],
+ *   S = num/den,
+ *   dS/dR at value r: g[r] = (E[r-rmin]/den) (1 - tau (r - S))  (r >= rmin).
+ * (The derivative of sum R w / sum w with w = e^{-tau R}.)  Sums ascending r.
+ * Returns via S[n], g[n*(K+1)+r], rmin[n]. */
+void or_smoothmin(int Nl, int K, const int32_t* h, const double* E, double tau,
+                  double* S, double* g, int32_t* rmin_out)
+{
+    for (int j = 0; j < Nl; ++j) {
+        const int32_t* hn = h + (size_t)j * (K + 1);
+        double* gn = g + (size_t)j * (K + 1);
+        int rmin = 0;
+        while (rmin <= K && hn[rmin] == 0) ++rmin;
+        for (int r = 0; r <= K; ++r) gn[r] = 0.0;
+        if (rmin > K) { /* C == 0: no clauses, nothing to minimise */
+            S[j] = 0.0; rmin_out[j] = 0;
+            continue;
+        }
+        double den = 0.0, num = 0.0;
+        for (int r = rmin; r <= K; ++r) {
+            den = den + (double)hn[r] * E[r - rmin];
+            num = num + (double)((int64_t)r * (int64_t)hn[r]) * E[r - rmin];
+        }
+        double s = num / den;
+        for (int r = rmin; r <= K; ++r) {
+            double w = E[r - rmin] / den;
+            double u = (double)r - s;
+            gn[r] = w * (1.0 - tau * u);
+        }
+        S[j] = s;
+        rmin_out[j] = rmin;
+    }
+}
+
+/* Eq. 4 written out over the C entries of one column (pin helper): shift by
+ * the column minimum, sum in clause order. */
+double or_smoothmin_direct(int C, const int32_t* Rcol, double tau)
+{
+    int mn = Rcol[0];
+    for (int c = 1; c < C; ++c) if (Rcol[c] < mn) mn = Rcol[c];
+    double den = 0.0, num = 0.0;
+    for (int c = 0; c < C; ++c) {
+        double w = exp(-tau * (double)(Rcol[c] - mn));
+        den += w;
+        num += (double)Rcol[c] * w;
+    }
+    return num / den;
+}
+
+/* (a7) Backward through R = P A and the STE (§3.2 l.189-191, l.226):
+ * dL/dR_cn = -g_n[R_cn]; dL/dA = P^T dL/dR; the binariser is the identity in
+ * the backward pass (STE), and since A_neg = 1 - A_pos (R2) the variable
+ * gradient folds as dL/dA_pos - dL/dA_neg:
+ *   G_vn = sum_{c contains -v} g_n[R_cn] - sum_{c contains +v} g_n[R_cn].
+ * Equal terms are grouped by value (exact integer counts, R12):
+ *   G_vn = sum_r (cneg_vn[r] - cpos_vn[r]) g_n[r], ascending r.
+ * occ lists (variable -> (clause, sign)) are built here from the CNF. */
+void or_backward(int V, int C, const int64_t* cptr, const int32_t* lits, int Nl, int K,
+                 const uint8_t* R, const double* g, double* G)
+{
+    /* transpose: count occurrences per variable */
+    int64_t* vptr = (int64_t*)calloc((size_t)V + 1, sizeof(int64_t));
+    int64_t nnz = cptr[C];
+    int32_t* occ_c = (int32_t*)malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(int32_t));
+    int8_t* occ_s = (int8_t*)malloc((size_t)(nnz > 0 ? nnz : 1));
+    for (int64_t l = 0; l < nnz; ++l) vptr[(lits[l] > 0 ? lits[l] : -lits[l])]++;
+    for (int v = 0; v < V; ++v) vptr[v + 1] += vptr[v];
+    int64_t* fill = (int64_t*)malloc(((size_t)V + 1) * sizeof(int64_t));
+    memcpy(fill, vptr, ((size_t)V + 1) * sizeof(int64_t));
+    for (int c = 0; c < C; ++c)
+        for (int64_t l = cptr[c]; l < cptr[c + 1]; ++l) {
+            int v = (lits[l] > 0 ? lits[l] : -lits[l]) - 1;
+            occ_c[fill[v]] = c;
+            occ_s[fill[v]] = lits[l] > 0 ? 1 : -1;
+            fill[v]++;
+        }
+    int32_t* cnt = (int32_t*)malloc((size_t)Nl * (K + 1) * sizeof(int32_t));
+    for (int v = 0; v < V; ++v) {
+        memset(cnt, 0, (size_t)Nl * (K + 1) * sizeof(int32_t));
+        for (int64_t o = vptr[v]; o < vptr[v + 1]; ++o) {
+            const uint8_t* Rrow = R + (size_t)occ_c[o] * Nl;
+            int delta = occ_s[o] < 0 ? +1 : -1;  /* cneg - cpos */
+            for (int j = 0; j < Nl; ++j) cnt[(size_t)j * (K + 1) + Rrow[j]] += delta;
+        }
+        for (int j = 0; j < Nl; ++j) {
+            double acc = 0.0;
+            for (int r = 0; r <= K; ++r)
+                acc = acc + (double)cnt[(size_t)j * (K + 1) + r] * g[(size_t)j * (K + 1) + r];
+            G[(size_t)v * Nl + j] = acc;
+        }
+    }
+    free(cnt); free(fill); free(occ_s); free(occ_c); free(vptr);
+}
+
+/* ceil(log2(x)) for finite x > 0, exactly (frexp: x = f 2^e, f in [0.5,1)). */
+static int ceil_log2(double x)
+{
+    int e;
+    double f = frexp(x, &e);
+    return (f == 0.5) ? e - 1 : e;
+}
+
+/* (a8) Eq. 5 Jacobian (l.269 "fully differentiable").  With x = theta/mu
+ * (mu the row mean over all N), dL/dtheta_vn = G_vn/d_v - J_v/(N d_v^2),
+ * J_v = sum_m G_vm theta_vm.  J_v is summed exactly in int64 fixed point:
+ * p = G theta (fp64); s_v = 61 - ceil(log2(N occ_v gmax thmax)) (a global
+ * bound on |sum p|); I_v = sum llrint(ldexp(p, s_v)).  This function returns
+ * the partial integer sums I_v over the local candidates and s_v (R13).
+ * occ_v = number of literal occurrences of v; gmax = max |g_n[r]| over all
+ * candidates and r in [rmin_n, K]; thmax = max |theta| over the batch. */
+void or_jacobian_partial(int V, int Nl, const double* G, const float* theta,
+                         const int32_t* occ, int64_t N, double gmax, float thmax,
+                         int64_t* I, int32_t* s_out, uint8_t* valid)
+{
+    for (int v = 0; v < V; ++v) {
+        double x = (double)N * (double)occ[v];
+        x = x * gmax;
+        x = x * (double)thmax;
+        I[v] = 0; s_out[v] = 0; valid[v] = 0;
+        if (occ[v] == 0 || !(x > 0.0)) continue;
+        int s = 61 - ceil_log2(x);
+        int64_t acc = 0;
+        for (int j = 0; j < Nl; ++j) {
+            double p = G[(size_t)v * Nl + j] * (double)theta[(size_t)v * Nl + j];
+            acc += (int64_t)llrint(ldexp(p, s));
+        }
+        I[v] = acc; s_out[v] = s; valid[v] = 1;
+    }
+}
+
+/* c_v = ((J_v/N) rho_v) rho_v = J_v / (N d_v^2); zero when the guard is
+ * active or normalisation is off (the guard's derivative is 0). */
+void or_jacobian_finish(int V, int64_t N, const int64_t* I, const int32_t* s, const uint8_t* valid,
+                        const double* rho, const uint8_t* guard, int normalize, double* J, double* cv)
+{
+    for (int v = 0; v < V; ++v) {
+        double j = valid[v] ? ldexp((double)I[v], -s[v]) : 0.0;
+        J[v] = j;
+        if (!normalize || guard[v]) { cv[v] = 0.0; continue; }
+        double t = j / (double)N;
+        t = t * rho[v];
+        cv[v] = t * rho[v];
+    }
+}
+
+/* grad_vn = (float)(G_vn rho_v - c_v). */
+void or_grad(int V, int Nl, const double* G, const double* rho, const double* cv, float* grad)
+{
+    for (int v = 0; v < V; ++v)
+        for (int j = 0; j < Nl; ++j) {
+            double a = G[(size_t)v * Nl + j] * rho[v];
+            grad[(size_t)v * Nl + j] = (float)(a - cv[v]);
+        }
+}
+
+/* (a9) LR schedule, §4.1 l.255-259: lr0 = 1e-1, /10 every 30
+ * iterations, floor 1e-15, restart to lr0 every 360 iterations (0-based t,
+ * R9).  lr = max(lr0 / factor^i, lr_min), i = (t mod restart) div decay;
+ * factor^i by repeated multiplication. */
+double or_lr_at(int64_t t, double lr0, double factor, int decay_every, int restart_every, double lr_min)
+{
+    int64_t i = (t % restart_every) / decay_every;
+    double p = 1.0;
+    for (int64_t k = 0; k < i; ++k) p = p * factor;
+    double lr = lr0 / p;
+    return lr < lr_min ? lr_min : lr;
+}
+
+/* AdamW (§4.1 l.255, "AdamW"; hyper-parameters = PyTorch defaults,
+ * R6), in PyTorch's single-tensor order (torch/optim/adam.py:419,457,476,
+ * 531-547) with its CPU kernels' rounding (lerp and addcmul use one fused
+ * multiply-add; R6b).  s = t + 1 is the bias-correction step.
+ *   theta *= (float)(1 - lr wd)
+ *   m      = fmaf(a1, g - m, m),           a1 = (float)(1 - beta1)
+ *   v      = fmaf(a2 g, g, v beta2),       a2 = (float)(1 - beta2)
+ *   den    = sqrtf(v)/(float)sqrt(1 - beta2^s) + eps
+ *   theta  = theta + ((float)(-lr/(1 - beta1^s)) m)/den
+ * Optional noise (R17, default sigma = 0): theta += (float)(lr sigma) xi,
+ * xi = (x>>8) 2^-24 - 1/2, x = Philox(key=seed, ctr=(n>>2, v, 1+t, 0))[n&3]. */
+void or_adamw(int V, int64_t n0, int Nl, float* theta, float* m, float* vv, const float* grad,
+              int64_t t, double lr, double beta1, double beta2, double eps, double wd,
+              double noise_sigma, uint64_t seed)
+{
+    double s = (double)(t + 1);
+    float wdf = (float)(1.0 - lr * wd);
+    float a1 = (float)(1.0 - beta1);
+    float b2f = (float)beta2;
+    float a2 = (float)(1.0 - beta2);
+    double bc1 = 1.0 - pow(beta1, s);
+    double bc2 = 1.0 - pow(beta2, s);
+    float nss = (float)(-(lr / bc1));
+    float bc2s = (float)sqrt(bc2);
+    float epsf = (float)eps;
+    float nz = (float)(lr * noise_sigma);
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    for (int v = 0; v < V; ++v)
+        for (int j = 0; j < Nl; ++j) {
+            size_t i = (size_t)v * Nl + j;
+            float g = grad[i];
+            float th = theta[i] * wdf;
+            float mm = fmaf(a1, g - m[i], m[i]);
+            float vb = vv[i] * b2f;
+            float vn = fmaf(a2 * g, g, vb);
+            float den = sqrtf(vn) / bc2s + epsf;
+            th = th + (nss * mm) / den;
+            if (noise_sigma != 0.0) {
+                int64_t n = n0 + j;
+                uint32_t ctr[4] = {(uint32_t)(n >> 2), (uint32_t)v, (uint32_t)(1 + t), 0u};
+                uint32_t x[4];
+                or_philox4x32_10(ctr, key, x);
+                float xi = (float)(x[n & 3] >> 8) * 5.9604644775390625e-08f - 0.5f;
+                th = th + nz * xi;
+            }
+            theta[i] = th; m[i] = mm; vv[i] = vn;
+        }
+}
+
+/* max |theta| (exact). */
+float or_abs_max(size_t n, const float* x)
+{
+    float mx = 0.0f;
+    for (size_t i = 0; i < n; ++i) { float a = fabsf(x[i]); if (a > mx) mx = a; }
+    return mx;
+}
+
+/* gmax = max over candidates and r in [rmin_n, K] of |g_n[r]|. */
+double or_gmax(int Nl, int K, const double* g, const int32_t* rmin)
+{
+    double mx = 0.0;
+    for (int j = 0; j < Nl; ++j)
+        for (int r = rmin[j]; r <= K; ++r) {
+            double a = fabs(g[(size_t)j * (K + 1) + r]);
+            if (a > mx) mx = a;
+        }
+    return mx;
+}
