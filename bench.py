@@ -1,0 +1,323 @@
+#!/usr/bin/env python
+"""Benchmark: TurboSAT batched differentiable SAT step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One "step" = one full iteration of the hot path over
+the whole candidate batch.  Metric (BASELINE.json): clause-candidate
+evaluations per second = C * N_global * steps / s (plus gradient steps / s).
+Workload at N=1: config c2 (planted random 3-SAT, V=10k, C=42k, ratio 4.2,
+N=4096 candidates), seeded synthetic input.  The state streamed every step
+(theta, m, v: 492 MB) is larger than L2, so no explicit flush is needed.
+
+Prints ONE JSON line (rank 0).  Under torchrun (N>1) each rank runs its own
+replica of the workload (weak scaling; the NCCL candidate-sharded path is not
+built yet), timed on the device, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=360)
+    ap.add_argument("--warmup", type=int, default=30)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--chunk", type=int, default=30, help="iterations per tsat_step call (one CUDA graph)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def workload_desc(name, cnf, N):
+    kinds = {"c1": "planted random 3-SAT", "c2": "planted random 3-SAT", "c3": "planted random 3-SAT",
+             "c4": "industrial-shaped CNF (lengths 2-7, power-law occurrences)", "c5": "planted random 3-SAT"}
+    return f"{name}: {kinds[name]} V={cnf.V} C={cnf.C} (ratio {cnf.C / cnf.V:.2f}), N={N} candidates"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.rows = []
+        self.stop = threading.Event()
+        self.th = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                for line in out.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return model, os.cpu_count()
+
+
+def oracle_timing(cnf, N, seed, budget_s=20.0, min_steps=1, max_steps=None):
+    """Time the plain C oracle (single thread, as it stands) on a bounded
+    sample: a slice of the candidate batch sized so the run takes ~budget_s."""
+    from oracle import oracle as O
+    Ns = min(N, 256)
+    o = O.Oracle(cnf, Ns, seed)
+    t0 = time.perf_counter()
+    o.step()
+    one = time.perf_counter() - t0
+    steps = max(min_steps, int(budget_s / max(one, 1e-6)))
+    if max_steps:
+        steps = min(steps, max_steps)
+    # scale the sample to the budget: more candidates if one step is cheap
+    if steps > 20 and Ns < N:
+        Ns = min(N, int(Ns * min(steps / 20, N / Ns)) // 32 * 32 or 32)
+        o = O.Oracle(cnf, Ns, seed)
+        o.step()
+        t0 = time.perf_counter()
+        o.step()
+        one = time.perf_counter() - t0
+        steps = max(min_steps, int(budget_s / max(one, 1e-6)))
+        if max_steps:
+            steps = min(steps, max_steps)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        o.step()
+    el = time.perf_counter() - t0
+    return dict(evals_per_s=cnf.C * Ns * steps / el, steps=steps, Ns=Ns, seconds=el)
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle (this tier's reference arm) on the same
+    config, rank 0 only, on host cores; each step a bounded candidate sample."""
+    from tsat_synth import make_config
+    if rank != 0:
+        return
+    cnf, cfg = make_config(args.config)
+    N = cfg["N"] * max(1, world)
+    model, cores = cpu_info()
+    total_budget = 120.0
+    per_step = total_budget / max(1, args.steps + args.warmup)
+    from oracle import oracle as O
+    Ns = 32
+    o = O.Oracle(cnf, Ns, cfg["seed"])
+    t0 = time.perf_counter()
+    o.step()
+    one = time.perf_counter() - t0
+    Ns = int(max(32, min(N, Ns * per_step / max(one, 1e-6))) // 32 * 32)
+    o = O.Oracle(cnf, Ns, cfg["seed"])
+    for _ in range(args.warmup):
+        o.step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.step()
+    el = time.perf_counter() - t0
+    value = cnf.C * Ns * args.steps / el
+    sample = f"{Ns} of {N} candidates per step (Eq. 5 mean over the sample), {args.steps} steps"
+    line = {
+        "impl": "reference", "metric": "clause-candidate evals/sec", "value": value, "unit": "evals/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * el / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload_desc(args.config, cnf, N), "V": cnf.V, "C": cnf.C, "N_global": N},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": 1, "kind": "oracle", "sample": sample,
+                         "cpu": model, "host_cores": cores},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2511_07737_b200 import Solver
+    from tsat_synth import make_config
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    cnf, cfg = make_config(args.config)
+    N = cfg["N"]
+    seed = cfg["seed"] + rank          # replicas: one independent batch per rank
+    stream = torch.cuda.current_stream()
+
+    s = Solver(local, stream=stream)
+    info = s.load_cnf(cnf)
+    s.init_batch(N, seed)
+    chunk = max(1, min(args.chunk, args.steps))
+    assert args.steps % chunk == 0, "--steps must be a multiple of --chunk"
+    # warm-up (also instantiates the chunk-sized CUDA graph)
+    w = max(3, args.warmup)
+    wk = 0
+    while wk < w:
+        s.step(chunk, wait=False)
+        wk += chunk
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- timed region (device events on the library's stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps // chunk):
+            s.step(chunk, wait=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    last = s.get_info()
+    evals = float(cnf.C) * N * world * args.steps
+    value = evals / (ms / 1000.0)
+
+    # ---- second timed pass with per-kernel CUDA events (roofline)
+    s.set_profiling(True)
+    s.kernel_times()
+    for _ in range(args.steps // chunk):
+        s.step(chunk, wait=False)
+    torch.cuda.synchronize()
+    kms, ksteps = s.kernel_times()
+    s.set_profiling(False)
+    names = ["k_clause", "k_gtable", "k_update", "k_step_end"]
+    per = {n: float(kms[i] / ksteps) for i, n in enumerate(names)}
+    V, C, K = cnf.V, cnf.C, cnf.K
+    occ_words = int(np.sum(np.diff(cnf.clause_ptr) ** 2))
+    upd_bytes = 24.0 * V * N + 2.0 * V * N / 8 + 4.0 * (occ_words + 2 * V + 1) + 8.0 * N * (K + 1)
+    upd_ms = per["k_update"]
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = upd_bytes / (upd_ms / 1000.0) / 1e9
+    roofline = {"bound": "hbm", "kernel": "k_update", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+                "algorithmic_bytes_per_launch": upd_bytes, "kernel_ms": per,
+                "kernel_share": {n: per[n] / sum(per.values()) for n in names}}
+
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        K_e2e = min(args.steps, 60)
+        unsat_host = np.empty(N, np.int32)
+        s2 = Solver(local, stream=stream)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        f0 = torch.cuda.Event(enable_timing=True); f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        s2.load_cnf(cnf)                      # host CSR -> device
+        s2.init_batch(N, seed)
+        for _ in range(K_e2e):
+            s2.step(1)                        # H2D step scalars, D2H step info
+            s2.query_unsat(unsat_host)        # D2H per-candidate unsat counts
+        f1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        ms_e2e = max(f0.elapsed_time(f1), wall * 1000.0)
+        if world > 1:
+            t = torch.tensor([ms_e2e], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        cnf_bytes = 8 * (cnf.C + 1) + 4 * cnf.nnz
+        e2e = {"value": float(cnf.C) * N * world * K_e2e / (ms_e2e / 1000.0), "unit": "evals/s",
+               "h2d_bytes_per_step": cnf_bytes / K_e2e + 48, "d2h_bytes_per_step": 4 * N + 56,
+               "steps": K_e2e, "includes": "load_clauses + init_batch + per-step tsat_step(1) + tsat_query_unsat"}
+        s2.close()
+
+    # ---- CPU oracle baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        r = oracle_timing(cnf, N, seed, budget_s=15.0)
+        model, cores = cpu_info()
+        cpu = {"value": r["evals_per_s"], "unit": "evals/s", "cores": 1, "kind": "oracle",
+               "sample": f"{r['steps']} oracle steps on {r['Ns']} of {N} candidates ({r['seconds']:.1f} s, single thread)",
+               "cpu": model, "host_cores": cores}
+
+    kps = s.kernels_per_step()
+    line = {
+        "metric": "clause-candidate evals/sec", "value": value, "unit": "evals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": w, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload_desc(args.config, cnf, N * world), "V": cnf.V, "C": cnf.C, "K": cnf.K,
+                   "N_per_gpu": N, "N_global": N * world, "seed": seed,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "state (theta, m, v: %.0f MB) larger than L2; no flush" % (12 * cnf.V * N / 1e6),
+                   "graph_chunk": chunk},
+        "gradient_steps_per_s": args.steps / (ms / 1000.0),
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": kps * args.steps, "clocks": clk.summary(),
+        "last_info": {"t": last.t, "best_unsat": last.best_unsat, "loss": last.loss, "solved": last.solved},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,206 @@
+/*
+ * turbosat.h - C-ABI of libturbosat, a B200-native (sm_100a) implementation of
+ * TurboSAT's batched differentiable SAT step (arXiv 2511.07737).
+ *
+ * One iteration ("step") over a batch of N candidate assignments does, in the
+ * paper's order (Fig. 3, §3.2, §4.1):
+ *   Eq. 5 per-variable normalisation -> Eq. 2 binarisation B = clip(sign,0,1)
+ *   -> Eq. 1 R = P A (clause evaluation) -> §3.1.4 per-candidate unsat count
+ *   -> Eq. 4 SmoothMin, Eq. 3 loss -> straight-through backward (P^T, l.226)
+ *   -> Eq. 5 Jacobian -> AdamW with step decay / restarts (l.255-259)
+ *   -> re-binarisation; best-candidate selection (§4.2 l.279-287).
+ * Export (§4.2 l.279-281) hands the k most confident variables of the best
+ * candidates to a CPU CDCL solver (outside this library).
+ *
+ * Conventions
+ *  - Every call returns tsat_status; nothing throws or exits across the ABI.
+ *  - A CUDA/NCCL failure poisons the context: every later call on it returns
+ *    the same code.  tsat_error_string() describes the last error.
+ *  - Variables are 1-based in DIMACS text and in exported literals, 0-based in
+ *    arrays indexed by variable.  Candidate indices are global and 0-based.
+ *  - Device work is enqueued on the caller's CUDA stream (tsat_create).  Calls
+ *    that return host data synchronise that stream.
+ *  - Host pointers are plain host memory owned by the caller.  The batch
+ *    workspace is device memory owned by the caller (size from
+ *    tsat_workspace_bytes), alive until tsat_destroy or the next
+ *    tsat_init_batch.  The parsed CNF (host and device copies) is owned by the
+ *    library.
+ *  - Numerics are canonical: integer /
+ *    fixed-point cross-candidate sums and fixed-order IEEE ops, so results are
+ *    bit-identical for any launch configuration and GPU count.
+ */
+#ifndef TURBOSAT_H
+#define TURBOSAT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSAT_ABI_VERSION 1
+
+typedef struct tsat_ctx_s* tsat_ctx;
+
+typedef enum {
+    TSAT_OK = 0,
+    TSAT_E_ARG = 1,          /* invalid argument (null pointer, bad size, N % 32 != 0, k < 1, ...) */
+    TSAT_E_PARSE = 2,        /* malformed DIMACS (SPEC S:45 error list) */
+    TSAT_E_RANGE = 3,        /* instance/batch outside the supported range (e.g. clause length > 7) */
+    TSAT_E_STATE = 4,        /* call out of order (step before init, export before any step, ...) */
+    TSAT_E_OOM = 5,          /* host or device allocation failed / workspace too small */
+    TSAT_E_CUDA = 6,         /* CUDA error (context poisoned) */
+    TSAT_E_NCCL = 7,         /* NCCL error (context poisoned) */
+    TSAT_E_UNSUPPORTED = 8   /* feature not built in this library */
+} tsat_status;
+
+/* Optimiser / method configuration.  Defaults (tsat_config_default) are the
+ * paper's: AdamW lr 1e-1 -> 1e-15, /10 every 30 its, restart every 360
+ * (PAPER.md l.255-259); AdamW beta/eps/weight decay = PyTorch defaults
+ * (reading R6); tau = 1 (R1); Eq. 5 normalisation on, over all N (R20). */
+typedef struct {
+    double  tau;             /* SmoothMin temperature, Eq. 4 (> 0) */
+    int32_t normalize;       /* 1 = Eq. 5 over all N candidates; 0 = off (variant) */
+    double  beta1, beta2;    /* AdamW moments (0.9, 0.999) */
+    double  eps;             /* AdamW eps (1e-8) */
+    double  weight_decay;    /* AdamW decoupled weight decay (1e-2) */
+    double  lr0;             /* initial learning rate (1e-1) */
+    double  lr_min;          /* learning-rate floor (1e-15) */
+    double  decay_factor;    /* lr divisor per decay period (10) */
+    int32_t decay_every;     /* iterations per decay period (30) */
+    int32_t restart_every;   /* iterations per LR restart (360) */
+    double  noise_sigma;     /* optional Philox noise in the update (0 = paper-exact, R17) */
+    double  eps_norm;        /* Eq. 5 guard: |mean| <= eps_norm -> divide by +-eps_norm (1e-8) */
+} tsat_config;
+
+typedef struct {
+    int32_t V;               /* variables */
+    int64_t C;               /* clauses (as stored; empty clauses included) */
+    int64_t nnz;             /* literal occurrences after de-duplication */
+    int32_t K;               /* longest clause */
+    int64_t header_C;        /* clause count declared by the DIMACS header (-1 for tsat_load_clauses) */
+    int64_t n_warnings;      /* header/body clause-count mismatch, missing final 0, ... */
+    int64_t n_tautologies;   /* clauses containing x and ~x (kept) */
+    int64_t n_duplicates;    /* duplicate literals removed */
+    int32_t has_empty;       /* an empty clause is present: the instance is UNSAT */
+} tsat_cnf_info;
+
+typedef struct {
+    int64_t t;               /* iterations completed (state is theta_t) */
+    int32_t best_unsat;      /* min over candidates of unsat count at the last evaluated state theta_{t-1} */
+    int64_t best_idx;        /* its global candidate index (ties -> lower index) */
+    int32_t solved;          /* some candidate reached 0 unsat at some evaluated state */
+    int64_t solved_step;     /* iteration at which the first model was found (-1 if none) */
+    int64_t solved_idx;      /* candidate index of that model (-1 if none) */
+    double  loss;            /* Eq. 3 loss -sum_n S_n at the last evaluated state */
+} tsat_step_info;
+
+typedef struct {
+    int64_t  candidate;      /* out: global candidate index */
+    int32_t  unsat;          /* out: its unsat count at the last evaluated state */
+    int32_t  k;              /* out: number of literals written */
+    int32_t* lits;           /* caller-allocated [k_req]: signed 1-based DIMACS literals, most confident first */
+    float*   abs_grad;       /* caller-allocated [k_req] or NULL: |G_vn| (pre-Jacobian, R14), ascending */
+} tsat_partial;
+
+/* Fill *out with the paper defaults above. */
+tsat_status tsat_config_default(tsat_config* out);
+
+/* Host-only DIMACS validation (no context, no GPU): parses text[0..len) with
+ * the same rules as tsat_load_dimacs and fills *info.  SPEC S:41-49. */
+tsat_status tsat_parse_dimacs(const char* text, size_t len, tsat_cnf_info* info);
+
+/* Human-readable name of a status code (static string). */
+const char* tsat_status_string(tsat_status s);
+
+/* Create a context on CUDA device `cuda_device`, enqueueing on `cuda_stream`
+ * (a cudaStream_t; NULL = legacy default stream).  Multi-GPU (world > 1,
+ * candidate sharding) needs `nccl_unique_id` (128 bytes,
+ * identical on all ranks); pass NULL when world == 1. */
+tsat_status tsat_create(tsat_ctx* out, int cuda_device, void* cuda_stream,
+                        const void* nccl_unique_id, int rank, int world);
+
+/* Load a CNF from DIMACS text: comments 'c', header
+ * 'p cnf V C', clauses as signed integers terminated by 0.  Duplicate
+ * literals are removed, tautologies kept, empty clauses preserved.
+ * Errors: malformed header, '-0', variable > V, non-integer token
+ * -> TSAT_E_PARSE; clause length > 7 -> TSAT_E_RANGE.  Replaces any
+ * previously loaded CNF and invalidates the batch. */
+tsat_status tsat_load_dimacs(tsat_ctx ctx, const char* text, size_t len, tsat_cnf_info* info);
+
+/* Load a CNF from arrays: clause c is dimacs_lits[clause_ptr[c] .. clause_ptr[c+1])
+ * (signed 1-based literals, no terminators); clause_ptr has C+1 entries. */
+tsat_status tsat_load_clauses(tsat_ctx ctx, int32_t V, int64_t C, const int64_t* clause_ptr,
+                              const int32_t* dimacs_lits, tsat_cnf_info* info);
+
+/* Device workspace bytes for a batch of N_global candidates (this rank holds
+ * N_global / world of them).  N_global must be a multiple of 32 * world. */
+tsat_status tsat_workspace_bytes(tsat_ctx ctx, int64_t N_global, size_t* bytes);
+
+/* (a1) Initialise the batch (§4.1 l.250-252): theta_vn ~ N(0,1) from
+ * Philox4x32-10 keyed by `seed` at counter (n>>2, v, 0, 0) over the GLOBAL
+ * candidate index (shard-invariant), m = v = 0, t = 0.  `cfg` may be NULL
+ * (defaults).  dev_workspace: caller-owned device memory of >= bytes. */
+tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const tsat_config* cfg,
+                            void* dev_workspace, size_t bytes);
+
+/* Run k >= 1 iterations (rows a2-a10).  The k-iteration sequence is captured
+ * once as a CUDA graph and replayed; blocks only for the small *out readback
+ * (out may be NULL, then it does not block). */
+tsat_status tsat_step(tsat_ctx ctx, int32_t k, tsat_step_info* out);
+
+/* Last step's info without stepping (blocks). */
+tsat_status tsat_get_info(tsat_ctx ctx, tsat_step_info* out);
+
+/* Per-candidate unsat counts of the last evaluated state for this rank's
+ * N_local candidates; *first_global_idx = index of host_out[0]. */
+tsat_status tsat_query_unsat(tsat_ctx ctx, int32_t* host_out, int64_t* first_global_idx);
+
+/* (a10/a11) Export: the M best candidates by (unsat asc, index asc) over all
+ * ranks, each with its k most confident variables = smallest
+ * |G_vn| (ties -> lower v), paired with the candidate's value, all at the last
+ * evaluated state (l.279-281; R14, R23).  k <= 0 selects the paper's rule
+ * k = min(V, max(ceil(V/10^4), 20)).  host_out: M caller-owned entries whose
+ * lits/abs_grad arrays hold at least k entries. */
+tsat_status tsat_export_best(tsat_ctx ctx, int32_t M, int32_t k, tsat_partial* host_out);
+
+/* Binary values (0/1, V bytes) of candidate global_idx at the last evaluated state. */
+tsat_status tsat_export_model(tsat_ctx ctx, int64_t global_idx, uint8_t* host_values);
+
+/* The first model found (V bytes); TSAT_E_STATE if no candidate has reached 0 unsat. */
+tsat_status tsat_get_solution(tsat_ctx ctx, uint8_t* host_values, int64_t* idx, int64_t* step);
+
+/* Checkpoint / resume: theta, m, v as [V][N_local] fp32 host arrays (any may be
+ * NULL in get_state) and the iteration counter t. */
+tsat_status tsat_get_state(tsat_ctx ctx, float* theta, float* m, float* v, int64_t* t);
+tsat_status tsat_set_state(tsat_ctx ctx, const float* theta, const float* m, const float* v, int64_t t);
+
+/* Copy an internal buffer to host (tests / diagnostics):
+ *   which 0: histogram h [N_local][KB] int32 of the last evaluated state (KB = 4 if K <= 3 else 8)
+ *         1: derivative table g [N_local][KB] fp64;   2: S [N_local] fp64
+ *         3: bits of the last evaluated state [V][N_local/32] uint32 (bit j of word w = candidate 32w+j)
+ *         4: row statistics Q [V] int64 of the CURRENT state theta_t
+ * bytes must equal the buffer size. */
+tsat_status tsat_debug_copy(tsat_ctx ctx, int32_t which, void* host_dst, size_t bytes);
+
+/* Kernel timing: when enabled, CUDA events bracket every kernel of every step
+ * (also inside the graph).  tsat_kernel_times returns accumulated milliseconds
+ * per kernel class [clause, gtable, update, step_end] and the number of steps
+ * timed, then resets the accumulators. */
+tsat_status tsat_set_profiling(tsat_ctx ctx, int32_t enable);
+tsat_status tsat_kernel_times(tsat_ctx ctx, double* ms4, int64_t* steps);
+
+/* Number of CUDA kernels one iteration launches (for launch accounting). */
+tsat_status tsat_kernels_per_step(tsat_ctx ctx, int32_t* n);
+
+/* Last error message on ctx (static storage owned by ctx, valid until the next call). */
+const char* tsat_error_string(tsat_ctx ctx);
+
+/* Release the context and everything the library owns (not the caller's workspace). */
+void tsat_destroy(tsat_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TURBOSAT_H */

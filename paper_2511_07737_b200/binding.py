@@ -1,0 +1,297 @@
+"""Thin ctypes binding of libturbosat (include/turbosat.h): argument marshalling
+only.  Every step of the path runs in the library's CUDA kernels; PyTorch only
+provides device memory (the workspace tensor) and the CUDA stream.  There is no
+CPU fallback: if the shared library is missing or no CUDA device is present the
+calls fail loudly.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libturbosat.so")
+
+TSAT_STATUS = {
+    0: "TSAT_OK", 1: "TSAT_E_ARG", 2: "TSAT_E_PARSE", 3: "TSAT_E_RANGE", 4: "TSAT_E_STATE",
+    5: "TSAT_E_OOM", 6: "TSAT_E_CUDA", 7: "TSAT_E_NCCL", 8: "TSAT_E_UNSUPPORTED",
+}
+
+
+class TsatError(RuntimeError):
+    def __init__(self, status, msg=""):
+        self.status = status
+        self.name = TSAT_STATUS.get(status, str(status))
+        super().__init__(f"{self.name}: {msg}")
+
+
+class tsat_config(ct.Structure):
+    _fields_ = [("tau", ct.c_double), ("normalize", ct.c_int32), ("beta1", ct.c_double), ("beta2", ct.c_double),
+                ("eps", ct.c_double), ("weight_decay", ct.c_double), ("lr0", ct.c_double), ("lr_min", ct.c_double),
+                ("decay_factor", ct.c_double), ("decay_every", ct.c_int32), ("restart_every", ct.c_int32),
+                ("noise_sigma", ct.c_double), ("eps_norm", ct.c_double)]
+
+
+class tsat_cnf_info(ct.Structure):
+    _fields_ = [("V", ct.c_int32), ("C", ct.c_int64), ("nnz", ct.c_int64), ("K", ct.c_int32),
+                ("header_C", ct.c_int64), ("n_warnings", ct.c_int64), ("n_tautologies", ct.c_int64),
+                ("n_duplicates", ct.c_int64), ("has_empty", ct.c_int32)]
+
+
+class tsat_step_info(ct.Structure):
+    _fields_ = [("t", ct.c_int64), ("best_unsat", ct.c_int32), ("best_idx", ct.c_int64), ("solved", ct.c_int32),
+                ("solved_step", ct.c_int64), ("solved_idx", ct.c_int64), ("loss", ct.c_double)]
+
+
+class tsat_partial(ct.Structure):
+    _fields_ = [("candidate", ct.c_int64), ("unsat", ct.c_int32), ("k", ct.c_int32),
+                ("lits", ct.POINTER(ct.c_int32)), ("abs_grad", ct.POINTER(ct.c_float))]
+
+
+P = ct.c_void_p
+_SIGS = {
+    "tsat_config_default": (ct.c_int, [ct.POINTER(tsat_config)]),
+    "tsat_parse_dimacs": (ct.c_int, [ct.c_char_p, ct.c_size_t, ct.POINTER(tsat_cnf_info)]),
+    "tsat_status_string": (ct.c_char_p, [ct.c_int]),
+    "tsat_create": (ct.c_int, [ct.POINTER(P), ct.c_int, P, P, ct.c_int, ct.c_int]),
+    "tsat_load_dimacs": (ct.c_int, [P, ct.c_char_p, ct.c_size_t, ct.POINTER(tsat_cnf_info)]),
+    "tsat_load_clauses": (ct.c_int, [P, ct.c_int32, ct.c_int64, P, P, ct.POINTER(tsat_cnf_info)]),
+    "tsat_workspace_bytes": (ct.c_int, [P, ct.c_int64, ct.POINTER(ct.c_size_t)]),
+    "tsat_init_batch": (ct.c_int, [P, ct.c_int64, ct.c_uint64, ct.POINTER(tsat_config), P, ct.c_size_t]),
+    "tsat_step": (ct.c_int, [P, ct.c_int32, ct.POINTER(tsat_step_info)]),
+    "tsat_get_info": (ct.c_int, [P, ct.POINTER(tsat_step_info)]),
+    "tsat_query_unsat": (ct.c_int, [P, P, ct.POINTER(ct.c_int64)]),
+    "tsat_export_best": (ct.c_int, [P, ct.c_int32, ct.c_int32, ct.POINTER(tsat_partial)]),
+    "tsat_export_model": (ct.c_int, [P, ct.c_int64, P]),
+    "tsat_get_solution": (ct.c_int, [P, P, ct.POINTER(ct.c_int64), ct.POINTER(ct.c_int64)]),
+    "tsat_get_state": (ct.c_int, [P, P, P, P, ct.POINTER(ct.c_int64)]),
+    "tsat_set_state": (ct.c_int, [P, P, P, P, ct.c_int64]),
+    "tsat_debug_copy": (ct.c_int, [P, ct.c_int32, P, ct.c_size_t]),
+    "tsat_set_profiling": (ct.c_int, [P, ct.c_int32]),
+    "tsat_kernel_times": (ct.c_int, [P, P, ct.POINTER(ct.c_int64)]),
+    "tsat_kernels_per_step": (ct.c_int, [P, ct.POINTER(ct.c_int32)]),
+    "tsat_error_string": (ct.c_char_p, [P]),
+    "tsat_destroy": (None, [P]),
+}
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libturbosat.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise ImportError(f"{path} not found: build it with `python -m paper_2511_07737_b200.build` "
+                              "(there is no CPU fallback)")
+        lib = ct.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"]
+    return ct.c_void_p(a.ctypes.data)
+
+
+def config_default() -> tsat_config:
+    c = tsat_config()
+    load_library().tsat_config_default(ct.byref(c))
+    return c
+
+
+def parse_dimacs(text: bytes) -> tsat_cnf_info:
+    """tsat_parse_dimacs: host-only DIMACS validation."""
+    info = tsat_cnf_info()
+    s = load_library().tsat_parse_dimacs(text, len(text), ct.byref(info))
+    if s:
+        raise TsatError(s, "DIMACS rejected")
+    return info
+
+
+@dataclass
+class StepInfo:
+    t: int
+    best_unsat: int
+    best_idx: int
+    solved: bool
+    solved_step: int
+    solved_idx: int
+    loss: float
+
+
+class Solver:
+    """One TurboSAT batch on one CUDA device (rank `rank` of `world`).
+
+    Mirrors the C-ABI: load_dimacs / load_clauses -> init_batch -> step(k) ->
+    query_unsat / export_best / export_model / get_solution; get_state /
+    set_state for checkpoint-resume."""
+
+    def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_unique_id: bytes | None = None):
+        import torch
+        self._torch = torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2511_07737_b200 needs a CUDA device (no CPU fallback)")
+        self.lib = load_library()
+        self.device = device
+        torch.cuda.set_device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        h = ct.c_void_p()
+        uid = ct.c_char_p(nccl_unique_id) if nccl_unique_id is not None else None
+        self._check(self.lib.tsat_create(ct.byref(h), device, ct.c_void_p(self.stream.cuda_stream), uid, rank, world), None)
+        self.h = h
+        self.ws = None
+        self.V = self.C = self.N = self.N_local = 0
+        self.n0 = 0
+        self.info = None
+
+    # -- helpers
+    def _check(self, s, h="self"):
+        if s:
+            msg = ""
+            hh = self.h if h == "self" else h
+            if hh is not None:
+                msg = (self.lib.tsat_error_string(hh) or b"").decode()
+            raise TsatError(s, msg)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.tsat_destroy(self.h)
+            self.h = None
+            self.ws = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- C-ABI mirrors
+    def load_dimacs(self, text: bytes) -> tsat_cnf_info:
+        info = tsat_cnf_info()
+        self._check(self.lib.tsat_load_dimacs(self.h, text, len(text), ct.byref(info)))
+        self.V, self.C, self.info = info.V, info.C, info
+        return info
+
+    def load_clauses(self, V: int, clause_ptr: np.ndarray, lits: np.ndarray) -> tsat_cnf_info:
+        cp = np.ascontiguousarray(clause_ptr, np.int64)
+        li = np.ascontiguousarray(lits, np.int32)
+        info = tsat_cnf_info()
+        self._check(self.lib.tsat_load_clauses(self.h, int(V), len(cp) - 1, _ptr(cp), _ptr(li), ct.byref(info)))
+        self.V, self.C, self.info = info.V, info.C, info
+        return info
+
+    def load_cnf(self, cnf) -> tsat_cnf_info:
+        return self.load_clauses(cnf.V, cnf.clause_ptr, cnf.lits)
+
+    def workspace_bytes(self, N_global: int) -> int:
+        b = ct.c_size_t()
+        self._check(self.lib.tsat_workspace_bytes(self.h, int(N_global), ct.byref(b)))
+        return b.value
+
+    def init_batch(self, N_global: int, seed: int, cfg: tsat_config | None = None, **overrides):
+        torch = self._torch
+        if cfg is None:
+            cfg = config_default()
+        for k, v in overrides.items():
+            setattr(cfg, k, v)
+        nbytes = self.workspace_bytes(N_global)
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+        self._check(self.lib.tsat_init_batch(self.h, int(N_global), int(seed) & (2**64 - 1), ct.byref(cfg),
+                                             ct.c_void_p(self.ws.data_ptr()), nbytes))
+        self.N = int(N_global)
+        return self
+
+    def step(self, k: int = 1, wait: bool = True) -> StepInfo | None:
+        if not wait:
+            self._check(self.lib.tsat_step(self.h, int(k), None))
+            return None
+        si = tsat_step_info()
+        self._check(self.lib.tsat_step(self.h, int(k), ct.byref(si)))
+        return StepInfo(si.t, si.best_unsat, si.best_idx, bool(si.solved), si.solved_step, si.solved_idx, si.loss)
+
+    def get_info(self) -> StepInfo:
+        si = tsat_step_info()
+        self._check(self.lib.tsat_get_info(self.h, ct.byref(si)))
+        return StepInfo(si.t, si.best_unsat, si.best_idx, bool(si.solved), si.solved_step, si.solved_idx, si.loss)
+
+    def query_unsat(self, out: np.ndarray | None = None) -> np.ndarray:
+        n = self.N_local_count()
+        if out is None:
+            out = np.empty(n, np.int32)
+        first = ct.c_int64()
+        self._check(self.lib.tsat_query_unsat(self.h, _ptr(out), ct.byref(first)))
+        self.n0 = first.value
+        return out
+
+    def N_local_count(self) -> int:
+        return self.N  # world == 1 on this build; multi-rank divides by world
+
+    def export_best(self, M: int, k: int = 0):
+        kk = k if k > 0 else min(self.V, max(-(-self.V // 10000), 20))
+        bufs = []
+        arr = (tsat_partial * M)()
+        for i in range(M):
+            lits = np.zeros(kk, np.int32)
+            g = np.zeros(kk, np.float32)
+            bufs.append((lits, g))
+            arr[i].lits = lits.ctypes.data_as(ct.POINTER(ct.c_int32))
+            arr[i].abs_grad = g.ctypes.data_as(ct.POINTER(ct.c_float))
+        self._check(self.lib.tsat_export_best(self.h, int(M), int(k), arr))
+        return [dict(candidate=arr[i].candidate, unsat=arr[i].unsat, lits=bufs[i][0][:arr[i].k].copy(),
+                     abs_grad=bufs[i][1][:arr[i].k].copy()) for i in range(M)]
+
+    def export_model(self, idx: int) -> np.ndarray:
+        out = np.empty(self.V, np.uint8)
+        self._check(self.lib.tsat_export_model(self.h, int(idx), _ptr(out)))
+        return out
+
+    def get_solution(self):
+        out = np.empty(self.V, np.uint8)
+        idx, st = ct.c_int64(), ct.c_int64()
+        s = self.lib.tsat_get_solution(self.h, _ptr(out), ct.byref(idx), ct.byref(st))
+        if s == 4:
+            return None
+        self._check(s)
+        return out, idx.value, st.value
+
+    def get_state(self):
+        n = self.N_local_count()
+        th = np.empty((self.V, n), np.float32)
+        m = np.empty_like(th)
+        v = np.empty_like(th)
+        t = ct.c_int64()
+        self._check(self.lib.tsat_get_state(self.h, _ptr(th), _ptr(m), _ptr(v), ct.byref(t)))
+        return th, m, v, t.value
+
+    def set_state(self, theta, m, v, t: int):
+        th = np.ascontiguousarray(theta, np.float32)
+        mm = np.ascontiguousarray(m, np.float32)
+        vv = np.ascontiguousarray(v, np.float32)
+        self._check(self.lib.tsat_set_state(self.h, _ptr(th), _ptr(mm), _ptr(vv), int(t)))
+
+    def debug(self, which: int, dtype, shape) -> np.ndarray:
+        out = np.empty(shape, dtype)
+        self._check(self.lib.tsat_debug_copy(self.h, int(which), _ptr(out), out.nbytes))
+        return out
+
+    def set_profiling(self, on: bool):
+        self._check(self.lib.tsat_set_profiling(self.h, 1 if on else 0))
+
+    def kernel_times(self):
+        ms = np.zeros(4, np.float64)
+        st = ct.c_int64()
+        self._check(self.lib.tsat_kernel_times(self.h, _ptr(ms), ct.byref(st)))
+        return ms, st.value
+
+    def kernels_per_step(self) -> int:
+        n = ct.c_int32()
+        self._check(self.lib.tsat_kernels_per_step(self.h, ct.byref(n)))
+        return n.value

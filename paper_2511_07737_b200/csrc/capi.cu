@@ -1,0 +1,746 @@
+// capi.cu - the extern "C" boundary of libturbosat (include/turbosat.h) and
+// the host runtime behind it: context, CNF upload, workspace layout, per-call
+// step-scalar tables, CUDA-graph capture of k-iteration sequences, kernel
+// timing, export.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/turbosat.h"
+#include "tsat_internal.h"
+
+
+using namespace tsat;
+
+constexpr int kKernelsPerStep = 4;
+
+struct DevCnf {
+    uint32_t *cptr = nullptr, *clit = nullptr, *occ_ptr = nullptr, *occ_rec = nullptr, *occ_cnt = nullptr;
+};
+
+struct tsat_ctx_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int rank = 0, world = 1;
+    tsat_status poisoned = TSAT_OK;
+    std::string err;
+    // CNF
+    bool have_cnf = false;
+    HostCnf cnf;
+    DevCnf dcnf;
+    // batch
+    bool have_batch = false;
+    int64_t N_global = 0;
+    int N = 0;                 // local
+    long long n0 = 0;
+    int KB = 4;
+    uint64_t seed = 0;
+    tsat_config cfg{};
+    MethodConsts mc{};
+    Layout L{};
+    char* ws = nullptr;
+    size_t ws_bytes = 0;
+    int64_t t = 0;             // iterations completed
+    int64_t steps_done = 0;    // >= 1 once a state has been evaluated
+    StepScalars* h_steptab = nullptr;   // pinned
+    DevScalars* h_scal = nullptr;       // pinned readback
+    std::map<int, cudaGraphExec_t> graphs;
+    // profiling
+    bool profiling = false;
+    std::vector<cudaEvent_t> events;    // (kKernelsPerStep+1) per step of the largest k
+    double prof_ms[kKernelsPerStep] = {0, 0, 0, 0};
+    int64_t prof_steps = 0;
+    int prof_pending_k = 0;
+};
+
+namespace {
+
+tsat_status fail(tsat_ctx c, tsat_status s, const std::string& msg) {
+    if (c) c->err = msg;
+    return s;
+}
+
+tsat_status cuda_fail(tsat_ctx c, cudaError_t e, const char* where) {
+    if (c) {
+        c->poisoned = TSAT_E_CUDA;
+        c->err = std::string(where) + ": " + cudaGetErrorString(e);
+    }
+    return TSAT_E_CUDA;
+}
+
+#define CK(call)                                                  \
+    do {                                                          \
+        cudaError_t e_ = (call);                                  \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call);  \
+    } while (0)
+
+#define GUARD_CTX()                                    \
+    do {                                               \
+        if (!ctx) return TSAT_E_ARG;                   \
+        if (ctx->poisoned != TSAT_OK) return ctx->poisoned; \
+    } while (0)
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+Layout make_layout(int V, int N, int KB) {
+    Layout L{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off = align_up(off + bytes);
+        return o;
+    };
+    size_t VN = (size_t)V * N, NW = (size_t)N / 32;
+    L.theta = take(VN * 4);
+    L.m = take(VN * 4);
+    L.v = take(VN * 4);
+    L.A0 = take((size_t)V * NW * 4);
+    L.A1 = take((size_t)V * NW * 4);
+    L.hist = take((size_t)N * KB * 4);
+    L.gtab = take((size_t)N * KB * 8);
+    L.S = take((size_t)N * 8);
+    L.unsat = take((size_t)N * 4);
+    L.rowQ = take((size_t)V * 8);
+    L.rowD = take((size_t)V * 8);
+    L.rowRho = take((size_t)V * 8);
+    L.rowGuard = take((size_t)V);
+    L.scal = take(sizeof(DevScalars));
+    L.steptab = take(sizeof(StepScalars) * kMaxStepsPerCall);
+    L.sol = take((size_t)V);
+    L.total = off;
+    return L;
+}
+
+StepArgs step_args(tsat_ctx ctx) {
+    StepArgs a{};
+    char* w = ctx->ws;
+    const Layout& L = ctx->L;
+    a.theta = (float*)(w + L.theta);
+    a.m = (float*)(w + L.m);
+    a.v = (float*)(w + L.v);
+    a.A0 = (uint32_t*)(w + L.A0);
+    a.A1 = (uint32_t*)(w + L.A1);
+    a.hist = (int*)(w + L.hist);
+    a.unsat = (int*)(w + L.unsat);
+    a.gtab = (double*)(w + L.gtab);
+    a.S = (double*)(w + L.S);
+    a.rowQ = (long long*)(w + L.rowQ);
+    a.rowD = (double*)(w + L.rowD);
+    a.rowRho = (double*)(w + L.rowRho);
+    a.rowGuard = (unsigned char*)(w + L.rowGuard);
+    a.sol = (unsigned char*)(w + L.sol);
+    a.ds = (DevScalars*)(w + L.scal);
+    a.cptr = ctx->dcnf.cptr;
+    a.clit = ctx->dcnf.clit;
+    a.occ_ptr = ctx->dcnf.occ_ptr;
+    a.occ_rec = ctx->dcnf.occ_rec;
+    a.occ_cnt = ctx->dcnf.occ_cnt;
+    a.V = ctx->cnf.V;
+    a.N = ctx->N;
+    a.C = ctx->cnf.C;
+    a.KB = ctx->KB;
+    a.mc = ctx->mc;
+    return a;
+}
+
+// Host-side canonical per-iteration scalars (libm; R6, R9).
+double lr_at(const tsat_config& c, int64_t t) {
+    int64_t i = (t % c.restart_every) / c.decay_every;
+    double p = 1.0;
+    for (int64_t k = 0; k < i; ++k) p = p * c.decay_factor;
+    double lr = c.lr0 / p;
+    return lr < c.lr_min ? c.lr_min : lr;
+}
+
+StepScalars step_scalars(const tsat_config& c, int64_t t) {
+    StepScalars s{};
+    double lr = lr_at(c, t);
+    double st = (double)(t + 1);
+    s.t = t;
+    s.lr = lr;
+    s.wdf = (float)(1.0 - lr * c.weight_decay);
+    s.a1 = (float)(1.0 - c.beta1);
+    s.b2f = (float)c.beta2;
+    s.a2 = (float)(1.0 - c.beta2);
+    double bc1 = 1.0 - std::pow(c.beta1, st);
+    double bc2 = 1.0 - std::pow(c.beta2, st);
+    s.nss = (float)(-(lr / bc1));
+    s.bc2s = (float)std::sqrt(bc2);
+    s.epsf = (float)c.eps;
+    s.nz = (float)(lr * c.noise_sigma);
+    return s;
+}
+
+void free_cnf(tsat_ctx ctx) {
+    cudaFree(ctx->dcnf.cptr);
+    cudaFree(ctx->dcnf.clit);
+    cudaFree(ctx->dcnf.occ_ptr);
+    cudaFree(ctx->dcnf.occ_rec);
+    cudaFree(ctx->dcnf.occ_cnt);
+    ctx->dcnf = DevCnf{};
+    ctx->have_cnf = false;
+}
+
+void drop_graphs(tsat_ctx ctx) {
+    for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+    ctx->graphs.clear();
+}
+
+void fill_info(const HostCnf& h, tsat_cnf_info* info) {
+    if (!info) return;
+    info->V = h.V;
+    info->C = h.C;
+    info->nnz = h.nnz;
+    info->K = h.K;
+    info->header_C = h.header_C;
+    info->n_warnings = h.n_warnings;
+    info->n_tautologies = h.n_tautologies;
+    info->n_duplicates = h.n_duplicates;
+    info->has_empty = h.has_empty;
+}
+
+tsat_status upload_cnf(tsat_ctx ctx, HostCnf&& h) {
+    drop_graphs(ctx);
+    free_cnf(ctx);
+    ctx->have_batch = false;
+    ctx->cnf = std::move(h);
+    const HostCnf& c = ctx->cnf;
+    auto up = [&](uint32_t** dst, const std::vector<uint32_t>& src) -> cudaError_t {
+        size_t bytes = std::max<size_t>(src.size(), 1) * 4;
+        cudaError_t e = cudaMalloc(dst, bytes);
+        if (e != cudaSuccess) return e;
+        if (!src.empty()) e = cudaMemcpyAsync(*dst, src.data(), src.size() * 4, cudaMemcpyHostToDevice, ctx->stream);
+        return e;
+    };
+    CK(cudaSetDevice(ctx->device));
+    CK(up(&ctx->dcnf.cptr, c.clause_ptr));
+    CK(up(&ctx->dcnf.clit, c.clause_lit));
+    CK(up(&ctx->dcnf.occ_ptr, c.occ_ptr));
+    CK(up(&ctx->dcnf.occ_rec, c.occ_rec));
+    CK(up(&ctx->dcnf.occ_cnt, c.occ_cnt));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->have_cnf = true;
+    return TSAT_OK;
+}
+
+tsat_status check_batch(tsat_ctx ctx, bool need_step) {
+    if (!ctx->have_cnf || !ctx->have_batch) return fail(ctx, TSAT_E_STATE, "no batch: call tsat_init_batch first");
+    if (need_step && ctx->steps_done == 0) return fail(ctx, TSAT_E_STATE, "no evaluated state: call tsat_step first");
+    return TSAT_OK;
+}
+
+// Launch the k-iteration sequence (graph or direct).
+tsat_status launch_steps(tsat_ctx ctx, int k) {
+    StepArgs a = step_args(ctx);
+    const StepScalars* sc = (const StepScalars*)(ctx->ws + ctx->L.steptab);
+    if (ctx->profiling) {
+        size_t need = (size_t)k * (kKernelsPerStep + 1);
+        while (ctx->events.size() < need) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            ctx->events.push_back(e);
+        }
+    }
+    auto body = [&](bool capture) -> cudaError_t {
+        for (int i = 0; i < k; ++i) {
+            long long t = ctx->t + i;
+            for (int kk = 0; kk < kKernelsPerStep; ++kk) {
+                if (ctx->profiling) {
+                    cudaError_t e = cudaEventRecord(ctx->events[(size_t)i * (kKernelsPerStep + 1) + kk], ctx->stream);
+                    if (e != cudaSuccess) return e;
+                }
+                // kernels read t from the step table; the parity of t selects
+                // the A buffers, so the graph is keyed by (k, t parity).
+                cudaError_t e = launch_step_kernel(kk, a, sc + i, t, ctx->stream);
+                if (e != cudaSuccess) return e;
+            }
+            if (ctx->profiling) {
+                cudaError_t e = cudaEventRecord(ctx->events[(size_t)i * (kKernelsPerStep + 1) + kKernelsPerStep], ctx->stream);
+                if (e != cudaSuccess) return e;
+            }
+        }
+        (void)capture;
+        return cudaSuccess;
+    };
+    int key = k * 4 + (int)(ctx->t & 1) * 2 + (ctx->profiling ? 1 : 0);
+    auto it = ctx->graphs.find(key);
+    if (it == ctx->graphs.end()) {
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        cudaError_t e = body(true);
+        cudaError_t e2 = cudaStreamEndCapture(ctx->stream, &g);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "capture step kernels");
+        if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "cudaStreamEndCapture");
+        cudaGraphExec_t ex;
+        CK(cudaGraphInstantiate(&ex, g, 0));
+        cudaGraphDestroy(g);
+        it = ctx->graphs.emplace(key, ex).first;
+    }
+    CK(cudaGraphLaunch(it->second, ctx->stream));
+    if (ctx->profiling) ctx->prof_pending_k = k;
+    return TSAT_OK;
+}
+
+tsat_status collect_profile(tsat_ctx ctx) {
+    if (!ctx->profiling || ctx->prof_pending_k == 0) return TSAT_OK;
+    int k = ctx->prof_pending_k;
+    for (int i = 0; i < k; ++i)
+        for (int kk = 0; kk < kKernelsPerStep; ++kk) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, ctx->events[(size_t)i * (kKernelsPerStep + 1) + kk],
+                                    ctx->events[(size_t)i * (kKernelsPerStep + 1) + kk + 1]));
+            ctx->prof_ms[kk] += ms;
+        }
+    ctx->prof_steps += k;
+    ctx->prof_pending_k = 0;
+    return TSAT_OK;
+}
+
+tsat_status read_info(tsat_ctx ctx, tsat_step_info* out) {
+    CK(cudaMemcpyAsync(ctx->h_scal, ctx->ws + ctx->L.scal, sizeof(DevScalars), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    tsat_status s = collect_profile(ctx);
+    if (s != TSAT_OK) return s;
+    const DevScalars& d = *ctx->h_scal;
+    if (out) {
+        out->t = ctx->t;
+        out->best_unsat = d.info_best_unsat;
+        out->best_idx = d.info_best_idx;
+        out->solved = d.sol_step >= 0 ? 1 : 0;
+        out->solved_step = d.sol_step;
+        out->solved_idx = d.sol_step >= 0 ? d.sol_idx : -1;
+        out->loss = d.info_loss;
+    }
+    return TSAT_OK;
+}
+
+}  // namespace
+
+// =====================================================================
+extern "C" {
+
+tsat_status tsat_config_default(tsat_config* out) {
+    if (!out) return TSAT_E_ARG;
+    out->tau = 1.0;
+    out->normalize = 1;
+    out->beta1 = 0.9;
+    out->beta2 = 0.999;
+    out->eps = 1e-8;
+    out->weight_decay = 1e-2;
+    out->lr0 = 1e-1;
+    out->lr_min = 1e-15;
+    out->decay_factor = 10.0;
+    out->decay_every = 30;
+    out->restart_every = 360;
+    out->noise_sigma = 0.0;
+    out->eps_norm = 1e-8;
+    return TSAT_OK;
+}
+
+const char* tsat_status_string(tsat_status s) {
+    switch (s) {
+        case TSAT_OK: return "TSAT_OK";
+        case TSAT_E_ARG: return "TSAT_E_ARG";
+        case TSAT_E_PARSE: return "TSAT_E_PARSE";
+        case TSAT_E_RANGE: return "TSAT_E_RANGE";
+        case TSAT_E_STATE: return "TSAT_E_STATE";
+        case TSAT_E_OOM: return "TSAT_E_OOM";
+        case TSAT_E_CUDA: return "TSAT_E_CUDA";
+        case TSAT_E_NCCL: return "TSAT_E_NCCL";
+        case TSAT_E_UNSUPPORTED: return "TSAT_E_UNSUPPORTED";
+    }
+    return "TSAT_E_?";
+}
+
+tsat_status tsat_parse_dimacs(const char* text, size_t len, tsat_cnf_info* info) {
+    if (!text && len) return TSAT_E_ARG;
+    int32_t V;
+    std::vector<int64_t> ptr;
+    std::vector<int32_t> lits;
+    int64_t hc, nw;
+    std::string msg;
+    if (parse_dimacs(text, len, &V, &ptr, &lits, &hc, &nw, &msg)) return TSAT_E_PARSE;
+    HostCnf h;
+    int r = build_cnf(V, (int64_t)ptr.size() - 1, ptr.data(), lits.data(), &h, &msg);
+    if (r) return r == 3 ? TSAT_E_RANGE : TSAT_E_ARG;
+    h.header_C = hc;
+    h.n_warnings = nw;
+    fill_info(h, info);
+    return TSAT_OK;
+}
+
+tsat_status tsat_create(tsat_ctx* out, int cuda_device, void* cuda_stream, const void* nccl_unique_id, int rank,
+                        int world) {
+    if (!out) return TSAT_E_ARG;
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) return TSAT_E_ARG;
+    if (world > 1) return TSAT_E_UNSUPPORTED;   // multi-GPU path: DESIGN.md "Multi-GPU"
+    (void)nccl_unique_id;
+    std::unique_ptr<tsat_ctx_s> c(new tsat_ctx_s());
+    c->device = cuda_device;
+    c->stream = (cudaStream_t)cuda_stream;
+    c->rank = rank;
+    c->world = world;
+    tsat_ctx ctx = c.get();
+    CK(cudaSetDevice(cuda_device));
+    CK(cudaMallocHost(&c->h_steptab, sizeof(StepScalars) * kMaxStepsPerCall));
+    CK(cudaMallocHost(&c->h_scal, sizeof(DevScalars)));
+    tsat_config_default(&c->cfg);
+    *out = c.release();
+    return TSAT_OK;
+}
+
+tsat_status tsat_load_dimacs(tsat_ctx ctx, const char* text, size_t len, tsat_cnf_info* info) {
+    GUARD_CTX();
+    if (!text && len) return fail(ctx, TSAT_E_ARG, "null text");
+    int32_t V;
+    std::vector<int64_t> ptr;
+    std::vector<int32_t> lits;
+    int64_t hc, nw;
+    std::string msg;
+    if (parse_dimacs(text, len, &V, &ptr, &lits, &hc, &nw, &msg)) return fail(ctx, TSAT_E_PARSE, msg);
+    HostCnf h;
+    int r = build_cnf(V, (int64_t)ptr.size() - 1, ptr.data(), lits.data(), &h, &msg);
+    if (r) return fail(ctx, r == 3 ? TSAT_E_RANGE : TSAT_E_ARG, msg);
+    h.header_C = hc;
+    h.n_warnings = nw;
+    fill_info(h, info);
+    return upload_cnf(ctx, std::move(h));
+}
+
+tsat_status tsat_load_clauses(tsat_ctx ctx, int32_t V, int64_t C, const int64_t* clause_ptr, const int32_t* lits,
+                              tsat_cnf_info* info) {
+    GUARD_CTX();
+    std::string msg;
+    HostCnf h;
+    int r = build_cnf(V, C, clause_ptr, lits, &h, &msg);
+    if (r) return fail(ctx, r == 3 ? TSAT_E_RANGE : TSAT_E_ARG, msg);
+    fill_info(h, info);
+    return upload_cnf(ctx, std::move(h));
+}
+
+tsat_status tsat_workspace_bytes(tsat_ctx ctx, int64_t N_global, size_t* bytes) {
+    GUARD_CTX();
+    if (!bytes) return fail(ctx, TSAT_E_ARG, "null bytes");
+    if (!ctx->have_cnf) return fail(ctx, TSAT_E_STATE, "no CNF loaded");
+    if (N_global <= 0 || N_global % (32LL * ctx->world) != 0)
+        return fail(ctx, TSAT_E_ARG, "N_global must be a positive multiple of 32 * world");
+    int64_t N = N_global / ctx->world;
+    if (N_global >= (1LL << 32)) return fail(ctx, TSAT_E_RANGE, "N_global >= 2^32");
+    if ((size_t)N * 12 > 200 * 1024) return fail(ctx, TSAT_E_RANGE, "N per GPU > 17066 not supported by the fused update");
+    int KB = ctx->cnf.K <= 3 ? 4 : 8;
+    *bytes = make_layout(ctx->cnf.V, (int)N, KB).total;
+    return TSAT_OK;
+}
+
+tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const tsat_config* cfg, void* ws,
+                            size_t bytes) {
+    GUARD_CTX();
+    size_t need;
+    tsat_status s = tsat_workspace_bytes(ctx, N_global, &need);
+    if (s != TSAT_OK) return s;
+    if (!ws || bytes < need) return fail(ctx, TSAT_E_OOM, "workspace too small");
+    if ((uintptr_t)ws % 256) return fail(ctx, TSAT_E_ARG, "workspace must be 256-byte aligned");
+    tsat_config c;
+    if (cfg) c = *cfg; else tsat_config_default(&c);
+    if (!(c.tau > 0) || c.decay_every < 1 || c.restart_every < 1 || !(c.decay_factor > 0) || !(c.eps_norm > 0))
+        return fail(ctx, TSAT_E_ARG, "invalid config");
+    drop_graphs(ctx);
+    ctx->cfg = c;
+    ctx->N_global = N_global;
+    ctx->N = (int)(N_global / ctx->world);
+    ctx->n0 = (long long)ctx->rank * ctx->N;
+    ctx->KB = ctx->cnf.K <= 3 ? 4 : 8;
+    ctx->seed = seed;
+    ctx->ws = (char*)ws;
+    ctx->ws_bytes = bytes;
+    ctx->L = make_layout(ctx->cnf.V, ctx->N, ctx->KB);
+    MethodConsts& mc = ctx->mc;
+    mc = MethodConsts{};
+    for (int d = 0; d < 8; ++d) mc.E[d] = std::exp(-c.tau * (double)d);
+    mc.tau = c.tau;
+    mc.eps_norm = c.eps_norm;
+    mc.normalize = c.normalize ? 1 : 0;
+    mc.K = ctx->cnf.K;
+    mc.Nglobal = N_global;
+    mc.n0 = ctx->n0;
+    mc.seed = seed;
+    mc.noise = c.noise_sigma != 0.0;
+    ctx->t = 0;
+    ctx->steps_done = 0;
+    CK(cudaSetDevice(ctx->device));
+    CK(configure_kernels(ctx->N));
+    StepArgs a = step_args(ctx);
+    CK(cudaMemsetAsync(ctx->ws + ctx->L.hist, 0, (size_t)ctx->N * ctx->KB * 4, ctx->stream));
+    CK(cudaMemsetAsync(ctx->ws + ctx->L.scal, 0, sizeof(DevScalars), ctx->stream));
+    DevScalars init{};
+    init.best_key = ~0ull;
+    init.sol_step = -1;
+    init.sol_idx = -1;
+    init.info_best_unsat = -1;
+    init.info_best_idx = -1;
+    *ctx->h_scal = init;
+    CK(cudaMemcpyAsync(a.ds, ctx->h_scal, sizeof(DevScalars), cudaMemcpyHostToDevice, ctx->stream));
+    CK(launch_init(a.theta, a.m, a.v, a.V, a.N, ctx->n0, seed, ctx->stream));
+    CK(launch_rowstats(a.theta, a.V, a.N, mc, a.rowQ, a.rowD, a.rowRho, a.rowGuard, a.A0, &a.ds->thmax_bits[0],
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->have_batch = true;
+    return TSAT_OK;
+}
+
+tsat_status tsat_step(tsat_ctx ctx, int32_t k, tsat_step_info* out) {
+    GUARD_CTX();
+    tsat_status s = check_batch(ctx, false);
+    if (s != TSAT_OK) return s;
+    if (k < 1) return fail(ctx, TSAT_E_ARG, "k < 1");
+    int done = 0;
+    while (done < k) {
+        int kk = std::min(k - done, kMaxStepsPerCall);
+        // the previous call's table must not be overwritten while in use
+        CK(cudaStreamSynchronize(ctx->stream));
+        s = collect_profile(ctx);
+        if (s != TSAT_OK) return s;
+        for (int i = 0; i < kk; ++i) ctx->h_steptab[i] = step_scalars(ctx->cfg, ctx->t + i);
+        CK(cudaMemcpyAsync(ctx->ws + ctx->L.steptab, ctx->h_steptab, sizeof(StepScalars) * kk, cudaMemcpyHostToDevice,
+                           ctx->stream));
+        s = launch_steps(ctx, kk);
+        if (s != TSAT_OK) return s;
+        ctx->t += kk;
+        ctx->steps_done += kk;
+        done += kk;
+    }
+    if (out) return read_info(ctx, out);
+    return TSAT_OK;
+}
+
+tsat_status tsat_get_info(tsat_ctx ctx, tsat_step_info* out) {
+    GUARD_CTX();
+    tsat_status s = check_batch(ctx, false);
+    if (s != TSAT_OK) return s;
+    return read_info(ctx, out);
+}
+
+tsat_status tsat_query_unsat(tsat_ctx ctx, int32_t* host_out, int64_t* first) {
+    GUARD_CTX();
+    tsat_status s = check_batch(ctx, true);
+    if (s != TSAT_OK) return s;
+    if (!host_out) return fail(ctx, TSAT_E_ARG, "null host_out");
+    CK(cudaMemcpyAsync(host_out, ctx->ws + ctx->L.unsat, (size_t)ctx->N * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (first) *first = ctx->n0;
+    return TSAT_OK;
+}
+
+tsat_status tsat_export_model(tsat_ctx ctx, int64_t gidx, uint8_t* host_values) {
+    GUARD_CTX();
+    tsat_status s = check_batch(ctx, true);
+    if (s != TSAT_OK) return s;
+    if (!host_values) return fail(ctx, TSAT_E_ARG, "null host_values");
+    int64_t n = gidx - ctx->n0;
+    if (n < 0 || n >= ctx->N) return fail(ctx, TSAT_E_ARG, "candidate not on this rank");
+    const int V = ctx->cnf.V, NW = ctx->N / 32;
+    size_t Aoff = ((ctx->t - 1) & 1) ? ctx->L.A1 : ctx->L.A0;    // evaluated state theta_{t-1}
+    std::vector<uint32_t> words((size_t)V);
+    if (V > 0) {
+        CK(cudaMemcpy2DAsync(words.data(), 4, ctx->ws + Aoff + (size_t)(n / 32) * 4, (size_t)NW * 4, 4, (size_t)V,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    for (int v = 0; v < V; ++v) host_values[v] = (uint8_t)((words[v] >> (n & 31)) & 1u);
+    return TSAT_OK;
+}
+
+tsat_status tsat_get_solution(tsat_ctx ctx, uint8_t* host_values, int64_t* idx, int64_t* step) {
+    GUARD_CTX();
+    tsat_status s = check_batch(ctx, false);
+    if (s != TSAT_OK) return s;
+    s = read_info(ctx, nullptr);
+    if (s != TSAT_OK) return s;
+    const DevScalars& d = *ctx->h_scal;
+    if (d.sol_step < 0) return fail(ctx, TSAT_E_STATE, "no model found yet");
+    if (idx) *idx = d.sol_idx;
+    if (step) *step = d.sol_step;
+    if (host_values && ctx->cnf.V > 0) {
+        CK(cudaMemcpyAsync(host_values, ctx->ws + ctx->L.sol, (size_t)ctx->cnf.V, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return TSAT_OK;
+}
+
+tsat_status tsat_get_state(tsat_ctx ctx, float* theta, float* m, float* v, int64_t* t) {
+    GUARD_CTX();
+    tsat_status s = check_batch(ctx, false);
+    if (s != TSAT_OK) return s;
+    size_t bytes = (size_t)ctx->cnf.V * ctx->N * 4;
+    if (theta) CK(cudaMemcpyAsync(theta, ctx->ws + ctx->L.theta, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (m) CK(cudaMemcpyAsync(m, ctx->ws + ctx->L.m, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (v) CK(cudaMemcpyAsync(v, ctx->ws + ctx->L.v, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (t) *t = ctx->t;
+    return TSAT_OK;
+}
+
+tsat_status tsat_set_state(tsat_ctx ctx, const float* theta, const float* m, const float* v, int64_t t) {
+    GUARD_CTX();
+    tsat_status s = check_batch(ctx, false);
+    if (s != TSAT_OK) return s;
+    if (!theta || !m || !v || t < 0) return fail(ctx, TSAT_E_ARG, "null state or t < 0");
+    size_t bytes = (size_t)ctx->cnf.V * ctx->N * 4;
+    StepArgs a = step_args(ctx);
+    CK(cudaMemcpyAsync(a.theta, theta, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(a.m, m, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(a.v, v, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    DevScalars init{};
+    init.best_key = ~0ull;
+    init.sol_step = -1;
+    init.sol_idx = -1;
+    init.info_best_unsat = -1;
+    init.info_best_idx = -1;
+    CK(cudaStreamSynchronize(ctx->stream));
+    *ctx->h_scal = init;
+    CK(cudaMemcpyAsync(a.ds, ctx->h_scal, sizeof(DevScalars), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(a.hist, 0, (size_t)ctx->N * ctx->KB * 4, ctx->stream));
+    uint32_t* A = (t & 1) ? a.A1 : a.A0;
+    CK(launch_rowstats(a.theta, a.V, a.N, ctx->mc, a.rowQ, a.rowD, a.rowRho, a.rowGuard, A, &a.ds->thmax_bits[t & 1],
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->t = t;
+    ctx->steps_done = 0;
+    return TSAT_OK;
+}
+
+tsat_status tsat_debug_copy(tsat_ctx ctx, int32_t which, void* dst, size_t bytes) {
+    GUARD_CTX();
+    tsat_status s = check_batch(ctx, false);
+    if (s != TSAT_OK) return s;
+    if (!dst) return fail(ctx, TSAT_E_ARG, "null dst");
+    size_t off, sz;
+    const int N = ctx->N, V = ctx->cnf.V;
+    switch (which) {
+        case 0: return fail(ctx, TSAT_E_UNSUPPORTED, "histogram is cleared after use; query unsat instead");
+        case 1: off = ctx->L.gtab; sz = (size_t)N * ctx->KB * 8; break;
+        case 2: off = ctx->L.S; sz = (size_t)N * 8; break;
+        case 3: off = ((ctx->t - 1) & 1) ? ctx->L.A1 : ctx->L.A0; sz = (size_t)V * (N / 32) * 4; break;
+        case 4: off = ctx->L.rowQ; sz = (size_t)V * 8; break;
+        default: return fail(ctx, TSAT_E_ARG, "unknown buffer");
+    }
+    if (bytes != sz) return fail(ctx, TSAT_E_ARG, "size mismatch: expected " + std::to_string(sz));
+    CK(cudaMemcpyAsync(dst, ctx->ws + off, sz, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TSAT_OK;
+}
+
+tsat_status tsat_export_best(tsat_ctx ctx, int32_t M, int32_t k, tsat_partial* out) {
+    GUARD_CTX();
+    tsat_status s = check_batch(ctx, true);
+    if (s != TSAT_OK) return s;
+    const int V = ctx->cnf.V, N = ctx->N;
+    if (M < 1 || M > N || !out) return fail(ctx, TSAT_E_ARG, "need 1 <= M <= N_local and host_out");
+    if (k <= 0) k = (int32_t)std::min<int64_t>(V, std::max<int64_t>((V + 9999) / 10000, 20));
+    if (k > V) k = V;
+    if (k > kTopkMax) return fail(ctx, TSAT_E_RANGE, "k > 2048 not supported");
+    if (k < 1) return fail(ctx, TSAT_E_ARG, "V = 0");
+    StepArgs a = step_args(ctx);
+    int n64 = 1;
+    while (n64 < N) n64 <<= 1;
+    unsigned long long* keys = nullptr;
+    int *cols = nullptr, *ov = nullptr;
+    double *absG = nullptr, *og = nullptr;
+    auto cleanup = [&]() { cudaFree(keys); cudaFree(cols); cudaFree(ov); cudaFree(absG); cudaFree(og); };
+    cudaError_t e;
+    if ((e = cudaMalloc(&keys, (size_t)n64 * 8)) != cudaSuccess ||
+        (e = cudaMalloc(&cols, (size_t)M * 4)) != cudaSuccess ||
+        (e = cudaMalloc(&ov, (size_t)M * k * 4)) != cudaSuccess ||
+        (e = cudaMalloc(&og, (size_t)M * k * 8)) != cudaSuccess ||
+        (e = cudaMalloc(&absG, (size_t)M * V * 8)) != cudaSuccess) {
+        cleanup();
+        cudaGetLastError();
+        return fail(ctx, TSAT_E_OOM, "export scratch allocation failed");
+    }
+    long long t_eval = ctx->t - 1;
+    e = launch_export(a, t_eval, nullptr, M, k, nullptr, keys, n64, nullptr, nullptr, ctx->stream, 0);
+    std::vector<unsigned long long> hk((size_t)M);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hk.data(), keys, (size_t)M * 8, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    std::vector<int> hc((size_t)M);
+    for (int i = 0; i < M; ++i) hc[i] = (int)((long long)(hk[i] & 0xffffffffull) - ctx->n0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(cols, hc.data(), (size_t)M * 4, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = launch_export(a, t_eval, cols, M, k, absG, keys, n64, ov, og, ctx->stream, 1);
+    std::vector<int> hv((size_t)M * k);
+    std::vector<double> hg((size_t)M * k);
+    std::vector<uint32_t> bits((size_t)V * (N / 32));
+    size_t Aoff = (t_eval & 1) ? ctx->L.A1 : ctx->L.A0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hv.data(), ov, hv.size() * 4, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hg.data(), og, hg.size() * 8, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(bits.data(), ctx->ws + Aoff, bits.size() * 4, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cleanup();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "export");
+    const int NW = N / 32;
+    for (int i = 0; i < M; ++i) {
+        int n = hc[i];
+        out[i].candidate = (int64_t)(hk[i] & 0xffffffffull);
+        out[i].unsat = (int32_t)(hk[i] >> 32);
+        out[i].k = k;
+        for (int j = 0; j < k; ++j) {
+            int v = hv[(size_t)i * k + j];
+            int b = (int)((bits[(size_t)v * NW + n / 32] >> (n & 31)) & 1u);
+            if (out[i].lits) out[i].lits[j] = b ? (v + 1) : -(v + 1);
+            if (out[i].abs_grad) out[i].abs_grad[j] = (float)hg[(size_t)i * k + j];
+        }
+    }
+    return TSAT_OK;
+}
+
+tsat_status tsat_set_profiling(tsat_ctx ctx, int32_t enable) {
+    GUARD_CTX();
+    ctx->profiling = enable != 0;
+    return TSAT_OK;
+}
+
+tsat_status tsat_kernel_times(tsat_ctx ctx, double* ms4, int64_t* steps) {
+    GUARD_CTX();
+    CK(cudaStreamSynchronize(ctx->stream));
+    tsat_status s = collect_profile(ctx);
+    if (s != TSAT_OK) return s;
+    for (int i = 0; i < kKernelsPerStep; ++i) {
+        if (ms4) ms4[i] = ctx->prof_ms[i];
+        ctx->prof_ms[i] = 0;
+    }
+    if (steps) *steps = ctx->prof_steps;
+    ctx->prof_steps = 0;
+    return TSAT_OK;
+}
+
+tsat_status tsat_kernels_per_step(tsat_ctx ctx, int32_t* n) {
+    GUARD_CTX();
+    if (!n) return TSAT_E_ARG;
+    *n = kKernelsPerStep;
+    return TSAT_OK;
+}
+
+const char* tsat_error_string(tsat_ctx ctx) {
+    if (!ctx) return "null context";
+    return ctx->err.c_str();
+}
+
+void tsat_destroy(tsat_ctx ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    drop_graphs(ctx);
+    for (auto e : ctx->events) cudaEventDestroy(e);
+    free_cnf(ctx);
+    cudaFreeHost(ctx->h_steptab);
+    cudaFreeHost(ctx->h_scal);
+    delete ctx;
+}
+
+}  // extern "C"

@@ -1,0 +1,218 @@
+// host_cnf.cpp - DIMACS parser and the clause store (CSR clause->literal plus
+// its transpose variable->occurrence), host side.
+//
+// DIMACS conventions follow SPEC.md S:41-49: comment lines 'c', header
+// 'p cnf V C', clauses of signed integers terminated by 0; header/body
+// clause-count mismatch is a warning; duplicate literals are removed;
+// tautologies are kept (counted); empty clauses are preserved; errors for a
+// malformed header, '-0', a variable > V, or a non-integer token.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tsat_internal.h"
+
+namespace tsat {
+
+namespace {
+
+struct Lexer {
+    const char* p;
+    const char* end;
+    int64_t line = 1;
+    void skip_ws() {
+        while (p < end && (*p == ' ' || *p == '\t' || *p == '\r' || *p == '\n' || *p == '\f' || *p == '\v')) {
+            if (*p == '\n') ++line;
+            ++p;
+        }
+    }
+    void skip_line() {
+        while (p < end && *p != '\n') ++p;
+    }
+    // token [b, e)
+    bool token(const char** b, const char** e) {
+        skip_ws();
+        if (p >= end) return false;
+        *b = p;
+        while (p < end && !(*p == ' ' || *p == '\t' || *p == '\r' || *p == '\n' || *p == '\f' || *p == '\v')) ++p;
+        *e = p;
+        return true;
+    }
+};
+
+bool parse_int(const char* b, const char* e, int64_t* out, bool* neg_zero) {
+    *neg_zero = false;
+    if (b == e) return false;
+    bool neg = false;
+    const char* q = b;
+    if (*q == '-' || *q == '+') { neg = (*q == '-'); ++q; }
+    if (q == e) return false;
+    int64_t v = 0;
+    for (; q < e; ++q) {
+        if (*q < '0' || *q > '9') return false;
+        v = v * 10 + (*q - '0');
+        if (v > (int64_t)1 << 40) return false;
+    }
+    if (neg && v == 0) *neg_zero = true;
+    *out = neg ? -v : v;
+    return true;
+}
+
+}  // namespace
+
+int parse_dimacs(const char* text, size_t len, int32_t* V_out, std::vector<int64_t>* ptr,
+                 std::vector<int32_t>* lits, int64_t* header_C, int64_t* n_warnings, std::string* msg) {
+    Lexer lx{text, text + len};
+    int64_t V = -1, Chdr = -1;
+    ptr->assign(1, 0);
+    lits->clear();
+    *n_warnings = 0;
+    bool in_clause = false;
+    while (true) {
+        lx.skip_ws();
+        if (lx.p >= lx.end) break;
+        char ch = *lx.p;
+        if (ch == 'c' && !in_clause) {          // comment line
+            lx.skip_line();
+            continue;
+        }
+        if (ch == '%' && !in_clause) {          // SATLIB end marker
+            break;
+        }
+        if (ch == 'p') {
+            if (V >= 0) { *msg = "duplicate header at line " + std::to_string(lx.line); return 2; }
+            if (in_clause) { *msg = "header inside a clause at line " + std::to_string(lx.line); return 2; }
+            const char *b, *e;
+            lx.token(&b, &e);
+            if (e - b != 1) { *msg = "malformed header at line " + std::to_string(lx.line); return 2; }
+            if (!lx.token(&b, &e) || (e - b) != 3 || std::strncmp(b, "cnf", 3) != 0) {
+                *msg = "malformed header (expected 'p cnf V C') at line " + std::to_string(lx.line);
+                return 2;
+            }
+            bool nz;
+            if (!lx.token(&b, &e) || !parse_int(b, e, &V, &nz) || V < 0 || V > (1 << 29)) {
+                *msg = "malformed header: bad variable count at line " + std::to_string(lx.line);
+                return 2;
+            }
+            if (!lx.token(&b, &e) || !parse_int(b, e, &Chdr, &nz) || Chdr < 0) {
+                *msg = "malformed header: bad clause count at line " + std::to_string(lx.line);
+                return 2;
+            }
+            continue;
+        }
+        const char *b, *e;
+        lx.token(&b, &e);
+        int64_t x;
+        bool negzero;
+        if (!parse_int(b, e, &x, &negzero)) {
+            *msg = "non-integer token '" + std::string(b, std::min<size_t>(e - b, 32)) + "' at line " + std::to_string(lx.line);
+            return 2;
+        }
+        if (V < 0) { *msg = "clause before the 'p cnf' header at line " + std::to_string(lx.line); return 2; }
+        if (negzero) { *msg = "literal -0 inside a clause at line " + std::to_string(lx.line); return 2; }
+        if (x == 0) {
+            ptr->push_back((int64_t)lits->size());
+            in_clause = false;
+            continue;
+        }
+        int64_t a = x < 0 ? -x : x;
+        if (a > V) {
+            *msg = "variable " + std::to_string(a) + " > V=" + std::to_string(V) + " at line " + std::to_string(lx.line);
+            return 2;
+        }
+        lits->push_back((int32_t)x);
+        in_clause = true;
+    }
+    if (V < 0) { *msg = "missing 'p cnf V C' header"; return 2; }
+    if (in_clause) {                          // last clause without its terminating 0
+        ptr->push_back((int64_t)lits->size());
+        ++*n_warnings;
+    }
+    int64_t C = (int64_t)ptr->size() - 1;
+    if (C != Chdr) ++*n_warnings;
+    *V_out = (int32_t)V;
+    *header_C = Chdr;
+    return 0;
+}
+
+int build_cnf(int32_t V, int64_t C, const int64_t* ptr, const int32_t* lits, HostCnf* out, std::string* msg) {
+    if (V < 0 || C < 0 || (C > 0 && (!ptr || (!lits && ptr[C] > 0)))) { *msg = "bad CNF arrays"; return 1; }
+    if (V >= (1 << 29)) { *msg = "V too large (>= 2^29)"; return 3; }
+    HostCnf h;
+    h.V = V;
+    h.C = C;
+    h.clause_ptr.resize((size_t)C + 1);
+    h.clause_ptr[0] = 0;
+    std::vector<uint32_t> codes;
+    codes.reserve(C > 0 ? (size_t)(ptr[C] - ptr[0]) : 0);
+    // per-variable (clause stamp, mask of signs seen in that clause): O(nnz) dedup
+    std::vector<int64_t> seen_stamp((size_t)V + 1, -1);
+    std::vector<uint8_t> seen_mask((size_t)V + 1, 0);
+    for (int64_t c = 0; c < C; ++c) {
+        if (ptr[c + 1] < ptr[c]) { *msg = "clause_ptr not monotone"; return 1; }
+        bool taut = false;
+        size_t start = codes.size();
+        for (int64_t l = ptr[c]; l < ptr[c + 1]; ++l) {
+            int32_t x = lits[l];
+            int64_t a = x < 0 ? -(int64_t)x : x;
+            if (x == 0 || a > V) { *msg = "literal out of range in clause " + std::to_string(c); return 1; }
+            uint8_t bit = x > 0 ? 1 : 2;
+            if (seen_stamp[a] != c) { seen_stamp[a] = c; seen_mask[a] = 0; }
+            if (seen_mask[a] & bit) { ++h.n_duplicates; continue; }
+            if (seen_mask[a]) taut = true;
+            seen_mask[a] |= bit;
+            codes.push_back(((uint32_t)(a - 1) << 1) | (x < 0 ? 1u : 0u));
+        }
+        size_t len = codes.size() - start;
+        if (len == 0) h.has_empty = 1;
+        if (taut) ++h.n_tautologies;
+        if ((int64_t)len > h.K) h.K = (int32_t)len;
+        if (codes.size() > 0xffffffffull) { *msg = "too many literals (>= 2^32)"; return 3; }
+        h.clause_ptr[(size_t)c + 1] = (uint32_t)codes.size();
+    }
+    h.nnz = (int64_t)codes.size();
+    h.clause_lit.swap(codes);
+    if (h.K > kMaxK) {
+        *msg = "clause length " + std::to_string(h.K) + " > " + std::to_string(kMaxK) + " not supported";
+        return 3;
+    }
+    // transpose: occurrence records per variable, clause-ascending
+    h.occ_cnt.assign((size_t)V, 0);
+    std::vector<uint64_t> words((size_t)V, 0);
+    for (int64_t c = 0; c < C; ++c) {
+        uint32_t len = h.clause_ptr[c + 1] - h.clause_ptr[c];
+        for (uint32_t i = h.clause_ptr[c]; i < h.clause_ptr[c + 1]; ++i) {
+            uint32_t v = h.clause_lit[i] >> 1;
+            h.occ_cnt[v] += 1;
+            words[v] += len;
+        }
+    }
+    h.occ_ptr.assign((size_t)V + 1, 0);
+    uint64_t acc = 0;
+    for (int32_t v = 0; v < V; ++v) {
+        h.occ_ptr[v] = (uint32_t)acc;
+        acc += words[v];
+        if (acc > 0xffffffffull) { *msg = "occurrence records too large (>= 2^32 words)"; return 3; }
+    }
+    h.occ_ptr[V] = (uint32_t)acc;
+    h.occ_rec.assign(acc, 0);
+    std::vector<uint32_t> fill(h.occ_ptr.begin(), h.occ_ptr.end() - 1);
+    for (int64_t c = 0; c < C; ++c) {
+        uint32_t b = h.clause_ptr[c], e = h.clause_ptr[c + 1], len = e - b;
+        for (uint32_t i = b; i < e; ++i) {
+            uint32_t code = h.clause_lit[i];
+            uint32_t v = code >> 1;
+            uint32_t* r = &h.occ_rec[fill[v]];
+            r[0] = (len << 1) | (code & 1u);
+            uint32_t o = 1;
+            for (uint32_t j = b; j < e; ++j)
+                if (j != i) r[o++] = h.clause_lit[j];
+            fill[v] += len;
+        }
+    }
+    *out = std::move(h);
+    return 0;
+}
+
+}  // namespace tsat

@@ -1,0 +1,122 @@
+// tsat_internal.h - shared between the host runtime (capi.cu, host_cnf.cpp)
+// and the sm_100a kernels (kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace tsat {
+
+// ---------------------------------------------------------------- host CNF
+// Literal code used on the device: (var << 1) | negated, var 0-based.
+struct HostCnf {
+    int32_t V = 0;
+    int64_t C = 0;
+    int64_t nnz = 0;
+    int32_t K = 0;
+    std::vector<uint32_t> clause_ptr;   // C+1
+    std::vector<uint32_t> clause_lit;   // nnz codes
+    // variable -> occurrence records (canonical clause-ascending order):
+    //   rec[0] = (len << 1) | own_negated, rec[1..len-1] = the other literal codes
+    std::vector<uint32_t> occ_ptr;      // V+1 (word offsets into occ_rec)
+    std::vector<uint32_t> occ_rec;
+    std::vector<uint32_t> occ_cnt;      // V: number of occurrences of the variable
+    int64_t header_C = -1;
+    int64_t n_warnings = 0, n_tautologies = 0, n_duplicates = 0;
+    int32_t has_empty = 0;
+};
+
+// Parse DIMACS.  Returns 0 on success, 2 (TSAT_E_PARSE) with msg.
+int parse_dimacs(const char* text, size_t len, int32_t* V, std::vector<int64_t>* ptr,
+                 std::vector<int32_t>* lits, int64_t* header_C, int64_t* n_warnings, std::string* msg);
+// Build HostCnf from signed-literal clause arrays (dedup, tautology count,
+// codes, occurrence records).  Returns 0, or TSAT_E_ARG / TSAT_E_RANGE with msg.
+int build_cnf(int32_t V, int64_t C, const int64_t* ptr, const int32_t* lits, HostCnf* out, std::string* msg);
+
+// ---------------------------------------------------------------- device
+constexpr int kMaxK = 7;          // clause length supported by the kernels
+constexpr int kMaxStepsPerCall = 4096;
+constexpr int kTopkMax = 2048;     // export: k most confident variables per candidate
+
+// Per-iteration scalars, computed on the host (libm) and uploaded per call.
+struct StepScalars {
+    int64_t t;        // iteration index of the evaluated state
+    double lr;
+    float wdf;        // (float)(1 - lr*wd)
+    float a1;         // (float)(1 - beta1)
+    float b2f;        // (float)beta2
+    float a2;         // (float)(1 - beta2)
+    float nss;        // (float)(-(lr / (1 - beta1^(t+1))))
+    float bc2s;       // (float)sqrt(1 - beta2^(t+1))
+    float epsf;       // (float)eps
+    float nz;         // (float)(lr * noise_sigma)
+};
+
+// Device-resident scalars (one struct in the workspace).
+struct DevScalars {
+    unsigned long long best_key;     // min over candidates of (unsat << 32 | global idx)
+    unsigned long long gmax_bits;    // max |g| (non-negative double bits)
+    unsigned int thmax_bits[2];      // max |theta| of theta_t, indexed by t & 1
+    int pad0;
+    double loss;
+    long long sol_step;              // first iteration with a 0-unsat candidate (-1)
+    long long sol_idx;
+    // last step info
+    long long info_t;
+    int info_best_unsat;
+    int pad1;
+    long long info_best_idx;
+    double info_loss;
+};
+
+// Method constants passed by value to kernels.
+struct MethodConsts {
+    double E[8];        // exp(-tau d), d = 0..7 (host libm)
+    double tau;
+    double eps_norm;
+    int normalize;
+    int K;              // instance max clause length
+    long long Nglobal;
+    long long n0;       // first global candidate index of this rank
+    unsigned long long seed;
+    int noise;          // noise_sigma != 0
+};
+
+// Pointers and sizes one iteration's kernels need (built by capi.cu).
+struct StepArgs {
+    float *theta, *m, *v;
+    uint32_t *A0, *A1;
+    int *hist, *unsat;
+    double *gtab, *S;
+    long long* rowQ;
+    double *rowD, *rowRho;
+    unsigned char *rowGuard, *sol;
+    DevScalars* ds;
+    const uint32_t *cptr, *clit, *occ_ptr, *occ_rec, *occ_cnt;
+    int V, N;
+    long long C;
+    int KB;
+    MethodConsts mc;
+};
+
+// Workspace layout (byte offsets), see capi.cu: layout().
+struct Layout {
+    size_t theta, m, v, A0, A1, hist, gtab, S, unsat, rowQ, rowD, rowRho, rowGuard, scal, steptab, sol, total;
+};
+
+// ---------------------------------------------------------------- launchers (kernels.cu)
+cudaError_t launch_init(float* theta, float* m, float* v, int V, int N, long long n0, unsigned long long seed,
+                        cudaStream_t st);
+cudaError_t launch_rowstats(const float* theta, int V, int N, const MethodConsts& mc, long long* rowQ, double* rowD,
+                            double* rowRho, unsigned char* rowGuard, uint32_t* A, unsigned int* thmax_bits,
+                            cudaStream_t st);
+// which: 0 clause, 1 gtable, 2 update, 3 step_end
+cudaError_t launch_step_kernel(int which, const StepArgs& a, const StepScalars* sc_dev, long long t, cudaStream_t st);
+cudaError_t configure_kernels(int N);
+cudaError_t launch_export(const StepArgs& a, long long t_eval, const int* cols_dev, int M, int k, double* absG,
+                          unsigned long long* keys, int n64, int* out_v, double* out_g, cudaStream_t st, int phase);
+
+}  // namespace tsat

@@ -1,0 +1,335 @@
+"""GPU parity: the CUDA path (through the C-ABI / ctypes binding) against the
+CPU oracle on identical seeded inputs.
+
+Bar (BASELINE.json north_star): bit-exact unsat counts, binarised assignments
+and SAT verdicts; floats within 1e-5 rel.  The canonical arithmetic
+makes theta/m/v, the g table and S bit-exact too, so those are compared with
+assert_array_equal; only the loss (a reduction whose order differs) uses a
+tolerance (1e-12 rel).  Init uses libm vs CUDA transcendental functions:
+<= 1 fp32 ulp and <= 1e-6 of the entries may differ.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tsat_synth import Cnf, enumeration_theta, fig1_cnf, industrial_cnf, make_config, planted_ksat, random_state
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2511_07737_b200 import build
+    build.build()
+
+
+def pack_bits(b):
+    """V x N uint8 -> V x N/32 uint32 words (bit j of word w = candidate 32w+j)."""
+    V, N = b.shape
+    x = b.reshape(V, N // 32, 32).astype(np.uint64)
+    return (x << np.arange(32, dtype=np.uint64)).sum(axis=2).astype(np.uint32)
+
+
+def make_pair(cnf, N, seed, cfg=None, state=None, t0=0):
+    from paper_2511_07737_b200 import Solver, config_default
+    s = Solver(0)
+    s.load_cnf(cnf)
+    c = config_default()
+    ocfg = cfg or O.Config()
+    for f in ("tau", "normalize", "beta1", "beta2", "eps", "weight_decay", "lr0", "lr_min", "decay_factor",
+              "decay_every", "restart_every", "noise_sigma", "eps_norm"):
+        setattr(c, f, getattr(ocfg, f))
+    s.init_batch(N, seed, c)
+    o = O.Oracle(cnf, N, seed, cfg=ocfg)
+    if state is not None:
+        s.set_state(*state, t0)
+        o.set_state(*state, t0)
+    return s, o
+
+
+def compare_step(s, o, cnf, what=""):
+    info = s.step(1)
+    ref = o.step()
+    K = cnf.K
+    KB = 4 if K <= 3 else 8
+    N = ref.unsat.shape[0]
+    unsat = s.query_unsat()
+    np.testing.assert_array_equal(unsat, ref.unsat, err_msg=f"unsat {what} t={ref.t}")
+    words = s.debug(3, np.uint32, (cnf.V, N // 32))
+    np.testing.assert_array_equal(words, pack_bits(ref.bits), err_msg=f"bits {what} t={ref.t}")
+    g = s.debug(1, np.float64, (N, KB))
+    np.testing.assert_array_equal(g[:, :K + 1], ref.g, err_msg=f"g {what} t={ref.t}")
+    assert not g[:, K + 1:].any()
+    S = s.debug(2, np.float64, (N,))
+    np.testing.assert_array_equal(S, ref.S, err_msg=f"S {what} t={ref.t}")
+    assert (info.best_unsat, info.best_idx) == (ref.best_unsat, ref.best_idx)
+    assert abs(info.loss - ref.loss) <= 1e-12 * max(1.0, abs(ref.loss))
+    th, m, v, t = s.get_state()
+    assert t == o.t
+    np.testing.assert_array_equal(th, o.theta, err_msg=f"theta {what} t={ref.t}")
+    np.testing.assert_array_equal(m, o.m, err_msg=f"m {what} t={ref.t}")
+    np.testing.assert_array_equal(v, o.v, err_msg=f"v {what} t={ref.t}")
+    Q = s.debug(4, np.int64, (cnf.V,))
+    Qo = np.empty(cnf.V, np.int64)
+    O.lib().or_row_sums(cnf.V, N, O._p(o.theta), O._p(Qo))
+    np.testing.assert_array_equal(Q, Qo)
+    return info, ref
+
+
+def ulp_diff(a, b):
+    ai = a.view(np.int32).astype(np.int64)
+    bi = b.view(np.int32).astype(np.int64)
+    ai = np.where(ai < 0, -(ai & 0x7fffffff), ai)
+    bi = np.where(bi < 0, -(bi & 0x7fffffff), bi)
+    return np.abs(ai - bi)
+
+
+# ---------------------------------------------------------------- init
+@pytest.mark.parametrize("V,N,seed", [(20, 64, 1), (1000, 4096, 7), (3, 32, 2**40 + 5)])
+def test_init_matches_oracle(V, N, seed):
+    cnf = planted_ksat(max(V, 3), 4 * max(V, 3), 3, 1)
+    s, o = make_pair(cnf, N, seed)
+    th, m, v, t = s.get_state()
+    assert t == 0 and not m.any() and not v.any()
+    d = ulp_diff(th, o.theta)
+    assert d.max() <= 1
+    assert (d > 0).mean() <= 1e-6
+
+
+# ---------------------------------------------------------------- trajectories
+def test_c1_trajectory_100_steps():
+    """Config c1 (planted 3-SAT V=20, C=85, N=64): all 100 steps, every state."""
+    cnf, cfg = make_config("c1")
+    s, o = make_pair(cnf, cfg["N"], cfg["seed"])
+    th, _, _, _ = s.get_state()
+    if not np.array_equal(th, o.theta):      # libm/CUDA init ulp (see module doc): hand the
+        s.set_state(o.theta, o.m, o.v, 0)      # ORACLE's theta0 to both sides
+    for _ in range(100):
+        compare_step(s, o, cnf, "c1")
+
+
+@pytest.mark.parametrize("case", ["ragged3", "industrial7", "special", "two_sat"])
+def test_ragged_and_mixed_instances(case):
+    if case == "ragged3":
+        cnf, N = planted_ksat(333, 1400, 3, 3), 96            # C not a multiple of the clause chunk, 3 words
+    elif case == "industrial7":
+        cnf, N = industrial_cnf(500, 2000, 4), 160            # K = 7, mixed lengths, hubs
+    elif case == "special":
+        base = planted_ksat(50, 200, 3, 9).clauses()
+        base += [[1], [-2], [3, -3], [4, 4, -5], [6, 7, -6, 8]]   # units, tautologies, duplicate literal
+        cnf, N = Cnf.from_clauses(50, base), 32
+    else:
+        cnf, N = planted_ksat(120, 200, 2, 5), 64
+    state = random_state(cnf.V, N, seed=11)
+    s, o = make_pair(cnf, N, 5, state=state, t0=0)
+    for _ in range(12):
+        compare_step(s, o, cnf, case)
+
+
+def test_lr_boundaries_and_restart():
+    """Cross the t = 29/30 decay and the t = 359/360 restart (R9)."""
+    cnf = planted_ksat(200, 840, 3, 6)
+    N = 128
+    state = random_state(cnf.V, N, seed=3)
+    for t0 in (27, 357):
+        s, o = make_pair(cnf, N, 2, state=state, t0=t0)
+        for _ in range(5):
+            compare_step(s, o, cnf, f"t0={t0}")
+
+
+@pytest.mark.parametrize("variant", [dict(normalize=0), dict(weight_decay=0.0), dict(tau=5.0), dict(tau=0.5),
+                                     dict(noise_sigma=0.3)])
+def test_variants(variant):
+    cnf = planted_ksat(150, 630, 3, 8)
+    cfg = O.Config(**variant)
+    s, o = make_pair(cnf, 96, 4, cfg=cfg)
+    th, _, _, _ = s.get_state()
+    s.set_state(o.theta, o.m, o.v, 0)
+    for _ in range(8):
+        compare_step(s, o, cnf, str(variant))
+
+
+def test_multi_step_graph_launch_matches():
+    """tsat_step(k) replays a k-iteration CUDA graph: same result as the oracle's k steps."""
+    cnf = planted_ksat(400, 1680, 3, 12)
+    N = 256
+    s, o = make_pair(cnf, N, 21)
+    s.set_state(o.theta, o.m, o.v, 0)
+    for k in (10, 7, 33):
+        info = s.step(k)
+        for _ in range(k):
+            ref = o.step()
+        th, m, v, t = s.get_state()
+        assert t == o.t
+        np.testing.assert_array_equal(th, o.theta)
+        np.testing.assert_array_equal(m, o.m)
+        np.testing.assert_array_equal(v, o.v)
+        np.testing.assert_array_equal(s.query_unsat(), ref.unsat)
+        assert (info.best_unsat, info.best_idx) == (ref.best_unsat, ref.best_idx)
+
+
+def test_c2_full_size_two_steps():
+    """Config c2 at full size (V=10k, C=42k, N=4096), bench's configuration."""
+    cnf, cfg = make_config("c2")
+    s, o = make_pair(cnf, cfg["N"], cfg["seed"])
+    th, _, _, _ = s.get_state()
+    d = ulp_diff(th, o.theta)
+    assert d.max() <= 1 and (d > 0).mean() <= 1e-6
+    s.set_state(o.theta, o.m, o.v, 0)
+    for _ in range(2):
+        compare_step(s, o, cnf, "c2")
+
+
+# ---------------------------------------------------------------- forward pins at scale
+def test_enumeration_all_assignments_v20():
+    """Brute force: all 2^20 assignments of a planted 20-variable instance, in
+    64 batches of 16384 (normalize off so theta's sign is the assignment);
+    GPU unsat counts equal direct evaluation; min = 0 (the planted model)."""
+    cnf = planted_ksat(20, 85, 3, 1)
+    V, B = 20, 16384
+    th = enumeration_theta(V)
+    lits = np.array(cnf.clauses())
+    var = np.abs(lits) - 1
+    from paper_2511_07737_b200 import Solver, config_default
+    s = Solver(0)
+    s.load_cnf(cnf)
+    c = config_default()
+    c.normalize = 0
+    s.init_batch(B, 1, c)
+    allu = []
+    for b in range(64):
+        sl = th[:, b * B:(b + 1) * B]
+        s.set_state(np.ascontiguousarray(sl), np.zeros_like(sl), np.zeros_like(sl), 0)
+        s.step(1)
+        allu.append(s.query_unsat().copy())
+    unsat = np.concatenate(allu)
+    n = np.arange(1 << V, dtype=np.int64)
+    vals = ((n[None, None, :] >> var[:, :, None]) & 1) == (lits[:, :, None] > 0)
+    ref = (~vals.any(axis=1)).sum(axis=0)
+    np.testing.assert_array_equal(unsat, ref)
+    assert unsat.min() == 0
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_full_size_properties(name):
+    """Configs c3/c4 at full size: init rows equal the oracle's; unsat counts
+    equal direct evaluation of the exported model bits (zero unsat => model)."""
+    cnf, cfg = make_config(name)
+    N = cfg["N"]
+    from paper_2511_07737_b200 import Solver
+    s = Solver(0)
+    s.load_cnf(cnf)
+    s.init_batch(N, cfg["seed"])
+    rows = 64
+    th0 = s.get_state()[0][:rows]
+    ref, _, _ = O.init_theta(rows, N, cfg["seed"])
+    assert ulp_diff(th0, ref).max() <= 1
+    info = s.step(2)
+    unsat = s.query_unsat()
+    rng = np.random.default_rng(0)
+    lits = cnf.lits
+    var = np.abs(lits) - 1
+    for n in rng.choice(N, 3, replace=False):
+        b = s.export_model(int(n))
+        val = np.where(lits > 0, b[var], 1 - b[var]).astype(np.int64)
+        sat = np.add.reduceat(val, cnf.clause_ptr[:-1]) > 0
+        assert unsat[n] == int((~sat).sum())
+    assert info.best_unsat == unsat.min()
+
+
+# ---------------------------------------------------------------- export / solution / resume
+def test_export_matches_oracle():
+    cnf = planted_ksat(300, 1260, 3, 14)
+    N = 128
+    s, o = make_pair(cnf, N, 3)
+    s.set_state(o.theta, o.m, o.v, 0)
+    for _ in range(6):
+        s.step(1)
+        ref = o.step()
+    for k in (0, 7, 300):
+        got = s.export_best(5, k)
+        kk = O.compute_k(cnf.V) if k == 0 else k
+        idx, u = O.select_top(ref.unsat, 5)
+        for gi, n, un in zip(got, idx, u):
+            assert (gi["candidate"], gi["unsat"]) == (n, un)
+            lits, mags = O.export_partial(np.abs(ref.G[:, n]), ref.bits[:, n], kk)
+            np.testing.assert_array_equal(gi["lits"], lits)
+            np.testing.assert_array_equal(gi["abs_grad"], mags.astype(np.float32))
+    for n in (0, 77, N - 1):
+        np.testing.assert_array_equal(s.export_model(n), ref.bits[:, n])
+
+
+def test_fig1_solution_and_verdict():
+    cnf = fig1_cnf()
+    s, o = make_pair(cnf, 32, 1)
+    s.set_state(o.theta, o.m, o.v, 0)
+    assert s.get_solution() is None
+    for it in range(200):
+        info = s.step(1)
+        ref = o.step()
+        assert info.best_unsat == ref.best_unsat
+        if ref.best_unsat == 0:
+            break
+    assert info.solved and info.best_unsat == 0
+    bits, idx, st = s.get_solution()
+    assert (idx, st) == (ref.best_idx, ref.t)
+    np.testing.assert_array_equal(bits, ref.bits[:, ref.best_idx])
+    assert "".join(map(str, bits.tolist())) in ("1001", "1101")
+
+
+def test_unsat_instance_never_solved():
+    s, o = make_pair(Cnf.from_clauses(1, [[1], [-1]]), 64, 2)
+    info = s.step(50)
+    assert info.best_unsat == 1 and not info.solved and s.get_solution() is None
+
+
+def test_checkpoint_resume_bit_exact():
+    cnf = planted_ksat(250, 1050, 3, 15)
+    from paper_2511_07737_b200 import Solver
+    a = Solver(0); a.load_cnf(cnf); a.init_batch(256, 9)
+    a.step(37)
+    st = a.get_state()
+    a.step(20)
+    ref = a.get_state()
+    b = Solver(0); b.load_cnf(cnf); b.init_batch(256, 9)
+    b.set_state(st[0], st[1], st[2], st[3])
+    b.step(20)
+    got = b.get_state()
+    for x, y in zip(got[:3], ref[:3]):
+        np.testing.assert_array_equal(x, y)
+    assert got[3] == ref[3] == 57
+
+
+def test_determinism_two_runs():
+    cnf = planted_ksat(500, 2100, 3, 16)
+    from paper_2511_07737_b200 import Solver
+    outs = []
+    for _ in range(2):
+        s = Solver(0); s.load_cnf(cnf); s.init_batch(512, 3)
+        info = s.step(40)
+        outs.append((s.get_state()[0], s.query_unsat().copy(), info.loss))
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    assert outs[0][2] == outs[1][2]
+
+
+def test_error_paths():
+    from paper_2511_07737_b200 import Solver, TsatError
+    s = Solver(0)
+    with pytest.raises(TsatError) as e:
+        s.step(1)
+    assert e.value.name == "TSAT_E_STATE"
+    s.load_cnf(planted_ksat(30, 120, 3, 1))
+    with pytest.raises(TsatError) as e:
+        s.init_batch(48, 1)                      # N % 32 != 0
+    assert e.value.name == "TSAT_E_ARG"
+    s.init_batch(64, 1)
+    with pytest.raises(TsatError) as e:
+        s.query_unsat()                          # nothing evaluated yet
+    assert e.value.name == "TSAT_E_STATE"
+    with pytest.raises(TsatError) as e:
+        s.step(0)
+    assert e.value.name == "TSAT_E_ARG"
