@@ -225,11 +225,31 @@ class StepOut:
     extra: dict = field(default_factory=dict)
 
 
+def binary_problem_matrix(cnf):
+    """The rows of P (§3.1.1, l.143-149): P is a 0/1 matrix, so a literal
+    repeated inside a clause is ONE entry (its column holds a 1).  Returns a
+    clause list with repeated literals removed (first occurrence kept); a
+    clause holding x and ~x keeps both (two distinct columns)."""
+    from tsat_synth import Cnf
+    out = []
+    changed = False
+    for cl in cnf.clauses():
+        seen, row = set(), []
+        for x in cl:
+            if x not in seen:
+                seen.add(x)
+                row.append(x)
+        changed |= len(row) != len(cl)
+        out.append(row)
+    return Cnf.from_clauses(cnf.V, out, cnf.sigma, cnf.name) if changed else cnf
+
+
 class Oracle:
     """One TurboSAT batch on the CPU: state theta, m, v (fp32, V x Nl) for the
     candidate shard [n0, n0 + Nl) of N global candidates."""
 
     def __init__(self, cnf, N, seed, cfg: Config | None = None, n0=0, Nl=None, init=True):
+        cnf = binary_problem_matrix(cnf)
         self.cnf = cnf
         self.N = int(N)
         self.n0 = int(n0)

@@ -26,7 +26,8 @@ struct DevCnf {
 
 struct tsat_ctx_s {
     int device = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;      // caller's stream: every launch / copy
+    cudaStream_t cap_stream = nullptr;  // private stream used only to capture graphs
     int rank = 0, world = 1;
     tsat_status poisoned = TSAT_OK;
     std::string err;
@@ -252,16 +253,18 @@ tsat_status launch_steps(tsat_ctx ctx, int k) {
             long long t = ctx->t + i;
             for (int kk = 0; kk < kKernelsPerStep; ++kk) {
                 if (ctx->profiling) {
-                    cudaError_t e = cudaEventRecord(ctx->events[(size_t)i * (kKernelsPerStep + 1) + kk], ctx->stream);
+                    cudaError_t e = cudaEventRecordWithFlags(ctx->events[(size_t)i * (kKernelsPerStep + 1) + kk], ctx->cap_stream,
+                                                            cudaEventRecordExternal);
                     if (e != cudaSuccess) return e;
                 }
                 // kernels read t from the step table; the parity of t selects
                 // the A buffers, so the graph is keyed by (k, t parity).
-                cudaError_t e = launch_step_kernel(kk, a, sc + i, t, ctx->stream);
+                cudaError_t e = launch_step_kernel(kk, a, sc + i, t, ctx->cap_stream);
                 if (e != cudaSuccess) return e;
             }
             if (ctx->profiling) {
-                cudaError_t e = cudaEventRecord(ctx->events[(size_t)i * (kKernelsPerStep + 1) + kKernelsPerStep], ctx->stream);
+                cudaError_t e = cudaEventRecordWithFlags(ctx->events[(size_t)i * (kKernelsPerStep + 1) + kKernelsPerStep],
+                                                        ctx->cap_stream, cudaEventRecordExternal);
                 if (e != cudaSuccess) return e;
             }
         }
@@ -272,9 +275,11 @@ tsat_status launch_steps(tsat_ctx ctx, int k) {
     auto it = ctx->graphs.find(key);
     if (it == ctx->graphs.end()) {
         cudaGraph_t g;
-        CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        // capture on the private stream (the caller's may be the legacy
+        // default stream, which cannot be captured); replay on the caller's
+        CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
         cudaError_t e = body(true);
-        cudaError_t e2 = cudaStreamEndCapture(ctx->stream, &g);
+        cudaError_t e2 = cudaStreamEndCapture(ctx->cap_stream, &g);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "capture step kernels");
         if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "cudaStreamEndCapture");
         cudaGraphExec_t ex;
@@ -389,6 +394,7 @@ tsat_status tsat_create(tsat_ctx* out, int cuda_device, void* cuda_stream, const
     c->world = world;
     tsat_ctx ctx = c.get();
     CK(cudaSetDevice(cuda_device));
+    CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
     CK(cudaMallocHost(&c->h_steptab, sizeof(StepScalars) * kMaxStepsPerCall));
     CK(cudaMallocHost(&c->h_scal, sizeof(DevScalars)));
     tsat_config_default(&c->cfg);
@@ -738,6 +744,7 @@ void tsat_destroy(tsat_ctx ctx) {
     drop_graphs(ctx);
     for (auto e : ctx->events) cudaEventDestroy(e);
     free_cnf(ctx);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     cudaFreeHost(ctx->h_steptab);
     cudaFreeHost(ctx->h_scal);
     delete ctx;

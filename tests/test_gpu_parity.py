@@ -53,7 +53,7 @@ def make_pair(cnf, N, seed, cfg=None, state=None, t0=0):
 def compare_step(s, o, cnf, what=""):
     info = s.step(1)
     ref = o.step()
-    K = cnf.K
+    K = o.K
     KB = 4 if K <= 3 else 8
     N = ref.unsat.shape[0]
     unsat = s.query_unsat()

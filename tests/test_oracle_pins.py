@@ -303,6 +303,21 @@ def test_euler_invariant():
     assert (np.abs(lhs) <= 1e-12 * scale).all()
 
 
+def test_repeated_literal_is_one_matrix_entry():
+    """§3.1.1 l.146-147: P holds only 0/1, so (x4 v x4 v ~x5) evaluates exactly
+    like (x4 v ~x5)."""
+    a = Cnf.from_clauses(5, [[4, 4, -5], [1, 2, 3]])
+    b = Cnf.from_clauses(5, [[4, -5], [1, 2, 3]])
+    th = enumeration_theta(5)
+    outs = []
+    for cnf in (a, b):
+        o = O.Oracle(cnf, 32, 0, init=False)
+        o.set_state(th, np.zeros_like(th), np.zeros_like(th), 0)
+        outs.append(o.step())
+    np.testing.assert_array_equal(outs[0].R, outs[1].R)
+    assert outs[0].R[0].max() == 2 and o.K == 3
+
+
 def test_tautology_and_unit_special_cases():
     """A tautology (x v ~x) contributes 0 to G; a unit clause (x1) pushes x1
     toward True; N = 1 gives a zero gradient (x = theta/mean = 1)."""
