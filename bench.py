@@ -239,7 +239,7 @@ def main():
     torch.cuda.synchronize()
     kms, ksteps = s.kernel_times()
     s.set_profiling(False)
-    names = ["k_clause", "k_gtable", "k_update", "k_step_end"]
+    names = ["k_clause", "k_gtable", "k_hub", "k_update", "k_step_end"]
     per = {n: float(kms[i] / ksteps) for i, n in enumerate(names)}
     V, C, K = cnf.V, cnf.C, cnf.K
     occ_words = int(np.sum(np.diff(cnf.clause_ptr) ** 2))

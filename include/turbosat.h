@@ -178,20 +178,21 @@ tsat_status tsat_set_state(tsat_ctx ctx, const float* theta, const float* m, con
 
 /* Copy an internal buffer to host (tests / diagnostics):
  *   which 0: histogram h [N_local][KB] int32 of the last evaluated state (KB = 4 if K <= 3 else 8)
- *         1: derivative table g [N_local][KB] fp64;   2: S [N_local] fp64
+ *         1: derivative table g [KB][N_local] fp32 (bin-major, R26);   2: S [N_local] fp64
  *         3: bits of the last evaluated state [V][N_local/32] uint32 (bit j of word w = candidate 32w+j)
  *         4: row statistics Q [V] int64 of the CURRENT state theta_t
  * bytes must equal the buffer size. */
 tsat_status tsat_debug_copy(tsat_ctx ctx, int32_t which, void* host_dst, size_t bytes);
 
 /* Kernel timing: when enabled, CUDA events bracket every kernel of every step
- * (also inside the graph).  tsat_kernel_times returns accumulated milliseconds
- * per kernel class [clause, gtable, update, step_end] and the number of steps
- * timed, then resets the accumulators. */
+ * (also inside the graph).  tsat_kernel_times fills ms5 with the accumulated
+ * milliseconds per kernel class [clause, gtable, hub, update, step_end] and
+ * *steps with the number of steps timed, then resets the accumulators. */
 tsat_status tsat_set_profiling(tsat_ctx ctx, int32_t enable);
-tsat_status tsat_kernel_times(tsat_ctx ctx, double* ms4, int64_t* steps);
+tsat_status tsat_kernel_times(tsat_ctx ctx, double* ms5, int64_t* steps);
 
-/* Number of CUDA kernels one iteration launches (for launch accounting). */
+/* Number of CUDA kernels one iteration launches (for launch accounting; the
+ * hub pre-pass only runs when the instance has hub variables). */
 tsat_status tsat_kernels_per_step(tsat_ctx ctx, int32_t* n);
 
 /* Last error message on ctx (static storage owned by ctx, valid until the next call). */

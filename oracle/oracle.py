@@ -140,11 +140,13 @@ def smoothmin_direct(col, tau):
     return lib().or_smoothmin_direct(len(c), _p(c), tau)
 
 
-def backward(cnf, R, g):
+def backward(cnf, R, g32):
+    """g32: the fp32 derivative table (R26)."""
     Nl = R.shape[1]
-    K = g.shape[1] - 1
+    K = g32.shape[1] - 1
     G = np.empty((cnf.V, Nl), np.float64)
-    lib().or_backward(cnf.V, cnf.C, _p(cnf.clause_ptr), _p(cnf.lits), Nl, K, _p(R), _p(np.ascontiguousarray(g)), _p(G))
+    g32 = np.ascontiguousarray(g32, np.float32)
+    lib().or_backward(cnf.V, cnf.C, _p(cnf.clause_ptr), _p(cnf.lits), Nl, K, _p(R), _p(g32), _p(G))
     return G
 
 
@@ -211,7 +213,8 @@ class StepOut:
     h: np.ndarray             # Nl x (K+1)
     unsat: np.ndarray         # Nl
     S: np.ndarray             # Nl
-    g: np.ndarray             # Nl x (K+1)
+    g: np.ndarray             # Nl x (K+1) fp64 (Eq. 4 derivative)
+    g32: np.ndarray           # Nl x (K+1) fp32 table used by the backward (R26)
     loss: float               # -sum_n S_n over ALL candidates
     G: np.ndarray             # V x Nl (pre-Jacobian variable gradient)
     grad: np.ndarray          # V x Nl fp32 (post-Jacobian)
@@ -296,12 +299,13 @@ class Oracle:
         unsat = h[:, 0].copy()
         # Eq. 4 / Eq. 3
         S, g, rmin = smoothmin(h, cfg.tau)
+        g32 = g.astype(np.float32)                 # R26: rounded once to fp32
         Sall = self.comm.gather_f64(S)
         loss = -float(sum(float(x) for x in Sall))
-        gmax = self.comm.max(L.or_gmax(Nl, K, _p(g), _p(rmin)))
+        gmax = self.comm.max(L.or_gmax(Nl, K, _p(g32), _p(rmin)))
         thmax = self.comm.max(L.or_abs_max(self.theta.size, _p(self.theta)))
         # STE backward and Eq. 5 Jacobian
-        G = backward(cnf, R, g)
+        G = backward(cnf, R, g32)
         I = np.empty(V, np.int64); s = np.empty(V, np.int32); valid = np.empty(V, np.uint8)
         L.or_jacobian_partial(V, Nl, _p(G), _p(self.theta), _p(self.occ), self.N, gmax, thmax, _p(I), _p(s), _p(valid))
         I = self.comm.sum_i64(I)
@@ -318,6 +322,6 @@ class Oracle:
         L.or_adamw(V, self.n0, Nl, _p(self.theta), _p(self.m), _p(self.v), _p(grad), t, lr,
                    cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, cfg.noise_sigma, self.seed)
         self.t = t + 1
-        return StepOut(t=t, bits=b, R=R, h=h, unsat=unsat, S=S, g=g, loss=loss, G=G, grad=grad,
+        return StepOut(t=t, bits=b, R=R, h=h, unsat=unsat, S=S, g=g, g32=g32, loss=loss, G=G, grad=grad,
                        J=J, d=d, gmax=gmax, thmax=thmax, best_unsat=best_unsat, best_idx=best_idx,
                        lr=lr, extra=dict(Q=Q, mu=mu, rho=rho, guard=guard, cv=cv, rmin=rmin, I=I, s=s))

@@ -225,10 +225,12 @@ double or_smoothmin_direct(int C, const int32_t* Rcol, double tau)
  * gradient folds as dL/dA_pos - dL/dA_neg:
  *   G_vn = sum_{c contains -v} g_n[R_cn] - sum_{c contains +v} g_n[R_cn].
  * Equal terms are grouped by value (exact integer counts, R12):
- *   G_vn = sum_r (cneg_vn[r] - cpos_vn[r]) g_n[r], ascending r.
+ *   G_vn = sum_r (cneg_vn[r] - cpos_vn[r]) g_n[r], ascending r,
+ * with g the fp32 table (R26: g rounded once to fp32, the paper's tensor
+ * precision; each product count * g is exact in fp64).
  * occ lists (variable -> (clause, sign)) are built here from the CNF. */
 void or_backward(int V, int C, const int64_t* cptr, const int32_t* lits, int Nl, int K,
-                 const uint8_t* R, const double* g, double* G)
+                 const uint8_t* R, const float* g, double* G)
 {
     /* transpose: count occurrences per variable */
     int64_t* vptr = (int64_t*)calloc((size_t)V + 1, sizeof(int64_t));
@@ -257,7 +259,7 @@ void or_backward(int V, int C, const int64_t* cptr, const int32_t* lits, int Nl,
         for (int j = 0; j < Nl; ++j) {
             double acc = 0.0;
             for (int r = 0; r <= K; ++r)
-                acc = acc + (double)cnt[(size_t)j * (K + 1) + r] * g[(size_t)j * (K + 1) + r];
+                acc = acc + (double)cnt[(size_t)j * (K + 1) + r] * (double)g[(size_t)j * (K + 1) + r];
             G[(size_t)v * Nl + j] = acc;
         }
     }
@@ -395,13 +397,13 @@ float or_abs_max(size_t n, const float* x)
     return mx;
 }
 
-/* gmax = max over candidates and r in [rmin_n, K] of |g_n[r]|. */
-double or_gmax(int Nl, int K, const double* g, const int32_t* rmin)
+/* gmax = max over candidates and r in [rmin_n, K] of |g_n[r]| (fp32 table). */
+double or_gmax(int Nl, int K, const float* g, const int32_t* rmin)
 {
     double mx = 0.0;
     for (int j = 0; j < Nl; ++j)
         for (int r = rmin[j]; r <= K; ++r) {
-            double a = fabs(g[(size_t)j * (K + 1) + r]);
+            double a = fabs((double)g[(size_t)j * (K + 1) + r]);
             if (a > mx) mx = a;
         }
     return mx;

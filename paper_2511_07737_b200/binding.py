@@ -286,7 +286,7 @@ class Solver:
         self._check(self.lib.tsat_set_profiling(self.h, 1 if on else 0))
 
     def kernel_times(self):
-        ms = np.zeros(4, np.float64)
+        ms = np.zeros(5, np.float64)
         st = ct.c_int64()
         self._check(self.lib.tsat_kernel_times(self.h, _ptr(ms), ct.byref(st)))
         return ms, st.value

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libturbosat.so")
-SOURCES = ["capi.cu", "kernels.cu", "host_cnf.cpp"]
+SOURCES = ["capi.cu", "launch.cu", "k_clause.cu", "k_misc.cu", "k_update.cu", "host_cnf.cpp"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -18,10 +18,11 @@
 
 using namespace tsat;
 
-constexpr int kKernelsPerStep = 4;
-
 struct DevCnf {
     uint32_t *cptr = nullptr, *clit = nullptr, *occ_ptr = nullptr, *occ_rec = nullptr, *occ_cnt = nullptr;
+    int2* occ_pn = nullptr;
+    int* hub_of = nullptr;
+    int4* hub_sc = nullptr;
 };
 
 struct tsat_ctx_s {
@@ -55,7 +56,10 @@ struct tsat_ctx_s {
     // profiling
     bool profiling = false;
     std::vector<cudaEvent_t> events;    // (kKernelsPerStep+1) per step of the largest k
-    double prof_ms[kKernelsPerStep] = {0, 0, 0, 0};
+    double prof_ms[kKernelsPerStep] = {0, 0, 0, 0, 0};
+    // k_update launch geometry (configure_kernels)
+    int upd_mode = 0, upd_GT = 0, upd_NG = 0, upd_grid = 0, num_sms = 0;
+    size_t upd_smem = 0;
     int64_t prof_steps = 0;
     int prof_pending_k = 0;
 };
@@ -89,7 +93,7 @@ tsat_status cuda_fail(tsat_ctx c, cudaError_t e, const char* where) {
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
-Layout make_layout(int V, int N, int KB) {
+Layout make_layout(int V, int N, int KB, int n_hubs) {
     Layout L{};
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -104,7 +108,7 @@ Layout make_layout(int V, int N, int KB) {
     L.A0 = take((size_t)V * NW * 4);
     L.A1 = take((size_t)V * NW * 4);
     L.hist = take((size_t)N * KB * 4);
-    L.gtab = take((size_t)N * KB * 8);
+    L.gtab = take((size_t)N * KB * 4);
     L.S = take((size_t)N * 8);
     L.unsat = take((size_t)N * 4);
     L.rowQ = take((size_t)V * 8);
@@ -114,6 +118,7 @@ Layout make_layout(int V, int N, int KB) {
     L.scal = take(sizeof(DevScalars));
     L.steptab = take(sizeof(StepScalars) * kMaxStepsPerCall);
     L.sol = take((size_t)V);
+    L.hubD = take((size_t)n_hubs * (KB - 1) * N * 4);
     L.total = off;
     return L;
 }
@@ -129,7 +134,8 @@ StepArgs step_args(tsat_ctx ctx) {
     a.A1 = (uint32_t*)(w + L.A1);
     a.hist = (int*)(w + L.hist);
     a.unsat = (int*)(w + L.unsat);
-    a.gtab = (double*)(w + L.gtab);
+    a.gtab = (float*)(w + L.gtab);
+    a.hubD = (int*)(w + L.hubD);
     a.S = (double*)(w + L.S);
     a.rowQ = (long long*)(w + L.rowQ);
     a.rowD = (double*)(w + L.rowD);
@@ -142,6 +148,18 @@ StepArgs step_args(tsat_ctx ctx) {
     a.occ_ptr = ctx->dcnf.occ_ptr;
     a.occ_rec = ctx->dcnf.occ_rec;
     a.occ_cnt = ctx->dcnf.occ_cnt;
+    a.occ_pn = ctx->dcnf.occ_pn;
+    a.hub_of = ctx->dcnf.hub_of;
+    a.hub_sc = ctx->dcnf.hub_sc;
+    a.n_hubs = ctx->cnf.n_hubs;
+    a.n_hub_sc = ctx->cnf.n_hub_sc;
+    a.uniform_len = ctx->cnf.uniform_len;
+    a.num_sms = ctx->num_sms;
+    a.upd_mode = ctx->upd_mode;
+    a.upd_GT = ctx->upd_GT;
+    a.upd_NG = ctx->upd_NG;
+    a.upd_grid = ctx->upd_grid;
+    a.upd_smem = ctx->upd_smem;
     a.V = ctx->cnf.V;
     a.N = ctx->N;
     a.C = ctx->cnf.C;
@@ -184,6 +202,9 @@ void free_cnf(tsat_ctx ctx) {
     cudaFree(ctx->dcnf.occ_ptr);
     cudaFree(ctx->dcnf.occ_rec);
     cudaFree(ctx->dcnf.occ_cnt);
+    cudaFree(ctx->dcnf.occ_pn);
+    cudaFree(ctx->dcnf.hub_of);
+    cudaFree(ctx->dcnf.hub_sc);
     ctx->dcnf = DevCnf{};
     ctx->have_cnf = false;
 }
@@ -225,6 +246,16 @@ tsat_status upload_cnf(tsat_ctx ctx, HostCnf&& h) {
     CK(up(&ctx->dcnf.occ_ptr, c.occ_ptr));
     CK(up(&ctx->dcnf.occ_rec, c.occ_rec));
     CK(up(&ctx->dcnf.occ_cnt, c.occ_cnt));
+    auto upi = [&](void** dst, const std::vector<int32_t>& src) -> cudaError_t {
+        size_t bytes = std::max<size_t>(src.size(), 4) * 4;
+        cudaError_t e = cudaMalloc(dst, bytes);
+        if (e != cudaSuccess) return e;
+        if (!src.empty()) e = cudaMemcpyAsync(*dst, src.data(), src.size() * 4, cudaMemcpyHostToDevice, ctx->stream);
+        return e;
+    };
+    CK(upi((void**)&ctx->dcnf.occ_pn, c.occ_pn));
+    CK(upi((void**)&ctx->dcnf.hub_of, c.hub_of));
+    CK(upi((void**)&ctx->dcnf.hub_sc, c.hub_sc));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->have_cnf = true;
     return TSAT_OK;
@@ -441,7 +472,7 @@ tsat_status tsat_workspace_bytes(tsat_ctx ctx, int64_t N_global, size_t* bytes) 
     if (N_global >= (1LL << 32)) return fail(ctx, TSAT_E_RANGE, "N_global >= 2^32");
     if ((size_t)N * 12 > 200 * 1024) return fail(ctx, TSAT_E_RANGE, "N per GPU > 17066 not supported by the fused update");
     int KB = ctx->cnf.K <= 3 ? 4 : 8;
-    *bytes = make_layout(ctx->cnf.V, (int)N, KB).total;
+    *bytes = make_layout(ctx->cnf.V, (int)N, KB, ctx->cnf.n_hubs).total;
     return TSAT_OK;
 }
 
@@ -466,7 +497,7 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
     ctx->seed = seed;
     ctx->ws = (char*)ws;
     ctx->ws_bytes = bytes;
-    ctx->L = make_layout(ctx->cnf.V, ctx->N, ctx->KB);
+    ctx->L = make_layout(ctx->cnf.V, ctx->N, ctx->KB, ctx->cnf.n_hubs);
     MethodConsts& mc = ctx->mc;
     mc = MethodConsts{};
     for (int d = 0; d < 8; ++d) mc.E[d] = std::exp(-c.tau * (double)d);
@@ -481,8 +512,19 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
     ctx->t = 0;
     ctx->steps_done = 0;
     CK(cudaSetDevice(ctx->device));
-    CK(configure_kernels(ctx->N));
+    {
+        StepArgs g = step_args(ctx);
+        CK(configure_kernels(&g));
+        ctx->upd_mode = g.upd_mode;
+        ctx->upd_GT = g.upd_GT;
+        ctx->upd_NG = g.upd_NG;
+        ctx->upd_grid = g.upd_grid;
+        ctx->upd_smem = g.upd_smem;
+        ctx->num_sms = g.num_sms;
+    }
     StepArgs a = step_args(ctx);
+    if (ctx->L.hubD != ctx->L.total)
+        CK(cudaMemsetAsync(ctx->ws + ctx->L.hubD, 0, ctx->L.total - ctx->L.hubD, ctx->stream));
     CK(cudaMemsetAsync(ctx->ws + ctx->L.hist, 0, (size_t)ctx->N * ctx->KB * 4, ctx->stream));
     CK(cudaMemsetAsync(ctx->ws + ctx->L.scal, 0, sizeof(DevScalars), ctx->stream));
     DevScalars init{};
@@ -631,7 +673,7 @@ tsat_status tsat_debug_copy(tsat_ctx ctx, int32_t which, void* dst, size_t bytes
     const int N = ctx->N, V = ctx->cnf.V;
     switch (which) {
         case 0: return fail(ctx, TSAT_E_UNSUPPORTED, "histogram is cleared after use; query unsat instead");
-        case 1: off = ctx->L.gtab; sz = (size_t)N * ctx->KB * 8; break;
+        case 1: off = ctx->L.gtab; sz = (size_t)N * ctx->KB * 4; break;
         case 2: off = ctx->L.S; sz = (size_t)N * 8; break;
         case 3: off = ((ctx->t - 1) & 1) ? ctx->L.A1 : ctx->L.A0; sz = (size_t)V * (N / 32) * 4; break;
         case 4: off = ctx->L.rowQ; sz = (size_t)V * 8; break;
@@ -711,13 +753,13 @@ tsat_status tsat_set_profiling(tsat_ctx ctx, int32_t enable) {
     return TSAT_OK;
 }
 
-tsat_status tsat_kernel_times(tsat_ctx ctx, double* ms4, int64_t* steps) {
+tsat_status tsat_kernel_times(tsat_ctx ctx, double* ms5, int64_t* steps) {
     GUARD_CTX();
     CK(cudaStreamSynchronize(ctx->stream));
     tsat_status s = collect_profile(ctx);
     if (s != TSAT_OK) return s;
     for (int i = 0; i < kKernelsPerStep; ++i) {
-        if (ms4) ms4[i] = ctx->prof_ms[i];
+        if (ms5) ms5[i] = ctx->prof_ms[i];
         ctx->prof_ms[i] = 0;
     }
     if (steps) *steps = ctx->prof_steps;
@@ -728,7 +770,13 @@ tsat_status tsat_kernel_times(tsat_ctx ctx, double* ms4, int64_t* steps) {
 tsat_status tsat_kernels_per_step(tsat_ctx ctx, int32_t* n) {
     GUARD_CTX();
     if (!n) return TSAT_E_ARG;
-    *n = kKernelsPerStep;
+    int k = 0;
+    if (ctx->have_cnf && ctx->cnf.C > 0) ++k;                                  // clause
+    k += 1;                                                                     // gtable
+    if (ctx->have_batch && ctx->upd_mode == 0 && ctx->cnf.n_hub_sc > 0) ++k;    // hub
+    if (ctx->have_cnf && ctx->cnf.V > 0) ++k;                                  // update
+    k += 1;                                                                     // step end
+    *n = k;
     return TSAT_OK;
 }
 

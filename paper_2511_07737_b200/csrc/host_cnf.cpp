@@ -211,6 +211,33 @@ int build_cnf(int32_t V, int64_t C, const int64_t* ptr, const int32_t* lits, Hos
             fill[v] += len;
         }
     }
+    // signed-count classes and hub super-chunks (see tsat_internal.h)
+    h.occ_pn.assign((size_t)V * 2, 0);
+    for (int64_t i = 0; i < h.nnz; ++i) {
+        uint32_t code = h.clause_lit[i];
+        h.occ_pn[(size_t)(code >> 1) * 2 + (code & 1u)] += 1;
+    }
+    h.hub_of.assign((size_t)V, -1);
+    for (int32_t v = 0; v < V; ++v) {
+        bool hub = h.occ_pn[2 * v] > 127 || h.occ_pn[2 * v + 1] > 127 || (h.occ_ptr[v + 1] - h.occ_ptr[v]) > (uint32_t)kRecCap;
+        if (!hub) continue;
+        int32_t hid = h.n_hubs++;
+        h.hub_of[v] = hid;
+        uint32_t p = h.occ_ptr[v], e = h.occ_ptr[v + 1], b = p;
+        int cnt = 0;
+        while (p < e) {
+            p += h.occ_rec[p] >> 1;
+            if (++cnt == kHubSlab || p >= e) {
+                h.hub_sc.insert(h.hub_sc.end(), {hid, v, (int32_t)b, (int32_t)p});
+                b = p;
+                cnt = 0;
+            }
+        }
+    }
+    h.n_hub_sc = (int32_t)(h.hub_sc.size() / 4);
+    h.uniform_len = 1;
+    for (int64_t c = 0; c < C; ++c)
+        if ((int32_t)(h.clause_ptr[c + 1] - h.clause_ptr[c]) != h.K) { h.uniform_len = 0; break; }
     *out = std::move(h);
     return 0;
 }

@@ -1,0 +1,544 @@
+// k_update.cu - rows (a7) STE backward, (a8) Eq. 5 Jacobian, (a9) AdamW +
+// re-binarisation, fused (§3.2 l.189-191, l.226; §4.1 l.255-269).
+//
+// k_update (fused, persistent): one CTA per SM holds the fp32 derivative
+// table g[r][n] of the whole batch in shared memory (loaded once per launch);
+// its warp groups pull rows v from a global counter.  For a row:
+//  1. gather (word-major, lane = 32-candidate word): for every occurrence of
+//     v the clause's R_cn is recomputed from the bit planes of the evaluated
+//     state (coalesced 128-byte gathers, no R matrix in HBM) and the one-hot
+//     masks [R = r] are added (+ for a negated occurrence, - for a positive
+//     one) to 8-bit two's-complement vertical counters d_r = cneg - cpos;
+//  2. a 32x32 bit transpose turns the counter planes into one packed word of
+//     signed bytes per candidate, staged in shared memory;
+//  3. candidate-major (float4 streams of theta, m, v): G = sum_r d_r g[r]
+//     (fp64, exact products), J_v = sum G theta in int64 fixed point (group
+//     reduction), c_v, grad = (float)(G rho - c), AdamW, Q_{t+1}, max|theta|,
+//     and the sign planes of theta_{t+1} -> bits of the next state.
+// Rows whose counts can leave int8 ("hubs", SURVEY §7 hard parts) get their
+// counts from k_hub, which splits a hub's occurrences over many CTAs and adds
+// exact int32 counts (integer atomics: order-free, deterministic).
+#include "device_common.cuh"
+
+namespace tsat {
+
+namespace {
+constexpr int kCtr = 8;        // counter planes (int8) in the fused kernel
+constexpr int kHubCtr = 11;    // counter planes (int11) in k_hub (kHubSlab = 1023 occurrences)
+
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) / 16 * 16; }
+}  // namespace
+
+// Shared-memory geometry of k_update (host and device agree through this).
+__host__ __device__ inline size_t upd_gs_bytes(int KB, int N) { return align16((size_t)KB * N * 4); }
+__host__ __device__ inline size_t upd_dpk_words(int N) { return (size_t)N + (N >> 5); }
+__host__ __device__ inline size_t upd_group_bytes(int KB, int N) {
+    const int NDW = KB == 4 ? 1 : 2;
+    return align16((size_t)NDW * upd_dpk_words(N) * 4) + (size_t)kRecCap * 4 + align16((size_t)2 * (N >> 5) * 4) + 128;
+}
+
+// Signed per-bin counts of candidate n of the current row.
+template <int KB>
+__device__ __forceinline__ void load_counts(int (&d)[KB], const uint32_t* dpk, size_t dpk_words, const int* hubrow,
+                                            int N, int n, int dsum, bool hub) {
+    int acc = 0;
+    if (hub) {
+#pragma unroll
+        for (int r = 0; r < KB - 1; ++r) { d[r] = hubrow[(size_t)r * N + n]; acc += d[r]; }
+    } else {
+        const uint32_t p0 = dpk[n + (n >> 5)];
+#pragma unroll
+        for (int r = 0; r < 4 && r < KB - 1; ++r) { d[r] = (int)(signed char)((p0 >> (8 * r)) & 0xffu); acc += d[r]; }
+        if (KB == 8) {
+            const uint32_t p1 = dpk[dpk_words + n + (n >> 5)];
+#pragma unroll
+            for (int r = 4; r < KB - 1; ++r) { d[r] = (int)(signed char)((p1 >> (8 * (r - 4))) & 0xffu); acc += d[r]; }
+        }
+    }
+    d[KB - 1] = dsum - acc;
+}
+
+template <int KB>
+__device__ __forceinline__ double fold_G(const int (&d)[KB], const float* gs, int N, int n) {
+    double G = 0.0;
+#pragma unroll
+    for (int r = 0; r < KB; ++r) G = G + (double)d[r] * (double)gs[(size_t)r * N + n];
+    return G;
+}
+
+template <int KB>
+__global__ void __launch_bounds__(512, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
+                                                    uint32_t* __restrict__ Anext, const StepScalars* __restrict__ sc) {
+    constexpr int NP = (KB == 4) ? 2 : 3;
+    constexpr int NCTR = KB - 1;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int N = a.N, NW = N >> 5, GT = a.upd_GT;
+    const size_t dpkw = upd_dpk_words(N);
+    float* gs = reinterpret_cast<float*>(smem);
+    const int grp = threadIdx.x / GT, tg = threadIdx.x - grp * GT;
+    unsigned char* gb = smem + upd_gs_bytes(KB, N) + (size_t)grp * upd_group_bytes(KB, N);
+    uint32_t* dpk = reinterpret_cast<uint32_t*>(gb);
+    uint32_t* rec = reinterpret_cast<uint32_t*>(gb + align16((size_t)(KB == 4 ? 1 : 2) * dpkw * 4));
+    uint32_t* posw = rec + kRecCap;
+    uint32_t* negw = posw + NW;
+    long long* red = reinterpret_cast<long long*>(gb + upd_group_bytes(KB, N) - 128);   // 4 + 4 slots
+    float* redf = reinterpret_cast<float*>(red + 8);                                    // 4 slots
+    double* bcast = reinterpret_cast<double*>(redf + 4);                                // 2 slots
+    int* rowslot = reinterpret_cast<int*>(bcast + 2);
+    const int bar = 1 + grp;
+    const int lane = threadIdx.x & 31, gw = tg >> 5, ngw = GT >> 5;
+
+    // fp32 derivative table of the whole batch -> shared memory
+    for (int i = threadIdx.x * 4; i < KB * N; i += blockDim.x * 4)
+        *reinterpret_cast<float4*>(gs + i) = *reinterpret_cast<const float4*>(a.gtab + i);
+    __syncthreads();
+
+    const long long t = sc->t;
+    const double gmax = __longlong_as_double((long long)a.ds->gmax_bits);
+    const float thmax = __uint_as_float(a.ds->thmax_bits[t & 1]);
+    const float wdf = sc->wdf, a1 = sc->a1, b2f = sc->b2f, a2 = sc->a2, nss = sc->nss, bc2s = sc->bc2s,
+                epsf = sc->epsf, nz = sc->nz;
+    const MethodConsts& mc = a.mc;
+
+    while (true) {
+        if (tg == 0) *rowslot = atomicAdd(&a.ds->row_counter, 1);
+        group_bar(bar, GT);
+        const int v = *rowslot;
+        if (v >= a.V) break;
+        const int hub = a.hub_of[v];
+        const int2 pn = a.occ_pn[v];
+        const int dsum = pn.y - pn.x;                       // sum_r (cneg - cpos)[r]
+        const unsigned rb = a.occ_ptr[v], re = a.occ_ptr[v + 1];
+        const double rho = a.rowRho[v];
+        const unsigned char guard = a.rowGuard[v];
+        const int occ = pn.x + pn.y;
+        int s = 0;
+        bool jvalid = false;
+        {
+            double x = (double)mc.Nglobal * (double)occ;
+            x = x * gmax;
+            x = x * (double)thmax;
+            if (occ > 0 && x > 0.0) { jvalid = true; s = 61 - ceil_log2(x); }
+        }
+        const int* hubrow = hub >= 0 ? a.hubD + (size_t)hub * NCTR * N : nullptr;
+        float* trow = a.theta + (size_t)v * N;
+        float* mrow = a.m + (size_t)v * N;
+        float* vrow = a.v + (size_t)v * N;
+
+        // ---- 1+2: bit-sliced gather of the row's occurrences, transpose to bytes
+        if (hub < 0) {
+            const unsigned nrec = re - rb;
+            for (unsigned i = tg; i < nrec; i += GT) rec[i] = a.occ_rec[rb + i];
+            group_bar(bar, GT);
+            for (int w = tg; w < NW; w += GT) {
+                const uint32_t own = __ldg(Acur + (size_t)v * NW + w);
+                uint32_t cnt[NCTR][kCtr];
+#pragma unroll
+                for (int r = 0; r < NCTR; ++r)
+#pragma unroll
+                    for (int b = 0; b < kCtr; ++b) cnt[r][b] = 0u;
+                for (unsigned p = 0; p < nrec;) {
+                    const uint32_t hdr = rec[p];
+                    const uint32_t len = hdr >> 1;
+                    uint32_t sp[NP];
+                    sp[0] = own ^ (0u - (hdr & 1u));
+#pragma unroll
+                    for (int q = 1; q < NP; ++q) sp[q] = 0u;
+                    for (uint32_t i = 1; i < len; ++i) {
+                        const uint32_t code = rec[p + i];
+                        bs_add<NP>(sp, __ldg(Acur + (size_t)(code >> 1) * NW + w) ^ (0u - (code & 1u)));
+                    }
+                    if (hdr & 1u) {
+#pragma unroll
+                        for (int r = 0; r < NCTR; ++r) vc_inc<kCtr>(cnt[r], bs_eq<NP>(sp, r));
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < NCTR; ++r) vc_dec<kCtr>(cnt[r], bs_eq<NP>(sp, r));
+                    }
+                    p += len;
+                }
+                uint32_t T[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) T[i] = (i / kCtr < NCTR && i / kCtr < 4) ? cnt[i / kCtr][i % kCtr] : 0u;
+                transpose32(T);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) dpk[33 * w + j] = T[j];
+                if (KB == 8) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) T[i] = (4 + i / kCtr < NCTR) ? cnt[4 + i / kCtr][i % kCtr] : 0u;
+                    transpose32(T);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) dpk[dpkw + 33 * w + j] = T[j];
+                }
+            }
+        }
+        group_bar(bar, GT);
+
+        // ---- 3a: J_v = sum_n G theta (int64 fixed point)
+        long long I = 0;
+        for (int base = 0; base < N; base += 4 * GT) {
+            const int n = base + 4 * tg;
+            if (n < N) {
+                const float4 th4 = *reinterpret_cast<const float4*>(trow + n);
+                const float th[4] = {th4.x, th4.y, th4.z, th4.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    int d[KB];
+                    load_counts<KB>(d, dpk, dpkw, hubrow, N, n + q, dsum, hub >= 0);
+                    const double G = fold_G<KB>(d, gs, N, n + q);
+                    if (jvalid) I += __double2ll_rn(scalbn(G * (double)th[q], s));
+                }
+            }
+        }
+        I = warp_sum(I);
+        if (lane == 0) red[gw] = I;
+        group_bar(bar, GT);
+        if (tg == 0) {
+            long long tot = 0;
+            for (int i = 0; i < ngw; ++i) tot += red[i];
+            double J = jvalid ? scalbn((double)tot, -s) : 0.0;
+            double c = 0.0;
+            if (mc.normalize && !guard) {
+                c = J / (double)mc.Nglobal;
+                c = c * rho;
+                c = c * rho;
+            }
+            bcast[0] = c;
+        }
+        group_bar(bar, GT);
+        const double c = bcast[0];
+
+        // ---- 3b: grad, AdamW, next-state statistics and sign planes
+        long long Qn = 0;
+        float mx = 0.0f;
+        for (int base = 0; base < N; base += 4 * GT) {
+            const int n = base + 4 * tg;
+            unsigned pnib = 0, nnib = 0;
+            if (n < N) {
+                float4 th4 = *reinterpret_cast<const float4*>(trow + n);
+                float4 m4 = *reinterpret_cast<const float4*>(mrow + n);
+                float4 v4 = *reinterpret_cast<const float4*>(vrow + n);
+                float th[4] = {th4.x, th4.y, th4.z, th4.w};
+                float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+                float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    int d[KB];
+                    load_counts<KB>(d, dpk, dpkw, hubrow, N, n + q, dsum, hub >= 0);
+                    const double G = fold_G<KB>(d, gs, N, n + q);
+                    const float g = (float)(G * rho - c);
+                    float x = th[q] * wdf;
+                    const float mn = __fmaf_rn(a1, g - mm[q], mm[q]);
+                    const float vb = vv[q] * b2f;
+                    const float vn = __fmaf_rn(a2 * g, g, vb);
+                    const float den = __fsqrt_rn(vn) / bc2s + epsf;
+                    x = x + (nss * mn) / den;
+                    if (mc.noise) {
+                        const long long ng = mc.n0 + n + q;
+                        uint32_t xr[4] = {(uint32_t)(ng >> 2), (uint32_t)v, (uint32_t)(1 + t), 0u};
+                        philox4x32_10(xr, (uint32_t)mc.seed, (uint32_t)(mc.seed >> 32));
+                        const float xi = (float)(xr[ng & 3] >> 8) * 5.9604644775390625e-08f - 0.5f;
+                        x = x + nz * xi;
+                    }
+                    th[q] = x; mm[q] = mn; vv[q] = vn;
+                    Qn += __double2ll_rn((double)x * 4294967296.0);
+                    mx = fmaxf(mx, fabsf(x));
+                    pnib |= (x > 0.0f ? 1u : 0u) << q;
+                    nnib |= (x < 0.0f ? 1u : 0u) << q;
+                }
+                *reinterpret_cast<float4*>(trow + n) = make_float4(th[0], th[1], th[2], th[3]);
+                *reinterpret_cast<float4*>(mrow + n) = make_float4(mm[0], mm[1], mm[2], mm[3]);
+                *reinterpret_cast<float4*>(vrow + n) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+                if (hub >= 0) {
+                    int* hr = a.hubD + (size_t)hub * NCTR * N;
+#pragma unroll
+                    for (int r = 0; r < NCTR; ++r) *reinterpret_cast<int4*>(hr + (size_t)r * N + n) = make_int4(0, 0, 0, 0);
+                }
+            }
+            // 8 lanes x 4 candidates = one 32-candidate word
+            unsigned pw = pnib << (4 * (lane & 7)), nw = nnib << (4 * (lane & 7));
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                pw |= __shfl_xor_sync(0xffffffffu, pw, o);
+                nw |= __shfl_xor_sync(0xffffffffu, nw, o);
+            }
+            if ((lane & 7) == 0 && n < N) { posw[n >> 5] = pw; negw[n >> 5] = nw; }
+        }
+        Qn = warp_sum(Qn);
+        mx = warp_maxf(mx);
+        if (lane == 0) { red[4 + gw] = Qn; redf[gw] = mx; }
+        group_bar(bar, GT);
+        if (tg == 0) {
+            long long tot = 0;
+            float m2 = 0.0f;
+            for (int i = 0; i < ngw; ++i) { tot += red[4 + i]; m2 = fmaxf(m2, redf[i]); }
+            double dn, rhon;
+            unsigned char gn;
+            row_finish(tot, mc, &dn, &rhon, &gn);
+            a.rowQ[v] = tot; a.rowD[v] = dn; a.rowRho[v] = rhon; a.rowGuard[v] = gn;
+            bcast[1] = dn;
+            atomicMax(&a.ds->thmax_bits[(t + 1) & 1], __float_as_uint(m2));
+            const unsigned long long bk = a.ds->best_key;
+            if ((bk >> 32) == 0ull && a.ds->sol_step < 0) {          // first model: keep its bits (A22)
+                const long long idx = (long long)(bk & 0xffffffffull) - mc.n0;
+                if (idx >= 0 && idx < N)
+                    a.sol[v] = (unsigned char)((Acur[(size_t)v * NW + (idx >> 5)] >> (idx & 31)) & 1u);
+            }
+        }
+        group_bar(bar, GT);
+        const bool dpos = bcast[1] > 0.0;
+        for (int w = tg; w < NW; w += GT) Anext[(size_t)v * NW + w] = dpos ? posw[w] : negw[w];
+        // (the next row's first group_bar orders these smem reads before reuse)
+    }
+}
+
+// ------------------------------------------------------------------ hub pre-pass
+// One warp per (32-word block, hub super-chunk of <= kHubSlab occurrences):
+// 11-bit signed vertical counters, two counters per 32x32 transpose (16-bit
+// fields), then exact int32 atomic adds into hubD[hub][r][n].
+template <int KB>
+__global__ void __launch_bounds__(32) k_hub(StepArgs a, const uint32_t* __restrict__ Acur) {
+    constexpr int NP = (KB == 4) ? 2 : 3;
+    constexpr int NCTR = KB - 1;
+    __shared__ int sh[NCTR][1024 + 32];
+    const int lane = threadIdx.x;
+    const int NW = a.N >> 5;
+    const int w = blockIdx.x * 32 + lane;
+    const bool valid = w < NW;
+    const int4 sc = a.hub_sc[blockIdx.y];          // hub, var, rec_begin, rec_end
+    const int v = sc.y;
+    const uint32_t own = valid ? __ldg(Acur + (size_t)v * NW + w) : 0u;
+    uint32_t cnt[NCTR][kHubCtr];
+#pragma unroll
+    for (int r = 0; r < NCTR; ++r)
+#pragma unroll
+        for (int b = 0; b < kHubCtr; ++b) cnt[r][b] = 0u;
+    const size_t wofs = valid ? (size_t)w : 0;
+    for (unsigned p = (unsigned)sc.z; p < (unsigned)sc.w;) {
+        const uint32_t hdr = __ldg(a.occ_rec + p);
+        const uint32_t len = hdr >> 1;
+        uint32_t sp[NP];
+        sp[0] = own ^ (0u - (hdr & 1u));
+#pragma unroll
+        for (int q = 1; q < NP; ++q) sp[q] = 0u;
+        for (uint32_t i = 1; i < len; ++i) {
+            const uint32_t code = __ldg(a.occ_rec + p + i);
+            bs_add<NP>(sp, __ldg(Acur + (size_t)(code >> 1) * NW + wofs) ^ (0u - (code & 1u)));
+        }
+        if (hdr & 1u) {
+#pragma unroll
+            for (int r = 0; r < NCTR; ++r) vc_inc<kHubCtr>(cnt[r], bs_eq<NP>(sp, r));
+        } else {
+#pragma unroll
+            for (int r = 0; r < NCTR; ++r) vc_dec<kHubCtr>(cnt[r], bs_eq<NP>(sp, r));
+        }
+        p += len;
+    }
+    // two counters per transpose: 16-bit fields, bits 11..15 = sign extension
+#pragma unroll
+    for (int r0 = 0; r0 < NCTR; r0 += 2) {
+        uint32_t T[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const int r = r0 + i / 16, b = i % 16;
+            T[i] = (r < NCTR) ? cnt[r][b < kHubCtr ? b : kHubCtr - 1] : 0u;
+        }
+        transpose32(T);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            sh[r0][33 * lane + j] = (int)(short)(T[j] & 0xffffu);
+            if (r0 + 1 < NCTR) sh[r0 + 1][33 * lane + j] = (int)(short)(T[j] >> 16);
+        }
+    }
+    __syncwarp();
+    int* dst = a.hubD + (size_t)sc.x * NCTR * a.N;
+    for (int r = 0; r < NCTR; ++r)
+        for (int k = 0; k < 32; ++k) {
+            const int nl = 32 * k + lane;                  // candidate within the block (coalesced)
+            const int n = blockIdx.x * 1024 + nl;
+            const int val = sh[r][33 * k + lane];
+            if (n < a.N && val) atomicAdd(dst + (size_t)r * a.N + n, val);
+        }
+}
+
+// ------------------------------------------------------------------ fallback: one CTA per row
+// Used when the batch is too large for the fused kernel's shared memory.
+// Thread per candidate; R recomputed per occurrence with broadcast loads.
+template <int KB>
+__global__ void __launch_bounds__(256) k_update_rowcta(StepArgs a, const uint32_t* __restrict__ Acur,
+                                                       uint32_t* __restrict__ Anext,
+                                                       const StepScalars* __restrict__ sc) {
+    extern __shared__ double smem_d[];
+    const int N = a.N;
+    double* Gs = smem_d;
+    float* Ts = reinterpret_cast<float*>(smem_d + N);
+    __shared__ long long sh_s[32];
+    __shared__ float sh_m[32];
+    __shared__ double sh_c, sh_d;
+    const MethodConsts& mc = a.mc;
+    const int v = blockIdx.x;
+    const int NW = N >> 5;
+    const long long t = sc->t;
+    const unsigned rb = a.occ_ptr[v], re = a.occ_ptr[v + 1];
+    const unsigned occ = a.occ_cnt[v];
+    const double rho = a.rowRho[v];
+    const unsigned char guard = a.rowGuard[v];
+    const double gmax = __longlong_as_double((long long)a.ds->gmax_bits);
+    const float thmax = __uint_as_float(a.ds->thmax_bits[t & 1]);
+    int s = 0;
+    bool jvalid = false;
+    {
+        double x = (double)mc.Nglobal * (double)occ;
+        x = x * gmax;
+        x = x * (double)thmax;
+        if (occ > 0 && x > 0.0) { jvalid = true; s = 61 - ceil_log2(x); }
+    }
+    const uint32_t* Arow = Acur + (size_t)v * NW;
+    float* trow = a.theta + (size_t)v * N;
+    float* mrow = a.m + (size_t)v * N;
+    float* vrow = a.v + (size_t)v * N;
+    long long I = 0;
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+        const int w = n >> 5, j = n & 31;
+        const uint32_t own = (Arow[w] >> j) & 1u;
+        int cnt[KB];
+#pragma unroll
+        for (int r = 0; r < KB; ++r) cnt[r] = 0;
+        for (unsigned p = rb; p < re;) {
+            const uint32_t hdr = a.occ_rec[p];
+            const uint32_t len = hdr >> 1;
+            uint32_t R = own ^ (hdr & 1u);
+            for (uint32_t i = 1; i < len; ++i) {
+                const uint32_t code = a.occ_rec[p + i];
+                R += ((Acur[(size_t)(code >> 1) * NW + w] >> j) & 1u) ^ (code & 1u);
+            }
+            const int delta = (hdr & 1u) ? 1 : -1;
+#pragma unroll
+            for (int r = 0; r < KB; ++r) cnt[r] += (R == (uint32_t)r) ? delta : 0;
+            p += len;
+        }
+        double G = 0.0;
+#pragma unroll
+        for (int r = 0; r < KB; ++r) G = G + (double)cnt[r] * (double)a.gtab[(size_t)r * N + n];
+        Gs[n] = G;
+        if (jvalid) I += __double2ll_rn(scalbn(G * (double)trow[n], s));
+    }
+    float dummy = 0.0f;
+    block_sum_max(I, dummy, sh_s, sh_m);
+    if (threadIdx.x == 0) {
+        double J = jvalid ? scalbn((double)I, -s) : 0.0;
+        double c = 0.0;
+        if (mc.normalize && !guard) {
+            c = J / (double)mc.Nglobal;
+            c = c * rho;
+            c = c * rho;
+        }
+        sh_c = c;
+    }
+    __syncthreads();
+    const double c = sh_c;
+    long long Qn = 0;
+    float mx = 0.0f;
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+        const float g = (float)(Gs[n] * rho - c);
+        float th = trow[n] * sc->wdf;
+        const float m0 = mrow[n];
+        const float mm = __fmaf_rn(sc->a1, g - m0, m0);
+        const float vb = vrow[n] * sc->b2f;
+        const float vn = __fmaf_rn(sc->a2 * g, g, vb);
+        const float den = __fsqrt_rn(vn) / sc->bc2s + sc->epsf;
+        th = th + (sc->nss * mm) / den;
+        if (mc.noise) {
+            const long long ng = mc.n0 + n;
+            uint32_t x[4] = {(uint32_t)(ng >> 2), (uint32_t)v, (uint32_t)(1 + t), 0u};
+            philox4x32_10(x, (uint32_t)mc.seed, (uint32_t)(mc.seed >> 32));
+            const float xi = (float)(x[ng & 3] >> 8) * 5.9604644775390625e-08f - 0.5f;
+            th = th + sc->nz * xi;
+        }
+        trow[n] = th;
+        mrow[n] = mm;
+        vrow[n] = vn;
+        Ts[n] = th;
+        Qn += __double2ll_rn((double)th * 4294967296.0);
+        mx = fmaxf(mx, fabsf(th));
+    }
+    block_sum_max(Qn, mx, sh_s, sh_m);
+    if (threadIdx.x == 0) {
+        double dn, rhon;
+        unsigned char gn;
+        row_finish(Qn, mc, &dn, &rhon, &gn);
+        a.rowQ[v] = Qn; a.rowD[v] = dn; a.rowRho[v] = rhon; a.rowGuard[v] = gn;
+        sh_d = dn;
+        atomicMax(&a.ds->thmax_bits[(t + 1) & 1], __float_as_uint(mx));
+        const unsigned long long bk = a.ds->best_key;
+        if ((bk >> 32) == 0ull && a.ds->sol_step < 0) {
+            const long long idx = (long long)(bk & 0xffffffffull) - mc.n0;
+            if (idx >= 0 && idx < N) a.sol[v] = (unsigned char)((Arow[idx >> 5] >> (idx & 31)) & 1u);
+        }
+    }
+    __syncthreads();
+    const bool dpos = sh_d > 0.0;
+    uint32_t* Anrow = Anext + (size_t)v * NW;
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+        const float x = Ts[n];
+        const unsigned wv = __ballot_sync(0xffffffffu, dpos ? (x > 0.0f) : (x < 0.0f));
+        if ((threadIdx.x & 31) == 0) Anrow[n >> 5] = wv;
+    }
+}
+
+// ------------------------------------------------------------------ configuration + launch
+cudaError_t configure_update(StepArgs* a) {
+    const int N = a->N, NW = N >> 5, KB = a->KB;
+    int dev = 0, optin = 0, sms = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    a->num_sms = sms;
+    const int GT = NW >= 128 ? 128 : (NW > 32 ? 64 : 32);
+    const size_t gsb = upd_gs_bytes(KB, N), grb = upd_group_bytes(KB, N);
+    long long ng = optin > (long long)gsb ? ((long long)optin - (long long)gsb) / (long long)grb : 0;
+    ng = ng < 512 / GT ? ng : 512 / GT;
+    ng = ng < 15 ? ng : 15;                       // named barriers 1..15
+    if (ng < 2 && !(ng == 1 && GT == 128)) {
+        a->upd_mode = 1;                          // too large for the fused kernel
+        size_t smem = (size_t)N * (sizeof(double) + sizeof(float));
+        if ((e = cudaFuncSetAttribute(k_update_rowcta<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+        if ((e = cudaFuncSetAttribute(k_update_rowcta<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+        a->upd_smem = smem;
+        return cudaSuccess;
+    }
+    a->upd_mode = 0;
+    a->upd_GT = GT;
+    a->upd_NG = (int)ng;
+    a->upd_smem = gsb + (size_t)ng * grb;
+    a->upd_grid = sms;
+    if (KB == 4) e = cudaFuncSetAttribute(k_update<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a->upd_smem);
+    else e = cudaFuncSetAttribute(k_update<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a->upd_smem);
+    return e;
+}
+
+cudaError_t launch_hub(const StepArgs& a, const uint32_t* Acur, cudaStream_t st) {
+    if (a.n_hub_sc == 0) return cudaGetLastError();
+    const int NW = a.N >> 5;
+    dim3 grid((NW + 31) / 32, a.n_hub_sc);
+    if (a.KB == 4) k_hub<4><<<grid, 32, 0, st>>>(a, Acur);
+    else k_hub<8><<<grid, 32, 0, st>>>(a, Acur);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_update(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
+                          cudaStream_t st) {
+    if (a.V == 0) return cudaGetLastError();
+    if (a.upd_mode == 0) {
+        const int threads = a.upd_GT * a.upd_NG;
+        if (a.KB == 4) k_update<4><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
+        else k_update<8><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
+    } else {
+        if (a.KB == 4) k_update_rowcta<4><<<a.V, 256, a.upd_smem, st>>>(a, Acur, Anext, sc);
+        else k_update_rowcta<8><<<a.V, 256, a.upd_smem, st>>>(a, Acur, Anext, sc);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace tsat

@@ -1,5 +1,5 @@
 // tsat_internal.h - shared between the host runtime (capi.cu, host_cnf.cpp)
-// and the sm_100a kernels (kernels.cu).  Not part of the public ABI.
+// and the sm_100a kernels.  Not part of the public ABI.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -9,6 +9,13 @@
 #include <vector>
 
 namespace tsat {
+
+// ---------------------------------------------------------------- limits
+constexpr int kMaxK = 7;               // clause length supported by the kernels
+constexpr int kMaxStepsPerCall = 4096;
+constexpr int kTopkMax = 2048;         // export: k most confident variables per candidate
+constexpr int kRecCap = 2048;          // occurrence-record words a warp group stages per row
+constexpr int kHubSlab = 1023;         // occurrences per hub super-chunk (11-bit signed counters)
 
 // ---------------------------------------------------------------- host CNF
 // Literal code used on the device: (var << 1) | negated, var 0-based.
@@ -23,24 +30,28 @@ struct HostCnf {
     //   rec[0] = (len << 1) | own_negated, rec[1..len-1] = the other literal codes
     std::vector<uint32_t> occ_ptr;      // V+1 (word offsets into occ_rec)
     std::vector<uint32_t> occ_rec;
-    std::vector<uint32_t> occ_cnt;      // V: number of occurrences of the variable
+    std::vector<uint32_t> occ_cnt;      // V: occurrences of the variable
+    std::vector<int32_t> occ_pn;        // 2V: (positive, negative) occurrences
+    // hub rows: a variable whose signed per-bin counts may leave int8, or whose
+    // records exceed kRecCap, is counted by the k_hub pre-pass (int32).
+    std::vector<int32_t> hub_of;        // V: hub index or -1
+    std::vector<int32_t> hub_sc;        // 4 per super-chunk: hub, var, rec_begin, rec_end
+    int32_t n_hubs = 0;
+    int32_t n_hub_sc = 0;
     int64_t header_C = -1;
     int64_t n_warnings = 0, n_tautologies = 0, n_duplicates = 0;
     int32_t has_empty = 0;
+    int32_t uniform_len = 0;            // every clause has exactly K literals
 };
 
 // Parse DIMACS.  Returns 0 on success, 2 (TSAT_E_PARSE) with msg.
 int parse_dimacs(const char* text, size_t len, int32_t* V, std::vector<int64_t>* ptr,
                  std::vector<int32_t>* lits, int64_t* header_C, int64_t* n_warnings, std::string* msg);
 // Build HostCnf from signed-literal clause arrays (dedup, tautology count,
-// codes, occurrence records).  Returns 0, or TSAT_E_ARG / TSAT_E_RANGE with msg.
+// codes, occurrence records, hub tables).  Returns 0, or 1 (arg) / 3 (range).
 int build_cnf(int32_t V, int64_t C, const int64_t* ptr, const int32_t* lits, HostCnf* out, std::string* msg);
 
 // ---------------------------------------------------------------- device
-constexpr int kMaxK = 7;          // clause length supported by the kernels
-constexpr int kMaxStepsPerCall = 4096;
-constexpr int kTopkMax = 2048;     // export: k most confident variables per candidate
-
 // Per-iteration scalars, computed on the host (libm) and uploaded per call.
 struct StepScalars {
     int64_t t;        // iteration index of the evaluated state
@@ -60,11 +71,11 @@ struct DevScalars {
     unsigned long long best_key;     // min over candidates of (unsat << 32 | global idx)
     unsigned long long gmax_bits;    // max |g| (non-negative double bits)
     unsigned int thmax_bits[2];      // max |theta| of theta_t, indexed by t & 1
+    int row_counter;                 // k_update dynamic row scheduler
     int pad0;
     double loss;
     long long sol_step;              // first iteration with a 0-unsat candidate (-1)
     long long sol_idx;
-    // last step info
     long long info_t;
     int info_best_unsat;
     int pad1;
@@ -90,32 +101,45 @@ struct StepArgs {
     float *theta, *m, *v;
     uint32_t *A0, *A1;
     int *hist, *unsat;
-    double *gtab, *S;
+    float* gtab;                     // [KB][N] fp32 derivative table (R26)
+    double* S;
     long long* rowQ;
     double *rowD, *rowRho;
     unsigned char *rowGuard, *sol;
+    int* hubD;                       // [n_hubs][KB-1][N] int32 signed bin counts
     DevScalars* ds;
     const uint32_t *cptr, *clit, *occ_ptr, *occ_rec, *occ_cnt;
+    const int2* occ_pn;
+    const int* hub_of;
+    const int4* hub_sc;
+    int n_hubs, n_hub_sc;
     int V, N;
     long long C;
     int KB;
+    int uniform_len;                 // every clause has exactly K literals
+    int num_sms;
+    int upd_mode;                    // 0 = fused persistent (v2), 1 = CTA-per-row fallback (v1)
+    int upd_GT, upd_NG, upd_grid;    // v2 launch geometry
+    size_t upd_smem;
     MethodConsts mc;
 };
 
-// Workspace layout (byte offsets), see capi.cu: layout().
+// Workspace layout (byte offsets), see capi.cu: make_layout().
 struct Layout {
-    size_t theta, m, v, A0, A1, hist, gtab, S, unsat, rowQ, rowD, rowRho, rowGuard, scal, steptab, sol, total;
+    size_t theta, m, v, A0, A1, hist, gtab, S, unsat, rowQ, rowD, rowRho, rowGuard, scal, steptab, sol, hubD, total;
 };
 
-// ---------------------------------------------------------------- launchers (kernels.cu)
+// ---------------------------------------------------------------- launchers
 cudaError_t launch_init(float* theta, float* m, float* v, int V, int N, long long n0, unsigned long long seed,
                         cudaStream_t st);
 cudaError_t launch_rowstats(const float* theta, int V, int N, const MethodConsts& mc, long long* rowQ, double* rowD,
                             double* rowRho, unsigned char* rowGuard, uint32_t* A, unsigned int* thmax_bits,
                             cudaStream_t st);
-// which: 0 clause, 1 gtable, 2 update, 3 step_end
+// Step kernels, in order: 0 clause, 1 gtable, 2 hub, 3 update, 4 step_end.
+constexpr int kKernelsPerStep = 5;
 cudaError_t launch_step_kernel(int which, const StepArgs& a, const StepScalars* sc_dev, long long t, cudaStream_t st);
-cudaError_t configure_kernels(int N);
+// Choose the k_update geometry for (N, KB) and set kernel attributes.
+cudaError_t configure_kernels(StepArgs* a);
 cudaError_t launch_export(const StepArgs& a, long long t_eval, const int* cols_dev, int M, int k, double* absG,
                           unsigned long long* keys, int n64, int* out_v, double* out_g, cudaStream_t st, int phase);
 

@@ -60,9 +60,9 @@ def compare_step(s, o, cnf, what=""):
     np.testing.assert_array_equal(unsat, ref.unsat, err_msg=f"unsat {what} t={ref.t}")
     words = s.debug(3, np.uint32, (cnf.V, N // 32))
     np.testing.assert_array_equal(words, pack_bits(ref.bits), err_msg=f"bits {what} t={ref.t}")
-    g = s.debug(1, np.float64, (N, KB))
-    np.testing.assert_array_equal(g[:, :K + 1], ref.g, err_msg=f"g {what} t={ref.t}")
-    assert not g[:, K + 1:].any()
+    g = s.debug(1, np.float32, (KB, N))
+    np.testing.assert_array_equal(g[:K + 1].T, ref.g32, err_msg=f"g {what} t={ref.t}")
+    assert not g[K + 1:].any()
     S = s.debug(2, np.float64, (N,))
     np.testing.assert_array_equal(S, ref.S, err_msg=f"S {what} t={ref.t}")
     assert (info.best_unsat, info.best_idx) == (ref.best_unsat, ref.best_idx)
