@@ -216,7 +216,7 @@ class StepOut:
     g: np.ndarray             # Nl x (K+1) fp64 (Eq. 4 derivative)
     g32: np.ndarray           # Nl x (K+1) fp32 table used by the backward (R26)
     loss: float               # -sum_n S_n over ALL candidates
-    G: np.ndarray             # V x Nl (pre-Jacobian variable gradient)
+    G: np.ndarray             # V x Nl pre-Jacobian variable gradient, fp32 values (R27) held in fp64
     grad: np.ndarray          # V x Nl fp32 (post-Jacobian)
     J: np.ndarray
     d: np.ndarray
@@ -305,7 +305,8 @@ class Oracle:
         gmax = self.comm.max(L.or_gmax(Nl, K, _p(g32), _p(rmin)))
         thmax = self.comm.max(L.or_abs_max(self.theta.size, _p(self.theta)))
         # STE backward and Eq. 5 Jacobian
-        G = backward(cnf, R, g32)
+        G64 = backward(cnf, R, g32)
+        G = G64.astype(np.float32).astype(np.float64)    # R27: G rounded once to fp32
         I = np.empty(V, np.int64); s = np.empty(V, np.int32); valid = np.empty(V, np.uint8)
         L.or_jacobian_partial(V, Nl, _p(G), _p(self.theta), _p(self.occ), self.N, gmax, thmax, _p(I), _p(s), _p(valid))
         I = self.comm.sum_i64(I)

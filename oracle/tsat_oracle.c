@@ -281,7 +281,8 @@ static int ceil_log2(double x)
  * bound on |sum p|); I_v = sum llrint(ldexp(p, s_v)).  This function returns
  * the partial integer sums I_v over the local candidates and s_v (R13).
  * occ_v = number of literal occurrences of v; gmax = max |g_n[r]| over all
- * candidates and r in [rmin_n, K]; thmax = max |theta| over the batch. */
+ * candidates and r in [rmin_n, K]; thmax = max |theta| over the batch.
+ * G holds the fp32-rounded variable gradient (R27), so p = G theta is exact. */
 void or_jacobian_partial(int V, int Nl, const double* G, const float* theta,
                          const int32_t* occ, int64_t N, double gmax, float thmax,
                          int64_t* I, int32_t* s_out, uint8_t* valid)

@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(256) k_grad_cols(int V, int N, const uint32_t*
 #pragma unroll
     for (int r = 0; r < KB; ++r)
         if (r <= K) G = G + (double)cnt[r] * (double)gtab[(size_t)r * N + n];
-    out[(size_t)mi * V + v] = fabs(G);
+    out[(size_t)mi * V + v] = fabs((double)(float)G);          // R27: G rounded to fp32
 }
 
 // Single-CTA bitonic sort of n64 (power of two) u64 keys in global memory.

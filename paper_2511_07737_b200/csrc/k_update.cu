@@ -66,6 +66,42 @@ __device__ __forceinline__ double fold_G(const int (&d)[KB], const float* gs, in
     return G;
 }
 
+// Bulk prefetch of [p, p + bytes) into L2 (TMA engine; bytes % 16 == 0).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// x * 2^s, exact (== scalbn) when 2^s is a normal double.
+__device__ __forceinline__ double times_pow2(double x, int s) {
+    if (s >= -1000 && s <= 1000) return x * __longlong_as_double((long long)(1023 + s) << 52);
+    return scalbn(x, s);
+}
+
+// Gather one occurrence record (own literal + others) into NP count planes.
+template <int NP>
+__device__ __forceinline__ void gather_rec(uint32_t (&sp)[NP], const uint32_t* rec, uint32_t hdr, uint32_t own,
+                                           const uint32_t* __restrict__ Acur, int NW, int w) {
+    const uint32_t len = hdr >> 1;
+    sp[0] = own ^ (0u - (hdr & 1u));
+#pragma unroll
+    for (int q = 1; q < NP; ++q) sp[q] = 0u;
+    for (uint32_t i = 1; i < len; ++i) {
+        const uint32_t code = rec[i];
+        bs_add<NP>(sp, __ldg(Acur + (size_t)(code >> 1) * NW + w) ^ (0u - (code & 1u)));
+    }
+}
+
+template <int NCTR, int NP>
+__device__ __forceinline__ void count_rec(uint32_t (&cnt)[NCTR][8], const uint32_t (&sp)[NP], bool neg) {
+    if (neg) {
+#pragma unroll
+        for (int r = 0; r < NCTR; ++r) vc_inc<8>(cnt[r], bs_eq<NP>(sp, r));
+    } else {
+#pragma unroll
+        for (int r = 0; r < NCTR; ++r) vc_dec<8>(cnt[r], bs_eq<NP>(sp, r));
+    }
+}
+
 template <int KB>
 __global__ void __launch_bounds__(512, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
                                                     uint32_t* __restrict__ Anext, const StepScalars* __restrict__ sc) {
@@ -84,13 +120,18 @@ __global__ void __launch_bounds__(512, 1) k_update(StepArgs a, const uint32_t* _
     long long* red = reinterpret_cast<long long*>(gb + upd_group_bytes(KB, N) - 128);   // 4 + 4 slots
     float* redf = reinterpret_cast<float*>(red + 8);                                    // 4 slots
     double* bcast = reinterpret_cast<double*>(redf + 4);                                // 2 slots
-    int* rowslot = reinterpret_cast<int*>(bcast + 2);
+    int* rowslot = reinterpret_cast<int*>(bcast + 2);                                   // 2 slots
     const int bar = 1 + grp;
     const int lane = threadIdx.x & 31, gw = tg >> 5, ngw = GT >> 5;
+    const bool uni3 = a.uniform_len && a.mc.K == 3 && KB == 4;
 
     // fp32 derivative table of the whole batch -> shared memory
     for (int i = threadIdx.x * 4; i < KB * N; i += blockDim.x * 4)
         *reinterpret_cast<float4*>(gs + i) = *reinterpret_cast<const float4*>(a.gtab + i);
+    if (tg == 0) {
+        rowslot[0] = atomicAdd(&a.ds->row_counter, 1);
+        rowslot[1] = atomicAdd(&a.ds->row_counter, 1);
+    }
     __syncthreads();
 
     const long long t = sc->t;
@@ -99,12 +140,16 @@ __global__ void __launch_bounds__(512, 1) k_update(StepArgs a, const uint32_t* _
     const float wdf = sc->wdf, a1 = sc->a1, b2f = sc->b2f, a2 = sc->a2, nss = sc->nss, bc2s = sc->bc2s,
                 epsf = sc->epsf, nz = sc->nz;
     const MethodConsts& mc = a.mc;
+    int v = rowslot[0], vnext = rowslot[1];
 
-    while (true) {
-        if (tg == 0) *rowslot = atomicAdd(&a.ds->row_counter, 1);
-        group_bar(bar, GT);
-        const int v = *rowslot;
-        if (v >= a.V) break;
+    while (v < a.V) {
+        // ---- prefetch the next row's streams into L2 while this row gathers
+        if (tg == 0 && vnext < a.V) {
+            const uint32_t rowbytes = (uint32_t)N * 4u;
+            prefetch_l2(a.theta + (size_t)vnext * N, rowbytes);
+            prefetch_l2(a.m + (size_t)vnext * N, rowbytes);
+            prefetch_l2(a.v + (size_t)vnext * N, rowbytes);
+        }
         const int hub = a.hub_of[v];
         const int2 pn = a.occ_pn[v];
         const int dsum = pn.y - pn.x;                       // sum_r (cneg - cpos)[r]
@@ -120,7 +165,7 @@ __global__ void __launch_bounds__(512, 1) k_update(StepArgs a, const uint32_t* _
             x = x * (double)thmax;
             if (occ > 0 && x > 0.0) { jvalid = true; s = 61 - ceil_log2(x); }
         }
-        const int* hubrow = hub >= 0 ? a.hubD + (size_t)hub * NCTR * N : nullptr;
+        int* hubrow = hub >= 0 ? a.hubD + (size_t)hub * NCTR * N : nullptr;
         float* trow = a.theta + (size_t)v * N;
         float* mrow = a.m + (size_t)v * N;
         float* vrow = a.v + (size_t)v * N;
@@ -137,25 +182,31 @@ __global__ void __launch_bounds__(512, 1) k_update(StepArgs a, const uint32_t* _
                 for (int r = 0; r < NCTR; ++r)
 #pragma unroll
                     for (int b = 0; b < kCtr; ++b) cnt[r][b] = 0u;
-                for (unsigned p = 0; p < nrec;) {
+                unsigned p = 0;
+                if (uni3) {
+                    // uniform 3-SAT: two records (4 independent gathers) per iteration
+                    for (; p + 6 <= nrec; p += 6) {
+                        const uint32_t h0 = rec[p], c01 = rec[p + 1], c02 = rec[p + 2];
+                        const uint32_t h1 = rec[p + 3], c11 = rec[p + 4], c12 = rec[p + 5];
+                        const uint32_t x01 = __ldg(Acur + (size_t)(c01 >> 1) * NW + w) ^ (0u - (c01 & 1u));
+                        const uint32_t x02 = __ldg(Acur + (size_t)(c02 >> 1) * NW + w) ^ (0u - (c02 & 1u));
+                        const uint32_t x11 = __ldg(Acur + (size_t)(c11 >> 1) * NW + w) ^ (0u - (c11 & 1u));
+                        const uint32_t x12 = __ldg(Acur + (size_t)(c12 >> 1) * NW + w) ^ (0u - (c12 & 1u));
+                        uint32_t s0[NP], s1[NP];
+                        s0[0] = own ^ (0u - (h0 & 1u)); s0[1] = 0u;
+                        s1[0] = own ^ (0u - (h1 & 1u)); s1[1] = 0u;
+                        bs_add<NP>(s0, x01); bs_add<NP>(s0, x02);
+                        bs_add<NP>(s1, x11); bs_add<NP>(s1, x12);
+                        count_rec<NCTR, NP>(cnt, s0, h0 & 1u);
+                        count_rec<NCTR, NP>(cnt, s1, h1 & 1u);
+                    }
+                }
+                while (p < nrec) {
                     const uint32_t hdr = rec[p];
-                    const uint32_t len = hdr >> 1;
                     uint32_t sp[NP];
-                    sp[0] = own ^ (0u - (hdr & 1u));
-#pragma unroll
-                    for (int q = 1; q < NP; ++q) sp[q] = 0u;
-                    for (uint32_t i = 1; i < len; ++i) {
-                        const uint32_t code = rec[p + i];
-                        bs_add<NP>(sp, __ldg(Acur + (size_t)(code >> 1) * NW + w) ^ (0u - (code & 1u)));
-                    }
-                    if (hdr & 1u) {
-#pragma unroll
-                        for (int r = 0; r < NCTR; ++r) vc_inc<kCtr>(cnt[r], bs_eq<NP>(sp, r));
-                    } else {
-#pragma unroll
-                        for (int r = 0; r < NCTR; ++r) vc_dec<kCtr>(cnt[r], bs_eq<NP>(sp, r));
-                    }
-                    p += len;
+                    gather_rec<NP>(sp, rec + p, hdr, own, Acur, NW, w);
+                    count_rec<NCTR, NP>(cnt, sp, hdr & 1u);
+                    p += hdr >> 1;
                 }
                 uint32_t T[32];
 #pragma unroll
@@ -174,7 +225,7 @@ __global__ void __launch_bounds__(512, 1) k_update(StepArgs a, const uint32_t* _
         }
         group_bar(bar, GT);
 
-        // ---- 3a: J_v = sum_n G theta (int64 fixed point)
+        // ---- 3a: G (fp64 fold, rounded to fp32, R27) -> smem; J_v = sum G theta (int64 fixed point)
         long long I = 0;
         for (int base = 0; base < N; base += 4 * GT) {
             const int n = base + 4 * tg;
@@ -185,8 +236,13 @@ __global__ void __launch_bounds__(512, 1) k_update(StepArgs a, const uint32_t* _
                 for (int q = 0; q < 4; ++q) {
                     int d[KB];
                     load_counts<KB>(d, dpk, dpkw, hubrow, N, n + q, dsum, hub >= 0);
-                    const double G = fold_G<KB>(d, gs, N, n + q);
-                    if (jvalid) I += __double2ll_rn(scalbn(G * (double)th[q], s));
+                    const float G32 = (float)fold_G<KB>(d, gs, N, n + q);
+                    dpk[n + q + ((n + q) >> 5)] = __float_as_uint(G32);
+                    if (jvalid) I += __double2ll_rn(times_pow2((double)G32 * (double)th[q], s));
+                }
+                if (hub >= 0) {
+#pragma unroll
+                    for (int r = 0; r < NCTR; ++r) *reinterpret_cast<int4*>(hubrow + (size_t)r * N + n) = make_int4(0, 0, 0, 0);
                 }
             }
         }
@@ -196,7 +252,7 @@ __global__ void __launch_bounds__(512, 1) k_update(StepArgs a, const uint32_t* _
         if (tg == 0) {
             long long tot = 0;
             for (int i = 0; i < ngw; ++i) tot += red[i];
-            double J = jvalid ? scalbn((double)tot, -s) : 0.0;
+            double J = jvalid ? times_pow2((double)tot, -s) : 0.0;
             double c = 0.0;
             if (mc.normalize && !guard) {
                 c = J / (double)mc.Nglobal;
@@ -223,10 +279,8 @@ __global__ void __launch_bounds__(512, 1) k_update(StepArgs a, const uint32_t* _
                 float vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    int d[KB];
-                    load_counts<KB>(d, dpk, dpkw, hubrow, N, n + q, dsum, hub >= 0);
-                    const double G = fold_G<KB>(d, gs, N, n + q);
-                    const float g = (float)(G * rho - c);
+                    const float G32 = __uint_as_float(dpk[n + q + ((n + q) >> 5)]);
+                    const float g = (float)((double)G32 * rho - c);
                     float x = th[q] * wdf;
                     const float mn = __fmaf_rn(a1, g - mm[q], mm[q]);
                     const float vb = vv[q] * b2f;
@@ -249,11 +303,6 @@ __global__ void __launch_bounds__(512, 1) k_update(StepArgs a, const uint32_t* _
                 *reinterpret_cast<float4*>(trow + n) = make_float4(th[0], th[1], th[2], th[3]);
                 *reinterpret_cast<float4*>(mrow + n) = make_float4(mm[0], mm[1], mm[2], mm[3]);
                 *reinterpret_cast<float4*>(vrow + n) = make_float4(vv[0], vv[1], vv[2], vv[3]);
-                if (hub >= 0) {
-                    int* hr = a.hubD + (size_t)hub * NCTR * N;
-#pragma unroll
-                    for (int r = 0; r < NCTR; ++r) *reinterpret_cast<int4*>(hr + (size_t)r * N + n) = make_int4(0, 0, 0, 0);
-                }
             }
             // 8 lanes x 4 candidates = one 32-candidate word
             unsigned pw = pnib << (4 * (lane & 7)), nw = nnib << (4 * (lane & 7));
@@ -284,10 +333,13 @@ __global__ void __launch_bounds__(512, 1) k_update(StepArgs a, const uint32_t* _
                 if (idx >= 0 && idx < N)
                     a.sol[v] = (unsigned char)((Acur[(size_t)v * NW + (idx >> 5)] >> (idx & 31)) & 1u);
             }
+            rowslot[0] = vnext < a.V ? atomicAdd(&a.ds->row_counter, 1) : a.V;
         }
         group_bar(bar, GT);
         const bool dpos = bcast[1] > 0.0;
         for (int w = tg; w < NW; w += GT) Anext[(size_t)v * NW + w] = dpos ? posw[w] : negw[w];
+        v = vnext;
+        vnext = rowslot[0];
         // (the next row's first group_bar orders these smem reads before reuse)
     }
 }
@@ -420,8 +472,8 @@ __global__ void __launch_bounds__(256) k_update_rowcta(StepArgs a, const uint32_
         double G = 0.0;
 #pragma unroll
         for (int r = 0; r < KB; ++r) G = G + (double)cnt[r] * (double)a.gtab[(size_t)r * N + n];
-        Gs[n] = G;
-        if (jvalid) I += __double2ll_rn(scalbn(G * (double)trow[n], s));
+        Gs[n] = (double)(float)G;                                  // R27
+        if (jvalid) I += __double2ll_rn(scalbn(Gs[n] * (double)trow[n], s));
     }
     float dummy = 0.0f;
     block_sum_max(I, dummy, sh_s, sh_m);

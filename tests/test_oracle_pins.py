@@ -292,13 +292,13 @@ def test_gradient_matches_torch_autograd(seed, tau, normalize):
     ref, Lref = _torch_dense_grad(cnf, theta, tau, bool(normalize))
     ours = s.G * s.extra["rho"][:, None] - s.extra["cv"][:, None]
     scale = np.abs(ref).max()
-    # the backward uses the fp32 g table (R26): agreement to fp32 rounding
-    assert np.abs(ours - ref).max() <= 2e-7 * scale
+    # the backward uses the fp32 g table (R26) and fp32 G (R27): fp32 rounding
+    assert np.abs(ours - ref).max() <= 4e-7 * scale
     # G itself is the P^T fold (numpy, fp64 table) up to the fp32 rounding of g
     G64 = _G_from_g64(o.cnf, s.R, s.g)
-    assert np.abs(s.G - G64).max() <= 1.2e-7 * np.abs(G64).max()
+    assert np.abs(s.G - G64).max() <= 2.4e-7 * np.abs(G64).max()
     G32 = _G_from_g64(o.cnf, s.R, s.g32.astype(np.float64))
-    assert np.abs(s.G - G32).max() <= 1e-13 * np.abs(G64).max()
+    np.testing.assert_array_equal(s.G, G32.astype(np.float32).astype(np.float64))
     assert abs(s.loss - Lref) <= 1e-12 * abs(Lref)
     np.testing.assert_array_equal(s.grad, ours.astype(np.float32))
 
