@@ -160,6 +160,7 @@ StepArgs step_args(tsat_ctx ctx) {
     a.upd_NG = ctx->upd_NG;
     a.upd_grid = ctx->upd_grid;
     a.upd_smem = ctx->upd_smem;
+    a.upd_rec_cap = std::max(64, (ctx->cnf.max_rec_words + 63) / 64 * 64);
     a.V = ctx->cnf.V;
     a.N = ctx->N;
     a.C = ctx->cnf.C;

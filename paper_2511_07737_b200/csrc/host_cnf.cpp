@@ -220,7 +220,10 @@ int build_cnf(int32_t V, int64_t C, const int64_t* ptr, const int32_t* lits, Hos
     h.hub_of.assign((size_t)V, -1);
     for (int32_t v = 0; v < V; ++v) {
         bool hub = h.occ_pn[2 * v] > 127 || h.occ_pn[2 * v + 1] > 127 || (h.occ_ptr[v + 1] - h.occ_ptr[v]) > (uint32_t)kRecCap;
-        if (!hub) continue;
+        if (!hub) {
+            h.max_rec_words = std::max<int32_t>(h.max_rec_words, (int32_t)(h.occ_ptr[v + 1] - h.occ_ptr[v]));
+            continue;
+        }
         int32_t hid = h.n_hubs++;
         h.hub_of[v] = hid;
         uint32_t p = h.occ_ptr[v], e = h.occ_ptr[v + 1], b = p;

@@ -32,9 +32,9 @@ __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) / 16 * 
 // Shared-memory geometry of k_update (host and device agree through this).
 __host__ __device__ inline size_t upd_gs_bytes(int KB, int N) { return align16((size_t)KB * N * 4); }
 __host__ __device__ inline size_t upd_dpk_words(int N) { return (size_t)N + (N >> 5); }
-__host__ __device__ inline size_t upd_group_bytes(int KB, int N) {
+__host__ __device__ inline size_t upd_group_bytes(int KB, int N, int rec_cap) {
     const int NDW = KB == 4 ? 1 : 2;
-    return align16((size_t)NDW * upd_dpk_words(N) * 4) + (size_t)kRecCap * 4 + align16((size_t)2 * (N >> 5) * 4) + 128;
+    return align16((size_t)NDW * upd_dpk_words(N) * 4) + align16((size_t)rec_cap * 4) + align16((size_t)2 * (N >> 5) * 4) + 128;
 }
 
 // Signed per-bin counts of candidate n of the current row.
@@ -103,7 +103,7 @@ __device__ __forceinline__ void count_rec(uint32_t (&cnt)[NCTR][8], const uint32
 }
 
 template <int KB>
-__global__ void __launch_bounds__(512, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
+__global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
                                                     uint32_t* __restrict__ Anext, const StepScalars* __restrict__ sc) {
     constexpr int NP = (KB == 4) ? 2 : 3;
     constexpr int NCTR = KB - 1;
@@ -112,12 +112,14 @@ __global__ void __launch_bounds__(512, 1) k_update(StepArgs a, const uint32_t* _
     const size_t dpkw = upd_dpk_words(N);
     float* gs = reinterpret_cast<float*>(smem);
     const int grp = threadIdx.x / GT, tg = threadIdx.x - grp * GT;
-    unsigned char* gb = smem + upd_gs_bytes(KB, N) + (size_t)grp * upd_group_bytes(KB, N);
+    const int rec_cap = a.upd_rec_cap;
+    const size_t grb = upd_group_bytes(KB, N, rec_cap);
+    unsigned char* gb = smem + upd_gs_bytes(KB, N) + (size_t)grp * grb;
     uint32_t* dpk = reinterpret_cast<uint32_t*>(gb);
     uint32_t* rec = reinterpret_cast<uint32_t*>(gb + align16((size_t)(KB == 4 ? 1 : 2) * dpkw * 4));
-    uint32_t* posw = rec + kRecCap;
+    uint32_t* posw = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(rec) + align16((size_t)rec_cap * 4));
     uint32_t* negw = posw + NW;
-    long long* red = reinterpret_cast<long long*>(gb + upd_group_bytes(KB, N) - 128);   // 4 + 4 slots
+    long long* red = reinterpret_cast<long long*>(gb + grb - 128);                      // 4 + 4 slots
     float* redf = reinterpret_cast<float*>(red + 8);                                    // 4 slots
     double* bcast = reinterpret_cast<double*>(redf + 4);                                // 2 slots
     int* rowslot = reinterpret_cast<int*>(bcast + 2);                                   // 2 slots
@@ -143,12 +145,14 @@ __global__ void __launch_bounds__(512, 1) k_update(StepArgs a, const uint32_t* _
     int v = rowslot[0], vnext = rowslot[1];
 
     while (v < a.V) {
-        // ---- prefetch the next row's streams into L2 while this row gathers
-        if (tg == 0 && vnext < a.V) {
+        // ---- prefetch this row's streams into L2 while it gathers (a short
+        // reuse distance: the streaming writes of other rows would evict a
+        // longer-range prefetch)
+        if (tg == 0) {
             const uint32_t rowbytes = (uint32_t)N * 4u;
-            prefetch_l2(a.theta + (size_t)vnext * N, rowbytes);
-            prefetch_l2(a.m + (size_t)vnext * N, rowbytes);
-            prefetch_l2(a.v + (size_t)vnext * N, rowbytes);
+            prefetch_l2(a.theta + (size_t)v * N, rowbytes);
+            prefetch_l2(a.m + (size_t)v * N, rowbytes);
+            prefetch_l2(a.v + (size_t)v * N, rowbytes);
         }
         const int hub = a.hub_of[v];
         const int2 pn = a.occ_pn[v];
@@ -548,9 +552,10 @@ cudaError_t configure_update(StepArgs* a) {
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
     a->num_sms = sms;
     const int GT = NW >= 128 ? 128 : (NW > 32 ? 64 : 32);
-    const size_t gsb = upd_gs_bytes(KB, N), grb = upd_group_bytes(KB, N);
+    const size_t gsb = upd_gs_bytes(KB, N), grb = upd_group_bytes(KB, N, a->upd_rec_cap);
     long long ng = optin > (long long)gsb ? ((long long)optin - (long long)gsb) / (long long)grb : 0;
-    ng = ng < 512 / GT ? ng : 512 / GT;
+    const int max_threads = KB == 4 ? 768 : 512;   // register budget (launch bounds)
+    ng = ng < max_threads / GT ? ng : max_threads / GT;
     ng = ng < 15 ? ng : 15;                       // named barriers 1..15
     if (ng < 2 && !(ng == 1 && GT == 128)) {
         a->upd_mode = 1;                          // too large for the fused kernel

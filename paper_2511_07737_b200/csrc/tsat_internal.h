@@ -42,6 +42,7 @@ struct HostCnf {
     int64_t n_warnings = 0, n_tautologies = 0, n_duplicates = 0;
     int32_t has_empty = 0;
     int32_t uniform_len = 0;            // every clause has exactly K literals
+    int32_t max_rec_words = 0;          // max occurrence-record words over non-hub rows
 };
 
 // Parse DIMACS.  Returns 0 on success, 2 (TSAT_E_PARSE) with msg.
@@ -120,6 +121,7 @@ struct StepArgs {
     int num_sms;
     int upd_mode;                    // 0 = fused persistent (v2), 1 = CTA-per-row fallback (v1)
     int upd_GT, upd_NG, upd_grid;    // v2 launch geometry
+    int upd_rec_cap;                 // record words a group stages per row (max over non-hub rows)
     size_t upd_smem;
     MethodConsts mc;
 };
