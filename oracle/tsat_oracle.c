@@ -344,11 +344,13 @@ double or_lr_at(int64_t t, double lr0, double factor, int decay_every, int resta
 /* AdamW (§4.1 l.255, "AdamW"; hyper-parameters = PyTorch defaults,
  * R6), in PyTorch's single-tensor order (torch/optim/adam.py:419,457,476,
  * 531-547) with its CPU kernels' rounding (lerp and addcmul use one fused
- * multiply-add; R6b).  s = t + 1 is the bias-correction step.
+ * multiply-add; R6b), except that v's bias correction multiplies by
+ * the host-rounded 1/sqrt(1 - beta2^s) (R6c: the same AdamW, one division
+ * fewer).  s = t + 1 is the bias-correction step.
  *   theta *= (float)(1 - lr wd)
  *   m      = fmaf(a1, g - m, m),           a1 = (float)(1 - beta1)
  *   v      = fmaf(a2 g, g, v beta2),       a2 = (float)(1 - beta2)
- *   den    = sqrtf(v)/(float)sqrt(1 - beta2^s) + eps
+ *   den    = sqrtf(v) (float)(1/sqrt(1 - beta2^s)) + eps
  *   theta  = theta + ((float)(-lr/(1 - beta1^s)) m)/den
  * Optional noise (R17, default sigma = 0): theta += (float)(lr sigma) xi,
  * xi = (x>>8) 2^-24 - 1/2, x = Philox(key=seed, ctr=(n>>2, v, 1+t, 0))[n&3]. */
@@ -364,7 +366,7 @@ void or_adamw(int V, int64_t n0, int Nl, float* theta, float* m, float* vv, cons
     double bc1 = 1.0 - pow(beta1, s);
     double bc2 = 1.0 - pow(beta2, s);
     float nss = (float)(-(lr / bc1));
-    float bc2s = (float)sqrt(bc2);
+    float rbc2 = (float)(1.0 / sqrt(bc2));
     float epsf = (float)eps;
     float nz = (float)(lr * noise_sigma);
     uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
@@ -376,7 +378,7 @@ void or_adamw(int V, int64_t n0, int Nl, float* theta, float* m, float* vv, cons
             float mm = fmaf(a1, g - m[i], m[i]);
             float vb = vv[i] * b2f;
             float vn = fmaf(a2 * g, g, vb);
-            float den = sqrtf(vn) / bc2s + epsf;
+            float den = sqrtf(vn) * rbc2 + epsf;
             th = th + (nss * mm) / den;
             if (noise_sigma != 0.0) {
                 int64_t n = n0 + j;

@@ -191,7 +191,7 @@ StepScalars step_scalars(const tsat_config& c, int64_t t) {
     double bc1 = 1.0 - std::pow(c.beta1, st);
     double bc2 = 1.0 - std::pow(c.beta2, st);
     s.nss = (float)(-(lr / bc1));
-    s.bc2s = (float)std::sqrt(bc2);
+    s.rbc2 = (float)(1.0 / std::sqrt(bc2));
     s.epsf = (float)c.eps;
     s.nz = (float)(lr * c.noise_sigma);
     return s;

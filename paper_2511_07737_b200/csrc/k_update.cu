@@ -60,9 +60,11 @@ __device__ __forceinline__ void load_counts(int (&d)[KB], const uint32_t* dpk, s
 
 template <int KB>
 __device__ __forceinline__ double fold_G(const int (&d)[KB], const float* gs, int N, int n) {
+    // each product d * g32 is exact in fp64 (|d| < 2^24, 24-bit g), so the
+    // fused multiply-add rounds exactly like the oracle's mul-then-add
     double G = 0.0;
 #pragma unroll
-    for (int r = 0; r < KB; ++r) G = G + (double)d[r] * (double)gs[(size_t)r * N + n];
+    for (int r = 0; r < KB; ++r) G = __fma_rn((double)d[r], (double)gs[(size_t)r * N + n], G);
     return G;
 }
 
@@ -87,7 +89,7 @@ __device__ __forceinline__ void gather_rec(uint32_t (&sp)[NP], const uint32_t* r
     for (int q = 1; q < NP; ++q) sp[q] = 0u;
     for (uint32_t i = 1; i < len; ++i) {
         const uint32_t code = rec[i];
-        bs_add<NP>(sp, __ldg(Acur + (size_t)(code >> 1) * NW + w) ^ (0u - (code & 1u)));
+        bs_add<NP>(sp, __ldg(Acur + ((code >> 1) * (unsigned)NW + (unsigned)w)) ^ (0u - (code & 1u)));
     }
 }
 
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
     const long long t = sc->t;
     const double gmax = __longlong_as_double((long long)a.ds->gmax_bits);
     const float thmax = __uint_as_float(a.ds->thmax_bits[t & 1]);
-    const float wdf = sc->wdf, a1 = sc->a1, b2f = sc->b2f, a2 = sc->a2, nss = sc->nss, bc2s = sc->bc2s,
+    const float wdf = sc->wdf, a1 = sc->a1, b2f = sc->b2f, a2 = sc->a2, nss = sc->nss, rbc2 = sc->rbc2,
                 epsf = sc->epsf, nz = sc->nz;
     const MethodConsts& mc = a.mc;
     int v = rowslot[0], vnext = rowslot[1];
@@ -192,10 +194,10 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
                     for (; p + 6 <= nrec; p += 6) {
                         const uint32_t h0 = rec[p], c01 = rec[p + 1], c02 = rec[p + 2];
                         const uint32_t h1 = rec[p + 3], c11 = rec[p + 4], c12 = rec[p + 5];
-                        const uint32_t x01 = __ldg(Acur + (size_t)(c01 >> 1) * NW + w) ^ (0u - (c01 & 1u));
-                        const uint32_t x02 = __ldg(Acur + (size_t)(c02 >> 1) * NW + w) ^ (0u - (c02 & 1u));
-                        const uint32_t x11 = __ldg(Acur + (size_t)(c11 >> 1) * NW + w) ^ (0u - (c11 & 1u));
-                        const uint32_t x12 = __ldg(Acur + (size_t)(c12 >> 1) * NW + w) ^ (0u - (c12 & 1u));
+                        const uint32_t x01 = __ldg(Acur + ((c01 >> 1) * (unsigned)NW + (unsigned)w)) ^ (0u - (c01 & 1u));
+                        const uint32_t x02 = __ldg(Acur + ((c02 >> 1) * (unsigned)NW + (unsigned)w)) ^ (0u - (c02 & 1u));
+                        const uint32_t x11 = __ldg(Acur + ((c11 >> 1) * (unsigned)NW + (unsigned)w)) ^ (0u - (c11 & 1u));
+                        const uint32_t x12 = __ldg(Acur + ((c12 >> 1) * (unsigned)NW + (unsigned)w)) ^ (0u - (c12 & 1u));
                         uint32_t s0[NP], s1[NP];
                         s0[0] = own ^ (0u - (h0 & 1u)); s0[1] = 0u;
                         s1[0] = own ^ (0u - (h1 & 1u)); s1[1] = 0u;
@@ -289,7 +291,7 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
                     const float mn = __fmaf_rn(a1, g - mm[q], mm[q]);
                     const float vb = vv[q] * b2f;
                     const float vn = __fmaf_rn(a2 * g, g, vb);
-                    const float den = __fsqrt_rn(vn) / bc2s + epsf;
+                    const float den = __fmul_rn(__fsqrt_rn(vn), rbc2) + epsf;
                     x = x + (nss * mn) / den;
                     if (mc.noise) {
                         const long long ng = mc.n0 + n + q;
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
                         x = x + nz * xi;
                     }
                     th[q] = x; mm[q] = mn; vv[q] = vn;
-                    Qn += __double2ll_rn((double)x * 4294967296.0);
+                    Qn += __float2ll_rn(x * 4294967296.0f);          // x 2^32 is exact in fp32
                     mx = fmaxf(mx, fabsf(x));
                     pnib |= (x > 0.0f ? 1u : 0u) << q;
                     nnib |= (x < 0.0f ? 1u : 0u) << q;
@@ -502,7 +504,7 @@ __global__ void __launch_bounds__(256) k_update_rowcta(StepArgs a, const uint32_
         const float mm = __fmaf_rn(sc->a1, g - m0, m0);
         const float vb = vrow[n] * sc->b2f;
         const float vn = __fmaf_rn(sc->a2 * g, g, vb);
-        const float den = __fsqrt_rn(vn) / sc->bc2s + sc->epsf;
+        const float den = __fmul_rn(__fsqrt_rn(vn), sc->rbc2) + sc->epsf;
         th = th + (sc->nss * mm) / den;
         if (mc.noise) {
             const long long ng = mc.n0 + n;

@@ -62,7 +62,7 @@ struct StepScalars {
     float b2f;        // (float)beta2
     float a2;         // (float)(1 - beta2)
     float nss;        // (float)(-(lr / (1 - beta1^(t+1))))
-    float bc2s;       // (float)sqrt(1 - beta2^(t+1))
+    float rbc2;       // (float)(1 / sqrt(1 - beta2^(t+1)))  (R6c)
     float epsf;       // (float)eps
     float nz;         // (float)(lr * noise_sigma)
 };

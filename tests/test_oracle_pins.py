@@ -406,7 +406,10 @@ def test_adamw_matches_torch():
         st = opt.state[p]
         np.testing.assert_allclose(st["exp_avg"].numpy(), m, rtol=0, atol=0)
         np.testing.assert_allclose(st["exp_avg_sq"].numpy(), v, rtol=0, atol=0)
-        np.testing.assert_allclose(p.detach().numpy(), th, rtol=2e-6, atol=1e-7)
+        # theta: torch's CPU sqrt is not correctly rounded and R6c multiplies by
+        # 1/sqrt(bc2) instead of dividing: each step may differ by ~1 ulp of the
+        # update (<= 0.3 here), which weight decay carries forward over 40 steps
+        np.testing.assert_allclose(p.detach().numpy(), th, rtol=2e-6, atol=2e-6)
 
 
 def test_adamw_closed_forms():
