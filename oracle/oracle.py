@@ -305,8 +305,7 @@ class Oracle:
         gmax = self.comm.max(L.or_gmax(Nl, K, _p(g32), _p(rmin)))
         thmax = self.comm.max(L.or_abs_max(self.theta.size, _p(self.theta)))
         # STE backward and Eq. 5 Jacobian
-        G64 = backward(cnf, R, g32)
-        G = G64.astype(np.float32).astype(np.float64)    # R27: G rounded once to fp32
+        G = backward(cnf, R, g32)                     # fp32 values (R27)
         I = np.empty(V, np.int64); s = np.empty(V, np.int32); valid = np.empty(V, np.uint8)
         L.or_jacobian_partial(V, Nl, _p(G), _p(self.theta), _p(self.occ), self.N, gmax, thmax, _p(I), _p(s), _p(valid))
         I = self.comm.sum_i64(I)

@@ -227,7 +227,8 @@ double or_smoothmin_direct(int C, const int32_t* Rcol, double tau)
  * Equal terms are grouped by value (exact integer counts, R12):
  *   G_vn = sum_r (cneg_vn[r] - cpos_vn[r]) g_n[r], ascending r,
  * with g the fp32 table (R26: g rounded once to fp32, the paper's tensor
- * precision; each product count * g is exact in fp64).
+ * precision) accumulated in fp32 by fused multiply-adds, r ascending (R27).
+ * G is returned in a double array (exact fp32 values).
  * occ lists (variable -> (clause, sign)) are built here from the CNF. */
 void or_backward(int V, int C, const int64_t* cptr, const int32_t* lits, int Nl, int K,
                  const uint8_t* R, const float* g, double* G)
@@ -257,10 +258,10 @@ void or_backward(int V, int C, const int64_t* cptr, const int32_t* lits, int Nl,
             for (int j = 0; j < Nl; ++j) cnt[(size_t)j * (K + 1) + Rrow[j]] += delta;
         }
         for (int j = 0; j < Nl; ++j) {
-            double acc = 0.0;
+            float acc = 0.0f;
             for (int r = 0; r <= K; ++r)
-                acc = acc + (double)cnt[(size_t)j * (K + 1) + r] * (double)g[(size_t)j * (K + 1) + r];
-            G[(size_t)v * Nl + j] = acc;
+                acc = fmaf((float)cnt[(size_t)j * (K + 1) + r], g[(size_t)j * (K + 1) + r], acc);
+            G[(size_t)v * Nl + j] = (double)acc;
         }
     }
     free(cnt); free(fill); free(occ_s); free(occ_c); free(vptr);

@@ -213,11 +213,11 @@ __global__ void __launch_bounds__(256) k_grad_cols(int V, int N, const uint32_t*
         for (int r = 0; r < KB; ++r) cnt[r] += (R == (uint32_t)r) ? delta : 0;
         p += len;
     }
-    double G = 0.0;
+    float G = 0.0f;                                               // R27: fp32 FMA chain
 #pragma unroll
     for (int r = 0; r < KB; ++r)
-        if (r <= K) G = G + (double)cnt[r] * (double)gtab[(size_t)r * N + n];
-    out[(size_t)mi * V + v] = fabs((double)(float)G);          // R27: G rounded to fp32
+        if (r <= K) G = __fmaf_rn((float)cnt[r], gtab[(size_t)r * N + n], G);
+    out[(size_t)mi * V + v] = fabs((double)G);
 }
 
 // Single-CTA bitonic sort of n64 (power of two) u64 keys in global memory.

@@ -37,46 +37,92 @@ __host__ __device__ inline size_t upd_group_bytes(int KB, int N, int rec_cap) {
     return align16((size_t)NDW * upd_dpk_words(N) * 4) + align16((size_t)rec_cap * 4) + align16((size_t)2 * (N >> 5) * 4) + 128;
 }
 
-// Signed per-bin counts of candidate n of the current row.
+// x * 2^s, exact (== scalbn) when 2^s is a normal double.
+__device__ __forceinline__ double times_pow2(double x, int s) {
+    if (s >= -1000 && s <= 1000) return x * __longlong_as_double((long long)(1023 + s) << 52);
+    return scalbn(x, s);
+}
+
+// Signed byte r of u (counts stored as int8) -> exact float: the byte, biased
+// by 128, goes into the mantissa of 2^23 (PRMT) and the bias is subtracted.
+__device__ __forceinline__ float sbyte_to_float(uint32_t ub, int r) {
+    return __uint_as_float(__byte_perm(ub, 0x4B000000u, 0x7540u + (unsigned)r)) - 8388736.0f;
+}
+
+// G = sum_r d_r g_r as an fp32 fused multiply-add chain, r ascending (R27).
+// d: the row's signed per-bin counts of one candidate (exact small integers),
+// the last bin derived from dsum = sum_r d_r.  gq[r]: g_r of this candidate.
 template <int KB>
-__device__ __forceinline__ void load_counts(int (&d)[KB], const uint32_t* dpk, size_t dpk_words, const int* hubrow,
-                                            int N, int n, int dsum, bool hub) {
-    int acc = 0;
-    if (hub) {
+__device__ __forceinline__ float fold_bytes(uint32_t p0, uint32_t p1, float dsumf, const float (&gq)[KB]) {
+    const uint32_t u0 = p0 ^ 0x80808080u, u1 = p1 ^ 0x80808080u;
+    float d[KB];
 #pragma unroll
-        for (int r = 0; r < KB - 1; ++r) { d[r] = hubrow[(size_t)r * N + n]; acc += d[r]; }
-    } else {
-        const uint32_t p0 = dpk[n + (n >> 5)];
+    for (int r = 0; r < KB - 1; ++r) d[r] = sbyte_to_float(r < 4 ? u0 : u1, r & 3);
+    float acc = 0.0f;
 #pragma unroll
-        for (int r = 0; r < 4 && r < KB - 1; ++r) { d[r] = (int)(signed char)((p0 >> (8 * r)) & 0xffu); acc += d[r]; }
-        if (KB == 8) {
-            const uint32_t p1 = dpk[dpk_words + n + (n >> 5)];
+    for (int r = 0; r < KB - 1; ++r) acc = acc + d[r];     // exact: small integers
+    d[KB - 1] = dsumf - acc;
+    float G = 0.0f;
 #pragma unroll
-            for (int r = 4; r < KB - 1; ++r) { d[r] = (int)(signed char)((p1 >> (8 * (r - 4))) & 0xffu); acc += d[r]; }
-        }
-    }
-    d[KB - 1] = dsum - acc;
+    for (int r = 0; r < KB; ++r) G = __fmaf_rn(d[r], gq[r], G);
+    return G;
 }
 
 template <int KB>
-__device__ __forceinline__ double fold_G(const int (&d)[KB], const float* gs, int N, int n) {
-    // each product d * g32 is exact in fp64 (|d| < 2^24, 24-bit g), so the
-    // fused multiply-add rounds exactly like the oracle's mul-then-add
-    double G = 0.0;
+__device__ __forceinline__ float fold_ints(const int* hubrow, int N, int n, int dsum, const float (&gq)[KB]) {
+    float d[KB];
+    int acc = 0;
 #pragma unroll
-    for (int r = 0; r < KB; ++r) G = __fma_rn((double)d[r], (double)gs[(size_t)r * N + n], G);
+    for (int r = 0; r < KB - 1; ++r) { const int x = hubrow[(size_t)r * N + n]; acc += x; d[r] = (float)x; }
+    d[KB - 1] = (float)(dsum - acc);
+    float G = 0.0f;
+#pragma unroll
+    for (int r = 0; r < KB; ++r) G = __fmaf_rn(d[r], gq[r], G);
     return G;
+}
+
+// Pass 3a of one row: G for every candidate (stored over its counts in dpk),
+// and the int64 fixed-point partial sum of J_v = sum_n G theta (R13).
+template <int KB, bool HUB>
+__device__ __forceinline__ long long pass_fold(const float* __restrict__ trow, uint32_t* dpk, size_t dpkw,
+                                               const float* gs, int* hubrow, int N, int GT, int tg, int dsum,
+                                               bool jvalid, int s) {
+    const float dsumf = (float)dsum;
+    const bool j32 = jvalid && s >= 0 && s <= 100;                 // theta 2^s exact in fp32
+    const float sc32 = j32 ? __uint_as_float((uint32_t)(127 + s) << 23) : 0.0f;
+    long long I = 0;
+    float4 th_nx = (4 * tg < N) ? *reinterpret_cast<const float4*>(trow + 4 * tg) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int n = 4 * tg; n < N; n += 4 * GT) {
+        const float4 th4 = th_nx;
+        if (n + 4 * GT < N) th_nx = *reinterpret_cast<const float4*>(trow + n + 4 * GT);
+        const float th[4] = {th4.x, th4.y, th4.z, th4.w};
+        float4 g4[KB];
+#pragma unroll
+        for (int r = 0; r < KB; ++r) g4[r] = *reinterpret_cast<const float4*>(gs + (size_t)r * N + n);
+        uint32_t* dp = dpk + n + (n >> 5);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float gq[KB];
+#pragma unroll
+            for (int r = 0; r < KB; ++r) gq[r] = q == 0 ? g4[r].x : q == 1 ? g4[r].y : q == 2 ? g4[r].z : g4[r].w;
+            float G;
+            if (HUB) G = fold_ints<KB>(hubrow, N, n + q, dsum, gq);
+            else G = fold_bytes<KB>(dp[q], KB == 8 ? dp[dpkw + q] : 0u, dsumf, gq);
+            dp[q] = __float_as_uint(G);
+            if (j32) I += __double2ll_rn((double)G * (double)(th[q] * sc32));
+            else if (jvalid) I += __double2ll_rn(times_pow2((double)G * (double)th[q], s));
+        }
+        if (HUB) {
+#pragma unroll
+            for (int r = 0; r < KB - 1; ++r) *reinterpret_cast<int4*>(hubrow + (size_t)r * N + n) = make_int4(0, 0, 0, 0);
+        }
+    }
+    return I;
 }
 
 // Bulk prefetch of [p, p + bytes) into L2 (TMA engine; bytes % 16 == 0).
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-// x * 2^s, exact (== scalbn) when 2^s is a normal double.
-__device__ __forceinline__ double times_pow2(double x, int s) {
-    if (s >= -1000 && s <= 1000) return x * __longlong_as_double((long long)(1023 + s) << 52);
-    return scalbn(x, s);
 }
 
 // Gather one occurrence record (own literal + others) into NP count planes.
@@ -189,15 +235,20 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
 #pragma unroll
                     for (int b = 0; b < kCtr; ++b) cnt[r][b] = 0u;
                 unsigned p = 0;
-                if (uni3) {
-                    // uniform 3-SAT: two records (4 independent gathers) per iteration
+                if (uni3 && nrec >= 6) {
+                    // uniform 3-SAT: two records (4 independent gathers) per
+                    // iteration, the next pair's gathers issued before counting
+                    auto ld = [&](uint32_t c) {
+                        return __ldg(Acur + ((c >> 1) * (unsigned)NW + (unsigned)w)) ^ (0u - (c & 1u));
+                    };
+                    uint32_t y01 = ld(rec[1]), y02 = ld(rec[2]), y11 = ld(rec[4]), y12 = ld(rec[5]);
                     for (; p + 6 <= nrec; p += 6) {
-                        const uint32_t h0 = rec[p], c01 = rec[p + 1], c02 = rec[p + 2];
-                        const uint32_t h1 = rec[p + 3], c11 = rec[p + 4], c12 = rec[p + 5];
-                        const uint32_t x01 = __ldg(Acur + ((c01 >> 1) * (unsigned)NW + (unsigned)w)) ^ (0u - (c01 & 1u));
-                        const uint32_t x02 = __ldg(Acur + ((c02 >> 1) * (unsigned)NW + (unsigned)w)) ^ (0u - (c02 & 1u));
-                        const uint32_t x11 = __ldg(Acur + ((c11 >> 1) * (unsigned)NW + (unsigned)w)) ^ (0u - (c11 & 1u));
-                        const uint32_t x12 = __ldg(Acur + ((c12 >> 1) * (unsigned)NW + (unsigned)w)) ^ (0u - (c12 & 1u));
+                        const uint32_t h0 = rec[p], h1 = rec[p + 3];
+                        const uint32_t x01 = y01, x02 = y02, x11 = y11, x12 = y12;
+                        if (p + 12 <= nrec) {
+                            y01 = ld(rec[p + 7]); y02 = ld(rec[p + 8]);
+                            y11 = ld(rec[p + 10]); y12 = ld(rec[p + 11]);
+                        }
                         uint32_t s0[NP], s1[NP];
                         s0[0] = own ^ (0u - (h0 & 1u)); s0[1] = 0u;
                         s1[0] = own ^ (0u - (h1 & 1u)); s1[1] = 0u;
@@ -231,27 +282,9 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
         }
         group_bar(bar, GT);
 
-        // ---- 3a: G (fp64 fold, rounded to fp32, R27) -> smem; J_v = sum G theta (int64 fixed point)
-        long long I = 0;
-        for (int base = 0; base < N; base += 4 * GT) {
-            const int n = base + 4 * tg;
-            if (n < N) {
-                const float4 th4 = *reinterpret_cast<const float4*>(trow + n);
-                const float th[4] = {th4.x, th4.y, th4.z, th4.w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    int d[KB];
-                    load_counts<KB>(d, dpk, dpkw, hubrow, N, n + q, dsum, hub >= 0);
-                    const float G32 = (float)fold_G<KB>(d, gs, N, n + q);
-                    dpk[n + q + ((n + q) >> 5)] = __float_as_uint(G32);
-                    if (jvalid) I += __double2ll_rn(times_pow2((double)G32 * (double)th[q], s));
-                }
-                if (hub >= 0) {
-#pragma unroll
-                    for (int r = 0; r < NCTR; ++r) *reinterpret_cast<int4*>(hubrow + (size_t)r * N + n) = make_int4(0, 0, 0, 0);
-                }
-            }
-        }
+        // ---- 3a: G (fp32 FMA chain over exact counts, R27) -> smem; J_v partial
+        long long I = hub >= 0 ? pass_fold<KB, true>(trow, dpk, dpkw, gs, hubrow, N, GT, tg, dsum, jvalid, s)
+                               : pass_fold<KB, false>(trow, dpk, dpkw, gs, hubrow, N, GT, tg, dsum, jvalid, s);
         I = warp_sum(I);
         if (lane == 0) red[gw] = I;
         group_bar(bar, GT);
@@ -273,19 +306,30 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
         // ---- 3b: grad, AdamW, next-state statistics and sign planes
         long long Qn = 0;
         float mx = 0.0f;
+        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 thn = z4, mn4 = z4, vn4 = z4;
+        if (4 * tg < N) {
+            thn = *reinterpret_cast<const float4*>(trow + 4 * tg);
+            mn4 = *reinterpret_cast<const float4*>(mrow + 4 * tg);
+            vn4 = *reinterpret_cast<const float4*>(vrow + 4 * tg);
+        }
         for (int base = 0; base < N; base += 4 * GT) {
             const int n = base + 4 * tg;
             unsigned pnib = 0, nnib = 0;
+            const float4 th4 = thn, m4 = mn4, v4 = vn4;
+            if (n + 4 * GT < N) {
+                thn = *reinterpret_cast<const float4*>(trow + n + 4 * GT);
+                mn4 = *reinterpret_cast<const float4*>(mrow + n + 4 * GT);
+                vn4 = *reinterpret_cast<const float4*>(vrow + n + 4 * GT);
+            }
             if (n < N) {
-                float4 th4 = *reinterpret_cast<const float4*>(trow + n);
-                float4 m4 = *reinterpret_cast<const float4*>(mrow + n);
-                float4 v4 = *reinterpret_cast<const float4*>(vrow + n);
                 float th[4] = {th4.x, th4.y, th4.z, th4.w};
                 float mm[4] = {m4.x, m4.y, m4.z, m4.w};
                 float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+                const uint32_t* dp = dpk + n + (n >> 5);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const float G32 = __uint_as_float(dpk[n + q + ((n + q) >> 5)]);
+                    const float G32 = __uint_as_float(dp[q]);
                     const float g = (float)((double)G32 * rho - c);
                     float x = th[q] * wdf;
                     const float mn = __fmaf_rn(a1, g - mm[q], mm[q]);
@@ -475,10 +519,10 @@ __global__ void __launch_bounds__(256) k_update_rowcta(StepArgs a, const uint32_
             for (int r = 0; r < KB; ++r) cnt[r] += (R == (uint32_t)r) ? delta : 0;
             p += len;
         }
-        double G = 0.0;
+        float G = 0.0f;                                            // R27: fp32 FMA chain
 #pragma unroll
-        for (int r = 0; r < KB; ++r) G = G + (double)cnt[r] * (double)a.gtab[(size_t)r * N + n];
-        Gs[n] = (double)(float)G;                                  // R27
+        for (int r = 0; r < KB; ++r) G = __fmaf_rn((float)cnt[r], a.gtab[(size_t)r * N + n], G);
+        Gs[n] = (double)G;
         if (jvalid) I += __double2ll_rn(scalbn(Gs[n] * (double)trow[n], s));
     }
     float dummy = 0.0f;

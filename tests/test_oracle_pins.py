@@ -298,7 +298,7 @@ def test_gradient_matches_torch_autograd(seed, tau, normalize):
     G64 = _G_from_g64(o.cnf, s.R, s.g)
     assert np.abs(s.G - G64).max() <= 2.4e-7 * np.abs(G64).max()
     G32 = _G_from_g64(o.cnf, s.R, s.g32.astype(np.float64))
-    np.testing.assert_array_equal(s.G, G32.astype(np.float32).astype(np.float64))
+    assert np.abs(s.G - G32).max() <= 4 * 2.0 ** -24 * np.abs(G32).max()
     assert abs(s.loss - Lref) <= 1e-12 * abs(Lref)
     np.testing.assert_array_equal(s.grad, ours.astype(np.float32))
 
