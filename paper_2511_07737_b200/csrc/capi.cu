@@ -471,6 +471,8 @@ tsat_status tsat_workspace_bytes(tsat_ctx ctx, int64_t N_global, size_t* bytes) 
         return fail(ctx, TSAT_E_ARG, "N_global must be a positive multiple of 32 * world");
     int64_t N = N_global / ctx->world;
     if (N_global >= (1LL << 32)) return fail(ctx, TSAT_E_RANGE, "N_global >= 2^32");
+    if ((int64_t)ctx->cnf.V * (N / 32) >= (1LL << 31))
+        return fail(ctx, TSAT_E_RANGE, "V * N / 32 >= 2^31 (32-bit bit-plane offsets)");
     if ((size_t)N * 12 > 200 * 1024) return fail(ctx, TSAT_E_RANGE, "N per GPU > 17066 not supported by the fused update");
     int KB = ctx->cnf.K <= 3 ? 4 : 8;
     *bytes = make_layout(ctx->cnf.V, (int)N, KB, ctx->cnf.n_hubs).total;

@@ -4,12 +4,14 @@
 // Bit-sliced design: lane = one 32-candidate word of the batch, warp = 32
 // consecutive words (1024 candidates), so every literal gather is one
 // 128-byte coalesced load of the bit plane.  R_cn is accumulated as NP
-// bit-planes; the one-hot masks [R = r] feed 7-bit vertical counters per bin;
-// after CH <= 127 clauses each lane extracts per-candidate counts into a
-// shared histogram (bank-rotated), and the CTA adds it to the global one.
-// A warp first stages its chunk's literal codes in shared memory (one
-// coalesced read of the CSR), then evaluates UNR clauses at a time so
-// UNR * KMAXC independent gathers are in flight.
+// bit-planes; the one-hot masks [R = r] of 4 clauses are combined by a
+// carry-save tree (ones, twos planes) before one ripple into the 7-bit
+// vertical counters of each bin.  After CH <= 127 clauses each lane extracts
+// per-candidate counts into a shared histogram (bank-rotated), and the CTA
+// adds it to the global one.  A warp first stages its chunk's literals in
+// shared memory as pre-multiplied bit-plane word offsets (one coalesced read
+// of the CSR), then evaluates 4 clauses at a time so 4 * KMAXC independent
+// gathers are in flight.
 #include "device_common.cuh"
 
 namespace tsat {
@@ -17,89 +19,130 @@ namespace tsat {
 namespace {
 constexpr int kWarps = 8;
 constexpr int kCH = 64;        // clauses per warp chunk (<= 127: 7-bit counters)
-constexpr int kUnr = 4;        // clauses evaluated together
+constexpr int kUnr = 4;        // clauses evaluated together (carry-save group)
 constexpr uint32_t kNone = 0xffffffffu;
+
+// full adder on bit planes: (a + b + c) = s + 2 * carry
+__device__ __forceinline__ void fa(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& carry) {
+    s = a ^ b ^ c;
+    carry = (a & b) | (c & (a ^ b));
+}
 }  // namespace
 
+// Counter of one bin: planes[0] = ones, planes[1] = twos, planes[2..6] weight 4..64.
+template <int CB>
+__device__ __forceinline__ void csa_add4(uint32_t (&c)[CB], uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3) {
+    uint32_t s, c1, c2, c4;
+    fa(c[0], m0, m1, s, c1);
+    fa(s, m2, m3, c[0], c2);
+    fa(c[1], c1, c2, c[1], c4);
+    uint32_t carry = c4;
+#pragma unroll
+    for (int b = 2; b < CB; ++b) {
+        uint32_t t = c[b] & carry;
+        c[b] ^= carry;
+        carry = t;
+    }
+}
+
 template <int KB, int KMAXC>
-__global__ void __launch_bounds__(256) k_clause(const uint32_t* __restrict__ A, int NW, const uint32_t* __restrict__ cptr,
-                                                const uint32_t* __restrict__ clit, long long C, int* __restrict__ hist,
-                                                int N, int uniform) {
+__global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t* __restrict__ A, int NW,
+                                                                const uint32_t* __restrict__ cptr,
+                                                                const uint32_t* __restrict__ clit, long long C,
+                                                                int* __restrict__ hist, int N, int uniform) {
     constexpr int NP = (KB == 4) ? 2 : 3;
     constexpr int CB = 7;
     __shared__ int sh[(KB - 1) * 1024];
-    __shared__ uint32_t scode[kWarps][kCH * KMAXC];
+    __shared__ uint32_t soff[kWarps][kCH * KMAXC];     // (var * NW) << 1 | negated, or kNone
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int w = blockIdx.x * 32 + lane;
     const bool valid = w < NW;
     for (int i = threadIdx.x; i < (KB - 1) * 1024; i += blockDim.x) sh[i] = 0;
-    const long long c0 = ((long long)blockIdx.y * kWarps + warp) * kCH;
-    const long long c1 = c0 + kCH < C ? c0 + kCH : C;
-    const int nc = c1 > c0 ? (int)(c1 - c0) : 0;
-    // stage codes: slot (c, l) of the chunk, kNone where clause c has < l+1 literals
-    uint32_t* my = scode[warp];
-    if (uniform) {
-        const uint32_t* src = clit + (size_t)c0 * KMAXC;
-        for (int i = lane; i < kCH * KMAXC; i += 32) my[i] = (i < nc * KMAXC) ? src[i] : kNone;
-    } else {
-        for (int i = lane; i < kCH * KMAXC; i += 32) {
-            const int c = i / KMAXC, l = i - c * KMAXC;
-            uint32_t code = kNone;
-            if (c < nc) {
-                const uint32_t b = cptr[c0 + c], e = cptr[c0 + c + 1];
-                if (b + l < e) code = clit[b + l];
-            }
-            my[i] = code;
-        }
-    }
     __syncthreads();
-    uint32_t cnt[KB - 1][CB];
-#pragma unroll
-    for (int r = 0; r < KB - 1; ++r)
-#pragma unroll
-        for (int b = 0; b < CB; ++b) cnt[r][b] = 0u;
-    const size_t wofs = valid ? (size_t)w : 0;
-    for (int cb = 0; cb < nc; cb += kUnr) {
-        uint32_t x[kUnr][KMAXC];
-#pragma unroll
-        for (int u = 0; u < kUnr; ++u)
-#pragma unroll
-            for (int l = 0; l < KMAXC; ++l) {
-                const uint32_t code = (cb + u < nc) ? my[(cb + u) * KMAXC + l] : kNone;
-                uint32_t val = 0u;
-                if (code != kNone && valid) val = __ldg(A + (size_t)(code >> 1) * NW + wofs) ^ (0u - (code & 1u));
-                x[u][l] = val;
+    uint32_t* my = soff[warp];
+    const uint32_t unw = (uint32_t)NW;
+    const uint32_t* Aw = A + (valid ? w : 0);
+    const long long nchunks = (C + kCH - 1) / kCH;
+    // grid-sized: warps stride over the clause chunks of this word block
+    for (long long chunk = (long long)blockIdx.y * kWarps + warp; chunk < nchunks;
+         chunk += (long long)gridDim.y * kWarps) {
+        const long long c0 = chunk * kCH;
+        const long long c1 = c0 + kCH < C ? c0 + kCH : C;
+        const int nc = (int)(c1 - c0);
+        __syncwarp();
+        if (uniform) {
+            const uint32_t* src = clit + (size_t)c0 * KMAXC;
+            for (int i = lane; i < kCH * KMAXC; i += 32) {
+                const uint32_t code = (i < nc * KMAXC) ? src[i] : kNone;
+                my[i] = code == kNone ? kNone : (((code >> 1) * unw) << 1) | (code & 1u);
             }
-#pragma unroll
-        for (int u = 0; u < kUnr; ++u) {
-            if (cb + u >= nc) break;
-            uint32_t s[NP];
-#pragma unroll
-            for (int p = 0; p < NP; ++p) s[p] = 0u;
-#pragma unroll
-            for (int l = 0; l < KMAXC; ++l) bs_add<NP>(s, x[u][l]);
-#pragma unroll
-            for (int r = 0; r < KB - 1; ++r) {
-                uint32_t carry = bs_eq<NP>(s, r);
-#pragma unroll
-                for (int b = 0; b < CB; ++b) {
-                    uint32_t t = cnt[r][b] & carry;
-                    cnt[r][b] ^= carry;
-                    carry = t;
+        } else {
+            for (int i = lane; i < kCH * KMAXC; i += 32) {
+                const int c = i / KMAXC, l = i - c * KMAXC;
+                uint32_t o = kNone;
+                if (c < nc) {
+                    const uint32_t b = cptr[c0 + c], e = cptr[c0 + c + 1];
+                    if (b + l < e) {
+                        const uint32_t code = clit[b + l];
+                        o = (((code >> 1) * unw) << 1) | (code & 1u);
+                    }
                 }
+                my[i] = o;
             }
         }
-    }
-    if (valid) {
+        __syncwarp();
+        uint32_t cnt[KB - 1][CB];
 #pragma unroll
         for (int r = 0; r < KB - 1; ++r)
-            for (int j0 = 0; j0 < 32; ++j0) {
-                int j = (j0 + lane) & 31;            // rotate: conflict-free smem banks
-                int val = 0;
 #pragma unroll
-                for (int b = 0; b < CB; ++b) val |= (int)((cnt[r][b] >> j) & 1u) << b;
-                if (val) atomicAdd(&sh[r * 1024 + lane * 32 + j], val);
+            for (int b = 0; b < CB; ++b) cnt[r][b] = 0u;
+        for (int cb = 0; cb < nc; cb += kUnr) {
+            uint32_t x[kUnr][KMAXC];
+#pragma unroll
+            for (int u = 0; u < kUnr; ++u)
+#pragma unroll
+                for (int l = 0; l < KMAXC; ++l) {
+                    const uint32_t o = (cb + u < nc) ? my[(cb + u) * KMAXC + l] : kNone;
+                    uint32_t val = 0u;
+                    if (o != kNone && valid) val = __ldg(Aw + (o >> 1)) ^ (0u - (o & 1u));
+                    x[u][l] = val;
+                }
+            // one-hot masks [R = r] per clause (padding clauses past nc have all
+            // literals 0 -> R = 0, so their bin-0 mask is cleared)
+            uint32_t m[kUnr][KB - 1];
+#pragma unroll
+            for (int u = 0; u < kUnr; ++u) {
+                const uint32_t live = (cb + u < nc) ? 0xffffffffu : 0u;
+                if (KMAXC == 3 && KB == 4) {
+                    const uint32_t a = x[u][0], b = x[u][1], c = x[u][2];
+                    m[u][0] = ~(a | b | c) & live;                     // R = 0
+                    const uint32_t s0 = a ^ b ^ c, s1 = (a & b) | (c & (a ^ b));
+                    m[u][1] = s0 & ~s1;                                 // R = 1
+                    m[u][2] = ~s0 & s1;                                 // R = 2
+                } else {
+                    uint32_t sp[NP];
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) sp[p] = 0u;
+#pragma unroll
+                    for (int l = 0; l < KMAXC; ++l) bs_add<NP>(sp, x[u][l]);
+#pragma unroll
+                    for (int r = 0; r < KB - 1; ++r) m[u][r] = bs_eq<NP>(sp, r) & (r == 0 ? live : 0xffffffffu);
+                }
             }
+#pragma unroll
+            for (int r = 0; r < KB - 1; ++r) csa_add4<CB>(cnt[r], m[0][r], m[1][r], m[2][r], m[3][r]);
+        }
+        if (valid) {
+#pragma unroll
+            for (int r = 0; r < KB - 1; ++r)
+                for (int j0 = 0; j0 < 32; ++j0) {
+                    int j = (j0 + lane) & 31;            // rotate: conflict-free smem banks
+                    int val = 0;
+#pragma unroll
+                    for (int b = 0; b < CB; ++b) val |= (int)((cnt[r][b] >> j) & 1u) << b;
+                    if (val) atomicAdd(&sh[r * 1024 + lane * 32 + j], val);
+                }
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < (KB - 1) * 1024; i += blockDim.x) {
@@ -113,8 +156,16 @@ __global__ void __launch_bounds__(256) k_clause(const uint32_t* __restrict__ A, 
 cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, cudaStream_t st) {
     if (a.C == 0) return cudaGetLastError();
     const int NW = a.N >> 5;
-    dim3 grid((NW + 31) / 32, (unsigned)((a.C + (long long)kWarps * kCH - 1) / ((long long)kWarps * kCH)));
+    const int nwb = (NW + 31) / 32;
+    const long long nchunks = (a.C + kCH - 1) / kCH;
+    const long long ctas_needed = (nchunks + kWarps - 1) / kWarps;
     const int K = a.mc.K;
+    // grid-sized: (CTAs resident per SM) x SMs, split over the word blocks
+    const int per_sm = K <= 3 ? 3 : 2;
+    long long gy = ((long long)a.num_sms * per_sm + nwb - 1) / nwb;
+    if (gy > ctas_needed) gy = ctas_needed;
+    if (gy < 1) gy = 1;
+    dim3 grid(nwb, (unsigned)gy);
     const int uni = a.uniform_len;
     if (K <= 2)
         k_clause<4, 2><<<grid, 256, 0, st>>>(Acur, NW, a.cptr, a.clit, a.C, a.hist, a.N, uni && K == 2);
