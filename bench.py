@@ -10,9 +10,11 @@ Workload at N=1: config c2 (planted random 3-SAT, V=10k, C=42k, ratio 4.2,
 N=4096 candidates), seeded synthetic input.  The state streamed every step
 (theta, m, v: 492 MB) is larger than L2, so no explicit flush is needed.
 
-Prints ONE JSON line (rank 0).  Under torchrun (N>1) each rank runs its own
-replica of the workload (weak scaling; the NCCL candidate-sharded path is not
-built yet), timed on the device, max over ranks.
+Prints ONE JSON line (rank 0).  Under torchrun (N>1) the candidate batch is
+sharded over the ranks (N_global = N_config * world, weak scaling): each rank
+holds N_config candidates, the CNF is replicated, and per iteration the ranks
+exchange Eq. 5's exact integer row / Jacobian sums and three maxima over NCCL
+(DESIGN.md §9).  Timed on the device, max over ranks.
 """
 from __future__ import annotations
 
@@ -190,13 +192,18 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     cnf, cfg = make_config(args.config)
-    N = cfg["N"]
-    seed = cfg["seed"] + rank          # replicas: one independent batch per rank
+    N = cfg["N"]                       # candidates per GPU
+    seed = cfg["seed"]
     stream = torch.cuda.current_stream()
 
-    s = Solver(local, stream=stream)
+    def make_solver():
+        if world > 1:
+            return Solver.distributed(local, rank, world, stream=stream)
+        return Solver(local, stream=stream)
+
+    s = make_solver()
     info = s.load_cnf(cnf)
-    s.init_batch(N, seed)
+    s.init_batch(N * world, seed)
     chunk = max(1, min(args.chunk, args.steps))
     assert args.steps % chunk == 0, "--steps must be a multiple of --chunk"
     # warm-up (also instantiates the chunk-sized CUDA graph)
@@ -263,14 +270,14 @@ def main():
     if not args.no_e2e:
         K_e2e = min(args.steps, 60)
         unsat_host = np.empty(N, np.int32)
-        s2 = Solver(local, stream=stream)
+        s2 = make_solver()
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
         f0 = torch.cuda.Event(enable_timing=True); f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         s2.load_cnf(cnf)                      # host CSR -> device
-        s2.init_batch(N, seed)
+        s2.init_batch(N * world, seed)
         for _ in range(K_e2e):
             s2.step(1)                        # H2D step scalars, D2H step info
             s2.query_unsat(unsat_host)        # D2H per-candidate unsat counts
@@ -304,7 +311,7 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_desc(args.config, cnf, N * world), "V": cnf.V, "C": cnf.C, "K": cnf.K,
                    "N_per_gpu": N, "N_global": N * world, "seed": seed,
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "parallelism": f"candidate-sharded x{world} (NCCL exact int64 exchanges)" if world > 1 else "single GPU",
                    "l2": "state (theta, m, v: %.0f MB) larger than L2; no flush" % (12 * cnf.V * N / 1e6),
                    "graph_chunk": chunk},
         "gradient_steps_per_s": args.steps / (ms / 1000.0),

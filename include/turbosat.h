@@ -115,11 +115,24 @@ tsat_status tsat_parse_dimacs(const char* text, size_t len, tsat_cnf_info* info)
 const char* tsat_status_string(tsat_status s);
 
 /* Create a context on CUDA device `cuda_device`, enqueueing on `cuda_stream`
- * (a cudaStream_t; NULL = legacy default stream).  Multi-GPU (world > 1,
- * candidate sharding) needs `nccl_unique_id` (128 bytes,
- * identical on all ranks); pass NULL when world == 1. */
+ * (a cudaStream_t; NULL = legacy default stream).
+ * Multi-GPU (candidate sharding): every rank calls
+ * tsat_create concurrently with the same `nccl_unique_id` (128 bytes from
+ * tsat_nccl_unique_id on one rank, broadcast by the caller), its `rank` and
+ * `world`; rank r then holds candidates [r N/W, (r+1) N/W).  Per iteration
+ * the ranks exchange, over NCCL on the caller's stream, only exact integer
+ * quantities (Eq. 5 row sums and Jacobian sums, the best candidate and two
+ * maxima), so results are bit-identical for every world size.
+ * nccl_unique_id == NULL requires world == 1 (single-GPU fused path); a
+ * non-NULL id with world == 1 runs the sharded kernels on a 1-rank
+ * communicator.  Errors: TSAT_E_ARG, TSAT_E_NCCL (libnccl.so.2 missing or
+ * communicator init failed), TSAT_E_CUDA. */
 tsat_status tsat_create(tsat_ctx* out, int cuda_device, void* cuda_stream,
                         const void* nccl_unique_id, int rank, int world);
+
+/* Write a fresh NCCL unique id (NCCL_UNIQUE_ID_BYTES = 128) to out[0..bytes).
+ * Host only; opens libnccl.so.2 at run time.  TSAT_E_NCCL if unavailable. */
+tsat_status tsat_nccl_unique_id(void* out, size_t bytes);
 
 /* Load a CNF from DIMACS text: comments 'c', header
  * 'p cnf V C', clauses as signed integers terminated by 0.  Duplicate
@@ -168,7 +181,9 @@ tsat_status tsat_export_best(tsat_ctx ctx, int32_t M, int32_t k, tsat_partial* h
 /* Binary values (0/1, V bytes) of candidate global_idx at the last evaluated state. */
 tsat_status tsat_export_model(tsat_ctx ctx, int64_t global_idx, uint8_t* host_values);
 
-/* The first model found (V bytes); TSAT_E_STATE if no candidate has reached 0 unsat. */
+/* The first model found (V bytes); TSAT_E_STATE if no candidate has reached 0
+ * unsat.  world > 1: *idx and *step are global; the bits are written only on
+ * the rank that owns candidate *idx (other ranks leave host_values untouched). */
 tsat_status tsat_get_solution(tsat_ctx ctx, uint8_t* host_values, int64_t* idx, int64_t* step);
 
 /* Checkpoint / resume: theta, m, v as [V][N_local] fp32 host arrays (any may be

@@ -18,7 +18,10 @@ from .binding import (  # noqa: F401
     TsatError,
     config_default,
     load_library,
+    merge_partials,
+    nccl_unique_id,
     parse_dimacs,
 )
 
-__all__ = ["Solver", "StepInfo", "TsatError", "config_default", "load_library", "parse_dimacs", "LIB_PATH"]
+__all__ = ["Solver", "StepInfo", "TsatError", "config_default", "load_library", "merge_partials", "nccl_unique_id",
+           "parse_dimacs", "LIB_PATH"]

@@ -56,6 +56,7 @@ _SIGS = {
     "tsat_config_default": (ct.c_int, [ct.POINTER(tsat_config)]),
     "tsat_parse_dimacs": (ct.c_int, [ct.c_char_p, ct.c_size_t, ct.POINTER(tsat_cnf_info)]),
     "tsat_status_string": (ct.c_char_p, [ct.c_int]),
+    "tsat_nccl_unique_id": (ct.c_int, [P, ct.c_size_t]),
     "tsat_create": (ct.c_int, [ct.POINTER(P), ct.c_int, P, P, ct.c_int, ct.c_int]),
     "tsat_load_dimacs": (ct.c_int, [P, ct.c_char_p, ct.c_size_t, ct.POINTER(tsat_cnf_info)]),
     "tsat_load_clauses": (ct.c_int, [P, ct.c_int32, ct.c_int64, P, P, ct.POINTER(tsat_cnf_info)]),
@@ -116,6 +117,23 @@ def parse_dimacs(text: bytes) -> tsat_cnf_info:
     return info
 
 
+def nccl_unique_id() -> bytes:
+    """tsat_nccl_unique_id: 128 bytes, to be broadcast to every rank."""
+    buf = ct.create_string_buffer(128)
+    s = load_library().tsat_nccl_unique_id(buf, 128)
+    if s:
+        raise TsatError(s, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def merge_partials(per_rank: list, M: int) -> list:
+    """Global top-M of per-rank export lists by (unsat asc, candidate asc)
+    (R15).  Host logic of the sharded export."""
+    allp = [p for lst in per_rank for p in lst]
+    allp.sort(key=lambda p: (p["unsat"], p["candidate"]))
+    return allp[:M]
+
+
 @dataclass
 class StepInfo:
     t: int
@@ -135,6 +153,9 @@ class Solver:
     set_state for checkpoint-resume."""
 
     def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_unique_id: bytes | None = None):
+        """world > 1 (or a unique id with world == 1): candidate-sharded path;
+        every rank must construct its Solver concurrently with the same id
+        (see Solver.distributed)."""
         import torch
         self._torch = torch
         if not torch.cuda.is_available():
@@ -149,8 +170,19 @@ class Solver:
         self.h = h
         self.ws = None
         self.V = self.C = self.N = self.N_local = 0
+        self.rank, self.world = rank, world
         self.n0 = 0
         self.info = None
+
+    @classmethod
+    def distributed(cls, device: int, rank: int, world: int, stream=None, group=None):
+        """Sharded solver over a torch.distributed group: rank 0 makes the NCCL
+        unique id, every rank receives it (broadcast_object_list) and joins."""
+        import torch.distributed as dist
+        obj = [nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(device, stream=stream, rank=rank, world=world, nccl_unique_id=obj[0])
 
     # -- helpers
     def _check(self, s, h="self"):
@@ -207,6 +239,8 @@ class Solver:
         self._check(self.lib.tsat_init_batch(self.h, int(N_global), int(seed) & (2**64 - 1), ct.byref(cfg),
                                              ct.c_void_p(self.ws.data_ptr()), nbytes))
         self.N = int(N_global)
+        self.N_local = self.N // self.world
+        self.n0 = self.rank * self.N_local
         return self
 
     def step(self, k: int = 1, wait: bool = True) -> StepInfo | None:
@@ -232,7 +266,7 @@ class Solver:
         return out
 
     def N_local_count(self) -> int:
-        return self.N  # world == 1 on this build; multi-rank divides by world
+        return self.N // self.world
 
     def export_best(self, M: int, k: int = 0):
         kk = k if k > 0 else min(self.V, max(-(-self.V // 10000), 20))

@@ -12,7 +12,17 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libturbosat.so")
-SOURCES = ["capi.cu", "launch.cu", "k_clause.cu", "k_misc.cu", "k_update.cu", "host_cnf.cpp"]
+def _nccl_include() -> str:
+    """nccl.h of the NCCL PyTorch ships (the library itself is dlopen'ed)."""
+    try:
+        import nvidia.nccl
+        return os.path.join(list(nvidia.nccl.__path__)[0], "include")
+    except Exception:
+        return "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/include"
+
+
+NCCL_INC = _nccl_include()
+SOURCES = ["capi.cu", "launch.cu", "k_clause.cu", "k_misc.cu", "k_update.cu", "k_shard.cu", "comm.cpp", "host_cnf.cpp"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -23,6 +33,8 @@ NVCC_FLAGS = [
     "--shared",
     "-cudart", "static",
     "-I", os.path.join(ROOT, "include"),
+    "-I", NCCL_INC,
+    "-ldl",
 ]
 
 

@@ -29,6 +29,8 @@ struct tsat_ctx_s {
     int device = 0;
     cudaStream_t stream = nullptr;      // caller's stream: every launch / copy
     cudaStream_t cap_stream = nullptr;  // private stream used only to capture graphs
+    bool sharded = false;               // candidate-sharded path (NCCL communicator)
+    void* comm = nullptr;               // ncclComm_t
     int rank = 0, world = 1;
     tsat_status poisoned = TSAT_OK;
     std::string err;
@@ -93,7 +95,7 @@ tsat_status cuda_fail(tsat_ctx c, cudaError_t e, const char* where) {
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
-Layout make_layout(int V, int N, int KB, int n_hubs) {
+Layout make_layout(int V, int N, int KB, int n_hubs, bool sharded) {
     Layout L{};
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -119,6 +121,13 @@ Layout make_layout(int V, int N, int KB, int n_hubs) {
     L.steptab = take(sizeof(StepScalars) * kMaxStepsPerCall);
     L.sol = take((size_t)V);
     L.hubD = take((size_t)n_hubs * (KB - 1) * N * 4);
+    const size_t sv = sharded ? 1 : 0;
+    L.Gbuf = take(sv * VN * 4);
+    L.Jbuf = take(sv * (size_t)V * 8);
+    L.Qbuf = take(sv * ((size_t)V + 1) * 8);
+    L.Pbuf = take(sv * (size_t)V * NW * 4);
+    L.Nbuf = take(sv * (size_t)V * NW * 4);
+    L.maxbuf = take(sv * 3 * 8);
     L.total = off;
     return L;
 }
@@ -161,6 +170,13 @@ StepArgs step_args(tsat_ctx ctx) {
     a.upd_grid = ctx->upd_grid;
     a.upd_smem = ctx->upd_smem;
     a.upd_rec_cap = std::max(64, (ctx->cnf.max_rec_words + 63) / 64 * 64);
+    a.sharded = ctx->sharded ? 1 : 0;
+    a.Gbuf = (float*)(w + L.Gbuf);
+    a.Jbuf = (long long*)(w + L.Jbuf);
+    a.Qbuf = (long long*)(w + L.Qbuf);
+    a.Pbuf = (uint32_t*)(w + L.Pbuf);
+    a.Nbuf = (uint32_t*)(w + L.Nbuf);
+    a.maxbuf = (unsigned long long*)(w + L.maxbuf);
     a.V = ctx->cnf.V;
     a.N = ctx->N;
     a.C = ctx->cnf.C;
@@ -268,6 +284,62 @@ tsat_status check_batch(tsat_ctx ctx, bool need_step) {
     return TSAT_OK;
 }
 
+// Eq. 5 row statistics and bit planes of the state theta_t (init / set_state):
+// one kernel for W = 1; partial sums + exact int64 exchange when sharded.
+tsat_status state_stats(tsat_ctx ctx, const StepArgs& a, int64_t t) {
+    uint32_t* A = (t & 1) ? a.A1 : a.A0;
+    unsigned int* thm = &a.ds->thmax_bits[t & 1];
+    if (!ctx->sharded) {
+        CK(launch_rowstats(a.theta, a.V, a.N, ctx->mc, a.rowQ, a.rowD, a.rowRho, a.rowGuard, A, thm, ctx->stream));
+    } else {
+        std::string err;
+        CK(launch_rows_partial(a, a.theta, thm, ctx->stream));
+        if (comm_allreduce_sum_i64(ctx->comm, a.Qbuf, (size_t)a.V + 1, ctx->stream, &err)) {
+            ctx->poisoned = TSAT_E_NCCL;
+            ctx->err = err;
+            return TSAT_E_NCCL;
+        }
+        CK(launch_rows_finish(a, A, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TSAT_OK;
+}
+
+// One profiling segment of an iteration.  W = 1: one kernel per segment.
+// Sharded: the segments also hold the collectives:
+//   0 clause | 1 gtable, MAX(best, gmax, thmax) | 2 hub |
+//   3 update A, SUM J, update B, SUM Q+loss, rows finish | 4 step end.
+// Returns 0, 6 (CUDA) or 7 (NCCL) with *err.
+int launch_segment(tsat_ctx ctx, const StepArgs& a, int seg, const StepScalars* sc, long long t, cudaStream_t st,
+                   std::string* err) {
+    auto ck = [&](cudaError_t e, const char* what) {
+        if (e == cudaSuccess) return 0;
+        *err = std::string(what) + ": " + cudaGetErrorString(e);
+        return 6;
+    };
+    if (!ctx->sharded) return ck(launch_step_kernel(seg, a, sc, t, st), "step kernel");
+    const uint32_t* Acur = (t & 1) ? a.A1 : a.A0;
+    uint32_t* Anext = (t & 1) ? a.A0 : a.A1;
+    int r = 0;
+    switch (seg) {
+        case 0: return ck(launch_step_kernel(0, a, sc, t, st), "k_clause");
+        case 1:
+            if ((r = ck(launch_step_kernel(1, a, sc, t, st), "k_gtable"))) return r;
+            if ((r = ck(launch_shard_pack_max(a, sc, st), "k_pack_max"))) return r;
+            if ((r = comm_allreduce_max_u64(ctx->comm, a.maxbuf, 3, st, err))) return r;
+            return ck(launch_shard_unpack_max(a, sc, st), "k_unpack_max");
+        case 2: return ck(launch_step_kernel(2, a, sc, t, st), "k_hub");
+        case 3:
+            if ((r = ck(launch_update_a(a, Acur, sc, st), "k_update(A)"))) return r;
+            if ((r = comm_allreduce_sum_i64(ctx->comm, a.Jbuf, (size_t)a.V, st, err))) return r;
+            if ((r = ck(launch_update_b(a, Acur, sc, st), "k_update_b"))) return r;
+            if ((r = comm_allreduce_sum_i64(ctx->comm, a.Qbuf, (size_t)a.V + 1, st, err))) return r;
+            return ck(launch_rows_finish(a, Anext, st), "k_rows_finish");
+        case 4: return ck(launch_step_end_sharded(a, sc, st), "k_step_end");
+    }
+    return 0;
+}
+
 // Launch the k-iteration sequence (graph or direct).
 tsat_status launch_steps(tsat_ctx ctx, int k) {
     StepArgs a = step_args(ctx);
@@ -280,6 +352,8 @@ tsat_status launch_steps(tsat_ctx ctx, int k) {
             ctx->events.push_back(e);
         }
     }
+    std::string serr;
+    int sstat = 0;
     auto body = [&](bool capture) -> cudaError_t {
         for (int i = 0; i < k; ++i) {
             long long t = ctx->t + i;
@@ -291,8 +365,8 @@ tsat_status launch_steps(tsat_ctx ctx, int k) {
                 }
                 // kernels read t from the step table; the parity of t selects
                 // the A buffers, so the graph is keyed by (k, t parity).
-                cudaError_t e = launch_step_kernel(kk, a, sc + i, t, ctx->cap_stream);
-                if (e != cudaSuccess) return e;
+                sstat = launch_segment(ctx, a, kk, sc + i, t, ctx->cap_stream, &serr);
+                if (sstat) return cudaErrorUnknown;
             }
             if (ctx->profiling) {
                 cudaError_t e = cudaEventRecordWithFlags(ctx->events[(size_t)i * (kKernelsPerStep + 1) + kKernelsPerStep],
@@ -312,6 +386,12 @@ tsat_status launch_steps(tsat_ctx ctx, int k) {
         CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
         cudaError_t e = body(true);
         cudaError_t e2 = cudaStreamEndCapture(ctx->cap_stream, &g);
+        if (sstat) {
+            if (e2 == cudaSuccess) cudaGraphDestroy(g);
+            ctx->poisoned = sstat == 7 ? TSAT_E_NCCL : TSAT_E_CUDA;
+            ctx->err = serr;
+            return ctx->poisoned;
+        }
         if (e != cudaSuccess) return cuda_fail(ctx, e, "capture step kernels");
         if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "cudaStreamEndCapture");
         cudaGraphExec_t ex;
@@ -417,8 +497,7 @@ tsat_status tsat_create(tsat_ctx* out, int cuda_device, void* cuda_stream, const
     if (!out) return TSAT_E_ARG;
     *out = nullptr;
     if (world < 1 || rank < 0 || rank >= world) return TSAT_E_ARG;
-    if (world > 1) return TSAT_E_UNSUPPORTED;   // multi-GPU path: DESIGN.md "Multi-GPU"
-    (void)nccl_unique_id;
+    if (world > 1 && !nccl_unique_id) return TSAT_E_ARG;
     std::unique_ptr<tsat_ctx_s> c(new tsat_ctx_s());
     c->device = cuda_device;
     c->stream = (cudaStream_t)cuda_stream;
@@ -430,8 +509,24 @@ tsat_status tsat_create(tsat_ctx* out, int cuda_device, void* cuda_stream, const
     CK(cudaMallocHost(&c->h_steptab, sizeof(StepScalars) * kMaxStepsPerCall));
     CK(cudaMallocHost(&c->h_scal, sizeof(DevScalars)));
     tsat_config_default(&c->cfg);
+    if (nccl_unique_id) {           // candidate-sharded path (also with a 1-rank communicator)
+        std::string err;
+        if (comm_init(&c->comm, nccl_unique_id, rank, world, &err)) {
+            cudaStreamDestroy(c->cap_stream);
+            cudaFreeHost(c->h_steptab);
+            cudaFreeHost(c->h_scal);
+            return TSAT_E_NCCL;
+        }
+        c->sharded = true;
+    }
     *out = c.release();
     return TSAT_OK;
+}
+
+tsat_status tsat_nccl_unique_id(void* out, size_t bytes) {
+    if (!out || bytes < 128) return TSAT_E_ARG;
+    std::string err;
+    return comm_unique_id(out, &err) ? TSAT_E_NCCL : TSAT_OK;
 }
 
 tsat_status tsat_load_dimacs(tsat_ctx ctx, const char* text, size_t len, tsat_cnf_info* info) {
@@ -475,7 +570,7 @@ tsat_status tsat_workspace_bytes(tsat_ctx ctx, int64_t N_global, size_t* bytes) 
         return fail(ctx, TSAT_E_RANGE, "V * N / 32 >= 2^31 (32-bit bit-plane offsets)");
     if ((size_t)N * 12 > 200 * 1024) return fail(ctx, TSAT_E_RANGE, "N per GPU > 17066 not supported by the fused update");
     int KB = ctx->cnf.K <= 3 ? 4 : 8;
-    *bytes = make_layout(ctx->cnf.V, (int)N, KB, ctx->cnf.n_hubs).total;
+    *bytes = make_layout(ctx->cnf.V, (int)N, KB, ctx->cnf.n_hubs, ctx->sharded).total;
     return TSAT_OK;
 }
 
@@ -500,7 +595,7 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
     ctx->seed = seed;
     ctx->ws = (char*)ws;
     ctx->ws_bytes = bytes;
-    ctx->L = make_layout(ctx->cnf.V, ctx->N, ctx->KB, ctx->cnf.n_hubs);
+    ctx->L = make_layout(ctx->cnf.V, ctx->N, ctx->KB, ctx->cnf.n_hubs, ctx->sharded);
     MethodConsts& mc = ctx->mc;
     mc = MethodConsts{};
     for (int d = 0; d < 8; ++d) mc.E[d] = std::exp(-c.tau * (double)d);
@@ -525,6 +620,8 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
         ctx->upd_smem = g.upd_smem;
         ctx->num_sms = g.num_sms;
     }
+    if (ctx->sharded && ctx->upd_mode != 0)
+        return fail(ctx, TSAT_E_RANGE, "sharded path needs the fused k_update geometry (N per GPU too large)");
     StepArgs a = step_args(ctx);
     if (ctx->L.hubD != ctx->L.total)
         CK(cudaMemsetAsync(ctx->ws + ctx->L.hubD, 0, ctx->L.total - ctx->L.hubD, ctx->stream));
@@ -539,9 +636,8 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
     *ctx->h_scal = init;
     CK(cudaMemcpyAsync(a.ds, ctx->h_scal, sizeof(DevScalars), cudaMemcpyHostToDevice, ctx->stream));
     CK(launch_init(a.theta, a.m, a.v, a.V, a.N, ctx->n0, seed, ctx->stream));
-    CK(launch_rowstats(a.theta, a.V, a.N, mc, a.rowQ, a.rowD, a.rowRho, a.rowGuard, a.A0, &a.ds->thmax_bits[0],
-                       ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    s = state_stats(ctx, a, 0);
+    if (s != TSAT_OK) return s;
     ctx->have_batch = true;
     return TSAT_OK;
 }
@@ -618,7 +714,8 @@ tsat_status tsat_get_solution(tsat_ctx ctx, uint8_t* host_values, int64_t* idx, 
     if (d.sol_step < 0) return fail(ctx, TSAT_E_STATE, "no model found yet");
     if (idx) *idx = d.sol_idx;
     if (step) *step = d.sol_step;
-    if (host_values && ctx->cnf.V > 0) {
+    const bool owner = d.sol_idx >= ctx->n0 && d.sol_idx < ctx->n0 + ctx->N;
+    if (host_values && ctx->cnf.V > 0 && owner) {
         CK(cudaMemcpyAsync(host_values, ctx->ws + ctx->L.sol, (size_t)ctx->cnf.V, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
     }
@@ -658,10 +755,8 @@ tsat_status tsat_set_state(tsat_ctx ctx, const float* theta, const float* m, con
     *ctx->h_scal = init;
     CK(cudaMemcpyAsync(a.ds, ctx->h_scal, sizeof(DevScalars), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemsetAsync(a.hist, 0, (size_t)ctx->N * ctx->KB * 4, ctx->stream));
-    uint32_t* A = (t & 1) ? a.A1 : a.A0;
-    CK(launch_rowstats(a.theta, a.V, a.N, ctx->mc, a.rowQ, a.rowD, a.rowRho, a.rowGuard, A, &a.ds->thmax_bits[t & 1],
-                       ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    s = state_stats(ctx, a, t);
+    if (s != TSAT_OK) return s;
     ctx->t = t;
     ctx->steps_done = 0;
     return TSAT_OK;
@@ -795,6 +890,7 @@ void tsat_destroy(tsat_ctx ctx) {
     drop_graphs(ctx);
     for (auto e : ctx->events) cudaEventDestroy(e);
     free_cnf(ctx);
+    comm_destroy(ctx->comm);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     cudaFreeHost(ctx->h_steptab);
     cudaFreeHost(ctx->h_scal);

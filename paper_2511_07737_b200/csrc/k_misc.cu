@@ -82,11 +82,12 @@ __global__ void __launch_bounds__(256) k_rowstats(const float* __restrict__ thet
 template <int KB>
 __global__ void __launch_bounds__(256) k_gtable(int* __restrict__ hist, int N, long long C, MethodConsts mc,
                                                 float* __restrict__ gtab, double* __restrict__ S,
-                                                int* __restrict__ unsat, DevScalars* __restrict__ ds) {
+                                                int* __restrict__ unsat, DevScalars* __restrict__ ds, int sharded) {
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     unsigned long long key = ~0ull;
     double gm = 0.0;
+    long long lfx = 0;               // sharded loss: S_n 2^40, exact int64 sum across ranks
     if (n < N) {
         long long h[KB];
         long long acc = 0;
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(256) k_gtable(int* __restrict__ hist, int N, l
 #pragma unroll
         for (int r = 0; r < KB; ++r) gtab[(size_t)r * N + n] = g[r];
         S[n] = s;
+        lfx = __double2ll_rn(s * 1099511627776.0);
         unsat[n] = (int)h[0];
         key = ((unsigned long long)h[0] << 32) | (unsigned long long)(mc.n0 + n);
     }
@@ -141,9 +143,11 @@ __global__ void __launch_bounds__(256) k_gtable(int* __restrict__ hist, int N, l
         key = k2 < key ? k2 : key;
         gb = g2 > gb ? g2 : gb;
     }
+    if (sharded) lfx = warp_sum(lfx);
     if (lane == 0) {
         atomicMin(&ds->best_key, key);
         atomicMax(&ds->gmax_bits, gb);
+        if (sharded) atomicAdd(reinterpret_cast<unsigned long long*>(&ds->loss_fx), (unsigned long long)lfx);
     }
 }
 
@@ -352,8 +356,8 @@ cudaError_t launch_rowstats(const float* theta, int V, int N, const MethodConsts
 
 cudaError_t launch_gtable(const StepArgs& a, cudaStream_t st) {
     int blocks = (a.N + 255) / 256;
-    if (a.KB == 4) k_gtable<4><<<blocks, 256, 0, st>>>(a.hist, a.N, a.C, a.mc, a.gtab, a.S, a.unsat, a.ds);
-    else k_gtable<8><<<blocks, 256, 0, st>>>(a.hist, a.N, a.C, a.mc, a.gtab, a.S, a.unsat, a.ds);
+    if (a.KB == 4) k_gtable<4><<<blocks, 256, 0, st>>>(a.hist, a.N, a.C, a.mc, a.gtab, a.S, a.unsat, a.ds, a.sharded);
+    else k_gtable<8><<<blocks, 256, 0, st>>>(a.hist, a.N, a.C, a.mc, a.gtab, a.S, a.unsat, a.ds, a.sharded);
     return cudaGetLastError();
 }
 

@@ -86,7 +86,7 @@ __device__ __forceinline__ float fold_ints(const int* hubrow, int N, int n, int 
 template <int KB, bool HUB>
 __device__ __forceinline__ long long pass_fold(const float* __restrict__ trow, uint32_t* dpk, size_t dpkw,
                                                const float* gs, int* hubrow, int N, int GT, int tg, int dsum,
-                                               bool jvalid, int s) {
+                                               bool jvalid, int s, float* __restrict__ gout) {
     const float dsumf = (float)dsum;
     const bool j32 = jvalid && s >= 0 && s <= 100;                 // theta 2^s exact in fp32
     const float sc32 = j32 ? __uint_as_float((uint32_t)(127 + s) << 23) : 0.0f;
@@ -100,6 +100,7 @@ __device__ __forceinline__ long long pass_fold(const float* __restrict__ trow, u
 #pragma unroll
         for (int r = 0; r < KB; ++r) g4[r] = *reinterpret_cast<const float4*>(gs + (size_t)r * N + n);
         uint32_t* dp = dpk + n + (n >> 5);
+        float Gq[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             float gq[KB];
@@ -109,9 +110,11 @@ __device__ __forceinline__ long long pass_fold(const float* __restrict__ trow, u
             if (HUB) G = fold_ints<KB>(hubrow, N, n + q, dsum, gq);
             else G = fold_bytes<KB>(dp[q], KB == 8 ? dp[dpkw + q] : 0u, dsumf, gq);
             dp[q] = __float_as_uint(G);
+            Gq[q] = G;
             if (j32) I += __double2ll_rn((double)G * (double)(th[q] * sc32));
             else if (jvalid) I += __double2ll_rn(times_pow2((double)G * (double)th[q], s));
         }
+        if (gout) *reinterpret_cast<float4*>(gout + n) = make_float4(Gq[0], Gq[1], Gq[2], Gq[3]);
         if (HUB) {
 #pragma unroll
             for (int r = 0; r < KB - 1; ++r) *reinterpret_cast<int4*>(hubrow + (size_t)r * N + n) = make_int4(0, 0, 0, 0);
@@ -150,7 +153,9 @@ __device__ __forceinline__ void count_rec(uint32_t (&cnt)[NCTR][8], const uint32
     }
 }
 
-template <int KB>
+// MODE 0: fused W = 1 iteration.  MODE 1: phase A of the sharded iteration
+// (G -> Gbuf, int64 J partial -> Jbuf; the AdamW phase runs after the J exchange).
+template <int KB, int MODE>
 __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
                                                     uint32_t* __restrict__ Anext, const StepScalars* __restrict__ sc) {
     constexpr int NP = (KB == 4) ? 2 : 3;
@@ -199,8 +204,10 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
         if (tg == 0) {
             const uint32_t rowbytes = (uint32_t)N * 4u;
             prefetch_l2(a.theta + (size_t)v * N, rowbytes);
-            prefetch_l2(a.m + (size_t)v * N, rowbytes);
-            prefetch_l2(a.v + (size_t)v * N, rowbytes);
+            if (MODE == 0) {
+                prefetch_l2(a.m + (size_t)v * N, rowbytes);
+                prefetch_l2(a.v + (size_t)v * N, rowbytes);
+            }
         }
         const int hub = a.hub_of[v];
         const int2 pn = a.occ_pn[v];
@@ -283,11 +290,24 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
         group_bar(bar, GT);
 
         // ---- 3a: G (fp32 FMA chain over exact counts, R27) -> smem; J_v partial
-        long long I = hub >= 0 ? pass_fold<KB, true>(trow, dpk, dpkw, gs, hubrow, N, GT, tg, dsum, jvalid, s)
-                               : pass_fold<KB, false>(trow, dpk, dpkw, gs, hubrow, N, GT, tg, dsum, jvalid, s);
+        float* gout = MODE == 1 ? a.Gbuf + (size_t)v * N : nullptr;
+        long long I = hub >= 0 ? pass_fold<KB, true>(trow, dpk, dpkw, gs, hubrow, N, GT, tg, dsum, jvalid, s, gout)
+                               : pass_fold<KB, false>(trow, dpk, dpkw, gs, hubrow, N, GT, tg, dsum, jvalid, s, gout);
         I = warp_sum(I);
         if (lane == 0) red[gw] = I;
         group_bar(bar, GT);
+        if (MODE == 1) {                                     // sharded: J partial out, next row
+            if (tg == 0) {
+                long long tot = 0;
+                for (int i = 0; i < ngw; ++i) tot += red[i];
+                a.Jbuf[v] = tot;
+                rowslot[0] = vnext < a.V ? atomicAdd(&a.ds->row_counter, 1) : a.V;
+            }
+            group_bar(bar, GT);
+            v = vnext;
+            vnext = rowslot[0];
+            continue;
+        }
         if (tg == 0) {
             long long tot = 0;
             for (int i = 0; i < ngw; ++i) tot += red[i];
@@ -616,8 +636,13 @@ cudaError_t configure_update(StepArgs* a) {
     a->upd_NG = (int)ng;
     a->upd_smem = gsb + (size_t)ng * grb;
     a->upd_grid = sms;
-    if (KB == 4) e = cudaFuncSetAttribute(k_update<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a->upd_smem);
-    else e = cudaFuncSetAttribute(k_update<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a->upd_smem);
+    if (KB == 4) {
+        if ((e = cudaFuncSetAttribute(k_update<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a->upd_smem)) != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k_update<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a->upd_smem);
+    } else {
+        if ((e = cudaFuncSetAttribute(k_update<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a->upd_smem)) != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k_update<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a->upd_smem);
+    }
     return e;
 }
 
@@ -635,12 +660,22 @@ cudaError_t launch_update(const StepArgs& a, const uint32_t* Acur, uint32_t* Ane
     if (a.V == 0) return cudaGetLastError();
     if (a.upd_mode == 0) {
         const int threads = a.upd_GT * a.upd_NG;
-        if (a.KB == 4) k_update<4><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
-        else k_update<8><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
+        if (a.KB == 4) k_update<4, 0><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
+        else k_update<8, 0><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
     } else {
         if (a.KB == 4) k_update_rowcta<4><<<a.V, 256, a.upd_smem, st>>>(a, Acur, Anext, sc);
         else k_update_rowcta<8><<<a.V, 256, a.upd_smem, st>>>(a, Acur, Anext, sc);
     }
+    return cudaGetLastError();
+}
+
+// Phase A of the sharded iteration (always the persistent kernel: the
+// sharded path requires the fused geometry, see configure_update).
+cudaError_t launch_update_a(const StepArgs& a, const uint32_t* Acur, const StepScalars* sc, cudaStream_t st) {
+    if (a.V == 0) return cudaGetLastError();
+    const int threads = a.upd_GT * a.upd_NG;
+    if (a.KB == 4) k_update<4, 1><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, nullptr, sc);
+    else k_update<8, 1><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, nullptr, sc);
     return cudaGetLastError();
 }
 

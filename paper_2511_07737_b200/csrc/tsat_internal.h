@@ -82,6 +82,7 @@ struct DevScalars {
     int pad1;
     long long info_best_idx;
     double info_loss;
+    long long loss_fx;               // sharded: this rank's sum of S_n * 2^40 (exact int64)
 };
 
 // Method constants passed by value to kernels.
@@ -123,12 +124,20 @@ struct StepArgs {
     int upd_GT, upd_NG, upd_grid;    // v2 launch geometry
     int upd_rec_cap;                 // record words a group stages per row (max over non-hub rows)
     size_t upd_smem;
+    // candidate-sharded path (world > 1, or a 1-rank communicator)
+    int sharded;
+    float* Gbuf;                     // [V][N] fp32 G of the evaluated state
+    long long* Jbuf;                 // [V] int64 partial / global J (fixed point)
+    long long* Qbuf;                 // [V+1] int64 partial / global Q, slot V = loss (fixed point)
+    uint32_t *Pbuf, *Nbuf;           // [V][N/32] sign planes of the next state
+    unsigned long long* maxbuf;      // [3] (~best key, gmax bits, thmax bits)
     MethodConsts mc;
 };
 
 // Workspace layout (byte offsets), see capi.cu: make_layout().
 struct Layout {
-    size_t theta, m, v, A0, A1, hist, gtab, S, unsat, rowQ, rowD, rowRho, rowGuard, scal, steptab, sol, hubD, total;
+    size_t theta, m, v, A0, A1, hist, gtab, S, unsat, rowQ, rowD, rowRho, rowGuard, scal, steptab, sol, hubD;
+    size_t Gbuf, Jbuf, Qbuf, Pbuf, Nbuf, maxbuf, total;
 };
 
 // ---------------------------------------------------------------- launchers
@@ -142,6 +151,24 @@ constexpr int kKernelsPerStep = 5;
 cudaError_t launch_step_kernel(int which, const StepArgs& a, const StepScalars* sc_dev, long long t, cudaStream_t st);
 // Choose the k_update geometry for (N, KB) and set kernel attributes.
 cudaError_t configure_kernels(StepArgs* a);
+// sharded path (k_shard.cu); phases of one iteration between the collectives
+cudaError_t launch_shard_pack_max(const StepArgs& a, const StepScalars* sc, cudaStream_t st);
+cudaError_t launch_shard_unpack_max(const StepArgs& a, const StepScalars* sc, cudaStream_t st);
+cudaError_t launch_update_a(const StepArgs& a, const uint32_t* Acur, const StepScalars* sc, cudaStream_t st);
+cudaError_t launch_update_b(const StepArgs& a, const uint32_t* Acur, const StepScalars* sc, cudaStream_t st);
+cudaError_t launch_rows_partial(const StepArgs& a, const float* theta, unsigned int* thmax_bits, cudaStream_t st);
+cudaError_t launch_rows_finish(const StepArgs& a, uint32_t* Anext, cudaStream_t st);
+cudaError_t launch_step_end_sharded(const StepArgs& a, const StepScalars* sc, cudaStream_t st);
+// NCCL (comm.cpp); return 0 or 7 (TSAT_E_NCCL) with err
+int comm_unique_id(void* out128, std::string* err);
+int comm_init(void** comm, const void* uid128, int rank, int world, std::string* err);
+void comm_destroy(void* comm);
+int comm_allreduce_max_u64(void* comm, unsigned long long* buf, size_t n, cudaStream_t st, std::string* err);
+int comm_allreduce_sum_i64(void* comm, long long* buf, size_t n, cudaStream_t st, std::string* err);
+int comm_allgather_u64(void* comm, const unsigned long long* send, unsigned long long* recv, size_t n, cudaStream_t st,
+                       std::string* err);
+int comm_async_error(void* comm, std::string* err);
+
 cudaError_t launch_export(const StepArgs& a, long long t_eval, const int* cols_dev, int M, int k, double* absG,
                           unsigned long long* keys, int n64, int* out_v, double* out_g, cudaStream_t st, int phase);
 

@@ -33,9 +33,16 @@ def pack_bits(b):
     return (x << np.arange(32, dtype=np.uint64)).sum(axis=2).astype(np.uint32)
 
 
-def make_pair(cnf, N, seed, cfg=None, state=None, t0=0):
-    from paper_2511_07737_b200 import Solver, config_default
-    s = Solver(0)
+def make_solver(sharded=False):
+    from paper_2511_07737_b200 import Solver, nccl_unique_id
+    if sharded:                     # candidate-sharded kernels + NCCL on a 1-rank communicator
+        return Solver(0, rank=0, world=1, nccl_unique_id=nccl_unique_id())
+    return Solver(0)
+
+
+def make_pair(cnf, N, seed, cfg=None, state=None, t0=0, sharded=False):
+    from paper_2511_07737_b200 import config_default
+    s = make_solver(sharded)
     s.load_cnf(cnf)
     c = config_default()
     ocfg = cfg or O.Config()
@@ -333,3 +340,43 @@ def test_error_paths():
     with pytest.raises(TsatError) as e:
         s.step(0)
     assert e.value.name == "TSAT_E_ARG"
+
+
+# ---------------------------------------------------------------- sharded path (1-rank NCCL communicator)
+@pytest.mark.parametrize("case", ["c1", "industrial7", "ragged3"])
+def test_sharded_path_matches_oracle(case):
+    """The multi-GPU kernels (phase A -> SUM J -> phase B -> SUM Q -> rows
+    finish, plus the MAX exchange) on a 1-rank communicator reproduce the
+    oracle bit for bit."""
+    if case == "c1":
+        cnf, N = planted_ksat(20, 85, 3, 1), 64
+    elif case == "industrial7":
+        cnf, N = industrial_cnf(500, 2000, 4), 160
+    else:
+        cnf, N = planted_ksat(333, 1400, 3, 3), 96
+    s, o = make_pair(cnf, N, 5, sharded=True)
+    th, _, _, _ = s.get_state()
+    if not np.array_equal(th, o.theta):
+        s.set_state(o.theta, o.m, o.v, 0)
+    for _ in range(15):
+        compare_step(s, o, cnf, "sharded-" + case)
+    info = s.step(20)
+    for _ in range(20):
+        ref = o.step()
+    th, m, v, t = s.get_state()
+    np.testing.assert_array_equal(th, o.theta)
+    assert (info.best_unsat, info.best_idx) == (ref.best_unsat, ref.best_idx)
+    assert abs(info.loss - ref.loss) <= 1e-9 * abs(ref.loss)
+
+
+def test_sharded_equals_fused_c2():
+    """Sharded (W = 1 communicator) and fused single-GPU paths give identical
+    states on config c2 (both are the canonical arithmetic)."""
+    cnf, cfg = make_config("c2")
+    a = make_solver(False); a.load_cnf(cnf); a.init_batch(cfg["N"], 3)
+    b = make_solver(True); b.load_cnf(cnf); b.init_batch(cfg["N"], 3)
+    ia, ib = a.step(12), b.step(12)
+    for x, y in zip(a.get_state()[:3], b.get_state()[:3]):
+        np.testing.assert_array_equal(x, y)
+    np.testing.assert_array_equal(a.query_unsat(), b.query_unsat())
+    assert (ia.best_unsat, ia.best_idx) == (ib.best_unsat, ib.best_idx)
