@@ -155,9 +155,13 @@ __device__ __forceinline__ void count_rec(uint32_t (&cnt)[NCTR][8], const uint32
 
 // MODE 0: fused W = 1 iteration.  MODE 1: phase A of the sharded iteration
 // (G -> Gbuf, int64 J partial -> Jbuf; the AdamW phase runs after the J exchange).
+// Rows come from a global counter (dynamic: hub rows, ragged occurrence counts
+// and the tail stay balanced); tg 0 fetches the next row at the start of the
+// current one into a parity-double-buffered slot, read after the J barrier.
 template <int KB, int MODE>
 __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
-                                                    uint32_t* __restrict__ Anext, const StepScalars* __restrict__ sc) {
+                                                                    uint32_t* __restrict__ Anext,
+                                                                    const StepScalars* __restrict__ sc) {
     constexpr int NP = (KB == 4) ? 2 : 3;
     constexpr int NCTR = KB - 1;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -174,8 +178,7 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
     uint32_t* negw = posw + NW;
     long long* red = reinterpret_cast<long long*>(gb + grb - 128);                      // 4 + 4 slots
     float* redf = reinterpret_cast<float*>(red + 8);                                    // 4 slots
-    double* bcast = reinterpret_cast<double*>(redf + 4);                                // 2 slots
-    int* rowslot = reinterpret_cast<int*>(bcast + 2);                                   // 2 slots
+    int* rowslot = reinterpret_cast<int*>(redf + 4);                                    // 2 slots
     const int bar = 1 + grp;
     const int lane = threadIdx.x & 31, gw = tg >> 5, ngw = GT >> 5;
     const bool uni3 = a.uniform_len && a.mc.K == 3 && KB == 4;
@@ -183,10 +186,7 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
     // fp32 derivative table of the whole batch -> shared memory
     for (int i = threadIdx.x * 4; i < KB * N; i += blockDim.x * 4)
         *reinterpret_cast<float4*>(gs + i) = *reinterpret_cast<const float4*>(a.gtab + i);
-    if (tg == 0) {
-        rowslot[0] = atomicAdd(&a.ds->row_counter, 1);
-        rowslot[1] = atomicAdd(&a.ds->row_counter, 1);
-    }
+    if (tg == 0) rowslot[1] = atomicAdd(&a.ds->row_counter, 1);
     __syncthreads();
 
     const long long t = sc->t;
@@ -195,13 +195,12 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
     const float wdf = sc->wdf, a1 = sc->a1, b2f = sc->b2f, a2 = sc->a2, nss = sc->nss, rbc2 = sc->rbc2,
                 epsf = sc->epsf, nz = sc->nz;
     const MethodConsts& mc = a.mc;
-    int v = rowslot[0], vnext = rowslot[1];
 
-    while (v < a.V) {
-        // ---- prefetch this row's streams into L2 while it gathers (a short
-        // reuse distance: the streaming writes of other rows would evict a
-        // longer-range prefetch)
+    int v = rowslot[1];
+    for (int it = 0; v < a.V; ++it) {
+        // ---- fetch the next row; prefetch this row's streams into L2
         if (tg == 0) {
+            rowslot[it & 1] = atomicAdd(&a.ds->row_counter, 1);
             const uint32_t rowbytes = (uint32_t)N * 4u;
             prefetch_l2(a.theta + (size_t)v * N, rowbytes);
             if (MODE == 0) {
@@ -296,32 +295,21 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
         I = warp_sum(I);
         if (lane == 0) red[gw] = I;
         group_bar(bar, GT);
+        long long Itot = 0;                                  // every thread folds the warp partials
+        for (int i = 0; i < ngw; ++i) Itot += red[i];
+        const int vnext = rowslot[it & 1];
         if (MODE == 1) {                                     // sharded: J partial out, next row
-            if (tg == 0) {
-                long long tot = 0;
-                for (int i = 0; i < ngw; ++i) tot += red[i];
-                a.Jbuf[v] = tot;
-                rowslot[0] = vnext < a.V ? atomicAdd(&a.ds->row_counter, 1) : a.V;
-            }
-            group_bar(bar, GT);
+            if (tg == 0) a.Jbuf[v] = Itot;
             v = vnext;
-            vnext = rowslot[0];
             continue;
         }
-        if (tg == 0) {
-            long long tot = 0;
-            for (int i = 0; i < ngw; ++i) tot += red[i];
-            double J = jvalid ? times_pow2((double)tot, -s) : 0.0;
-            double c = 0.0;
-            if (mc.normalize && !guard) {
-                c = J / (double)mc.Nglobal;
-                c = c * rho;
-                c = c * rho;
-            }
-            bcast[0] = c;
+        double c = 0.0;
+        if (mc.normalize && !guard) {
+            const double J = jvalid ? times_pow2((double)Itot, -s) : 0.0;
+            c = J / (double)mc.Nglobal;
+            c = c * rho;
+            c = c * rho;
         }
-        group_bar(bar, GT);
-        const double c = bcast[0];
 
         // ---- 3b: grad, AdamW, next-state statistics and sign planes
         long long Qn = 0;
@@ -387,15 +375,19 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
         mx = warp_maxf(mx);
         if (lane == 0) { red[4 + gw] = Qn; redf[gw] = mx; }
         group_bar(bar, GT);
+        long long Qtot = 0;
+        for (int i = 0; i < ngw; ++i) Qtot += red[4 + i];
+        // sign(d_{t+1}) = sign(mu) with sign(0) = +1, i.e. Q >= 0 (R3): the bits
+        // of the next state need no division; tg 0 finishes Eq. 5's statistics.
+        const bool dpos = !mc.normalize || Qtot >= 0;
+        for (int w = tg; w < NW; w += GT) Anext[(size_t)v * NW + w] = dpos ? posw[w] : negw[w];
         if (tg == 0) {
-            long long tot = 0;
             float m2 = 0.0f;
-            for (int i = 0; i < ngw; ++i) { tot += red[4 + i]; m2 = fmaxf(m2, redf[i]); }
+            for (int i = 0; i < ngw; ++i) m2 = fmaxf(m2, redf[i]);
             double dn, rhon;
             unsigned char gn;
-            row_finish(tot, mc, &dn, &rhon, &gn);
-            a.rowQ[v] = tot; a.rowD[v] = dn; a.rowRho[v] = rhon; a.rowGuard[v] = gn;
-            bcast[1] = dn;
+            row_finish(Qtot, mc, &dn, &rhon, &gn);
+            a.rowQ[v] = Qtot; a.rowD[v] = dn; a.rowRho[v] = rhon; a.rowGuard[v] = gn;
             atomicMax(&a.ds->thmax_bits[(t + 1) & 1], __float_as_uint(m2));
             const unsigned long long bk = a.ds->best_key;
             if ((bk >> 32) == 0ull && a.ds->sol_step < 0) {          // first model: keep its bits (A22)
@@ -403,14 +395,9 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
                 if (idx >= 0 && idx < N)
                     a.sol[v] = (unsigned char)((Acur[(size_t)v * NW + (idx >> 5)] >> (idx & 31)) & 1u);
             }
-            rowslot[0] = vnext < a.V ? atomicAdd(&a.ds->row_counter, 1) : a.V;
         }
-        group_bar(bar, GT);
-        const bool dpos = bcast[1] > 0.0;
-        for (int w = tg; w < NW; w += GT) Anext[(size_t)v * NW + w] = dpos ? posw[w] : negw[w];
         v = vnext;
-        vnext = rowslot[0];
-        // (the next row's first group_bar orders these smem reads before reuse)
+        // (the next row's barriers order these smem reads before any reuse)
     }
 }
 
