@@ -68,6 +68,26 @@ __device__ __forceinline__ float fold_bytes(uint32_t p0, uint32_t p1, float dsum
     return G;
 }
 
+// a * b per lane, correctly rounded, never contracted with a following add:
+// ptxas fuses FMUL2 + FADD2 into FFMA2 even with --fmad=false (and folds an
+// FFMA2 with a -0 addend the same way; scripts/micro/fuse_check.cu), so
+// products that feed an add are two scalar __fmul_rn (which ptxas respects).
+__device__ __forceinline__ float2 mul2_unfused(float2 a, float2 b) {
+    return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y));
+}
+
+// Per-bin counts of one candidate as exact floats (bytes + derived last bin).
+template <int KB>
+__device__ __forceinline__ void fold_counts(float (&d)[KB], uint32_t p0, uint32_t p1, float dsumf) {
+    const uint32_t u0 = p0 ^ 0x80808080u, u1 = p1 ^ 0x80808080u;
+#pragma unroll
+    for (int r = 0; r < KB - 1; ++r) d[r] = sbyte_to_float(r < 4 ? u0 : u1, r & 3);
+    float acc = 0.0f;
+#pragma unroll
+    for (int r = 0; r < KB - 1; ++r) acc = acc + d[r];     // exact: small integers
+    d[KB - 1] = dsumf - acc;
+}
+
 template <int KB>
 __device__ __forceinline__ float fold_ints(const int* hubrow, int N, int n, int dsum, const float (&gq)[KB]) {
     float d[KB];
@@ -101,16 +121,35 @@ __device__ __forceinline__ long long pass_fold(const float* __restrict__ trow, u
         for (int r = 0; r < KB; ++r) g4[r] = *reinterpret_cast<const float4*>(gs + (size_t)r * N + n);
         uint32_t* dp = dpk + n + (n >> 5);
         float Gq[4];
+        if (HUB) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                float gq[KB];
+#pragma unroll
+                for (int r = 0; r < KB; ++r) gq[r] = q == 0 ? g4[r].x : q == 1 ? g4[r].y : q == 2 ? g4[r].z : g4[r].w;
+                Gq[q] = fold_ints<KB>(hubrow, N, n + q, dsum, gq);
+            }
+        } else {
+            // candidate pairs: d_r as floats (exact small integers), then the
+            // r-ascending FMA chain with packed fp32x2 FMAs (per-lane exact FMA)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float dA[KB], dB[KB];
+                fold_counts<KB>(dA, dp[2 * h], KB == 8 ? dp[dpkw + 2 * h] : 0u, dsumf);
+                fold_counts<KB>(dB, dp[2 * h + 1], KB == 8 ? dp[dpkw + 2 * h + 1] : 0u, dsumf);
+                float2 G2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+                for (int r = 0; r < KB; ++r)
+                    G2 = __ffma2_rn(make_float2(dA[r], dB[r]),
+                                    h == 0 ? make_float2(g4[r].x, g4[r].y) : make_float2(g4[r].z, g4[r].w), G2);
+                Gq[2 * h] = G2.x;
+                Gq[2 * h + 1] = G2.y;
+            }
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            float gq[KB];
-#pragma unroll
-            for (int r = 0; r < KB; ++r) gq[r] = q == 0 ? g4[r].x : q == 1 ? g4[r].y : q == 2 ? g4[r].z : g4[r].w;
-            float G;
-            if (HUB) G = fold_ints<KB>(hubrow, N, n + q, dsum, gq);
-            else G = fold_bytes<KB>(dp[q], KB == 8 ? dp[dpkw + q] : 0u, dsumf, gq);
+            const float G = Gq[q];
             dp[q] = __float_as_uint(G);
-            Gq[q] = G;
             if (j32) I += __double2ll_rn((double)G * (double)(th[q] * sc32));
             else if (jvalid) I += __double2ll_rn(times_pow2((double)G * (double)th[q], s));
         }
@@ -335,28 +374,48 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
                 float mm[4] = {m4.x, m4.y, m4.z, m4.w};
                 float vv[4] = {v4.x, v4.y, v4.z, v4.w};
                 const uint32_t* dp = dpk + n + (n >> 5);
+                float gg[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float G32 = __uint_as_float(dp[q]);
-                    const float g = (float)((double)G32 * rho - c);
-                    float x = th[q] * wdf;
-                    const float mn = __fmaf_rn(a1, g - mm[q], mm[q]);
-                    const float vb = vv[q] * b2f;
-                    const float vn = __fmaf_rn(a2 * g, g, vb);
-                    const float den = __fmul_rn(__fsqrt_rn(vn), rbc2) + epsf;
-                    x = x + (nss * mn) / den;
+                for (int q = 0; q < 4; ++q) gg[q] = (float)((double)__uint_as_float(dp[q]) * rho - c);
+                // AdamW on candidate pairs: packed fp32x2 ops are per-lane
+                // correctly rounded, i.e. the same canonical ops (R6-R6c)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const float2 g2 = make_float2(gg[2 * h], gg[2 * h + 1]);
+                    const float2 m2 = make_float2(mm[2 * h], mm[2 * h + 1]);
+                    const float2 v2 = make_float2(vv[2 * h], vv[2 * h + 1]);
+                    float2 x2 = mul2_unfused(make_float2(th[2 * h], th[2 * h + 1]), make_float2(wdf, wdf));
+                    const float2 mn2 = __ffma2_rn(make_float2(a1, a1), __fadd2_rn(g2, make_float2(-m2.x, -m2.y)), m2);
+                    const float2 vb2 = __fmul2_rn(v2, make_float2(b2f, b2f));
+                    const float2 vn2 = __ffma2_rn(__fmul2_rn(make_float2(a2, a2), g2), g2, vb2);
+                    const float2 sq2 = make_float2(__fsqrt_rn(vn2.x), __fsqrt_rn(vn2.y));
+                    const float2 den2 = __fadd2_rn(mul2_unfused(sq2, make_float2(rbc2, rbc2)), make_float2(epsf, epsf));
+                    const float2 num2 = __fmul2_rn(make_float2(nss, nss), mn2);
+                    x2 = __fadd2_rn(x2, make_float2(num2.x / den2.x, num2.y / den2.y));
+                    float xs[2] = {x2.x, x2.y};
                     if (mc.noise) {
-                        const long long ng = mc.n0 + n + q;
-                        uint32_t xr[4] = {(uint32_t)(ng >> 2), (uint32_t)v, (uint32_t)(1 + t), 0u};
-                        philox4x32_10(xr, (uint32_t)mc.seed, (uint32_t)(mc.seed >> 32));
-                        const float xi = (float)(xr[ng & 3] >> 8) * 5.9604644775390625e-08f - 0.5f;
-                        x = x + nz * xi;
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const long long ng = mc.n0 + n + 2 * h + e;
+                            uint32_t xr[4] = {(uint32_t)(ng >> 2), (uint32_t)v, (uint32_t)(1 + t), 0u};
+                            philox4x32_10(xr, (uint32_t)mc.seed, (uint32_t)(mc.seed >> 32));
+                            const float xi = (float)(xr[ng & 3] >> 8) * 5.9604644775390625e-08f - 0.5f;
+                            xs[e] = xs[e] + nz * xi;
+                        }
                     }
-                    th[q] = x; mm[q] = mn; vv[q] = vn;
-                    Qn += __float2ll_rn(x * 4294967296.0f);          // x 2^32 is exact in fp32
-                    mx = fmaxf(mx, fabsf(x));
-                    pnib |= (x > 0.0f ? 1u : 0u) << q;
-                    nnib |= (x < 0.0f ? 1u : 0u) << q;
+                    const float2 q2 = __fmul2_rn(make_float2(xs[0], xs[1]), make_float2(4294967296.0f, 4294967296.0f));
+                    Qn += __float2ll_rn(q2.x) + __float2ll_rn(q2.y);      // x 2^32 is exact in fp32
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int q = 2 * h + e;
+                        const float x = xs[e];
+                        th[q] = x;
+                        mm[q] = e ? mn2.y : mn2.x;
+                        vv[q] = e ? vn2.y : vn2.x;
+                        mx = fmaxf(mx, fabsf(x));
+                        pnib |= (x > 0.0f ? 1u : 0u) << q;
+                        nnib |= (x < 0.0f ? 1u : 0u) << q;
+                    }
                 }
                 *reinterpret_cast<float4*>(trow + n) = make_float4(th[0], th[1], th[2], th[3]);
                 *reinterpret_cast<float4*>(mrow + n) = make_float4(mm[0], mm[1], mm[2], mm[3]);
