@@ -113,6 +113,54 @@ __device__ __forceinline__ void vc_dec(uint32_t (&c)[B], uint32_t m) {
     }
 }
 
+// 4 one-bit masks -> their 3-bit bit-sliced sum (s0 + 2 s1 + 4 s2), carry-save.
+__device__ __forceinline__ void sum4(uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3, uint32_t& s0, uint32_t& s1,
+                                     uint32_t& s2) {
+    const uint32_t sa = m0 ^ m1 ^ m2;
+    const uint32_t ca = (m0 & m1) | (m2 & (m0 ^ m1));
+    s0 = sa ^ m3;
+    const uint32_t cb = sa & m3;
+    s1 = ca ^ cb;
+    s2 = ca & cb;
+}
+
+// Signed B-plane counters (two's complement): c += S / c -= S for a bit-sliced
+// 3-bit S (ripple of full adders; subtraction adds ~S with carry-in 1).
+template <int B>
+__device__ __forceinline__ void vc_add3(uint32_t (&c)[B], uint32_t s0, uint32_t s1, uint32_t s2) {
+    uint32_t carry = c[0] & s0;
+    c[0] ^= s0;
+    uint32_t x = c[1];
+    c[1] = x ^ s1 ^ carry;
+    carry = (x & s1) | (carry & (x ^ s1));
+    x = c[2];
+    c[2] = x ^ s2 ^ carry;
+    carry = (x & s2) | (carry & (x ^ s2));
+#pragma unroll
+    for (int b = 3; b < B; ++b) {
+        const uint32_t t = c[b] & carry;
+        c[b] ^= carry;
+        carry = t;
+    }
+}
+template <int B>
+__device__ __forceinline__ void vc_sub3(uint32_t (&c)[B], uint32_t s0, uint32_t s1, uint32_t s2) {
+    uint32_t carry = 0xffffffffu;
+    const uint32_t ns[3] = {~s0, ~s1, ~s2};
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+        const uint32_t x = c[b];
+        c[b] = x ^ ns[b] ^ carry;
+        carry = (x & ns[b]) | (carry & (x ^ ns[b]));
+    }
+#pragma unroll
+    for (int b = 3; b < B; ++b) {           // operand bits are all 1 here
+        const uint32_t x = c[b];
+        c[b] = ~(x ^ carry);
+        carry = x | carry;
+    }
+}
+
 // Bit-sliced addition of a 0/1 mask into an NP-plane unsigned count.
 template <int NP>
 __device__ __forceinline__ void bs_add(uint32_t (&s)[NP], uint32_t x) {
@@ -131,6 +179,106 @@ __device__ __forceinline__ uint32_t bs_eq(const uint32_t (&s)[NP], int r) {
 #pragma unroll
     for (int p = 0; p < NP; ++p) m &= ((r >> p) & 1) ? s[p] : ~s[p];
     return m;
+}
+
+// One record's literal values for one 32-candidate word: own literal plus the
+// clause's other literals (codes), as NP count planes.
+template <int NP, typename RecFn>
+__device__ __forceinline__ void rec_planes(uint32_t (&sp)[NP], RecFn rec, unsigned p, uint32_t hdr, uint32_t own,
+                                           const uint32_t* __restrict__ Acur, unsigned NW, unsigned w) {
+    const uint32_t len = hdr >> 1;
+    sp[0] = own ^ (0u - (hdr & 1u));
+#pragma unroll
+    for (int q = 1; q < NP; ++q) sp[q] = 0u;
+    for (uint32_t i = 1; i < len; ++i) {
+        const uint32_t code = rec(p + i);
+        bs_add<NP>(sp, __ldg(Acur + ((code >> 1) * NW + w)) ^ (0u - (code & 1u)));
+    }
+}
+
+// Signed per-bin counts d_r = cneg[r] - cpos[r], r < NCTR, of one variable's
+// occurrence records [0, nrec) for one 32-candidate word w, as B-plane
+// two's-complement counters.  Records are sign-sorted (negated first, host
+// side), so runs of 4 same-sign records are summed by carry-save adders and
+// added (negated) or subtracted (positive) once.  UNI3: every record has 3
+// words (uniform 3-SAT), so a group's 8 gathers are issued together.  GROUP
+// false: one record at a time (smaller code, for I-cache-bound callers).
+template <int NP, int NCTR, int B, bool UNI3, bool GROUP, typename RecFn>
+__device__ __forceinline__ void count_occurrences(uint32_t (&cnt)[NCTR][B], RecFn rec, unsigned nrec, uint32_t own,
+                                                  const uint32_t* __restrict__ Acur, unsigned NW, unsigned w) {
+#pragma unroll
+    for (int r = 0; r < NCTR; ++r)
+#pragma unroll
+        for (int b = 0; b < B; ++b) cnt[r][b] = 0u;
+    auto ld = [&](uint32_t code) { return __ldg(Acur + ((code >> 1) * NW + w)) ^ (0u - (code & 1u)); };
+    unsigned p = 0;
+    while (p < nrec) {
+        const uint32_t h0 = rec(p);
+        unsigned p4 = 0;
+        bool grp = false;
+        uint32_t h[4];
+        unsigned pp[4];
+        h[0] = h0;
+        pp[0] = p;
+        if (!GROUP) {
+        } else if (UNI3) {
+            if (p + 12 <= nrec) {
+                h[1] = rec(p + 3); h[2] = rec(p + 6); h[3] = rec(p + 9);
+                pp[1] = p + 3; pp[2] = p + 6; pp[3] = p + 9;
+                p4 = p + 12;
+                grp = ((h0 ^ h[3]) & 1u) == 0u;          // signs are monotone in the row
+            }
+        } else {
+            unsigned q = p + (h0 >> 1);
+            grp = true;
+#pragma unroll
+            for (int k = 1; k < 4; ++k) {
+                if (q >= nrec) { grp = false; break; }
+                h[k] = rec(q);
+                pp[k] = q;
+                q += h[k] >> 1;
+            }
+            if (grp) { p4 = q; grp = ((h0 ^ h[3]) & 1u) == 0u; }
+        }
+        if (grp) {
+            uint32_t sp[4][NP];
+            if (UNI3) {
+                uint32_t x[4][2];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) { x[k][0] = ld(rec(pp[k] + 1)); x[k][1] = ld(rec(pp[k] + 2)); }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    sp[k][0] = own ^ (0u - (h[k] & 1u));
+#pragma unroll
+                    for (int q = 1; q < NP; ++q) sp[k][q] = 0u;
+                    bs_add<NP>(sp[k], x[k][0]);
+                    bs_add<NP>(sp[k], x[k][1]);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) rec_planes<NP>(sp[k], rec, pp[k], h[k], own, Acur, NW, w);
+            }
+#pragma unroll
+            for (int r = 0; r < NCTR; ++r) {
+                uint32_t s0, s1, s2;
+                sum4(bs_eq<NP>(sp[0], r), bs_eq<NP>(sp[1], r), bs_eq<NP>(sp[2], r), bs_eq<NP>(sp[3], r), s0, s1, s2);
+                if (h0 & 1u) vc_add3<B>(cnt[r], s0, s1, s2);
+                else vc_sub3<B>(cnt[r], s0, s1, s2);
+            }
+            p = p4;
+        } else {
+            uint32_t sp[NP];
+            rec_planes<NP>(sp, rec, p, h0, own, Acur, NW, w);
+            if (h0 & 1u) {
+#pragma unroll
+                for (int r = 0; r < NCTR; ++r) vc_inc<B>(cnt[r], bs_eq<NP>(sp, r));
+            } else {
+#pragma unroll
+                for (int r = 0; r < NCTR; ++r) vc_dec<B>(cnt[r], bs_eq<NP>(sp, r));
+            }
+            p += h0 >> 1;
+        }
+    }
 }
 
 }  // namespace tsat

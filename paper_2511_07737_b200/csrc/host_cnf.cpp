@@ -197,18 +197,29 @@ int build_cnf(int32_t V, int64_t C, const int64_t* ptr, const int32_t* lits, Hos
     }
     h.occ_ptr[V] = (uint32_t)acc;
     h.occ_rec.assign(acc, 0);
-    std::vector<uint32_t> fill(h.occ_ptr.begin(), h.occ_ptr.end() - 1);
+    // records of negated occurrences first, then positive ones, each in clause
+    // order: the kernels sum runs of same-sign occurrences with carry-save
+    // adders (the counts do not depend on the order, R12)
+    std::vector<uint64_t> negw((size_t)V, 0);
+    for (int64_t c = 0; c < C; ++c) {
+        uint32_t len = h.clause_ptr[c + 1] - h.clause_ptr[c];
+        for (uint32_t i = h.clause_ptr[c]; i < h.clause_ptr[c + 1]; ++i)
+            if (h.clause_lit[i] & 1u) negw[h.clause_lit[i] >> 1] += len;
+    }
+    std::vector<uint32_t> fill_neg(h.occ_ptr.begin(), h.occ_ptr.end() - 1), fill_pos((size_t)V);
+    for (int32_t v = 0; v < V; ++v) fill_pos[v] = h.occ_ptr[v] + (uint32_t)negw[v];
     for (int64_t c = 0; c < C; ++c) {
         uint32_t b = h.clause_ptr[c], e = h.clause_ptr[c + 1], len = e - b;
         for (uint32_t i = b; i < e; ++i) {
             uint32_t code = h.clause_lit[i];
             uint32_t v = code >> 1;
-            uint32_t* r = &h.occ_rec[fill[v]];
+            uint32_t& f = (code & 1u) ? fill_neg[v] : fill_pos[v];
+            uint32_t* r = &h.occ_rec[f];
             r[0] = (len << 1) | (code & 1u);
             uint32_t o = 1;
             for (uint32_t j = b; j < e; ++j)
                 if (j != i) r[o++] = h.clause_lit[j];
-            fill[v] += len;
+            f += len;
         }
     }
     // signed-count classes and hub super-chunks (see tsat_internal.h)

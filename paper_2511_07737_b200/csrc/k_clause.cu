@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t*
         if (valid) {
 #pragma unroll
             for (int r = 0; r < KB - 1; ++r)
+#pragma unroll 2
                 for (int j0 = 0; j0 < 32; ++j0) {
                     int j = (j0 + lane) & 31;            // rotate: conflict-free smem banks
                     int val = 0;

@@ -167,29 +167,20 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// Gather one occurrence record (own literal + others) into NP count planes.
-template <int NP>
-__device__ __forceinline__ void gather_rec(uint32_t (&sp)[NP], const uint32_t* rec, uint32_t hdr, uint32_t own,
-                                           const uint32_t* __restrict__ Acur, int NW, int w) {
-    const uint32_t len = hdr >> 1;
-    sp[0] = own ^ (0u - (hdr & 1u));
-#pragma unroll
-    for (int q = 1; q < NP; ++q) sp[q] = 0u;
-    for (uint32_t i = 1; i < len; ++i) {
-        const uint32_t code = rec[i];
-        bs_add<NP>(sp, __ldg(Acur + ((code >> 1) * (unsigned)NW + (unsigned)w)) ^ (0u - (code & 1u)));
-    }
+// Optional update noise (R17): xi = (x >> 8) 2^-24 - 1/2 with
+// x = Philox(key = seed, ctr = (n>>2, v, 1+t, 0))[n & 3].  Out of line: it is
+// off by default and would otherwise bloat the hot loop's instruction footprint.
+__device__ __noinline__ float noise_xi(unsigned long long seed, long long ng, int v, long long t) {
+    uint32_t xr[4] = {(uint32_t)(ng >> 2), (uint32_t)v, (uint32_t)(1 + t), 0u};
+    philox4x32_10(xr, (uint32_t)seed, (uint32_t)(seed >> 32));
+    return (float)(xr[ng & 3] >> 8) * 5.9604644775390625e-08f - 0.5f;
 }
 
-template <int NCTR, int NP>
-__device__ __forceinline__ void count_rec(uint32_t (&cnt)[NCTR][8], const uint32_t (&sp)[NP], bool neg) {
-    if (neg) {
-#pragma unroll
-        for (int r = 0; r < NCTR; ++r) vc_inc<8>(cnt[r], bs_eq<NP>(sp, r));
-    } else {
-#pragma unroll
-        for (int r = 0; r < NCTR; ++r) vc_dec<8>(cnt[r], bs_eq<NP>(sp, r));
-    }
+// Barrier over one warp group: a warp-sized group only needs __syncwarp, so
+// more than 15 groups (the named-barrier limit) can share a CTA.
+__device__ __forceinline__ void gsync(int bar, int GT) {
+    if (GT == 32) __syncwarp();
+    else group_bar(bar, GT);
 }
 
 // MODE 0: fused W = 1 iteration.  MODE 1: phase A of the sharded iteration
@@ -271,45 +262,15 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
         if (hub < 0) {
             const unsigned nrec = re - rb;
             for (unsigned i = tg; i < nrec; i += GT) rec[i] = a.occ_rec[rb + i];
-            group_bar(bar, GT);
+            gsync(bar, GT);
             for (int w = tg; w < NW; w += GT) {
                 const uint32_t own = __ldg(Acur + (size_t)v * NW + w);
                 uint32_t cnt[NCTR][kCtr];
-#pragma unroll
-                for (int r = 0; r < NCTR; ++r)
-#pragma unroll
-                    for (int b = 0; b < kCtr; ++b) cnt[r][b] = 0u;
-                unsigned p = 0;
-                if (uni3 && nrec >= 6) {
-                    // uniform 3-SAT: two records (4 independent gathers) per
-                    // iteration, the next pair's gathers issued before counting
-                    auto ld = [&](uint32_t c) {
-                        return __ldg(Acur + ((c >> 1) * (unsigned)NW + (unsigned)w)) ^ (0u - (c & 1u));
-                    };
-                    uint32_t y01 = ld(rec[1]), y02 = ld(rec[2]), y11 = ld(rec[4]), y12 = ld(rec[5]);
-                    for (; p + 6 <= nrec; p += 6) {
-                        const uint32_t h0 = rec[p], h1 = rec[p + 3];
-                        const uint32_t x01 = y01, x02 = y02, x11 = y11, x12 = y12;
-                        if (p + 12 <= nrec) {
-                            y01 = ld(rec[p + 7]); y02 = ld(rec[p + 8]);
-                            y11 = ld(rec[p + 10]); y12 = ld(rec[p + 11]);
-                        }
-                        uint32_t s0[NP], s1[NP];
-                        s0[0] = own ^ (0u - (h0 & 1u)); s0[1] = 0u;
-                        s1[0] = own ^ (0u - (h1 & 1u)); s1[1] = 0u;
-                        bs_add<NP>(s0, x01); bs_add<NP>(s0, x02);
-                        bs_add<NP>(s1, x11); bs_add<NP>(s1, x12);
-                        count_rec<NCTR, NP>(cnt, s0, h0 & 1u);
-                        count_rec<NCTR, NP>(cnt, s1, h1 & 1u);
-                    }
-                }
-                while (p < nrec) {
-                    const uint32_t hdr = rec[p];
-                    uint32_t sp[NP];
-                    gather_rec<NP>(sp, rec + p, hdr, own, Acur, NW, w);
-                    count_rec<NCTR, NP>(cnt, sp, hdr & 1u);
-                    p += hdr >> 1;
-                }
+                auto recf = [&](unsigned i) { return rec[i]; };
+                // KB = 8 rows are short (hub rows go to k_hub) and the kernel is
+                // I-cache bound there: count one record at a time
+                if (uni3) count_occurrences<NP, NCTR, kCtr, true, true>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w);
+                else count_occurrences<NP, NCTR, kCtr, false, KB == 4>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w);
                 uint32_t T[32];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) T[i] = (i / kCtr < NCTR && i / kCtr < 4) ? cnt[i / kCtr][i % kCtr] : 0u;
@@ -325,7 +286,7 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
                 }
             }
         }
-        group_bar(bar, GT);
+        gsync(bar, GT);
 
         // ---- 3a: G (fp32 FMA chain over exact counts, R27) -> smem; J_v partial
         float* gout = MODE == 1 ? a.Gbuf + (size_t)v * N : nullptr;
@@ -333,7 +294,7 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
                                : pass_fold<KB, false>(trow, dpk, dpkw, gs, hubrow, N, GT, tg, dsum, jvalid, s, gout);
         I = warp_sum(I);
         if (lane == 0) red[gw] = I;
-        group_bar(bar, GT);
+        gsync(bar, GT);
         long long Itot = 0;                                  // every thread folds the warp partials
         for (int i = 0; i < ngw; ++i) Itot += red[i];
         const int vnext = rowslot[it & 1];
@@ -394,14 +355,8 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
                     x2 = __fadd2_rn(x2, make_float2(num2.x / den2.x, num2.y / den2.y));
                     float xs[2] = {x2.x, x2.y};
                     if (mc.noise) {
-#pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const long long ng = mc.n0 + n + 2 * h + e;
-                            uint32_t xr[4] = {(uint32_t)(ng >> 2), (uint32_t)v, (uint32_t)(1 + t), 0u};
-                            philox4x32_10(xr, (uint32_t)mc.seed, (uint32_t)(mc.seed >> 32));
-                            const float xi = (float)(xr[ng & 3] >> 8) * 5.9604644775390625e-08f - 0.5f;
-                            xs[e] = xs[e] + nz * xi;
-                        }
+#pragma unroll 1
+                        for (int e = 0; e < 2; ++e) xs[e] = xs[e] + nz * noise_xi(mc.seed, mc.n0 + n + 2 * h + e, v, t);
                     }
                     const float2 q2 = __fmul2_rn(make_float2(xs[0], xs[1]), make_float2(4294967296.0f, 4294967296.0f));
                     Qn += __float2ll_rn(q2.x) + __float2ll_rn(q2.y);      // x 2^32 is exact in fp32
@@ -433,7 +388,7 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
         Qn = warp_sum(Qn);
         mx = warp_maxf(mx);
         if (lane == 0) { red[4 + gw] = Qn; redf[gw] = mx; }
-        group_bar(bar, GT);
+        gsync(bar, GT);
         long long Qtot = 0;
         for (int i = 0; i < ngw; ++i) Qtot += red[4 + i];
         // sign(d_{t+1}) = sign(mu) with sign(0) = +1, i.e. Q >= 0 (R3): the bits
@@ -477,31 +432,10 @@ __global__ void __launch_bounds__(32) k_hub(StepArgs a, const uint32_t* __restri
     const int v = sc.y;
     const uint32_t own = valid ? __ldg(Acur + (size_t)v * NW + w) : 0u;
     uint32_t cnt[NCTR][kHubCtr];
-#pragma unroll
-    for (int r = 0; r < NCTR; ++r)
-#pragma unroll
-        for (int b = 0; b < kHubCtr; ++b) cnt[r][b] = 0u;
-    const size_t wofs = valid ? (size_t)w : 0;
-    for (unsigned p = (unsigned)sc.z; p < (unsigned)sc.w;) {
-        const uint32_t hdr = __ldg(a.occ_rec + p);
-        const uint32_t len = hdr >> 1;
-        uint32_t sp[NP];
-        sp[0] = own ^ (0u - (hdr & 1u));
-#pragma unroll
-        for (int q = 1; q < NP; ++q) sp[q] = 0u;
-        for (uint32_t i = 1; i < len; ++i) {
-            const uint32_t code = __ldg(a.occ_rec + p + i);
-            bs_add<NP>(sp, __ldg(Acur + (size_t)(code >> 1) * NW + wofs) ^ (0u - (code & 1u)));
-        }
-        if (hdr & 1u) {
-#pragma unroll
-            for (int r = 0; r < NCTR; ++r) vc_inc<kHubCtr>(cnt[r], bs_eq<NP>(sp, r));
-        } else {
-#pragma unroll
-            for (int r = 0; r < NCTR; ++r) vc_dec<kHubCtr>(cnt[r], bs_eq<NP>(sp, r));
-        }
-        p += len;
-    }
+    const uint32_t* recg = a.occ_rec + sc.z;
+    auto recf = [&](unsigned i) { return __ldg(recg + i); };
+    count_occurrences<NP, NCTR, kHubCtr, false, true>(cnt, recf, (unsigned)(sc.w - sc.z), own, Acur, (unsigned)NW,
+                                                valid ? (unsigned)w : 0u);
     // two counters per transpose: 16-bit fields, bits 11..15 = sign extension
 #pragma unroll
     for (int r0 = 0; r0 < NCTR; r0 += 2) {
@@ -520,7 +454,9 @@ __global__ void __launch_bounds__(32) k_hub(StepArgs a, const uint32_t* __restri
     }
     __syncwarp();
     int* dst = a.hubD + (size_t)sc.x * NCTR * a.N;
+#pragma unroll 1
     for (int r = 0; r < NCTR; ++r)
+#pragma unroll 4
         for (int k = 0; k < 32; ++k) {
             const int nl = 32 * k + lane;                  // candidate within the block (coalesced)
             const int n = blockIdx.x * 1024 + nl;
@@ -668,7 +604,7 @@ cudaError_t configure_update(StepArgs* a) {
     long long ng = optin > (long long)gsb ? ((long long)optin - (long long)gsb) / (long long)grb : 0;
     const int max_threads = KB == 4 ? 768 : 512;   // register budget (launch bounds)
     ng = ng < max_threads / GT ? ng : max_threads / GT;
-    ng = ng < 15 ? ng : 15;                       // named barriers 1..15
+    if (GT > 32) ng = ng < 15 ? ng : 15;          // named barriers 1..15 (warp groups use __syncwarp)
     if (ng < 2 && !(ng == 1 && GT == 128)) {
         a->upd_mode = 1;                          // too large for the fused kernel
         size_t smem = (size_t)N * (sizeof(double) + sizeof(float));
