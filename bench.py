@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--chunk", type=int, default=30, help="iterations per tsat_step call (one CUDA graph)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-quality", action="store_true")
     return ap.parse_args()
 
 
@@ -304,6 +305,29 @@ def main():
                "sample": f"{r['steps']} oracle steps on {r['Ns']} of {N} candidates ({r['seconds']:.1f} s, single thread)",
                "cpu": model, "host_cores": cores}
 
+    # ---- trajectory quality (not a timing): one LR cycle (360 iterations) of
+    # the paper-exact Eq. 5 reading (R3) and of the normalize-off variant;
+    # best satisfied fraction and whether the 99 % gate fires
+    quality = None
+    if world == 1 and not args.no_quality:
+        from paper_2511_07737_b200 import config_default
+        quality = {"iterations": 360, "gate": "best candidate satisfies > 99% of clauses"}
+        for label, norm in (("paper_exact_R3", 1), ("normalize_off", 0)):
+            q = Solver(local, stream=stream)
+            q.load_cnf(cnf)
+            c = config_default()
+            c.normalize = norm
+            q.init_batch(N, seed, c)
+            best, gate = None, None
+            for _ in range(12):
+                inf = q.step(30)
+                best = inf.best_unsat if best is None else min(best, inf.best_unsat)
+                if gate is None and (cnf.C - inf.best_unsat) / cnf.C > 0.99:
+                    gate = inf.t
+            quality[label] = {"best_unsat": best, "best_satisfied_frac": (cnf.C - best) / cnf.C,
+                              "gate_99_at_iteration": gate, "solved": bool(inf.solved)}
+            q.close()
+
     kps = s.kernels_per_step()
     line = {
         "metric": "clause-candidate evals/sec", "value": value, "unit": "evals/s", "n_gpus": world,
@@ -318,6 +342,7 @@ def main():
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": kps * args.steps, "clocks": clk.summary(),
         "last_info": {"t": last.t, "best_unsat": last.best_unsat, "loss": last.loss, "solved": last.solved},
+        "quality": quality,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
