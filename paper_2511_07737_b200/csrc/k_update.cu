@@ -34,7 +34,7 @@ __host__ __device__ inline size_t upd_gs_bytes(int KB, int N) { return align16((
 __host__ __device__ inline size_t upd_dpk_words(int N) { return (size_t)N + (N >> 5); }
 __host__ __device__ inline size_t upd_group_bytes(int KB, int N, int rec_cap) {
     const int NDW = KB == 4 ? 1 : 2;
-    return align16((size_t)NDW * upd_dpk_words(N) * 4) + align16((size_t)rec_cap * 4) + align16((size_t)2 * (N >> 5) * 4) + 128;
+    return align16((size_t)NDW * upd_dpk_words(N) * 4) + 2 * align16((size_t)rec_cap * 4) + align16((size_t)2 * (N >> 5) * 4) + 128;
 }
 
 // x * 2^s, exact (== scalbn) when 2^s is a normal double.
@@ -176,6 +176,14 @@ __device__ __noinline__ float noise_xi(unsigned long long seed, long long ng, in
     return (float)(xr[ng & 3] >> 8) * 5.9604644775390625e-08f - 0.5f;
 }
 
+// 4-byte asynchronous global -> shared copy (LDGSTS) and its group fences.
+__device__ __forceinline__ void cp_async4(uint32_t* smem_dst, const uint32_t* gsrc) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // Barrier over one warp group: a warp-sized group only needs __syncwarp, so
 // more than 15 groups (the named-barrier limit) can share a CTA.
 __device__ __forceinline__ void gsync(int bar, int GT) {
@@ -204,7 +212,8 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
     unsigned char* gb = smem + upd_gs_bytes(KB, N) + (size_t)grp * grb;
     uint32_t* dpk = reinterpret_cast<uint32_t*>(gb);
     uint32_t* rec = reinterpret_cast<uint32_t*>(gb + align16((size_t)(KB == 4 ? 1 : 2) * dpkw * 4));
-    uint32_t* posw = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(rec) + align16((size_t)rec_cap * 4));
+    const size_t recw = align16((size_t)rec_cap * 4) / 4;            // words per record buffer (two buffers)
+    uint32_t* posw = rec + 2 * recw;
     uint32_t* negw = posw + NW;
     long long* red = reinterpret_cast<long long*>(gb + grb - 128);                      // 4 + 4 slots
     float* redf = reinterpret_cast<float*>(red + 8);                                    // 4 slots
@@ -227,7 +236,14 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
     const MethodConsts& mc = a.mc;
 
     int v = rowslot[1];
+    if (v < a.V && a.hub_of[v] < 0) {                      // first row: stage its records now
+        const unsigned rb0 = a.occ_ptr[v], re0 = a.occ_ptr[v + 1];
+        for (unsigned i = tg; i < re0 - rb0; i += GT) rec[i] = a.occ_rec[rb0 + i];
+    }
+    gsync(bar, GT);
     for (int it = 0; v < a.V; ++it) {
+        uint32_t* rb_cur = rec + (size_t)(it & 1) * recw;    // this row's records (staged by the previous row)
+        uint32_t* rb_nxt = rec + (size_t)((it + 1) & 1) * recw;
         // ---- fetch the next row; prefetch this row's streams into L2
         if (tg == 0) {
             rowslot[it & 1] = atomicAdd(&a.ds->row_counter, 1);
@@ -261,12 +277,10 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
         // ---- 1+2: bit-sliced gather of the row's occurrences, transpose to bytes
         if (hub < 0) {
             const unsigned nrec = re - rb;
-            for (unsigned i = tg; i < nrec; i += GT) rec[i] = a.occ_rec[rb + i];
-            gsync(bar, GT);
             for (int w = tg; w < NW; w += GT) {
                 const uint32_t own = __ldg(Acur + (size_t)v * NW + w);
                 uint32_t cnt[NCTR][kCtr];
-                auto recf = [&](unsigned i) { return rec[i]; };
+                auto recf = [&](unsigned i) { return rb_cur[i]; };
                 // KB = 8 rows are short (hub rows go to k_hub) and the kernel is
                 // I-cache bound there: count one record at a time
                 if (uni3) count_occurrences<NP, NCTR, kCtr, true, true>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w);
@@ -298,8 +312,17 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
         long long Itot = 0;                                  // every thread folds the warp partials
         for (int i = 0; i < ngw; ++i) Itot += red[i];
         const int vnext = rowslot[it & 1];
+        // stage the next row's records asynchronously (cp.async global -> smem);
+        // they land while this row streams, and are waited for before the Q barrier
+        if (vnext < a.V && a.hub_of[vnext] < 0) {
+            const unsigned nb = a.occ_ptr[vnext], ne = a.occ_ptr[vnext + 1];
+            for (unsigned i = tg; i < ne - nb; i += GT) cp_async4(rb_nxt + i, a.occ_rec + nb + i);
+        }
+        cp_async_commit();
         if (MODE == 1) {                                     // sharded: J partial out, next row
             if (tg == 0) a.Jbuf[v] = Itot;
+            cp_async_wait_all();
+            gsync(bar, GT);
             v = vnext;
             continue;
         }
@@ -353,12 +376,13 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
                     const float2 den2 = __fadd2_rn(mul2_unfused(sq2, make_float2(rbc2, rbc2)), make_float2(epsf, epsf));
                     const float2 num2 = __fmul2_rn(make_float2(nss, nss), mn2);
                     x2 = __fadd2_rn(x2, make_float2(num2.x / den2.x, num2.y / den2.y));
-                    float xs[2] = {x2.x, x2.y};
+                    float xs0 = x2.x, xs1 = x2.y;
                     if (mc.noise) {
-#pragma unroll 1
-                        for (int e = 0; e < 2; ++e) xs[e] = xs[e] + nz * noise_xi(mc.seed, mc.n0 + n + 2 * h + e, v, t);
+                        xs0 = xs0 + nz * noise_xi(mc.seed, mc.n0 + n + 2 * h, v, t);
+                        xs1 = xs1 + nz * noise_xi(mc.seed, mc.n0 + n + 2 * h + 1, v, t);
                     }
-                    const float2 q2 = __fmul2_rn(make_float2(xs[0], xs[1]), make_float2(4294967296.0f, 4294967296.0f));
+                    const float xs[2] = {xs0, xs1};
+                    const float2 q2 = __fmul2_rn(make_float2(xs0, xs1), make_float2(4294967296.0f, 4294967296.0f));
                     Qn += __float2ll_rn(q2.x) + __float2ll_rn(q2.y);      // x 2^32 is exact in fp32
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
@@ -388,6 +412,7 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
         Qn = warp_sum(Qn);
         mx = warp_maxf(mx);
         if (lane == 0) { red[4 + gw] = Qn; redf[gw] = mx; }
+        cp_async_wait_all();                                 // next row's records visible after this barrier
         gsync(bar, GT);
         long long Qtot = 0;
         for (int i = 0; i < ngw; ++i) Qtot += red[4 + i];
