@@ -319,14 +319,13 @@ void or_jacobian_finish(int V, int64_t N, const int64_t* I, const int32_t* s, co
     }
 }
 
-/* grad_vn = (float)(G_vn rho_v - c_v). */
+/* grad_vn = (float)(G_vn rho_v - c_v), the fp64 product and difference as one
+ * fused multiply-add (R27b). */
 void or_grad(int V, int Nl, const double* G, const double* rho, const double* cv, float* grad)
 {
     for (int v = 0; v < V; ++v)
-        for (int j = 0; j < Nl; ++j) {
-            double a = G[(size_t)v * Nl + j] * rho[v];
-            grad[(size_t)v * Nl + j] = (float)(a - cv[v]);
-        }
+        for (int j = 0; j < Nl; ++j)
+            grad[(size_t)v * Nl + j] = (float)fma(G[(size_t)v * Nl + j], rho[v], -cv[v]);
 }
 
 /* (a9) LR schedule, §4.1 l.255-259: lr0 = 1e-1, /10 every 30

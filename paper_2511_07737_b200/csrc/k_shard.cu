@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(256) k_update_b(StepArgs a, const uint32_t* __
             const float G[4] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const float g = (float)((double)G[q] * rho - c);
+                const float g = (float)__fma_rn((double)G[q], rho, -c);     // R27b
                 float x = th[q] * wdf;
                 const float mn = __fmaf_rn(a1, g - mm[q], mm[q]);
                 const float vb = vv[q] * b2f;

@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
         for (int base = 0; base < N; base += 4 * GT) {
             const int n = base + 4 * tg;
             unsigned pnib = 0, nnib = 0;
-            const float4 th4 = thn, m4 = mn4, v4 = vn4;
+            const float4 th4 = thn, m4 = mn4, v4 = vn4;       // software pipeline: next loads in flight
             if (n + 4 * GT < N) {
                 thn = *reinterpret_cast<const float4*>(trow + n + 4 * GT);
                 mn4 = *reinterpret_cast<const float4*>(mrow + n + 4 * GT);
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
                 const uint32_t* dp = dpk + n + (n >> 5);
                 float gg[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) gg[q] = (float)((double)__uint_as_float(dp[q]) * rho - c);
+                for (int q = 0; q < 4; ++q) gg[q] = (float)__fma_rn((double)__uint_as_float(dp[q]), rho, -c);   // R27b
                 // AdamW on candidate pairs: packed fp32x2 ops are per-lane
                 // correctly rounded, i.e. the same canonical ops (R6-R6c)
 #pragma unroll
@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(256) k_update_rowcta(StepArgs a, const uint32_
     long long Qn = 0;
     float mx = 0.0f;
     for (int n = threadIdx.x; n < N; n += blockDim.x) {
-        const float g = (float)(Gs[n] * rho - c);
+        const float g = (float)__fma_rn(Gs[n], rho, -c);                 // R27b
         float th = trow[n] * sc->wdf;
         const float m0 = mrow[n];
         const float mm = __fmaf_rn(sc->a1, g - m0, m0);
