@@ -260,8 +260,14 @@ def main():
         pass
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     achieved = upd_bytes / (upd_ms / 1000.0) / 1e9
+    traffic, traffic_src = None, None
+    try:      # dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture (profiles/)
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[args.config]["k_update"]
+        traffic, traffic_src = tr["bytes"], "profiles/" + tr["report"]
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "kernel": "k_update", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None,
+                "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
                 "algorithmic_bytes_per_launch": upd_bytes, "kernel_ms": per,
                 "kernel_share": {n: per[n] / sum(per.values()) for n in names}}
