@@ -448,7 +448,7 @@ template <int KB>
 __global__ void __launch_bounds__(32) k_hub(StepArgs a, const uint32_t* __restrict__ Acur) {
     constexpr int NP = (KB == 4) ? 2 : 3;
     constexpr int NCTR = KB - 1;
-    __shared__ int sh[NCTR][1024 + 32];
+    __shared__ int sh[2][1024 + 32];
     const int lane = threadIdx.x;
     const int NW = a.N >> 5;
     const int w = blockIdx.x * 32 + lane;
@@ -461,7 +461,9 @@ __global__ void __launch_bounds__(32) k_hub(StepArgs a, const uint32_t* __restri
     auto recf = [&](unsigned i) { return __ldg(recg + i); };
     count_occurrences<NP, NCTR, kHubCtr, false, true>(cnt, recf, (unsigned)(sc.w - sc.z), own, Acur, (unsigned)NW,
                                                 valid ? (unsigned)w : 0u);
-    // two counters per transpose: 16-bit fields, bits 11..15 = sign extension
+    // two counters per transpose (16-bit fields, bits 11..15 = sign extension),
+    // staged through shared memory two bins at a time so the atomics coalesce
+    int* dst = a.hubD + (size_t)sc.x * NCTR * a.N;
 #pragma unroll
     for (int r0 = 0; r0 < NCTR; r0 += 2) {
         uint32_t T[32];
@@ -471,23 +473,22 @@ __global__ void __launch_bounds__(32) k_hub(StepArgs a, const uint32_t* __restri
             T[i] = (r < NCTR) ? cnt[r][b < kHubCtr ? b : kHubCtr - 1] : 0u;
         }
         transpose32(T);
+        __syncwarp();
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-            sh[r0][33 * lane + j] = (int)(short)(T[j] & 0xffffu);
-            if (r0 + 1 < NCTR) sh[r0 + 1][33 * lane + j] = (int)(short)(T[j] >> 16);
+            sh[0][33 * lane + j] = (int)(short)(T[j] & 0xffffu);
+            sh[1][33 * lane + j] = (int)(short)(T[j] >> 16);
         }
-    }
-    __syncwarp();
-    int* dst = a.hubD + (size_t)sc.x * NCTR * a.N;
-#pragma unroll 1
-    for (int r = 0; r < NCTR; ++r)
+        __syncwarp();
+        for (int rr = 0; rr < 2 && r0 + rr < NCTR; ++rr)
 #pragma unroll 4
-        for (int k = 0; k < 32; ++k) {
-            const int nl = 32 * k + lane;                  // candidate within the block (coalesced)
-            const int n = blockIdx.x * 1024 + nl;
-            const int val = sh[r][33 * k + lane];
-            if (n < a.N && val) atomicAdd(dst + (size_t)r * a.N + n, val);
-        }
+            for (int k = 0; k < 32; ++k) {
+                const int nl = 32 * k + lane;                  // candidate within the block (coalesced)
+                const int n = blockIdx.x * 1024 + nl;
+                const int val = sh[rr][33 * k + lane];
+                if (n < a.N && val) atomicAdd(dst + (size_t)(r0 + rr) * a.N + n, val);
+            }
+    }
 }
 
 // ------------------------------------------------------------------ fallback: one CTA per row

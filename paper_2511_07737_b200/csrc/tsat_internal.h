@@ -14,7 +14,7 @@ namespace tsat {
 constexpr int kMaxK = 7;               // clause length supported by the kernels
 constexpr int kMaxStepsPerCall = 4096;
 constexpr int kTopkMax = 2048;         // export: k most confident variables per candidate
-constexpr int kRecCap = 2048;          // occurrence-record words a warp group stages per row
+constexpr int kRecCap = 512;           // occurrence-record words a warp group stages per row (longer rows: hubs)
 constexpr int kHubSlab = 1023;         // occurrences per hub super-chunk (11-bit signed counters)
 
 // ---------------------------------------------------------------- host CNF
