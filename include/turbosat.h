@@ -84,6 +84,7 @@ typedef struct {
     int64_t n_tautologies;   /* clauses containing x and ~x (kept) */
     int64_t n_duplicates;    /* duplicate literals removed */
     int32_t has_empty;       /* an empty clause is present: the instance is UNSAT */
+    int32_t n_hub_rows;      /* variables whose occurrences are counted by the hub pre-pass */
 } tsat_cnf_info;
 
 typedef struct {

@@ -38,7 +38,7 @@ class tsat_config(ct.Structure):
 class tsat_cnf_info(ct.Structure):
     _fields_ = [("V", ct.c_int32), ("C", ct.c_int64), ("nnz", ct.c_int64), ("K", ct.c_int32),
                 ("header_C", ct.c_int64), ("n_warnings", ct.c_int64), ("n_tautologies", ct.c_int64),
-                ("n_duplicates", ct.c_int64), ("has_empty", ct.c_int32)]
+                ("n_duplicates", ct.c_int64), ("has_empty", ct.c_int32), ("n_hub_rows", ct.c_int32)]
 
 
 class tsat_step_info(ct.Structure):

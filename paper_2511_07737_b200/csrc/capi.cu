@@ -242,6 +242,7 @@ void fill_info(const HostCnf& h, tsat_cnf_info* info) {
     info->n_tautologies = h.n_tautologies;
     info->n_duplicates = h.n_duplicates;
     info->has_empty = h.has_empty;
+    info->n_hub_rows = h.n_hubs;
 }
 
 tsat_status upload_cnf(tsat_ctx ctx, HostCnf&& h) {

@@ -380,3 +380,38 @@ def test_sharded_equals_fused_c2():
         np.testing.assert_array_equal(x, y)
     np.testing.assert_array_equal(a.query_unsat(), b.query_unsat())
     assert (ia.best_unsat, ia.best_idx) == (ib.best_unsat, ib.best_idx)
+
+
+# ---------------------------------------------------------------- other code paths
+@pytest.mark.parametrize("kind", ["kb4", "kb8"])
+def test_fallback_row_cta_path(kind):
+    """Batches too large for the fused kernel's shared memory (the g table of
+    N candidates) use the row-per-CTA k_update; same canonical results."""
+    if kind == "kb4":
+        cnf, N = planted_ksat(60, 250, 3, 2), 16384        # g table 256 KB > smem
+    else:
+        cnf, N = industrial_cnf(80, 300, 6), 8192          # KB = 8: 256 KB
+    s, o = make_pair(cnf, N, 3)
+    s.set_state(o.theta, o.m, o.v, 0)
+    for _ in range(4):
+        compare_step(s, o, cnf, "fallback-" + kind)
+
+
+def test_hub_rows_parity_and_export():
+    """An industrial-shaped instance with hub variables (k_hub pre-pass, split
+    occurrence lists, int32 counts): bit-exact steps and export."""
+    cnf = industrial_cnf(1500, 9000, 8)
+    N = 192
+    s, o = make_pair(cnf, N, 4)
+    assert s.info.n_hub_rows > 0
+    s.set_state(o.theta, o.m, o.v, 0)
+    for _ in range(6):
+        _, ref = compare_step(s, o, cnf, "hubs")
+    got = s.export_best(3, 0)
+    idx, u = O.select_top(ref.unsat, 3)
+    k = O.compute_k(cnf.V)
+    for gi, n, un in zip(got, idx, u):
+        assert (gi["candidate"], gi["unsat"]) == (n, un)
+        lits, mags = O.export_partial(np.abs(ref.G[:, n]), ref.bits[:, n], k)
+        np.testing.assert_array_equal(gi["lits"], lits)
+        np.testing.assert_array_equal(gi["abs_grad"], mags.astype(np.float32))
