@@ -96,17 +96,25 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t*
         for (int r = 0; r < KB - 1; ++r)
 #pragma unroll
             for (int b = 0; b < CB; ++b) cnt[r][b] = 0u;
-        for (int cb = 0; cb < nc; cb += kUnr) {
-            uint32_t x[kUnr][KMAXC];
+        constexpr int kG = KMAXC <= 3 ? 2 : 1;          // carry-save groups per iteration (gathers in flight)
+        for (int cb0 = 0; cb0 < nc; cb0 += kUnr * kG) {
+            uint32_t xx[kG][kUnr][KMAXC];
 #pragma unroll
-            for (int u = 0; u < kUnr; ++u)
+            for (int gq = 0; gq < kG; ++gq)
 #pragma unroll
-                for (int l = 0; l < KMAXC; ++l) {
-                    const uint32_t o = (cb + u < nc) ? my[(cb + u) * KMAXC + l] : kNone;
-                    uint32_t val = 0u;
-                    if (o != kNone && valid) val = __ldg(Aw + (o >> 1)) ^ (0u - (o & 1u));
-                    x[u][l] = val;
-                }
+                for (int u = 0; u < kUnr; ++u)
+#pragma unroll
+                    for (int l = 0; l < KMAXC; ++l) {
+                        const int c = cb0 + gq * kUnr + u;
+                        const uint32_t o = (c < nc) ? my[c * KMAXC + l] : kNone;
+                        uint32_t val = 0u;
+                        if (o != kNone && valid) val = __ldg(Aw + (o >> 1)) ^ (0u - (o & 1u));
+                        xx[gq][u][l] = val;
+                    }
+#pragma unroll
+          for (int gq = 0; gq < kG; ++gq) {
+            const int cb = cb0 + gq * kUnr;
+            uint32_t (&x)[kUnr][KMAXC] = xx[gq];
             // one-hot masks [R = r] per clause (padding clauses past nc have all
             // literals 0 -> R = 0, so their bin-0 mask is cleared)
             uint32_t m[kUnr][KB - 1];
@@ -131,26 +139,61 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t*
             }
 #pragma unroll
             for (int r = 0; r < KB - 1; ++r) csa_add4<CB>(cnt[r], m[0][r], m[1][r], m[2][r], m[3][r]);
+          }
         }
         if (valid) {
+            if (KB == 4) {
+                // one 32x32 transpose packs the three 7-bit counts of each
+                // candidate into 10-bit fields of one word; they are widened to
+                // 21-bit fields of a 64-bit CTA accumulator (< 2^21 clauses per
+                // CTA and word block, see launch_clause)
+                uint32_t T[32];
 #pragma unroll
-            for (int r = 0; r < KB - 1; ++r)
+                for (int i = 0; i < 32; ++i) T[i] = (i % 10 < CB && i / 10 < KB - 1) ? cnt[i / 10][i % 10] : 0u;
+                transpose32(T);
+                unsigned long long* shp = reinterpret_cast<unsigned long long*>(sh);
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (T[j]) {
+                        const unsigned long long pk = T[j];
+                        const unsigned long long wide = (pk & 0x3FFull) | ((pk & 0xFFC00ull) << 11) | ((pk & 0x3FF00000ull) << 22);
+                        atomicAdd(&shp[33 * lane + j], wide);             // padded layout
+                    }
+            } else {
+#pragma unroll
+                for (int r = 0; r < KB - 1; ++r)
 #pragma unroll 2
-                for (int j0 = 0; j0 < 32; ++j0) {
-                    int j = (j0 + lane) & 31;            // rotate: conflict-free smem banks
-                    int val = 0;
+                    for (int j0 = 0; j0 < 32; ++j0) {
+                        int j = (j0 + lane) & 31;            // rotate: conflict-free smem banks
+                        int val = 0;
 #pragma unroll
-                    for (int b = 0; b < CB; ++b) val |= (int)((cnt[r][b] >> j) & 1u) << b;
-                    if (val) atomicAdd(&sh[r * 1024 + lane * 32 + j], val);
-                }
+                        for (int b = 0; b < CB; ++b) val |= (int)((cnt[r][b] >> j) & 1u) << b;
+                        if (val) atomicAdd(&sh[r * 1024 + lane * 32 + j], val);
+                    }
+            }
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < (KB - 1) * 1024; i += blockDim.x) {
-        int r = i >> 10, cl = i & 1023;
-        int n = blockIdx.x * 1024 + cl;
-        int val = sh[i];
-        if (n < N && val) atomicAdd(&hist[(size_t)n * KB + r], val);
+    if (KB == 4) {
+        const unsigned long long* shp = reinterpret_cast<const unsigned long long*>(sh);
+        for (int cl = threadIdx.x; cl < 1024; cl += blockDim.x) {
+            const int n = blockIdx.x * 1024 + cl;
+            const unsigned long long pk = shp[33 * (cl >> 5) + (cl & 31)];
+            if (n < N && pk) {
+#pragma unroll
+                for (int r = 0; r < KB - 1; ++r) {
+                    const int val = (int)((pk >> (21 * r)) & 0x1FFFFFull);
+                    if (val) atomicAdd(&hist[(size_t)n * KB + r], val);
+                }
+            }
+        }
+    } else {
+        for (int i = threadIdx.x; i < (KB - 1) * 1024; i += blockDim.x) {
+            int r = i >> 10, cl = i & 1023;
+            int n = blockIdx.x * 1024 + cl;
+            int val = sh[i];
+            if (n < N && val) atomicAdd(&hist[(size_t)n * KB + r], val);
+        }
     }
 }
 
@@ -165,6 +208,9 @@ cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, cudaStream_t 
     const int per_sm = K <= 3 ? 3 : 2;
     long long gy = ((long long)a.num_sms * per_sm + nwb - 1) / nwb;
     if (gy > ctas_needed) gy = ctas_needed;
+    // packed 21-bit CTA histogram fields (KB = 4): < 2^21 clauses per CTA
+    const long long gy_min = (a.C + (1LL << 20) - 1) >> 20;
+    if (gy < gy_min) gy = gy_min;
     if (gy < 1) gy = 1;
     dim3 grid(nwb, (unsigned)gy);
     const int uni = a.uniform_len;
