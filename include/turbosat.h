@@ -202,7 +202,8 @@ tsat_status tsat_debug_copy(tsat_ctx ctx, int32_t which, void* host_dst, size_t 
 
 /* Kernel timing: when enabled, CUDA events bracket every kernel of every step
  * (also inside the graph).  tsat_kernel_times fills ms5 with the accumulated
- * milliseconds per kernel class [clause, gtable, hub, update, step_end] and
+ * milliseconds per segment [clause, gtable, hub, update, end] (sharded: the
+ * segments also hold the collectives and small bookkeeping kernels) and
  * *steps with the number of steps timed, then resets the accumulators. */
 tsat_status tsat_set_profiling(tsat_ctx ctx, int32_t enable);
 tsat_status tsat_kernel_times(tsat_ctx ctx, double* ms5, int64_t* steps);

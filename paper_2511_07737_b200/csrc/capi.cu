@@ -112,6 +112,7 @@ Layout make_layout(int V, int N, int KB, int n_hubs, bool sharded) {
     L.hist = take((size_t)N * KB * 4);
     L.gtab = take((size_t)N * KB * 4);
     L.S = take((size_t)N * 8);
+    L.lossp = take((size_t)((N + 255) / 256) * 8);
     L.unsat = take((size_t)N * 4);
     L.rowQ = take((size_t)V * 8);
     L.rowD = take((size_t)V * 8);
@@ -146,6 +147,7 @@ StepArgs step_args(tsat_ctx ctx) {
     a.gtab = (float*)(w + L.gtab);
     a.hubD = (int*)(w + L.hubD);
     a.S = (double*)(w + L.S);
+    a.lossp = (double*)(w + L.lossp);
     a.rowQ = (long long*)(w + L.rowQ);
     a.rowD = (double*)(w + L.rowD);
     a.rowRho = (double*)(w + L.rowRho);
@@ -870,11 +872,11 @@ tsat_status tsat_kernels_per_step(tsat_ctx ctx, int32_t* n) {
     GUARD_CTX();
     if (!n) return TSAT_E_ARG;
     int k = 0;
-    if (ctx->have_cnf && ctx->cnf.C > 0) ++k;                                  // clause
+    k += 1;                                                                     // clause (or accumulator reset)
     k += 1;                                                                     // gtable
     if (ctx->have_batch && ctx->upd_mode == 0 && ctx->cnf.n_hub_sc > 0) ++k;    // hub
-    if (ctx->have_cnf && ctx->cnf.V > 0) ++k;                                  // update
-    k += 1;                                                                     // step end
+    if (ctx->have_cnf && ctx->cnf.V > 0) ++k;                                  // update (phase A when sharded)
+    if (ctx->sharded) k += 5;   // pack/unpack max, update B, rows finish, step end (NCCL's own kernels not counted)
     *n = k;
     return TSAT_OK;
 }

@@ -49,7 +49,9 @@ template <int KB, int KMAXC>
 __global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t* __restrict__ A, int NW,
                                                                 const uint32_t* __restrict__ cptr,
                                                                 const uint32_t* __restrict__ clit, long long C,
-                                                                int* __restrict__ hist, int N, int uniform) {
+                                                                int* __restrict__ hist, int N, int uniform,
+                                                                DevScalars* __restrict__ ds,
+                                                                const StepScalars* __restrict__ sc) {
     constexpr int NP = (KB == 4) ? 2 : 3;
     constexpr int CB = 7;
     __shared__ int sh[(KB - 1) * 1024];
@@ -57,6 +59,15 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t*
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int w = blockIdx.x * 32 + lane;
     const bool valid = w < NW;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+        // the iteration's accumulators (the previous k_update consumed them):
+        // best key and gmax (k_gtable), row scheduler and max|theta_{t+1}| (k_update)
+        const long long t = sc->t;
+        ds->best_key = ~0ull;
+        ds->gmax_bits = 0ull;
+        ds->row_counter = 0;
+        ds->thmax_bits[(t + 1) & 1] = 0u;
+    }
     for (int i = threadIdx.x; i < (KB - 1) * 1024; i += blockDim.x) sh[i] = 0;
     __syncthreads();
     uint32_t* my = soff[warp];
@@ -197,8 +208,19 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t*
     }
 }
 
-cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, cudaStream_t st) {
-    if (a.C == 0) return cudaGetLastError();
+__global__ void k_reset_accumulators(DevScalars* __restrict__ ds, const StepScalars* __restrict__ sc) {
+    const long long t = sc->t;
+    ds->best_key = ~0ull;
+    ds->gmax_bits = 0ull;
+    ds->row_counter = 0;
+    ds->thmax_bits[(t + 1) & 1] = 0u;
+}
+
+cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, const StepScalars* sc, cudaStream_t st) {
+    if (a.C == 0) {
+        k_reset_accumulators<<<1, 1, 0, st>>>(a.ds, sc);
+        return cudaGetLastError();
+    }
     const int NW = a.N >> 5;
     const int nwb = (NW + 31) / 32;
     const long long nchunks = (a.C + kCH - 1) / kCH;
@@ -215,11 +237,11 @@ cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, cudaStream_t 
     dim3 grid(nwb, (unsigned)gy);
     const int uni = a.uniform_len;
     if (K <= 2)
-        k_clause<4, 2><<<grid, 256, 0, st>>>(Acur, NW, a.cptr, a.clit, a.C, a.hist, a.N, uni && K == 2);
+        k_clause<4, 2><<<grid, 256, 0, st>>>(Acur, NW, a.cptr, a.clit, a.C, a.hist, a.N, uni && K == 2, a.ds, sc);
     else if (K == 3)
-        k_clause<4, 3><<<grid, 256, 0, st>>>(Acur, NW, a.cptr, a.clit, a.C, a.hist, a.N, uni);
+        k_clause<4, 3><<<grid, 256, 0, st>>>(Acur, NW, a.cptr, a.clit, a.C, a.hist, a.N, uni, a.ds, sc);
     else
-        k_clause<8, 7><<<grid, 256, 0, st>>>(Acur, NW, a.cptr, a.clit, a.C, a.hist, a.N, uni && K == 7);
+        k_clause<8, 7><<<grid, 256, 0, st>>>(Acur, NW, a.cptr, a.clit, a.C, a.hist, a.N, uni && K == 7, a.ds, sc);
     return cudaGetLastError();
 }
 

@@ -79,10 +79,17 @@ __global__ void __launch_bounds__(256) k_rowstats(const float* __restrict__ thet
 // the E table, g[r] = (E[r-rmin]/den)(1 - tau(r - S)) rounded to fp32 (R26)
 // into the bin-major table gtab[r][n]; unsat; best key; gmax over |g32|.
 // Clears the histogram for the next iteration.
+// W = 1: the last block to finish also closes the iteration's bookkeeping
+// (what a separate end-of-step kernel did): the loss -sum_n S_n from the
+// per-block sums in block order (deterministic), the step info, and the first
+// model's iteration / index (its bits are kept by k_update, A22).
 template <int KB>
 __global__ void __launch_bounds__(256) k_gtable(int* __restrict__ hist, int N, long long C, MethodConsts mc,
                                                 float* __restrict__ gtab, double* __restrict__ S,
-                                                int* __restrict__ unsat, DevScalars* __restrict__ ds, int sharded) {
+                                                int* __restrict__ unsat, DevScalars* __restrict__ ds, int sharded,
+                                                double* __restrict__ lossp, const StepScalars* __restrict__ sc) {
+    __shared__ double shS[8];
+    __shared__ bool last;
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     unsigned long long key = ~0ull;
@@ -149,40 +156,36 @@ __global__ void __launch_bounds__(256) k_gtable(int* __restrict__ hist, int N, l
         atomicMax(&ds->gmax_bits, gb);
         if (sharded) atomicAdd(reinterpret_cast<unsigned long long*>(&ds->loss_fx), (unsigned long long)lfx);
     }
-}
-
-// ------------------------------------------------------------------ end of iteration
-// Loss (deterministic fixed-shape reduction), first-model bookkeeping, step
-// info, and reset of the per-iteration accumulators.
-__global__ void __launch_bounds__(1024) k_step_end(const double* __restrict__ S, int N, DevScalars* __restrict__ ds,
-                                                   const StepScalars* __restrict__ sc) {
-    __shared__ double sh[32];
-    double a = 0.0;
-    for (int n = threadIdx.x; n < N; n += blockDim.x) a = a + S[n];
+    if (sharded) return;                       // the sharded step ends in k_step_end_sharded
+    // block sum of S in a fixed order (warp trees, then warps ascending)
+    double sv = n < N ? S[n] : 0.0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a = a + __shfl_xor_sync(0xffffffffu, a, o);
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = a;
+    for (int o = 16; o > 0; o >>= 1) sv = sv + __shfl_xor_sync(0xffffffffu, sv, o);
+    if (lane == 0) shS[threadIdx.x >> 5] = sv;
     __syncthreads();
-    if (threadIdx.x < 32) {
-        double b = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) b = b + __shfl_xor_sync(0xffffffffu, b, o);
-        if (threadIdx.x == 0) {
-            const long long t = sc->t;
-            const unsigned long long bk = ds->best_key;
-            const int bu = (int)(bk >> 32);
-            const long long bi = (long long)(bk & 0xffffffffull);
-            if (bu == 0 && ds->sol_step < 0) { ds->sol_step = t; ds->sol_idx = bi; }
-            ds->loss = -b;
-            ds->info_t = t + 1;
-            ds->info_best_unsat = bu;
-            ds->info_best_idx = bi;
-            ds->info_loss = -b;
-            ds->best_key = ~0ull;
-            ds->gmax_bits = 0ull;
-            ds->thmax_bits[t & 1] = 0u;
-            ds->row_counter = 0;
-        }
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) b = b + shS[i];
+        lossp[blockIdx.x] = b;
+        __threadfence();
+        last = atomicAdd(&ds->gt_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double tot = 0.0;
+        for (unsigned i = 0; i < gridDim.x; ++i) tot = tot + *((volatile double*)lossp + i);
+        const long long t = sc->t;
+        const unsigned long long bk = *((volatile unsigned long long*)&ds->best_key);
+        const int bu = (int)(bk >> 32);
+        const long long bi = (long long)(bk & 0xffffffffull);
+        if (bu == 0 && ds->sol_step < 0) { ds->sol_step = t; ds->sol_idx = bi; }
+        ds->loss = -tot;
+        ds->info_t = t + 1;
+        ds->info_best_unsat = bu;
+        ds->info_best_idx = bi;
+        ds->info_loss = -tot;
+        ds->gt_done = 0u;
     }
 }
 
@@ -354,15 +357,10 @@ cudaError_t launch_rowstats(const float* theta, int V, int N, const MethodConsts
     return cudaGetLastError();
 }
 
-cudaError_t launch_gtable(const StepArgs& a, cudaStream_t st) {
+cudaError_t launch_gtable(const StepArgs& a, const StepScalars* sc, cudaStream_t st) {
     int blocks = (a.N + 255) / 256;
-    if (a.KB == 4) k_gtable<4><<<blocks, 256, 0, st>>>(a.hist, a.N, a.C, a.mc, a.gtab, a.S, a.unsat, a.ds, a.sharded);
-    else k_gtable<8><<<blocks, 256, 0, st>>>(a.hist, a.N, a.C, a.mc, a.gtab, a.S, a.unsat, a.ds, a.sharded);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_step_end(const StepArgs& a, const StepScalars* sc, cudaStream_t st) {
-    k_step_end<<<1, 1024, 0, st>>>(a.S, a.N, a.ds, sc);
+    if (a.KB == 4) k_gtable<4><<<blocks, 256, 0, st>>>(a.hist, a.N, a.C, a.mc, a.gtab, a.S, a.unsat, a.ds, a.sharded, a.lossp, sc);
+    else k_gtable<8><<<blocks, 256, 0, st>>>(a.hist, a.N, a.C, a.mc, a.gtab, a.S, a.unsat, a.ds, a.sharded, a.lossp, sc);
     return cudaGetLastError();
 }
 

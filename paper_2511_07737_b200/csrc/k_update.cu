@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
             a.rowQ[v] = Qtot; a.rowD[v] = dn; a.rowRho[v] = rhon; a.rowGuard[v] = gn;
             atomicMax(&a.ds->thmax_bits[(t + 1) & 1], __float_as_uint(m2));
             const unsigned long long bk = a.ds->best_key;
-            if ((bk >> 32) == 0ull && a.ds->sol_step < 0) {          // first model: keep its bits (A22)
+            if ((bk >> 32) == 0ull && (a.ds->sol_step < 0 || a.ds->sol_step == t)) {          // first model: keep its bits (A22)
                 const long long idx = (long long)(bk & 0xffffffffull) - mc.n0;
                 if (idx >= 0 && idx < N)
                     a.sol[v] = (unsigned char)((Acur[(size_t)v * NW + (idx >> 5)] >> (idx & 31)) & 1u);
@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(256) k_update_rowcta(StepArgs a, const uint32_
         sh_d = dn;
         atomicMax(&a.ds->thmax_bits[(t + 1) & 1], __float_as_uint(mx));
         const unsigned long long bk = a.ds->best_key;
-        if ((bk >> 32) == 0ull && a.ds->sol_step < 0) {
+        if ((bk >> 32) == 0ull && (a.ds->sol_step < 0 || a.ds->sol_step == t)) {
             const long long idx = (long long)(bk & 0xffffffffull) - mc.n0;
             if (idx >= 0 && idx < N) a.sol[v] = (unsigned char)((Arow[idx >> 5] >> (idx & 31)) & 1u);
         }

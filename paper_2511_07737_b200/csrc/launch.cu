@@ -3,25 +3,26 @@
 
 namespace tsat {
 
-cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, cudaStream_t st);
-cudaError_t launch_gtable(const StepArgs& a, cudaStream_t st);
+cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, const StepScalars* sc, cudaStream_t st);
+cudaError_t launch_gtable(const StepArgs& a, const StepScalars* sc, cudaStream_t st);
 cudaError_t launch_hub(const StepArgs& a, const uint32_t* Acur, cudaStream_t st);
 cudaError_t launch_update(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
                           cudaStream_t st);
-cudaError_t launch_step_end(const StepArgs& a, const StepScalars* sc, cudaStream_t st);
 cudaError_t configure_update(StepArgs* a);
 
-// which: 0 clause (a4,a5), 1 gtable (a6), 2 hub counts (a7, hub rows),
-//        3 fused backward/Jacobian/AdamW/re-binarise (a7-a9), 4 step end (a10)
+// which: 0 clause (a4,a5; also resets the iteration's accumulators),
+//        1 gtable (a6, a10: loss, best candidate, first model), 2 hub counts (a7,
+//        hub rows), 3 fused backward/Jacobian/AdamW/re-binarise (a7-a9),
+//        4 nothing on the W = 1 path (the sharded path ends in k_step_end_sharded)
 cudaError_t launch_step_kernel(int which, const StepArgs& a, const StepScalars* sc_dev, long long t, cudaStream_t st) {
     const uint32_t* Acur = (t & 1) ? a.A1 : a.A0;
     uint32_t* Anext = (t & 1) ? a.A0 : a.A1;
     switch (which) {
-        case 0: return launch_clause(a, Acur, st);
-        case 1: return launch_gtable(a, st);
+        case 0: return launch_clause(a, Acur, sc_dev, st);
+        case 1: return launch_gtable(a, sc_dev, st);
         case 2: return a.upd_mode == 0 ? launch_hub(a, Acur, st) : cudaGetLastError();
         case 3: return launch_update(a, Acur, Anext, sc_dev, st);
-        case 4: return launch_step_end(a, sc_dev, st);
+        case 4: return cudaGetLastError();
     }
     return cudaErrorInvalidValue;
 }

@@ -83,6 +83,8 @@ struct DevScalars {
     long long info_best_idx;
     double info_loss;
     long long loss_fx;               // sharded: this rank's sum of S_n * 2^40 (exact int64)
+    unsigned int gt_done;            // k_gtable blocks finished (last block does the step bookkeeping)
+    int pad2;
 };
 
 // Method constants passed by value to kernels.
@@ -105,6 +107,7 @@ struct StepArgs {
     int *hist, *unsat;
     float* gtab;                     // [KB][N] fp32 derivative table (R26)
     double* S;
+    double* lossp;                   // [ceil(N/256)] k_gtable per-block sums of S_n
     long long* rowQ;
     double *rowD, *rowRho;
     unsigned char *rowGuard, *sol;
@@ -136,7 +139,7 @@ struct StepArgs {
 
 // Workspace layout (byte offsets), see capi.cu: make_layout().
 struct Layout {
-    size_t theta, m, v, A0, A1, hist, gtab, S, unsat, rowQ, rowD, rowRho, rowGuard, scal, steptab, sol, hubD;
+    size_t theta, m, v, A0, A1, hist, gtab, S, lossp, unsat, rowQ, rowD, rowRho, rowGuard, scal, steptab, sol, hubD;
     size_t Gbuf, Jbuf, Qbuf, Pbuf, Nbuf, maxbuf, total;
 };
 
