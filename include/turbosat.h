@@ -192,6 +192,10 @@ tsat_status tsat_get_solution(tsat_ctx ctx, uint8_t* host_values, int64_t* idx, 
 tsat_status tsat_get_state(tsat_ctx ctx, float* theta, float* m, float* v, int64_t* t);
 tsat_status tsat_set_state(tsat_ctx ctx, const float* theta, const float* m, const float* v, int64_t t);
 
+/* Rows rows[0..nrows) (0-based variables) of theta, m, v into host arrays of
+ * [nrows][N_local] fp32 (any may be NULL): sampled checks at full size. */
+tsat_status tsat_get_rows(tsat_ctx ctx, const int32_t* rows, int32_t nrows, float* theta, float* m, float* v);
+
 /* Copy an internal buffer to host (tests / diagnostics):
  *   which 0: histogram h [N_local][KB] int32 of the last evaluated state (KB = 4 if K <= 3 else 8)
  *         1: derivative table g [KB][N_local] fp32 (bin-major, R26);   2: S [N_local] fp64

@@ -70,6 +70,8 @@ def lib():
             "or_adamw": (None, [i32, i64, i32, P, P, P, P, i64, f64, f64, f64, f64, f64, f64, u64]),
             "or_abs_max": (f32, [ct.c_size_t, P]),
             "or_gmax": (f64, [i32, i32, P, P]),
+            "or_hist_stream": (None, [i32, P, P, i32, i32, P, P, P]),
+            "or_backward_rows": (None, [i32, P, P, i32, i32, P, P, P, i32, P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(_lib, name)
@@ -325,3 +327,54 @@ class Oracle:
         return StepOut(t=t, bits=b, R=R, h=h, unsat=unsat, S=S, g=g, g32=g32, loss=loss, G=G, grad=grad,
                        J=J, d=d, gmax=gmax, thmax=thmax, best_unsat=best_unsat, best_idx=best_idx,
                        lr=lr, extra=dict(Q=Q, mu=mu, rho=rho, guard=guard, cv=cv, rmin=rmin, I=I, s=s))
+
+
+def step_sampled(cnf, theta, m, v, t, rows, cfg: Config | None = None):
+    """One iteration at full size, for a sample of variable rows (test only).
+
+    Same arithmetic as Oracle.step, organised for large instances: row
+    statistics and bits for all variables, the histogram streamed clause by
+    clause (no C x N matrix), the g table for all candidates, then the
+    backward / Jacobian / AdamW only for `rows`.  theta, m, v are the full
+    (V x N) state; returns (unsat, g32, S, loss, theta1, m1, v1) with the last
+    three for the sampled rows only."""
+    cfg = cfg or Config()
+    cnf = binary_problem_matrix(cnf)
+    L = lib()
+    V, N = theta.shape
+    K = cnf.K
+    Q = np.empty(V, np.int64)
+    L.or_row_sums(V, N, _p(theta), _p(Q))
+    mu = np.empty(V); d = np.empty(V); rho = np.empty(V); guard = np.empty(V, np.uint8)
+    L.or_row_finish(V, N, _p(Q), cfg.normalize, cfg.eps_norm, _p(mu), _p(d), _p(rho), _p(guard))
+    b = np.empty((V, N), np.uint8)
+    L.or_binarize(V, N, _p(theta), _p(d), _p(b))
+    h = np.empty((N, K + 1), np.int32)
+    rowbuf = np.empty(N, np.uint8)
+    L.or_hist_stream(cnf.C, _p(cnf.clause_ptr), _p(cnf.lits), N, K, _p(b), _p(h), _p(rowbuf))
+    S, g, rmin = smoothmin(h, cfg.tau)
+    g32 = g.astype(np.float32)
+    loss = -float(sum(float(x) for x in S))
+    gmax = L.or_gmax(N, K, _p(g32), _p(rmin))
+    thmax = L.or_abs_max(theta.size, _p(theta))
+    rows = np.ascontiguousarray(rows, np.int32)
+    nr = len(rows)
+    G = np.empty((nr, N), np.float64)
+    cnt = np.empty((N, K + 1), np.int32)
+    L.or_backward_rows(cnf.C, _p(cnf.clause_ptr), _p(cnf.lits), N, K, _p(b), _p(np.ascontiguousarray(g32)),
+                       _p(rows), nr, _p(G), _p(cnt), _p(rowbuf))
+    occ = np.bincount(np.abs(cnf.lits.astype(np.int64)) - 1, minlength=V).astype(np.int32)[rows]
+    th = np.ascontiguousarray(theta[rows]); mm = np.ascontiguousarray(m[rows]); vv = np.ascontiguousarray(v[rows])
+    I = np.empty(nr, np.int64); s = np.empty(nr, np.int32); valid = np.empty(nr, np.uint8)
+    L.or_jacobian_partial(nr, N, _p(G), _p(th), _p(np.ascontiguousarray(occ)), N, gmax, thmax, _p(I), _p(s), _p(valid))
+    J = np.empty(nr); cv = np.empty(nr)
+    rho_r = np.ascontiguousarray(rho[rows]); guard_r = np.ascontiguousarray(guard[rows])
+    L.or_jacobian_finish(nr, N, _p(I), _p(s), _p(valid), _p(rho_r), _p(guard_r), cfg.normalize, _p(J), _p(cv))
+    grad = np.empty((nr, N), np.float32)
+    L.or_grad(nr, N, _p(G), _p(rho_r), _p(cv), _p(grad))
+    lr = lr_at(t, cfg)
+    # noise is keyed by the variable index: only sigma = 0 here
+    assert cfg.noise_sigma == 0.0
+    L.or_adamw(nr, 0, N, _p(th), _p(mm), _p(vv), _p(grad), t, lr, cfg.beta1, cfg.beta2, cfg.eps,
+               cfg.weight_decay, 0.0, 0)
+    return h[:, 0].copy(), g32, S, loss, th, mm, vv

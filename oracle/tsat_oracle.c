@@ -411,3 +411,70 @@ double or_gmax(int Nl, int K, const float* g, const int32_t* rmin)
         }
     return mx;
 }
+
+/* ------------------------------------------------------------------ */
+/* Full-size sampled checks (tests/test_gpu_fullsize.py): the same steps as   */
+/* above, but the histogram is accumulated clause by clause without storing  */
+/* R (C x N bytes), and the backward is evaluated only for listed rows.      */
+/* ------------------------------------------------------------------ */
+
+/* §3.1.4 histogram h[n][r] of R = P A (Eq. 1), streaming over clauses. */
+void or_hist_stream(int C, const int64_t* cptr, const int32_t* lits, int Nl, int K,
+                    const uint8_t* b, int32_t* h, uint8_t* rowbuf)
+{
+    for (int j = 0; j < Nl * (K + 1); ++j) h[j] = 0;
+    for (int c = 0; c < C; ++c) {
+        for (int j = 0; j < Nl; ++j) rowbuf[j] = 0;
+        for (int64_t l = cptr[c]; l < cptr[c + 1]; ++l) {
+            int32_t lit = lits[l];
+            int v = (lit > 0 ? lit : -lit) - 1;
+            const uint8_t* brow = b + (size_t)v * Nl;
+            for (int j = 0; j < Nl; ++j) rowbuf[j] = (uint8_t)(rowbuf[j] + (lit > 0 ? brow[j] : (uint8_t)(1 - brow[j])));
+        }
+        for (int j = 0; j < Nl; ++j) h[(size_t)j * (K + 1) + rowbuf[j]] += 1;
+    }
+}
+
+/* Backward (as or_backward) for the variables rows[0..nrows): G[i][n] for
+ * variable rows[i], evaluating R_cn of each of its clauses directly. */
+void or_backward_rows(int C, const int64_t* cptr, const int32_t* lits, int Nl, int K, const uint8_t* b,
+                      const float* g, const int32_t* rows, int nrows, double* G, int32_t* cnt, uint8_t* rowbuf)
+{
+    for (int i = 0; i < nrows; ++i) {
+        int v = rows[i];
+        memset(cnt, 0, (size_t)Nl * (K + 1) * sizeof(int32_t));
+        for (int c = 0; c < C; ++c) {
+            int sign = 0;
+            for (int64_t l = cptr[c]; l < cptr[c + 1]; ++l) {
+                int32_t lit = lits[l];
+                if ((lit > 0 ? lit : -lit) - 1 == v) sign += lit > 0 ? -1 : +1;   /* cneg - cpos */
+            }
+            if (sign == 0) {
+                /* v absent, or a tautology x v ~x whose two terms cancel */
+                int present = 0;
+                for (int64_t l = cptr[c]; l < cptr[c + 1]; ++l)
+                    if (((lits[l] > 0 ? lits[l] : -lits[l]) - 1) == v) present = 1;
+                if (!present) continue;
+            }
+            for (int j = 0; j < Nl; ++j) rowbuf[j] = 0;
+            for (int64_t l = cptr[c]; l < cptr[c + 1]; ++l) {
+                int32_t lit = lits[l];
+                int u = (lit > 0 ? lit : -lit) - 1;
+                const uint8_t* brow = b + (size_t)u * Nl;
+                for (int j = 0; j < Nl; ++j) rowbuf[j] = (uint8_t)(rowbuf[j] + (lit > 0 ? brow[j] : (uint8_t)(1 - brow[j])));
+            }
+            for (int64_t l = cptr[c]; l < cptr[c + 1]; ++l) {
+                int32_t lit = lits[l];
+                if (((lit > 0 ? lit : -lit) - 1) != v) continue;
+                int delta = lit > 0 ? -1 : +1;
+                for (int j = 0; j < Nl; ++j) cnt[(size_t)j * (K + 1) + rowbuf[j]] += delta;
+            }
+        }
+        for (int j = 0; j < Nl; ++j) {
+            float acc = 0.0f;
+            for (int r = 0; r <= K; ++r)
+                acc = fmaf((float)cnt[(size_t)j * (K + 1) + r], g[(size_t)j * (K + 1) + r], acc);
+            G[(size_t)i * Nl + j] = (double)acc;
+        }
+    }
+}

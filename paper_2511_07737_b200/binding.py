@@ -71,6 +71,7 @@ _SIGS = {
     "tsat_get_state": (ct.c_int, [P, P, P, P, ct.POINTER(ct.c_int64)]),
     "tsat_set_state": (ct.c_int, [P, P, P, P, ct.c_int64]),
     "tsat_debug_copy": (ct.c_int, [P, ct.c_int32, P, ct.c_size_t]),
+    "tsat_get_rows": (ct.c_int, [P, P, ct.c_int32, P, P, P]),
     "tsat_set_profiling": (ct.c_int, [P, ct.c_int32]),
     "tsat_kernel_times": (ct.c_int, [P, P, ct.POINTER(ct.c_int64)]),
     "tsat_kernels_per_step": (ct.c_int, [P, ct.POINTER(ct.c_int32)]),
@@ -310,6 +311,15 @@ class Solver:
         mm = np.ascontiguousarray(m, np.float32)
         vv = np.ascontiguousarray(v, np.float32)
         self._check(self.lib.tsat_set_state(self.h, _ptr(th), _ptr(mm), _ptr(vv), int(t)))
+
+    def get_rows(self, rows):
+        r = np.ascontiguousarray(rows, np.int32)
+        n = self.N_local_count()
+        th = np.empty((len(r), n), np.float32)
+        m = np.empty_like(th)
+        v = np.empty_like(th)
+        self._check(self.lib.tsat_get_rows(self.h, _ptr(r), len(r), _ptr(th), _ptr(m), _ptr(v)))
+        return th, m, v
 
     def debug(self, which: int, dtype, shape) -> np.ndarray:
         out = np.empty(shape, dtype)

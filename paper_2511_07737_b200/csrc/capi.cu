@@ -765,6 +765,23 @@ tsat_status tsat_set_state(tsat_ctx ctx, const float* theta, const float* m, con
     return TSAT_OK;
 }
 
+tsat_status tsat_get_rows(tsat_ctx ctx, const int32_t* rows, int32_t nrows, float* theta, float* m, float* v) {
+    GUARD_CTX();
+    tsat_status s = check_batch(ctx, false);
+    if (s != TSAT_OK) return s;
+    if (nrows < 0 || (nrows > 0 && !rows)) return fail(ctx, TSAT_E_ARG, "bad rows");
+    const size_t rb = (size_t)ctx->N * 4;
+    for (int32_t i = 0; i < nrows; ++i) {
+        if (rows[i] < 0 || rows[i] >= ctx->cnf.V) return fail(ctx, TSAT_E_ARG, "row out of range");
+        const size_t off = (size_t)rows[i] * rb;
+        if (theta) CK(cudaMemcpyAsync((char*)theta + i * rb, ctx->ws + ctx->L.theta + off, rb, cudaMemcpyDeviceToHost, ctx->stream));
+        if (m) CK(cudaMemcpyAsync((char*)m + i * rb, ctx->ws + ctx->L.m + off, rb, cudaMemcpyDeviceToHost, ctx->stream));
+        if (v) CK(cudaMemcpyAsync((char*)v + i * rb, ctx->ws + ctx->L.v + off, rb, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TSAT_OK;
+}
+
 tsat_status tsat_debug_copy(tsat_ctx ctx, int32_t which, void* dst, size_t bytes) {
     GUARD_CTX();
     tsat_status s = check_batch(ctx, false);
