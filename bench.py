@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-quality", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="W=1: run the candidate-sharded (multi-GPU) kernels")
     return ap.parse_args()
 
 
@@ -200,6 +201,9 @@ def main():
     def make_solver():
         if world > 1:
             return Solver.distributed(local, rank, world, stream=stream)
+        if args.sharded:       # the multi-GPU kernels + NCCL on a 1-rank communicator
+            from paper_2511_07737_b200 import nccl_unique_id
+            return Solver(local, stream=stream, rank=0, world=1, nccl_unique_id=nccl_unique_id())
         return Solver(local, stream=stream)
 
     s = make_solver()
@@ -341,7 +345,8 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_desc(args.config, cnf, N * world), "V": cnf.V, "C": cnf.C, "K": cnf.K,
                    "N_per_gpu": N, "N_global": N * world, "seed": seed,
-                   "parallelism": f"candidate-sharded x{world} (NCCL exact int64 exchanges)" if world > 1 else "single GPU",
+                   "parallelism": (f"candidate-sharded x{world} (NCCL exact int64 exchanges)" if world > 1 else
+                                   "single GPU, sharded kernels on a 1-rank NCCL communicator" if args.sharded else "single GPU"),
                    "l2": "state (theta, m, v: %.0f MB) larger than L2; no flush" % (12 * cnf.V * N / 1e6),
                    "graph_chunk": chunk},
         "gradient_steps_per_s": args.steps / (ms / 1000.0),
