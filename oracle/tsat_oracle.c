@@ -277,13 +277,16 @@ static int ceil_log2(double x)
 
 /* (a8) Eq. 5 Jacobian (l.269 "fully differentiable").  With x = theta/mu
  * (mu the row mean over all N), dL/dtheta_vn = G_vn/d_v - J_v/(N d_v^2),
- * J_v = sum_m G_vm theta_vm.  J_v is summed exactly in int64 fixed point:
- * p = G theta (fp64); s_v = 61 - ceil(log2(N occ_v gmax thmax)) (a global
- * bound on |sum p|); I_v = sum llrint(ldexp(p, s_v)).  This function returns
- * the partial integer sums I_v over the local candidates and s_v (R13).
- * occ_v = number of literal occurrences of v; gmax = max |g_n[r]| over all
- * candidates and r in [rmin_n, K]; thmax = max |theta| over the batch.
- * G holds the fp32-rounded variable gradient (R27), so p = G theta is exact. */
+ * J_v = sum_m G_vm theta_vm.  J_v is summed in int64 fixed point (R13):
+ * s_v = 61 - ceil(log2(N occ_v gmax thmax)) (a global bound on |sum|),
+ * clamped to [-126, 127] so 2^s_v is an fp32; each term is the fp32 product
+ * p = G * (theta * 2^s_v) (the paper's arithmetic is fp32; theta * 2^s_v is
+ * exact) rounded to the nearest integer, I_v = sum llrintf(p).  The integer
+ * sum makes J_v independent of summation order and of the candidate sharding.
+ * This function returns the partial sums I_v over the local candidates and
+ * s_v.  occ_v = number of literal occurrences of v; gmax = max |g_n[r]| over
+ * all candidates and r in [rmin_n, K]; thmax = max |theta| over the batch.
+ * G holds the fp32 variable gradient (R27). */
 void or_jacobian_partial(int V, int Nl, const double* G, const float* theta,
                          const int32_t* occ, int64_t N, double gmax, float thmax,
                          int64_t* I, int32_t* s_out, uint8_t* valid)
@@ -295,10 +298,14 @@ void or_jacobian_partial(int V, int Nl, const double* G, const float* theta,
         I[v] = 0; s_out[v] = 0; valid[v] = 0;
         if (occ[v] == 0 || !(x > 0.0)) continue;
         int s = 61 - ceil_log2(x);
+        if (s > 127) s = 127;
+        if (s < -126) s = -126;
+        const float p2 = ldexpf(1.0f, s);
         int64_t acc = 0;
         for (int j = 0; j < Nl; ++j) {
-            double p = G[(size_t)v * Nl + j] * (double)theta[(size_t)v * Nl + j];
-            acc += (int64_t)llrint(ldexp(p, s));
+            float ts = theta[(size_t)v * Nl + j] * p2;
+            float p = (float)G[(size_t)v * Nl + j] * ts;
+            acc += (int64_t)llrintf(p);
         }
         I[v] = acc; s_out[v] = s; valid[v] = 1;
     }
@@ -319,13 +326,15 @@ void or_jacobian_finish(int V, int64_t N, const int64_t* I, const int32_t* s, co
     }
 }
 
-/* grad_vn = (float)(G_vn rho_v - c_v), the fp64 product and difference as one
- * fused multiply-add (R27b). */
+/* grad_vn = G_vn rho_v - c_v in fp32 (the paper's precision): one fused
+ * multiply-add of the fp32 G with the row scalars rounded to fp32 (R27b). */
 void or_grad(int V, int Nl, const double* G, const double* rho, const double* cv, float* grad)
 {
-    for (int v = 0; v < V; ++v)
+    for (int v = 0; v < V; ++v) {
+        const float rf = (float)rho[v], cf = (float)cv[v];
         for (int j = 0; j < Nl; ++j)
-            grad[(size_t)v * Nl + j] = (float)fma(G[(size_t)v * Nl + j], rho[v], -cv[v]);
+            grad[(size_t)v * Nl + j] = fmaf((float)G[(size_t)v * Nl + j], rf, -cf);
+    }
 }
 
 /* (a9) LR schedule, §4.1 l.255-259: lr0 = 1e-1, /10 every 30

@@ -64,6 +64,29 @@ __device__ __forceinline__ int ceil_log2(double x) {
     return (f == 0.5) ? e - 1 : e;
 }
 
+// R13 fixed-point scale of J_v: s = 61 - ceil(log2(N occ gmax thmax)),
+// clamped to the fp32 exponent range [-126, 127]; p2 = 2^s as fp32.
+// Returns false (J_v = 0) when the row has no occurrences or x = 0.
+__device__ __forceinline__ bool jscale(long long Nglobal, int occ, double gmax, float thmax, int* s, float* p2) {
+    double x = (double)Nglobal * (double)occ;
+    x = x * gmax;
+    x = x * (double)thmax;
+    *s = 0;
+    *p2 = 1.0f;
+    if (!(occ > 0 && x > 0.0)) return false;
+    int e = 61 - ceil_log2(x);
+    e = e > 127 ? 127 : (e < -126 ? -126 : e);
+    *s = e;
+    *p2 = __uint_as_float((uint32_t)(127 + e) << 23);
+    return true;
+}
+
+// One term of J_v's fixed-point sum (R13): llrintf(G (x) (theta (x) 2^s)),
+// both products fp32 round-to-nearest-even.
+__device__ __forceinline__ long long jterm(float G, float th, float p2) {
+    return __float2ll_rn(__fmul_rn(G, __fmul_rn(th, p2)));
+}
+
 // Eq. 5 row statistics from the exact fixed-point row sum Q (R3, R10).
 __device__ __forceinline__ void row_finish(long long Q, const MethodConsts& mc, double* d, double* rho,
                                            unsigned char* guard) {

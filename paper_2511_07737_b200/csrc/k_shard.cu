@@ -43,14 +43,9 @@ __global__ void __launch_bounds__(256) k_update_b(StepArgs a, const uint32_t* __
     const float thmax = __uint_as_float(a.ds->thmax_bits[t & 1]);
     const int2 pn = a.occ_pn[v];
     const int occ = pn.x + pn.y;
-    int s = 0;
-    bool jvalid = false;
-    {
-        double x = (double)mc.Nglobal * (double)occ;
-        x = x * gmax;
-        x = x * (double)thmax;
-        if (occ > 0 && x > 0.0) { jvalid = true; s = 61 - ceil_log2(x); }
-    }
+    int s;
+    float p2;
+    const bool jvalid = jscale(mc.Nglobal, occ, gmax, thmax, &s, &p2);
     const double rho = a.rowRho[v];
     double c = 0.0;
     if (mc.normalize && !a.rowGuard[v]) {
@@ -59,6 +54,7 @@ __global__ void __launch_bounds__(256) k_update_b(StepArgs a, const uint32_t* __
         c = c * rho;
         c = c * rho;
     }
+    const float rhof = __double2float_rn(rho), ncf = -__double2float_rn(c);     // R27b: fp32 operands
     const float wdf = sc->wdf, a1 = sc->a1, b2f = sc->b2f, a2 = sc->a2, nss = sc->nss, rbc2 = sc->rbc2,
                 epsf = sc->epsf, nz = sc->nz;
     float* trow = a.theta + (size_t)v * N;
@@ -82,7 +78,7 @@ __global__ void __launch_bounds__(256) k_update_b(StepArgs a, const uint32_t* __
             const float G[4] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const float g = (float)__fma_rn((double)G[q], rho, -c);     // R27b
+                const float g = __fmaf_rn(G[q], rhof, ncf);                 // R27b
                 float x = th[q] * wdf;
                 const float mn = __fmaf_rn(a1, g - mm[q], mm[q]);
                 const float vb = vv[q] * b2f;

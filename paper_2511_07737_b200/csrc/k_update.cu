@@ -106,10 +106,8 @@ __device__ __forceinline__ float fold_ints(const int* hubrow, int N, int n, int 
 template <int KB, bool HUB>
 __device__ __forceinline__ long long pass_fold(const float* __restrict__ trow, uint32_t* dpk, size_t dpkw,
                                                const float* gs, int* hubrow, int N, int GT, int tg, int dsum,
-                                               bool jvalid, int s, float* __restrict__ gout) {
+                                               bool jvalid, float p2, float* __restrict__ gout) {
     const float dsumf = (float)dsum;
-    const bool j32 = jvalid && s >= 0 && s <= 100;                 // theta 2^s exact in fp32
-    const float sc32 = j32 ? __uint_as_float((uint32_t)(127 + s) << 23) : 0.0f;
     long long I = 0;
     float4 th_nx = (4 * tg < N) ? *reinterpret_cast<const float4*>(trow + 4 * tg) : make_float4(0.f, 0.f, 0.f, 0.f);
     for (int n = 4 * tg; n < N; n += 4 * GT) {
@@ -150,8 +148,7 @@ __device__ __forceinline__ long long pass_fold(const float* __restrict__ trow, u
         for (int q = 0; q < 4; ++q) {
             const float G = Gq[q];
             dp[q] = __float_as_uint(G);
-            if (j32) I += __double2ll_rn((double)G * (double)(th[q] * sc32));
-            else if (jvalid) I += __double2ll_rn(times_pow2((double)G * (double)th[q], s));
+            if (jvalid) I += jterm(G, th[q], p2);
         }
         if (gout) *reinterpret_cast<float4*>(gout + n) = make_float4(Gq[0], Gq[1], Gq[2], Gq[3]);
         if (HUB) {
@@ -261,14 +258,9 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
         const double rho = a.rowRho[v];
         const unsigned char guard = a.rowGuard[v];
         const int occ = pn.x + pn.y;
-        int s = 0;
-        bool jvalid = false;
-        {
-            double x = (double)mc.Nglobal * (double)occ;
-            x = x * gmax;
-            x = x * (double)thmax;
-            if (occ > 0 && x > 0.0) { jvalid = true; s = 61 - ceil_log2(x); }
-        }
+        int s;
+        float p2;
+        const bool jvalid = jscale(mc.Nglobal, occ, gmax, thmax, &s, &p2);
         int* hubrow = hub >= 0 ? a.hubD + (size_t)hub * NCTR * N : nullptr;
         float* trow = a.theta + (size_t)v * N;
         float* mrow = a.m + (size_t)v * N;
@@ -304,8 +296,8 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
 
         // ---- 3a: G (fp32 FMA chain over exact counts, R27) -> smem; J_v partial
         float* gout = MODE == 1 ? a.Gbuf + (size_t)v * N : nullptr;
-        long long I = hub >= 0 ? pass_fold<KB, true>(trow, dpk, dpkw, gs, hubrow, N, GT, tg, dsum, jvalid, s, gout)
-                               : pass_fold<KB, false>(trow, dpk, dpkw, gs, hubrow, N, GT, tg, dsum, jvalid, s, gout);
+        long long I = hub >= 0 ? pass_fold<KB, true>(trow, dpk, dpkw, gs, hubrow, N, GT, tg, dsum, jvalid, p2, gout)
+                               : pass_fold<KB, false>(trow, dpk, dpkw, gs, hubrow, N, GT, tg, dsum, jvalid, p2, gout);
         I = warp_sum(I);
         if (lane == 0) red[gw] = I;
         gsync(bar, GT);
@@ -333,6 +325,7 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
             c = c * rho;
             c = c * rho;
         }
+        const float rhof = __double2float_rn(rho), ncf = -__double2float_rn(c);     // R27b: fp32 operands
 
         // ---- 3b: grad, AdamW, next-state statistics and sign planes
         long long Qn = 0;
@@ -360,7 +353,7 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
                 const uint32_t* dp = dpk + n + (n >> 5);
                 float gg[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) gg[q] = (float)__fma_rn((double)__uint_as_float(dp[q]), rho, -c);   // R27b
+                for (int q = 0; q < 4; ++q) gg[q] = __fmaf_rn(__uint_as_float(dp[q]), rhof, ncf);   // R27b
                 // AdamW on candidate pairs: packed fp32x2 ops are per-lane
                 // correctly rounded, i.e. the same canonical ops (R6-R6c)
 #pragma unroll
@@ -515,14 +508,9 @@ __global__ void __launch_bounds__(256) k_update_rowcta(StepArgs a, const uint32_
     const unsigned char guard = a.rowGuard[v];
     const double gmax = __longlong_as_double((long long)a.ds->gmax_bits);
     const float thmax = __uint_as_float(a.ds->thmax_bits[t & 1]);
-    int s = 0;
-    bool jvalid = false;
-    {
-        double x = (double)mc.Nglobal * (double)occ;
-        x = x * gmax;
-        x = x * (double)thmax;
-        if (occ > 0 && x > 0.0) { jvalid = true; s = 61 - ceil_log2(x); }
-    }
+    int s;
+    float p2;
+    const bool jvalid = jscale(mc.Nglobal, (int)occ, gmax, thmax, &s, &p2);
     const uint32_t* Arow = Acur + (size_t)v * NW;
     float* trow = a.theta + (size_t)v * N;
     float* mrow = a.m + (size_t)v * N;
@@ -551,7 +539,7 @@ __global__ void __launch_bounds__(256) k_update_rowcta(StepArgs a, const uint32_
 #pragma unroll
         for (int r = 0; r < KB; ++r) G = __fmaf_rn((float)cnt[r], a.gtab[(size_t)r * N + n], G);
         Gs[n] = (double)G;
-        if (jvalid) I += __double2ll_rn(scalbn(Gs[n] * (double)trow[n], s));
+        if (jvalid) I += jterm(G, trow[n], p2);
     }
     float dummy = 0.0f;
     block_sum_max(I, dummy, sh_s, sh_m);
@@ -567,10 +555,11 @@ __global__ void __launch_bounds__(256) k_update_rowcta(StepArgs a, const uint32_
     }
     __syncthreads();
     const double c = sh_c;
+    const float rhof = __double2float_rn(rho), ncf = -__double2float_rn(c);
     long long Qn = 0;
     float mx = 0.0f;
     for (int n = threadIdx.x; n < N; n += blockDim.x) {
-        const float g = (float)__fma_rn(Gs[n], rho, -c);                 // R27b
+        const float g = __fmaf_rn((float)Gs[n], rhof, ncf);              // R27b
         float th = trow[n] * sc->wdf;
         const float m0 = mrow[n];
         const float mm = __fmaf_rn(sc->a1, g - m0, m0);
