@@ -13,7 +13,7 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libturbosat.so")
+LIB_PATH = os.environ.get("TSAT_LIB") or os.path.join(HERE, "libturbosat.so")
 
 TSAT_STATUS = {
     0: "TSAT_OK", 1: "TSAT_E_ARG", 2: "TSAT_E_PARSE", 3: "TSAT_E_RANGE", 4: "TSAT_E_STATE",

@@ -304,4 +304,70 @@ __device__ __forceinline__ void count_occurrences(uint32_t (&cnt)[NCTR][B], RecF
     }
 }
 
+// count_occurrences for uniform 3-SAT rows (3-word records: header + two
+// literal codes), nneg negated records first, then npos positive ones.  Each
+// sign section is cut into batches of 4 records (the last one masked), so
+// every batch is one carry-save sum4 + one 3-bit counter update, and the next
+// batch's 8 gathers are issued before the current batch is counted: a row
+// costs ~ceil(nneg/4) + ceil(npos/4) overlapped L2 round trips instead of one
+// per leftover record.
+template <int NCTR, int B, bool PIPE, typename RecFn>
+__device__ __forceinline__ void count_uni3(uint32_t (&cnt)[NCTR][B], RecFn rec, unsigned nneg, unsigned npos,
+                                           uint32_t own, const uint32_t* __restrict__ Acur, unsigned NW, unsigned w) {
+#pragma unroll
+    for (int r = 0; r < NCTR; ++r)
+#pragma unroll
+        for (int b = 0; b < B; ++b) cnt[r][b] = 0u;
+    const unsigned nbn = (nneg + 3) >> 2, nb = nbn + ((npos + 3) >> 2);
+    if (nb == 0) return;
+    const unsigned nrec = nneg + npos;
+    auto ld = [&](uint32_t code) { return __ldg(Acur + ((code >> 1) * NW + w)) ^ (0u - (code & 1u)); };
+    // batch b: records [first, first + count), all of one sign
+    auto batch = [&](unsigned b, unsigned& first, unsigned& count) {
+        if (b < nbn) { first = 4 * b; count = min(4u, nneg - 4 * b); }
+        else { first = nneg + 4 * (b - nbn); count = min(4u, nrec - first); }
+    };
+    uint32_t xn[4][2];
+    auto load = [&](unsigned b) {
+        unsigned first, count;
+        batch(b, first, count);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const unsigned i = 3 * (first + min((unsigned)k, count - 1));   // masked lanes re-read a valid record
+            xn[k][0] = ld(rec(i + 1));
+            xn[k][1] = ld(rec(i + 2));
+        }
+    };
+    if (PIPE) load(0);
+    for (unsigned b = 0; b < nb; ++b) {
+        uint32_t x[4][2];
+        if (!PIPE) load(b);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { x[k][0] = xn[k][0]; x[k][1] = xn[k][1]; }
+        if (PIPE && b + 1 < nb) load(b + 1);
+        unsigned first, count;
+        batch(b, first, count);
+        const bool neg = b < nbn;
+        const uint32_t os = neg ? ~own : own;               // own literal's value in this section
+        uint32_t p0[4], p1[4], mk[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            p0[k] = os ^ x[k][0] ^ x[k][1];                 // 2-plane count of true literals
+            p1[k] = (os & x[k][0]) | (x[k][1] & (os ^ x[k][0]));
+            mk[k] = (unsigned)k < count ? 0xffffffffu : 0u;
+        }
+#pragma unroll
+        for (int r = 0; r < NCTR; ++r) {
+            uint32_t e[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                e[k] = ((r & 1) ? p0[k] : ~p0[k]) & ((r & 2) ? p1[k] : ~p1[k]) & mk[k];
+            uint32_t s0, s1, s2;
+            sum4(e[0], e[1], e[2], e[3], s0, s1, s2);
+            if (neg) vc_add3<B>(cnt[r], s0, s1, s2);
+            else vc_sub3<B>(cnt[r], s0, s1, s2);
+        }
+    }
+}
+
 }  // namespace tsat

@@ -20,6 +20,13 @@
 // exact int32 counts (integer atomics: order-free, deterministic).
 #include "device_common.cuh"
 
+#ifndef TSAT_UNI3
+#define TSAT_UNI3 2
+#endif
+#ifndef TSAT_UPD_THREADS4
+#define TSAT_UPD_THREADS4 768       // KB = 4 block size bound (register budget)
+#endif
+
 namespace tsat {
 
 namespace {
@@ -194,7 +201,7 @@ __device__ __forceinline__ void gsync(int bar, int GT) {
 // and the tail stay balanced); tg 0 fetches the next row at the start of the
 // current one into a parity-double-buffered slot, read after the J barrier.
 template <int KB, int MODE>
-__global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
+__global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
                                                                     uint32_t* __restrict__ Anext,
                                                                     const StepScalars* __restrict__ sc) {
     constexpr int NP = (KB == 4) ? 2 : 3;
@@ -275,7 +282,14 @@ __global__ void __launch_bounds__(KB == 4 ? 768 : 512, 1) k_update(StepArgs a, c
                 auto recf = [&](unsigned i) { return rb_cur[i]; };
                 // KB = 8 rows are short (hub rows go to k_hub) and the kernel is
                 // I-cache bound there: count one record at a time
-                if (uni3) count_occurrences<NP, NCTR, kCtr, true, true>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w);
+                if (uni3) {
+#if TSAT_UNI3 == 0
+                    count_occurrences<NP, NCTR, kCtr, true, true>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w);
+#else
+                    count_uni3<NCTR, kCtr, TSAT_UNI3 == 1>(cnt, recf, (unsigned)pn.y, (unsigned)pn.x, own, Acur,
+                                                          (unsigned)NW, (unsigned)w);
+#endif
+                }
                 else count_occurrences<NP, NCTR, kCtr, false, KB == 4>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w);
                 uint32_t T[32];
 #pragma unroll
@@ -617,7 +631,7 @@ cudaError_t configure_update(StepArgs* a) {
     const int GT = NW >= 128 ? 128 : (NW > 32 ? 64 : 32);
     const size_t gsb = upd_gs_bytes(KB, N), grb = upd_group_bytes(KB, N, a->upd_rec_cap);
     long long ng = optin > (long long)gsb ? ((long long)optin - (long long)gsb) / (long long)grb : 0;
-    const int max_threads = KB == 4 ? 768 : 512;   // register budget (launch bounds)
+    const int max_threads = KB == 4 ? TSAT_UPD_THREADS4 : 512;   // register budget (launch bounds)
     ng = ng < max_threads / GT ? ng : max_threads / GT;
     if (GT > 32) ng = ng < 15 ? ng : 15;          // named barriers 1..15 (warp groups use __syncwarp)
     if (ng < 2 && !(ng == 1 && GT == 128)) {
