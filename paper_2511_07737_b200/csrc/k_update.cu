@@ -23,6 +23,10 @@
 #ifndef TSAT_UNI3
 #define TSAT_UNI3 2
 #endif
+#ifndef TSAT_3B_UNROLL
+#define TSAT_3B_UNROLL 2
+#endif
+constexpr int kUnroll3b = TSAT_3B_UNROLL;
 #ifndef TSAT_UPD_THREADS4
 #define TSAT_UPD_THREADS4 768       // KB = 4 block size bound (register budget)
 #endif
@@ -351,6 +355,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
             mn4 = *reinterpret_cast<const float4*>(mrow + 4 * tg);
             vn4 = *reinterpret_cast<const float4*>(vrow + 4 * tg);
         }
+#pragma unroll kUnroll3b
         for (int base = 0; base < N; base += 4 * GT) {
             const int n = base + 4 * tg;
             unsigned pnib = 0, nnib = 0;
