@@ -107,8 +107,8 @@ Layout make_layout(int V, int N, int KB, int n_hubs, bool sharded) {
     L.theta = take(VN * 4);
     L.m = take(VN * 4);
     L.v = take(VN * 4);
-    L.A0 = take((size_t)V * NW * 4);
-    L.A1 = take((size_t)V * NW * 4);
+    L.A0 = take((size_t)(V + 1) * NW * 4);            // + row V: all-zero padding row (k_clause)
+    L.A1 = take((size_t)(V + 1) * NW * 4);
     L.hist = take((size_t)N * KB * 4);
     L.gtab = take((size_t)N * KB * 4);
     L.S = take((size_t)N * 8);
@@ -630,6 +630,11 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
         CK(cudaMemsetAsync(ctx->ws + ctx->L.hubD, 0, ctx->L.total - ctx->L.hubD, ctx->stream));
     CK(cudaMemsetAsync(ctx->ws + ctx->L.hist, 0, (size_t)ctx->N * ctx->KB * 4, ctx->stream));
     CK(cudaMemsetAsync(ctx->ws + ctx->L.scal, 0, sizeof(DevScalars), ctx->stream));
+    {
+        const size_t rowb = (size_t)(ctx->N / 32) * 4, zoff = (size_t)ctx->cnf.V * rowb;
+        CK(cudaMemsetAsync(ctx->ws + ctx->L.A0 + zoff, 0, rowb, ctx->stream));
+        CK(cudaMemsetAsync(ctx->ws + ctx->L.A1 + zoff, 0, rowb, ctx->stream));
+    }
     DevScalars init{};
     init.best_key = ~0ull;
     init.sol_step = -1;

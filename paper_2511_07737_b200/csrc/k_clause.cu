@@ -18,7 +18,9 @@ namespace tsat {
 
 namespace {
 constexpr int kWarps = 8;
-constexpr int kCH = 64;        // clauses per warp chunk (<= 127: 7-bit counters)
+// clauses per warp chunk (<= 127: 7-bit counters); K = 7 halves it to keep
+// the staged literals within the 48 KB static shared memory
+__host__ __device__ constexpr int chunk_clauses(int kmaxc) { return kmaxc > 3 ? 32 : 64; }
 constexpr int kUnr = 4;        // clauses evaluated together (carry-save group)
 constexpr uint32_t kNone = 0xffffffffu;
 
@@ -46,7 +48,7 @@ __device__ __forceinline__ void csa_add4(uint32_t (&c)[CB], uint32_t m0, uint32_
 }
 
 template <int KB, int KMAXC>
-__global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t* __restrict__ A, int NW,
+__global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t* __restrict__ A, int NW, int V,
                                                                 const uint32_t* __restrict__ cptr,
                                                                 const uint32_t* __restrict__ clit, long long C,
                                                                 int* __restrict__ hist, int N, int uniform,
@@ -55,7 +57,10 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t*
     constexpr int NP = (KB == 4) ? 2 : 3;
     constexpr int CB = 7;
     __shared__ int sh[(KB - 1) * 1024];
-    __shared__ uint32_t soff[kWarps][kCH * KMAXC];     // (var * NW) << 1 | negated, or kNone
+    // staged literals: {element offset var * NW, sign mask}; empty slots and
+    // padding clauses read the all-zero row V with mask 0 (literal false)
+    __shared__ uint2 soff[kWarps][chunk_clauses(KMAXC) * KMAXC];
+    constexpr int kCH = chunk_clauses(KMAXC);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int w = blockIdx.x * 32 + lane;
     const bool valid = w < NW;
@@ -70,9 +75,10 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t*
     }
     for (int i = threadIdx.x; i < (KB - 1) * 1024; i += blockDim.x) sh[i] = 0;
     __syncthreads();
-    uint32_t* my = soff[warp];
+    uint2* my = soff[warp];
     const uint32_t unw = (uint32_t)NW;
-    const uint32_t* Aw = A + (valid ? w : 0);
+    const uint2 zero_lit = make_uint2((uint32_t)V * unw, 0u);
+    const uint32_t* Aw = A + (valid ? w : 0);          // lanes past NW read a valid word, results unused
     const long long nchunks = (C + kCH - 1) / kCH;
     // grid-sized: warps stride over the clause chunks of this word block
     for (long long chunk = (long long)blockIdx.y * kWarps + warp; chunk < nchunks;
@@ -85,17 +91,17 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t*
             const uint32_t* src = clit + (size_t)c0 * KMAXC;
             for (int i = lane; i < kCH * KMAXC; i += 32) {
                 const uint32_t code = (i < nc * KMAXC) ? src[i] : kNone;
-                my[i] = code == kNone ? kNone : (((code >> 1) * unw) << 1) | (code & 1u);
+                my[i] = code == kNone ? zero_lit : make_uint2((code >> 1) * unw, 0u - (code & 1u));
             }
         } else {
             for (int i = lane; i < kCH * KMAXC; i += 32) {
                 const int c = i / KMAXC, l = i - c * KMAXC;
-                uint32_t o = kNone;
+                uint2 o = zero_lit;
                 if (c < nc) {
                     const uint32_t b = cptr[c0 + c], e = cptr[c0 + c + 1];
                     if (b + l < e) {
                         const uint32_t code = clit[b + l];
-                        o = (((code >> 1) * unw) << 1) | (code & 1u);
+                        o = make_uint2((code >> 1) * unw, 0u - (code & 1u));
                     }
                 }
                 my[i] = o;
@@ -116,11 +122,9 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t*
                 for (int u = 0; u < kUnr; ++u)
 #pragma unroll
                     for (int l = 0; l < KMAXC; ++l) {
-                        const int c = cb0 + gq * kUnr + u;
-                        const uint32_t o = (c < nc) ? my[c * KMAXC + l] : kNone;
-                        uint32_t val = 0u;
-                        if (o != kNone && valid) val = __ldg(Aw + (o >> 1)) ^ (0u - (o & 1u));
-                        xx[gq][u][l] = val;
+                        const int c = cb0 + gq * kUnr + u;      // < kCH: the chunk is padded
+                        const uint2 o = my[c * KMAXC + l];
+                        xx[gq][u][l] = __ldg(Aw + o.x) ^ o.y;
                     }
 #pragma unroll
           for (int gq = 0; gq < kG; ++gq) {
@@ -223,6 +227,7 @@ cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, const StepSca
     }
     const int NW = a.N >> 5;
     const int nwb = (NW + 31) / 32;
+    const int kCH = chunk_clauses(a.mc.K <= 3 ? 3 : 7);
     const long long nchunks = (a.C + kCH - 1) / kCH;
     const long long ctas_needed = (nchunks + kWarps - 1) / kWarps;
     const int K = a.mc.K;
@@ -237,11 +242,11 @@ cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, const StepSca
     dim3 grid(nwb, (unsigned)gy);
     const int uni = a.uniform_len;
     if (K <= 2)
-        k_clause<4, 2><<<grid, 256, 0, st>>>(Acur, NW, a.cptr, a.clit, a.C, a.hist, a.N, uni && K == 2, a.ds, sc);
+        k_clause<4, 2><<<grid, 256, 0, st>>>(Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist, a.N, uni && K == 2, a.ds, sc);
     else if (K == 3)
-        k_clause<4, 3><<<grid, 256, 0, st>>>(Acur, NW, a.cptr, a.clit, a.C, a.hist, a.N, uni, a.ds, sc);
+        k_clause<4, 3><<<grid, 256, 0, st>>>(Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist, a.N, uni, a.ds, sc);
     else
-        k_clause<8, 7><<<grid, 256, 0, st>>>(Acur, NW, a.cptr, a.clit, a.C, a.hist, a.N, uni && K == 7, a.ds, sc);
+        k_clause<8, 7><<<grid, 256, 0, st>>>(Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist, a.N, uni && K == 7, a.ds, sc);
     return cudaGetLastError();
 }
 
