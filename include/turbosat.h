@@ -61,7 +61,8 @@ typedef enum {
  * (reading R6); tau = 1 (R1); Eq. 5 normalisation on, over all N (R20). */
 typedef struct {
     double  tau;             /* SmoothMin temperature, Eq. 4 (> 0) */
-    int32_t normalize;       /* 1 = Eq. 5 over all N candidates; 0 = off (variant) */
+    int32_t normalize;       /* 1 = Eq. 5 over all N candidates; 0 = off; 2 = per shard: each GPU averages
+                                over its own N/W candidates and keeps J local (variants) */
     double  beta1, beta2;    /* AdamW moments (0.9, 0.999) */
     double  eps;             /* AdamW eps (1e-8) */
     double  weight_decay;    /* AdamW decoupled weight decay (1e-2) */
@@ -72,6 +73,9 @@ typedef struct {
     int32_t restart_every;   /* iterations per LR restart (360) */
     double  noise_sigma;     /* optional Philox noise in the update (0 = paper-exact, R17) */
     double  eps_norm;        /* Eq. 5 guard: |mean| <= eps_norm -> divide by +-eps_norm (1e-8) */
+    int32_t reset_moments_on_restart;  /* 1 = re-create AdamW at each LR restart (t > 0, t % restart_every
+                                          == 0): m = v = 0 and the bias-correction step restarts at 1
+                                          (variant; 0 = paper default, R8) */
 } tsat_config;
 
 typedef struct {

@@ -67,7 +67,7 @@ def lib():
             "or_jacobian_finish": (None, [i32, i64, P, P, P, P, P, i32, P, P]),
             "or_grad": (None, [i32, i32, P, P, P, P]),
             "or_lr_at": (f64, [i64, f64, f64, i32, i32, f64]),
-            "or_adamw": (None, [i32, i64, i32, P, P, P, P, i64, f64, f64, f64, f64, f64, f64, u64]),
+            "or_adamw": (None, [i32, i64, i32, P, P, P, P, i64, i64, f64, f64, f64, f64, f64, f64, u64]),
             "or_abs_max": (f32, [ct.c_size_t, P]),
             "or_gmax": (f64, [i32, i32, P, P]),
             "or_hist_stream": (None, [i32, P, P, i32, i32, P, P, P]),
@@ -105,6 +105,16 @@ def init_theta(V, N, seed, n0=0, Nl=None):
 
 def lr_at(t, cfg):
     return lib().or_lr_at(t, cfg.lr0, cfg.decay_factor, cfg.decay_every, cfg.restart_every, cfg.lr_min)
+
+
+def adam_step(t, cfg):
+    """(moments reset at t?, bias-correction step).  Variant:
+    with reset_moments_on_restart the AdamW optimiser is re-created at every
+    LR restart (t > 0, t mod restart_every = 0), as a fresh torch.optim.AdamW
+    would be: m = v = 0 and its step count starts again at 1."""
+    if not cfg.reset_moments_on_restart:
+        return False, t + 1
+    return (t > 0 and t % cfg.restart_every == 0), t % cfg.restart_every + 1
 
 
 def clause_eval(cnf, b):
@@ -189,6 +199,7 @@ class Config:
     restart_every: int = 360
     noise_sigma: float = 0.0
     eps_norm: float = 1e-8
+    reset_moments_on_restart: int = 0
 
 
 class LocalComm:
@@ -269,6 +280,18 @@ class Oracle:
             self.theta, self.m, self.v = init_theta(cnf.V, self.N, self.seed, self.n0, self.Nl)
         self.comm = LocalComm()
 
+    @property
+    def per_shard(self):
+        """normalize = 2 (variant f2): Eq. 5 over this shard's Nl candidates
+        only; row sums, J and the J scale's maxima stay local, only the
+        selection and the loss are global (each shard is an independent
+        instance)."""
+        return self.cfg.normalize == 2
+
+    @property
+    def Nnorm(self):
+        return self.Nl if self.per_shard else self.N
+
     def set_state(self, theta, m, v, t):
         self.theta = np.ascontiguousarray(theta, np.float32).copy()
         self.m = np.ascontiguousarray(m, np.float32).copy()
@@ -280,11 +303,13 @@ class Oracle:
         Q = np.empty(V, np.int64)
         L = lib()
         L.or_row_sums(V, self.Nl, _p(self.theta), _p(Q))
-        Q = self.comm.sum_i64(Q)
+        if not self.per_shard:
+            Q = self.comm.sum_i64(Q)
         thmax_local = float(np.abs(self.theta).max()) if self.theta.size else 0.0
         assert self.N * thmax_local < 2.0 ** 30, "row-sum fixed-point bound (R10)"
         mu = np.empty(V); d = np.empty(V); rho = np.empty(V); guard = np.empty(V, np.uint8)
-        L.or_row_finish(V, self.N, _p(Q), self.cfg.normalize, self.cfg.eps_norm, _p(mu), _p(d), _p(rho), _p(guard))
+        L.or_row_finish(V, self.Nnorm, _p(Q), self.cfg.normalize, self.cfg.eps_norm, _p(mu), _p(d), _p(rho),
+                        _p(guard))
         return Q, mu, d, rho, guard
 
     def step(self) -> StepOut:
@@ -304,15 +329,20 @@ class Oracle:
         g32 = g.astype(np.float32)                 # R26: rounded once to fp32
         Sall = self.comm.gather_f64(S)
         loss = -float(sum(float(x) for x in Sall))
-        gmax = self.comm.max(L.or_gmax(Nl, K, _p(g32), _p(rmin)))
-        thmax = self.comm.max(L.or_abs_max(self.theta.size, _p(self.theta)))
+        gmax = L.or_gmax(Nl, K, _p(g32), _p(rmin))
+        thmax = L.or_abs_max(self.theta.size, _p(self.theta))
+        if not self.per_shard:
+            gmax, thmax = self.comm.max(gmax), self.comm.max(thmax)
         # STE backward and Eq. 5 Jacobian
         G = backward(cnf, R, g32)                     # fp32 values (R27)
         I = np.empty(V, np.int64); s = np.empty(V, np.int32); valid = np.empty(V, np.uint8)
-        L.or_jacobian_partial(V, Nl, _p(G), _p(self.theta), _p(self.occ), self.N, gmax, thmax, _p(I), _p(s), _p(valid))
-        I = self.comm.sum_i64(I)
+        L.or_jacobian_partial(V, Nl, _p(G), _p(self.theta), _p(self.occ), self.Nnorm, gmax, thmax, _p(I), _p(s),
+                              _p(valid))
+        if not self.per_shard:
+            I = self.comm.sum_i64(I)
         J = np.empty(V); cv = np.empty(V)
-        L.or_jacobian_finish(V, self.N, _p(I), _p(s), _p(valid), _p(rho), _p(guard), cfg.normalize, _p(J), _p(cv))
+        L.or_jacobian_finish(V, self.Nnorm, _p(I), _p(s), _p(valid), _p(rho), _p(guard), cfg.normalize, _p(J),
+                             _p(cv))
         grad = np.empty((V, Nl), np.float32)
         L.or_grad(V, Nl, _p(G), _p(rho), _p(cv), _p(grad))
         # selection (§4.2): best = argmin (unsat, n)
@@ -321,7 +351,11 @@ class Oracle:
         best_unsat, best_idx = self.comm.min_key(key)
         # AdamW + LR schedule (§4.1)
         lr = lr_at(t, cfg)
-        L.or_adamw(V, self.n0, Nl, _p(self.theta), _p(self.m), _p(self.v), _p(grad), t, lr,
+        reset, bstep = adam_step(t, cfg)
+        if reset:
+            self.m[:] = 0.0
+            self.v[:] = 0.0
+        L.or_adamw(V, self.n0, Nl, _p(self.theta), _p(self.m), _p(self.v), _p(grad), t, bstep, lr,
                    cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, cfg.noise_sigma, self.seed)
         self.t = t + 1
         return StepOut(t=t, bits=b, R=R, h=h, unsat=unsat, S=S, g=g, g32=g32, loss=loss, G=G, grad=grad,
@@ -375,6 +409,10 @@ def step_sampled(cnf, theta, m, v, t, rows, cfg: Config | None = None):
     lr = lr_at(t, cfg)
     # noise is keyed by the variable index: only sigma = 0 here
     assert cfg.noise_sigma == 0.0
-    L.or_adamw(nr, 0, N, _p(th), _p(mm), _p(vv), _p(grad), t, lr, cfg.beta1, cfg.beta2, cfg.eps,
+    reset, bstep = adam_step(t, cfg)
+    if reset:
+        mm[:] = 0.0
+        vv[:] = 0.0
+    L.or_adamw(nr, 0, N, _p(th), _p(mm), _p(vv), _p(grad), t, bstep, lr, cfg.beta1, cfg.beta2, cfg.eps,
                cfg.weight_decay, 0.0, 0)
     return h[:, 0].copy(), g32, S, loss, th, mm, vv

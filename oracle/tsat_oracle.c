@@ -355,7 +355,9 @@ double or_lr_at(int64_t t, double lr0, double factor, int decay_every, int resta
  * 531-547) with its CPU kernels' rounding (lerp and addcmul use one fused
  * multiply-add; R6b), except that v's bias correction multiplies by
  * the host-rounded 1/sqrt(1 - beta2^s) (R6c: the same AdamW, one division
- * fewer).  s = t + 1 is the bias-correction step.
+ * fewer).  s = bstep is the bias-correction step: t + 1, or (t mod restart) + 1
+ * when the moments are reset at each LR restart (variant, the caller zeroes
+ * m and v at those iterations).
  *   theta *= (float)(1 - lr wd)
  *   m      = fmaf(a1, g - m, m),           a1 = (float)(1 - beta1)
  *   v      = fmaf(a2 g, g, v beta2),       a2 = (float)(1 - beta2)
@@ -364,10 +366,10 @@ double or_lr_at(int64_t t, double lr0, double factor, int decay_every, int resta
  * Optional noise (R17, default sigma = 0): theta += (float)(lr sigma) xi,
  * xi = (x>>8) 2^-24 - 1/2, x = Philox(key=seed, ctr=(n>>2, v, 1+t, 0))[n&3]. */
 void or_adamw(int V, int64_t n0, int Nl, float* theta, float* m, float* vv, const float* grad,
-              int64_t t, double lr, double beta1, double beta2, double eps, double wd,
+              int64_t t, int64_t bstep, double lr, double beta1, double beta2, double eps, double wd,
               double noise_sigma, uint64_t seed)
 {
-    double s = (double)(t + 1);
+    double s = (double)bstep;
     float wdf = (float)(1.0 - lr * wd);
     float a1 = (float)(1.0 - beta1);
     float b2f = (float)beta2;

@@ -32,7 +32,7 @@ class tsat_config(ct.Structure):
     _fields_ = [("tau", ct.c_double), ("normalize", ct.c_int32), ("beta1", ct.c_double), ("beta2", ct.c_double),
                 ("eps", ct.c_double), ("weight_decay", ct.c_double), ("lr0", ct.c_double), ("lr_min", ct.c_double),
                 ("decay_factor", ct.c_double), ("decay_every", ct.c_int32), ("restart_every", ct.c_int32),
-                ("noise_sigma", ct.c_double), ("eps_norm", ct.c_double)]
+                ("noise_sigma", ct.c_double), ("eps_norm", ct.c_double), ("reset_moments_on_restart", ct.c_int32)]
 
 
 class tsat_cnf_info(ct.Structure):

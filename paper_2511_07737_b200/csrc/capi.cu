@@ -199,12 +199,15 @@ double lr_at(const tsat_config& c, int64_t t) {
 StepScalars step_scalars(const tsat_config& c, int64_t t) {
     StepScalars s{};
     double lr = lr_at(c, t);
-    double st = (double)(t + 1);
+    // AdamW bias-correction step; a moment reset re-creates the optimizer
+    const bool reset = c.reset_moments_on_restart && t > 0 && t % c.restart_every == 0;
+    double st = (double)((c.reset_moments_on_restart ? t % c.restart_every : t) + 1);
     s.t = t;
     s.lr = lr;
     s.wdf = (float)(1.0 - lr * c.weight_decay);
     s.a1 = (float)(1.0 - c.beta1);
-    s.b2f = (float)c.beta2;
+    s.b2f = reset ? 0.0f : (float)c.beta2;
+    s.mkeep = reset ? 0.0f : 1.0f;
     s.a2 = (float)(1.0 - c.beta2);
     double bc1 = 1.0 - std::pow(c.beta1, st);
     double bc2 = 1.0 - std::pow(c.beta2, st);
@@ -297,7 +300,7 @@ tsat_status state_stats(tsat_ctx ctx, const StepArgs& a, int64_t t) {
     } else {
         std::string err;
         CK(launch_rows_partial(a, a.theta, thm, ctx->stream));
-        if (comm_allreduce_sum_i64(ctx->comm, a.Qbuf, (size_t)a.V + 1, ctx->stream, &err)) {
+        if (ctx->cfg.normalize != 2 && comm_allreduce_sum_i64(ctx->comm, a.Qbuf, (size_t)a.V + 1, ctx->stream, &err)) {
             ctx->poisoned = TSAT_E_NCCL;
             ctx->err = err;
             return TSAT_E_NCCL;
@@ -330,13 +333,18 @@ int launch_segment(tsat_ctx ctx, const StepArgs& a, int seg, const StepScalars* 
             if ((r = ck(launch_step_kernel(1, a, sc, t, st), "k_gtable"))) return r;
             if ((r = ck(launch_shard_pack_max(a, sc, st), "k_pack_max"))) return r;
             if ((r = comm_allreduce_max_u64(ctx->comm, a.maxbuf, 3, st, err))) return r;
-            return ck(launch_shard_unpack_max(a, sc, st), "k_unpack_max");
+            return ck(launch_shard_unpack_max(a, sc, st, a.mc.normalize == 2), "k_unpack_max");
         case 2: return ck(launch_step_kernel(2, a, sc, t, st), "k_hub");
         case 3:
             if ((r = ck(launch_update_a(a, Acur, sc, st), "k_update(A)"))) return r;
-            if ((r = comm_allreduce_sum_i64(ctx->comm, a.Jbuf, (size_t)a.V, st, err))) return r;
+            // normalize 2 (per shard): J and the row sums stay local, only the loss slot is summed
+            if (a.mc.normalize != 2 && (r = comm_allreduce_sum_i64(ctx->comm, a.Jbuf, (size_t)a.V, st, err))) return r;
             if ((r = ck(launch_update_b(a, Acur, sc, st), "k_update_b"))) return r;
-            if ((r = comm_allreduce_sum_i64(ctx->comm, a.Qbuf, (size_t)a.V + 1, st, err))) return r;
+            if (a.mc.normalize == 2) {
+                if ((r = comm_allreduce_sum_i64(ctx->comm, a.Qbuf + a.V, 1, st, err))) return r;
+            } else if ((r = comm_allreduce_sum_i64(ctx->comm, a.Qbuf, (size_t)a.V + 1, st, err))) {
+                return r;
+            }
             return ck(launch_rows_finish(a, Anext, st), "k_rows_finish");
         case 4: return ck(launch_step_end_sharded(a, sc, st), "k_step_end");
     }
@@ -459,6 +467,7 @@ tsat_status tsat_config_default(tsat_config* out) {
     out->decay_every = 30;
     out->restart_every = 360;
     out->noise_sigma = 0.0;
+    out->reset_moments_on_restart = 0;
     out->eps_norm = 1e-8;
     return TSAT_OK;
 }
@@ -587,7 +596,8 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
     if ((uintptr_t)ws % 256) return fail(ctx, TSAT_E_ARG, "workspace must be 256-byte aligned");
     tsat_config c;
     if (cfg) c = *cfg; else tsat_config_default(&c);
-    if (!(c.tau > 0) || c.decay_every < 1 || c.restart_every < 1 || !(c.decay_factor > 0) || !(c.eps_norm > 0))
+    if (!(c.tau > 0) || c.decay_every < 1 || c.restart_every < 1 || !(c.decay_factor > 0) || !(c.eps_norm > 0) ||
+        c.normalize < 0 || c.normalize > 2 || (c.reset_moments_on_restart & ~1))
         return fail(ctx, TSAT_E_ARG, "invalid config");
     drop_graphs(ctx);
     ctx->cfg = c;
@@ -604,9 +614,9 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
     for (int d = 0; d < 8; ++d) mc.E[d] = std::exp(-c.tau * (double)d);
     mc.tau = c.tau;
     mc.eps_norm = c.eps_norm;
-    mc.normalize = c.normalize ? 1 : 0;
+    mc.normalize = c.normalize;                 // 0 off, 1 global, 2 per shard
     mc.K = ctx->cnf.K;
-    mc.Nglobal = N_global;
+    mc.Nnorm = c.normalize == 2 ? N_global / ctx->world : N_global;
     mc.n0 = ctx->n0;
     mc.seed = seed;
     mc.noise = c.noise_sigma != 0.0;

@@ -67,8 +67,8 @@ __device__ __forceinline__ int ceil_log2(double x) {
 // R13 fixed-point scale of J_v: s = 61 - ceil(log2(N occ gmax thmax)),
 // clamped to the fp32 exponent range [-126, 127]; p2 = 2^s as fp32.
 // Returns false (J_v = 0) when the row has no occurrences or x = 0.
-__device__ __forceinline__ bool jscale(long long Nglobal, int occ, double gmax, float thmax, int* s, float* p2) {
-    double x = (double)Nglobal * (double)occ;
+__device__ __forceinline__ bool jscale(long long Nnorm, int occ, double gmax, float thmax, int* s, float* p2) {
+    double x = (double)Nnorm * (double)occ;
     x = x * gmax;
     x = x * (double)thmax;
     *s = 0;
@@ -91,7 +91,7 @@ __device__ __forceinline__ long long jterm(float G, float th, float p2) {
 __device__ __forceinline__ void row_finish(long long Q, const MethodConsts& mc, double* d, double* rho,
                                            unsigned char* guard) {
     if (!mc.normalize) { *d = 1.0; *rho = 1.0; *guard = 1; return; }
-    double mu = ((double)Q * 2.3283064365386963e-10) / (double)mc.Nglobal;
+    double mu = ((double)Q * 2.3283064365386963e-10) / (double)mc.Nnorm;
     double a = fabs(mu);
     double mag = a > mc.eps_norm ? a : mc.eps_norm;
     double dd = mu >= 0.0 ? mag : -mag;

@@ -20,10 +20,12 @@ __global__ void k_pack_max(DevScalars* __restrict__ ds, const StepScalars* __res
     buf[2] = ds->thmax_bits[t & 1];
 }
 
+// key_only (normalize 2, per shard): gmax and max|theta| of J's scale stay local.
 __global__ void k_unpack_max(DevScalars* __restrict__ ds, const StepScalars* __restrict__ sc,
-                             const unsigned long long* __restrict__ buf) {
+                             const unsigned long long* __restrict__ buf, int key_only) {
     const long long t = sc->t;
     ds->best_key = ~buf[0];
+    if (key_only) return;
     ds->gmax_bits = buf[1];
     ds->thmax_bits[t & 1] = (unsigned int)buf[2];
 }
@@ -45,12 +47,12 @@ __global__ void __launch_bounds__(256) k_update_b(StepArgs a, const uint32_t* __
     const int occ = pn.x + pn.y;
     int s;
     float p2;
-    const bool jvalid = jscale(mc.Nglobal, occ, gmax, thmax, &s, &p2);
+    const bool jvalid = jscale(mc.Nnorm, occ, gmax, thmax, &s, &p2);
     const double rho = a.rowRho[v];
     double c = 0.0;
     if (mc.normalize && !a.rowGuard[v]) {
         const double J = jvalid ? scalbn((double)a.Jbuf[v], -s) : 0.0;
-        c = J / (double)mc.Nglobal;
+        c = J / (double)mc.Nnorm;
         c = c * rho;
         c = c * rho;
     }
@@ -80,7 +82,8 @@ __global__ void __launch_bounds__(256) k_update_b(StepArgs a, const uint32_t* __
             for (int q = 0; q < 4; ++q) {
                 const float g = __fmaf_rn(G[q], rhof, ncf);                 // R27b
                 float x = th[q] * wdf;
-                const float mn = __fmaf_rn(a1, g - mm[q], mm[q]);
+                const float m0 = mm[q] * sc->mkeep;
+                const float mn = __fmaf_rn(a1, g - m0, m0);
                 const float vb = vv[q] * b2f;
                 const float vn = __fmaf_rn(a2 * g, g, vb);
                 const float den = __fmul_rn(__fsqrt_rn(vn), rbc2) + epsf;
@@ -200,8 +203,8 @@ cudaError_t launch_shard_pack_max(const StepArgs& a, const StepScalars* sc, cuda
     k_pack_max<<<1, 1, 0, st>>>(a.ds, sc, a.maxbuf);
     return cudaGetLastError();
 }
-cudaError_t launch_shard_unpack_max(const StepArgs& a, const StepScalars* sc, cudaStream_t st) {
-    k_unpack_max<<<1, 1, 0, st>>>(a.ds, sc, a.maxbuf);
+cudaError_t launch_shard_unpack_max(const StepArgs& a, const StepScalars* sc, cudaStream_t st, bool key_only) {
+    k_unpack_max<<<1, 1, 0, st>>>(a.ds, sc, a.maxbuf, key_only ? 1 : 0);
     return cudaGetLastError();
 }
 cudaError_t launch_update_b(const StepArgs& a, const uint32_t* Acur, const StepScalars* sc, cudaStream_t st) {

@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
     const double gmax = __longlong_as_double((long long)a.ds->gmax_bits);
     const float thmax = __uint_as_float(a.ds->thmax_bits[t & 1]);
     const float wdf = sc->wdf, a1 = sc->a1, b2f = sc->b2f, a2 = sc->a2, nss = sc->nss, rbc2 = sc->rbc2,
-                epsf = sc->epsf, nz = sc->nz;
+                epsf = sc->epsf, nz = sc->nz, mkeep = sc->mkeep;
     const MethodConsts& mc = a.mc;
 
     int v = rowslot[1];
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
         const int occ = pn.x + pn.y;
         int s;
         float p2;
-        const bool jvalid = jscale(mc.Nglobal, occ, gmax, thmax, &s, &p2);
+        const bool jvalid = jscale(mc.Nnorm, occ, gmax, thmax, &s, &p2);
         int* hubrow = hub >= 0 ? a.hubD + (size_t)hub * NCTR * N : nullptr;
         float* trow = a.theta + (size_t)v * N;
         float* mrow = a.m + (size_t)v * N;
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
         double c = 0.0;
         if (mc.normalize && !guard) {
             const double J = jvalid ? times_pow2((double)Itot, -s) : 0.0;
-            c = J / (double)mc.Nglobal;
+            c = J / (double)mc.Nnorm;
             c = c * rho;
             c = c * rho;
         }
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const float2 g2 = make_float2(gg[2 * h], gg[2 * h + 1]);
-                    const float2 m2 = make_float2(mm[2 * h], mm[2 * h + 1]);
+                    const float2 m2 = mul2_unfused(make_float2(mm[2 * h], mm[2 * h + 1]), make_float2(mkeep, mkeep));
                     const float2 v2 = make_float2(vv[2 * h], vv[2 * h + 1]);
                     float2 x2 = mul2_unfused(make_float2(th[2 * h], th[2 * h + 1]), make_float2(wdf, wdf));
                     const float2 mn2 = __ffma2_rn(make_float2(a1, a1), __fadd2_rn(g2, make_float2(-m2.x, -m2.y)), m2);
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(256) k_update_rowcta(StepArgs a, const uint32_
     const float thmax = __uint_as_float(a.ds->thmax_bits[t & 1]);
     int s;
     float p2;
-    const bool jvalid = jscale(mc.Nglobal, (int)occ, gmax, thmax, &s, &p2);
+    const bool jvalid = jscale(mc.Nnorm, (int)occ, gmax, thmax, &s, &p2);
     const uint32_t* Arow = Acur + (size_t)v * NW;
     float* trow = a.theta + (size_t)v * N;
     float* mrow = a.m + (size_t)v * N;
@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(256) k_update_rowcta(StepArgs a, const uint32_
         double J = jvalid ? scalbn((double)I, -s) : 0.0;
         double c = 0.0;
         if (mc.normalize && !guard) {
-            c = J / (double)mc.Nglobal;
+            c = J / (double)mc.Nnorm;
             c = c * rho;
             c = c * rho;
         }
@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(256) k_update_rowcta(StepArgs a, const uint32_
     for (int n = threadIdx.x; n < N; n += blockDim.x) {
         const float g = __fmaf_rn((float)Gs[n], rhof, ncf);              // R27b
         float th = trow[n] * sc->wdf;
-        const float m0 = mrow[n];
+        const float m0 = mrow[n] * sc->mkeep;
         const float mm = __fmaf_rn(sc->a1, g - m0, m0);
         const float vb = vrow[n] * sc->b2f;
         const float vn = __fmaf_rn(sc->a2 * g, g, vb);

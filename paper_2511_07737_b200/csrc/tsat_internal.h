@@ -65,6 +65,7 @@ struct StepScalars {
     float rbc2;       // (float)(1 / sqrt(1 - beta2^(t+1)))  (R6c)
     float epsf;       // (float)eps
     float nz;         // (float)(lr * noise_sigma)
+    float mkeep;      // 0 at a moment reset (m *= 0; b2f = 0 zeroes v), else 1
 };
 
 // Device-resident scalars (one struct in the workspace).
@@ -94,7 +95,7 @@ struct MethodConsts {
     double eps_norm;
     int normalize;
     int K;              // instance max clause length
-    long long Nglobal;
+    long long Nnorm;    // candidates Eq. 5 averages over: N (normalize 0/1) or N/W (2, per shard)
     long long n0;       // first global candidate index of this rank
     unsigned long long seed;
     int noise;          // noise_sigma != 0
@@ -156,7 +157,7 @@ cudaError_t launch_step_kernel(int which, const StepArgs& a, const StepScalars* 
 cudaError_t configure_kernels(StepArgs* a);
 // sharded path (k_shard.cu); phases of one iteration between the collectives
 cudaError_t launch_shard_pack_max(const StepArgs& a, const StepScalars* sc, cudaStream_t st);
-cudaError_t launch_shard_unpack_max(const StepArgs& a, const StepScalars* sc, cudaStream_t st);
+cudaError_t launch_shard_unpack_max(const StepArgs& a, const StepScalars* sc, cudaStream_t st, bool key_only);
 cudaError_t launch_update_a(const StepArgs& a, const uint32_t* Acur, const StepScalars* sc, cudaStream_t st);
 cudaError_t launch_update_b(const StepArgs& a, const uint32_t* Acur, const StepScalars* sc, cudaStream_t st);
 cudaError_t launch_rows_partial(const StepArgs& a, const float* theta, unsigned int* thmax_bits, cudaStream_t st);

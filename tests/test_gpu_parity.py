@@ -47,7 +47,7 @@ def make_pair(cnf, N, seed, cfg=None, state=None, t0=0, sharded=False):
     c = config_default()
     ocfg = cfg or O.Config()
     for f in ("tau", "normalize", "beta1", "beta2", "eps", "weight_decay", "lr0", "lr_min", "decay_factor",
-              "decay_every", "restart_every", "noise_sigma", "eps_norm"):
+              "decay_every", "restart_every", "noise_sigma", "eps_norm", "reset_moments_on_restart"):
         setattr(c, f, getattr(ocfg, f))
     s.init_batch(N, seed, c)
     o = O.Oracle(cnf, N, seed, cfg=ocfg)
@@ -148,7 +148,9 @@ def test_lr_boundaries_and_restart():
 
 
 @pytest.mark.parametrize("variant", [dict(normalize=0), dict(weight_decay=0.0), dict(tau=5.0), dict(tau=0.5),
-                                     dict(noise_sigma=0.3)])
+                                     dict(noise_sigma=0.3),
+                                     dict(reset_moments_on_restart=1, restart_every=3, decay_every=2),
+                                     dict(normalize=2)])
 def test_variants(variant):
     cnf = planted_ksat(150, 630, 3, 8)
     cfg = O.Config(**variant)
@@ -343,18 +345,24 @@ def test_error_paths():
 
 
 # ---------------------------------------------------------------- sharded path (1-rank NCCL communicator)
-@pytest.mark.parametrize("case", ["c1", "industrial7", "ragged3"])
+@pytest.mark.parametrize("case", ["c1", "industrial7", "ragged3", "c1-per-shard", "ragged3-reset"])
 def test_sharded_path_matches_oracle(case):
     """The multi-GPU kernels (phase A -> SUM J -> phase B -> SUM Q -> rows
     finish, plus the MAX exchange) on a 1-rank communicator reproduce the
-    oracle bit for bit."""
+    oracle bit for bit; also with the f2 variants (per-shard
+    normalisation: no J/Q exchange; moment reset at LR restarts)."""
+    cfg = None
+    if case == "c1-per-shard":
+        case, cfg = "c1", O.Config(normalize=2)
+    elif case == "ragged3-reset":
+        case, cfg = "ragged3", O.Config(reset_moments_on_restart=1, restart_every=7, decay_every=3)
     if case == "c1":
         cnf, N = planted_ksat(20, 85, 3, 1), 64
     elif case == "industrial7":
         cnf, N = industrial_cnf(500, 2000, 4), 160
     else:
         cnf, N = planted_ksat(333, 1400, 3, 3), 96
-    s, o = make_pair(cnf, N, 5, sharded=True)
+    s, o = make_pair(cnf, N, 5, cfg=cfg, sharded=True)
     th, _, _, _ = s.get_state()
     if not np.array_equal(th, o.theta):
         s.set_state(o.theta, o.m, o.v, 0)

@@ -390,6 +390,37 @@ def test_jacobian_fixed_point_is_exact_sum():
         assert np.abs(s.G[v] * th[v]).max() * 2.0 ** sv <= 2.0 ** 61
 
 
+def test_moment_reset_is_a_fresh_optimizer():
+    """Variant f2: with reset_moments_on_restart the iteration
+    at an LR restart equals the first iteration of a freshly created AdamW
+    (m = v = 0, step 1, lr0) from the same theta; without it, it does not."""
+    cnf = planted_ksat(40, 170, 3, 2)
+    N = 64
+    cfg = O.Config(reset_moments_on_restart=1, restart_every=5, decay_every=2)
+    o = O.Oracle(cnf, N, seed=11, cfg=cfg)
+    for _ in range(5):
+        o.step()
+    assert o.t == 5 and np.abs(o.m).max() > 0
+    th5 = o.theta.copy()
+    fresh = O.Oracle(cnf, N, seed=11, cfg=cfg, init=False)
+    fresh.set_state(th5, np.zeros_like(th5), np.zeros_like(th5), 0)
+    o.step()
+    fresh.step()
+    np.testing.assert_array_equal(o.theta, fresh.theta)
+    np.testing.assert_array_equal(o.m, fresh.m)
+    np.testing.assert_array_equal(o.v, fresh.v)
+    plain = O.Oracle(cnf, N, seed=11, cfg=O.Config(restart_every=5, decay_every=2))
+    for _ in range(6):
+        plain.step()
+    assert not np.array_equal(plain.theta, o.theta)
+    # before the first restart the two runs coincide
+    a = O.Oracle(cnf, N, seed=11, cfg=cfg)
+    b = O.Oracle(cnf, N, seed=11, cfg=O.Config(restart_every=5, decay_every=2))
+    for _ in range(5):
+        a.step(); b.step()
+    np.testing.assert_array_equal(a.theta, b.theta)
+
+
 # ------------------------------------------------------------ AdamW / LR
 def test_lr_schedule():
     """PAPER.md §4.1 l.255-259 (0-based iterations, R9)."""
@@ -425,7 +456,7 @@ def test_adamw_matches_torch():
             gr["lr"] = lr
         p.grad = torch.tensor(g)
         opt.step()
-        L.or_adamw(V, 0, N, O._p(th), O._p(m), O._p(v), O._p(g), t, lr, 0.9, 0.999, 1e-8, 1e-2, 0.0, 0)
+        L.or_adamw(V, 0, N, O._p(th), O._p(m), O._p(v), O._p(g), t, t + 1, lr, 0.9, 0.999, 1e-8, 1e-2, 0.0, 0)
         st = opt.state[p]
         np.testing.assert_allclose(st["exp_avg"].numpy(), m, rtol=0, atol=0)
         np.testing.assert_allclose(st["exp_avg_sq"].numpy(), v, rtol=0, atol=0)
@@ -444,12 +475,12 @@ def test_adamw_closed_forms():
     g = np.zeros_like(th)
     L = O.lib()
     for t in range(5):
-        L.or_adamw(V, 0, N, O._p(th), O._p(m), O._p(v), O._p(g), t, 0.1, 0.9, 0.999, 1e-8, 0.0, 0.0, 0)
+        L.or_adamw(V, 0, N, O._p(th), O._p(m), O._p(v), O._p(g), t, t + 1, 0.1, 0.9, 0.999, 1e-8, 0.0, 0.0, 0)
     assert (th == 0.75).all()
     g = np.full((V, N), 0.5, np.float32)
     prev = th.copy()
     for t in range(200):
-        L.or_adamw(V, 0, N, O._p(th), O._p(m), O._p(v), O._p(g), t, 0.01, 0.9, 0.999, 1e-8, 0.0, 0.0, 0)
+        L.or_adamw(V, 0, N, O._p(th), O._p(m), O._p(v), O._p(g), t, t + 1, 0.01, 0.9, 0.999, 1e-8, 0.0, 0.0, 0)
         step = prev - th
         prev = th.copy()
     assert abs(step.mean() - 0.01) < 1e-4
@@ -555,6 +586,37 @@ def run_sharded(cnf, N, seed, world, steps, cfg=None):
     [x.start() for x in th]
     [x.join() for x in th]
     return shards, outs
+
+
+def test_per_shard_normalisation_is_independent_shards():
+    """Variant f2 normalize = 2: W = 2 shards normalising over their own
+    candidates evolve exactly like two independent single-shard runs
+    (normalize = 1, N = N/2) on the candidate slices; best and loss are still
+    the global ones.  With W = 1 it is the default (normalize = 1)."""
+    cnf = planted_ksat(50, 212, 3, 6)
+    N, T = 64, 8
+    shards, outs = run_sharded(cnf, N, 4, 2, T, cfg=O.Config(normalize=2))
+    init = O.Oracle(cnf, N, seed=4)
+    for r in range(2):
+        sl = slice(32 * r, 32 * (r + 1))
+        ind = O.Oracle(cnf, 32, seed=0, init=False)
+        ind.set_state(init.theta[:, sl], init.m[:, sl], init.v[:, sl], 0)
+        for t in range(T):
+            st = ind.step()
+            assert np.array_equal(outs[t][r].unsat, st.unsat)
+        assert np.array_equal(ind.theta, shards[r].theta)
+    for t in range(T):
+        u = np.concatenate([o.unsat for o in outs[t]])
+        j = int(np.lexsort((np.arange(N), u))[0])
+        assert (outs[t][1].best_unsat, outs[t][1].best_idx) == (int(u[j]), j)
+    # the global-normalisation run differs
+    g_shards, _ = run_sharded(cnf, N, 4, 2, T)
+    assert not np.array_equal(g_shards[0].theta, shards[0].theta)
+    one = O.Oracle(cnf, N, seed=4, cfg=O.Config(normalize=2))
+    ref = O.Oracle(cnf, N, seed=4)
+    for _ in range(4):
+        one.step(); ref.step()
+    assert np.array_equal(one.theta, ref.theta)
 
 
 def test_trajectory_determinism_and_shard_invariance():
