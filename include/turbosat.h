@@ -137,6 +137,26 @@ tsat_status tsat_create(tsat_ctx* out, int cuda_device, void* cuda_stream,
 
 /* Write a fresh NCCL unique id (NCCL_UNIQUE_ID_BYTES = 128) to out[0..bytes).
  * Host only; opens libnccl.so.2 at run time.  TSAT_E_NCCL if unavailable. */
+/* Peer-exchange multi-GPU path: one process (or context) per
+ * GPU of one NVLink/NVSwitch node, world <= 8.  The per-iteration exchanges
+ * (per-row J and Q partials, the best key / maxima / loss) run inside the
+ * step kernels as system-scope stores into every rank's exchange buffer,
+ * mapped by CUDA IPC: no NCCL call and no extra kernel on the step path.
+ * Sequence on every rank: tsat_create_peer -> tsat_load_* (allocates the
+ * exchange buffer, sized by V) -> tsat_peer_handle -> all-gather the handles
+ * (any host transport, e.g. torch.distributed) -> tsat_peer_open(all W handles
+ * in rank order) -> tsat_init_batch / tsat_step as usual.  Every rank must make
+ * the same sequence of init / set_state / step calls (they are collective).
+ * world = 1 runs the same kernels exchanging with itself.  A peer that stops
+ * responding makes the waiting kernels give up after 20 s: the step returns
+ * TSAT_E_NCCL and the context is poisoned. */
+#define TSAT_PEER_HANDLE_BYTES 64
+tsat_status tsat_create_peer(tsat_ctx* out, int cuda_device, void* cuda_stream, int rank, int world);
+/* This rank's exchange-buffer handle (TSAT_PEER_HANDLE_BYTES bytes into out). */
+tsat_status tsat_peer_handle(tsat_ctx ctx, void* out, size_t bytes);
+/* Map every rank's buffer: handles = world * TSAT_PEER_HANDLE_BYTES bytes, rank order. */
+tsat_status tsat_peer_open(tsat_ctx ctx, const void* handles, size_t bytes);
+
 tsat_status tsat_nccl_unique_id(void* out, size_t bytes);
 
 /* Load a CNF from DIMACS text: comments 'c', header

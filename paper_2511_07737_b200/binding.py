@@ -14,6 +14,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TSAT_LIB") or os.path.join(HERE, "libturbosat.so")
+PEER_HANDLE_BYTES = 64          # TSAT_PEER_HANDLE_BYTES
 
 TSAT_STATUS = {
     0: "TSAT_OK", 1: "TSAT_E_ARG", 2: "TSAT_E_PARSE", 3: "TSAT_E_RANGE", 4: "TSAT_E_STATE",
@@ -58,6 +59,9 @@ _SIGS = {
     "tsat_status_string": (ct.c_char_p, [ct.c_int]),
     "tsat_nccl_unique_id": (ct.c_int, [P, ct.c_size_t]),
     "tsat_create": (ct.c_int, [ct.POINTER(P), ct.c_int, P, P, ct.c_int, ct.c_int]),
+    "tsat_create_peer": (ct.c_int, [ct.POINTER(P), ct.c_int, P, ct.c_int, ct.c_int]),
+    "tsat_peer_handle": (ct.c_int, [P, P, ct.c_size_t]),
+    "tsat_peer_open": (ct.c_int, [P, P, ct.c_size_t]),
     "tsat_load_dimacs": (ct.c_int, [P, ct.c_char_p, ct.c_size_t, ct.POINTER(tsat_cnf_info)]),
     "tsat_load_clauses": (ct.c_int, [P, ct.c_int32, ct.c_int64, P, P, ct.POINTER(tsat_cnf_info)]),
     "tsat_workspace_bytes": (ct.c_int, [P, ct.c_int64, ct.POINTER(ct.c_size_t)]),
@@ -153,10 +157,13 @@ class Solver:
     query_unsat / export_best / export_model / get_solution; get_state /
     set_state for checkpoint-resume."""
 
-    def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_unique_id: bytes | None = None):
+    def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_unique_id: bytes | None = None,
+                 peer: bool = False):
         """world > 1 (or a unique id with world == 1): candidate-sharded path;
         every rank must construct its Solver concurrently with the same id
-        (see Solver.distributed)."""
+        (see Solver.distributed).  peer=True: the peer-exchange path
+        (tsat_create_peer; connect with peer_handle / peer_open after loading
+        the CNF, see Solver.connect_peers)."""
         import torch
         self._torch = torch
         if not torch.cuda.is_available():
@@ -166,8 +173,14 @@ class Solver:
         torch.cuda.set_device(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(device)
         h = ct.c_void_p()
-        uid = ct.c_char_p(nccl_unique_id) if nccl_unique_id is not None else None
-        self._check(self.lib.tsat_create(ct.byref(h), device, ct.c_void_p(self.stream.cuda_stream), uid, rank, world), None)
+        if peer:
+            self._check(self.lib.tsat_create_peer(ct.byref(h), device, ct.c_void_p(self.stream.cuda_stream), rank, world),
+                        None)
+        else:
+            uid = ct.c_char_p(nccl_unique_id) if nccl_unique_id is not None else None
+            self._check(self.lib.tsat_create(ct.byref(h), device, ct.c_void_p(self.stream.cuda_stream), uid, rank, world),
+                        None)
+        self.peer = peer
         self.h = h
         self.ws = None
         self.V = self.C = self.N = self.N_local = 0
@@ -184,6 +197,30 @@ class Solver:
         if world > 1:
             dist.broadcast_object_list(obj, src=0, group=group)
         return cls(device, stream=stream, rank=rank, world=world, nccl_unique_id=obj[0])
+
+    # -- peer-exchange path
+    def peer_handle(self) -> bytes:
+        """This rank's exchange-buffer IPC handle (after load_*)."""
+        buf = ct.create_string_buffer(PEER_HANDLE_BYTES)
+        self._check(self.lib.tsat_peer_handle(self.h, buf, PEER_HANDLE_BYTES))
+        return buf.raw
+
+    def peer_open(self, handles) -> None:
+        """Map every rank's exchange buffer (handles in rank order)."""
+        blob = b"".join(handles)
+        self._check(self.lib.tsat_peer_open(self.h, blob, len(blob)))
+
+    def connect_peers(self, group=None) -> None:
+        """All-gather the handles over torch.distributed (any backend, e.g.
+        gloo) and map them; call on every rank after load_*."""
+        import torch.distributed as dist
+        hs = [None] * self.world
+        mine = self.peer_handle()
+        if self.world > 1:
+            dist.all_gather_object(hs, mine, group=group)
+        else:
+            hs = [mine]
+        self.peer_open(hs)
 
     # -- helpers
     def _check(self, s, h="self"):

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <string>
 #include <vector>
@@ -31,6 +32,15 @@ struct tsat_ctx_s {
     cudaStream_t cap_stream = nullptr;  // private stream used only to capture graphs
     bool sharded = false;               // candidate-sharded path (NCCL communicator)
     void* comm = nullptr;               // ncclComm_t
+    // peer-exchange path (tsat_create_peer): exchanges inside the kernels over
+    // NVLink peer memory, buffers shared by CUDA IPC
+    bool peer = false;
+    void* xbuf = nullptr;               // this rank's exchange buffer (PeerLayout)
+    cudaIpcMemHandle_t xhandle{};
+    char* peer_ptr[kMaxPeers] = {};
+    bool peer_ipc[kMaxPeers] = {};      // opened with cudaIpcOpenMemHandle (close on destroy)
+    bool peers_ready = false;
+    unsigned xgen = 0;                  // exchange generation (same sequence on every rank)
     int rank = 0, world = 1;
     tsat_status poisoned = TSAT_OK;
     std::string err;
@@ -95,7 +105,31 @@ tsat_status cuda_fail(tsat_ctx c, cudaError_t e, const char* where) {
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
-Layout make_layout(int V, int N, int KB, int n_hubs, bool sharded) {
+// Exchange buffers created in this process, by IPC handle: a rank whose peer
+// lives in the same process (tests: several ranks on one GPU) maps it directly
+// (cudaIpcOpenMemHandle refuses handles of its own process).
+std::mutex g_xreg_mu;
+std::map<std::string, void*> g_xreg;
+std::string handle_key(const cudaIpcMemHandle_t& h) { return std::string(h.reserved, sizeof(h.reserved)); }
+
+void peer_release(tsat_ctx ctx) {
+    for (int r = 0; r < kMaxPeers; ++r) {
+        if (ctx->peer_ipc[r] && ctx->peer_ptr[r]) cudaIpcCloseMemHandle(ctx->peer_ptr[r]);
+        ctx->peer_ipc[r] = false;
+        ctx->peer_ptr[r] = nullptr;
+    }
+    ctx->peers_ready = false;
+    if (ctx->xbuf) {
+        {
+            std::lock_guard<std::mutex> lk(g_xreg_mu);
+            g_xreg.erase(handle_key(ctx->xhandle));
+        }
+        cudaFree(ctx->xbuf);
+        ctx->xbuf = nullptr;
+    }
+}
+
+Layout make_layout(int V, int N, int KB, int n_hubs, bool sharded, bool peer) {
     Layout L{};
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -123,11 +157,12 @@ Layout make_layout(int V, int N, int KB, int n_hubs, bool sharded) {
     L.sol = take((size_t)V);
     L.hubD = take((size_t)n_hubs * (KB - 1) * N * 4);
     const size_t sv = sharded ? 1 : 0;
+    const size_t sr = (sharded || peer) ? 1 : 0;      // row-statistics buffers (init / set_state)
     L.Gbuf = take(sv * VN * 4);
     L.Jbuf = take(sv * (size_t)V * 8);
-    L.Qbuf = take(sv * ((size_t)V + 1) * 8);
-    L.Pbuf = take(sv * (size_t)V * NW * 4);
-    L.Nbuf = take(sv * (size_t)V * NW * 4);
+    L.Qbuf = take(sr * ((size_t)V + 1) * 8);
+    L.Pbuf = take(sr * (size_t)V * NW * 4);
+    L.Nbuf = take(sr * (size_t)V * NW * 4);
     L.maxbuf = take(sv * 3 * 8);
     L.total = off;
     return L;
@@ -179,6 +214,15 @@ StepArgs step_args(tsat_ctx ctx) {
     a.Pbuf = (uint32_t*)(w + L.Pbuf);
     a.Nbuf = (uint32_t*)(w + L.Nbuf);
     a.maxbuf = (unsigned long long*)(w + L.maxbuf);
+    a.peer = ctx->peer ? 1 : 0;
+    if (ctx->peer) {
+        for (int r = 0; r < ctx->world; ++r) a.px.xb[r] = ctx->peer_ptr[r];
+        a.px.W = ctx->world;
+        a.px.rank = ctx->rank;
+        a.px.V = ctx->cnf.V;
+        a.px.exchange_rows = ctx->cfg.normalize != 2;
+        a.px.L = peer_layout(ctx->cnf.V, ctx->world);
+    }
     a.V = ctx->cnf.V;
     a.N = ctx->N;
     a.C = ctx->cnf.C;
@@ -279,6 +323,15 @@ tsat_status upload_cnf(tsat_ctx ctx, HostCnf&& h) {
     CK(upi((void**)&ctx->dcnf.occ_pn, c.occ_pn));
     CK(upi((void**)&ctx->dcnf.hub_of, c.hub_of));
     CK(upi((void**)&ctx->dcnf.hub_sc, c.hub_sc));
+    if (ctx->peer) {                    // a fresh, zeroed exchange buffer for this V; peers must reconnect
+        peer_release(ctx);
+        const size_t xb = peer_layout(c.V, ctx->world).total;
+        CK(cudaMalloc(&ctx->xbuf, xb));
+        CK(cudaMemsetAsync(ctx->xbuf, 0, xb, ctx->stream));
+        CK(cudaIpcGetMemHandle(&ctx->xhandle, ctx->xbuf));
+        std::lock_guard<std::mutex> lk(g_xreg_mu);
+        g_xreg[handle_key(ctx->xhandle)] = ctx->xbuf;
+    }
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->have_cnf = true;
     return TSAT_OK;
@@ -295,7 +348,18 @@ tsat_status check_batch(tsat_ctx ctx, bool need_step) {
 tsat_status state_stats(tsat_ctx ctx, const StepArgs& a, int64_t t) {
     uint32_t* A = (t & 1) ? a.A1 : a.A0;
     unsigned int* thm = &a.ds->thmax_bits[t & 1];
-    if (!ctx->sharded) {
+    if (ctx->peer) {
+        const unsigned gen = ++ctx->xgen;
+        CK(launch_rows_partial(a, a.theta, thm, ctx->stream));
+        if (ctx->cfg.normalize != 2) CK(launch_peer_rows_exchange(a, gen, ctx->stream));
+        CK(launch_rows_finish(a, A, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->h_scal, ctx->ws + ctx->L.scal, sizeof(DevScalars), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->h_scal->xerr) {
+            ctx->poisoned = TSAT_E_NCCL;
+            return fail(ctx, TSAT_E_NCCL, "peer exchange timed out (row statistics)");
+        }
+    } else if (!ctx->sharded) {
         CK(launch_rowstats(a.theta, a.V, a.N, ctx->mc, a.rowQ, a.rowD, a.rowRho, a.rowGuard, A, thm, ctx->stream));
     } else {
         std::string err;
@@ -436,6 +500,10 @@ tsat_status read_info(tsat_ctx ctx, tsat_step_info* out) {
     tsat_status s = collect_profile(ctx);
     if (s != TSAT_OK) return s;
     const DevScalars& d = *ctx->h_scal;
+    if (d.xerr) {
+        ctx->poisoned = TSAT_E_NCCL;
+        return fail(ctx, TSAT_E_NCCL, "peer exchange timed out");
+    }
     if (out) {
         out->t = ctx->t;
         out->best_unsat = d.info_best_unsat;
@@ -535,6 +603,73 @@ tsat_status tsat_create(tsat_ctx* out, int cuda_device, void* cuda_stream, const
     return TSAT_OK;
 }
 
+tsat_status tsat_create_peer(tsat_ctx* out, int cuda_device, void* cuda_stream, int rank, int world) {
+    if (!out) return TSAT_E_ARG;
+    *out = nullptr;
+    if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world) return TSAT_E_ARG;
+    std::unique_ptr<tsat_ctx_s> c(new tsat_ctx_s());
+    c->device = cuda_device;
+    c->stream = (cudaStream_t)cuda_stream;
+    c->rank = rank;
+    c->world = world;
+    c->peer = true;
+    tsat_ctx ctx = c.get();
+    CK(cudaSetDevice(cuda_device));
+    CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+    CK(cudaMallocHost(&c->h_steptab, sizeof(StepScalars) * kMaxStepsPerCall));
+    CK(cudaMallocHost(&c->h_scal, sizeof(DevScalars)));
+    tsat_config_default(&c->cfg);
+    *out = c.release();
+    return TSAT_OK;
+}
+
+tsat_status tsat_peer_handle(tsat_ctx ctx, void* out, size_t bytes) {
+    GUARD_CTX();
+    if (!ctx->peer) return fail(ctx, TSAT_E_STATE, "not a peer context (tsat_create_peer)");
+    if (!out || bytes < TSAT_PEER_HANDLE_BYTES) return fail(ctx, TSAT_E_ARG, "handle buffer too small");
+    if (!ctx->xbuf) return fail(ctx, TSAT_E_STATE, "no CNF loaded (the exchange buffer is sized by V)");
+    static_assert(sizeof(cudaIpcMemHandle_t) == TSAT_PEER_HANDLE_BYTES, "IPC handle size");
+    memcpy(out, &ctx->xhandle, sizeof(cudaIpcMemHandle_t));
+    return TSAT_OK;
+}
+
+tsat_status tsat_peer_open(tsat_ctx ctx, const void* handles, size_t bytes) {
+    GUARD_CTX();
+    if (!ctx->peer) return fail(ctx, TSAT_E_STATE, "not a peer context (tsat_create_peer)");
+    if (!handles || bytes != (size_t)ctx->world * TSAT_PEER_HANDLE_BYTES)
+        return fail(ctx, TSAT_E_ARG, "expected world * TSAT_PEER_HANDLE_BYTES bytes of handles");
+    if (!ctx->xbuf) return fail(ctx, TSAT_E_STATE, "no CNF loaded");
+    CK(cudaSetDevice(ctx->device));
+    for (int r = 0; r < kMaxPeers; ++r) {
+        if (ctx->peer_ipc[r] && ctx->peer_ptr[r]) cudaIpcCloseMemHandle(ctx->peer_ptr[r]);
+        ctx->peer_ipc[r] = false;
+        ctx->peer_ptr[r] = nullptr;
+    }
+    for (int r = 0; r < ctx->world; ++r) {
+        cudaIpcMemHandle_t h;
+        memcpy(&h, (const char*)handles + (size_t)r * TSAT_PEER_HANDLE_BYTES, sizeof(h));
+        if (r == ctx->rank) {
+            if (memcmp(&h, &ctx->xhandle, sizeof(h)) != 0)
+                return fail(ctx, TSAT_E_ARG, "handle of this rank does not match tsat_peer_handle");
+            ctx->peer_ptr[r] = (char*)ctx->xbuf;
+            continue;
+        }
+        void* p = nullptr;
+        {
+            std::lock_guard<std::mutex> lk(g_xreg_mu);
+            auto it = g_xreg.find(handle_key(h));
+            if (it != g_xreg.end()) p = it->second;
+        }
+        if (!p) {
+            CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+            ctx->peer_ipc[r] = true;
+        }
+        ctx->peer_ptr[r] = (char*)p;
+    }
+    ctx->peers_ready = true;
+    return TSAT_OK;
+}
+
 tsat_status tsat_nccl_unique_id(void* out, size_t bytes) {
     if (!out || bytes < 128) return TSAT_E_ARG;
     std::string err;
@@ -582,7 +717,7 @@ tsat_status tsat_workspace_bytes(tsat_ctx ctx, int64_t N_global, size_t* bytes) 
         return fail(ctx, TSAT_E_RANGE, "V * N / 32 >= 2^31 (32-bit bit-plane offsets)");
     if ((size_t)N * 12 > 200 * 1024) return fail(ctx, TSAT_E_RANGE, "N per GPU > 17066 not supported by the fused update");
     int KB = ctx->cnf.K <= 3 ? 4 : 8;
-    *bytes = make_layout(ctx->cnf.V, (int)N, KB, ctx->cnf.n_hubs, ctx->sharded).total;
+    *bytes = make_layout(ctx->cnf.V, (int)N, KB, ctx->cnf.n_hubs, ctx->sharded, ctx->peer).total;
     return TSAT_OK;
 }
 
@@ -594,6 +729,7 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
     if (s != TSAT_OK) return s;
     if (!ws || bytes < need) return fail(ctx, TSAT_E_OOM, "workspace too small");
     if ((uintptr_t)ws % 256) return fail(ctx, TSAT_E_ARG, "workspace must be 256-byte aligned");
+    if (ctx->peer && !ctx->peers_ready) return fail(ctx, TSAT_E_STATE, "peer context: call tsat_peer_open first");
     tsat_config c;
     if (cfg) c = *cfg; else tsat_config_default(&c);
     if (!(c.tau > 0) || c.decay_every < 1 || c.restart_every < 1 || !(c.decay_factor > 0) || !(c.eps_norm > 0) ||
@@ -608,7 +744,7 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
     ctx->seed = seed;
     ctx->ws = (char*)ws;
     ctx->ws_bytes = bytes;
-    ctx->L = make_layout(ctx->cnf.V, ctx->N, ctx->KB, ctx->cnf.n_hubs, ctx->sharded);
+    ctx->L = make_layout(ctx->cnf.V, ctx->N, ctx->KB, ctx->cnf.n_hubs, ctx->sharded, ctx->peer);
     MethodConsts& mc = ctx->mc;
     mc = MethodConsts{};
     for (int d = 0; d < 8; ++d) mc.E[d] = std::exp(-c.tau * (double)d);
@@ -633,7 +769,7 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
         ctx->upd_smem = g.upd_smem;
         ctx->num_sms = g.num_sms;
     }
-    if (ctx->sharded && ctx->upd_mode != 0)
+    if ((ctx->sharded || ctx->peer) && ctx->upd_mode != 0)
         return fail(ctx, TSAT_E_RANGE, "sharded path needs the fused k_update geometry (N per GPU too large)");
     StepArgs a = step_args(ctx);
     if (ctx->L.hubD != ctx->L.total)
@@ -672,13 +808,17 @@ tsat_status tsat_step(tsat_ctx ctx, int32_t k, tsat_step_info* out) {
         CK(cudaStreamSynchronize(ctx->stream));
         s = collect_profile(ctx);
         if (s != TSAT_OK) return s;
-        for (int i = 0; i < kk; ++i) ctx->h_steptab[i] = step_scalars(ctx->cfg, ctx->t + i);
+        for (int i = 0; i < kk; ++i) {
+            ctx->h_steptab[i] = step_scalars(ctx->cfg, ctx->t + i);
+            ctx->h_steptab[i].xgen = ctx->xgen + 1 + (unsigned)i;
+        }
         CK(cudaMemcpyAsync(ctx->ws + ctx->L.steptab, ctx->h_steptab, sizeof(StepScalars) * kk, cudaMemcpyHostToDevice,
                            ctx->stream));
         s = launch_steps(ctx, kk);
         if (s != TSAT_OK) return s;
         ctx->t += kk;
         ctx->steps_done += kk;
+        ctx->xgen += (unsigned)kk;
         done += kk;
     }
     if (out) return read_info(ctx, out);
@@ -926,6 +1066,7 @@ void tsat_destroy(tsat_ctx ctx) {
     for (auto e : ctx->events) cudaEventDestroy(e);
     free_cnf(ctx);
     comm_destroy(ctx->comm);
+    peer_release(ctx);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     cudaFreeHost(ctx->h_steptab);
     cudaFreeHost(ctx->h_scal);

@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t*
         ds->gmax_bits = 0ull;
         ds->row_counter = 0;
         ds->thmax_bits[(t + 1) & 1] = 0u;
+        ds->loss_fx = 0;
     }
     for (int i = threadIdx.x; i < (KB - 1) * 1024; i += blockDim.x) sh[i] = 0;
     __syncthreads();
@@ -218,6 +219,7 @@ __global__ void k_reset_accumulators(DevScalars* __restrict__ ds, const StepScal
     ds->gmax_bits = 0ull;
     ds->row_counter = 0;
     ds->thmax_bits[(t + 1) & 1] = 0u;
+    ds->loss_fx = 0;
 }
 
 cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, const StepScalars* sc, cudaStream_t st) {

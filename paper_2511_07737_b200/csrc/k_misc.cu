@@ -4,6 +4,7 @@
 // Compiled with -fmad=false: every floating operation is a separate IEEE
 // round-to-nearest op unless written as an explicit fma.
 #include "device_common.cuh"
+#include "peer.cuh"
 
 namespace tsat {
 
@@ -87,7 +88,8 @@ template <int KB>
 __global__ void __launch_bounds__(256) k_gtable(int* __restrict__ hist, int N, long long C, MethodConsts mc,
                                                 float* __restrict__ gtab, double* __restrict__ S,
                                                 int* __restrict__ unsat, DevScalars* __restrict__ ds, int sharded,
-                                                double* __restrict__ lossp, const StepScalars* __restrict__ sc) {
+                                                double* __restrict__ lossp, const StepScalars* __restrict__ sc,
+                                                int peer, const PeerArgs px) {
     __shared__ double shS[8];
     __shared__ bool last;
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
@@ -150,13 +152,35 @@ __global__ void __launch_bounds__(256) k_gtable(int* __restrict__ hist, int N, l
         key = k2 < key ? k2 : key;
         gb = g2 > gb ? g2 : gb;
     }
-    if (sharded) lfx = warp_sum(lfx);
+    const bool fx = sharded || peer;            // exact fixed-point loss, summed across ranks
+    if (fx) lfx = warp_sum(lfx);
     if (lane == 0) {
         atomicMin(&ds->best_key, key);
         atomicMax(&ds->gmax_bits, gb);
-        if (sharded) atomicAdd(reinterpret_cast<unsigned long long*>(&ds->loss_fx), (unsigned long long)lfx);
+        if (fx) atomicAdd(reinterpret_cast<unsigned long long*>(&ds->loss_fx), (unsigned long long)lfx);
     }
     if (sharded) return;                       // the sharded step ends in k_step_end_sharded
+    if (peer) {
+        // peer path: the last block publishes this rank's (best key, gmax,
+        // max|theta_t|, loss) to every rank; k_update combines them
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            last = atomicAdd(&ds->gt_done, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (last && threadIdx.x == 0) {
+            __threadfence();
+            const long long t = sc->t;
+            const unsigned long long x[4] = {~*((volatile unsigned long long*)&ds->best_key),
+                                             *((volatile unsigned long long*)&ds->gmax_bits),
+                                             (unsigned long long)*((volatile unsigned int*)&ds->thmax_bits[t & 1]),
+                                             (unsigned long long)*((volatile long long*)&ds->loss_fx)};
+            ds->gt_done = 0u;
+            peer_send_scalars(px, x, sc->xgen);
+        }
+        return;
+    }
     // block sum of S in a fixed order (warp trees, then warps ascending)
     double sv = n < N ? S[n] : 0.0;
 #pragma unroll
@@ -359,8 +383,12 @@ cudaError_t launch_rowstats(const float* theta, int V, int N, const MethodConsts
 
 cudaError_t launch_gtable(const StepArgs& a, const StepScalars* sc, cudaStream_t st) {
     int blocks = (a.N + 255) / 256;
-    if (a.KB == 4) k_gtable<4><<<blocks, 256, 0, st>>>(a.hist, a.N, a.C, a.mc, a.gtab, a.S, a.unsat, a.ds, a.sharded, a.lossp, sc);
-    else k_gtable<8><<<blocks, 256, 0, st>>>(a.hist, a.N, a.C, a.mc, a.gtab, a.S, a.unsat, a.ds, a.sharded, a.lossp, sc);
+    if (a.KB == 4)
+        k_gtable<4><<<blocks, 256, 0, st>>>(a.hist, a.N, a.C, a.mc, a.gtab, a.S, a.unsat, a.ds, a.sharded, a.lossp, sc,
+                                            a.peer, a.px);
+    else
+        k_gtable<8><<<blocks, 256, 0, st>>>(a.hist, a.N, a.C, a.mc, a.gtab, a.S, a.unsat, a.ds, a.sharded, a.lossp, sc,
+                                            a.peer, a.px);
     return cudaGetLastError();
 }
 

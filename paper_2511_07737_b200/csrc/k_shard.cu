@@ -9,6 +9,7 @@
 // All reduced quantities are integers (or maxima), so every rank sees the
 // same values and the result is bit-identical for any W (and to W = 1).
 #include "device_common.cuh"
+#include "peer.cuh"
 
 namespace tsat {
 
@@ -179,6 +180,34 @@ __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a, uint32_t* __res
         Anext[(size_t)v * NW + w] = dpos ? a.Pbuf[(size_t)v * NW + w] : a.Nbuf[(size_t)v * NW + w];
 }
 
+// Peer path, init / set_state: exchange of the Q row partials in Qbuf.  Two
+// kernels (all sends, then all receives) so no CTA waits on a CTA of its own
+// grid that may not be resident.
+__global__ void k_peer_send_rows(StepArgs a, unsigned gen) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= a.V) return;
+    const PeerArgs& px = a.px;
+    const size_t slot = (size_t)px.rank * px.V + v;
+    for (int p = 0; p < px.W; ++p) {
+        st_relaxed_sys(reinterpret_cast<long long*>(px.xb[p] + px.L.qx) + slot, a.Qbuf[v]);
+        st_release_sys(reinterpret_cast<unsigned*>(px.xb[p] + px.L.qf) + slot, gen);
+    }
+}
+__global__ void k_peer_recv_rows(StepArgs a, unsigned gen) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= a.V) return;
+    const PeerArgs& px = a.px;
+    const long long* xs = reinterpret_cast<const long long*>(px.xb[px.rank] + px.L.qx);
+    const unsigned* fs = reinterpret_cast<const unsigned*>(px.xb[px.rank] + px.L.qf);
+    long long s = 0;
+    for (int r = 0; r < px.W; ++r) {
+        const size_t i = (size_t)r * px.V + v;
+        if (!peer_wait(fs + i, gen, a.ds)) return;
+        s += ld_relaxed_sys(xs + i);
+    }
+    a.Qbuf[v] = s;
+}
+
 // End of a sharded iteration: first-model bookkeeping (global best), step
 // info and accumulator reset; the loss was reduced exactly with Q.
 __global__ void k_step_end_sharded(DevScalars* __restrict__ ds, const StepScalars* __restrict__ sc) {
@@ -225,6 +254,14 @@ cudaError_t launch_rows_finish(const StepArgs& a, uint32_t* Anext, cudaStream_t 
 }
 cudaError_t launch_step_end_sharded(const StepArgs& a, const StepScalars* sc, cudaStream_t st) {
     k_step_end_sharded<<<1, 1, 0, st>>>(a.ds, sc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_peer_rows_exchange(const StepArgs& a, unsigned gen, cudaStream_t st) {
+    if (a.V == 0) return cudaGetLastError();
+    const unsigned blocks = (unsigned)((a.V + 255) / 256);
+    k_peer_send_rows<<<blocks, 256, 0, st>>>(a, gen);
+    k_peer_recv_rows<<<blocks, 256, 0, st>>>(a, gen);
     return cudaGetLastError();
 }
 

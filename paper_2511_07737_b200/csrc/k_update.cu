@@ -18,7 +18,10 @@
 // Rows whose counts can leave int8 ("hubs", SURVEY §7 hard parts) get their
 // counts from k_hub, which splits a hub's occurrences over many CTAs and adds
 // exact int32 counts (integer atomics: order-free, deterministic).
+#include <cstdlib>
+
 #include "device_common.cuh"
+#include "peer.cuh"
 
 #ifndef TSAT_UNI3
 #define TSAT_UNI3 2
@@ -201,6 +204,10 @@ __device__ __forceinline__ void gsync(int bar, int GT) {
 
 // MODE 0: fused W = 1 iteration.  MODE 1: phase A of the sharded iteration
 // (G -> Gbuf, int64 J partial -> Jbuf; the AdamW phase runs after the J exchange).
+// MODE 2: the fused iteration on W GPUs with the exchanges inside the kernel
+// over peer memory (peer.cuh): the per-step scalars at the start, and per row
+// the J partial (before the gradient) and the Q partial (before the next
+// state's statistics); other warp groups keep streaming while one waits.
 // Rows come from a global counter (dynamic: hub rows, ragged occurrence counts
 // and the tail stay balanced); tg 0 fetches the next row at the start of the
 // current one into a parity-double-buffered slot, read after the J barrier.
@@ -226,6 +233,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
     long long* red = reinterpret_cast<long long*>(gb + grb - 128);                      // 4 + 4 slots
     float* redf = reinterpret_cast<float*>(red + 8);                                    // 4 slots
     int* rowslot = reinterpret_cast<int*>(redf + 4);                                    // 2 slots
+    long long* pxs = red + 11;                                                          // 2 slots (MODE 2)
     const int bar = 1 + grp;
     const int lane = threadIdx.x & 31, gw = tg >> 5, ngw = GT >> 5;
     const bool uni3 = a.uniform_len && a.mc.K == 3 && KB == 4;
@@ -234,11 +242,30 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
     for (int i = threadIdx.x * 4; i < KB * N; i += blockDim.x * 4)
         *reinterpret_cast<float4*>(gs + i) = *reinterpret_cast<const float4*>(a.gtab + i);
     if (tg == 0) rowslot[1] = atomicAdd(&a.ds->row_counter, 1);
+    const long long t = sc->t;
+    __shared__ unsigned long long pscal[3];         // MODE 2: global best key, gmax bits, thmax bits
+    if (MODE == 2 && threadIdx.x == 0) {
+        unsigned long long x[4];
+        peer_recv_scalars(a.px, sc->xgen, a.ds, x);
+        pscal[0] = ~x[0];
+        pscal[1] = a.px.exchange_rows ? x[1] : a.ds->gmax_bits;           // per shard: J scale stays local
+        pscal[2] = a.px.exchange_rows ? x[2] : (unsigned long long)a.ds->thmax_bits[t & 1];
+        if (blockIdx.x == 0) {                      // step bookkeeping with the global values
+            const int bu = (int)(pscal[0] >> 32);
+            const long long bi = (long long)(pscal[0] & 0xffffffffull);
+            if (bu == 0 && a.ds->sol_step < 0) { a.ds->sol_step = t; a.ds->sol_idx = bi; }
+            const double loss = -((double)(long long)x[3] * 9.094947017729282e-13);     // * 2^-40
+            a.ds->loss = loss;
+            a.ds->info_t = t + 1;
+            a.ds->info_best_unsat = bu;
+            a.ds->info_best_idx = bi;
+            a.ds->info_loss = loss;
+        }
+    }
     __syncthreads();
 
-    const long long t = sc->t;
-    const double gmax = __longlong_as_double((long long)a.ds->gmax_bits);
-    const float thmax = __uint_as_float(a.ds->thmax_bits[t & 1]);
+    const double gmax = __longlong_as_double((long long)(MODE == 2 ? pscal[1] : a.ds->gmax_bits));
+    const float thmax = __uint_as_float(MODE == 2 ? (unsigned)pscal[2] : a.ds->thmax_bits[t & 1]);
     const float wdf = sc->wdf, a1 = sc->a1, b2f = sc->b2f, a2 = sc->a2, nss = sc->nss, rbc2 = sc->rbc2,
                 epsf = sc->epsf, nz = sc->nz, mkeep = sc->mkeep;
     const MethodConsts& mc = a.mc;
@@ -321,6 +348,11 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
         gsync(bar, GT);
         long long Itot = 0;                                  // every thread folds the warp partials
         for (int i = 0; i < ngw; ++i) Itot += red[i];
+        if (MODE == 2 && a.px.exchange_rows) {               // J_v over all ranks
+            if (tg == 0) pxs[0] = peer_row_sum(a.px, 0, v, Itot, sc->xgen, a.ds);
+            gsync(bar, GT);
+            Itot = pxs[0];
+        }
         const int vnext = rowslot[it & 1];
         // stage the next row's records asynchronously (cp.async global -> smem);
         // they land while this row streams, and are waited for before the Q barrier
@@ -428,6 +460,11 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
         gsync(bar, GT);
         long long Qtot = 0;
         for (int i = 0; i < ngw; ++i) Qtot += red[4 + i];
+        if (MODE == 2 && a.px.exchange_rows) {               // Q_{t+1,v} over all ranks
+            if (tg == 0) pxs[1] = peer_row_sum(a.px, 1, v, Qtot, sc->xgen, a.ds);
+            gsync(bar, GT);
+            Qtot = pxs[1];
+        }
         // sign(d_{t+1}) = sign(mu) with sign(0) = +1, i.e. Q >= 0 (R3): the bits
         // of the next state need no division; tg 0 finishes Eq. 5's statistics.
         const bool dpos = !mc.normalize || Qtot >= 0;
@@ -440,7 +477,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
             row_finish(Qtot, mc, &dn, &rhon, &gn);
             a.rowQ[v] = Qtot; a.rowD[v] = dn; a.rowRho[v] = rhon; a.rowGuard[v] = gn;
             atomicMax(&a.ds->thmax_bits[(t + 1) & 1], __float_as_uint(m2));
-            const unsigned long long bk = a.ds->best_key;
+            const unsigned long long bk = MODE == 2 ? pscal[0] : a.ds->best_key;
             if ((bk >> 32) == 0ull && (a.ds->sol_step < 0 || a.ds->sol_step == t)) {          // first model: keep its bits (A22)
                 const long long idx = (long long)(bk & 0xffffffffull) - mc.n0;
                 if (idx >= 0 && idx < N)
@@ -652,12 +689,22 @@ cudaError_t configure_update(StepArgs* a) {
     a->upd_NG = (int)ng;
     a->upd_smem = gsb + (size_t)ng * grb;
     a->upd_grid = sms;
+    // test hook: several ranks' persistent kernels sharing one GPU must be
+    // co-resident, so each may be limited to a part of the SMs
+    if (const char* g = std::getenv("TSAT_UPD_GRID")) {
+        const int x = std::atoi(g);
+        if (x > 0 && x < sms) a->upd_grid = x;
+    }
+    const int smem = (int)a->upd_smem;
+    const cudaFuncAttribute attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
     if (KB == 4) {
-        if ((e = cudaFuncSetAttribute(k_update<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a->upd_smem)) != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k_update<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a->upd_smem);
+        if ((e = cudaFuncSetAttribute(k_update<4, 0>, attr, smem)) != cudaSuccess) return e;
+        if ((e = cudaFuncSetAttribute(k_update<4, 1>, attr, smem)) != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k_update<4, 2>, attr, smem);
     } else {
-        if ((e = cudaFuncSetAttribute(k_update<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a->upd_smem)) != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k_update<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a->upd_smem);
+        if ((e = cudaFuncSetAttribute(k_update<8, 0>, attr, smem)) != cudaSuccess) return e;
+        if ((e = cudaFuncSetAttribute(k_update<8, 1>, attr, smem)) != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k_update<8, 2>, attr, smem);
     }
     return e;
 }
@@ -676,8 +723,14 @@ cudaError_t launch_update(const StepArgs& a, const uint32_t* Acur, uint32_t* Ane
     if (a.V == 0) return cudaGetLastError();
     if (a.upd_mode == 0) {
         const int threads = a.upd_GT * a.upd_NG;
-        if (a.KB == 4) k_update<4, 0><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
-        else k_update<8, 0><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
+        if (a.peer) {
+            if (a.KB == 4) k_update<4, 2><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
+            else k_update<8, 2><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
+        } else if (a.KB == 4) {
+            k_update<4, 0><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
+        } else {
+            k_update<8, 0><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
+        }
     } else {
         if (a.KB == 4) k_update_rowcta<4><<<a.V, 256, a.upd_smem, st>>>(a, Acur, Anext, sc);
         else k_update_rowcta<8><<<a.V, 256, a.upd_smem, st>>>(a, Acur, Anext, sc);

@@ -16,6 +16,37 @@ constexpr int kMaxStepsPerCall = 4096;
 constexpr int kTopkMax = 2048;         // export: k most confident variables per candidate
 constexpr int kRecCap = 512;           // occurrence-record words a warp group stages per row (longer rows: hubs)
 constexpr int kHubSlab = 1023;         // occurrences per hub super-chunk (11-bit signed counters)
+constexpr int kMaxPeers = 8;           // peer-exchange path: ranks (GPUs of one NVSwitch node)
+
+// Peer-exchange buffer of one rank (cudaMalloc'd, CUDA-IPC shared).
+// Every rank writes its slot [src = its rank] of every rank's buffer:
+//   S: [2][W] x {~best key, gmax bits, thmax bits, loss S 2^40} + flags [2][W]
+//      (once per step, double-buffered by generation parity)
+//   J, Q: [W][V] int64 row partials + u32 flags [W][V]                   (per row, per step)
+// A flag holds the exchange generation its value belongs to (monotone per
+// context, identical on every rank: the ranks run the same call sequence).
+struct PeerLayout {
+    size_t sx, sf, jx, jf, qx, qf, total;
+};
+inline PeerLayout peer_layout(int V, int W) {
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    PeerLayout L{};
+    size_t o = 0;
+    L.sx = o; o = al(o + (size_t)2 * W * 32);
+    L.sf = o; o = al(o + (size_t)2 * W * 4);
+    L.jx = o; o = al(o + (size_t)W * V * 8);
+    L.jf = o; o = al(o + (size_t)W * V * 4);
+    L.qx = o; o = al(o + (size_t)W * V * 8);
+    L.qf = o; o = al(o + (size_t)W * V * 4);
+    L.total = o;
+    return L;
+}
+struct PeerArgs {
+    char* xb[kMaxPeers];               // every rank's buffer in this process's address space
+    int W, rank, V;
+    int exchange_rows;                 // 0 with normalize = 2 (per shard): J, Q stay local
+    PeerLayout L;
+};
 
 // ---------------------------------------------------------------- host CNF
 // Literal code used on the device: (var << 1) | negated, var 0-based.
@@ -66,6 +97,8 @@ struct StepScalars {
     float epsf;       // (float)eps
     float nz;         // (float)(lr * noise_sigma)
     float mkeep;      // 0 at a moment reset (m *= 0; b2f = 0 zeroes v), else 1
+    unsigned xgen;    // peer path: exchange generation of this iteration
+    int pad;
 };
 
 // Device-resident scalars (one struct in the workspace).
@@ -85,7 +118,7 @@ struct DevScalars {
     double info_loss;
     long long loss_fx;               // sharded: this rank's sum of S_n * 2^40 (exact int64)
     unsigned int gt_done;            // k_gtable blocks finished (last block does the step bookkeeping)
-    int pad2;
+    unsigned int xerr;               // peer path: an exchange timed out (step result invalid)
 };
 
 // Method constants passed by value to kernels.
@@ -135,6 +168,9 @@ struct StepArgs {
     long long* Qbuf;                 // [V+1] int64 partial / global Q, slot V = loss (fixed point)
     uint32_t *Pbuf, *Nbuf;           // [V][N/32] sign planes of the next state
     unsigned long long* maxbuf;      // [3] (~best key, gmax bits, thmax bits)
+    // peer-exchange path (W GPUs, exchanges over NVLink peer memory inside the kernels)
+    int peer;
+    PeerArgs px;
     MethodConsts mc;
 };
 
@@ -162,6 +198,8 @@ cudaError_t launch_update_a(const StepArgs& a, const uint32_t* Acur, const StepS
 cudaError_t launch_update_b(const StepArgs& a, const uint32_t* Acur, const StepScalars* sc, cudaStream_t st);
 cudaError_t launch_rows_partial(const StepArgs& a, const float* theta, unsigned int* thmax_bits, cudaStream_t st);
 cudaError_t launch_rows_finish(const StepArgs& a, uint32_t* Anext, cudaStream_t st);
+// peer path: exchange of Qbuf[0..V) row partials (init / set_state), gen = exchange generation
+cudaError_t launch_peer_rows_exchange(const StepArgs& a, unsigned gen, cudaStream_t st);
 cudaError_t launch_step_end_sharded(const StepArgs& a, const StepScalars* sc, cudaStream_t st);
 // NCCL (comm.cpp); return 0 or 7 (TSAT_E_NCCL) with err
 int comm_unique_id(void* out128, std::string* err);

@@ -1,0 +1,200 @@
+"""Peer-exchange multi-GPU path (tsat_create_peer): the
+exchanges run inside the step kernels over peer memory.
+
+This box has one GPU, so W = 2 runs as two ranks sharing it: two contexts in
+one process (two host threads, each persistent k_update limited to part of
+the SMs so both are resident), and two processes (CUDA IPC handles exchanged
+over torch.distributed gloo).  Every case is compared bit for bit with the
+oracle, which is shard-invariant (tests/test_oracle_pins.py)."""
+import os
+import threading
+
+import numpy as np
+import pytest
+
+import oracle.oracle as O
+from tsat_synth import industrial_cnf, planted_ksat
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg(ocfg):
+    from paper_2511_07737_b200 import config_default
+    c = config_default()
+    for f in ("tau", "normalize", "beta1", "beta2", "eps", "weight_decay", "lr0", "lr_min", "decay_factor",
+              "decay_every", "restart_every", "noise_sigma", "eps_norm", "reset_moments_on_restart"):
+        setattr(c, f, getattr(ocfg, f))
+    return c
+
+
+def _pack(bits):
+    V, N = bits.shape
+    b = bits.reshape(V, N // 32, 32).astype(np.uint64)
+    return (b << np.arange(32, dtype=np.uint64)).sum(axis=2).astype(np.uint32)
+
+
+def _peer_solver(rank, world, stream=None):
+    from paper_2511_07737_b200 import Solver
+    return Solver(0, stream=stream, rank=rank, world=world, peer=True)
+
+
+@pytest.mark.parametrize("case", ["c1", "industrial7", "ragged3", "c1-per-shard"])
+def test_peer_w1_matches_oracle(case):
+    """W = 1: the MODE 2 kernels exchanging with themselves reproduce the
+    oracle bit for bit, step by step and through a multi-step graph."""
+    ocfg = O.Config(normalize=2) if case == "c1-per-shard" else O.Config()
+    if case.startswith("c1"):
+        cnf, N = planted_ksat(20, 85, 3, 1), 64
+    elif case == "industrial7":
+        cnf, N = industrial_cnf(500, 2000, 4), 160
+    else:
+        cnf, N = planted_ksat(333, 1400, 3, 3), 96
+    s = _peer_solver(0, 1)
+    s.load_cnf(cnf)
+    s.connect_peers()
+    s.init_batch(N, 5, _cfg(ocfg))
+    o = O.Oracle(cnf, N, 5, cfg=ocfg)
+    th, m, v, _ = s.get_state()
+    np.testing.assert_array_equal(th, o.theta)
+    K = o.K
+    KB = 4 if K <= 3 else 8
+    for _ in range(12):
+        info = s.step(1)
+        ref = o.step()
+        np.testing.assert_array_equal(s.query_unsat(), ref.unsat)
+        np.testing.assert_array_equal(s.debug(3, np.uint32, (cnf.V, N // 32)), _pack(ref.bits))
+        g = s.debug(1, np.float32, (KB, N))
+        np.testing.assert_array_equal(g[:K + 1].T, ref.g32)
+        th, m, v, _ = s.get_state()
+        np.testing.assert_array_equal(th, o.theta)
+        np.testing.assert_array_equal(m, o.m)
+        np.testing.assert_array_equal(v, o.v)
+        assert (info.best_unsat, info.best_idx) == (ref.best_unsat, ref.best_idx)
+        assert abs(info.loss - ref.loss) <= 1e-9 * abs(ref.loss)
+    info = s.step(17)
+    for _ in range(17):
+        ref = o.step()
+    th, _, _, t = s.get_state()
+    assert t == o.t
+    np.testing.assert_array_equal(th, o.theta)
+    assert (info.best_unsat, info.best_idx) == (ref.best_unsat, ref.best_idx)
+    s.close()
+
+
+def _run_threads(fns):
+    errs = []
+
+    def wrap(f):
+        try:
+            f()
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=wrap, args=(f,)) for f in fns]
+    [t.start() for t in th]
+    [t.join(timeout=600) for t in th]
+    if errs:
+        raise errs[0]
+
+
+@pytest.mark.parametrize("normalize", [1, 2])
+def test_peer_two_ranks_one_gpu(normalize, monkeypatch):
+    """W = 2 in one process: two contexts on their own streams, stepped from two
+    host threads; the rank-concatenated state equals the oracle's (1 shard
+    for normalize = 1; per-shard oracle ranks for normalize = 2)."""
+    import torch
+    monkeypatch.setenv("TSAT_UPD_GRID", "70")        # both persistent kernels resident on one GPU
+    cnf = planted_ksat(400, 1680, 3, 7)
+    N, W, seed = 256, 2, 11
+    ocfg = O.Config(normalize=normalize)
+    streams = [torch.cuda.Stream(0) for _ in range(W)]
+    ss = [_peer_solver(r, W, stream=streams[r]) for r in range(W)]
+    for s in ss:
+        s.load_cnf(cnf)
+    hs = [s.peer_handle() for s in ss]
+    for s in ss:
+        s.peer_open(hs)
+    _run_threads([lambda s=s: s.init_batch(N, seed, _cfg(ocfg)) for s in ss])
+    if normalize == 1:
+        o = O.Oracle(cnf, N, seed, cfg=ocfg)
+        refs = None
+    else:
+        import test_oracle_pins as P
+        shards, _ = P.run_sharded(cnf, N, seed, W, 0, cfg=ocfg)
+    infos = [None] * W
+    for k in (1, 1, 6, 13):
+        def go(r):
+            infos[r] = ss[r].step(k)
+        _run_threads([lambda r=r: go(r) for r in range(W)])
+        if normalize == 1:
+            for _ in range(k):
+                refs = o.step()
+            ref_theta = o.theta
+            ref_unsat = refs.unsat
+            best = (refs.best_unsat, refs.best_idx)
+        else:
+            outs = [None] * W
+            import threading as _t
+            comm = P.ThreadComm(W)
+            for r, sh in enumerate(shards):
+                sh.comm = comm.rank(r)
+
+            def work(r):
+                for _ in range(k):
+                    outs[r] = shards[r].step()
+            tt = [_t.Thread(target=work, args=(r,)) for r in range(W)]
+            [x.start() for x in tt]
+            [x.join() for x in tt]
+            ref_theta = np.concatenate([sh.theta for sh in shards], axis=1)
+            ref_unsat = np.concatenate([x.unsat for x in outs])
+            best = (outs[0].best_unsat, outs[0].best_idx)
+        th = np.concatenate([s.get_state()[0] for s in ss], axis=1)
+        np.testing.assert_array_equal(th, ref_theta)
+        un = np.concatenate([s.query_unsat() for s in ss])
+        np.testing.assert_array_equal(un, ref_unsat)
+        for r in range(W):
+            assert (infos[r].best_unsat, infos[r].best_idx) == best
+    for s in ss:
+        s.close()
+
+
+def _mp_worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    os.environ["TSAT_UPD_GRID"] = "70"
+    from paper_2511_07737_b200 import Solver
+    cnf = planted_ksat(300, 1260, 3, 9)
+    s = Solver(0, rank=rank, world=world, peer=True)
+    s.load_cnf(cnf)
+    s.connect_peers()
+    s.init_batch(192, 3)
+    info = s.step(9)
+    th = s.get_state()[0]
+    np.save(os.path.join(out_dir, f"theta{rank}.npy"), th)
+    np.save(os.path.join(out_dir, f"info{rank}.npy"), np.array([info.best_unsat, info.best_idx, info.t]))
+    s.close()
+    torch.cuda.synchronize()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_peer_two_processes_ipc(tmp_path):
+    """W = 2 as two processes on one GPU: exchange buffers mapped with CUDA IPC
+    (handles all-gathered over gloo), 9 steps in one graph; equals the oracle."""
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    mp.start_processes(_mp_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True, start_method="spawn")
+    cnf = planted_ksat(300, 1260, 3, 9)
+    o = O.Oracle(cnf, 192, 3)
+    for _ in range(9):
+        ref = o.step()
+    th = np.concatenate([np.load(tmp_path / f"theta{r}.npy") for r in range(2)], axis=1)
+    np.testing.assert_array_equal(th, o.theta)
+    for r in range(2):
+        bu, bi, t = np.load(tmp_path / f"info{r}.npy")
+        assert (bu, bi, t) == (ref.best_unsat, ref.best_idx, 9)
