@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-quality", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="W=1: run the candidate-sharded (multi-GPU) kernels")
+    ap.add_argument("--nccl", action="store_true",
+                    help="N>1: use the NCCL-exchange sharded path instead of the peer-exchange path (default)")
+    ap.add_argument("--peer", action="store_true", help="W=1: run the peer-exchange kernels exchanging with themselves")
     return ap.parse_args()
 
 
@@ -198,7 +201,11 @@ def main():
     seed = cfg["seed"]
     stream = torch.cuda.current_stream()
 
+    use_peer = (world > 1 and not args.nccl) or args.peer
+
     def make_solver():
+        if use_peer:           # exchanges inside the kernels over NVLink peer memory (CUDA IPC)
+            return Solver(local, stream=stream, rank=rank, world=world, peer=True)
         if world > 1:
             return Solver.distributed(local, rank, world, stream=stream)
         if args.sharded:       # the multi-GPU kernels + NCCL on a 1-rank communicator
@@ -206,8 +213,14 @@ def main():
             return Solver(local, stream=stream, rank=0, world=1, nccl_unique_id=nccl_unique_id())
         return Solver(local, stream=stream)
 
+    def load(sv):
+        inf = sv.load_cnf(cnf)
+        if use_peer:
+            sv.connect_peers()
+        return inf
+
     s = make_solver()
-    info = s.load_cnf(cnf)
+    info = load(s)
     s.init_batch(N * world, seed)
     chunk = max(1, min(args.chunk, args.steps))
     assert args.steps % chunk == 0, "--steps must be a multiple of --chunk"
@@ -287,7 +300,7 @@ def main():
         t0 = time.perf_counter()
         f0 = torch.cuda.Event(enable_timing=True); f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        s2.load_cnf(cnf)                      # host CSR -> device
+        load(s2)                              # host CSR -> device
         s2.init_batch(N * world, seed)
         for _ in range(K_e2e):
             s2.step(1)                        # H2D step scalars, D2H step info
@@ -345,8 +358,12 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_desc(args.config, cnf, N * world), "V": cnf.V, "C": cnf.C, "K": cnf.K,
                    "N_per_gpu": N, "N_global": N * world, "seed": seed,
-                   "parallelism": (f"candidate-sharded x{world} (NCCL exact int64 exchanges)" if world > 1 else
-                                   "single GPU, sharded kernels on a 1-rank NCCL communicator" if args.sharded else "single GPU"),
+                   "parallelism": (f"candidate-sharded x{world}, exact exchanges inside the kernels over NVLink peer "
+                                   "memory" if world > 1 and use_peer else
+                                   f"candidate-sharded x{world} (NCCL exact int64 exchanges)" if world > 1 else
+                                   "single GPU, peer-exchange kernels (self)" if args.peer else
+                                   "single GPU, sharded kernels on a 1-rank NCCL communicator" if args.sharded else
+                                   "single GPU"),
                    "l2": "state (theta, m, v: %.0f MB) larger than L2; no flush" % (12 * cnf.V * N / 1e6),
                    "graph_chunk": chunk},
         "gradient_steps_per_s": args.steps / (ms / 1000.0),

@@ -186,26 +186,12 @@ __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a, uint32_t* __res
 __global__ void k_peer_send_rows(StepArgs a, unsigned gen) {
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= a.V) return;
-    const PeerArgs& px = a.px;
-    const size_t slot = (size_t)px.rank * px.V + v;
-    for (int p = 0; p < px.W; ++p) {
-        st_relaxed_sys(reinterpret_cast<long long*>(px.xb[p] + px.L.qx) + slot, a.Qbuf[v]);
-        st_release_sys(reinterpret_cast<unsigned*>(px.xb[p] + px.L.qf) + slot, gen);
-    }
+    peer_row_send(a.px, 1, v, a.Qbuf[v], gen);
 }
 __global__ void k_peer_recv_rows(StepArgs a, unsigned gen) {
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= a.V) return;
-    const PeerArgs& px = a.px;
-    const long long* xs = reinterpret_cast<const long long*>(px.xb[px.rank] + px.L.qx);
-    const unsigned* fs = reinterpret_cast<const unsigned*>(px.xb[px.rank] + px.L.qf);
-    long long s = 0;
-    for (int r = 0; r < px.W; ++r) {
-        const size_t i = (size_t)r * px.V + v;
-        if (!peer_wait(fs + i, gen, a.ds)) return;
-        s += ld_relaxed_sys(xs + i);
-    }
-    a.Qbuf[v] = s;
+    a.Qbuf[v] = peer_row_recv(a.px, 1, v, gen, a.ds);
 }
 
 // End of a sharded iteration: first-model bookkeeping (global best), step

@@ -48,7 +48,8 @@ __host__ __device__ inline size_t upd_gs_bytes(int KB, int N) { return align16((
 __host__ __device__ inline size_t upd_dpk_words(int N) { return (size_t)N + (N >> 5); }
 __host__ __device__ inline size_t upd_group_bytes(int KB, int N, int rec_cap) {
     const int NDW = KB == 4 ? 1 : 2;
-    return align16((size_t)NDW * upd_dpk_words(N) * 4) + 2 * align16((size_t)rec_cap * 4) + align16((size_t)2 * (N >> 5) * 4) + 128;
+    // dpk | 2 record buffers | sign planes [2 parities][pos, neg][NW] | 128 B scratch
+    return align16((size_t)NDW * upd_dpk_words(N) * 4) + 2 * align16((size_t)rec_cap * 4) + align16((size_t)4 * (N >> 5) * 4) + 128;
 }
 
 // x * 2^s, exact (== scalbn) when 2^s is a normal double.
@@ -228,8 +229,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
     uint32_t* dpk = reinterpret_cast<uint32_t*>(gb);
     uint32_t* rec = reinterpret_cast<uint32_t*>(gb + align16((size_t)(KB == 4 ? 1 : 2) * dpkw * 4));
     const size_t recw = align16((size_t)rec_cap * 4) / 4;            // words per record buffer (two buffers)
-    uint32_t* posw = rec + 2 * recw;
-    uint32_t* negw = posw + NW;
+    uint32_t* posw0 = rec + 2 * recw;                   // [parity][pos | neg][NW] (MODE 2 finishes a row late)
     long long* red = reinterpret_cast<long long*>(gb + grb - 128);                      // 4 + 4 slots
     float* redf = reinterpret_cast<float*>(red + 8);                                    // 4 slots
     int* rowslot = reinterpret_cast<int*>(redf + 4);                                    // 2 slots
@@ -270,6 +270,30 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
                 epsf = sc->epsf, nz = sc->nz, mkeep = sc->mkeep;
     const MethodConsts& mc = a.mc;
 
+    // Row v of theta_{t+1} is complete once its global Q is known: bit planes
+    // (sign(d) = sign(Q), R3) and, by tg 0, Eq. 5's statistics, max |theta|
+    // and the first model's bits.
+    auto finish_row = [&](int vr, long long Qg, const uint32_t* pw, float m2) {
+        const bool dpos = !mc.normalize || Qg >= 0;
+        const uint32_t* src = dpos ? pw : pw + NW;
+        for (int w = tg; w < NW; w += GT) Anext[(size_t)vr * NW + w] = src[w];
+        if (tg == 0) {
+            double dn, rhon;
+            unsigned char gn;
+            row_finish(Qg, mc, &dn, &rhon, &gn);
+            a.rowQ[vr] = Qg; a.rowD[vr] = dn; a.rowRho[vr] = rhon; a.rowGuard[vr] = gn;
+            atomicMax(&a.ds->thmax_bits[(t + 1) & 1], __float_as_uint(m2));
+            const unsigned long long bk = MODE == 2 ? pscal[0] : a.ds->best_key;
+            if ((bk >> 32) == 0ull && (a.ds->sol_step < 0 || a.ds->sol_step == t)) {          // first model: keep its bits (A22)
+                const long long idx = (long long)(bk & 0xffffffffull) - mc.n0;
+                if (idx >= 0 && idx < N)
+                    a.sol[vr] = (unsigned char)((Acur[(size_t)vr * NW + (idx >> 5)] >> (idx & 31)) & 1u);
+            }
+        }
+    };
+    int pend_v = -1, pend_pb = 0;                          // MODE 2: row awaiting its global Q
+    float pend_m2 = 0.0f;
+
     int v = rowslot[1];
     if (v < a.V && a.hub_of[v] < 0) {                      // first row: stage its records now
         const unsigned rb0 = a.occ_ptr[v], re0 = a.occ_ptr[v + 1];
@@ -284,11 +308,13 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
             rowslot[it & 1] = atomicAdd(&a.ds->row_counter, 1);
             const uint32_t rowbytes = (uint32_t)N * 4u;
             prefetch_l2(a.theta + (size_t)v * N, rowbytes);
-            if (MODE == 0) {
+            if (MODE != 1) {
                 prefetch_l2(a.m + (size_t)v * N, rowbytes);
                 prefetch_l2(a.v + (size_t)v * N, rowbytes);
             }
         }
+        uint32_t* posw = posw0 + (MODE == 2 ? (size_t)(it & 1) * 2 * NW : 0);
+        uint32_t* negw = posw + NW;
         const int hub = a.hub_of[v];
         const int2 pn = a.occ_pn[v];
         const int dsum = pn.y - pn.x;                       // sum_r (cneg - cpos)[r]
@@ -337,7 +363,13 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
                 }
             }
         }
+        if (MODE == 2 && pend_v >= 0 && tg == 0)             // previous row's Q, sent a row ago
+            pxs[1] = peer_row_recv(a.px, 1, pend_v, sc->xgen, a.ds);
         gsync(bar, GT);
+        if (MODE == 2 && pend_v >= 0) {
+            finish_row(pend_v, pxs[1], posw0 + (size_t)pend_pb * 2 * NW, pend_m2);
+            pend_v = -1;
+        }
 
         // ---- 3a: G (fp32 FMA chain over exact counts, R27) -> smem; J_v partial
         float* gout = MODE == 1 ? a.Gbuf + (size_t)v * N : nullptr;
@@ -349,7 +381,10 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
         long long Itot = 0;                                  // every thread folds the warp partials
         for (int i = 0; i < ngw; ++i) Itot += red[i];
         if (MODE == 2 && a.px.exchange_rows) {               // J_v over all ranks
-            if (tg == 0) pxs[0] = peer_row_sum(a.px, 0, v, Itot, sc->xgen, a.ds);
+            if (tg == 0) {
+                peer_row_send(a.px, 0, v, Itot, sc->xgen);
+                pxs[0] = peer_row_recv(a.px, 0, v, sc->xgen, a.ds);
+            }
             gsync(bar, GT);
             Itot = pxs[0];
         }
@@ -460,32 +495,26 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
         gsync(bar, GT);
         long long Qtot = 0;
         for (int i = 0; i < ngw; ++i) Qtot += red[4 + i];
-        if (MODE == 2 && a.px.exchange_rows) {               // Q_{t+1,v} over all ranks
-            if (tg == 0) pxs[1] = peer_row_sum(a.px, 1, v, Qtot, sc->xgen, a.ds);
-            gsync(bar, GT);
-            Qtot = pxs[1];
-        }
-        // sign(d_{t+1}) = sign(mu) with sign(0) = +1, i.e. Q >= 0 (R3): the bits
-        // of the next state need no division; tg 0 finishes Eq. 5's statistics.
-        const bool dpos = !mc.normalize || Qtot >= 0;
-        for (int w = tg; w < NW; w += GT) Anext[(size_t)v * NW + w] = dpos ? posw[w] : negw[w];
-        if (tg == 0) {
-            float m2 = 0.0f;
+        float m2 = 0.0f;
+        if (tg == 0)
             for (int i = 0; i < ngw; ++i) m2 = fmaxf(m2, redf[i]);
-            double dn, rhon;
-            unsigned char gn;
-            row_finish(Qtot, mc, &dn, &rhon, &gn);
-            a.rowQ[v] = Qtot; a.rowD[v] = dn; a.rowRho[v] = rhon; a.rowGuard[v] = gn;
-            atomicMax(&a.ds->thmax_bits[(t + 1) & 1], __float_as_uint(m2));
-            const unsigned long long bk = MODE == 2 ? pscal[0] : a.ds->best_key;
-            if ((bk >> 32) == 0ull && (a.ds->sol_step < 0 || a.ds->sol_step == t)) {          // first model: keep its bits (A22)
-                const long long idx = (long long)(bk & 0xffffffffull) - mc.n0;
-                if (idx >= 0 && idx < N)
-                    a.sol[v] = (unsigned char)((Acur[(size_t)v * NW + (idx >> 5)] >> (idx & 31)) & 1u);
-            }
+        if (MODE == 2 && a.px.exchange_rows) {
+            // Q_{t+1,v} over all ranks: send now, finish the row after the
+            // next row's gather (the peers' partials have arrived by then)
+            if (tg == 0) peer_row_send(a.px, 1, v, Qtot, sc->xgen);
+            pend_v = v;
+            pend_pb = it & 1;
+            pend_m2 = m2;
+        } else {
+            finish_row(v, Qtot, posw, m2);
         }
         v = vnext;
         // (the next row's barriers order these smem reads before any reuse)
+    }
+    if (MODE == 2 && pend_v >= 0) {
+        if (tg == 0) pxs[1] = peer_row_recv(a.px, 1, pend_v, sc->xgen, a.ds);
+        gsync(bar, GT);
+        finish_row(pend_v, pxs[1], posw0 + (size_t)pend_pb * 2 * NW, pend_m2);
     }
 }
 

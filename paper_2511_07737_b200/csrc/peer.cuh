@@ -8,9 +8,12 @@
 // order.  Reduced values are int64 (fixed point) or maxima, so every rank
 // computes identical results, bit for bit equal to W = 1.
 //
-// Ordering: slot store (relaxed.sys) -> flag store (release.sys) on the
-// writer; flag load (acquire.sys) -> slot load (relaxed.sys, bypasses L1) on
-// the reader.  Row slots are reused every iteration: a rank writes the rows
+// Row values (J, Q) need no fence: each int64 travels as two u64 words
+// (generation << 32 | 32-bit half), and a naturally aligned 8-byte store is
+// single-copy atomic, so a reader that sees the expected generation in both
+// words has the value (relaxed.sys stores and loads, L1 bypassed).  The
+// per-step scalars use a release-stored flag instead (4 words, once a step).
+// Row slots are reused every iteration: a rank writes the rows
 // of generation g+1 only after receiving every rank's g+1 scalars, which each
 // rank sends after its k_update(g) has completed, so no row slot is
 // overwritten before it is read.  The scalar slots themselves are
@@ -45,6 +48,14 @@ __device__ __forceinline__ long long ld_relaxed_sys(const long long* p) {
     asm volatile("ld.relaxed.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -68,23 +79,44 @@ __device__ __forceinline__ bool peer_wait(const unsigned* flag, unsigned gen, De
     return true;
 }
 
-// All-reduce (sum) of one int64 row value: which = 0 (J) or 1 (Q).
-// Called by one thread.
-__device__ __forceinline__ long long peer_row_sum(const PeerArgs& px, int which, int v, long long val, unsigned gen,
-                                                  DevScalars* ds) {
-    const size_t ox = which ? px.L.qx : px.L.jx, of = which ? px.L.qf : px.L.jf;
-    const size_t slot = (size_t)px.rank * px.V + v;
+// Row all-reduce (sum of one int64 per rank), which = 0 (J) or 1 (Q); one
+// thread sends, later one thread receives (they may be apart in time).
+__device__ __forceinline__ void peer_row_send(const PeerArgs& px, int which, int v, long long val, unsigned gen) {
+    const size_t slot = 2 * ((size_t)px.rank * px.V + v);
+    const unsigned long long g = (unsigned long long)gen << 32;
+    const unsigned long long w0 = g | (unsigned long long)(unsigned)val;
+    const unsigned long long w1 = g | (unsigned long long)(unsigned)((unsigned long long)val >> 32);
     for (int p = 0; p < px.W; ++p) {
-        st_relaxed_sys(reinterpret_cast<long long*>(px.xb[p] + ox) + slot, val);
-        st_release_sys(reinterpret_cast<unsigned*>(px.xb[p] + of) + slot, gen);
+        unsigned long long* d = reinterpret_cast<unsigned long long*>(px.xb[p] + (which ? px.L.qx : px.L.jx)) + slot;
+        st_relaxed_sys_u64(d, w0);
+        st_relaxed_sys_u64(d + 1, w1);
     }
-    const long long* xs = reinterpret_cast<const long long*>(px.xb[px.rank] + ox);
-    const unsigned* fs = reinterpret_cast<const unsigned*>(px.xb[px.rank] + of);
+}
+
+__device__ __forceinline__ long long peer_row_recv(const PeerArgs& px, int which, int v, unsigned gen,
+                                                   DevScalars* ds) {
+    const unsigned long long* xs =
+        reinterpret_cast<const unsigned long long*>(px.xb[px.rank] + (which ? px.L.qx : px.L.jx));
     long long s = 0;
     for (int r = 0; r < px.W; ++r) {
-        const size_t i = (size_t)r * px.V + v;
-        if (!peer_wait(fs + i, gen, ds)) return val;
-        s += ld_relaxed_sys(xs + i);
+        const unsigned long long* q = xs + 2 * ((size_t)r * px.V + v);
+        unsigned long long w0 = ld_relaxed_sys_u64(q), w1 = ld_relaxed_sys_u64(q + 1);
+        if ((unsigned)(w0 >> 32) != gen || (unsigned)(w1 >> 32) != gen) {
+            const unsigned long long t0 = globaltimer_ns();
+            unsigned ns = 32;
+            while ((unsigned)(w0 >> 32) != gen || (unsigned)(w1 >> 32) != gen) {
+                if (*(volatile unsigned*)&ds->xerr) return 0;
+                __nanosleep(ns);
+                if (ns < 1024) ns <<= 1;
+                if (globaltimer_ns() - t0 > kPeerTimeoutNs) {
+                    atomicExch(&ds->xerr, 1u);
+                    return 0;
+                }
+                w0 = ld_relaxed_sys_u64(q);
+                w1 = ld_relaxed_sys_u64(q + 1);
+            }
+        }
+        s += (long long)(((w1 & 0xffffffffull) << 32) | (w0 & 0xffffffffull));
     }
     return s;
 }

@@ -22,11 +22,12 @@ constexpr int kMaxPeers = 8;           // peer-exchange path: ranks (GPUs of one
 // Every rank writes its slot [src = its rank] of every rank's buffer:
 //   S: [2][W] x {~best key, gmax bits, thmax bits, loss S 2^40} + flags [2][W]
 //      (once per step, double-buffered by generation parity)
-//   J, Q: [W][V] int64 row partials + u32 flags [W][V]                   (per row, per step)
-// A flag holds the exchange generation its value belongs to (monotone per
-// context, identical on every rank: the ranks run the same call sequence).
+//   J, Q: [W][V] int64 row partials, each as two self-validating u64 words
+//         (generation << 32 | 32-bit half)                                   (per row, per step)
+// The generation is monotone per context and identical on every rank (the
+// ranks run the same call sequence).
 struct PeerLayout {
-    size_t sx, sf, jx, jf, qx, qf, total;
+    size_t sx, sf, jx, qx, total;
 };
 inline PeerLayout peer_layout(int V, int W) {
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -34,10 +35,8 @@ inline PeerLayout peer_layout(int V, int W) {
     size_t o = 0;
     L.sx = o; o = al(o + (size_t)2 * W * 32);
     L.sf = o; o = al(o + (size_t)2 * W * 4);
-    L.jx = o; o = al(o + (size_t)W * V * 8);
-    L.jf = o; o = al(o + (size_t)W * V * 4);
-    L.qx = o; o = al(o + (size_t)W * V * 8);
-    L.qf = o; o = al(o + (size_t)W * V * 4);
+    L.jx = o; o = al(o + (size_t)W * V * 16);
+    L.qx = o; o = al(o + (size_t)W * V * 16);
     L.total = o;
     return L;
 }
