@@ -5,7 +5,9 @@ path's host logic:
   done by torch.distributed all-reduces, is bit-identical to 1 shard (the
   exchange is exact: int64 sums and maxima);
 * the global export merge (top-M by (unsat, index)) equals the single-rank one;
-* the NCCL unique-id broadcast gives every rank the same id.
+* the NCCL unique-id broadcast gives every rank the same id;
+* the peer path's handle exchange (Solver.connect_peers) hands every rank all
+  W exchange-buffer handles in rank order.
 """
 import os
 import socket
@@ -84,6 +86,22 @@ def _worker(rank, world, port, steps, q):
         obj = [bytes(range(128)) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         out["uid"] = obj[0]
+        # peer-path handle exchange (host logic of Solver.connect_peers)
+        from paper_2511_07737_b200.binding import Solver
+
+        class _Stub:
+            def __init__(self):
+                self.world, self.rank, self.opened = world, rank, None
+
+            def peer_handle(self):
+                return bytes([rank + 1]) * 64
+
+            def peer_open(self, hs):
+                self.opened = list(hs)
+
+        st = _Stub()
+        Solver.connect_peers(st)
+        out["peer_handles"] = st.opened
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -118,3 +136,5 @@ def test_gloo_sharded_oracle_bit_identical(world):
         for r in range(world):
             assert res[r][name]["merged"] == [(int(i), int(x)) for i, x in zip(idx, u)]
     assert res[0]["uid"] == res[1]["uid"] == bytes(range(128))
+    for r in range(world):
+        assert res[r]["peer_handles"] == [bytes([k + 1]) * 64 for k in range(world)]
