@@ -71,6 +71,8 @@ struct tsat_ctx_s {
     double prof_ms[kKernelsPerStep] = {0, 0, 0, 0, 0};
     // k_update launch geometry (configure_kernels)
     int upd_mode = 0, upd_GT = 0, upd_NG = 0, upd_grid = 0, num_sms = 0;
+    int upd_chunk = 0, upd_gs_global = 0;
+    bool chunked = false;               // N too large for the fused kernel: split sequence, no collectives at W = 1
     size_t upd_smem = 0;
     int64_t prof_steps = 0;
     int prof_pending_k = 0;
@@ -168,6 +170,17 @@ Layout make_layout(int V, int N, int KB, int n_hubs, bool sharded, bool peer) {
     return L;
 }
 
+// Whether N candidates per GPU need the chunked split sequence (the fused
+// k_update's shared memory would not hold the batch's g table + 2 groups).
+tsat_status batch_chunked(tsat_ctx ctx, int N, int KB, bool* out) {
+    int optin = 0;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    const int rec_cap = std::max(64, (ctx->cnf.max_rec_words + 63) / 64 * 64);
+    *out = !update_fits_fused(KB, N, rec_cap, optin);
+    return TSAT_OK;
+}
+
 StepArgs step_args(tsat_ctx ctx) {
     StepArgs a{};
     char* w = ctx->ws;
@@ -202,12 +215,14 @@ StepArgs step_args(tsat_ctx ctx) {
     a.uniform_len = ctx->cnf.uniform_len;
     a.num_sms = ctx->num_sms;
     a.upd_mode = ctx->upd_mode;
+    a.upd_chunk = ctx->upd_chunk;
+    a.upd_gs_global = ctx->upd_gs_global;
     a.upd_GT = ctx->upd_GT;
     a.upd_NG = ctx->upd_NG;
     a.upd_grid = ctx->upd_grid;
     a.upd_smem = ctx->upd_smem;
     a.upd_rec_cap = std::max(64, (ctx->cnf.max_rec_words + 63) / 64 * 64);
-    a.sharded = ctx->sharded ? 1 : 0;
+    a.sharded = (ctx->sharded || ctx->chunked) ? 1 : 0;     // kernels: the split (phase A / B) sequence
     a.Gbuf = (float*)(w + L.Gbuf);
     a.Jbuf = (long long*)(w + L.Jbuf);
     a.Qbuf = (long long*)(w + L.Qbuf);
@@ -387,7 +402,8 @@ int launch_segment(tsat_ctx ctx, const StepArgs& a, int seg, const StepScalars* 
         *err = std::string(what) + ": " + cudaGetErrorString(e);
         return 6;
     };
-    if (!ctx->sharded) return ck(launch_step_kernel(seg, a, sc, t, st), "step kernel");
+    if (!ctx->sharded && !ctx->chunked) return ck(launch_step_kernel(seg, a, sc, t, st), "step kernel");
+    const bool comm = ctx->sharded;           // chunked at W = 1: the same sequence without exchanges
     const uint32_t* Acur = (t & 1) ? a.A1 : a.A0;
     uint32_t* Anext = (t & 1) ? a.A0 : a.A1;
     int r = 0;
@@ -395,16 +411,20 @@ int launch_segment(tsat_ctx ctx, const StepArgs& a, int seg, const StepScalars* 
         case 0: return ck(launch_step_kernel(0, a, sc, t, st), "k_clause");
         case 1:
             if ((r = ck(launch_step_kernel(1, a, sc, t, st), "k_gtable"))) return r;
+            if (!comm) return 0;
             if ((r = ck(launch_shard_pack_max(a, sc, st), "k_pack_max"))) return r;
             if ((r = comm_allreduce_max_u64(ctx->comm, a.maxbuf, 3, st, err))) return r;
             return ck(launch_shard_unpack_max(a, sc, st, a.mc.normalize == 2), "k_unpack_max");
         case 2: return ck(launch_step_kernel(2, a, sc, t, st), "k_hub");
         case 3:
+            if (ctx->chunked && (r = ck(cudaMemsetAsync(a.Jbuf, 0, (size_t)a.V * 8, st), "J reset"))) return r;
             if ((r = ck(launch_update_a(a, Acur, sc, st), "k_update(A)"))) return r;
             // normalize 2 (per shard): J and the row sums stay local, only the loss slot is summed
-            if (a.mc.normalize != 2 && (r = comm_allreduce_sum_i64(ctx->comm, a.Jbuf, (size_t)a.V, st, err))) return r;
+            if (comm && a.mc.normalize != 2 && (r = comm_allreduce_sum_i64(ctx->comm, a.Jbuf, (size_t)a.V, st, err)))
+                return r;
             if ((r = ck(launch_update_b(a, Acur, sc, st), "k_update_b"))) return r;
-            if (a.mc.normalize == 2) {
+            if (!comm) {
+            } else if (a.mc.normalize == 2) {
                 if ((r = comm_allreduce_sum_i64(ctx->comm, a.Qbuf + a.V, 1, st, err))) return r;
             } else if ((r = comm_allreduce_sum_i64(ctx->comm, a.Qbuf, (size_t)a.V + 1, st, err))) {
                 return r;
@@ -715,9 +735,13 @@ tsat_status tsat_workspace_bytes(tsat_ctx ctx, int64_t N_global, size_t* bytes) 
     if (N_global >= (1LL << 32)) return fail(ctx, TSAT_E_RANGE, "N_global >= 2^32");
     if ((int64_t)ctx->cnf.V * (N / 32) >= (1LL << 31))
         return fail(ctx, TSAT_E_RANGE, "V * N / 32 >= 2^31 (32-bit bit-plane offsets)");
-    if ((size_t)N * 12 > 200 * 1024) return fail(ctx, TSAT_E_RANGE, "N per GPU > 17066 not supported by the fused update");
     int KB = ctx->cnf.K <= 3 ? 4 : 8;
-    *bytes = make_layout(ctx->cnf.V, (int)N, KB, ctx->cnf.n_hubs, ctx->sharded, ctx->peer).total;
+    bool chunked = false;
+    tsat_status s = batch_chunked(ctx, (int)N, KB, &chunked);
+    if (s != TSAT_OK) return s;
+    if (chunked && ctx->peer)
+        return fail(ctx, TSAT_E_RANGE, "peer path: N per GPU too large for the fused kernel (use more GPUs)");
+    *bytes = make_layout(ctx->cnf.V, (int)N, KB, ctx->cnf.n_hubs, ctx->sharded || chunked, ctx->peer).total;
     return TSAT_OK;
 }
 
@@ -744,7 +768,15 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
     ctx->seed = seed;
     ctx->ws = (char*)ws;
     ctx->ws_bytes = bytes;
-    ctx->L = make_layout(ctx->cnf.V, ctx->N, ctx->KB, ctx->cnf.n_hubs, ctx->sharded, ctx->peer);
+    {
+        bool ch = false;
+        tsat_status s2 = batch_chunked(ctx, ctx->N, ctx->KB, &ch);
+        if (s2 != TSAT_OK) return s2;
+        ctx->chunked = ch;
+    }
+    if (ctx->chunked && ctx->peer)
+        return fail(ctx, TSAT_E_RANGE, "peer path: N per GPU too large for the fused kernel (use more GPUs)");
+    ctx->L = make_layout(ctx->cnf.V, ctx->N, ctx->KB, ctx->cnf.n_hubs, ctx->sharded || ctx->chunked, ctx->peer);
     MethodConsts& mc = ctx->mc;
     mc = MethodConsts{};
     for (int d = 0; d < 8; ++d) mc.E[d] = std::exp(-c.tau * (double)d);
@@ -768,9 +800,11 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
         ctx->upd_grid = g.upd_grid;
         ctx->upd_smem = g.upd_smem;
         ctx->num_sms = g.num_sms;
+        ctx->upd_chunk = g.upd_chunk;
+        ctx->upd_gs_global = g.upd_gs_global;
     }
-    if ((ctx->sharded || ctx->peer) && ctx->upd_mode != 0)
-        return fail(ctx, TSAT_E_RANGE, "sharded path needs the fused k_update geometry (N per GPU too large)");
+    if (ctx->chunked != (ctx->upd_chunk < ctx->N))
+        return fail(ctx, TSAT_E_STATE, "internal: chunking decision changed between layout and launch");
     StepArgs a = step_args(ctx);
     if (ctx->L.hubD != ctx->L.total)
         CK(cudaMemsetAsync(ctx->ws + ctx->L.hubD, 0, ctx->L.total - ctx->L.hubD, ctx->stream));
@@ -1046,9 +1080,10 @@ tsat_status tsat_kernels_per_step(tsat_ctx ctx, int32_t* n) {
     int k = 0;
     k += 1;                                                                     // clause (or accumulator reset)
     k += 1;                                                                     // gtable
-    if (ctx->have_batch && ctx->upd_mode == 0 && ctx->cnf.n_hub_sc > 0) ++k;    // hub
-    if (ctx->have_cnf && ctx->cnf.V > 0) ++k;                                  // update (phase A when sharded)
+    if (ctx->have_batch && ctx->cnf.n_hub_sc > 0) ++k;                         // hub
+    if (ctx->have_cnf && ctx->cnf.V > 0) ++k;                                  // update (phase A when split)
     if (ctx->sharded) k += 5;   // pack/unpack max, update B, rows finish, step end (NCCL's own kernels not counted)
+    else if (ctx->chunked) k += 3;   // update B, rows finish, step end (+ the J reset memset)
     *n = k;
     return TSAT_OK;
 }

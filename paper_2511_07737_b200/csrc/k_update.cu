@@ -120,8 +120,9 @@ __device__ __forceinline__ float fold_ints(const int* hubrow, int N, int n, int 
 // and the int64 fixed-point partial sum of J_v = sum_n G theta (R13).
 template <int KB, bool HUB>
 __device__ __forceinline__ long long pass_fold(const float* __restrict__ trow, uint32_t* dpk, size_t dpkw,
-                                               const float* gs, int* hubrow, int N, int GT, int tg, int dsum,
+                                               const float* gs, int* hubrow, int N, int Nst, int GT, int tg, int dsum,
                                                bool jvalid, float p2, float* __restrict__ gout) {
+    // N candidates from the pointers' origin; Nst = row stride of gs / hubrow
     const float dsumf = (float)dsum;
     long long I = 0;
     float4 th_nx = (4 * tg < N) ? *reinterpret_cast<const float4*>(trow + 4 * tg) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -131,7 +132,7 @@ __device__ __forceinline__ long long pass_fold(const float* __restrict__ trow, u
         const float th[4] = {th4.x, th4.y, th4.z, th4.w};
         float4 g4[KB];
 #pragma unroll
-        for (int r = 0; r < KB; ++r) g4[r] = *reinterpret_cast<const float4*>(gs + (size_t)r * N + n);
+        for (int r = 0; r < KB; ++r) g4[r] = *reinterpret_cast<const float4*>(gs + (size_t)r * Nst + n);
         uint32_t* dp = dpk + n + (n >> 5);
         float Gq[4];
         if (HUB) {
@@ -140,7 +141,7 @@ __device__ __forceinline__ long long pass_fold(const float* __restrict__ trow, u
                 float gq[KB];
 #pragma unroll
                 for (int r = 0; r < KB; ++r) gq[r] = q == 0 ? g4[r].x : q == 1 ? g4[r].y : q == 2 ? g4[r].z : g4[r].w;
-                Gq[q] = fold_ints<KB>(hubrow, N, n + q, dsum, gq);
+                Gq[q] = fold_ints<KB>(hubrow, Nst, n + q, dsum, gq);
             }
         } else {
             // candidate pairs: d_r as floats (exact small integers), then the
@@ -168,7 +169,7 @@ __device__ __forceinline__ long long pass_fold(const float* __restrict__ trow, u
         if (gout) *reinterpret_cast<float4*>(gout + n) = make_float4(Gq[0], Gq[1], Gq[2], Gq[3]);
         if (HUB) {
 #pragma unroll
-            for (int r = 0; r < KB - 1; ++r) *reinterpret_cast<int4*>(hubrow + (size_t)r * N + n) = make_int4(0, 0, 0, 0);
+            for (int r = 0; r < KB - 1; ++r) *reinterpret_cast<int4*>(hubrow + (size_t)r * Nst + n) = make_int4(0, 0, 0, 0);
         }
     }
     return I;
@@ -220,12 +221,18 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
     constexpr int NCTR = KB - 1;
     extern __shared__ __align__(16) unsigned char smem[];
     const int N = a.N, NW = N >> 5, GT = a.upd_GT;
-    const size_t dpkw = upd_dpk_words(N);
-    float* gs = reinterpret_cast<float*>(smem);
+    // work item = (row, chunk of NCH candidates); NCH == N except for batches
+    // too large for shared memory (MODE 1 only), whose g table stays in L2
+    const int NCH = MODE == 1 ? a.upd_chunk : N;
+    const int nch = MODE == 1 ? (N + NCH - 1) / NCH : 1;  // compile-time 1: fused modes keep smem addressing
+    const bool gs_global = MODE == 1 && a.upd_gs_global != 0;
+    const size_t dpkw = upd_dpk_words(NCH);
+    float* gs = gs_global ? a.gtab : reinterpret_cast<float*>(smem);
     const int grp = threadIdx.x / GT, tg = threadIdx.x - grp * GT;
     const int rec_cap = a.upd_rec_cap;
-    const size_t grb = upd_group_bytes(KB, N, rec_cap);
-    unsigned char* gb = smem + upd_gs_bytes(KB, N) + (size_t)grp * grb;
+    const size_t grb = upd_group_bytes(KB, NCH, rec_cap);
+    unsigned char* gb = smem + (gs_global ? 0 : upd_gs_bytes(KB, N)) + (size_t)grp * grb;
+    const int nitems = a.V * nch;
     uint32_t* dpk = reinterpret_cast<uint32_t*>(gb);
     uint32_t* rec = reinterpret_cast<uint32_t*>(gb + align16((size_t)(KB == 4 ? 1 : 2) * dpkw * 4));
     const size_t recw = align16((size_t)rec_cap * 4) / 4;            // words per record buffer (two buffers)
@@ -239,8 +246,9 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
     const bool uni3 = a.uniform_len && a.mc.K == 3 && KB == 4;
 
     // fp32 derivative table of the whole batch -> shared memory
-    for (int i = threadIdx.x * 4; i < KB * N; i += blockDim.x * 4)
-        *reinterpret_cast<float4*>(gs + i) = *reinterpret_cast<const float4*>(a.gtab + i);
+    if (!gs_global)
+        for (int i = threadIdx.x * 4; i < KB * N; i += blockDim.x * 4)
+            *reinterpret_cast<float4*>(gs + i) = *reinterpret_cast<const float4*>(a.gtab + i);
     if (tg == 0) rowslot[1] = atomicAdd(&a.ds->row_counter, 1);
     const long long t = sc->t;
     __shared__ unsigned long long pscal[3];         // MODE 2: global best key, gmax bits, thmax bits
@@ -294,20 +302,24 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
     int pend_v = -1, pend_pb = 0;                          // MODE 2: row awaiting its global Q
     float pend_m2 = 0.0f;
 
-    int v = rowslot[1];
-    if (v < a.V && a.hub_of[v] < 0) {                      // first row: stage its records now
-        const unsigned rb0 = a.occ_ptr[v], re0 = a.occ_ptr[v + 1];
+    int item = rowslot[1];
+    if (item < nitems && a.hub_of[item / nch] < 0) {      // first row: stage its records now
+        const int v0 = item / nch;
+        const unsigned rb0 = a.occ_ptr[v0], re0 = a.occ_ptr[v0 + 1];
         for (unsigned i = tg; i < re0 - rb0; i += GT) rec[i] = a.occ_rec[rb0 + i];
     }
     gsync(bar, GT);
-    for (int it = 0; v < a.V; ++it) {
+    for (int it = 0; item < nitems; ++it) {
+        const int v = item / nch;
+        const int n0c = (item - v * nch) * NCH;            // first candidate of this chunk
+        const int ncand = min(NCH, N - n0c), w0 = n0c >> 5, NWc = ncand >> 5;
         uint32_t* rb_cur = rec + (size_t)(it & 1) * recw;    // this row's records (staged by the previous row)
         uint32_t* rb_nxt = rec + (size_t)((it + 1) & 1) * recw;
         // ---- fetch the next row; prefetch this row's streams into L2
         if (tg == 0) {
             rowslot[it & 1] = atomicAdd(&a.ds->row_counter, 1);
-            const uint32_t rowbytes = (uint32_t)N * 4u;
-            prefetch_l2(a.theta + (size_t)v * N, rowbytes);
+            const uint32_t rowbytes = (uint32_t)ncand * 4u;
+            prefetch_l2(a.theta + (size_t)v * N + n0c, rowbytes);
             if (MODE != 1) {
                 prefetch_l2(a.m + (size_t)v * N, rowbytes);
                 prefetch_l2(a.v + (size_t)v * N, rowbytes);
@@ -333,7 +345,8 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
         // ---- 1+2: bit-sliced gather of the row's occurrences, transpose to bytes
         if (hub < 0) {
             const unsigned nrec = re - rb;
-            for (int w = tg; w < NW; w += GT) {
+            for (int wl = tg; wl < NWc; wl += GT) {
+                const int w = w0 + wl;
                 const uint32_t own = __ldg(Acur + (size_t)v * NW + w);
                 uint32_t cnt[NCTR][kCtr];
                 auto recf = [&](unsigned i) { return rb_cur[i]; };
@@ -353,13 +366,13 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
                 for (int i = 0; i < 32; ++i) T[i] = (i / kCtr < NCTR && i / kCtr < 4) ? cnt[i / kCtr][i % kCtr] : 0u;
                 transpose32(T);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) dpk[33 * w + j] = T[j];
+                for (int j = 0; j < 32; ++j) dpk[33 * wl + j] = T[j];
                 if (KB == 8) {
 #pragma unroll
                     for (int i = 0; i < 32; ++i) T[i] = (4 + i / kCtr < NCTR) ? cnt[4 + i / kCtr][i % kCtr] : 0u;
                     transpose32(T);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) dpk[dpkw + 33 * w + j] = T[j];
+                    for (int j = 0; j < 32; ++j) dpk[dpkw + 33 * wl + j] = T[j];
                 }
             }
         }
@@ -372,9 +385,11 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
         }
 
         // ---- 3a: G (fp32 FMA chain over exact counts, R27) -> smem; J_v partial
-        float* gout = MODE == 1 ? a.Gbuf + (size_t)v * N : nullptr;
-        long long I = hub >= 0 ? pass_fold<KB, true>(trow, dpk, dpkw, gs, hubrow, N, GT, tg, dsum, jvalid, p2, gout)
-                               : pass_fold<KB, false>(trow, dpk, dpkw, gs, hubrow, N, GT, tg, dsum, jvalid, p2, gout);
+        float* gout = MODE == 1 ? a.Gbuf + (size_t)v * N + n0c : nullptr;
+        int* hubc = hubrow ? hubrow + n0c : nullptr;
+        long long I = hub >= 0
+            ? pass_fold<KB, true>(trow + n0c, dpk, dpkw, gs + n0c, hubc, ncand, N, GT, tg, dsum, jvalid, p2, gout)
+            : pass_fold<KB, false>(trow + n0c, dpk, dpkw, gs + n0c, hubc, ncand, N, GT, tg, dsum, jvalid, p2, gout);
         I = warp_sum(I);
         if (lane == 0) red[gw] = I;
         gsync(bar, GT);
@@ -388,7 +403,8 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
             gsync(bar, GT);
             Itot = pxs[0];
         }
-        const int vnext = rowslot[it & 1];
+        const int item_next = rowslot[it & 1];
+        const int vnext = item_next < nitems ? item_next / nch : a.V;
         // stage the next row's records asynchronously (cp.async global -> smem);
         // they land while this row streams, and are waited for before the Q barrier
         if (vnext < a.V && a.hub_of[vnext] < 0) {
@@ -396,11 +412,14 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
             for (unsigned i = tg; i < ne - nb; i += GT) cp_async4(rb_nxt + i, a.occ_rec + nb + i);
         }
         cp_async_commit();
-        if (MODE == 1) {                                     // sharded: J partial out, next row
-            if (tg == 0) a.Jbuf[v] = Itot;
+        if (MODE == 1) {                                     // sharded / chunked: J partial out, next item
+            if (tg == 0) {
+                if (nch > 1) atomicAdd(reinterpret_cast<unsigned long long*>(a.Jbuf + v), (unsigned long long)Itot);
+                else a.Jbuf[v] = Itot;
+            }
             cp_async_wait_all();
             gsync(bar, GT);
-            v = vnext;
+            item = item_next;
             continue;
         }
         double c = 0.0;
@@ -508,7 +527,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update
         } else {
             finish_row(v, Qtot, posw, m2);
         }
-        v = vnext;
+        item = item_next;
         // (the next row's barriers order these smem reads before any reuse)
     }
     if (MODE == 2 && pend_v >= 0) {
@@ -569,150 +588,41 @@ __global__ void __launch_bounds__(32) k_hub(StepArgs a, const uint32_t* __restri
     }
 }
 
-// ------------------------------------------------------------------ fallback: one CTA per row
-// Used when the batch is too large for the fused kernel's shared memory.
-// Thread per candidate; R recomputed per occurrence with broadcast loads.
-template <int KB>
-__global__ void __launch_bounds__(256) k_update_rowcta(StepArgs a, const uint32_t* __restrict__ Acur,
-                                                       uint32_t* __restrict__ Anext,
-                                                       const StepScalars* __restrict__ sc) {
-    extern __shared__ double smem_d[];
-    const int N = a.N;
-    double* Gs = smem_d;
-    float* Ts = reinterpret_cast<float*>(smem_d + N);
-    __shared__ long long sh_s[32];
-    __shared__ float sh_m[32];
-    __shared__ double sh_c, sh_d;
-    const MethodConsts& mc = a.mc;
-    const int v = blockIdx.x;
+// Fused geometry (g table of the batch in smem, one work item per row) when
+// at least two warp groups fit; otherwise work items of NCH candidates with
+// the g table read from L2 (MODE 1, the split sequence; capi.cu).
+bool update_fits_fused(int KB, int N, int rec_cap, int optin) {
     const int NW = N >> 5;
-    const long long t = sc->t;
-    const unsigned rb = a.occ_ptr[v], re = a.occ_ptr[v + 1];
-    const unsigned occ = a.occ_cnt[v];
-    const double rho = a.rowRho[v];
-    const unsigned char guard = a.rowGuard[v];
-    const double gmax = __longlong_as_double((long long)a.ds->gmax_bits);
-    const float thmax = __uint_as_float(a.ds->thmax_bits[t & 1]);
-    int s;
-    float p2;
-    const bool jvalid = jscale(mc.Nnorm, (int)occ, gmax, thmax, &s, &p2);
-    const uint32_t* Arow = Acur + (size_t)v * NW;
-    float* trow = a.theta + (size_t)v * N;
-    float* mrow = a.m + (size_t)v * N;
-    float* vrow = a.v + (size_t)v * N;
-    long long I = 0;
-    for (int n = threadIdx.x; n < N; n += blockDim.x) {
-        const int w = n >> 5, j = n & 31;
-        const uint32_t own = (Arow[w] >> j) & 1u;
-        int cnt[KB];
-#pragma unroll
-        for (int r = 0; r < KB; ++r) cnt[r] = 0;
-        for (unsigned p = rb; p < re;) {
-            const uint32_t hdr = a.occ_rec[p];
-            const uint32_t len = hdr >> 1;
-            uint32_t R = own ^ (hdr & 1u);
-            for (uint32_t i = 1; i < len; ++i) {
-                const uint32_t code = a.occ_rec[p + i];
-                R += ((Acur[(size_t)(code >> 1) * NW + w] >> j) & 1u) ^ (code & 1u);
-            }
-            const int delta = (hdr & 1u) ? 1 : -1;
-#pragma unroll
-            for (int r = 0; r < KB; ++r) cnt[r] += (R == (uint32_t)r) ? delta : 0;
-            p += len;
-        }
-        float G = 0.0f;                                            // R27: fp32 FMA chain
-#pragma unroll
-        for (int r = 0; r < KB; ++r) G = __fmaf_rn((float)cnt[r], a.gtab[(size_t)r * N + n], G);
-        Gs[n] = (double)G;
-        if (jvalid) I += jterm(G, trow[n], p2);
-    }
-    float dummy = 0.0f;
-    block_sum_max(I, dummy, sh_s, sh_m);
-    if (threadIdx.x == 0) {
-        double J = jvalid ? scalbn((double)I, -s) : 0.0;
-        double c = 0.0;
-        if (mc.normalize && !guard) {
-            c = J / (double)mc.Nnorm;
-            c = c * rho;
-            c = c * rho;
-        }
-        sh_c = c;
-    }
-    __syncthreads();
-    const double c = sh_c;
-    const float rhof = __double2float_rn(rho), ncf = -__double2float_rn(c);
-    long long Qn = 0;
-    float mx = 0.0f;
-    for (int n = threadIdx.x; n < N; n += blockDim.x) {
-        const float g = __fmaf_rn((float)Gs[n], rhof, ncf);              // R27b
-        float th = trow[n] * sc->wdf;
-        const float m0 = mrow[n] * sc->mkeep;
-        const float mm = __fmaf_rn(sc->a1, g - m0, m0);
-        const float vb = vrow[n] * sc->b2f;
-        const float vn = __fmaf_rn(sc->a2 * g, g, vb);
-        const float den = __fmul_rn(__fsqrt_rn(vn), sc->rbc2) + sc->epsf;
-        th = th + (sc->nss * mm) / den;
-        if (mc.noise) {
-            const long long ng = mc.n0 + n;
-            uint32_t x[4] = {(uint32_t)(ng >> 2), (uint32_t)v, (uint32_t)(1 + t), 0u};
-            philox4x32_10(x, (uint32_t)mc.seed, (uint32_t)(mc.seed >> 32));
-            const float xi = (float)(x[ng & 3] >> 8) * 5.9604644775390625e-08f - 0.5f;
-            th = th + sc->nz * xi;
-        }
-        trow[n] = th;
-        mrow[n] = mm;
-        vrow[n] = vn;
-        Ts[n] = th;
-        Qn += __double2ll_rn((double)th * 4294967296.0);
-        mx = fmaxf(mx, fabsf(th));
-    }
-    block_sum_max(Qn, mx, sh_s, sh_m);
-    if (threadIdx.x == 0) {
-        double dn, rhon;
-        unsigned char gn;
-        row_finish(Qn, mc, &dn, &rhon, &gn);
-        a.rowQ[v] = Qn; a.rowD[v] = dn; a.rowRho[v] = rhon; a.rowGuard[v] = gn;
-        sh_d = dn;
-        atomicMax(&a.ds->thmax_bits[(t + 1) & 1], __float_as_uint(mx));
-        const unsigned long long bk = a.ds->best_key;
-        if ((bk >> 32) == 0ull && (a.ds->sol_step < 0 || a.ds->sol_step == t)) {
-            const long long idx = (long long)(bk & 0xffffffffull) - mc.n0;
-            if (idx >= 0 && idx < N) a.sol[v] = (unsigned char)((Arow[idx >> 5] >> (idx & 31)) & 1u);
-        }
-    }
-    __syncthreads();
-    const bool dpos = sh_d > 0.0;
-    uint32_t* Anrow = Anext + (size_t)v * NW;
-    for (int n = threadIdx.x; n < N; n += blockDim.x) {
-        const float x = Ts[n];
-        const unsigned wv = __ballot_sync(0xffffffffu, dpos ? (x > 0.0f) : (x < 0.0f));
-        if ((threadIdx.x & 31) == 0) Anrow[n >> 5] = wv;
-    }
+    const int GT = NW >= 128 ? 128 : (NW > 32 ? 64 : 32);
+    const size_t gsb = upd_gs_bytes(KB, N), grb = upd_group_bytes(KB, N, rec_cap);
+    const long long ng = optin > (long long)gsb ? ((long long)optin - (long long)gsb) / (long long)grb : 0;
+    return ng >= 2 || (ng == 1 && GT == 128);
 }
 
-// ------------------------------------------------------------------ configuration + launch
+int update_chunk(int KB, int N) {
+    const int c = KB == 4 ? 4096 : 2048;
+    return N < c ? N : c;
+}
+
 cudaError_t configure_update(StepArgs* a) {
-    const int N = a->N, NW = N >> 5, KB = a->KB;
+    const int N = a->N, KB = a->KB;
     int dev = 0, optin = 0, sms = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
     a->num_sms = sms;
-    const int GT = NW >= 128 ? 128 : (NW > 32 ? 64 : 32);
-    const size_t gsb = upd_gs_bytes(KB, N), grb = upd_group_bytes(KB, N, a->upd_rec_cap);
+    const bool fused = update_fits_fused(KB, N, a->upd_rec_cap, optin);
+    a->upd_chunk = fused ? N : update_chunk(KB, N);
+    a->upd_gs_global = fused ? 0 : 1;
+    const int NWc = a->upd_chunk >> 5;
+    const int GT = NWc >= 128 ? 128 : (NWc > 32 ? 64 : 32);
+    const size_t gsb = fused ? upd_gs_bytes(KB, N) : 0, grb = upd_group_bytes(KB, a->upd_chunk, a->upd_rec_cap);
     long long ng = optin > (long long)gsb ? ((long long)optin - (long long)gsb) / (long long)grb : 0;
     const int max_threads = KB == 4 ? TSAT_UPD_THREADS4 : 512;   // register budget (launch bounds)
     ng = ng < max_threads / GT ? ng : max_threads / GT;
     if (GT > 32) ng = ng < 15 ? ng : 15;          // named barriers 1..15 (warp groups use __syncwarp)
-    if (ng < 2 && !(ng == 1 && GT == 128)) {
-        a->upd_mode = 1;                          // too large for the fused kernel
-        size_t smem = (size_t)N * (sizeof(double) + sizeof(float));
-        if ((e = cudaFuncSetAttribute(k_update_rowcta<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
-        if ((e = cudaFuncSetAttribute(k_update_rowcta<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
-        a->upd_smem = smem;
-        return cudaSuccess;
-    }
+    if (ng < 1) return cudaErrorInvalidConfiguration;
     a->upd_mode = 0;
     a->upd_GT = GT;
     a->upd_NG = (int)ng;
@@ -750,19 +660,14 @@ cudaError_t launch_hub(const StepArgs& a, const uint32_t* Acur, cudaStream_t st)
 cudaError_t launch_update(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
                           cudaStream_t st) {
     if (a.V == 0) return cudaGetLastError();
-    if (a.upd_mode == 0) {
-        const int threads = a.upd_GT * a.upd_NG;
-        if (a.peer) {
-            if (a.KB == 4) k_update<4, 2><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
-            else k_update<8, 2><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
-        } else if (a.KB == 4) {
-            k_update<4, 0><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
-        } else {
-            k_update<8, 0><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
-        }
+    const int threads = a.upd_GT * a.upd_NG;
+    if (a.peer) {
+        if (a.KB == 4) k_update<4, 2><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
+        else k_update<8, 2><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
+    } else if (a.KB == 4) {
+        k_update<4, 0><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
     } else {
-        if (a.KB == 4) k_update_rowcta<4><<<a.V, 256, a.upd_smem, st>>>(a, Acur, Anext, sc);
-        else k_update_rowcta<8><<<a.V, 256, a.upd_smem, st>>>(a, Acur, Anext, sc);
+        k_update<8, 0><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
     }
     return cudaGetLastError();
 }

@@ -156,7 +156,9 @@ struct StepArgs {
     int KB;
     int uniform_len;                 // every clause has exactly K literals
     int num_sms;
-    int upd_mode;                    // 0 = fused persistent (v2), 1 = CTA-per-row fallback (v1)
+    int upd_mode;                    // 0 (persistent k_update; kept for the ABI's geometry report)
+    int upd_chunk;                   // candidates per k_update work item (== N: fused; < N: split sequence)
+    int upd_gs_global;               // g table read from global memory (chunked)
     int upd_GT, upd_NG, upd_grid;    // v2 launch geometry
     int upd_rec_cap;                 // record words a group stages per row (max over non-hub rows)
     size_t upd_smem;
@@ -197,6 +199,8 @@ cudaError_t launch_update_a(const StepArgs& a, const uint32_t* Acur, const StepS
 cudaError_t launch_update_b(const StepArgs& a, const uint32_t* Acur, const StepScalars* sc, cudaStream_t st);
 cudaError_t launch_rows_partial(const StepArgs& a, const float* theta, unsigned int* thmax_bits, cudaStream_t st);
 cudaError_t launch_rows_finish(const StepArgs& a, uint32_t* Anext, cudaStream_t st);
+// whether the fused k_update geometry fits (else: chunked split sequence)
+bool update_fits_fused(int KB, int N, int rec_cap, int optin);
 // peer path: exchange of Qbuf[0..V) row partials (init / set_state), gen = exchange generation
 cudaError_t launch_peer_rows_exchange(const StepArgs& a, unsigned gen, cudaStream_t st);
 cudaError_t launch_step_end_sharded(const StepArgs& a, const StepScalars* sc, cudaStream_t st);

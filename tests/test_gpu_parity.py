@@ -222,10 +222,11 @@ def test_enumeration_all_assignments_v20():
     assert unsat.min() == 0
 
 
-@pytest.mark.parametrize("name", ["c3", "c4"])
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
 def test_full_size_properties(name):
-    """Configs c3/c4 at full size: init rows equal the oracle's; unsat counts
-    equal direct evaluation of the exported model bits (zero unsat => model)."""
+    """Configs c3/c4/c5 at full size (c5: N = 65536 on one GPU, 26 GB of
+    state, the chunked split sequence): init rows equal the oracle's; unsat
+    counts equal direct evaluation of the exported model bits."""
     cnf, cfg = make_config(name)
     N = cfg["N"]
     from paper_2511_07737_b200 import Solver
@@ -233,7 +234,7 @@ def test_full_size_properties(name):
     s.load_cnf(cnf)
     s.init_batch(N, cfg["seed"])
     rows = 64
-    th0 = s.get_state()[0][:rows]
+    th0 = s.get_rows(np.arange(rows, dtype=np.int32))[0]
     ref, _, _ = O.init_theta(rows, N, cfg["seed"])
     assert ulp_diff(th0, ref).max() <= 1
     info = s.step(2)
@@ -391,18 +392,31 @@ def test_sharded_equals_fused_c2():
 
 
 # ---------------------------------------------------------------- other code paths
-@pytest.mark.parametrize("kind", ["kb4", "kb8"])
-def test_fallback_row_cta_path(kind):
+@pytest.mark.parametrize("kind", ["kb4", "kb8", "kb4-ragged"])
+def test_chunked_large_batch_path(kind):
     """Batches too large for the fused kernel's shared memory (the g table of
-    N candidates) use the row-per-CTA k_update; same canonical results."""
+    N candidates) run the split sequence with k_update work items of 4096
+    (KB = 8: 2048) candidates, the g table read from L2 and exact int64 J
+    atomics; same canonical results (also with a ragged last chunk)."""
     if kind == "kb4":
-        cnf, N = planted_ksat(60, 250, 3, 2), 16384        # g table 256 KB > smem
+        cnf, N = planted_ksat(60, 250, 3, 2), 16384        # g table 256 KB > smem: 4 chunks
+    elif kind == "kb8":
+        cnf, N = industrial_cnf(80, 300, 6), 8192          # KB = 8: 256 KB, 4 chunks
     else:
-        cnf, N = industrial_cnf(80, 300, 6), 8192          # KB = 8: 256 KB
+        cnf, N = planted_ksat(70, 290, 3, 5), 17408        # 4 x 4096 + 1024
     s, o = make_pair(cnf, N, 3)
+    base = 3 if cnf.V else 0
+    assert s.kernels_per_step() >= base + 3               # update B, rows finish, step end
     s.set_state(o.theta, o.m, o.v, 0)
     for _ in range(4):
-        compare_step(s, o, cnf, "fallback-" + kind)
+        compare_step(s, o, cnf, "chunked-" + kind)
+    info = s.step(5)
+    for _ in range(5):
+        ref = o.step()
+    th, m, v, _ = s.get_state()
+    np.testing.assert_array_equal(th, o.theta)
+    np.testing.assert_array_equal(v, o.v)
+    assert (info.best_unsat, info.best_idx) == (ref.best_unsat, ref.best_idx)
 
 
 def test_hub_rows_parity_and_export():
