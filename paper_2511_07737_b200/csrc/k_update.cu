@@ -30,6 +30,9 @@
 #define TSAT_3B_UNROLL 2
 #endif
 constexpr int kUnroll3b = TSAT_3B_UNROLL;
+#ifndef TSAT_UPD_THREADS8
+#define TSAT_UPD_THREADS8 512        // KB = 8 block size bound
+#endif
 #ifndef TSAT_UPD_THREADS4
 #define TSAT_UPD_THREADS4 768       // KB = 4 block size bound (register budget)
 #endif
@@ -214,7 +217,7 @@ __device__ __forceinline__ void gsync(int bar, int GT) {
 // and the tail stay balanced); tg 0 fetches the next row at the start of the
 // current one into a parity-double-buffered slot, read after the J barrier.
 template <int KB, int MODE>
-__global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : 512, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
+__global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS8, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
                                                                     uint32_t* __restrict__ Anext,
                                                                     const StepScalars* __restrict__ sc) {
     constexpr int NP = (KB == 4) ? 2 : 3;
@@ -619,7 +622,7 @@ cudaError_t configure_update(StepArgs* a) {
     const int GT = NWc >= 128 ? 128 : (NWc > 32 ? 64 : 32);
     const size_t gsb = fused ? upd_gs_bytes(KB, N) : 0, grb = upd_group_bytes(KB, a->upd_chunk, a->upd_rec_cap);
     long long ng = optin > (long long)gsb ? ((long long)optin - (long long)gsb) / (long long)grb : 0;
-    const int max_threads = KB == 4 ? TSAT_UPD_THREADS4 : 512;   // register budget (launch bounds)
+    const int max_threads = KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS8;   // register budget (launch bounds)
     ng = ng < max_threads / GT ? ng : max_threads / GT;
     if (GT > 32) ng = ng < 15 ? ng : 15;          // named barriers 1..15 (warp groups use __syncwarp)
     if (ng < 1) return cudaErrorInvalidConfiguration;
