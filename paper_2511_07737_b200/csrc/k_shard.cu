@@ -191,7 +191,7 @@ __global__ void k_peer_send_rows(StepArgs a, unsigned gen) {
 __global__ void k_peer_recv_rows(StepArgs a, unsigned gen) {
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= a.V) return;
-    a.Qbuf[v] = peer_row_recv(a.px, 1, v, gen, a.ds);
+    a.Qbuf[v] = peer_row_recv(a.px, 1, v, gen, a.ds, a.Qbuf[v]);
 }
 
 // End of a sharded iteration: first-model bookkeeping (global best), step

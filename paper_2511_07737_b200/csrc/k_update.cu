@@ -256,8 +256,11 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
     const long long t = sc->t;
     __shared__ unsigned long long pscal[3];         // MODE 2: global best key, gmax bits, thmax bits
     if (MODE == 2 && threadIdx.x == 0) {
+        const unsigned long long own[4] = {~a.ds->best_key, a.ds->gmax_bits,
+                                           (unsigned long long)a.ds->thmax_bits[t & 1],
+                                           (unsigned long long)a.ds->loss_fx};
         unsigned long long x[4];
-        peer_recv_scalars(a.px, sc->xgen, a.ds, x);
+        peer_recv_scalars(a.px, sc->xgen, a.ds, own, x);
         pscal[0] = ~x[0];
         pscal[1] = a.px.exchange_rows ? x[1] : a.ds->gmax_bits;           // per shard: J scale stays local
         pscal[2] = a.px.exchange_rows ? x[2] : (unsigned long long)a.ds->thmax_bits[t & 1];
@@ -304,6 +307,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
     };
     int pend_v = -1, pend_pb = 0;                          // MODE 2: row awaiting its global Q
     float pend_m2 = 0.0f;
+    long long pend_q = 0;
 
     int item = rowslot[1];
     if (item < nitems && a.hub_of[item / nch] < 0) {      // first row: stage its records now
@@ -380,7 +384,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
             }
         }
         if (MODE == 2 && pend_v >= 0 && tg == 0)             // previous row's Q, sent a row ago
-            pxs[1] = peer_row_recv(a.px, 1, pend_v, sc->xgen, a.ds);
+            pxs[1] = peer_row_recv(a.px, 1, pend_v, sc->xgen, a.ds, pend_q);
         gsync(bar, GT);
         if (MODE == 2 && pend_v >= 0) {
             finish_row(pend_v, pxs[1], posw0 + (size_t)pend_pb * 2 * NW, pend_m2);
@@ -399,12 +403,9 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
         long long Itot = 0;                                  // every thread folds the warp partials
         for (int i = 0; i < ngw; ++i) Itot += red[i];
         if (MODE == 2 && a.px.exchange_rows) {               // J_v over all ranks
-            if (tg == 0) {
-                peer_row_send(a.px, 0, v, Itot, sc->xgen);
-                pxs[0] = peer_row_recv(a.px, 0, v, sc->xgen, a.ds);
-            }
-            gsync(bar, GT);
-            Itot = pxs[0];
+            // every thread adds the W - 1 remote partials itself: no broadcast barrier
+            if (tg == 0) peer_row_send(a.px, 0, v, Itot, sc->xgen);
+            Itot = peer_row_recv(a.px, 0, v, sc->xgen, a.ds, Itot);
         }
         const int item_next = rowslot[it & 1];
         const int vnext = item_next < nitems ? item_next / nch : a.V;
@@ -527,6 +528,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
             pend_v = v;
             pend_pb = it & 1;
             pend_m2 = m2;
+            pend_q = Qtot;
         } else {
             finish_row(v, Qtot, posw, m2);
         }
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
         // (the next row's barriers order these smem reads before any reuse)
     }
     if (MODE == 2 && pend_v >= 0) {
-        if (tg == 0) pxs[1] = peer_row_recv(a.px, 1, pend_v, sc->xgen, a.ds);
+        if (tg == 0) pxs[1] = peer_row_recv(a.px, 1, pend_v, sc->xgen, a.ds, pend_q);
         gsync(bar, GT);
         finish_row(pend_v, pxs[1], posw0 + (size_t)pend_pb * 2 * NW, pend_m2);
     }

@@ -80,13 +80,17 @@ __device__ __forceinline__ bool peer_wait(const unsigned* flag, unsigned gen, De
 }
 
 // Row all-reduce (sum of one int64 per rank), which = 0 (J) or 1 (Q); one
-// thread sends, later one thread receives (they may be apart in time).
+// thread sends, later one thread receives (they may be apart in time).  A
+// rank's own partial never goes through memory: the receiver adds it locally
+// (int64 sums are exact in any order), so only the W - 1 remote slots are
+// written and awaited.
 __device__ __forceinline__ void peer_row_send(const PeerArgs& px, int which, int v, long long val, unsigned gen) {
     const size_t slot = 2 * ((size_t)px.rank * px.V + v);
     const unsigned long long g = (unsigned long long)gen << 32;
     const unsigned long long w0 = g | (unsigned long long)(unsigned)val;
     const unsigned long long w1 = g | (unsigned long long)(unsigned)((unsigned long long)val >> 32);
     for (int p = 0; p < px.W; ++p) {
+        if (p == px.rank) continue;
         unsigned long long* d = reinterpret_cast<unsigned long long*>(px.xb[p] + (which ? px.L.qx : px.L.jx)) + slot;
         st_relaxed_sys_u64(d, w0);
         st_relaxed_sys_u64(d + 1, w1);
@@ -94,11 +98,12 @@ __device__ __forceinline__ void peer_row_send(const PeerArgs& px, int which, int
 }
 
 __device__ __forceinline__ long long peer_row_recv(const PeerArgs& px, int which, int v, unsigned gen,
-                                                   DevScalars* ds) {
+                                                   DevScalars* ds, long long own) {
     const unsigned long long* xs =
         reinterpret_cast<const unsigned long long*>(px.xb[px.rank] + (which ? px.L.qx : px.L.jx));
-    long long s = 0;
+    long long s = own;
     for (int r = 0; r < px.W; ++r) {
+        if (r == px.rank) continue;
         const unsigned long long* q = xs + 2 * ((size_t)r * px.V + v);
         unsigned long long w0 = ld_relaxed_sys_u64(q), w1 = ld_relaxed_sys_u64(q + 1);
         if ((unsigned)(w0 >> 32) != gen || (unsigned)(w1 >> 32) != gen) {
@@ -121,10 +126,12 @@ __device__ __forceinline__ long long peer_row_recv(const PeerArgs& px, int which
     return s;
 }
 
-// Per-iteration scalars: x = {~best key, gmax bits, thmax bits, loss fixed point}.
+// Per-iteration scalars: x = {~best key, gmax bits, thmax bits, loss fixed point};
+// the own rank's values are combined locally by the receiver.
 __device__ __forceinline__ void peer_send_scalars(const PeerArgs& px, const unsigned long long (&x)[4], unsigned gen) {
     const int par = (int)(gen & 1u);
     for (int p = 0; p < px.W; ++p) {
+        if (p == px.rank) continue;
         long long* d = reinterpret_cast<long long*>(px.xb[p] + px.L.sx) + 4 * ((size_t)par * px.W + px.rank);
 #pragma unroll
         for (int k = 0; k < 4; ++k) st_relaxed_sys(d + k, (long long)x[k]);
@@ -135,12 +142,14 @@ __device__ __forceinline__ void peer_send_scalars(const PeerArgs& px, const unsi
 // Combine: max of ~key, gmax, thmax (non-negative bit patterns order like
 // their values); sum of the loss.  Returns false on timeout.
 __device__ __forceinline__ bool peer_recv_scalars(const PeerArgs& px, unsigned gen, DevScalars* ds,
-                                                  unsigned long long (&out)[4]) {
+                                                  const unsigned long long (&own)[4], unsigned long long (&out)[4]) {
     const int par = (int)(gen & 1u);
     const long long* xs = reinterpret_cast<const long long*>(px.xb[px.rank] + px.L.sx) + (size_t)4 * par * px.W;
     const unsigned* fs = reinterpret_cast<const unsigned*>(px.xb[px.rank] + px.L.sf) + (size_t)par * px.W;
-    out[0] = out[1] = out[2] = out[3] = 0ull;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) out[k] = own[k];
     for (int r = 0; r < px.W; ++r) {
+        if (r == px.rank) continue;
         if (!peer_wait(fs + r, gen, ds)) return false;
         unsigned long long x[4];
 #pragma unroll
