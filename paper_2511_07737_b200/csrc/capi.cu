@@ -21,6 +21,7 @@ using namespace tsat;
 
 struct DevCnf {
     uint32_t *cptr = nullptr, *clit = nullptr, *occ_ptr = nullptr, *occ_rec = nullptr, *occ_cnt = nullptr;
+    uint32_t *bat_ptr = nullptr, *bat_rec = nullptr;
     int2* occ_pn = nullptr;
     int* hub_of = nullptr;
     int4* hub_sc = nullptr;
@@ -207,6 +208,8 @@ StepArgs step_args(tsat_ctx ctx) {
     a.occ_ptr = ctx->dcnf.occ_ptr;
     a.occ_rec = ctx->dcnf.occ_rec;
     a.occ_cnt = ctx->dcnf.occ_cnt;
+    a.upd_ptr = ctx->cnf.batched ? ctx->dcnf.bat_ptr : ctx->dcnf.occ_ptr;
+    a.upd_rec = ctx->cnf.batched ? ctx->dcnf.bat_rec : ctx->dcnf.occ_rec;
     a.occ_pn = ctx->dcnf.occ_pn;
     a.hub_of = ctx->dcnf.hub_of;
     a.hub_sc = ctx->dcnf.hub_sc;
@@ -282,6 +285,8 @@ void free_cnf(tsat_ctx ctx) {
     cudaFree(ctx->dcnf.clit);
     cudaFree(ctx->dcnf.occ_ptr);
     cudaFree(ctx->dcnf.occ_rec);
+    cudaFree(ctx->dcnf.bat_ptr);
+    cudaFree(ctx->dcnf.bat_rec);
     cudaFree(ctx->dcnf.occ_cnt);
     cudaFree(ctx->dcnf.occ_pn);
     cudaFree(ctx->dcnf.hub_of);
@@ -328,6 +333,10 @@ tsat_status upload_cnf(tsat_ctx ctx, HostCnf&& h) {
     CK(up(&ctx->dcnf.occ_ptr, c.occ_ptr));
     CK(up(&ctx->dcnf.occ_rec, c.occ_rec));
     CK(up(&ctx->dcnf.occ_cnt, c.occ_cnt));
+    if (c.batched) {
+        CK(up(&ctx->dcnf.bat_ptr, c.bat_ptr));
+        CK(up(&ctx->dcnf.bat_rec, c.bat_rec));
+    }
     auto upi = [&](void** dst, const std::vector<int32_t>& src) -> cudaError_t {
         size_t bytes = std::max<size_t>(src.size(), 4) * 4;
         cudaError_t e = cudaMalloc(dst, bytes);

@@ -370,4 +370,58 @@ __device__ __forceinline__ void count_uni3(uint32_t (&cnt)[NCTR][B], RecFn rec, 
     }
 }
 
+// count_occurrences over batched records (host_cnf.cpp build_batched): every
+// instance except uniform 3-SAT.  A batch holds up to 4 same-sign records
+// padded to the longest; its gathers are issued two literal steps (8 loads)
+// at a time, absent records start at the all-ones count KB - 1 = 2^NP - 1
+// (the derived bin, never counted), and each bin takes one carry-save sum4
+// and one counter update per batch.
+template <int NP, int NCTR, int B, typename RecFn>
+__device__ __forceinline__ void count_batched(uint32_t (&cnt)[NCTR][B], RecFn rec, unsigned nwords, uint32_t own,
+                                              const uint32_t* __restrict__ Acur, unsigned NW, unsigned w) {
+    static_assert(NCTR == (1 << NP) - 1, "absent records rely on bin 2^NP - 1 being derived");
+#pragma unroll
+    for (int r = 0; r < NCTR; ++r)
+#pragma unroll
+        for (int b = 0; b < B; ++b) cnt[r][b] = 0u;
+    auto ld = [&](uint32_t code) { return __ldg(Acur + ((code >> 1) * NW + w)) ^ (0u - (code & 1u)); };
+    unsigned p = 0;
+    while (p < nwords) {
+        const uint32_t hdr = rec(p);
+        const unsigned J = hdr >> 4, nk = (hdr >> 1) & 7u;
+        const bool neg = (hdr & 1u) != 0u;
+        const uint32_t os = neg ? ~own : own;              // own literal's value in this section
+        uint32_t sp[4][NP];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool on = (unsigned)k < nk;
+            sp[k][0] = on ? os : 0xffffffffu;
+#pragma unroll
+            for (int q = 1; q < NP; ++q) sp[k][q] = on ? 0u : 0xffffffffu;
+        }
+        for (unsigned j = 0; j < J; j += 2) {
+            const unsigned q0 = p + 1 + 4 * j;
+            const bool two = j + 1 < J;
+            uint32_t x[8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) x[k] = ld(rec(q0 + k));
+#pragma unroll
+            for (int k = 0; k < 4; ++k) x[4 + k] = two ? ld(rec(q0 + 4 + k)) : 0u;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                bs_add<NP>(sp[k], x[k]);
+                bs_add<NP>(sp[k], x[4 + k]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < NCTR; ++r) {
+            uint32_t s0, s1, s2;
+            sum4(bs_eq<NP>(sp[0], r), bs_eq<NP>(sp[1], r), bs_eq<NP>(sp[2], r), bs_eq<NP>(sp[3], r), s0, s1, s2);
+            if (neg) vc_add3<B>(cnt[r], s0, s1, s2);
+            else vc_sub3<B>(cnt[r], s0, s1, s2);
+        }
+        p += 1 + 4 * J;
+    }
+}
+
 }  // namespace tsat

@@ -136,6 +136,51 @@ int parse_dimacs(const char* text, size_t len, int32_t* V_out, std::vector<int64
     return 0;
 }
 
+// Batched occurrence records (k_update's general gather): per row and sign
+// section (negated first), the records sorted by clause length, longest first
+// (stable; the counts do not depend on the order, R12), cut into batches of
+// 4.  A batch is a header word (J << 4) | (count << 1) | negated, count =
+// records in the batch (1..4), J = longest length - 1, then J x 4 literal
+// codes [j][k] = the (j+1)-th other literal of record k, or the padding code
+// V << 1 (row V of each bit-plane buffer is all zero, so it adds nothing) for
+// a shorter or absent record.  The 4 records' gathers of one j are
+// independent, and one batch is one carry-save sum4 per bin.
+static void build_batched(HostCnf* hp) {
+    HostCnf& h = *hp;
+    const int32_t V = h.V;
+    const uint32_t pad = (uint32_t)V << 1;
+    h.bat_ptr.assign((size_t)V + 1, 0);
+    h.bat_rec.clear();
+    std::vector<uint32_t> sec;
+    for (int32_t v = 0; v < V; ++v) {
+        h.bat_ptr[v] = (uint32_t)h.bat_rec.size();
+        const uint32_t b = h.occ_ptr[v], e = h.occ_ptr[v + 1];
+        for (int sidx = 0; sidx < 2; ++sidx) {
+            const uint32_t neg = 1 - sidx;                       // negated section, then positive
+            sec.clear();
+            for (uint32_t p = b; p < e; p += h.occ_rec[p] >> 1)
+                if ((h.occ_rec[p] & 1u) == neg) sec.push_back(p);
+            std::stable_sort(sec.begin(), sec.end(),
+                             [&](uint32_t x, uint32_t y) { return (h.occ_rec[x] >> 1) > (h.occ_rec[y] >> 1); });
+            for (size_t i = 0; i < sec.size(); i += 4) {
+                const uint32_t cnt = (uint32_t)std::min<size_t>(4, sec.size() - i);
+                const uint32_t J = (h.occ_rec[sec[i]] >> 1) - 1;
+                h.bat_rec.push_back((J << 4) | (cnt << 1) | neg);
+                for (uint32_t j = 0; j < J; ++j)
+                    for (uint32_t k = 0; k < 4; ++k) {
+                        uint32_t code = pad;
+                        if (k < cnt) {
+                            const uint32_t p = sec[i + k];
+                            if (j + 1 < (h.occ_rec[p] >> 1)) code = h.occ_rec[p + 1 + j];
+                        }
+                        h.bat_rec.push_back(code);
+                    }
+            }
+        }
+    }
+    h.bat_ptr[V] = (uint32_t)h.bat_rec.size();
+}
+
 int build_cnf(int32_t V, int64_t C, const int64_t* ptr, const int32_t* lits, HostCnf* out, std::string* msg) {
     if (V < 0 || C < 0 || (C > 0 && (!ptr || (!lits && ptr[C] > 0)))) { *msg = "bad CNF arrays"; return 1; }
     if (V >= (1 << 29)) { *msg = "V too large (>= 2^29)"; return 3; }
@@ -228,11 +273,21 @@ int build_cnf(int32_t V, int64_t C, const int64_t* ptr, const int32_t* lits, Hos
         uint32_t code = h.clause_lit[i];
         h.occ_pn[(size_t)(code >> 1) * 2 + (code & 1u)] += 1;
     }
+    h.uniform_len = 1;
+    for (int64_t c = 0; c < C; ++c)
+        if ((int32_t)(h.clause_ptr[c + 1] - h.clause_ptr[c]) != h.K) { h.uniform_len = 0; break; }
+    // k_update stages uniform 3-SAT rows as plain records, every other
+    // instance as batched records (build_batched)
+    h.batched = !(h.uniform_len && h.K == 3);
+    if (h.batched) build_batched(&h);
+    const std::vector<uint32_t>& sptr = h.batched ? h.bat_ptr : h.occ_ptr;
     h.hub_of.assign((size_t)V, -1);
     for (int32_t v = 0; v < V; ++v) {
-        bool hub = h.occ_pn[2 * v] > 127 || h.occ_pn[2 * v + 1] > 127 || (h.occ_ptr[v + 1] - h.occ_ptr[v]) > (uint32_t)kRecCap;
+        const uint32_t staged = sptr[v + 1] - sptr[v];
+        bool hub = h.occ_pn[2 * v] > 127 || h.occ_pn[2 * v + 1] > 127 || (h.occ_ptr[v + 1] - h.occ_ptr[v]) > (uint32_t)kRecCap ||
+                   staged > (uint32_t)kRecCap;
         if (!hub) {
-            h.max_rec_words = std::max<int32_t>(h.max_rec_words, (int32_t)(h.occ_ptr[v + 1] - h.occ_ptr[v]));
+            h.max_rec_words = std::max<int32_t>(h.max_rec_words, (int32_t)staged);
             continue;
         }
         int32_t hid = h.n_hubs++;
@@ -249,9 +304,6 @@ int build_cnf(int32_t V, int64_t C, const int64_t* ptr, const int32_t* lits, Hos
         }
     }
     h.n_hub_sc = (int32_t)(h.hub_sc.size() / 4);
-    h.uniform_len = 1;
-    for (int64_t c = 0; c < C; ++c)
-        if ((int32_t)(h.clause_ptr[c + 1] - h.clause_ptr[c]) != h.K) { h.uniform_len = 0; break; }
     *out = std::move(h);
     return 0;
 }

@@ -312,8 +312,8 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
     int item = rowslot[1];
     if (item < nitems && a.hub_of[item / nch] < 0) {      // first row: stage its records now
         const int v0 = item / nch;
-        const unsigned rb0 = a.occ_ptr[v0], re0 = a.occ_ptr[v0 + 1];
-        for (unsigned i = tg; i < re0 - rb0; i += GT) rec[i] = a.occ_rec[rb0 + i];
+        const unsigned rb0 = a.upd_ptr[v0], re0 = a.upd_ptr[v0 + 1];
+        for (unsigned i = tg; i < re0 - rb0; i += GT) rec[i] = a.upd_rec[rb0 + i];
     }
     gsync(bar, GT);
     for (int it = 0; item < nitems; ++it) {
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
         const int hub = a.hub_of[v];
         const int2 pn = a.occ_pn[v];
         const int dsum = pn.y - pn.x;                       // sum_r (cneg - cpos)[r]
-        const unsigned rb = a.occ_ptr[v], re = a.occ_ptr[v + 1];
+        const unsigned rb = a.upd_ptr[v], re = a.upd_ptr[v + 1];
         const double rho = a.rowRho[v];
         const unsigned char guard = a.rowGuard[v];
         const int occ = pn.x + pn.y;
@@ -357,8 +357,6 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
                 const uint32_t own = __ldg(Acur + (size_t)v * NW + w);
                 uint32_t cnt[NCTR][kCtr];
                 auto recf = [&](unsigned i) { return rb_cur[i]; };
-                // KB = 8 rows are short (hub rows go to k_hub) and the kernel is
-                // I-cache bound there: count one record at a time
                 if (uni3) {
 #if TSAT_UNI3 == 0
                     count_occurrences<NP, NCTR, kCtr, true, true>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w);
@@ -367,7 +365,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
                                                           (unsigned)NW, (unsigned)w);
 #endif
                 }
-                else count_occurrences<NP, NCTR, kCtr, false, KB == 4>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w);
+                else count_batched<NP, NCTR, kCtr>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w);
                 uint32_t T[32];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) T[i] = (i / kCtr < NCTR && i / kCtr < 4) ? cnt[i / kCtr][i % kCtr] : 0u;
@@ -412,8 +410,8 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
         // stage the next row's records asynchronously (cp.async global -> smem);
         // they land while this row streams, and are waited for before the Q barrier
         if (vnext < a.V && a.hub_of[vnext] < 0) {
-            const unsigned nb = a.occ_ptr[vnext], ne = a.occ_ptr[vnext + 1];
-            for (unsigned i = tg; i < ne - nb; i += GT) cp_async4(rb_nxt + i, a.occ_rec + nb + i);
+            const unsigned nb = a.upd_ptr[vnext], ne = a.upd_ptr[vnext + 1];
+            for (unsigned i = tg; i < ne - nb; i += GT) cp_async4(rb_nxt + i, a.upd_rec + nb + i);
         }
         cp_async_commit();
         if (MODE == 1) {                                     // sharded / chunked: J partial out, next item

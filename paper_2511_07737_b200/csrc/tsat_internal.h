@@ -72,7 +72,12 @@ struct HostCnf {
     int64_t n_warnings = 0, n_tautologies = 0, n_duplicates = 0;
     int32_t has_empty = 0;
     int32_t uniform_len = 0;            // every clause has exactly K literals
-    int32_t max_rec_words = 0;          // max occurrence-record words over non-hub rows
+    int32_t max_rec_words = 0;          // max record words k_update stages, over non-hub rows
+    // batched records (host_cnf.cpp build_batched), staged by k_update for
+    // every instance except uniform 3-SAT
+    int32_t batched = 0;
+    std::vector<uint32_t> bat_ptr;      // V+1
+    std::vector<uint32_t> bat_rec;
 };
 
 // Parse DIMACS.  Returns 0 on success, 2 (TSAT_E_PARSE) with msg.
@@ -147,6 +152,7 @@ struct StepArgs {
     int* hubD;                       // [n_hubs][KB-1][N] int32 signed bin counts
     DevScalars* ds;
     const uint32_t *cptr, *clit, *occ_ptr, *occ_rec, *occ_cnt;
+    const uint32_t *upd_ptr, *upd_rec;  // records k_update stages: occ_* (uniform 3-SAT) or batched
     const int2* occ_pn;
     const int* hub_of;
     const int4* hub_sc;
