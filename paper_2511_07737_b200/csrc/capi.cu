@@ -31,6 +31,8 @@ struct tsat_ctx_s {
     int device = 0;
     cudaStream_t stream = nullptr;      // caller's stream: every launch / copy
     cudaStream_t cap_stream = nullptr;  // private stream used only to capture graphs
+    cudaStream_t cap_side = nullptr;    // capture fork: k_hub beside k_clause / k_gtable
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool sharded = false;               // candidate-sharded path (NCCL communicator)
     void* comm = nullptr;               // ncclComm_t
     // peer-exchange path (tsat_create_peer): exchanges inside the kernels over
@@ -456,12 +458,34 @@ tsat_status launch_steps(tsat_ctx ctx, int k) {
             ctx->events.push_back(e);
         }
     }
+    // k_hub reads only the evaluated state's bit planes, so (unless every
+    // kernel is being timed) it runs on a forked capture branch beside
+    // k_clause and k_gtable and joins before k_update
+    const bool fork_hub = !ctx->profiling && ctx->cnf.n_hub_sc > 0;
+    if (fork_hub && !ctx->cap_side) {
+        CK(cudaStreamCreateWithFlags(&ctx->cap_side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+    }
     std::string serr;
     int sstat = 0;
     auto body = [&](bool capture) -> cudaError_t {
         for (int i = 0; i < k; ++i) {
             long long t = ctx->t + i;
+            if (fork_hub) {
+                cudaError_t e = cudaEventRecord(ctx->ev_fork, ctx->cap_stream);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->cap_side, ctx->ev_fork, 0);
+                if (e != cudaSuccess) return e;
+                sstat = launch_segment(ctx, a, 2, sc + i, t, ctx->cap_side, &serr);
+                if (sstat) return cudaErrorUnknown;
+                if ((e = cudaEventRecord(ctx->ev_join, ctx->cap_side)) != cudaSuccess) return e;
+            }
             for (int kk = 0; kk < kKernelsPerStep; ++kk) {
+                if (fork_hub && kk == 2) {
+                    cudaError_t e = cudaStreamWaitEvent(ctx->cap_stream, ctx->ev_join, 0);
+                    if (e != cudaSuccess) return e;
+                    continue;
+                }
                 if (ctx->profiling) {
                     cudaError_t e = cudaEventRecordWithFlags(ctx->events[(size_t)i * (kKernelsPerStep + 1) + kk], ctx->cap_stream,
                                                             cudaEventRecordExternal);
@@ -1112,6 +1136,9 @@ void tsat_destroy(tsat_ctx ctx) {
     comm_destroy(ctx->comm);
     peer_release(ctx);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+    if (ctx->cap_side) cudaStreamDestroy(ctx->cap_side);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     cudaFreeHost(ctx->h_steptab);
     cudaFreeHost(ctx->h_scal);
     delete ctx;

@@ -292,6 +292,19 @@ int build_cnf(int32_t V, int64_t C, const int64_t* ptr, const int32_t* lits, Hos
         }
         int32_t hid = h.n_hubs++;
         h.hub_of[v] = hid;
+        if (h.batched) {                 // super-chunks of kHubSlabBatches batched-record batches
+            uint32_t p = h.bat_ptr[v], e = h.bat_ptr[v + 1], b = p;
+            int cnt = 0;
+            while (p < e) {
+                p += 1 + 4 * (h.bat_rec[p] >> 4);
+                if (++cnt == kHubSlabBatches || p >= e) {
+                    h.hub_sc.insert(h.hub_sc.end(), {hid, v, (int32_t)b, (int32_t)p});
+                    b = p;
+                    cnt = 0;
+                }
+            }
+            continue;
+        }
         uint32_t p = h.occ_ptr[v], e = h.occ_ptr[v + 1], b = p;
         int cnt = 0;
         while (p < e) {

@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
 }
 
 // ------------------------------------------------------------------ hub pre-pass
-// One warp per (32-word block, hub super-chunk of <= kHubSlab occurrences):
+// One warp per (hub super-chunk: <= kHubSlab occurrences, or kHubSlabBatches batches, 32-word block):
 // 11-bit signed vertical counters, two counters per 32x32 transpose (16-bit
 // fields), then exact int32 atomic adds into hubD[hub][r][n].
 template <int KB>
@@ -551,16 +551,20 @@ __global__ void __launch_bounds__(32) k_hub(StepArgs a, const uint32_t* __restri
     __shared__ int sh[2][1024 + 32];
     const int lane = threadIdx.x;
     const int NW = a.N >> 5;
-    const int w = blockIdx.x * 32 + lane;
+    const int w = blockIdx.y * 32 + lane;
     const bool valid = w < NW;
-    const int4 sc = a.hub_sc[blockIdx.y];          // hub, var, rec_begin, rec_end
+    const int4 sc = a.hub_sc[blockIdx.x];          // hub, var, rec_begin, rec_end
     const int v = sc.y;
     const uint32_t own = valid ? __ldg(Acur + (size_t)v * NW + w) : 0u;
     uint32_t cnt[NCTR][kHubCtr];
-    const uint32_t* recg = a.occ_rec + sc.z;
+    const uint32_t* recg = a.upd_rec + sc.z;             // the records k_update stages (plain or batched)
     auto recf = [&](unsigned i) { return __ldg(recg + i); };
-    count_occurrences<NP, NCTR, kHubCtr, false, true>(cnt, recf, (unsigned)(sc.w - sc.z), own, Acur, (unsigned)NW,
-                                                valid ? (unsigned)w : 0u);
+    if (a.upd_rec != a.occ_rec)
+        count_batched<NP, NCTR, kHubCtr>(cnt, recf, (unsigned)(sc.w - sc.z), own, Acur, (unsigned)NW,
+                                         valid ? (unsigned)w : 0u);
+    else
+        count_occurrences<NP, NCTR, kHubCtr, false, true>(cnt, recf, (unsigned)(sc.w - sc.z), own, Acur, (unsigned)NW,
+                                                          valid ? (unsigned)w : 0u);
     // two counters per transpose (16-bit fields, bits 11..15 = sign extension),
     // staged through shared memory two bins at a time so the atomics coalesce
     int* dst = a.hubD + (size_t)sc.x * NCTR * a.N;
@@ -584,7 +588,7 @@ __global__ void __launch_bounds__(32) k_hub(StepArgs a, const uint32_t* __restri
 #pragma unroll 4
             for (int k = 0; k < 32; ++k) {
                 const int nl = 32 * k + lane;                  // candidate within the block (coalesced)
-                const int n = blockIdx.x * 1024 + nl;
+                const int n = blockIdx.y * 1024 + nl;
                 const int val = sh[rr][33 * k + lane];
                 if (n < a.N && val) atomicAdd(dst + (size_t)(r0 + rr) * a.N + n, val);
             }
@@ -654,7 +658,7 @@ cudaError_t configure_update(StepArgs* a) {
 cudaError_t launch_hub(const StepArgs& a, const uint32_t* Acur, cudaStream_t st) {
     if (a.n_hub_sc == 0) return cudaGetLastError();
     const int NW = a.N >> 5;
-    dim3 grid((NW + 31) / 32, a.n_hub_sc);
+    dim3 grid(a.n_hub_sc, (NW + 31) / 32);            // super-chunks on x (no 65535 limit)
     if (a.KB == 4) k_hub<4><<<grid, 32, 0, st>>>(a, Acur);
     else k_hub<8><<<grid, 32, 0, st>>>(a, Acur);
     return cudaGetLastError();

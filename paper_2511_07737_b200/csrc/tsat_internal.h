@@ -16,6 +16,7 @@ constexpr int kMaxStepsPerCall = 4096;
 constexpr int kTopkMax = 2048;         // export: k most confident variables per candidate
 constexpr int kRecCap = 512;           // occurrence-record words a warp group stages per row (longer rows: hubs)
 constexpr int kHubSlab = 1023;         // occurrences per hub super-chunk (11-bit signed counters)
+constexpr int kHubSlabBatches = 128;   // batched records: batches (<= 4 occurrences) per hub super-chunk
 constexpr int kMaxPeers = 8;           // peer-exchange path: ranks (GPUs of one NVSwitch node)
 
 // Peer-exchange buffer of one rank (cudaMalloc'd, CUDA-IPC shared).
@@ -65,7 +66,8 @@ struct HostCnf {
     // hub rows: a variable whose signed per-bin counts may leave int8, or whose
     // records exceed kRecCap, is counted by the k_hub pre-pass (int32).
     std::vector<int32_t> hub_of;        // V: hub index or -1
-    std::vector<int32_t> hub_sc;        // 4 per super-chunk: hub, var, rec_begin, rec_end
+    std::vector<int32_t> hub_sc;        // 4 per super-chunk: hub, var, rec_begin, rec_end (word offsets
+                                        // into occ_rec, or into bat_rec when batched)
     int32_t n_hubs = 0;
     int32_t n_hub_sc = 0;
     int64_t header_C = -1;
