@@ -184,6 +184,20 @@ __device__ __forceinline__ void vc_sub3(uint32_t (&c)[B], uint32_t s0, uint32_t 
     }
 }
 
+// c += (x0 + 2 x1 + 4 x2 + hi (2^3 + ... + 2^(B-1))) + cin, B-plane ripple of
+// full adders; with x = ~S, hi = cin = all ones this is c -= S.
+template <int B>
+__device__ __forceinline__ void vc_addc(uint32_t (&c)[B], uint32_t x0, uint32_t x1, uint32_t x2, uint32_t hi) {
+    uint32_t carry = hi;
+    const uint32_t x[3] = {x0, x1, x2};
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+        const uint32_t y = b < 3 ? x[b] : hi, cb = c[b];
+        c[b] = cb ^ y ^ carry;
+        carry = (cb & y) | (carry & (cb ^ y));
+    }
+}
+
 // Bit-sliced addition of a 0/1 mask into an NP-plane unsigned count.
 template <int NP>
 __device__ __forceinline__ void bs_add(uint32_t (&s)[NP], uint32_t x) {
@@ -413,12 +427,13 @@ __device__ __forceinline__ void count_batched(uint32_t (&cnt)[NCTR][B], RecFn re
                 bs_add<NP>(sp[k], x[4 + k]);
             }
         }
+        // one code path for both signs: c - S = c + ~S + 1 (two's complement)
+        const uint32_t cm = neg ? 0u : 0xffffffffu;
 #pragma unroll
         for (int r = 0; r < NCTR; ++r) {
             uint32_t s0, s1, s2;
             sum4(bs_eq<NP>(sp[0], r), bs_eq<NP>(sp[1], r), bs_eq<NP>(sp[2], r), bs_eq<NP>(sp[3], r), s0, s1, s2);
-            if (neg) vc_add3<B>(cnt[r], s0, s1, s2);
-            else vc_sub3<B>(cnt[r], s0, s1, s2);
+            vc_addc<B>(cnt[r], s0 ^ cm, s1 ^ cm, s2 ^ cm, cm);
         }
         p += 1 + 4 * J;
     }

@@ -366,18 +366,22 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
 #endif
                 }
                 else count_batched<NP, NCTR, kCtr>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w);
-                uint32_t T[32];
+                // counter planes of bins 4 blk .. 4 blk + 3 -> one packed word per
+                // candidate; KB = 8 loops over two blocks (one transpose in the
+                // code: the kernel is instruction-cache bound there)
+#pragma unroll 1
+                for (int blk = 0; blk < (KB == 8 ? 2 : 1); ++blk) {
+                    uint32_t T[32];
 #pragma unroll
-                for (int i = 0; i < 32; ++i) T[i] = (i / kCtr < NCTR && i / kCtr < 4) ? cnt[i / kCtr][i % kCtr] : 0u;
-                transpose32(T);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) dpk[33 * wl + j] = T[j];
-                if (KB == 8) {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) T[i] = (4 + i / kCtr < NCTR) ? cnt[4 + i / kCtr][i % kCtr] : 0u;
+                    for (int i = 0; i < 32; ++i) {
+                        const int r = i / kCtr;
+                        const uint32_t lo = (r < NCTR && r < 4) ? cnt[r][i % kCtr] : 0u;
+                        const uint32_t hi = (4 + r < NCTR) ? cnt[4 + r][i % kCtr] : 0u;
+                        T[i] = blk ? hi : lo;
+                    }
                     transpose32(T);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) dpk[dpkw + 33 * wl + j] = T[j];
+                    for (int j = 0; j < 32; ++j) dpk[blk * dpkw + 33 * wl + j] = T[j];
                 }
             }
         }
@@ -443,7 +447,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
             mn4 = *reinterpret_cast<const float4*>(mrow + 4 * tg);
             vn4 = *reinterpret_cast<const float4*>(vrow + 4 * tg);
         }
-#pragma unroll kUnroll3b
+#pragma unroll (KB == 8 ? 1 : kUnroll3b)
         for (int base = 0; base < N; base += 4 * GT) {
             const int n = base + 4 * tg;
             unsigned pnib = 0, nnib = 0;
