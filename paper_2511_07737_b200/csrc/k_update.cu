@@ -37,11 +37,33 @@ constexpr int kUnroll3b = TSAT_3B_UNROLL;
 #define TSAT_UPD_THREADS4 768       // KB = 4 block size bound (register budget)
 #endif
 
+#ifndef TSAT_HINTS
+#define TSAT_HINTS 1
+#endif
+
 namespace tsat {
+
+// Pass 3b's last reads and writes of theta, m, v: with TSAT_HINTS, streaming
+// (evict-first) so the bit planes and records keep their L2 lines.
+__device__ __forceinline__ float4 ld_last(const float* p) {
+#if TSAT_HINTS
+    return __ldcs(reinterpret_cast<const float4*>(p));
+#else
+    return *reinterpret_cast<const float4*>(p);
+#endif
+}
+__device__ __forceinline__ void st_stream(float* p, float4 x) {
+#if TSAT_HINTS
+    __stcs(reinterpret_cast<float4*>(p), x);
+#else
+    *reinterpret_cast<float4*>(p) = x;
+#endif
+}
 
 namespace {
 constexpr int kCtr = 8;        // counter planes (int8) in the fused kernel
-constexpr int kHubCtr = 11;    // counter planes (int11) in k_hub (kHubSlab = 1023 occurrences)
+constexpr int kHubCtrPlain = 11;    // counter planes (int11) in k_hub (kHubSlab = 1023 occurrences)
+constexpr int kHubCtrBatched = 10;  // batched super-chunks: kHubSlabBatches * 4 <= 511 occurrences
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) / 16 * 16; }
 }  // namespace
@@ -443,9 +465,9 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
         const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
         float4 thn = z4, mn4 = z4, vn4 = z4;
         if (4 * tg < N) {
-            thn = *reinterpret_cast<const float4*>(trow + 4 * tg);
-            mn4 = *reinterpret_cast<const float4*>(mrow + 4 * tg);
-            vn4 = *reinterpret_cast<const float4*>(vrow + 4 * tg);
+            thn = ld_last(trow + 4 * tg);
+            mn4 = ld_last(mrow + 4 * tg);
+            vn4 = ld_last(vrow + 4 * tg);
         }
 #pragma unroll (KB == 8 ? 1 : kUnroll3b)
         for (int base = 0; base < N; base += 4 * GT) {
@@ -453,9 +475,9 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
             unsigned pnib = 0, nnib = 0;
             const float4 th4 = thn, m4 = mn4, v4 = vn4;       // software pipeline: next loads in flight
             if (n + 4 * GT < N) {
-                thn = *reinterpret_cast<const float4*>(trow + n + 4 * GT);
-                mn4 = *reinterpret_cast<const float4*>(mrow + n + 4 * GT);
-                vn4 = *reinterpret_cast<const float4*>(vrow + n + 4 * GT);
+                thn = ld_last(trow + n + 4 * GT);
+                mn4 = ld_last(mrow + n + 4 * GT);
+                vn4 = ld_last(vrow + n + 4 * GT);
             }
             if (n < N) {
                 float th[4] = {th4.x, th4.y, th4.z, th4.w};
@@ -500,9 +522,9 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
                         nnib |= (x < 0.0f ? 1u : 0u) << q;
                     }
                 }
-                *reinterpret_cast<float4*>(trow + n) = make_float4(th[0], th[1], th[2], th[3]);
-                *reinterpret_cast<float4*>(mrow + n) = make_float4(mm[0], mm[1], mm[2], mm[3]);
-                *reinterpret_cast<float4*>(vrow + n) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+                st_stream(trow + n, make_float4(th[0], th[1], th[2], th[3]));
+                st_stream(mrow + n, make_float4(mm[0], mm[1], mm[2], mm[3]));
+                st_stream(vrow + n, make_float4(vv[0], vv[1], vv[2], vv[3]));
             }
             // 8 lanes x 4 candidates = one 32-candidate word
             unsigned pw = pnib << (4 * (lane & 7)), nw = nnib << (4 * (lane & 7));
@@ -548,10 +570,11 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
 // One warp per (hub super-chunk: <= kHubSlab occurrences, or kHubSlabBatches batches, 32-word block):
 // 11-bit signed vertical counters, two counters per 32x32 transpose (16-bit
 // fields), then exact int32 atomic adds into hubD[hub][r][n].
-template <int KB>
+template <int KB, bool BATCHED>
 __global__ void __launch_bounds__(32) k_hub(StepArgs a, const uint32_t* __restrict__ Acur) {
     constexpr int NP = (KB == 4) ? 2 : 3;
     constexpr int NCTR = KB - 1;
+    constexpr int kHubCtr = BATCHED ? kHubCtrBatched : kHubCtrPlain;
     __shared__ int sh[2][1024 + 32];
     const int lane = threadIdx.x;
     const int NW = a.N >> 5;
@@ -563,7 +586,7 @@ __global__ void __launch_bounds__(32) k_hub(StepArgs a, const uint32_t* __restri
     uint32_t cnt[NCTR][kHubCtr];
     const uint32_t* recg = a.upd_rec + sc.z;             // the records k_update stages (plain or batched)
     auto recf = [&](unsigned i) { return __ldg(recg + i); };
-    if (a.upd_rec != a.occ_rec)
+    if (BATCHED)
         count_batched<NP, NCTR, kHubCtr>(cnt, recf, (unsigned)(sc.w - sc.z), own, Acur, (unsigned)NW,
                                          valid ? (unsigned)w : 0u);
     else
@@ -663,8 +686,14 @@ cudaError_t launch_hub(const StepArgs& a, const uint32_t* Acur, cudaStream_t st)
     if (a.n_hub_sc == 0) return cudaGetLastError();
     const int NW = a.N >> 5;
     dim3 grid(a.n_hub_sc, (NW + 31) / 32);            // super-chunks on x (no 65535 limit)
-    if (a.KB == 4) k_hub<4><<<grid, 32, 0, st>>>(a, Acur);
-    else k_hub<8><<<grid, 32, 0, st>>>(a, Acur);
+    const bool bat = a.upd_rec != a.occ_rec;
+    if (a.KB == 4) {
+        if (bat) k_hub<4, true><<<grid, 32, 0, st>>>(a, Acur);
+        else k_hub<4, false><<<grid, 32, 0, st>>>(a, Acur);
+    } else {
+        if (bat) k_hub<8, true><<<grid, 32, 0, st>>>(a, Acur);
+        else k_hub<8, false><<<grid, 32, 0, st>>>(a, Acur);
+    }
     return cudaGetLastError();
 }
 

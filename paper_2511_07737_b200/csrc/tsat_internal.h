@@ -16,7 +16,7 @@ constexpr int kMaxStepsPerCall = 4096;
 constexpr int kTopkMax = 2048;         // export: k most confident variables per candidate
 constexpr int kRecCap = 512;           // occurrence-record words a warp group stages per row (longer rows: hubs)
 constexpr int kHubSlab = 1023;         // occurrences per hub super-chunk (11-bit signed counters)
-constexpr int kHubSlabBatches = 128;   // batched records: batches (<= 4 occurrences) per hub super-chunk
+constexpr int kHubSlabBatches = 127;   // batched records: batches (<= 4 occurrences) per hub super-chunk (k_hub int10)
 constexpr int kMaxPeers = 8;           // peer-exchange path: ranks (GPUs of one NVSwitch node)
 
 // Peer-exchange buffer of one rank (cudaMalloc'd, CUDA-IPC shared).
