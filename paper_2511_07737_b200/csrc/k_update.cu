@@ -27,7 +27,7 @@
 #define TSAT_UNI3 2
 #endif
 #ifndef TSAT_3B_UNROLL
-#define TSAT_3B_UNROLL 2
+#define TSAT_3B_UNROLL 1
 #endif
 constexpr int kUnroll3b = TSAT_3B_UNROLL;
 #ifndef TSAT_UPD_THREADS8
@@ -89,25 +89,6 @@ __device__ __forceinline__ float sbyte_to_float(uint32_t ub, int r) {
     return __uint_as_float(__byte_perm(ub, 0x4B000000u, 0x7540u + (unsigned)r)) - 8388736.0f;
 }
 
-// G = sum_r d_r g_r as an fp32 fused multiply-add chain, r ascending (R27).
-// d: the row's signed per-bin counts of one candidate (exact small integers),
-// the last bin derived from dsum = sum_r d_r.  gq[r]: g_r of this candidate.
-template <int KB>
-__device__ __forceinline__ float fold_bytes(uint32_t p0, uint32_t p1, float dsumf, const float (&gq)[KB]) {
-    const uint32_t u0 = p0 ^ 0x80808080u, u1 = p1 ^ 0x80808080u;
-    float d[KB];
-#pragma unroll
-    for (int r = 0; r < KB - 1; ++r) d[r] = sbyte_to_float(r < 4 ? u0 : u1, r & 3);
-    float acc = 0.0f;
-#pragma unroll
-    for (int r = 0; r < KB - 1; ++r) acc = acc + d[r];     // exact: small integers
-    d[KB - 1] = dsumf - acc;
-    float G = 0.0f;
-#pragma unroll
-    for (int r = 0; r < KB; ++r) G = __fmaf_rn(d[r], gq[r], G);
-    return G;
-}
-
 // a * b per lane, correctly rounded, never contracted with a following add:
 // ptxas fuses FMUL2 + FADD2 into FFMA2 even with --fmad=false (and folds an
 // FFMA2 with a -0 addend the same way; scripts/micro/fuse_check.cu), so
@@ -122,9 +103,9 @@ __device__ __forceinline__ void fold_counts(float (&d)[KB], uint32_t p0, uint32_
     const uint32_t u0 = p0 ^ 0x80808080u, u1 = p1 ^ 0x80808080u;
 #pragma unroll
     for (int r = 0; r < KB - 1; ++r) d[r] = sbyte_to_float(r < 4 ? u0 : u1, r & 3);
-    float acc = 0.0f;
+    float acc = d[0];
 #pragma unroll
-    for (int r = 0; r < KB - 1; ++r) acc = acc + d[r];     // exact: small integers
+    for (int r = 1; r < KB - 1; ++r) acc = acc + d[r];     // exact: small integers (never -0)
     d[KB - 1] = dsumf - acc;
 }
 
@@ -469,7 +450,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
             mn4 = ld_last(mrow + 4 * tg);
             vn4 = ld_last(vrow + 4 * tg);
         }
-#pragma unroll (KB == 8 ? 1 : kUnroll3b)
+#pragma unroll kUnroll3b
         for (int base = 0; base < N; base += 4 * GT) {
             const int n = base + 4 * tg;
             unsigned pnib = 0, nnib = 0;
