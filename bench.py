@@ -292,7 +292,7 @@ def main():
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        K_e2e = min(args.steps, 60)
+        K_e2e = args.steps                    # setup (load + init) amortised over the run
         unsat_host = np.empty(N, np.int32)
         s2 = make_solver()
         torch.cuda.synchronize()

@@ -73,7 +73,7 @@ struct tsat_ctx_s {
     std::vector<cudaEvent_t> events;    // (kKernelsPerStep+1) per step of the largest k
     double prof_ms[kKernelsPerStep] = {0, 0, 0, 0, 0};
     // k_update launch geometry (configure_kernels)
-    int upd_mode = 0, upd_GT = 0, upd_NG = 0, upd_grid = 0, num_sms = 0;
+    int upd_mode = 0, upd_GT = 0, upd_NG = 0, upd_grid = 0, num_sms = 0, upd_recbufs = 2;
     int upd_chunk = 0, upd_gs_global = 0;
     bool chunked = false;               // N too large for the fused kernel: split sequence, no collectives at W = 1
     size_t upd_smem = 0;
@@ -223,6 +223,7 @@ StepArgs step_args(tsat_ctx ctx) {
     a.upd_chunk = ctx->upd_chunk;
     a.upd_gs_global = ctx->upd_gs_global;
     a.upd_GT = ctx->upd_GT;
+    a.upd_recbufs = ctx->upd_recbufs;
     a.upd_NG = ctx->upd_NG;
     a.upd_grid = ctx->upd_grid;
     a.upd_smem = ctx->upd_smem;
@@ -829,6 +830,7 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
         CK(configure_kernels(&g));
         ctx->upd_mode = g.upd_mode;
         ctx->upd_GT = g.upd_GT;
+        ctx->upd_recbufs = g.upd_recbufs;
         ctx->upd_NG = g.upd_NG;
         ctx->upd_grid = g.upd_grid;
         ctx->upd_smem = g.upd_smem;

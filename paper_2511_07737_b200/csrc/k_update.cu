@@ -18,6 +18,7 @@
 // Rows whose counts can leave int8 ("hubs", SURVEY §7 hard parts) get their
 // counts from k_hub, which splits a hub's occurrences over many CTAs and adds
 // exact int32 counts (integer atomics: order-free, deterministic).
+#include <cstdio>
 #include <cstdlib>
 
 #include "device_common.cuh"
@@ -71,10 +72,16 @@ __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) / 16 * 
 // Shared-memory geometry of k_update (host and device agree through this).
 __host__ __device__ inline size_t upd_gs_bytes(int KB, int N) { return align16((size_t)KB * N * 4); }
 __host__ __device__ inline size_t upd_dpk_words(int N) { return (size_t)N + (N >> 5); }
-__host__ __device__ inline size_t upd_group_bytes(int KB, int N, int rec_cap) {
+// nbufs: 2 record buffers (the next row's records land during this row's
+// streams), or 1 (staged after this row's gather) when that buys a warp group:
+// KB = 8 (shared-memory bound), a compile-time choice (a runtime one costs
+// the instruction-cache-bound KB = 8 kernel ~7 %).
+__host__ __device__ constexpr int upd_recbufs(int KB) { return KB == 8 ? 1 : 2; }
+__host__ __device__ inline size_t upd_group_bytes(int KB, int N, int rec_cap, int nbufs) {
     const int NDW = KB == 4 ? 1 : 2;
-    // dpk | 2 record buffers | sign planes [2 parities][pos, neg][NW] | 128 B scratch
-    return align16((size_t)NDW * upd_dpk_words(N) * 4) + 2 * align16((size_t)rec_cap * 4) + align16((size_t)4 * (N >> 5) * 4) + 128;
+    // dpk | nbufs record buffers | sign planes [2 parities][pos, neg][NW] | 128 B scratch
+    return align16((size_t)NDW * upd_dpk_words(N) * 4) + nbufs * align16((size_t)rec_cap * 4) +
+           align16((size_t)4 * (N >> 5) * 4) + 128;
 }
 
 // x * 2^s, exact (== scalbn) when 2^s is a normal double.
@@ -236,13 +243,14 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
     float* gs = gs_global ? a.gtab : reinterpret_cast<float*>(smem);
     const int grp = threadIdx.x / GT, tg = threadIdx.x - grp * GT;
     const int rec_cap = a.upd_rec_cap;
-    const size_t grb = upd_group_bytes(KB, NCH, rec_cap);
+    constexpr int nbufs = upd_recbufs(KB);
+    const size_t grb = upd_group_bytes(KB, NCH, rec_cap, nbufs);
     unsigned char* gb = smem + (gs_global ? 0 : upd_gs_bytes(KB, N)) + (size_t)grp * grb;
     const int nitems = a.V * nch;
     uint32_t* dpk = reinterpret_cast<uint32_t*>(gb);
     uint32_t* rec = reinterpret_cast<uint32_t*>(gb + align16((size_t)(KB == 4 ? 1 : 2) * dpkw * 4));
-    const size_t recw = align16((size_t)rec_cap * 4) / 4;            // words per record buffer (two buffers)
-    uint32_t* posw0 = rec + 2 * recw;                   // [parity][pos | neg][NW] (MODE 2 finishes a row late)
+    const size_t recw = align16((size_t)rec_cap * 4) / 4;            // words per record buffer
+    uint32_t* posw0 = rec + nbufs * recw;            // [parity][pos | neg][NW] (MODE 2 finishes a row late)
     long long* red = reinterpret_cast<long long*>(gb + grb - 128);                      // 4 + 4 slots
     float* redf = reinterpret_cast<float*>(red + 8);                                    // 4 slots
     int* rowslot = reinterpret_cast<int*>(redf + 4);                                    // 2 slots
@@ -323,8 +331,8 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
         const int v = item / nch;
         const int n0c = (item - v * nch) * NCH;            // first candidate of this chunk
         const int ncand = min(NCH, N - n0c), w0 = n0c >> 5, NWc = ncand >> 5;
-        uint32_t* rb_cur = rec + (size_t)(it & 1) * recw;    // this row's records (staged by the previous row)
-        uint32_t* rb_nxt = rec + (size_t)((it + 1) & 1) * recw;
+        uint32_t* rb_cur = rec + (size_t)(nbufs == 2 ? (it & 1) : 0) * recw;     // this row's records
+        uint32_t* rb_nxt = rec + (size_t)(nbufs == 2 ? ((it + 1) & 1) : 0) * recw;
         // ---- fetch the next row; prefetch this row's streams into L2
         if (tg == 0) {
             rowslot[it & 1] = atomicAdd(&a.ds->row_counter, 1);
@@ -391,6 +399,19 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
         if (MODE == 2 && pend_v >= 0 && tg == 0)             // previous row's Q, sent a row ago
             pxs[1] = peer_row_recv(a.px, 1, pend_v, sc->xgen, a.ds, pend_q);
         gsync(bar, GT);
+        const int item_next = rowslot[it & 1];              // fetched by tg 0 before the gather
+        const int vnext = item_next < nitems ? item_next / nch : a.V;
+        // stage the next row's records asynchronously (cp.async global -> smem);
+        // they land while this row streams and are waited for before the Q
+        // barrier.  One buffer: this row's records are dead after the gather.
+        auto stage_next = [&]() {
+            if (vnext < a.V && a.hub_of[vnext] < 0) {
+                const unsigned nb = a.upd_ptr[vnext], ne = a.upd_ptr[vnext + 1];
+                for (unsigned i = tg; i < ne - nb; i += GT) cp_async4(rb_nxt + i, a.upd_rec + nb + i);
+            }
+            cp_async_commit();
+        };
+        if (nbufs == 1) stage_next();
         if (MODE == 2 && pend_v >= 0) {
             finish_row(pend_v, pxs[1], posw0 + (size_t)pend_pb * 2 * NW, pend_m2);
             pend_v = -1;
@@ -412,15 +433,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
             if (tg == 0) peer_row_send(a.px, 0, v, Itot, sc->xgen);
             Itot = peer_row_recv(a.px, 0, v, sc->xgen, a.ds, Itot);
         }
-        const int item_next = rowslot[it & 1];
-        const int vnext = item_next < nitems ? item_next / nch : a.V;
-        // stage the next row's records asynchronously (cp.async global -> smem);
-        // they land while this row streams, and are waited for before the Q barrier
-        if (vnext < a.V && a.hub_of[vnext] < 0) {
-            const unsigned nb = a.upd_ptr[vnext], ne = a.upd_ptr[vnext + 1];
-            for (unsigned i = tg; i < ne - nb; i += GT) cp_async4(rb_nxt + i, a.upd_rec + nb + i);
-        }
-        cp_async_commit();
+        if (nbufs == 2) stage_next();
         if (MODE == 1) {                                     // sharded / chunked: J partial out, next item
             if (tg == 0) {
                 if (nch > 1) atomicAdd(reinterpret_cast<unsigned long long*>(a.Jbuf + v), (unsigned long long)Itot);
@@ -609,7 +622,7 @@ __global__ void __launch_bounds__(32) k_hub(StepArgs a, const uint32_t* __restri
 bool update_fits_fused(int KB, int N, int rec_cap, int optin) {
     const int NW = N >> 5;
     const int GT = NW >= 128 ? 128 : (NW > 32 ? 64 : 32);
-    const size_t gsb = upd_gs_bytes(KB, N), grb = upd_group_bytes(KB, N, rec_cap);
+    const size_t gsb = upd_gs_bytes(KB, N), grb = upd_group_bytes(KB, N, rec_cap, upd_recbufs(KB));
     const long long ng = optin > (long long)gsb ? ((long long)optin - (long long)gsb) / (long long)grb : 0;
     return ng >= 2 || (ng == 1 && GT == 128);
 }
@@ -632,12 +645,25 @@ cudaError_t configure_update(StepArgs* a) {
     a->upd_gs_global = fused ? 0 : 1;
     const int NWc = a->upd_chunk >> 5;
     const int GT = NWc >= 128 ? 128 : (NWc > 32 ? 64 : 32);
-    const size_t gsb = fused ? upd_gs_bytes(KB, N) : 0, grb = upd_group_bytes(KB, a->upd_chunk, a->upd_rec_cap);
-    long long ng = optin > (long long)gsb ? ((long long)optin - (long long)gsb) / (long long)grb : 0;
+    const size_t gsb = fused ? upd_gs_bytes(KB, N) : 0;
     const int max_threads = KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS8;   // register budget (launch bounds)
-    ng = ng < max_threads / GT ? ng : max_threads / GT;
-    if (GT > 32) ng = ng < 15 ? ng : 15;          // named barriers 1..15 (warp groups use __syncwarp)
+    auto groups = [&](int nbufs) {
+        const size_t grb = upd_group_bytes(KB, a->upd_chunk, a->upd_rec_cap, nbufs);
+        long long ng = optin > (long long)gsb ? ((long long)optin - (long long)gsb) / (long long)grb : 0;
+        ng = ng < max_threads / GT ? ng : max_threads / GT;
+        if (GT > 32) ng = ng < 15 ? ng : 15;      // named barriers 1..15 (warp groups use __syncwarp)
+        return ng;
+    };
+    // (upd_recbufs: measured c4 7 -> 8 groups with one buffer, k_update -11 %;
+    // c2 / c3 are register-bound, and two buffers are faster there, c2 +4 %)
+    const int nbufs = upd_recbufs(KB);
+    const long long ng = groups(nbufs);
+    const size_t grb = upd_group_bytes(KB, a->upd_chunk, a->upd_rec_cap, nbufs);
     if (ng < 1) return cudaErrorInvalidConfiguration;
+    a->upd_recbufs = nbufs;
+    if (std::getenv("TSAT_GEOM_VERBOSE"))
+        std::fprintf(stderr, "k_update geometry: KB %d N %d GT %d groups %lld recbufs %d rec_cap %d smem %zu\n", KB, N, GT, ng,
+                     nbufs, a->upd_rec_cap, gsb + (size_t)ng * grb);
     a->upd_mode = 0;
     a->upd_GT = GT;
     a->upd_NG = (int)ng;

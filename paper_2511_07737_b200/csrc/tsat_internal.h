@@ -169,6 +169,7 @@ struct StepArgs {
     int upd_gs_global;               // g table read from global memory (chunked)
     int upd_GT, upd_NG, upd_grid;    // v2 launch geometry
     int upd_rec_cap;                 // record words a group stages per row (max over non-hub rows)
+    int upd_recbufs;                 // record buffers per group (1 or 2, configure_update)
     size_t upd_smem;
     // candidate-sharded path (world > 1, or a 1-rank communicator)
     int sharded;
