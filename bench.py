@@ -289,6 +289,8 @@ def main():
                 "algorithmic_bytes_per_launch": upd_bytes, "kernel_ms": per,
                 "kernel_share": {n: per[n] / sum(per.values()) for n in names}}
 
+    kps = s.kernels_per_step()
+    s.close()                                 # the e2e solver below needs the memory (c5: 100 GB each)
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -351,7 +353,6 @@ def main():
                               "gate_99_at_iteration": gate, "solved": bool(inf.solved)}
             q.close()
 
-    kps = s.kernels_per_step()
     line = {
         "metric": "clause-candidate evals/sec", "value": value, "unit": "evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": w, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -374,7 +375,6 @@ def main():
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    s.close()
     if world > 1:
         dist.destroy_process_group()
 
