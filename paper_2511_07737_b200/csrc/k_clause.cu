@@ -14,13 +14,20 @@
 // gathers are in flight.
 #include "device_common.cuh"
 
+#ifndef TSAT_CL_CH3
+#define TSAT_CL_CH3 64             // clauses per warp chunk, K <= 3
+#endif
+#ifndef TSAT_CL_G3
+#define TSAT_CL_G3 2               // carry-save groups of 4 clauses per iteration, K <= 3
+#endif
+
 namespace tsat {
 
 namespace {
 constexpr int kWarps = 8;
 // clauses per warp chunk (<= 127: 7-bit counters); K = 7 halves it to keep
 // the staged literals within the 48 KB static shared memory
-__host__ __device__ constexpr int chunk_clauses(int kmaxc) { return kmaxc > 3 ? 32 : 64; }
+__host__ __device__ constexpr int chunk_clauses(int kmaxc) { return kmaxc > 3 ? 32 : TSAT_CL_CH3; }
 constexpr int kUnr = 4;        // clauses evaluated together (carry-save group)
 constexpr uint32_t kNone = 0xffffffffu;
 
@@ -114,7 +121,7 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t*
         for (int r = 0; r < KB - 1; ++r)
 #pragma unroll
             for (int b = 0; b < CB; ++b) cnt[r][b] = 0u;
-        constexpr int kG = KMAXC <= 3 ? 2 : 1;          // carry-save groups per iteration (gathers in flight)
+        constexpr int kG = KMAXC <= 3 ? TSAT_CL_G3 : 1;  // carry-save groups per iteration (gathers in flight)
         for (int cb0 = 0; cb0 < nc; cb0 += kUnr * kG) {
             uint32_t xx[kG][kUnr][KMAXC];
 #pragma unroll
