@@ -7,6 +7,25 @@
 
 namespace tsat {
 
+// L2 cache policy for the bit-plane gathers (created once per kernel):
+// evict-last when both plane buffers fit comfortably in L2 (they are re-read
+// by every occurrence), evict-normal otherwise.
+__device__ __forceinline__ unsigned long long plane_policy(bool keep) {
+    unsigned long long pol;
+    if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// Whether both bit-plane buffers ((V + 1) x NW words each) fit comfortably in L2.
+__host__ __device__ __forceinline__ bool planes_fit_l2(int V, int NW) {
+    return 2.0 * 4.0 * ((double)V + 1.0) * (double)NW <= 48.0e6;
+}
+__device__ __forceinline__ uint32_t ld_plane(const uint32_t* p, unsigned long long pol) {
+    uint32_t x;
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(x) : "l"(p), "l"(pol));
+    return x;
+}
+
 // Philox4x32-10 (Salmon et al., SC'11), 10 rounds, in place.
 __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
 #pragma unroll
@@ -222,14 +241,15 @@ __device__ __forceinline__ uint32_t bs_eq(const uint32_t (&s)[NP], int r) {
 // clause's other literals (codes), as NP count planes.
 template <int NP, typename RecFn>
 __device__ __forceinline__ void rec_planes(uint32_t (&sp)[NP], RecFn rec, unsigned p, uint32_t hdr, uint32_t own,
-                                           const uint32_t* __restrict__ Acur, unsigned NW, unsigned w) {
+                                           const uint32_t* __restrict__ Acur, unsigned NW, unsigned w,
+                                           unsigned long long pol) {
     const uint32_t len = hdr >> 1;
     sp[0] = own ^ (0u - (hdr & 1u));
 #pragma unroll
     for (int q = 1; q < NP; ++q) sp[q] = 0u;
     for (uint32_t i = 1; i < len; ++i) {
         const uint32_t code = rec(p + i);
-        bs_add<NP>(sp, __ldg(Acur + ((code >> 1) * NW + w)) ^ (0u - (code & 1u)));
+        bs_add<NP>(sp, ld_plane(Acur + ((code >> 1) * NW + w), pol) ^ (0u - (code & 1u)));
     }
 }
 
@@ -242,12 +262,12 @@ __device__ __forceinline__ void rec_planes(uint32_t (&sp)[NP], RecFn rec, unsign
 // false: one record at a time (smaller code, for I-cache-bound callers).
 template <int NP, int NCTR, int B, bool UNI3, bool GROUP, typename RecFn>
 __device__ __forceinline__ void count_occurrences(uint32_t (&cnt)[NCTR][B], RecFn rec, unsigned nrec, uint32_t own,
-                                                  const uint32_t* __restrict__ Acur, unsigned NW, unsigned w) {
+                                                  const uint32_t* __restrict__ Acur, unsigned NW, unsigned w, unsigned long long pol) {
 #pragma unroll
     for (int r = 0; r < NCTR; ++r)
 #pragma unroll
         for (int b = 0; b < B; ++b) cnt[r][b] = 0u;
-    auto ld = [&](uint32_t code) { return __ldg(Acur + ((code >> 1) * NW + w)) ^ (0u - (code & 1u)); };
+    auto ld = [&](uint32_t code) { return ld_plane(Acur + ((code >> 1) * NW + w), pol) ^ (0u - (code & 1u)); };
     unsigned p = 0;
     while (p < nrec) {
         const uint32_t h0 = rec(p);
@@ -293,7 +313,7 @@ __device__ __forceinline__ void count_occurrences(uint32_t (&cnt)[NCTR][B], RecF
                 }
             } else {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) rec_planes<NP>(sp[k], rec, pp[k], h[k], own, Acur, NW, w);
+                for (int k = 0; k < 4; ++k) rec_planes<NP>(sp[k], rec, pp[k], h[k], own, Acur, NW, w, pol);
             }
 #pragma unroll
             for (int r = 0; r < NCTR; ++r) {
@@ -305,7 +325,7 @@ __device__ __forceinline__ void count_occurrences(uint32_t (&cnt)[NCTR][B], RecF
             p = p4;
         } else {
             uint32_t sp[NP];
-            rec_planes<NP>(sp, rec, p, h0, own, Acur, NW, w);
+            rec_planes<NP>(sp, rec, p, h0, own, Acur, NW, w, pol);
             if (h0 & 1u) {
 #pragma unroll
                 for (int r = 0; r < NCTR; ++r) vc_inc<B>(cnt[r], bs_eq<NP>(sp, r));
@@ -327,7 +347,7 @@ __device__ __forceinline__ void count_occurrences(uint32_t (&cnt)[NCTR][B], RecF
 // per leftover record.
 template <int NCTR, int B, bool PIPE, typename RecFn>
 __device__ __forceinline__ void count_uni3(uint32_t (&cnt)[NCTR][B], RecFn rec, unsigned nneg, unsigned npos,
-                                           uint32_t own, const uint32_t* __restrict__ Acur, unsigned NW, unsigned w) {
+                                           uint32_t own, const uint32_t* __restrict__ Acur, unsigned NW, unsigned w, unsigned long long pol) {
 #pragma unroll
     for (int r = 0; r < NCTR; ++r)
 #pragma unroll
@@ -335,7 +355,7 @@ __device__ __forceinline__ void count_uni3(uint32_t (&cnt)[NCTR][B], RecFn rec, 
     const unsigned nbn = (nneg + 3) >> 2, nb = nbn + ((npos + 3) >> 2);
     if (nb == 0) return;
     const unsigned nrec = nneg + npos;
-    auto ld = [&](uint32_t code) { return __ldg(Acur + ((code >> 1) * NW + w)) ^ (0u - (code & 1u)); };
+    auto ld = [&](uint32_t code) { return ld_plane(Acur + ((code >> 1) * NW + w), pol) ^ (0u - (code & 1u)); };
     // batch b: records [first, first + count), all of one sign
     auto batch = [&](unsigned b, unsigned& first, unsigned& count) {
         if (b < nbn) { first = 4 * b; count = min(4u, nneg - 4 * b); }
@@ -392,13 +412,13 @@ __device__ __forceinline__ void count_uni3(uint32_t (&cnt)[NCTR][B], RecFn rec, 
 // and one counter update per batch.
 template <int NP, int NCTR, int B, typename RecFn>
 __device__ __forceinline__ void count_batched(uint32_t (&cnt)[NCTR][B], RecFn rec, unsigned nwords, uint32_t own,
-                                              const uint32_t* __restrict__ Acur, unsigned NW, unsigned w) {
+                                              const uint32_t* __restrict__ Acur, unsigned NW, unsigned w, unsigned long long pol) {
     static_assert(NCTR == (1 << NP) - 1, "absent records rely on bin 2^NP - 1 being derived");
 #pragma unroll
     for (int r = 0; r < NCTR; ++r)
 #pragma unroll
         for (int b = 0; b < B; ++b) cnt[r][b] = 0u;
-    auto ld = [&](uint32_t code) { return __ldg(Acur + ((code >> 1) * NW + w)) ^ (0u - (code & 1u)); };
+    auto ld = [&](uint32_t code) { return ld_plane(Acur + ((code >> 1) * NW + w), pol) ^ (0u - (code & 1u)); };
     unsigned p = 0;
     while (p < nwords) {
         const uint32_t hdr = rec(p);

@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t*
     const uint32_t unw = (uint32_t)NW;
     const uint2 zero_lit = make_uint2((uint32_t)V * unw, 0u);
     const uint32_t* Aw = A + (valid ? w : 0);          // lanes past NW read a valid word, results unused
+    const unsigned long long pol = plane_policy(planes_fit_l2(V, NW));
     const long long nchunks = (C + kCH - 1) / kCH;
     // grid-sized: warps stride over the clause chunks of this word block
     for (long long chunk = (long long)blockIdx.y * kWarps + warp; chunk < nchunks;
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t*
                     for (int l = 0; l < KMAXC; ++l) {
                         const int c = cb0 + gq * kUnr + u;      // < kCH: the chunk is padded
                         const uint2 o = my[c * KMAXC + l];
-                        xx[gq][u][l] = __ldg(Aw + o.x) ^ o.y;
+                        xx[gq][u][l] = ld_plane(Aw + o.x, pol) ^ o.y;
                     }
 #pragma unroll
           for (int gq = 0; gq < kG; ++gq) {

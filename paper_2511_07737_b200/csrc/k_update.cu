@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
     const int bar = 1 + grp;
     const int lane = threadIdx.x & 31, gw = tg >> 5, ngw = GT >> 5;
     const bool uni3 = a.uniform_len && a.mc.K == 3 && KB == 4;
+    const unsigned long long pol = plane_policy(planes_fit_l2(a.V, NW));
 
     // fp32 derivative table of the whole batch -> shared memory
     if (!gs_global)
@@ -370,13 +371,13 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
                 auto recf = [&](unsigned i) { return rb_cur[i]; };
                 if (uni3) {
 #if TSAT_UNI3 == 0
-                    count_occurrences<NP, NCTR, kCtr, true, true>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w);
+                    count_occurrences<NP, NCTR, kCtr, true, true>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w, pol);
 #else
                     count_uni3<NCTR, kCtr, TSAT_UNI3 == 1>(cnt, recf, (unsigned)pn.y, (unsigned)pn.x, own, Acur,
-                                                          (unsigned)NW, (unsigned)w);
+                                                          (unsigned)NW, (unsigned)w, pol);
 #endif
                 }
-                else count_batched<NP, NCTR, kCtr>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w);
+                else count_batched<NP, NCTR, kCtr>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w, pol);
                 // counter planes of bins 4 blk .. 4 blk + 3 -> one packed word per
                 // candidate; KB = 8 loops over two blocks (one transpose in the
                 // code: the kernel is instruction-cache bound there)
@@ -577,15 +578,16 @@ __global__ void __launch_bounds__(32) k_hub(StepArgs a, const uint32_t* __restri
     const int4 sc = a.hub_sc[blockIdx.x];          // hub, var, rec_begin, rec_end
     const int v = sc.y;
     const uint32_t own = valid ? __ldg(Acur + (size_t)v * NW + w) : 0u;
+    const unsigned long long pol = plane_policy(planes_fit_l2(a.V, NW));
     uint32_t cnt[NCTR][kHubCtr];
     const uint32_t* recg = a.upd_rec + sc.z;             // the records k_update stages (plain or batched)
     auto recf = [&](unsigned i) { return __ldg(recg + i); };
     if (BATCHED)
         count_batched<NP, NCTR, kHubCtr>(cnt, recf, (unsigned)(sc.w - sc.z), own, Acur, (unsigned)NW,
-                                         valid ? (unsigned)w : 0u);
+                                         valid ? (unsigned)w : 0u, pol);
     else
         count_occurrences<NP, NCTR, kHubCtr, false, true>(cnt, recf, (unsigned)(sc.w - sc.z), own, Acur, (unsigned)NW,
-                                                          valid ? (unsigned)w : 0u);
+                                                          valid ? (unsigned)w : 0u, pol);
     // two counters per transpose (16-bit fields, bits 11..15 = sign extension),
     // staged through shared memory two bins at a time so the atomics coalesce
     int* dst = a.hubD + (size_t)sc.x * NCTR * a.N;
