@@ -195,6 +195,17 @@ tsat_status tsat_get_info(tsat_ctx ctx, tsat_step_info* out);
  * N_local candidates; *first_global_idx = index of host_out[0]. */
 tsat_status tsat_query_unsat(tsat_ctx ctx, int32_t* host_out, int64_t* first_global_idx);
 
+/* Asynchronous variants (§3.1.4 l.169-177, same data).  tsat_query_unsat_async
+ * enqueues the device->host copy of the N_local counts on the context's
+ * stream and returns at once: host_out must be PINNED host memory
+ * (cudaMallocHost / torch pin_memory) owned by the caller, and is valid only
+ * after a later blocking call (tsat_sync, tsat_get_info, tsat_step with a
+ * non-NULL out, or a synchronisation of the stream).  With tsat_step(ctx, k,
+ * NULL) this lets a caller read every step's result while the next step
+ * runs.  tsat_sync blocks until all work queued by this context is done. */
+tsat_status tsat_query_unsat_async(tsat_ctx ctx, int32_t* host_out, int64_t* first_global_idx);
+tsat_status tsat_sync(tsat_ctx ctx);
+
 /* (a10/a11) Export: the M best candidates by (unsat asc, index asc) over all
  * ranks, each with its k most confident variables = smallest
  * |G_vn| (ties -> lower v), paired with the candidate's value, all at the last

@@ -68,6 +68,8 @@ _SIGS = {
     "tsat_init_batch": (ct.c_int, [P, ct.c_int64, ct.c_uint64, ct.POINTER(tsat_config), P, ct.c_size_t]),
     "tsat_step": (ct.c_int, [P, ct.c_int32, ct.POINTER(tsat_step_info)]),
     "tsat_get_info": (ct.c_int, [P, ct.POINTER(tsat_step_info)]),
+    "tsat_query_unsat_async": (ct.c_int, [P, P, ct.POINTER(ct.c_int64)]),
+    "tsat_sync": (ct.c_int, [P]),
     "tsat_query_unsat": (ct.c_int, [P, P, ct.POINTER(ct.c_int64)]),
     "tsat_export_best": (ct.c_int, [P, ct.c_int32, ct.c_int32, ct.POINTER(tsat_partial)]),
     "tsat_export_model": (ct.c_int, [P, ct.c_int64, P]),
@@ -302,6 +304,16 @@ class Solver:
         self._check(self.lib.tsat_query_unsat(self.h, _ptr(out), ct.byref(first)))
         self.n0 = first.value
         return out
+
+    def query_unsat_async(self, out_ptr: int) -> None:
+        """Enqueue the unsat-count copy into PINNED host memory at out_ptr
+        (N_local int32); valid after sync() or another blocking call."""
+        first = ct.c_int64()
+        self._check(self.lib.tsat_query_unsat_async(self.h, ct.c_void_p(int(out_ptr)), ct.byref(first)))
+        self.n0 = first.value
+
+    def sync(self) -> None:
+        self._check(self.lib.tsat_sync(self.h))
 
     def N_local_count(self) -> int:
         return self.N // self.world

@@ -65,7 +65,9 @@ struct tsat_ctx_s {
     size_t ws_bytes = 0;
     int64_t t = 0;             // iterations completed
     int64_t steps_done = 0;    // >= 1 once a state has been evaluated
-    StepScalars* h_steptab = nullptr;   // pinned
+    StepScalars* h_steptab = nullptr;   // pinned, 2 slots of kMaxStepsPerCall (alternating tsat_step calls)
+    cudaEvent_t tab_ev[2] = {nullptr, nullptr};   // slot's upload done (the host may rewrite it)
+    int tab_slot = 0;
     DevScalars* h_scal = nullptr;       // pinned readback
     std::map<int, cudaGraphExec_t> graphs;
     // profiling
@@ -640,7 +642,8 @@ tsat_status tsat_create(tsat_ctx* out, int cuda_device, void* cuda_stream, const
     tsat_ctx ctx = c.get();
     CK(cudaSetDevice(cuda_device));
     CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
-    CK(cudaMallocHost(&c->h_steptab, sizeof(StepScalars) * kMaxStepsPerCall));
+    CK(cudaMallocHost(&c->h_steptab, 2 * sizeof(StepScalars) * kMaxStepsPerCall));
+    for (auto& e : c->tab_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CK(cudaMallocHost(&c->h_scal, sizeof(DevScalars)));
     tsat_config_default(&c->cfg);
     if (nccl_unique_id) {           // candidate-sharded path (also with a 1-rank communicator)
@@ -670,7 +673,8 @@ tsat_status tsat_create_peer(tsat_ctx* out, int cuda_device, void* cuda_stream, 
     tsat_ctx ctx = c.get();
     CK(cudaSetDevice(cuda_device));
     CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
-    CK(cudaMallocHost(&c->h_steptab, sizeof(StepScalars) * kMaxStepsPerCall));
+    CK(cudaMallocHost(&c->h_steptab, 2 * sizeof(StepScalars) * kMaxStepsPerCall));
+    for (auto& e : c->tab_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CK(cudaMallocHost(&c->h_scal, sizeof(DevScalars)));
     tsat_config_default(&c->cfg);
     *out = c.release();
@@ -873,16 +877,25 @@ tsat_status tsat_step(tsat_ctx ctx, int32_t k, tsat_step_info* out) {
     int done = 0;
     while (done < k) {
         int kk = std::min(k - done, kMaxStepsPerCall);
-        // the previous call's table must not be overwritten while in use
-        CK(cudaStreamSynchronize(ctx->stream));
-        s = collect_profile(ctx);
-        if (s != TSAT_OK) return s;
-        for (int i = 0; i < kk; ++i) {
-            ctx->h_steptab[i] = step_scalars(ctx->cfg, ctx->t + i);
-            ctx->h_steptab[i].xgen = ctx->xgen + 1 + (unsigned)i;
+        if (ctx->profiling) {                       // the previous call's kernel events
+            CK(cudaStreamSynchronize(ctx->stream));
+            s = collect_profile(ctx);
+            if (s != TSAT_OK) return s;
         }
-        CK(cudaMemcpyAsync(ctx->ws + ctx->L.steptab, ctx->h_steptab, sizeof(StepScalars) * kk, cudaMemcpyHostToDevice,
+        // the device table is rewritten in stream order (after the previous
+        // graph has used it); the host slot only once its last upload is done,
+        // so consecutive calls queue without draining the GPU
+        const int slot = ctx->tab_slot;
+        ctx->tab_slot ^= 1;
+        CK(cudaEventSynchronize(ctx->tab_ev[slot]));
+        StepScalars* tab = ctx->h_steptab + (size_t)slot * kMaxStepsPerCall;
+        for (int i = 0; i < kk; ++i) {
+            tab[i] = step_scalars(ctx->cfg, ctx->t + i);
+            tab[i].xgen = ctx->xgen + 1 + (unsigned)i;
+        }
+        CK(cudaMemcpyAsync(ctx->ws + ctx->L.steptab, tab, sizeof(StepScalars) * kk, cudaMemcpyHostToDevice,
                            ctx->stream));
+        CK(cudaEventRecord(ctx->tab_ev[slot], ctx->stream));
         s = launch_steps(ctx, kk);
         if (s != TSAT_OK) return s;
         ctx->t += kk;
@@ -899,6 +912,22 @@ tsat_status tsat_get_info(tsat_ctx ctx, tsat_step_info* out) {
     tsat_status s = check_batch(ctx, false);
     if (s != TSAT_OK) return s;
     return read_info(ctx, out);
+}
+
+tsat_status tsat_query_unsat_async(tsat_ctx ctx, int32_t* host_out, int64_t* first) {
+    GUARD_CTX();
+    tsat_status s = check_batch(ctx, true);
+    if (s != TSAT_OK) return s;
+    if (!host_out) return fail(ctx, TSAT_E_ARG, "null host_out");
+    CK(cudaMemcpyAsync(host_out, ctx->ws + ctx->L.unsat, (size_t)ctx->N * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (first) *first = ctx->n0;
+    return TSAT_OK;
+}
+
+tsat_status tsat_sync(tsat_ctx ctx) {
+    GUARD_CTX();
+    CK(cudaStreamSynchronize(ctx->stream));
+    return collect_profile(ctx);
 }
 
 tsat_status tsat_query_unsat(tsat_ctx ctx, int32_t* host_out, int64_t* first) {
@@ -1143,6 +1172,8 @@ void tsat_destroy(tsat_ctx ctx) {
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     cudaFreeHost(ctx->h_steptab);
     cudaFreeHost(ctx->h_scal);
+    for (auto e : ctx->tab_ev)
+        if (e) cudaEventDestroy(e);
     delete ctx;
 }
 

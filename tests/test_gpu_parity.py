@@ -180,6 +180,38 @@ def test_multi_step_graph_launch_matches():
         assert (info.best_unsat, info.best_idx) == (ref.best_unsat, ref.best_idx)
 
 
+def test_async_steps_and_unsat_readback():
+    """tsat_step(1, NULL) calls queue without draining the GPU (double-buffered
+    step table) and tsat_query_unsat_async copies each step's counts into
+    pinned memory read during the next step: the same counts and state as the
+    oracle's step by step."""
+    import torch
+    cnf = planted_ksat(300, 1275, 3, 5)
+    N = 128
+    s, o = make_pair(cnf, N, 31)
+    pins = [torch.empty(N, dtype=torch.int32, pin_memory=True) for _ in range(3)]
+    for i in range(3):
+        s.step(1, wait=False)
+        s.query_unsat_async(pins[i].data_ptr())
+    s.sync()
+    for i in range(3):
+        ref = o.step()
+        np.testing.assert_array_equal(pins[i].numpy(), ref.unsat)
+    th, m, v, t = s.get_state()
+    assert t == o.t == 3
+    np.testing.assert_array_equal(th, o.theta)
+    np.testing.assert_array_equal(v, o.v)
+    for _ in range(70):                       # many queued calls: the table slots alternate
+        s.step(1, wait=False)
+    for _ in range(70):
+        ref = o.step()
+    info = s.get_info()
+    np.testing.assert_array_equal(s.query_unsat(), ref.unsat)
+    assert (info.best_unsat, info.best_idx) == (ref.best_unsat, ref.best_idx)
+    th, m, v, t = s.get_state()
+    np.testing.assert_array_equal(th, o.theta)
+
+
 def test_c2_full_size_two_steps():
     """Config c2 at full size (V=10k, C=42k, N=4096), bench's configuration."""
     cnf, cfg = make_config("c2")
