@@ -136,6 +136,47 @@ def test_ragged_and_mixed_instances(case):
         compare_step(s, o, cnf, case)
 
 
+def _uni3_with_hub(V=200, C=900, hub_occ=300, seed=4):
+    """Uniform 3-SAT in which variable 1 occurs in hub_occ clauses (> 127 of
+    one sign): a hub row of the uniform 3-SAT (plain-record) layout."""
+    rng = np.random.default_rng(seed)
+    cl = planted_ksat(V, C - hub_occ, 3, seed).clauses()
+    for i in range(hub_occ):
+        a, b = rng.choice(np.arange(2, V + 1), 2, replace=False)
+        s1 = -1 if i % 3 else 1                   # 200 negated, 100 positive occurrences
+        cl.append([s1 * 1, int(a) * (1 if rng.random() < .5 else -1), int(b) * (1 if rng.random() < .5 else -1)])
+    return Cnf.from_clauses(V, cl)
+
+
+@pytest.mark.parametrize("case", ["empty_clause", "no_clauses", "unused_vars", "uniform7", "k5_mixed", "uni3_hub"])
+def test_degenerate_and_shape_cases(case):
+    """Degenerate instances and layouts the bench configs do not reach: an
+    empty clause (never satisfiable, R = 0 always), C = 0, variables without
+    occurrences, uniform K = 7 (k_clause's uniform staging at K = 7), K = 5
+    mixed lengths (KB = 8 with fewer bins live), and a uniform 3-SAT hub row."""
+    if case == "empty_clause":
+        cnf, N = Cnf.from_clauses(30, planted_ksat(30, 120, 3, 2).clauses() + [[]]), 64
+    elif case == "no_clauses":
+        cnf, N = Cnf.from_clauses(12, []), 32
+    elif case == "unused_vars":
+        cnf, N = Cnf.from_clauses(400, planted_ksat(100, 420, 3, 6).clauses()), 96
+    elif case == "uniform7":
+        cnf, N = planted_ksat(300, 1200, 7, 8), 128
+    elif case == "k5_mixed":
+        base = planted_ksat(200, 500, 3, 3).clauses() + planted_ksat(200, 300, 5, 4).clauses()
+        cnf, N = Cnf.from_clauses(200, base), 64
+    else:
+        cnf, N = _uni3_with_hub(), 256
+    state = random_state(cnf.V, N, seed=13)
+    s, o = make_pair(cnf, N, 7, state=state, t0=0)
+    for _ in range(6):
+        compare_step(s, o, cnf, case)
+    if case == "uni3_hub":
+        assert s.info.n_hub_rows >= 1
+    if case == "empty_clause":
+        assert s.get_info().best_unsat >= 1 and s.get_solution() is None
+
+
 def test_lr_boundaries_and_restart():
     """Cross the t = 29/30 decay and the t = 359/360 restart (R9)."""
     cnf = planted_ksat(200, 840, 3, 6)
