@@ -202,6 +202,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     use_peer = (world > 1 and not args.nccl) or args.peer
+    peer_fallback = None
 
     def make_solver():
         if use_peer:           # exchanges inside the kernels over NVLink peer memory (CUDA IPC)
@@ -219,9 +220,34 @@ def main():
             sv.connect_peers()
         return inf
 
-    s = make_solver()
-    info = load(s)
-    s.init_batch(N * world, seed)
+    if world > 1 and use_peer:
+        # the peer path needs CUDA IPC + peer access between the ranks' GPUs;
+        # if any rank cannot set it up (or its first step fails), every rank
+        # falls back to the NCCL-exchange path (same results, bit for bit)
+        ok, why = 1, ""
+        try:
+            s = make_solver()
+            info = load(s)
+            s.init_batch(N * world, seed)
+            s.step(1)
+        except Exception as ex:  # noqa: BLE001
+            ok, why = 0, f"{type(ex).__name__}: {ex}"[:200]
+        flag = torch.tensor([ok], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            try:
+                s.close()
+            except Exception:  # noqa: BLE001
+                pass
+            use_peer = False
+            peer_fallback = why or "another rank failed to set up the peer path"
+            s = make_solver()
+            info = load(s)
+            s.init_batch(N * world, seed)
+    else:
+        s = make_solver()
+        info = load(s)
+        s.init_batch(N * world, seed)
     chunk = max(1, min(args.chunk, args.steps))
     assert args.steps % chunk == 0, "--steps must be a multiple of --chunk"
     # warm-up (also instantiates the chunk-sized CUDA graph)
@@ -385,7 +411,7 @@ def main():
                                    "single GPU, sharded kernels on a 1-rank NCCL communicator" if args.sharded else
                                    "single GPU"),
                    "l2": "state (theta, m, v: %.0f MB) larger than L2; no flush" % (12 * cnf.V * N / 1e6),
-                   "graph_chunk": chunk},
+                   "graph_chunk": chunk, "peer_fallback": peer_fallback},
         "gradient_steps_per_s": args.steps / (ms / 1000.0),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": kps * args.steps, "clocks": clk.summary(),
