@@ -52,7 +52,8 @@ def parse():
 
 def workload_desc(name, cnf, N):
     kinds = {"c1": "planted random 3-SAT", "c2": "planted random 3-SAT", "c3": "planted random 3-SAT",
-             "c4": "industrial-shaped CNF (lengths 2-7, power-law occurrences)", "c5": "planted random 3-SAT"}
+             "c4": "industrial-shaped CNF (lengths 2-7, power-law occurrences)", "c5": "planted random 3-SAT",
+             "c2h": "2-hidden planted random 3-SAT (SURVEY f2 variant)"}
     return f"{name}: {kinds[name]} V={cnf.V} C={cnf.C} (ratio {cnf.C / cnf.V:.2f}), N={N} candidates"
 
 

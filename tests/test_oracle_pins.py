@@ -640,3 +640,30 @@ def test_trajectory_determinism_and_shard_invariance():
             assert np.array_equal(np.concatenate([o.unsat for o in outs[t]]), sa.unsat)
             assert outs[t][0].loss == sa.loss
             assert (outs[t][0].best_unsat, outs[t][0].best_idx) == (sa.best_unsat, sa.best_idx)
+
+
+def _agreement(cnf):
+    """Fraction of literals true under the planted sigma; every clause's
+    satisfaction under sigma and under its complement."""
+    lits = np.asarray(cnf.lits)
+    var = np.abs(lits) - 1
+    true_sigma = (lits > 0) == (cnf.sigma[var] == 1)
+    ptr = np.asarray(cnf.clause_ptr)
+    sat_sigma = np.logical_or.reduceat(true_sigma, ptr[:-1])
+    sat_comp = np.logical_or.reduceat(~true_sigma, ptr[:-1])
+    return true_sigma.mean(), sat_sigma.all(), sat_comp.all()
+
+
+def test_generator_planting_statistics():
+    """naive planting makes a literal agree with sigma with
+    probability 4/7 (3-SAT); 2-hidden planting (§8(f) f2) with probability
+    1/2, and the complement of sigma satisfies every clause as well."""
+    f1, s1, c1 = _agreement(planted_ksat(10_000, 42_000, 3, 1))
+    assert s1 and not c1
+    assert abs(f1 - 4 / 7) < 0.005
+    f2, s2, c2 = _agreement(planted_ksat(10_000, 42_000, 3, 1, hidden=2))
+    assert s2 and c2
+    assert abs(f2 - 0.5) < 0.005
+    # the naive instances are unchanged by the new option (same RNG stream)
+    a, b = planted_ksat(50, 200, 3, 7), planted_ksat(50, 200, 3, 7, hidden=1)
+    np.testing.assert_array_equal(a.lits, b.lits)

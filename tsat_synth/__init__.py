@@ -99,30 +99,39 @@ def _distinct_rows(rng, draw, rows, k):
         out[bad] = draw(bad.size * k).reshape(bad.size, k)
 
 
-def _plant_signs(rng, vars_, sigma, lens=None):
+def _plant_signs(rng, vars_, sigma, lens=None, hidden=1):
     """Signs uniform over the patterns that sigma satisfies.
 
     vars_ is (C, kmax) (entries beyond ``lens`` ignored).  For each clause a
     truth pattern t in [1, 2^len - 1] is drawn uniformly; literal i is made
-    true under sigma iff bit i of t is set."""
+    true under sigma iff bit i of t is set.  hidden=2 ("2-hidden" planting,
+    SURVEY §8(f) f2): t in [1, 2^len - 2], so the complement of sigma
+    satisfies every clause too and a literal's polarity carries no majority
+    signal about sigma (each literal agrees with sigma with probability 1/2)."""
     C, kmax = vars_.shape
     if lens is None:
         lens = np.full(C, kmax, dtype=np.int64)
-    t = np.floor(rng.random(C) * ((1 << lens) - 1)).astype(np.int64) + 1
+    npat = (1 << lens) - (1 if hidden == 1 else 2)
+    t = np.floor(rng.random(C) * npat).astype(np.int64) + 1
     bits = (t[:, None] >> np.arange(kmax)[None, :]) & 1          # literal true under sigma?
     sv = sigma[vars_].astype(np.int64)                             # sigma value of the variable
     positive = (bits == sv)                                        # positive literal true iff sigma=1
     return np.where(positive, vars_ + 1, -(vars_ + 1)).astype(np.int32)
 
 
-def planted_ksat(V: int, C: int, k: int = 3, seed: int = 1) -> Cnf:
-    """Planted random k-SAT (SURVEY §8(d) 'planted-k-SAT (naive)')."""
-    rng = np.random.default_rng([0x7A7, int(seed), int(V), int(C), int(k)])
+def planted_ksat(V: int, C: int, k: int = 3, seed: int = 1, hidden: int = 1) -> Cnf:
+    """Planted random k-SAT (SURVEY §8(d) 'planted-k-SAT (naive)'); hidden=2:
+    2-hidden planting (sigma and its complement both satisfy, k >= 2)."""
+    if hidden == 2 and k < 2:
+        raise ValueError("2-hidden planting needs k >= 2")
+    key = [0x7A7, int(seed), int(V), int(C), int(k)] + ([2] if hidden == 2 else [])
+    rng = np.random.default_rng(key)
     sigma = rng.integers(0, 2, size=V, dtype=np.uint8)
     vars_ = _distinct_rows(rng, lambda n: rng.integers(0, V, size=n), C, k)
-    lits = _plant_signs(rng, vars_, sigma)
+    lits = _plant_signs(rng, vars_, sigma, hidden=hidden)
     ptr = np.arange(C + 1, dtype=np.int64) * k
-    return Cnf(V, ptr, lits.reshape(-1), sigma, f"planted-{k}sat-V{V}-C{C}-s{seed}")
+    tag = "planted2" if hidden == 2 else "planted"
+    return Cnf(V, ptr, lits.reshape(-1), sigma, f"{tag}-{k}sat-V{V}-C{C}-s{seed}")
 
 
 INDUSTRIAL_LENGTHS = {2: 0.40, 3: 0.30, 4: 0.12, 5: 0.08, 6: 0.06, 7: 0.04}
@@ -220,6 +229,8 @@ CONFIGS = {
     "c3": dict(kind="planted", V=1_000_000, C=4_200_000, k=3, N=1024, steps=360, seed=1),
     "c4": dict(kind="industrial", V=500_000, C=2_000_000, N=2048, steps=360, seed=1),
     "c5": dict(kind="planted", V=100_000, C=425_000, k=3, N=65536, steps=3600, seed=1),
+    # c2's shape with 2-hidden planting (not a BASELINE config)
+    "c2h": dict(kind="planted", V=10_000, C=42_000, k=3, N=4096, steps=360, seed=1, hidden=2),
 }
 
 
@@ -228,7 +239,7 @@ def make_config(name: str, seed: int | None = None) -> tuple[Cnf, dict]:
     if seed is not None:
         cfg["seed"] = seed
     if cfg["kind"] == "planted":
-        cnf = planted_ksat(cfg["V"], cfg["C"], cfg["k"], cfg["seed"])
+        cnf = planted_ksat(cfg["V"], cfg["C"], cfg["k"], cfg["seed"], cfg.get("hidden", 1))
     else:
         cnf = industrial_cnf(cfg["V"], cfg["C"], cfg["seed"])
     return cnf, cfg
