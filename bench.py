@@ -383,7 +383,7 @@ def main():
     if world == 1 and not args.no_quality:
         from paper_2511_07737_b200 import config_default
         quality = {"iterations": 360, "gate": "best candidate satisfies > 99% of clauses"}
-        for label, norm in (("paper_exact_R3", 1), ("normalize_off", 0)):
+        for label, norm in (("paper_exact_R3", 1), ("normalize_off", 0), ("mean_magnitude_R28", 3)):
             q = Solver(local, stream=stream)
             q.load_cnf(cnf)
             c = config_default()

@@ -62,7 +62,9 @@ typedef enum {
 typedef struct {
     double  tau;             /* SmoothMin temperature, Eq. 4 (> 0) */
     int32_t normalize;       /* 1 = Eq. 5 over all N candidates; 0 = off; 2 = per shard: each GPU averages
-                                over its own N/W candidates and keeps J local (variants) */
+                                over its own N/W candidates and keeps J local; 3 = Eq. 5 with the row's
+                                mean MAGNITUDE mean_n |theta_vn| as denominator (reading R28; its
+                                Jacobian term carries sign(theta_vn))  (variants) */
     double  beta1, beta2;    /* AdamW moments (0.9, 0.999) */
     double  eps;             /* AdamW eps (1e-8) */
     double  weight_decay;    /* AdamW decoupled weight decay (1e-2) */

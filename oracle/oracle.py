@@ -56,6 +56,7 @@ def lib():
             "or_philox4x32_10": (None, [P, P, P]),
             "or_init": (None, [i32, i64, i32, u64, P, P, P]),
             "or_row_sums": (i32, [i32, i32, P, P]),
+            "or_row_sums_abs": (i32, [i32, i32, P, P]),
             "or_row_finish": (None, [i32, i64, P, i32, f64, P, P, P, P]),
             "or_binarize": (None, [i32, i32, P, P, P]),
             "or_clause_eval": (None, [i32, P, P, i32, P, P]),
@@ -66,6 +67,7 @@ def lib():
             "or_jacobian_partial": (None, [i32, i32, P, P, P, i64, f64, f32, P, P, P]),
             "or_jacobian_finish": (None, [i32, i64, P, P, P, P, P, i32, P, P]),
             "or_grad": (None, [i32, i32, P, P, P, P]),
+            "or_grad_mag": (None, [i32, i32, P, P, P, P, P]),
             "or_lr_at": (f64, [i64, f64, f64, i32, i32, f64]),
             "or_adamw": (None, [i32, i64, i32, P, P, P, P, i64, i64, f64, f64, f64, f64, f64, f64, u64]),
             "or_abs_max": (f32, [ct.c_size_t, P]),
@@ -187,7 +189,7 @@ def export_partial(absG_col: np.ndarray, bits_col: np.ndarray, k: int):
 @dataclass
 class Config:
     tau: float = 1.0
-    normalize: int = 1
+    normalize: int = 1          # 0 off (R20), 1 Eq. 5 global (R3), 2 per shard, 3 mean magnitude (R28)
     beta1: float = 0.9
     beta2: float = 0.999
     eps: float = 1e-8
@@ -302,7 +304,7 @@ class Oracle:
         V = self.cnf.V
         Q = np.empty(V, np.int64)
         L = lib()
-        L.or_row_sums(V, self.Nl, _p(self.theta), _p(Q))
+        (L.or_row_sums_abs if self.cfg.normalize == 3 else L.or_row_sums)(V, self.Nl, _p(self.theta), _p(Q))
         if not self.per_shard:
             Q = self.comm.sum_i64(Q)
         thmax_local = float(np.abs(self.theta).max()) if self.theta.size else 0.0
@@ -344,7 +346,10 @@ class Oracle:
         L.or_jacobian_finish(V, self.Nnorm, _p(I), _p(s), _p(valid), _p(rho), _p(guard), cfg.normalize, _p(J),
                              _p(cv))
         grad = np.empty((V, Nl), np.float32)
-        L.or_grad(V, Nl, _p(G), _p(rho), _p(cv), _p(grad))
+        if cfg.normalize == 3:
+            L.or_grad_mag(V, Nl, _p(G), _p(rho), _p(cv), _p(self.theta), _p(grad))
+        else:
+            L.or_grad(V, Nl, _p(G), _p(rho), _p(cv), _p(grad))
         # selection (§4.2): best = argmin (unsat, n)
         j = int(np.lexsort((np.arange(Nl), unsat))[0]) if Nl else 0
         key = (int(unsat[j]), self.n0 + j)
@@ -378,7 +383,7 @@ def step_sampled(cnf, theta, m, v, t, rows, cfg: Config | None = None):
     V, N = theta.shape
     K = cnf.K
     Q = np.empty(V, np.int64)
-    L.or_row_sums(V, N, _p(theta), _p(Q))
+    (L.or_row_sums_abs if cfg.normalize == 3 else L.or_row_sums)(V, N, _p(theta), _p(Q))
     mu = np.empty(V); d = np.empty(V); rho = np.empty(V); guard = np.empty(V, np.uint8)
     L.or_row_finish(V, N, _p(Q), cfg.normalize, cfg.eps_norm, _p(mu), _p(d), _p(rho), _p(guard))
     b = np.empty((V, N), np.uint8)
@@ -405,7 +410,10 @@ def step_sampled(cnf, theta, m, v, t, rows, cfg: Config | None = None):
     rho_r = np.ascontiguousarray(rho[rows]); guard_r = np.ascontiguousarray(guard[rows])
     L.or_jacobian_finish(nr, N, _p(I), _p(s), _p(valid), _p(rho_r), _p(guard_r), cfg.normalize, _p(J), _p(cv))
     grad = np.empty((nr, N), np.float32)
-    L.or_grad(nr, N, _p(G), _p(rho_r), _p(cv), _p(grad))
+    if cfg.normalize == 3:
+        L.or_grad_mag(nr, N, _p(G), _p(rho_r), _p(cv), _p(th), _p(grad))
+    else:
+        L.or_grad(nr, N, _p(G), _p(rho_r), _p(cv), _p(grad))
     lr = lr_at(t, cfg)
     # noise is keyed by the variable index: only sigma = 0 here
     assert cfg.noise_sigma == 0.0

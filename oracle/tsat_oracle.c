@@ -103,6 +103,22 @@ int or_row_sums(int V, int Nl, const float* theta, int64_t* Q)
     return 0;
 }
 
+/* normalize == 3 (variant f2, reading R28): Eq. 5's denominator is the mean
+ * MAGNITUDE of the row, mean_n |theta_vn|, so Q_v = sum_n round(|theta| 2^32)
+ * (same exact fixed point, Q_v >= 0). */
+int or_row_sums_abs(int V, int Nl, const float* theta, int64_t* Q)
+{
+    for (int v = 0; v < V; ++v) {
+        int64_t s = 0;
+        for (int j = 0; j < Nl; ++j) {
+            double x = fabs((double)theta[(size_t)v * Nl + j]) * 4294967296.0; /* exact */
+            s += (int64_t)llrint(x);
+        }
+        Q[v] = s;
+    }
+    return 0;
+}
+
 /* mu_v = (Q_v 2^-32)/N; d_v = sign(mu_v) max(|mu_v|, eps), sign(0)=+1;
  * rho_v = 1/d_v (R3: x/mu computed as x * (1/mu)); guard_v = |mu_v| <= eps.
  * normalize == 0 (variant, R20): d = rho = 1, guard = 1. */
@@ -334,6 +350,23 @@ void or_grad(int V, int Nl, const double* G, const double* rho, const double* cv
         const float rf = (float)rho[v], cf = (float)cv[v];
         for (int j = 0; j < Nl; ++j)
             grad[(size_t)v * Nl + j] = fmaf((float)G[(size_t)v * Nl + j], rf, -cf);
+    }
+}
+
+/* normalize == 3 (R28): d_v = mean_n |theta_vn|, so d(theta_vm/d_v)/d theta_vn
+ * = delta_mn/d_v - theta_vm sign(theta_vn)/(N d_v^2) and
+ * grad_vn = G_vn rho_v - sign(theta_vn) c_v, c_v = J_v/(N d_v^2) as above:
+ * fmaf(G, (float)rho, -t) with t = (float)c, -(float)c or 0 by the sign of
+ * theta_vn (the subgradient of |x| at 0 is taken as 0). */
+void or_grad_mag(int V, int Nl, const double* G, const double* rho, const double* cv, const float* theta, float* grad)
+{
+    for (int v = 0; v < V; ++v) {
+        const float rf = (float)rho[v], cf = (float)cv[v];
+        for (int j = 0; j < Nl; ++j) {
+            const float x = theta[(size_t)v * Nl + j];
+            const float t = x > 0.0f ? cf : (x < 0.0f ? -cf : 0.0f);
+            grad[(size_t)v * Nl + j] = fmaf((float)G[(size_t)v * Nl + j], rf, -t);
+        }
     }
 }
 

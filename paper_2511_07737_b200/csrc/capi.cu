@@ -795,7 +795,7 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
     tsat_config c;
     if (cfg) c = *cfg; else tsat_config_default(&c);
     if (!(c.tau > 0) || c.decay_every < 1 || c.restart_every < 1 || !(c.decay_factor > 0) || !(c.eps_norm > 0) ||
-        c.normalize < 0 || c.normalize > 2 || (c.reset_moments_on_restart & ~1))
+        c.normalize < 0 || c.normalize > 3 || (c.reset_moments_on_restart & ~1))
         return fail(ctx, TSAT_E_ARG, "invalid config");
     drop_graphs(ctx);
     ctx->cfg = c;
@@ -820,7 +820,7 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
     for (int d = 0; d < 8; ++d) mc.E[d] = std::exp(-c.tau * (double)d);
     mc.tau = c.tau;
     mc.eps_norm = c.eps_norm;
-    mc.normalize = c.normalize;                 // 0 off, 1 global, 2 per shard
+    mc.normalize = c.normalize;                 // 0 off, 1 global, 2 per shard, 3 global mean magnitude (R28)
     mc.K = ctx->cnf.K;
     mc.Nnorm = c.normalize == 2 ? N_global / ctx->world : N_global;
     mc.n0 = ctx->n0;

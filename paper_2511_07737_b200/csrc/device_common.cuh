@@ -16,6 +16,13 @@ __device__ __forceinline__ unsigned long long plane_policy(bool keep) {
     else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+// Eq. 5 gradient addend (R27b): grad = fmaf(G, rho, addend) with addend = -c;
+// normalize 3 (R28, d = mean |theta|): -sign(theta) c, and -0 at theta = 0.
+__device__ __forceinline__ float jac_addend(float ncf, float th, bool mag) {
+    if (!mag) return ncf;
+    return th > 0.0f ? ncf : (th < 0.0f ? -ncf : -0.0f);
+}
+
 // Whether both bit-plane buffers ((V + 1) x NW words each) fit comfortably in L2.
 __host__ __device__ __forceinline__ bool planes_fit_l2(int V, int NW) {
     return 2.0 * 4.0 * ((double)V + 1.0) * (double)NW <= 48.0e6;

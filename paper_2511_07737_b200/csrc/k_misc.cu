@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(256) k_rowstats(const float* __restrict__ thet
     float mx = 0.0f;
     for (int n = threadIdx.x; n < N; n += blockDim.x) {
         float x = row[n];
-        s += __float2ll_rn(x * 4294967296.0f);          // x 2^32 is exact in fp32
+        s += __float2ll_rn((mc.normalize == 3 ? fabsf(x) : x) * 4294967296.0f);   // x 2^32 is exact in fp32
         mx = fmaxf(mx, fabsf(x));
     }
     block_sum_max(s, mx, sh_s, sh_m);

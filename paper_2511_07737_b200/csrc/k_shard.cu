@@ -34,6 +34,7 @@ __global__ void k_unpack_max(DevScalars* __restrict__ ds, const StepScalars* __r
 // Phase B of one row (one CTA per row): c_v from the global J, grad, AdamW
 // (PyTorch order, R6-R6c), Q partial, max |theta|, sign planes of theta_{t+1}.
 // Identical arithmetic to the fused k_update.
+template <bool MAG>           // normalize 3 (R28), as k_update's MAG
 __global__ void __launch_bounds__(256) k_update_b(StepArgs a, const uint32_t* __restrict__ Acur,
                                                   const StepScalars* __restrict__ sc) {
     __shared__ long long sh_s[32];
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(256) k_update_b(StepArgs a, const uint32_t* __
             const float G[4] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const float g = __fmaf_rn(G[q], rhof, ncf);                 // R27b
+                const float g = __fmaf_rn(G[q], rhof, jac_addend(ncf, th[q], MAG));   // R27b, R28
                 float x = th[q] * wdf;
                 const float m0 = mm[q] * sc->mkeep;
                 const float mn = __fmaf_rn(a1, g - m0, m0);
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(256) k_update_b(StepArgs a, const uint32_t* __
                     x = x + nz * xi;
                 }
                 th[q] = x; mm[q] = mn; vv[q] = vn;
-                Qn += __float2ll_rn(x * 4294967296.0f);
+                Qn += __float2ll_rn((MAG ? fabsf(x) : x) * 4294967296.0f);
                 mx = fmaxf(mx, fabsf(x));
                 pnib |= (x > 0.0f ? 1u : 0u) << q;
                 nnib |= (x < 0.0f ? 1u : 0u) << q;
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(256) k_rows_partial(StepArgs a, const float* _
     float mx = 0.0f;
     for (int n = threadIdx.x; n < N; n += blockDim.x) {
         const float x = row[n];
-        s += __float2ll_rn(x * 4294967296.0f);
+        s += __float2ll_rn((a.mc.normalize == 3 ? fabsf(x) : x) * 4294967296.0f);
         mx = fmaxf(mx, fabsf(x));
         const unsigned pw = __ballot_sync(0xffffffffu, x > 0.0f), nw = __ballot_sync(0xffffffffu, x < 0.0f);
         if ((threadIdx.x & 31) == 0) {
@@ -226,7 +227,8 @@ cudaError_t launch_update_b(const StepArgs& a, const uint32_t* Acur, const StepS
     if (a.V == 0) return cudaGetLastError();
     int threads = a.N / 4;
     threads = threads < 32 ? 32 : (threads > 256 ? 256 : (threads + 31) / 32 * 32);
-    k_update_b<<<a.V, threads, 0, st>>>(a, Acur, sc);
+    if (a.mc.normalize == 3) k_update_b<true><<<a.V, threads, 0, st>>>(a, Acur, sc);
+    else k_update_b<false><<<a.V, threads, 0, st>>>(a, Acur, sc);
     return cudaGetLastError();
 }
 cudaError_t launch_rows_partial(const StepArgs& a, const float* theta, unsigned int* thmax_bits, cudaStream_t st) {

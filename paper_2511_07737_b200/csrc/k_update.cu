@@ -226,7 +226,10 @@ __device__ __forceinline__ void gsync(int bar, int GT) {
 // Rows come from a global counter (dynamic: hub rows, ragged occurrence counts
 // and the tail stay balanced); tg 0 fetches the next row at the start of the
 // current one into a parity-double-buffered slot, read after the J barrier.
-template <int KB, int MODE>
+// MAG: normalize 3 (R28, d = mean |theta|): the Jacobian addend carries
+// sign(theta) and the next row sums are of |theta| (a template flag: a
+// run-time one costs the default path ~3 % at c2 / c3).
+template <int KB, int MODE, bool MAG = false>
 __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS8, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
                                                                     uint32_t* __restrict__ Anext,
                                                                     const StepScalars* __restrict__ sc) {
@@ -453,6 +456,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
             c = c * rho;
         }
         const float rhof = __double2float_rn(rho), ncf = -__double2float_rn(c);     // R27b: fp32 operands
+        constexpr bool mag = MAG;
 
         // ---- 3b: grad, AdamW, next-state statistics and sign planes
         long long Qn = 0;
@@ -481,7 +485,7 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
                 const uint32_t* dp = dpk + n + (n >> 5);
                 float gg[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) gg[q] = __fmaf_rn(__uint_as_float(dp[q]), rhof, ncf);   // R27b
+                for (int q = 0; q < 4; ++q) gg[q] = __fmaf_rn(__uint_as_float(dp[q]), rhof, jac_addend(ncf, th[q], mag));
                 // AdamW on candidate pairs: packed fp32x2 ops are per-lane
                 // correctly rounded, i.e. the same canonical ops (R6-R6c)
 #pragma unroll
@@ -503,7 +507,8 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
                         xs1 = xs1 + nz * noise_xi(mc.seed, mc.n0 + n + 2 * h + 1, v, t);
                     }
                     const float xs[2] = {xs0, xs1};
-                    const float2 q2 = __fmul2_rn(make_float2(xs0, xs1), make_float2(4294967296.0f, 4294967296.0f));
+                    const float2 q2 = __fmul2_rn(mag ? make_float2(fabsf(xs0), fabsf(xs1)) : make_float2(xs0, xs1),
+                                                 make_float2(4294967296.0f, 4294967296.0f));   // R28: |theta|
                     Qn += __float2ll_rn(q2.x) + __float2ll_rn(q2.y);      // x 2^32 is exact in fp32
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
@@ -682,11 +687,15 @@ cudaError_t configure_update(StepArgs* a) {
     if (KB == 4) {
         if ((e = cudaFuncSetAttribute(k_update<4, 0>, attr, smem)) != cudaSuccess) return e;
         if ((e = cudaFuncSetAttribute(k_update<4, 1>, attr, smem)) != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k_update<4, 2>, attr, smem);
+        if ((e = cudaFuncSetAttribute(k_update<4, 2>, attr, smem)) != cudaSuccess) return e;
+        if ((e = cudaFuncSetAttribute(k_update<4, 0, true>, attr, smem)) != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k_update<4, 2, true>, attr, smem);
     } else {
         if ((e = cudaFuncSetAttribute(k_update<8, 0>, attr, smem)) != cudaSuccess) return e;
         if ((e = cudaFuncSetAttribute(k_update<8, 1>, attr, smem)) != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k_update<8, 2>, attr, smem);
+        if ((e = cudaFuncSetAttribute(k_update<8, 2>, attr, smem)) != cudaSuccess) return e;
+        if ((e = cudaFuncSetAttribute(k_update<8, 0, true>, attr, smem)) != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k_update<8, 2, true>, attr, smem);
     }
     return e;
 }
@@ -710,13 +719,16 @@ cudaError_t launch_update(const StepArgs& a, const uint32_t* Acur, uint32_t* Ane
                           cudaStream_t st) {
     if (a.V == 0) return cudaGetLastError();
     const int threads = a.upd_GT * a.upd_NG;
+    const bool mag = a.mc.normalize == 3;
+    const dim3 g(a.upd_grid), b(threads);
+    const size_t sm = a.upd_smem;
     if (a.peer) {
-        if (a.KB == 4) k_update<4, 2><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
-        else k_update<8, 2><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
+        if (a.KB == 4) mag ? k_update<4, 2, true><<<g, b, sm, st>>>(a, Acur, Anext, sc) : k_update<4, 2><<<g, b, sm, st>>>(a, Acur, Anext, sc);
+        else mag ? k_update<8, 2, true><<<g, b, sm, st>>>(a, Acur, Anext, sc) : k_update<8, 2><<<g, b, sm, st>>>(a, Acur, Anext, sc);
     } else if (a.KB == 4) {
-        k_update<4, 0><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
+        mag ? k_update<4, 0, true><<<g, b, sm, st>>>(a, Acur, Anext, sc) : k_update<4, 0><<<g, b, sm, st>>>(a, Acur, Anext, sc);
     } else {
-        k_update<8, 0><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, Anext, sc);
+        mag ? k_update<8, 0, true><<<g, b, sm, st>>>(a, Acur, Anext, sc) : k_update<8, 0><<<g, b, sm, st>>>(a, Acur, Anext, sc);
     }
     return cudaGetLastError();
 }

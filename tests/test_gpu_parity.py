@@ -81,7 +81,8 @@ def compare_step(s, o, cnf, what=""):
     np.testing.assert_array_equal(v, o.v, err_msg=f"v {what} t={ref.t}")
     Q = s.debug(4, np.int64, (cnf.V,))
     Qo = np.empty(cnf.V, np.int64)
-    O.lib().or_row_sums(cnf.V, N, O._p(o.theta), O._p(Qo))
+    rows = O.lib().or_row_sums_abs if o.cfg.normalize == 3 else O.lib().or_row_sums     # R28: sum |theta|
+    rows(cnf.V, N, O._p(o.theta), O._p(Qo))
     np.testing.assert_array_equal(Q, Qo)
     return info, ref
 
@@ -188,7 +189,7 @@ def test_lr_boundaries_and_restart():
             compare_step(s, o, cnf, f"t0={t0}")
 
 
-@pytest.mark.parametrize("variant", [dict(normalize=0), dict(weight_decay=0.0), dict(tau=5.0), dict(tau=0.5),
+@pytest.mark.parametrize("variant", [dict(normalize=0), dict(normalize=3), dict(weight_decay=0.0), dict(tau=5.0), dict(tau=0.5),
                                      dict(noise_sigma=0.3),
                                      dict(reset_moments_on_restart=1, restart_every=3, decay_every=2),
                                      dict(normalize=2)])
@@ -419,7 +420,7 @@ def test_error_paths():
 
 
 # ---------------------------------------------------------------- sharded path (1-rank NCCL communicator)
-@pytest.mark.parametrize("case", ["c1", "industrial7", "ragged3", "c1-per-shard", "ragged3-reset"])
+@pytest.mark.parametrize("case", ["c1", "industrial7", "ragged3", "c1-per-shard", "ragged3-reset", "industrial7-mag"])
 def test_sharded_path_matches_oracle(case):
     """The multi-GPU kernels (phase A -> SUM J -> phase B -> SUM Q -> rows
     finish, plus the MAX exchange) on a 1-rank communicator reproduce the
@@ -430,6 +431,8 @@ def test_sharded_path_matches_oracle(case):
         case, cfg = "c1", O.Config(normalize=2)
     elif case == "ragged3-reset":
         case, cfg = "ragged3", O.Config(reset_moments_on_restart=1, restart_every=7, decay_every=3)
+    elif case == "industrial7-mag":
+        case, cfg = "industrial7", O.Config(normalize=3)
     if case == "c1":
         cnf, N = planted_ksat(20, 85, 3, 1), 64
     elif case == "industrial7":

@@ -97,11 +97,11 @@ def _run_threads(fns):
         raise errs[0]
 
 
-@pytest.mark.parametrize("normalize", [1, 2])
+@pytest.mark.parametrize("normalize", [1, 2, 3])
 def test_peer_two_ranks_one_gpu(normalize, monkeypatch):
     """W = 2 in one process: two contexts on their own streams, stepped from two
     host threads; the rank-concatenated state equals the oracle's (1 shard
-    for normalize = 1; per-shard oracle ranks for normalize = 2)."""
+    for normalize = 1 and 3; per-shard oracle ranks for normalize = 2)."""
     import torch
     monkeypatch.setenv("TSAT_UPD_GRID", "70")        # both persistent kernels resident on one GPU
     cnf = planted_ksat(400, 1680, 3, 7)
@@ -115,7 +115,7 @@ def test_peer_two_ranks_one_gpu(normalize, monkeypatch):
     for s in ss:
         s.peer_open(hs)
     _run_threads([lambda s=s: s.init_batch(N, seed, _cfg(ocfg)) for s in ss])
-    if normalize == 1:
+    if normalize != 2:
         o = O.Oracle(cnf, N, seed, cfg=ocfg)
         refs = None
     else:
@@ -126,7 +126,7 @@ def test_peer_two_ranks_one_gpu(normalize, monkeypatch):
         def go(r):
             infos[r] = ss[r].step(k)
         _run_threads([lambda r=r: go(r) for r in range(W)])
-        if normalize == 1:
+        if normalize != 2:
             for _ in range(k):
                 refs = o.step()
             ref_theta = o.theta

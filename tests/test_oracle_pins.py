@@ -247,7 +247,10 @@ def _torch_dense_grad(cnf, theta, tau, normalize=True, eps=1e-8):
         for x in cl:
             (Pp if x > 0 else Pn)[c, abs(x) - 1] = 1.0
     th = torch.tensor(theta.astype(np.float64), requires_grad=True)
-    if normalize:
+    if normalize == 3:                       # R28: mean magnitude (variant f2)
+        d = torch.clamp(th.abs().mean(dim=1, keepdim=True), min=eps)
+        x = th / d
+    elif normalize:
         mu = th.mean(dim=1, keepdim=True)
         mag = torch.clamp(mu.abs(), min=eps)
         d = torch.where(mu >= 0, mag, -mag)
@@ -275,7 +278,8 @@ def _G_from_g64(cnf, R, g):
     return G
 
 
-@pytest.mark.parametrize("seed,tau,normalize", [(1, 1.0, 1), (2, 0.5, 1), (3, 5.0, 1), (4, 1.0, 0), (5, 2.0, 1)])
+@pytest.mark.parametrize("seed,tau,normalize", [(1, 1.0, 1), (2, 0.5, 1), (3, 5.0, 1), (4, 1.0, 0), (5, 2.0, 1),
+                                                (6, 1.0, 3), (7, 2.0, 3)])
 def test_gradient_matches_torch_autograd(seed, tau, normalize):
     """STE backward + Eq. 5 Jacobian
     against torch autograd of the dense formulation, fp64."""
@@ -289,8 +293,9 @@ def test_gradient_matches_torch_autograd(seed, tau, normalize):
     assert o.cnf is cnf
     o.set_state(theta, np.zeros_like(theta), np.zeros_like(theta), 0)
     s = o.step()
-    ref, Lref = _torch_dense_grad(cnf, theta, tau, bool(normalize))
-    ours = s.G * s.extra["rho"][:, None] - s.extra["cv"][:, None]
+    ref, Lref = _torch_dense_grad(cnf, theta, tau, normalize)
+    sgn = np.sign(theta).astype(np.float64) if normalize == 3 else 1.0
+    ours = s.G * s.extra["rho"][:, None] - sgn * s.extra["cv"][:, None]
     scale = np.abs(ref).max()
     # the backward uses the fp32 g table (R26) and fp32 G (R27): fp32 rounding
     assert np.abs(ours - ref).max() <= 4e-7 * scale
@@ -300,10 +305,10 @@ def test_gradient_matches_torch_autograd(seed, tau, normalize):
     G32 = _G_from_g64(o.cnf, s.R, s.g32.astype(np.float64))
     assert np.abs(s.G - G32).max() <= 4 * 2.0 ** -24 * np.abs(G32).max()
     assert abs(s.loss - Lref) <= 1e-12 * abs(Lref)
-    _assert_fp32_fma(s.grad, s.G, s.extra["rho"], s.extra["cv"])
+    _assert_fp32_fma(s.grad, s.G, s.extra["rho"], s.extra["cv"], theta if normalize == 3 else None)
 
 
-def _assert_fp32_fma(grad, G, rho, cv):
+def _assert_fp32_fma(grad, G, rho, cv, theta=None):
     """R27b: grad = fmaf(G, (float)rho, -(float)c), i.e. the exact value
     G rho_f - c_f correctly rounded to fp32 (|err| <= 1/2 ulp, exact rationals)."""
     from fractions import Fraction
@@ -312,7 +317,10 @@ def _assert_fp32_fma(grad, G, rho, cv):
     for v in range(G.shape[0]):
         for j in range(G.shape[1]):
             g = np.float32(grad[v, j])
-            exact = Fraction(float(np.float32(G[v, j]))) * Fraction(float(rf[v])) - Fraction(float(cf[v]))
+            c = Fraction(float(cf[v]))
+            if theta is not None:                 # R28: the Jacobian term carries sign(theta)
+                c = c * int(np.sign(theta[v, j]))
+            exact = Fraction(float(np.float32(G[v, j]))) * Fraction(float(rf[v])) - c
             half_ulp = Fraction(float(np.spacing(np.abs(g)))) / 2
             assert abs(Fraction(float(g)) - exact) <= half_ulp, (v, j)
 
