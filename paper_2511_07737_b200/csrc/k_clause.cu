@@ -54,8 +54,11 @@ __device__ __forceinline__ void csa_add4(uint32_t (&c)[CB], uint32_t m0, uint32_
     }
 }
 
+#ifndef TSAT_CL_MINB8
+#define TSAT_CL_MINB8 2            // CTAs per SM the K <= 7 kernel is compiled for
+#endif
 template <int KB, int KMAXC>
-__global__ void __launch_bounds__(256, KB == 4 ? 3 : 2) k_clause(const uint32_t* __restrict__ A, int NW, int V,
+__global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(const uint32_t* __restrict__ A, int NW, int V,
                                                                 const uint32_t* __restrict__ cptr,
                                                                 const uint32_t* __restrict__ clit, long long C,
                                                                 int* __restrict__ hist, int N, int uniform,
@@ -242,7 +245,7 @@ cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, const StepSca
     const long long ctas_needed = (nchunks + kWarps - 1) / kWarps;
     const int K = a.mc.K;
     // grid-sized: (CTAs resident per SM) x SMs, split over the word blocks
-    const int per_sm = K <= 3 ? 3 : 2;
+    const int per_sm = K <= 3 ? 3 : TSAT_CL_MINB8;
     long long gy = ((long long)a.num_sms * per_sm + nwb - 1) / nwb;
     if (gy > ctas_needed) gy = ctas_needed;
     // packed 21-bit CTA histogram fields (KB = 4): < 2^21 clauses per CTA

@@ -570,8 +570,11 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
 // One warp per (hub super-chunk: <= kHubSlab occurrences, or kHubSlabBatches batches, 32-word block):
 // 11-bit signed vertical counters, two counters per 32x32 transpose (16-bit
 // fields), then exact int32 atomic adds into hubD[hub][r][n].
+#ifndef TSAT_HUB_MINB
+#define TSAT_HUB_MINB 16          // k_hub blocks (warps) per SM the kernel is compiled for (<= 128 registers)
+#endif
 template <int KB, bool BATCHED>
-__global__ void __launch_bounds__(32) k_hub(StepArgs a, const uint32_t* __restrict__ Acur) {
+__global__ void __launch_bounds__(32, TSAT_HUB_MINB) k_hub(StepArgs a, const uint32_t* __restrict__ Acur) {
     constexpr int NP = (KB == 4) ? 2 : 3;
     constexpr int NCTR = KB - 1;
     constexpr int kHubCtr = BATCHED ? kHubCtrBatched : kHubCtrPlain;
