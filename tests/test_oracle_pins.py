@@ -325,17 +325,20 @@ def _assert_fp32_fma(grad, G, rho, cv, theta=None):
             assert abs(Fraction(float(g)) - exact) <= half_ulp, (v, j)
 
 
-def test_euler_invariant():
-    """Eq. 5 is scale invariant per row, so sum_n theta_vn dL/dtheta_vn = 0.
+@pytest.mark.parametrize("normalize", [1, 3])
+def test_euler_invariant(normalize):
+    """Eq. 5 is scale invariant per row (also with the mean-magnitude
+    denominator, R28), so sum_n theta_vn dL/dtheta_vn = 0.
     (theta on a 2^-20 grid so the fixed-point row mean, R10, is exact.)"""
     cnf = planted_ksat(50, 210, 3, 9)
     rng = np.random.default_rng(4)
     th = (np.round(rng.standard_normal((50, 128)) * 2 ** 20) / 2 ** 20).astype(np.float32)
-    o = O.Oracle(cnf, 128, seed=0, init=False)
+    o = O.Oracle(cnf, 128, seed=0, init=False, cfg=O.Config(normalize=normalize))
     o.set_state(th, np.zeros_like(th), np.zeros_like(th), 0)
     s = o.step()
     th = th.astype(np.float64)
-    ours = s.G * s.extra["rho"][:, None] - s.extra["cv"][:, None]
+    sgn = np.sign(th) if normalize == 3 else 1.0
+    ours = s.G * s.extra["rho"][:, None] - sgn * s.extra["cv"][:, None]
     lhs = (th * ours).sum(axis=1)
     scale = np.abs(th * ours).sum(axis=1) + 1e-300
     act = s.extra["guard"] == 0
@@ -627,20 +630,23 @@ def test_per_shard_normalisation_is_independent_shards():
     assert np.array_equal(one.theta, ref.theta)
 
 
-def test_trajectory_determinism_and_shard_invariance():
+@pytest.mark.parametrize("normalize", [1, 3])
+def test_trajectory_determinism_and_shard_invariance(normalize):
     """Same (instance, seed) twice gives identical trajectories; 2- and 4-shard
-    runs (candidate sharding) equal the 1-shard run bit for bit."""
+    runs (candidate sharding) equal the 1-shard run bit for bit
+    (global Eq. 5 and its mean-magnitude reading R28)."""
     cnf = planted_ksat(60, 255, 3, 2)
     N, T = 64, 12
-    a = O.Oracle(cnf, N, seed=9)
-    b = O.Oracle(cnf, N, seed=9)
+    cfg = O.Config(normalize=normalize)
+    a = O.Oracle(cnf, N, seed=9, cfg=cfg)
+    b = O.Oracle(cnf, N, seed=9, cfg=cfg)
     ref = []
     for t in range(T):
         sa, sb = a.step(), b.step()
         assert np.array_equal(a.theta, b.theta) and sa.loss == sb.loss
         ref.append((a.theta.copy(), sa))
     for world in (2, 4):
-        shards, outs = run_sharded(cnf, N, 9, world, T)
+        shards, outs = run_sharded(cnf, N, 9, world, T, cfg=cfg)
         th = np.concatenate([o.theta for o in shards], axis=1)
         assert np.array_equal(th, a.theta)
         for t in range(T):
