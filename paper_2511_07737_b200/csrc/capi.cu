@@ -226,6 +226,11 @@ StepArgs step_args(tsat_ctx ctx) {
     a.upd_gs_global = ctx->upd_gs_global;
     a.upd_GT = ctx->upd_GT;
     a.upd_recbufs = ctx->upd_recbufs;
+#ifndef TSAT_PDL
+#define TSAT_PDL 1
+#endif
+    // PDL on the fused W = 1 sequence (one stream, no forked k_hub branch)
+    a.pdl = TSAT_PDL && !ctx->profiling && !ctx->sharded && !ctx->chunked && !ctx->peer && ctx->cnf.n_hub_sc == 0;
     a.upd_NG = ctx->upd_NG;
     a.upd_grid = ctx->upd_grid;
     a.upd_smem = ctx->upd_smem;

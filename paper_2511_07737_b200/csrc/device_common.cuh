@@ -33,6 +33,12 @@ __device__ __forceinline__ uint32_t ld_plane(const uint32_t* p, unsigned long lo
     return x;
 }
 
+// Programmatic dependent launch: wait for the preceding kernel in the stream
+// (complete, memory visible) and let the next one be scheduled.  Both are
+// no-ops for a kernel launched without the PDL attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Philox4x32-10 (Salmon et al., SC'11), 10 rounds, in place.
 __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
 #pragma unroll

@@ -74,6 +74,8 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(con
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int w = blockIdx.x * 32 + lane;
     const bool valid = w < NW;
+    pdl_wait();
+    pdl_trigger();
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
         // the iteration's accumulators (the previous k_update consumed them):
         // best key and gmax (k_gtable), row scheduler and max|theta_{t+1}| (k_update)
@@ -255,11 +257,14 @@ cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, const StepSca
     dim3 grid(nwb, (unsigned)gy);
     const int uni = a.uniform_len;
     if (K <= 2)
-        k_clause<4, 2><<<grid, 256, 0, st>>>(Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist, a.N, uni && K == 2, a.ds, sc);
+        return launch_maybe_pdl(a.pdl, k_clause<4, 2>, grid, dim3(256), 0, st, Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist,
+                                a.N, (int)(uni && K == 2), a.ds, sc);
     else if (K == 3)
-        k_clause<4, 3><<<grid, 256, 0, st>>>(Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist, a.N, uni, a.ds, sc);
+        return launch_maybe_pdl(a.pdl, k_clause<4, 3>, grid, dim3(256), 0, st, Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist,
+                                a.N, uni, a.ds, sc);
     else
-        k_clause<8, 7><<<grid, 256, 0, st>>>(Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist, a.N, uni && K == 7, a.ds, sc);
+        return launch_maybe_pdl(a.pdl, k_clause<8, 7>, grid, dim3(256), 0, st, Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist,
+                                a.N, (int)(uni && K == 7), a.ds, sc);
     return cudaGetLastError();
 }
 

@@ -92,6 +92,8 @@ __global__ void __launch_bounds__(256) k_gtable(int* __restrict__ hist, int N, l
                                                 int peer, const PeerArgs px) {
     __shared__ double shS[8];
     __shared__ bool last;
+    pdl_wait();
+    pdl_trigger();
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     unsigned long long key = ~0ull;
@@ -384,12 +386,10 @@ cudaError_t launch_rowstats(const float* theta, int V, int N, const MethodConsts
 cudaError_t launch_gtable(const StepArgs& a, const StepScalars* sc, cudaStream_t st) {
     int blocks = (a.N + 255) / 256;
     if (a.KB == 4)
-        k_gtable<4><<<blocks, 256, 0, st>>>(a.hist, a.N, a.C, a.mc, a.gtab, a.S, a.unsat, a.ds, a.sharded, a.lossp, sc,
-                                            a.peer, a.px);
-    else
-        k_gtable<8><<<blocks, 256, 0, st>>>(a.hist, a.N, a.C, a.mc, a.gtab, a.S, a.unsat, a.ds, a.sharded, a.lossp, sc,
-                                            a.peer, a.px);
-    return cudaGetLastError();
+        return launch_maybe_pdl(a.pdl, k_gtable<4>, dim3(blocks), dim3(256), 0, st, a.hist, a.N, a.C, a.mc, a.gtab, a.S,
+                                a.unsat, a.ds, a.sharded, a.lossp, sc, a.peer, a.px);
+    return launch_maybe_pdl(a.pdl, k_gtable<8>, dim3(blocks), dim3(256), 0, st, a.hist, a.N, a.C, a.mc, a.gtab, a.S,
+                            a.unsat, a.ds, a.sharded, a.lossp, sc, a.peer, a.px);
 }
 
 cudaError_t launch_export(const StepArgs& a, long long t_eval, const int* cols_dev, int M, int k, double* absG,

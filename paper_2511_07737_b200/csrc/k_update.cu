@@ -263,6 +263,8 @@ __global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS
     const bool uni3 = a.uniform_len && a.mc.K == 3 && KB == 4;
     const unsigned long long pol = plane_policy(planes_fit_l2(a.V, NW));
 
+    pdl_wait();                                          // k_gtable's table and scalars
+    pdl_trigger();
     // fp32 derivative table of the whole batch -> shared memory
     if (!gs_global)
         for (int i = threadIdx.x * 4; i < KB * N; i += blockDim.x * 4)
@@ -729,9 +731,11 @@ cudaError_t launch_update(const StepArgs& a, const uint32_t* Acur, uint32_t* Ane
         if (a.KB == 4) mag ? k_update<4, 2, true><<<g, b, sm, st>>>(a, Acur, Anext, sc) : k_update<4, 2><<<g, b, sm, st>>>(a, Acur, Anext, sc);
         else mag ? k_update<8, 2, true><<<g, b, sm, st>>>(a, Acur, Anext, sc) : k_update<8, 2><<<g, b, sm, st>>>(a, Acur, Anext, sc);
     } else if (a.KB == 4) {
-        mag ? k_update<4, 0, true><<<g, b, sm, st>>>(a, Acur, Anext, sc) : k_update<4, 0><<<g, b, sm, st>>>(a, Acur, Anext, sc);
+        return mag ? launch_maybe_pdl(a.pdl, k_update<4, 0, true>, g, b, sm, st, a, Acur, Anext, sc)
+                   : launch_maybe_pdl(a.pdl, k_update<4, 0>, g, b, sm, st, a, Acur, Anext, sc);
     } else {
-        mag ? k_update<8, 0, true><<<g, b, sm, st>>>(a, Acur, Anext, sc) : k_update<8, 0><<<g, b, sm, st>>>(a, Acur, Anext, sc);
+        return mag ? launch_maybe_pdl(a.pdl, k_update<8, 0, true>, g, b, sm, st, a, Acur, Anext, sc)
+                   : launch_maybe_pdl(a.pdl, k_update<8, 0>, g, b, sm, st, a, Acur, Anext, sc);
     }
     return cudaGetLastError();
 }

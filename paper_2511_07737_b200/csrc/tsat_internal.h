@@ -6,6 +6,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace tsat {
@@ -170,6 +171,8 @@ struct StepArgs {
     int upd_GT, upd_NG, upd_grid;    // v2 launch geometry
     int upd_rec_cap;                 // record words a group stages per row (max over non-hub rows)
     int upd_recbufs;                 // record buffers per group (1 or 2, configure_update)
+    int pdl;                         // launch k_clause / k_gtable / k_update with programmatic
+                                     // stream serialisation (PDL; fused W = 1 path without hubs)
     size_t upd_smem;
     // candidate-sharded path (world > 1, or a 1-rank communicator)
     int sharded;
@@ -191,6 +194,24 @@ struct Layout {
 };
 
 // ---------------------------------------------------------------- launchers
+// Launch with programmatic stream serialisation when pdl: the kernel may be
+// scheduled while its predecessor in the stream drains, and waits for it with
+// griddepcontrol.wait (pdl_wait) before touching any of its outputs.
+template <typename... Exp, typename... Act>
+inline cudaError_t launch_maybe_pdl(bool pdl, void (*k)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                    Act&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Act>(args)...);
+}
 cudaError_t launch_init(float* theta, float* m, float* v, int V, int N, long long n0, unsigned long long seed,
                         cudaStream_t st);
 cudaError_t launch_rowstats(const float* theta, int V, int N, const MethodConsts& mc, long long* rowQ, double* rowD,
