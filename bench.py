@@ -173,7 +173,9 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": "clause-candidate evals/sec", "value": value, "unit": "evals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * el / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": workload_desc(args.config, cnf, N), "V": cnf.V, "C": cnf.C, "N_global": N},
+        "config": {"workload": workload_desc(args.config, cnf, N), "V": cnf.V, "C": cnf.C, "K": cnf.K,
+                   "N_per_gpu": cfg["N"], "N_global": N, "seed": cfg["seed"],
+                   "parallelism": "CPU oracle, one host thread, on a bounded candidate sample"},
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": 1, "kind": "oracle", "sample": sample,
                          "cpu": model, "host_cores": cores},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
