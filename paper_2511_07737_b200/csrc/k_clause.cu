@@ -189,16 +189,39 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(con
                         atomicAdd(&shp[33 * lane + j], wide);             // padded layout
                     }
             } else {
+                // two 32x32 transposes (bins 0-3, 4-6) give each candidate's
+                // 7-bit counts as bytes; they are widened into 21-bit fields of
+                // three 64-bit CTA accumulators per candidate:
+                // [0] = bins 0, 1, 2   [1] = bins 3, 4, 5   [2] = bin 6
+                unsigned long long* shp = reinterpret_cast<unsigned long long*>(sh);
+                constexpr int kAcc = 33 * 32;                // one padded accumulator plane
+#pragma unroll 1
+                for (int blk = 0; blk < 2; ++blk) {
+                    uint32_t T[32];
 #pragma unroll
-                for (int r = 0; r < KB - 1; ++r)
-#pragma unroll 2
-                    for (int j0 = 0; j0 < 32; ++j0) {
-                        int j = (j0 + lane) & 31;            // rotate: conflict-free smem banks
-                        int val = 0;
-#pragma unroll
-                        for (int b = 0; b < CB; ++b) val |= (int)((cnt[r][b] >> j) & 1u) << b;
-                        if (val) atomicAdd(&sh[r * 1024 + lane * 32 + j], val);
+                    for (int i = 0; i < 32; ++i) {
+                        const int r = i / 8, b = i % 8;
+                        const uint32_t lo = (b < CB) ? cnt[r][b] : 0u;
+                        const uint32_t hi = (b < CB && 4 + r < KB - 1) ? cnt[4 + r][b] : 0u;
+                        T[i] = blk ? hi : lo;
                     }
+                    transpose32(T);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const unsigned long long x = T[j];
+                        if (!x) continue;
+                        const int o = 33 * lane + j;
+                        if (blk == 0) {
+                            const unsigned long long w0 = (x & 0xFFull) | ((x & 0xFF00ull) << 13) | ((x & 0xFF0000ull) << 26);
+                            if (w0) atomicAdd(&shp[o], w0);
+                            if (x >> 24) atomicAdd(&shp[kAcc + o], x >> 24);
+                        } else {
+                            const unsigned long long w1 = ((x & 0xFFull) << 21) | ((x & 0xFF00ull) << 34);
+                            if (w1) atomicAdd(&shp[kAcc + o], w1);
+                            if (x & 0xFF0000ull) atomicAdd(&shp[2 * kAcc + o], (x >> 16) & 0xFFull);
+                        }
+                    }
+                }
             }
         }
     }
@@ -217,11 +240,18 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(con
             }
         }
     } else {
-        for (int i = threadIdx.x; i < (KB - 1) * 1024; i += blockDim.x) {
-            int r = i >> 10, cl = i & 1023;
-            int n = blockIdx.x * 1024 + cl;
-            int val = sh[i];
-            if (n < N && val) atomicAdd(&hist[(size_t)n * KB + r], val);
+        const unsigned long long* shp = reinterpret_cast<const unsigned long long*>(sh);
+        constexpr int kAcc = 33 * 32;
+        for (int cl = threadIdx.x; cl < 1024; cl += blockDim.x) {
+            const int n = blockIdx.x * 1024 + cl;
+            if (n >= N) continue;
+            const int o = 33 * (cl >> 5) + (cl & 31);
+#pragma unroll
+            for (int r = 0; r < KB - 1; ++r) {
+                const unsigned long long pk = shp[(r / 3) * kAcc + o];
+                const int val = (int)((pk >> (21 * (r % 3))) & 0x1FFFFFull);
+                if (val) atomicAdd(&hist[(size_t)n * KB + r], val);
+            }
         }
     }
 }
