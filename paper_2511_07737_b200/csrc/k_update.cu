@@ -34,6 +34,9 @@ constexpr int kUnroll3b = TSAT_3B_UNROLL;
 #ifndef TSAT_UPD_THREADS8
 #define TSAT_UPD_THREADS8 512        // KB = 8 block size bound
 #endif
+#ifndef TSAT_UPD_THREADS4P
+#define TSAT_UPD_THREADS4P 768      // KB = 4 block size bound of the peer-exchange kernel (MODE 2)
+#endif
 #ifndef TSAT_UPD_THREADS4
 #define TSAT_UPD_THREADS4 768       // KB = 4 block size bound (register budget)
 #endif
@@ -230,7 +233,7 @@ __device__ __forceinline__ void gsync(int bar, int GT) {
 // sign(theta) and the next row sums are of |theta| (a template flag: a
 // run-time one costs the default path ~3 % at c2 / c3).
 template <int KB, int MODE, bool MAG = false>
-__global__ void __launch_bounds__(KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS8, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
+__global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TSAT_UPD_THREADS4) : TSAT_UPD_THREADS8, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
                                                                     uint32_t* __restrict__ Anext,
                                                                     const StepScalars* __restrict__ sc) {
     constexpr int NP = (KB == 4) ? 2 : 3;
@@ -658,7 +661,8 @@ cudaError_t configure_update(StepArgs* a) {
     const int NWc = a->upd_chunk >> 5;
     const int GT = NWc >= 128 ? 128 : (NWc > 32 ? 64 : 32);
     const size_t gsb = fused ? upd_gs_bytes(KB, N) : 0;
-    const int max_threads = KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS8;   // register budget (launch bounds)
+    const int max_threads = KB == 4 ? (a->peer ? TSAT_UPD_THREADS4P : TSAT_UPD_THREADS4)
+                                    : TSAT_UPD_THREADS8;   // register budget (launch bounds)
     auto groups = [&](int nbufs) {
         const size_t grb = upd_group_bytes(KB, a->upd_chunk, a->upd_rec_cap, nbufs);
         long long ng = optin > (long long)gsb ? ((long long)optin - (long long)gsb) / (long long)grb : 0;
