@@ -325,9 +325,12 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
             }
         }
     };
-    int pend_v = -1, pend_pb = 0;                          // MODE 2: row awaiting its global Q
-    float pend_m2 = 0.0f;
-    long long pend_q = 0;
+    // MODE 2: the row awaiting its global Q (finished one row late); its
+    // local Q partial and max |theta| live in the group's scratch (tg 0 alone
+    // writes and reads them), its sign planes in the other parity slot
+    int pend_v = -1;
+    long long* pend_q = red + 13;
+    float* pend_m2 = reinterpret_cast<float*>(red + 14);
 
     int item = rowslot[1];
     if (item < nitems && a.hub_of[item / nch] < 0) {      // first row: stage its records now
@@ -336,7 +339,8 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
         for (unsigned i = tg; i < re0 - rb0; i += GT) rec[i] = a.upd_rec[rb0 + i];
     }
     gsync(bar, GT);
-    for (int it = 0; item < nitems; ++it) {
+    int it = 0;
+    for (; item < nitems; ++it) {
         const int v = item / nch;
         const int n0c = (item - v * nch) * NCH;            // first candidate of this chunk
         const int ncand = min(NCH, N - n0c), w0 = n0c >> 5, NWc = ncand >> 5;
@@ -406,7 +410,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
             }
         }
         if (MODE == 2 && pend_v >= 0 && tg == 0)             // previous row's Q, sent a row ago
-            pxs[1] = peer_row_recv(a.px, 1, pend_v, sc->xgen, a.ds, pend_q);
+            pxs[1] = peer_row_recv(a.px, 1, pend_v, sc->xgen, a.ds, *pend_q);
         gsync(bar, GT);
         const int item_next = rowslot[it & 1];              // fetched by tg 0 before the gather
         const int vnext = item_next < nitems ? item_next / nch : a.V;
@@ -422,7 +426,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
         };
         if (nbufs == 1) stage_next();
         if (MODE == 2 && pend_v >= 0) {
-            finish_row(pend_v, pxs[1], posw0 + (size_t)pend_pb * 2 * NW, pend_m2);
+            finish_row(pend_v, pxs[1], posw0 + (size_t)((it + 1) & 1) * 2 * NW, *pend_m2);
             pend_v = -1;
         }
 
@@ -555,9 +559,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
             // next row's gather (the peers' partials have arrived by then)
             if (tg == 0) peer_row_send(a.px, 1, v, Qtot, sc->xgen);
             pend_v = v;
-            pend_pb = it & 1;
-            pend_m2 = m2;
-            pend_q = Qtot;
+            if (tg == 0) { *pend_m2 = m2; *pend_q = Qtot; }
         } else {
             finish_row(v, Qtot, posw, m2);
         }
@@ -565,9 +567,9 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
         // (the next row's barriers order these smem reads before any reuse)
     }
     if (MODE == 2 && pend_v >= 0) {
-        if (tg == 0) pxs[1] = peer_row_recv(a.px, 1, pend_v, sc->xgen, a.ds, pend_q);
+        if (tg == 0) pxs[1] = peer_row_recv(a.px, 1, pend_v, sc->xgen, a.ds, *pend_q);
         gsync(bar, GT);
-        finish_row(pend_v, pxs[1], posw0 + (size_t)pend_pb * 2 * NW, pend_m2);
+        finish_row(pend_v, pxs[1], posw0 + (size_t)((it + 1) & 1) * 2 * NW, *pend_m2);
     }
 }
 
