@@ -5,6 +5,10 @@
 
 #include "tsat_internal.h"
 
+#ifndef TSAT_PLANE_KEEP_BYTES
+#define TSAT_PLANE_KEEP_BYTES 48.0e6     // both plane buffers below this: evict-last gathers
+#endif
+
 namespace tsat {
 
 // L2 cache policy for the bit-plane gathers (created once per kernel):
@@ -25,7 +29,7 @@ __device__ __forceinline__ float jac_addend(float ncf, float th, bool mag) {
 
 // Whether both bit-plane buffers ((V + 1) x NW words each) fit comfortably in L2.
 __host__ __device__ __forceinline__ bool planes_fit_l2(int V, int NW) {
-    return 2.0 * 4.0 * ((double)V + 1.0) * (double)NW <= 48.0e6;
+    return 2.0 * 4.0 * ((double)V + 1.0) * (double)NW <= TSAT_PLANE_KEEP_BYTES;
 }
 __device__ __forceinline__ uint32_t ld_plane(const uint32_t* p, unsigned long long pol) {
     uint32_t x;
