@@ -12,9 +12,12 @@
 //  2. a 32x32 bit transpose turns the counter planes into one packed word of
 //     signed bytes per candidate, staged in shared memory;
 //  3. candidate-major (float4 streams of theta, m, v): G = sum_r d_r g[r]
-//     (fp64, exact products), J_v = sum G theta in int64 fixed point (group
-//     reduction), c_v, grad = (float)(G rho - c), AdamW, Q_{t+1}, max|theta|,
-//     and the sign planes of theta_{t+1} -> bits of the next state.
+//     (fp32 FMA chain over the exact counts, r ascending: R27), J_v = sum G
+//     theta in int64 fixed point (R13, group reduction), c_v, grad =
+//     fmaf(G, rho, -c) (R27b), AdamW, Q_{t+1}, max|theta|, and the sign planes
+//     of theta_{t+1} -> bits of the next state.
+// Records: uniform 3-SAT rows are staged as plain occurrence records, every
+// other instance as batched records (host_cnf.cpp build_batched).
 // Rows whose counts can leave int8 ("hubs", SURVEY §7 hard parts) get their
 // counts from k_hub, which splits a hub's occurrences over many CTAs and adds
 // exact int32 counts (integer atomics: order-free, deterministic).
