@@ -64,10 +64,11 @@ def _worker(rank, world, port, steps, q):
         from tsat_synth import industrial_cnf, planted_ksat
         from paper_2511_07737_b200.binding import merge_partials
         out = {}
-        for name, cnf in (("planted", planted_ksat(80, 336, 3, 7)), ("industrial", industrial_cnf(150, 500, 5))):
+        for name, cnf, nz in (("planted", planted_ksat(80, 336, 3, 7), 1), ("industrial", industrial_cnf(150, 500, 5), 1),
+                              ("planted-mag", planted_ksat(80, 336, 3, 7), 3)):
             N = 64
             Nl = N // world
-            o = O.Oracle(cnf, N, 11, n0=rank * Nl, Nl=Nl)
+            o = O.Oracle(cnf, N, 11, n0=rank * Nl, Nl=Nl, cfg=O.Config(normalize=nz))
             o.comm = GlooComm()
             unsat, losses, best = [], [], []
             for _ in range(steps):
@@ -120,8 +121,9 @@ def test_gloo_sharded_oracle_bit_identical(world):
     res = dict(q.get(timeout=300) for _ in range(world))
     [p.join(timeout=60) for p in procs]
     assert all(p.exitcode == 0 for p in procs)
-    for name, cnf in (("planted", planted_ksat(80, 336, 3, 7)), ("industrial", industrial_cnf(150, 500, 5))):
-        ref = O.Oracle(cnf, 64, 11)
+    for name, cnf, nz in (("planted", planted_ksat(80, 336, 3, 7), 1), ("industrial", industrial_cnf(150, 500, 5), 1),
+                          ("planted-mag", planted_ksat(80, 336, 3, 7), 3)):      # R28 over gloo too
+        ref = O.Oracle(cnf, 64, 11, cfg=O.Config(normalize=nz))
         refs = [ref.step() for _ in range(steps)]
         th = np.concatenate([res[r][name]["theta"] for r in range(world)], axis=1)
         np.testing.assert_array_equal(th, ref.theta)
