@@ -30,56 +30,85 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "tsat_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
 
 CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle (gcc -O2 -ffp-contract=off)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
+    """Compile the oracle (gcc -O2 -ffp-contract=off): the single-thread
+    library and the OpenMP build of the same source (liboracle_omp.so)."""
+    for out, extra in ((_LIB, []), (_LIB_OMP, ["-fopenmp"])):
+        if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+            tmp = out + f".tmp{os.getpid()}"
+            subprocess.check_call(["gcc", *CFLAGS, *extra, "-o", tmp, _SRC, "-lm"])
+            os.replace(tmp, out)
     return _LIB
 
 
 _lib = None
+_lib_omp = None
+_use_omp = False
+
+
+def use_openmp(enabled: bool = True, threads: int | None = None) -> None:
+    """Route every oracle call through the OpenMP build (all host cores, or
+    `threads`).  Results are identical to the single-thread build."""
+    global _use_omp
+    _use_omp = bool(enabled)
+    if threads:
+        os.environ["OMP_NUM_THREADS"] = str(int(threads))
+
+
+def omp_threads() -> int:
+    """Threads the OpenMP build uses (OMP_NUM_THREADS, else all cores)."""
+    return int(os.environ.get("OMP_NUM_THREADS", "0") or 0) or (os.cpu_count() or 1)
 
 
 def lib():
-    global _lib
+    global _lib, _lib_omp
+    if _use_omp:
+        if _lib_omp is None:
+            build()
+            _lib_omp = _bind(ct.CDLL(_LIB_OMP))
+        return _lib_omp
     if _lib is None:
-        _lib = ct.CDLL(build())
-        P = ct.c_void_p
-        i32, i64, u64, f64, f32 = ct.c_int, ct.c_int64, ct.c_uint64, ct.c_double, ct.c_float
-        sig = {
-            "or_philox4x32_10": (None, [P, P, P]),
-            "or_init": (None, [i32, i64, i32, u64, P, P, P]),
-            "or_row_sums": (i32, [i32, i32, P, P]),
-            "or_row_sums_abs": (i32, [i32, i32, P, P]),
-            "or_row_finish": (None, [i32, i64, P, i32, f64, P, P, P, P]),
-            "or_binarize": (None, [i32, i32, P, P, P]),
-            "or_clause_eval": (None, [i32, P, P, i32, P, P]),
-            "or_histogram": (None, [i32, i32, i32, P, P]),
-            "or_smoothmin": (None, [i32, i32, P, P, f64, P, P, P]),
-            "or_smoothmin_direct": (f64, [i32, P, f64]),
-            "or_backward": (None, [i32, i32, P, P, i32, i32, P, P, P]),
-            "or_jacobian_partial": (None, [i32, i32, P, P, P, i64, f64, f32, P, P, P]),
-            "or_jacobian_finish": (None, [i32, i64, P, P, P, P, P, i32, P, P]),
-            "or_grad": (None, [i32, i32, P, P, P, P]),
-            "or_grad_mag": (None, [i32, i32, P, P, P, P, P]),
-            "or_lr_at": (f64, [i64, f64, f64, i32, i32, f64]),
-            "or_adamw": (None, [i32, i64, i32, P, P, P, P, i64, i64, f64, f64, f64, f64, f64, f64, u64]),
-            "or_abs_max": (f32, [ct.c_size_t, P]),
-            "or_gmax": (f64, [i32, i32, P, P]),
-            "or_hist_stream": (None, [i32, P, P, i32, i32, P, P, P]),
-            "or_backward_rows": (None, [i32, P, P, i32, i32, P, P, P, i32, P, P, P]),
-        }
-        for name, (res, args) in sig.items():
-            fn = getattr(_lib, name)
-            fn.restype = res
-            fn.argtypes = args
+        _lib = _bind(ct.CDLL(build()))
     return _lib
+
+
+def _bind(L):
+    """Declare the C signatures on a loaded oracle library."""
+    P = ct.c_void_p
+    i32, i64, u64, f64, f32 = ct.c_int, ct.c_int64, ct.c_uint64, ct.c_double, ct.c_float
+    sig = {
+        "or_philox4x32_10": (None, [P, P, P]),
+        "or_init": (None, [i32, i64, i32, u64, P, P, P]),
+        "or_row_sums": (i32, [i32, i32, P, P]),
+        "or_row_sums_abs": (i32, [i32, i32, P, P]),
+        "or_row_finish": (None, [i32, i64, P, i32, f64, P, P, P, P]),
+        "or_binarize": (None, [i32, i32, P, P, P]),
+        "or_clause_eval": (None, [i32, P, P, i32, P, P]),
+        "or_histogram": (None, [i32, i32, i32, P, P]),
+        "or_smoothmin": (None, [i32, i32, P, P, f64, P, P, P]),
+        "or_smoothmin_direct": (f64, [i32, P, f64]),
+        "or_backward": (None, [i32, i32, P, P, i32, i32, P, P, P]),
+        "or_jacobian_partial": (None, [i32, i32, P, P, P, i64, f64, f32, P, P, P]),
+        "or_jacobian_finish": (None, [i32, i64, P, P, P, P, P, i32, P, P]),
+        "or_grad": (None, [i32, i32, P, P, P, P]),
+        "or_grad_mag": (None, [i32, i32, P, P, P, P, P]),
+        "or_lr_at": (f64, [i64, f64, f64, i32, i32, f64]),
+        "or_adamw": (None, [i32, i64, i32, P, P, P, P, i64, i64, f64, f64, f64, f64, f64, f64, u64]),
+        "or_abs_max": (f32, [ct.c_size_t, P]),
+        "or_gmax": (f64, [i32, i32, P, P]),
+        "or_hist_stream": (None, [i32, P, P, i32, i32, P, P, P]),
+        "or_backward_rows": (None, [i32, P, P, i32, i32, P, P, P, i32, P, P, P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    return L
 
 
 def _p(a: np.ndarray):

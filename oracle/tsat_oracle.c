@@ -11,6 +11,12 @@
  * Build: gcc -O2 -ffp-contract=off -fPIC -shared -o liboracle.so tsat_oracle.c -lm
  * (-ffp-contract=off: every floating operation below is a separate IEEE
  *  round-to-nearest op; fused multiply-adds appear only as explicit fmaf()).
+ * OpenMP mode (SURVEY §8(c) "Form"): the same source built with -fopenmp
+ * (liboracle_omp.so).  The `#pragma omp` lines split only loops whose
+ * iterations write disjoint outputs (rows v, clauses c, candidates j); the
+ * histograms are integer counts summed from per-thread copies.  No value
+ * depends on the thread count (tests/test_oracle_pins2.py checks the two
+ * builds bit for bit); without -fopenmp the pragmas are ignored.
  *
  * Notation follows the paper: V variables, C clauses, N candidate
  * assignments; theta = A_real (one parameter per variable and candidate,
@@ -20,9 +26,26 @@
  * Array layouts: theta/m/v/G/b are [V][N] row-major (candidate fastest);
  * R is [C][N]; h and g are [N][K+1].
  *
- * Where the paper is silent the readings are DESIGN.md §"Readings" R1..R25.
- * Parity pins: tests/test_oracle_pins.py.  "parity unpinned": none of the
- * functions below; trajectory QUALITY (steps-to-SAT) is unpinned.
+ * Where the paper is silent the readings are DESIGN.md §"Readings" R1..R28.
+ * Parity pins (tests/, all -m "not gpu"), one per function:
+ *   or_philox4x32_10   Random123 KAT vectors              test_oracle_pins
+ *   or_init            N(0,1) statistics, KS, shard slices test_oracle_pins
+ *   or_row_sums(_abs), or_row_finish, or_binarize, or_clause_eval, or_histogram
+ *                      Fig. 2 values, brute-force enumeration (V <= 20),
+ *                      double-counting invariants          test_oracle_pins
+ *   or_smoothmin(_direct) 40-digit mpmath of Eq. 4 and its derivative
+ *   or_backward, or_jacobian_*, or_grad(_mag), or_gmax, or_abs_max
+ *                      fp64 torch autograd of the dense graph, element by
+ *                      element at 1e-5 rel (+ operand floor); Euler
+ *                      invariant; fsum                     test_oracle_pins(2)
+ *   or_lr_at           schedule values (R9)
+ *   or_adamw           torch.optim.AdamW fp32 (m, v bit-exact) and fp64
+ *                      (element-wise 1e-5 rel); noise xi distribution (R17)
+ *   or_hist_stream, or_backward_rows (and oracle.step_sampled)
+ *                      bit-exact against or_histogram / or_backward /
+ *                      Oracle.step                         test_oracle_pins2
+ * "parity unpinned": none of the functions; only trajectory QUALITY
+ * (steps-to-SAT) is unpinned (the paper prints no value).
  */
 #include <math.h>
 #include <stdint.h>
@@ -64,6 +87,7 @@ void or_init(int V, int64_t n0, int Nl, uint64_t seed, float* theta, float* m, f
     const double two_pi = 6.283185307179586;
     const double two_m32 = 2.3283064365386963e-10; /* 2^-32 */
     uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    #pragma omp parallel for schedule(static)
     for (int v = 0; v < V; ++v) {
         for (int j = 0; j < Nl; ++j) {
             int64_t n = n0 + j;
@@ -92,6 +116,7 @@ void or_init(int V, int64_t n0, int Nl, uint64_t seed, float* theta, float* m, f
 /* ------------------------------------------------------------------ */
 int or_row_sums(int V, int Nl, const float* theta, int64_t* Q)
 {
+    #pragma omp parallel for schedule(static)
     for (int v = 0; v < V; ++v) {
         int64_t s = 0;
         for (int j = 0; j < Nl; ++j) {
@@ -108,6 +133,7 @@ int or_row_sums(int V, int Nl, const float* theta, int64_t* Q)
  * (same exact fixed point, Q_v >= 0). */
 int or_row_sums_abs(int V, int Nl, const float* theta, int64_t* Q)
 {
+    #pragma omp parallel for schedule(static)
     for (int v = 0; v < V; ++v) {
         int64_t s = 0;
         for (int j = 0; j < Nl; ++j) {
@@ -145,6 +171,7 @@ void or_row_finish(int V, int64_t N, const int64_t* Q, int normalize, double eps
  * theta = 0 gives 0 (R5). */
 void or_binarize(int V, int Nl, const float* theta, const double* d, uint8_t* b)
 {
+    #pragma omp parallel for schedule(static)
     for (int v = 0; v < V; ++v)
         for (int j = 0; j < Nl; ++j) {
             float x = theta[(size_t)v * Nl + j];
@@ -158,6 +185,7 @@ void or_binarize(int V, int Nl, const float* theta, const double* d, uint8_t* b)
 void or_clause_eval(int C, const int64_t* cptr, const int32_t* lits, int Nl,
                     const uint8_t* b, uint8_t* R)
 {
+#pragma omp parallel for schedule(static)
     for (int c = 0; c < C; ++c) {
         uint8_t* row = R + (size_t)c * Nl;
         for (int j = 0; j < Nl; ++j) row[j] = 0;
@@ -178,8 +206,21 @@ void or_clause_eval(int C, const int64_t* cptr, const int32_t* lits, int Nl,
 void or_histogram(int C, int Nl, int K, const uint8_t* R, int32_t* h)
 {
     for (int j = 0; j < Nl * (K + 1); ++j) h[j] = 0;
-    for (int c = 0; c < C; ++c)
-        for (int j = 0; j < Nl; ++j) h[(size_t)j * (K + 1) + R[(size_t)c * Nl + j]] += 1;
+#pragma omp parallel
+    {
+        int32_t* hl = h;
+#ifdef _OPENMP
+        hl = (int32_t*)calloc((size_t)Nl * (K + 1), sizeof(int32_t));   /* this thread's counts */
+#endif
+#pragma omp for schedule(static)
+        for (int c = 0; c < C; ++c)
+            for (int j = 0; j < Nl; ++j) hl[(size_t)j * (K + 1) + R[(size_t)c * Nl + j]] += 1;
+#ifdef _OPENMP
+#pragma omp critical
+        for (int j = 0; j < Nl * (K + 1); ++j) h[j] += hl[j];
+        free(hl);
+#endif
+    }
 }
 
 /* (a6) Eq. 4 SmoothMin and its derivative, per candidate.
@@ -194,6 +235,7 @@ void or_histogram(int C, int Nl, int K, const uint8_t* R, int32_t* h)
 void or_smoothmin(int Nl, int K, const int32_t* h, const double* E, double tau,
                   double* S, double* g, int32_t* rmin_out)
 {
+#pragma omp parallel for schedule(static)
     for (int j = 0; j < Nl; ++j) {
         const int32_t* hn = h + (size_t)j * (K + 1);
         double* gn = g + (size_t)j * (K + 1);
@@ -265,7 +307,10 @@ void or_backward(int V, int C, const int64_t* cptr, const int32_t* lits, int Nl,
             occ_s[fill[v]] = lits[l] > 0 ? 1 : -1;
             fill[v]++;
         }
+#pragma omp parallel
+    {
     int32_t* cnt = (int32_t*)malloc((size_t)Nl * (K + 1) * sizeof(int32_t));
+#pragma omp for schedule(dynamic, 16)
     for (int v = 0; v < V; ++v) {
         memset(cnt, 0, (size_t)Nl * (K + 1) * sizeof(int32_t));
         for (int64_t o = vptr[v]; o < vptr[v + 1]; ++o) {
@@ -280,7 +325,9 @@ void or_backward(int V, int C, const int64_t* cptr, const int32_t* lits, int Nl,
             G[(size_t)v * Nl + j] = (double)acc;
         }
     }
-    free(cnt); free(fill); free(occ_s); free(occ_c); free(vptr);
+    free(cnt);
+    }
+    free(fill); free(occ_s); free(occ_c); free(vptr);
 }
 
 /* ceil(log2(x)) for finite x > 0, exactly (frexp: x = f 2^e, f in [0.5,1)). */
@@ -307,6 +354,7 @@ void or_jacobian_partial(int V, int Nl, const double* G, const float* theta,
                          const int32_t* occ, int64_t N, double gmax, float thmax,
                          int64_t* I, int32_t* s_out, uint8_t* valid)
 {
+    #pragma omp parallel for schedule(static)
     for (int v = 0; v < V; ++v) {
         double x = (double)N * (double)occ[v];
         x = x * gmax;
@@ -346,6 +394,7 @@ void or_jacobian_finish(int V, int64_t N, const int64_t* I, const int32_t* s, co
  * multiply-add of the fp32 G with the row scalars rounded to fp32 (R27b). */
 void or_grad(int V, int Nl, const double* G, const double* rho, const double* cv, float* grad)
 {
+    #pragma omp parallel for schedule(static)
     for (int v = 0; v < V; ++v) {
         const float rf = (float)rho[v], cf = (float)cv[v];
         for (int j = 0; j < Nl; ++j)
@@ -360,6 +409,7 @@ void or_grad(int V, int Nl, const double* G, const double* rho, const double* cv
  * theta_vn (the subgradient of |x| at 0 is taken as 0). */
 void or_grad_mag(int V, int Nl, const double* G, const double* rho, const double* cv, const float* theta, float* grad)
 {
+    #pragma omp parallel for schedule(static)
     for (int v = 0; v < V; ++v) {
         const float rf = (float)rho[v], cf = (float)cv[v];
         for (int j = 0; j < Nl; ++j) {
@@ -414,6 +464,7 @@ void or_adamw(int V, int64_t n0, int Nl, float* theta, float* m, float* vv, cons
     float epsf = (float)eps;
     float nz = (float)(lr * noise_sigma);
     uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+#pragma omp parallel for schedule(static)
     for (int v = 0; v < V; ++v)
         for (int j = 0; j < Nl; ++j) {
             size_t i = (size_t)v * Nl + j;
@@ -467,15 +518,30 @@ void or_hist_stream(int C, const int64_t* cptr, const int32_t* lits, int Nl, int
                     const uint8_t* b, int32_t* h, uint8_t* rowbuf)
 {
     for (int j = 0; j < Nl * (K + 1); ++j) h[j] = 0;
+#pragma omp parallel
+    {
+    int32_t* hl = h;
+    uint8_t* rb = rowbuf;
+#ifdef _OPENMP
+    hl = (int32_t*)calloc((size_t)Nl * (K + 1), sizeof(int32_t));
+    rb = (uint8_t*)malloc((size_t)Nl);
+#endif
+#pragma omp for schedule(static)
     for (int c = 0; c < C; ++c) {
-        for (int j = 0; j < Nl; ++j) rowbuf[j] = 0;
+        for (int j = 0; j < Nl; ++j) rb[j] = 0;
         for (int64_t l = cptr[c]; l < cptr[c + 1]; ++l) {
             int32_t lit = lits[l];
             int v = (lit > 0 ? lit : -lit) - 1;
             const uint8_t* brow = b + (size_t)v * Nl;
-            for (int j = 0; j < Nl; ++j) rowbuf[j] = (uint8_t)(rowbuf[j] + (lit > 0 ? brow[j] : (uint8_t)(1 - brow[j])));
+            for (int j = 0; j < Nl; ++j) rb[j] = (uint8_t)(rb[j] + (lit > 0 ? brow[j] : (uint8_t)(1 - brow[j])));
         }
-        for (int j = 0; j < Nl; ++j) h[(size_t)j * (K + 1) + rowbuf[j]] += 1;
+        for (int j = 0; j < Nl; ++j) hl[(size_t)j * (K + 1) + rb[j]] += 1;
+    }
+#ifdef _OPENMP
+#pragma omp critical
+    for (int j = 0; j < Nl * (K + 1); ++j) h[j] += hl[j];
+    free(hl); free(rb);
+#endif
     }
 }
 

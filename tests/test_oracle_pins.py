@@ -296,9 +296,13 @@ def test_gradient_matches_torch_autograd(seed, tau, normalize):
     ref, Lref = _torch_dense_grad(cnf, theta, tau, normalize)
     sgn = np.sign(theta).astype(np.float64) if normalize == 3 else 1.0
     ours = s.G * s.extra["rho"][:, None] - sgn * s.extra["cv"][:, None]
-    scale = np.abs(ref).max()
-    # the backward uses the fp32 g table (R26) and fp32 G (R27): fp32 rounding
-    assert np.abs(ours - ref).max() <= 4e-7 * scale
+    # element by element (the fp32 g table R26 and fp32 G R27 round each P^T
+    # term): 1e-5 relative, floor 2^-20 x the magnitude of the summed terms
+    # (tests/test_oracle_pins2.py states the criterion)
+    from test_oracle_pins2 import _check_elementwise, _pt_abs
+    terms = _pt_abs(o.cnf, s.R, s.g) * np.abs(s.extra["rho"][:, None]) + np.abs(s.extra["cv"][:, None])
+    _check_elementwise(ours, ref, terms, "G rho - c")
+    _check_elementwise(s.grad, ref, terms, "fp32 grad")
     # G itself is the P^T fold (numpy, fp64 table) up to the fp32 rounding of g
     G64 = _G_from_g64(o.cnf, s.R, s.g)
     assert np.abs(s.G - G64).max() <= 2.4e-7 * np.abs(G64).max()
