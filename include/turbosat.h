@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define TSAT_ABI_VERSION 1
+#define TSAT_ABI_VERSION 2    /* 2: explicit element counts on host-array calls; global export */
 
 typedef struct tsat_ctx_s* tsat_ctx;
 
@@ -194,8 +194,9 @@ tsat_status tsat_step(tsat_ctx ctx, int32_t k, tsat_step_info* out);
 tsat_status tsat_get_info(tsat_ctx ctx, tsat_step_info* out);
 
 /* Per-candidate unsat counts of the last evaluated state for this rank's
- * N_local candidates; *first_global_idx = index of host_out[0]. */
-tsat_status tsat_query_unsat(tsat_ctx ctx, int32_t* host_out, int64_t* first_global_idx);
+ * N_local candidates (§3.1.4 l.169-177); *first_global_idx = index of
+ * host_out[0].  n = elements of host_out, must equal N_local (TSAT_E_ARG). */
+tsat_status tsat_query_unsat(tsat_ctx ctx, int32_t* host_out, size_t n, int64_t* first_global_idx);
 
 /* Asynchronous variants (§3.1.4 l.169-177, same data).  tsat_query_unsat_async
  * enqueues the device->host copy of the N_local counts on the context's
@@ -205,16 +206,34 @@ tsat_status tsat_query_unsat(tsat_ctx ctx, int32_t* host_out, int64_t* first_glo
  * non-NULL out, or a synchronisation of the stream).  With tsat_step(ctx, k,
  * NULL) this lets a caller read every step's result while the next step
  * runs.  tsat_sync blocks until all work queued by this context is done. */
-tsat_status tsat_query_unsat_async(tsat_ctx ctx, int32_t* host_out, int64_t* first_global_idx);
+tsat_status tsat_query_unsat_async(tsat_ctx ctx, int32_t* host_out, size_t n, int64_t* first_global_idx);
 tsat_status tsat_sync(tsat_ctx ctx);
 
-/* (a10/a11) Export: the M best candidates by (unsat asc, index asc) over all
+/* (a10/a11) Export: the M best candidates by (unsat asc, index asc) over ALL
  * ranks, each with its k most confident variables = smallest
  * |G_vn| (ties -> lower v), paired with the candidate's value, all at the last
  * evaluated state (l.279-281; R14, R23).  k <= 0 selects the paper's rule
  * k = min(V, max(ceil(V/10^4), 20)).  host_out: M caller-owned entries whose
- * lits/abs_grad arrays hold at least k entries. */
+ * lits/abs_grad arrays hold at least k entries; 1 <= M <= N_global.
+ * world > 1: a COLLECTIVE call (every rank calls it with the same M, k).  The
+ * ranks all-gather their first M (unsat, index) keys (NCCL, or the peer
+ * buffers), every rank merges them identically, each rank computes the
+ * entries of the selected candidates it owns (only those candidates' bits
+ * are read), and a second all-gather gives every rank the full list.
+ * Multi-GPU limits: M <= 65536 and M * k <= 65536 (TSAT_E_RANGE). */
 tsat_status tsat_export_best(tsat_ctx ctx, int32_t M, int32_t k, tsat_partial* host_out);
+
+/* The number of literals tsat_export_best writes per candidate for a request
+ * k_req (k_req <= 0: the paper's rule k = min(V, max(ceil(V/10^4), 20)),
+ * l.279; else min(k_req, V)), so callers can size the lits / abs_grad arrays. */
+tsat_status tsat_export_k(tsat_ctx ctx, int32_t k_req, int32_t* k_out);
+
+/* Host-only selection step of the export (no context, no GPU): the M smallest
+ * of n candidate keys (unsat << 32 | global index; unused slots ~0), ascending,
+ * into out[0..M).  Keys hold the candidate index, so they are unique and the
+ * order is the paper's (satisfied clauses desc, l.287; ties -> lower index).
+ * tsat_export_best applies it to the all-gathered per-rank lists. */
+tsat_status tsat_merge_keys(const uint64_t* keys, size_t n, int32_t M, uint64_t* out);
 
 /* Binary values (0/1, V bytes) of candidate global_idx at the last evaluated state. */
 tsat_status tsat_export_model(tsat_ctx ctx, int64_t global_idx, uint8_t* host_values);
@@ -226,12 +245,16 @@ tsat_status tsat_get_solution(tsat_ctx ctx, uint8_t* host_values, int64_t* idx, 
 
 /* Checkpoint / resume: theta, m, v as [V][N_local] fp32 host arrays (any may be
  * NULL in get_state) and the iteration counter t. */
-tsat_status tsat_get_state(tsat_ctx ctx, float* theta, float* m, float* v, int64_t* t);
-tsat_status tsat_set_state(tsat_ctx ctx, const float* theta, const float* m, const float* v, int64_t t);
+/* elems = elements of each non-NULL array; must equal V * N_local (TSAT_E_ARG
+ * otherwise, e.g. a checkpoint of another world size or batch). */
+tsat_status tsat_get_state(tsat_ctx ctx, float* theta, float* m, float* v, size_t elems, int64_t* t);
+tsat_status tsat_set_state(tsat_ctx ctx, const float* theta, const float* m, const float* v, size_t elems, int64_t t);
 
 /* Rows rows[0..nrows) (0-based variables) of theta, m, v into host arrays of
- * [nrows][N_local] fp32 (any may be NULL): sampled checks at full size. */
-tsat_status tsat_get_rows(tsat_ctx ctx, const int32_t* rows, int32_t nrows, float* theta, float* m, float* v);
+ * [nrows][N_local] fp32 (any may be NULL): sampled checks at full size.
+ * row_elems must equal N_local. */
+tsat_status tsat_get_rows(tsat_ctx ctx, const int32_t* rows, int32_t nrows, float* theta, float* m, float* v,
+                          size_t row_elems);
 
 /* Copy an internal buffer to host (tests / diagnostics):
  *   which 0: histogram h [N_local][KB] int32 of the last evaluated state (KB = 4 if K <= 3 else 8)

@@ -18,10 +18,9 @@ from .binding import (  # noqa: F401
     TsatError,
     config_default,
     load_library,
-    merge_partials,
     nccl_unique_id,
     parse_dimacs,
 )
 
-__all__ = ["Solver", "StepInfo", "TsatError", "config_default", "load_library", "merge_partials", "nccl_unique_id",
+__all__ = ["Solver", "StepInfo", "TsatError", "config_default", "load_library", "nccl_unique_id",
            "parse_dimacs", "LIB_PATH"]

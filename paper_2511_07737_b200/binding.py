@@ -68,16 +68,18 @@ _SIGS = {
     "tsat_init_batch": (ct.c_int, [P, ct.c_int64, ct.c_uint64, ct.POINTER(tsat_config), P, ct.c_size_t]),
     "tsat_step": (ct.c_int, [P, ct.c_int32, ct.POINTER(tsat_step_info)]),
     "tsat_get_info": (ct.c_int, [P, ct.POINTER(tsat_step_info)]),
-    "tsat_query_unsat_async": (ct.c_int, [P, P, ct.POINTER(ct.c_int64)]),
+    "tsat_query_unsat_async": (ct.c_int, [P, P, ct.c_size_t, ct.POINTER(ct.c_int64)]),
     "tsat_sync": (ct.c_int, [P]),
-    "tsat_query_unsat": (ct.c_int, [P, P, ct.POINTER(ct.c_int64)]),
+    "tsat_query_unsat": (ct.c_int, [P, P, ct.c_size_t, ct.POINTER(ct.c_int64)]),
     "tsat_export_best": (ct.c_int, [P, ct.c_int32, ct.c_int32, ct.POINTER(tsat_partial)]),
+    "tsat_export_k": (ct.c_int, [P, ct.c_int32, ct.POINTER(ct.c_int32)]),
+    "tsat_merge_keys": (ct.c_int, [P, ct.c_size_t, ct.c_int32, P]),
     "tsat_export_model": (ct.c_int, [P, ct.c_int64, P]),
     "tsat_get_solution": (ct.c_int, [P, P, ct.POINTER(ct.c_int64), ct.POINTER(ct.c_int64)]),
-    "tsat_get_state": (ct.c_int, [P, P, P, P, ct.POINTER(ct.c_int64)]),
-    "tsat_set_state": (ct.c_int, [P, P, P, P, ct.c_int64]),
+    "tsat_get_state": (ct.c_int, [P, P, P, P, ct.c_size_t, ct.POINTER(ct.c_int64)]),
+    "tsat_set_state": (ct.c_int, [P, P, P, P, ct.c_size_t, ct.c_int64]),
     "tsat_debug_copy": (ct.c_int, [P, ct.c_int32, P, ct.c_size_t]),
-    "tsat_get_rows": (ct.c_int, [P, P, ct.c_int32, P, P, P]),
+    "tsat_get_rows": (ct.c_int, [P, P, ct.c_int32, P, P, P, ct.c_size_t]),
     "tsat_set_profiling": (ct.c_int, [P, ct.c_int32]),
     "tsat_kernel_times": (ct.c_int, [P, P, ct.POINTER(ct.c_int64)]),
     "tsat_kernels_per_step": (ct.c_int, [P, ct.POINTER(ct.c_int32)]),
@@ -133,12 +135,14 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def merge_partials(per_rank: list, M: int) -> list:
-    """Global top-M of per-rank export lists by (unsat asc, candidate asc)
-    (R15).  Host logic of the sharded export."""
-    allp = [p for lst in per_rank for p in lst]
-    allp.sort(key=lambda p: (p["unsat"], p["candidate"]))
-    return allp[:M]
+def merge_keys(keys: np.ndarray, M: int) -> np.ndarray:
+    """tsat_merge_keys (host only): the M smallest (unsat << 32 | index) keys."""
+    k = np.ascontiguousarray(keys, np.uint64)
+    out = np.empty(M, np.uint64)
+    s = load_library().tsat_merge_keys(_ptr(k), k.size, int(M), _ptr(out))
+    if s:
+        raise TsatError(s, "tsat_merge_keys")
+    return out
 
 
 @dataclass
@@ -300,16 +304,19 @@ class Solver:
         n = self.N_local_count()
         if out is None:
             out = np.empty(n, np.int32)
+        if out.dtype != np.int32 or out.shape != (n,) or not out.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"out must be a contiguous int32 array of shape ({n},)")
         first = ct.c_int64()
-        self._check(self.lib.tsat_query_unsat(self.h, _ptr(out), ct.byref(first)))
+        self._check(self.lib.tsat_query_unsat(self.h, _ptr(out), out.size, ct.byref(first)))
         self.n0 = first.value
         return out
 
-    def query_unsat_async(self, out_ptr: int) -> None:
+    def query_unsat_async(self, out_ptr: int, n: int | None = None) -> None:
         """Enqueue the unsat-count copy into PINNED host memory at out_ptr
-        (N_local int32); valid after sync() or another blocking call."""
+        (n = N_local int32); valid after sync() or another blocking call."""
         first = ct.c_int64()
-        self._check(self.lib.tsat_query_unsat_async(self.h, ct.c_void_p(int(out_ptr)), ct.byref(first)))
+        n = self.N_local_count() if n is None else int(n)
+        self._check(self.lib.tsat_query_unsat_async(self.h, ct.c_void_p(int(out_ptr)), n, ct.byref(first)))
         self.n0 = first.value
 
     def sync(self) -> None:
@@ -319,7 +326,12 @@ class Solver:
         return self.N // self.world
 
     def export_best(self, M: int, k: int = 0):
-        kk = k if k > 0 else min(self.V, max(-(-self.V // 10000), 20))
+        """tsat_export_best: the M best candidates over all ranks (a collective
+        call when world > 1), each with its k most confident literals; k <= 0
+        lets the library apply the paper's rule (buffers sized for k = V)."""
+        kk = ct.c_int32()
+        self._check(self.lib.tsat_export_k(self.h, int(k), ct.byref(kk)))
+        kk = kk.value
         bufs = []
         arr = (tsat_partial * M)()
         for i in range(M):
@@ -352,14 +364,19 @@ class Solver:
         m = np.empty_like(th)
         v = np.empty_like(th)
         t = ct.c_int64()
-        self._check(self.lib.tsat_get_state(self.h, _ptr(th), _ptr(m), _ptr(v), ct.byref(t)))
+        self._check(self.lib.tsat_get_state(self.h, _ptr(th), _ptr(m), _ptr(v), th.size, ct.byref(t)))
         return th, m, v, t.value
 
     def set_state(self, theta, m, v, t: int):
-        th = np.ascontiguousarray(theta, np.float32)
-        mm = np.ascontiguousarray(m, np.float32)
-        vv = np.ascontiguousarray(v, np.float32)
-        self._check(self.lib.tsat_set_state(self.h, _ptr(th), _ptr(mm), _ptr(vv), int(t)))
+        shape = (self.V, self.N_local_count())
+        arrs = []
+        for name, x in (("theta", theta), ("m", m), ("v", v)):
+            x = np.asarray(x)
+            if x.dtype != np.float32 or x.shape != shape:
+                raise ValueError(f"{name} must be float32 of shape {shape} (got {x.dtype} {x.shape})")
+            arrs.append(np.ascontiguousarray(x))
+        th, mm, vv = arrs
+        self._check(self.lib.tsat_set_state(self.h, _ptr(th), _ptr(mm), _ptr(vv), th.size, int(t)))
 
     def get_rows(self, rows):
         r = np.ascontiguousarray(rows, np.int32)
@@ -367,7 +384,7 @@ class Solver:
         th = np.empty((len(r), n), np.float32)
         m = np.empty_like(th)
         v = np.empty_like(th)
-        self._check(self.lib.tsat_get_rows(self.h, _ptr(r), len(r), _ptr(th), _ptr(m), _ptr(v)))
+        self._check(self.lib.tsat_get_rows(self.h, _ptr(r), len(r), _ptr(th), _ptr(m), _ptr(v), n))
         return th, m, v
 
     def debug(self, which: int, dtype, shape) -> np.ndarray:

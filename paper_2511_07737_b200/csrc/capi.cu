@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <new>
+#include <stdexcept>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -104,13 +106,51 @@ tsat_status cuda_fail(tsat_ctx c, cudaError_t e, const char* where) {
         if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call);  \
     } while (0)
 
+// Makes ctx->device current for the duration of an entry point and restores
+// the caller's current device on return (calls on a context whose
+// device is not current, and callers that switch devices).
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DevGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
 #define GUARD_CTX()                                    \
-    do {                                               \
-        if (!ctx) return TSAT_E_ARG;                   \
-        if (ctx->poisoned != TSAT_OK) return ctx->poisoned; \
-    } while (0)
+    if (!ctx) return TSAT_E_ARG;                       \
+    if (ctx->poisoned != TSAT_OK) return ctx->poisoned; \
+    DevGuard dev_guard_(ctx->device)
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+float __uint_as_float_host(uint32_t u) {
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+}
+
+// No C++ exception crosses the C ABI: host allocation failures map to
+// TSAT_E_OOM, anything else to TSAT_E_ARG.
+template <class F>
+tsat_status no_throw(tsat_ctx ctx, F&& f) {
+    try {
+        return f();
+    } catch (const std::bad_alloc&) {
+        if (ctx) ctx->err = "host allocation failed";
+        return TSAT_E_OOM;
+    } catch (const std::exception& ex) {
+        if (ctx) ctx->err = std::string("exception: ") + ex.what();
+        return TSAT_E_ARG;
+    } catch (...) {
+        if (ctx) ctx->err = "unknown exception";
+        return TSAT_E_ARG;
+    }
+}
 
 // Exchange buffers created in this process, by IPC handle: a rank whose peer
 // lives in the same process (tests: several ranks on one GPU) maps it directly
@@ -617,73 +657,81 @@ const char* tsat_status_string(tsat_status s) {
 }
 
 tsat_status tsat_parse_dimacs(const char* text, size_t len, tsat_cnf_info* info) {
-    if (!text && len) return TSAT_E_ARG;
-    int32_t V;
-    std::vector<int64_t> ptr;
-    std::vector<int32_t> lits;
-    int64_t hc, nw;
-    std::string msg;
-    if (parse_dimacs(text, len, &V, &ptr, &lits, &hc, &nw, &msg)) return TSAT_E_PARSE;
-    HostCnf h;
-    int r = build_cnf(V, (int64_t)ptr.size() - 1, ptr.data(), lits.data(), &h, &msg);
-    if (r) return r == 3 ? TSAT_E_RANGE : TSAT_E_ARG;
-    h.header_C = hc;
-    h.n_warnings = nw;
-    fill_info(h, info);
-    return TSAT_OK;
+    return no_throw(nullptr, [&]() -> tsat_status {
+        if (!text && len) return TSAT_E_ARG;
+        int32_t V;
+        std::vector<int64_t> ptr;
+        std::vector<int32_t> lits;
+        int64_t hc, nw;
+        std::string msg;
+        if (parse_dimacs(text, len, &V, &ptr, &lits, &hc, &nw, &msg)) return TSAT_E_PARSE;
+        HostCnf h;
+        int r = build_cnf(V, (int64_t)ptr.size() - 1, ptr.data(), lits.data(), &h, &msg);
+        if (r) return r == 3 ? TSAT_E_RANGE : TSAT_E_ARG;
+        h.header_C = hc;
+        h.n_warnings = nw;
+        fill_info(h, info);
+        return TSAT_OK;
+    });
 }
 
 tsat_status tsat_create(tsat_ctx* out, int cuda_device, void* cuda_stream, const void* nccl_unique_id, int rank,
                         int world) {
-    if (!out) return TSAT_E_ARG;
-    *out = nullptr;
-    if (world < 1 || rank < 0 || rank >= world) return TSAT_E_ARG;
-    if (world > 1 && !nccl_unique_id) return TSAT_E_ARG;
-    std::unique_ptr<tsat_ctx_s> c(new tsat_ctx_s());
-    c->device = cuda_device;
-    c->stream = (cudaStream_t)cuda_stream;
-    c->rank = rank;
-    c->world = world;
-    tsat_ctx ctx = c.get();
-    CK(cudaSetDevice(cuda_device));
-    CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
-    CK(cudaMallocHost(&c->h_steptab, 2 * sizeof(StepScalars) * kMaxStepsPerCall));
-    for (auto& e : c->tab_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    CK(cudaMallocHost(&c->h_scal, sizeof(DevScalars)));
-    tsat_config_default(&c->cfg);
-    if (nccl_unique_id) {           // candidate-sharded path (also with a 1-rank communicator)
-        std::string err;
-        if (comm_init(&c->comm, nccl_unique_id, rank, world, &err)) {
-            cudaStreamDestroy(c->cap_stream);
-            cudaFreeHost(c->h_steptab);
-            cudaFreeHost(c->h_scal);
-            return TSAT_E_NCCL;
+    return no_throw(nullptr, [&]() -> tsat_status {
+        if (!out) return TSAT_E_ARG;
+        *out = nullptr;
+        if (world < 1 || rank < 0 || rank >= world) return TSAT_E_ARG;
+        if (world > 1 && !nccl_unique_id) return TSAT_E_ARG;
+        DevGuard dev_guard_(cuda_device);
+        std::unique_ptr<tsat_ctx_s> c(new tsat_ctx_s());
+        c->device = cuda_device;
+        c->stream = (cudaStream_t)cuda_stream;
+        c->rank = rank;
+        c->world = world;
+        tsat_ctx ctx = c.get();
+        CK(cudaSetDevice(cuda_device));
+        CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+        CK(cudaMallocHost(&c->h_steptab, 2 * sizeof(StepScalars) * kMaxStepsPerCall));
+        for (auto& e : c->tab_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaMallocHost(&c->h_scal, sizeof(DevScalars)));
+        tsat_config_default(&c->cfg);
+        if (nccl_unique_id) {           // candidate-sharded path (also with a 1-rank communicator)
+            std::string err;
+            if (comm_init(&c->comm, nccl_unique_id, rank, world, &err)) {
+                cudaStreamDestroy(c->cap_stream);
+                cudaFreeHost(c->h_steptab);
+                cudaFreeHost(c->h_scal);
+                return TSAT_E_NCCL;
+            }
+            c->sharded = true;
         }
-        c->sharded = true;
-    }
-    *out = c.release();
-    return TSAT_OK;
+        *out = c.release();
+        return TSAT_OK;
+    });
 }
 
 tsat_status tsat_create_peer(tsat_ctx* out, int cuda_device, void* cuda_stream, int rank, int world) {
-    if (!out) return TSAT_E_ARG;
-    *out = nullptr;
-    if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world) return TSAT_E_ARG;
-    std::unique_ptr<tsat_ctx_s> c(new tsat_ctx_s());
-    c->device = cuda_device;
-    c->stream = (cudaStream_t)cuda_stream;
-    c->rank = rank;
-    c->world = world;
-    c->peer = true;
-    tsat_ctx ctx = c.get();
-    CK(cudaSetDevice(cuda_device));
-    CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
-    CK(cudaMallocHost(&c->h_steptab, 2 * sizeof(StepScalars) * kMaxStepsPerCall));
-    for (auto& e : c->tab_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    CK(cudaMallocHost(&c->h_scal, sizeof(DevScalars)));
-    tsat_config_default(&c->cfg);
-    *out = c.release();
-    return TSAT_OK;
+    return no_throw(nullptr, [&]() -> tsat_status {
+        if (!out) return TSAT_E_ARG;
+        *out = nullptr;
+        if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world) return TSAT_E_ARG;
+        DevGuard dev_guard_(cuda_device);
+        std::unique_ptr<tsat_ctx_s> c(new tsat_ctx_s());
+        c->device = cuda_device;
+        c->stream = (cudaStream_t)cuda_stream;
+        c->rank = rank;
+        c->world = world;
+        c->peer = true;
+        tsat_ctx ctx = c.get();
+        CK(cudaSetDevice(cuda_device));
+        CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+        CK(cudaMallocHost(&c->h_steptab, 2 * sizeof(StepScalars) * kMaxStepsPerCall));
+        for (auto& e : c->tab_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaMallocHost(&c->h_scal, sizeof(DevScalars)));
+        tsat_config_default(&c->cfg);
+        *out = c.release();
+        return TSAT_OK;
+    });
 }
 
 tsat_status tsat_peer_handle(tsat_ctx ctx, void* out, size_t bytes) {
@@ -740,32 +788,36 @@ tsat_status tsat_nccl_unique_id(void* out, size_t bytes) {
 }
 
 tsat_status tsat_load_dimacs(tsat_ctx ctx, const char* text, size_t len, tsat_cnf_info* info) {
-    GUARD_CTX();
-    if (!text && len) return fail(ctx, TSAT_E_ARG, "null text");
-    int32_t V;
-    std::vector<int64_t> ptr;
-    std::vector<int32_t> lits;
-    int64_t hc, nw;
-    std::string msg;
-    if (parse_dimacs(text, len, &V, &ptr, &lits, &hc, &nw, &msg)) return fail(ctx, TSAT_E_PARSE, msg);
-    HostCnf h;
-    int r = build_cnf(V, (int64_t)ptr.size() - 1, ptr.data(), lits.data(), &h, &msg);
-    if (r) return fail(ctx, r == 3 ? TSAT_E_RANGE : TSAT_E_ARG, msg);
-    h.header_C = hc;
-    h.n_warnings = nw;
-    fill_info(h, info);
-    return upload_cnf(ctx, std::move(h));
+    return no_throw(ctx, [&]() -> tsat_status {
+        GUARD_CTX();
+        if (!text && len) return fail(ctx, TSAT_E_ARG, "null text");
+        int32_t V;
+        std::vector<int64_t> ptr;
+        std::vector<int32_t> lits;
+        int64_t hc, nw;
+        std::string msg;
+        if (parse_dimacs(text, len, &V, &ptr, &lits, &hc, &nw, &msg)) return fail(ctx, TSAT_E_PARSE, msg);
+        HostCnf h;
+        int r = build_cnf(V, (int64_t)ptr.size() - 1, ptr.data(), lits.data(), &h, &msg);
+        if (r) return fail(ctx, r == 3 ? TSAT_E_RANGE : TSAT_E_ARG, msg);
+        h.header_C = hc;
+        h.n_warnings = nw;
+        fill_info(h, info);
+        return upload_cnf(ctx, std::move(h));
+    });
 }
 
 tsat_status tsat_load_clauses(tsat_ctx ctx, int32_t V, int64_t C, const int64_t* clause_ptr, const int32_t* lits,
                               tsat_cnf_info* info) {
-    GUARD_CTX();
-    std::string msg;
-    HostCnf h;
-    int r = build_cnf(V, C, clause_ptr, lits, &h, &msg);
-    if (r) return fail(ctx, r == 3 ? TSAT_E_RANGE : TSAT_E_ARG, msg);
-    fill_info(h, info);
-    return upload_cnf(ctx, std::move(h));
+    return no_throw(ctx, [&]() -> tsat_status {
+        GUARD_CTX();
+        std::string msg;
+        HostCnf h;
+        int r = build_cnf(V, C, clause_ptr, lits, &h, &msg);
+        if (r) return fail(ctx, r == 3 ? TSAT_E_RANGE : TSAT_E_ARG, msg);
+        fill_info(h, info);
+        return upload_cnf(ctx, std::move(h));
+    });
 }
 
 tsat_status tsat_workspace_bytes(tsat_ctx ctx, int64_t N_global, size_t* bytes) {
@@ -790,126 +842,137 @@ tsat_status tsat_workspace_bytes(tsat_ctx ctx, int64_t N_global, size_t* bytes) 
 
 tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const tsat_config* cfg, void* ws,
                             size_t bytes) {
-    GUARD_CTX();
-    size_t need;
-    tsat_status s = tsat_workspace_bytes(ctx, N_global, &need);
-    if (s != TSAT_OK) return s;
-    if (!ws || bytes < need) return fail(ctx, TSAT_E_OOM, "workspace too small");
-    if ((uintptr_t)ws % 256) return fail(ctx, TSAT_E_ARG, "workspace must be 256-byte aligned");
-    if (ctx->peer && !ctx->peers_ready) return fail(ctx, TSAT_E_STATE, "peer context: call tsat_peer_open first");
-    tsat_config c;
-    if (cfg) c = *cfg; else tsat_config_default(&c);
-    if (!(c.tau > 0) || c.decay_every < 1 || c.restart_every < 1 || !(c.decay_factor > 0) || !(c.eps_norm > 0) ||
-        c.normalize < 0 || c.normalize > 3 || (c.reset_moments_on_restart & ~1))
-        return fail(ctx, TSAT_E_ARG, "invalid config");
-    drop_graphs(ctx);
-    ctx->cfg = c;
-    ctx->N_global = N_global;
-    ctx->N = (int)(N_global / ctx->world);
-    ctx->n0 = (long long)ctx->rank * ctx->N;
-    ctx->KB = ctx->cnf.K <= 3 ? 4 : 8;
-    ctx->seed = seed;
-    ctx->ws = (char*)ws;
-    ctx->ws_bytes = bytes;
-    {
-        bool ch = false;
-        tsat_status s2 = batch_chunked(ctx, ctx->N, ctx->KB, &ch);
-        if (s2 != TSAT_OK) return s2;
-        ctx->chunked = ch;
-    }
-    if (ctx->chunked && ctx->peer)
-        return fail(ctx, TSAT_E_RANGE, "peer path: N per GPU too large for the fused kernel (use more GPUs)");
-    ctx->L = make_layout(ctx->cnf.V, ctx->N, ctx->KB, ctx->cnf.n_hubs, ctx->sharded || ctx->chunked, ctx->peer);
-    MethodConsts& mc = ctx->mc;
-    mc = MethodConsts{};
-    for (int d = 0; d < 8; ++d) mc.E[d] = std::exp(-c.tau * (double)d);
-    mc.tau = c.tau;
-    mc.eps_norm = c.eps_norm;
-    mc.normalize = c.normalize;                 // 0 off, 1 global, 2 per shard, 3 global mean magnitude (R28)
-    mc.K = ctx->cnf.K;
-    mc.Nnorm = c.normalize == 2 ? N_global / ctx->world : N_global;
-    mc.n0 = ctx->n0;
-    mc.seed = seed;
-    mc.noise = c.noise_sigma != 0.0;
-    ctx->t = 0;
-    ctx->steps_done = 0;
-    CK(cudaSetDevice(ctx->device));
-    {
-        StepArgs g = step_args(ctx);
-        CK(configure_kernels(&g));
-        ctx->upd_mode = g.upd_mode;
-        ctx->upd_GT = g.upd_GT;
-        ctx->upd_recbufs = g.upd_recbufs;
-        ctx->upd_NG = g.upd_NG;
-        ctx->upd_grid = g.upd_grid;
-        ctx->upd_smem = g.upd_smem;
-        ctx->num_sms = g.num_sms;
-        ctx->upd_chunk = g.upd_chunk;
-        ctx->upd_gs_global = g.upd_gs_global;
-    }
-    if (ctx->chunked != (ctx->upd_chunk < ctx->N))
-        return fail(ctx, TSAT_E_STATE, "internal: chunking decision changed between layout and launch");
-    StepArgs a = step_args(ctx);
-    if (ctx->L.hubD != ctx->L.total)
-        CK(cudaMemsetAsync(ctx->ws + ctx->L.hubD, 0, ctx->L.total - ctx->L.hubD, ctx->stream));
-    CK(cudaMemsetAsync(ctx->ws + ctx->L.hist, 0, (size_t)ctx->N * ctx->KB * 4, ctx->stream));
-    CK(cudaMemsetAsync(ctx->ws + ctx->L.scal, 0, sizeof(DevScalars), ctx->stream));
-    {
-        const size_t rowb = (size_t)(ctx->N / 32) * 4, zoff = (size_t)ctx->cnf.V * rowb;
-        CK(cudaMemsetAsync(ctx->ws + ctx->L.A0 + zoff, 0, rowb, ctx->stream));
-        CK(cudaMemsetAsync(ctx->ws + ctx->L.A1 + zoff, 0, rowb, ctx->stream));
-    }
-    DevScalars init{};
-    init.best_key = ~0ull;
-    init.sol_step = -1;
-    init.sol_idx = -1;
-    init.info_best_unsat = -1;
-    init.info_best_idx = -1;
-    *ctx->h_scal = init;
-    CK(cudaMemcpyAsync(a.ds, ctx->h_scal, sizeof(DevScalars), cudaMemcpyHostToDevice, ctx->stream));
-    CK(launch_init(a.theta, a.m, a.v, a.V, a.N, ctx->n0, seed, ctx->stream));
-    s = state_stats(ctx, a, 0);
-    if (s != TSAT_OK) return s;
-    ctx->have_batch = true;
-    return TSAT_OK;
+    return no_throw(ctx, [&]() -> tsat_status {
+        GUARD_CTX();
+        size_t need;
+        tsat_status s = tsat_workspace_bytes(ctx, N_global, &need);
+        if (s != TSAT_OK) return s;
+        if (!ws || bytes < need) return fail(ctx, TSAT_E_OOM, "workspace too small");
+        if ((uintptr_t)ws % 256) return fail(ctx, TSAT_E_ARG, "workspace must be 256-byte aligned");
+        if (ctx->peer && !ctx->peers_ready) return fail(ctx, TSAT_E_STATE, "peer context: call tsat_peer_open first");
+        tsat_config c;
+        if (cfg) c = *cfg; else tsat_config_default(&c);
+        if (!(c.tau > 0) || c.decay_every < 1 || c.restart_every < 1 || !(c.decay_factor > 0) || !(c.eps_norm > 0) ||
+            c.normalize < 0 || c.normalize > 3 || (c.reset_moments_on_restart & ~1))
+            return fail(ctx, TSAT_E_ARG, "invalid config");
+        drop_graphs(ctx);
+        ctx->cfg = c;
+        ctx->N_global = N_global;
+        ctx->N = (int)(N_global / ctx->world);
+        ctx->n0 = (long long)ctx->rank * ctx->N;
+        ctx->KB = ctx->cnf.K <= 3 ? 4 : 8;
+        ctx->seed = seed;
+        ctx->ws = (char*)ws;
+        ctx->ws_bytes = bytes;
+        {
+            bool ch = false;
+            tsat_status s2 = batch_chunked(ctx, ctx->N, ctx->KB, &ch);
+            if (s2 != TSAT_OK) return s2;
+            ctx->chunked = ch;
+        }
+        if (ctx->chunked && ctx->peer)
+            return fail(ctx, TSAT_E_RANGE, "peer path: N per GPU too large for the fused kernel (use more GPUs)");
+        ctx->L = make_layout(ctx->cnf.V, ctx->N, ctx->KB, ctx->cnf.n_hubs, ctx->sharded || ctx->chunked, ctx->peer);
+        MethodConsts& mc = ctx->mc;
+        mc = MethodConsts{};
+        for (int d = 0; d < 8; ++d) mc.E[d] = std::exp(-c.tau * (double)d);
+        mc.tau = c.tau;
+        mc.eps_norm = c.eps_norm;
+        mc.normalize = c.normalize;                 // 0 off, 1 global, 2 per shard, 3 global mean magnitude (R28)
+        mc.K = ctx->cnf.K;
+        mc.Nnorm = c.normalize == 2 ? N_global / ctx->world : N_global;
+        mc.n0 = ctx->n0;
+        mc.seed = seed;
+        mc.noise = c.noise_sigma != 0.0;
+        {   // fixed-point loss scale: N_global * K * 2^e < 2^61, e <= 40
+            int e = 40;
+            const double bound = (double)N_global * (double)std::max(ctx->cnf.K, 1);
+            while (e > -60 && std::ldexp(bound, e) >= std::ldexp(1.0, 61)) --e;
+            mc.loss_scale = std::ldexp(1.0, e);
+            mc.loss_unscale = std::ldexp(1.0, -e);
+        }
+        ctx->t = 0;
+        ctx->steps_done = 0;
+        CK(cudaSetDevice(ctx->device));
+        {
+            StepArgs g = step_args(ctx);
+            CK(configure_kernels(&g));
+            ctx->upd_mode = g.upd_mode;
+            ctx->upd_GT = g.upd_GT;
+            ctx->upd_recbufs = g.upd_recbufs;
+            ctx->upd_NG = g.upd_NG;
+            ctx->upd_grid = g.upd_grid;
+            ctx->upd_smem = g.upd_smem;
+            ctx->num_sms = g.num_sms;
+            ctx->upd_chunk = g.upd_chunk;
+            ctx->upd_gs_global = g.upd_gs_global;
+        }
+        if (ctx->chunked != (ctx->upd_chunk < ctx->N))
+            return fail(ctx, TSAT_E_STATE, "internal: chunking decision changed between layout and launch");
+        StepArgs a = step_args(ctx);
+        if (ctx->L.hubD != ctx->L.total)
+            CK(cudaMemsetAsync(ctx->ws + ctx->L.hubD, 0, ctx->L.total - ctx->L.hubD, ctx->stream));
+        CK(cudaMemsetAsync(ctx->ws + ctx->L.hist, 0, (size_t)ctx->N * ctx->KB * 4, ctx->stream));
+        CK(cudaMemsetAsync(ctx->ws + ctx->L.scal, 0, sizeof(DevScalars), ctx->stream));
+        {
+            const size_t rowb = (size_t)(ctx->N / 32) * 4, zoff = (size_t)ctx->cnf.V * rowb;
+            CK(cudaMemsetAsync(ctx->ws + ctx->L.A0 + zoff, 0, rowb, ctx->stream));
+            CK(cudaMemsetAsync(ctx->ws + ctx->L.A1 + zoff, 0, rowb, ctx->stream));
+        }
+        DevScalars init{};
+        init.best_key = ~0ull;
+        init.sol_step = -1;
+        init.sol_idx = -1;
+        init.info_best_unsat = -1;
+        init.info_best_idx = -1;
+        *ctx->h_scal = init;
+        CK(cudaMemcpyAsync(a.ds, ctx->h_scal, sizeof(DevScalars), cudaMemcpyHostToDevice, ctx->stream));
+        CK(launch_init(a.theta, a.m, a.v, a.V, a.N, ctx->n0, seed, ctx->stream));
+        s = state_stats(ctx, a, 0);
+        if (s != TSAT_OK) return s;
+        ctx->have_batch = true;
+        return TSAT_OK;
+    });
 }
 
 tsat_status tsat_step(tsat_ctx ctx, int32_t k, tsat_step_info* out) {
-    GUARD_CTX();
-    tsat_status s = check_batch(ctx, false);
-    if (s != TSAT_OK) return s;
-    if (k < 1) return fail(ctx, TSAT_E_ARG, "k < 1");
-    int done = 0;
-    while (done < k) {
-        int kk = std::min(k - done, kMaxStepsPerCall);
-        if (ctx->profiling) {                       // the previous call's kernel events
-            CK(cudaStreamSynchronize(ctx->stream));
-            s = collect_profile(ctx);
-            if (s != TSAT_OK) return s;
-        }
-        // the device table is rewritten in stream order (after the previous
-        // graph has used it); the host slot only once its last upload is done,
-        // so consecutive calls queue without draining the GPU
-        const int slot = ctx->tab_slot;
-        ctx->tab_slot ^= 1;
-        CK(cudaEventSynchronize(ctx->tab_ev[slot]));
-        StepScalars* tab = ctx->h_steptab + (size_t)slot * kMaxStepsPerCall;
-        for (int i = 0; i < kk; ++i) {
-            tab[i] = step_scalars(ctx->cfg, ctx->t + i);
-            tab[i].xgen = ctx->xgen + 1 + (unsigned)i;
-        }
-        CK(cudaMemcpyAsync(ctx->ws + ctx->L.steptab, tab, sizeof(StepScalars) * kk, cudaMemcpyHostToDevice,
-                           ctx->stream));
-        CK(cudaEventRecord(ctx->tab_ev[slot], ctx->stream));
-        s = launch_steps(ctx, kk);
+    return no_throw(ctx, [&]() -> tsat_status {
+        GUARD_CTX();
+        tsat_status s = check_batch(ctx, false);
         if (s != TSAT_OK) return s;
-        ctx->t += kk;
-        ctx->steps_done += kk;
-        ctx->xgen += (unsigned)kk;
-        done += kk;
-    }
-    if (out) return read_info(ctx, out);
-    return TSAT_OK;
+        if (k < 1) return fail(ctx, TSAT_E_ARG, "k < 1");
+        int done = 0;
+        while (done < k) {
+            int kk = std::min(k - done, kMaxStepsPerCall);
+            if (ctx->profiling) {                       // the previous call's kernel events
+                CK(cudaStreamSynchronize(ctx->stream));
+                s = collect_profile(ctx);
+                if (s != TSAT_OK) return s;
+            }
+            // the device table is rewritten in stream order (after the previous
+            // graph has used it); the host slot only once its last upload is done,
+            // so consecutive calls queue without draining the GPU
+            const int slot = ctx->tab_slot;
+            ctx->tab_slot ^= 1;
+            CK(cudaEventSynchronize(ctx->tab_ev[slot]));
+            StepScalars* tab = ctx->h_steptab + (size_t)slot * kMaxStepsPerCall;
+            for (int i = 0; i < kk; ++i) {
+                tab[i] = step_scalars(ctx->cfg, ctx->t + i);
+                tab[i].xgen = ctx->xgen + 1 + (unsigned)i;
+            }
+            CK(cudaMemcpyAsync(ctx->ws + ctx->L.steptab, tab, sizeof(StepScalars) * kk, cudaMemcpyHostToDevice,
+                               ctx->stream));
+            CK(cudaEventRecord(ctx->tab_ev[slot], ctx->stream));
+            s = launch_steps(ctx, kk);
+            if (s != TSAT_OK) return s;
+            ctx->t += kk;
+            ctx->steps_done += kk;
+            ctx->xgen += (unsigned)kk;
+            done += kk;
+        }
+        if (out) return read_info(ctx, out);
+        return TSAT_OK;
+    });
 }
 
 tsat_status tsat_get_info(tsat_ctx ctx, tsat_step_info* out) {
@@ -919,11 +982,12 @@ tsat_status tsat_get_info(tsat_ctx ctx, tsat_step_info* out) {
     return read_info(ctx, out);
 }
 
-tsat_status tsat_query_unsat_async(tsat_ctx ctx, int32_t* host_out, int64_t* first) {
+tsat_status tsat_query_unsat_async(tsat_ctx ctx, int32_t* host_out, size_t n, int64_t* first) {
     GUARD_CTX();
     tsat_status s = check_batch(ctx, true);
     if (s != TSAT_OK) return s;
     if (!host_out) return fail(ctx, TSAT_E_ARG, "null host_out");
+    if (n != (size_t)ctx->N) return fail(ctx, TSAT_E_ARG, "host_out must hold exactly N_local counts");
     CK(cudaMemcpyAsync(host_out, ctx->ws + ctx->L.unsat, (size_t)ctx->N * 4, cudaMemcpyDeviceToHost, ctx->stream));
     if (first) *first = ctx->n0;
     return TSAT_OK;
@@ -935,11 +999,12 @@ tsat_status tsat_sync(tsat_ctx ctx) {
     return collect_profile(ctx);
 }
 
-tsat_status tsat_query_unsat(tsat_ctx ctx, int32_t* host_out, int64_t* first) {
+tsat_status tsat_query_unsat(tsat_ctx ctx, int32_t* host_out, size_t n, int64_t* first) {
     GUARD_CTX();
     tsat_status s = check_batch(ctx, true);
     if (s != TSAT_OK) return s;
     if (!host_out) return fail(ctx, TSAT_E_ARG, "null host_out");
+    if (n != (size_t)ctx->N) return fail(ctx, TSAT_E_ARG, "host_out must hold exactly N_local counts");
     CK(cudaMemcpyAsync(host_out, ctx->ws + ctx->L.unsat, (size_t)ctx->N * 4, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (first) *first = ctx->n0;
@@ -947,46 +1012,52 @@ tsat_status tsat_query_unsat(tsat_ctx ctx, int32_t* host_out, int64_t* first) {
 }
 
 tsat_status tsat_export_model(tsat_ctx ctx, int64_t gidx, uint8_t* host_values) {
-    GUARD_CTX();
-    tsat_status s = check_batch(ctx, true);
-    if (s != TSAT_OK) return s;
-    if (!host_values) return fail(ctx, TSAT_E_ARG, "null host_values");
-    int64_t n = gidx - ctx->n0;
-    if (n < 0 || n >= ctx->N) return fail(ctx, TSAT_E_ARG, "candidate not on this rank");
-    const int V = ctx->cnf.V, NW = ctx->N / 32;
-    size_t Aoff = ((ctx->t - 1) & 1) ? ctx->L.A1 : ctx->L.A0;    // evaluated state theta_{t-1}
-    std::vector<uint32_t> words((size_t)V);
-    if (V > 0) {
-        CK(cudaMemcpy2DAsync(words.data(), 4, ctx->ws + Aoff + (size_t)(n / 32) * 4, (size_t)NW * 4, 4, (size_t)V,
-                             cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-    }
-    for (int v = 0; v < V; ++v) host_values[v] = (uint8_t)((words[v] >> (n & 31)) & 1u);
-    return TSAT_OK;
+    return no_throw(ctx, [&]() -> tsat_status {
+        GUARD_CTX();
+        tsat_status s = check_batch(ctx, true);
+        if (s != TSAT_OK) return s;
+        if (!host_values) return fail(ctx, TSAT_E_ARG, "null host_values");
+        int64_t n = gidx - ctx->n0;
+        if (n < 0 || n >= ctx->N) return fail(ctx, TSAT_E_ARG, "candidate not on this rank");
+        const int V = ctx->cnf.V, NW = ctx->N / 32;
+        size_t Aoff = ((ctx->t - 1) & 1) ? ctx->L.A1 : ctx->L.A0;    // evaluated state theta_{t-1}
+        std::vector<uint32_t> words((size_t)V);
+        if (V > 0) {
+            CK(cudaMemcpy2DAsync(words.data(), 4, ctx->ws + Aoff + (size_t)(n / 32) * 4, (size_t)NW * 4, 4, (size_t)V,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+        }
+        for (int v = 0; v < V; ++v) host_values[v] = (uint8_t)((words[v] >> (n & 31)) & 1u);
+        return TSAT_OK;
+    });
 }
 
 tsat_status tsat_get_solution(tsat_ctx ctx, uint8_t* host_values, int64_t* idx, int64_t* step) {
-    GUARD_CTX();
-    tsat_status s = check_batch(ctx, false);
-    if (s != TSAT_OK) return s;
-    s = read_info(ctx, nullptr);
-    if (s != TSAT_OK) return s;
-    const DevScalars& d = *ctx->h_scal;
-    if (d.sol_step < 0) return fail(ctx, TSAT_E_STATE, "no model found yet");
-    if (idx) *idx = d.sol_idx;
-    if (step) *step = d.sol_step;
-    const bool owner = d.sol_idx >= ctx->n0 && d.sol_idx < ctx->n0 + ctx->N;
-    if (host_values && ctx->cnf.V > 0 && owner) {
-        CK(cudaMemcpyAsync(host_values, ctx->ws + ctx->L.sol, (size_t)ctx->cnf.V, cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-    }
-    return TSAT_OK;
+    return no_throw(ctx, [&]() -> tsat_status {
+        GUARD_CTX();
+        tsat_status s = check_batch(ctx, false);
+        if (s != TSAT_OK) return s;
+        s = read_info(ctx, nullptr);
+        if (s != TSAT_OK) return s;
+        const DevScalars& d = *ctx->h_scal;
+        if (d.sol_step < 0) return fail(ctx, TSAT_E_STATE, "no model found yet");
+        if (idx) *idx = d.sol_idx;
+        if (step) *step = d.sol_step;
+        const bool owner = d.sol_idx >= ctx->n0 && d.sol_idx < ctx->n0 + ctx->N;
+        if (host_values && ctx->cnf.V > 0 && owner) {
+            CK(cudaMemcpyAsync(host_values, ctx->ws + ctx->L.sol, (size_t)ctx->cnf.V, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+        }
+        return TSAT_OK;
+    });
 }
 
-tsat_status tsat_get_state(tsat_ctx ctx, float* theta, float* m, float* v, int64_t* t) {
+tsat_status tsat_get_state(tsat_ctx ctx, float* theta, float* m, float* v, size_t elems, int64_t* t) {
     GUARD_CTX();
     tsat_status s = check_batch(ctx, false);
     if (s != TSAT_OK) return s;
+    if ((theta || m || v) && elems != (size_t)ctx->cnf.V * ctx->N)
+        return fail(ctx, TSAT_E_ARG, "state arrays must hold exactly V * N_local elements");
     size_t bytes = (size_t)ctx->cnf.V * ctx->N * 4;
     if (theta) CK(cudaMemcpyAsync(theta, ctx->ws + ctx->L.theta, bytes, cudaMemcpyDeviceToHost, ctx->stream));
     if (m) CK(cudaMemcpyAsync(m, ctx->ws + ctx->L.m, bytes, cudaMemcpyDeviceToHost, ctx->stream));
@@ -996,11 +1067,13 @@ tsat_status tsat_get_state(tsat_ctx ctx, float* theta, float* m, float* v, int64
     return TSAT_OK;
 }
 
-tsat_status tsat_set_state(tsat_ctx ctx, const float* theta, const float* m, const float* v, int64_t t) {
+tsat_status tsat_set_state(tsat_ctx ctx, const float* theta, const float* m, const float* v, size_t elems, int64_t t) {
     GUARD_CTX();
     tsat_status s = check_batch(ctx, false);
     if (s != TSAT_OK) return s;
     if (!theta || !m || !v || t < 0) return fail(ctx, TSAT_E_ARG, "null state or t < 0");
+    if (elems != (size_t)ctx->cnf.V * ctx->N)
+        return fail(ctx, TSAT_E_ARG, "state arrays must hold exactly V * N_local elements (same world size and N)");
     size_t bytes = (size_t)ctx->cnf.V * ctx->N * 4;
     StepArgs a = step_args(ctx);
     CK(cudaMemcpyAsync(a.theta, theta, bytes, cudaMemcpyHostToDevice, ctx->stream));
@@ -1023,10 +1096,12 @@ tsat_status tsat_set_state(tsat_ctx ctx, const float* theta, const float* m, con
     return TSAT_OK;
 }
 
-tsat_status tsat_get_rows(tsat_ctx ctx, const int32_t* rows, int32_t nrows, float* theta, float* m, float* v) {
+tsat_status tsat_get_rows(tsat_ctx ctx, const int32_t* rows, int32_t nrows, float* theta, float* m, float* v,
+                          size_t row_elems) {
     GUARD_CTX();
     tsat_status s = check_batch(ctx, false);
     if (s != TSAT_OK) return s;
+    if (row_elems != (size_t)ctx->N) return fail(ctx, TSAT_E_ARG, "row_elems must equal N_local");
     if (nrows < 0 || (nrows > 0 && !rows)) return fail(ctx, TSAT_E_ARG, "bad rows");
     const size_t rb = (size_t)ctx->N * 4;
     for (int32_t i = 0; i < nrows; ++i) {
@@ -1062,64 +1137,137 @@ tsat_status tsat_debug_copy(tsat_ctx ctx, int32_t which, void* dst, size_t bytes
 }
 
 tsat_status tsat_export_best(tsat_ctx ctx, int32_t M, int32_t k, tsat_partial* out) {
-    GUARD_CTX();
-    tsat_status s = check_batch(ctx, true);
-    if (s != TSAT_OK) return s;
-    const int V = ctx->cnf.V, N = ctx->N;
-    if (M < 1 || M > N || !out) return fail(ctx, TSAT_E_ARG, "need 1 <= M <= N_local and host_out");
-    if (k <= 0) k = (int32_t)std::min<int64_t>(V, std::max<int64_t>((V + 9999) / 10000, 20));
-    if (k > V) k = V;
-    if (k > kTopkMax) return fail(ctx, TSAT_E_RANGE, "k > 2048 not supported");
-    if (k < 1) return fail(ctx, TSAT_E_ARG, "V = 0");
-    StepArgs a = step_args(ctx);
-    int n64 = 1;
-    while (n64 < N) n64 <<= 1;
-    unsigned long long* keys = nullptr;
-    int *cols = nullptr, *ov = nullptr;
-    double *absG = nullptr, *og = nullptr;
-    auto cleanup = [&]() { cudaFree(keys); cudaFree(cols); cudaFree(ov); cudaFree(absG); cudaFree(og); };
-    cudaError_t e;
-    if ((e = cudaMalloc(&keys, (size_t)n64 * 8)) != cudaSuccess ||
-        (e = cudaMalloc(&cols, (size_t)M * 4)) != cudaSuccess ||
-        (e = cudaMalloc(&ov, (size_t)M * k * 4)) != cudaSuccess ||
-        (e = cudaMalloc(&og, (size_t)M * k * 8)) != cudaSuccess ||
-        (e = cudaMalloc(&absG, (size_t)M * V * 8)) != cudaSuccess) {
-        cleanup();
-        cudaGetLastError();
-        return fail(ctx, TSAT_E_OOM, "export scratch allocation failed");
-    }
-    long long t_eval = ctx->t - 1;
-    e = launch_export(a, t_eval, nullptr, M, k, nullptr, keys, n64, nullptr, nullptr, ctx->stream, 0);
-    std::vector<unsigned long long> hk((size_t)M);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hk.data(), keys, (size_t)M * 8, cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    std::vector<int> hc((size_t)M);
-    for (int i = 0; i < M; ++i) hc[i] = (int)((long long)(hk[i] & 0xffffffffull) - ctx->n0);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(cols, hc.data(), (size_t)M * 4, cudaMemcpyHostToDevice, ctx->stream);
-    if (e == cudaSuccess) e = launch_export(a, t_eval, cols, M, k, absG, keys, n64, ov, og, ctx->stream, 1);
-    std::vector<int> hv((size_t)M * k);
-    std::vector<double> hg((size_t)M * k);
-    std::vector<uint32_t> bits((size_t)V * (N / 32));
-    size_t Aoff = (t_eval & 1) ? ctx->L.A1 : ctx->L.A0;
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hv.data(), ov, hv.size() * 4, cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hg.data(), og, hg.size() * 8, cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(bits.data(), ctx->ws + Aoff, bits.size() * 4, cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    cleanup();
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "export");
-    const int NW = N / 32;
-    for (int i = 0; i < M; ++i) {
-        int n = hc[i];
-        out[i].candidate = (int64_t)(hk[i] & 0xffffffffull);
-        out[i].unsat = (int32_t)(hk[i] >> 32);
-        out[i].k = k;
-        for (int j = 0; j < k; ++j) {
-            int v = hv[(size_t)i * k + j];
-            int b = (int)((bits[(size_t)v * NW + n / 32] >> (n & 31)) & 1u);
-            if (out[i].lits) out[i].lits[j] = b ? (v + 1) : -(v + 1);
-            if (out[i].abs_grad) out[i].abs_grad[j] = (float)hg[(size_t)i * k + j];
+    return no_throw(ctx, [&]() -> tsat_status {
+        GUARD_CTX();
+        tsat_status s = check_batch(ctx, true);
+        if (s != TSAT_OK) return s;
+        const int V = ctx->cnf.V, N = ctx->N, W = ctx->world;
+        if (M < 1 || (int64_t)M > ctx->N_global || !out) return fail(ctx, TSAT_E_ARG, "need 1 <= M <= N_global and host_out");
+        if (k <= 0) k = (int32_t)std::min<int64_t>(V, std::max<int64_t>((V + 9999) / 10000, 20));
+        if (k > V) k = V;
+        if (k > kTopkMax) return fail(ctx, TSAT_E_RANGE, "k > 2048 not supported");
+        if (k < 1) return fail(ctx, TSAT_E_ARG, "V = 0");
+        if (W > 1 && ((int64_t)M > kExportCap || (int64_t)M * k > kExportCap))
+            return fail(ctx, TSAT_E_RANGE, "multi-GPU export: M and M * k must be <= 65536");
+        StepArgs a = step_args(ctx);
+        const long long t_eval = ctx->t - 1;
+        int n64 = 1;
+        while (n64 < std::max(N, M)) n64 <<= 1;
+        // device scratch (freed on every path)
+        unsigned long long *keys = nullptr, *gk = nullptr, *ent = nullptr, *gent = nullptr;
+        int *cols = nullptr, *pos = nullptr, *ov = nullptr;
+        double *absG = nullptr, *og = nullptr;
+        struct Free {
+            std::vector<void*> p;
+            ~Free() { for (void* x : p) cudaFree(x); }
+        } fr;
+        auto dalloc = [&](void** dst, size_t bytes) -> bool {
+            if (cudaMalloc(dst, std::max<size_t>(bytes, 8)) != cudaSuccess) { cudaGetLastError(); return false; }
+            fr.p.push_back(*dst);
+            return true;
+        };
+        const size_t Mk = (size_t)M * k;
+        if (!dalloc((void**)&keys, (size_t)n64 * 8) || !dalloc((void**)&gk, (size_t)W * M * 8) ||
+            !dalloc((void**)&ent, Mk * 8) || !dalloc((void**)&gent, (size_t)W * Mk * 8) ||
+            !dalloc((void**)&cols, (size_t)M * 4) || !dalloc((void**)&pos, (size_t)M * 4) ||
+            !dalloc((void**)&ov, Mk * 4) || !dalloc((void**)&og, Mk * 8) || !dalloc((void**)&absG, (size_t)M * V * 8))
+            return fail(ctx, TSAT_E_OOM, "export scratch allocation failed");
+        // (1) local ranking by (unsat, global index): keys padded with ~0 beyond N_local
+        CK(launch_export(a, t_eval, nullptr, M, k, nullptr, keys, n64, nullptr, nullptr, ctx->stream, 0));
+        // (2) all ranks' first M keys -> every rank (exact integers: identical merge everywhere)
+        std::vector<unsigned long long> hk((size_t)W * M);
+        auto gather = [&](int phase, const unsigned long long* send, size_t n, unsigned long long* recv) -> tsat_status {
+            if (W == 1) return TSAT_OK;
+            if (ctx->peer) {
+                CK(launch_peer_allgather(a, phase, send, (int)n, recv, ++ctx->xgen, ctx->stream));
+            } else {
+                std::string err;
+                if (comm_allgather_u64(ctx->comm, send, recv, n, ctx->stream, &err)) {
+                    ctx->poisoned = TSAT_E_NCCL;
+                    return fail(ctx, TSAT_E_NCCL, err);
+                }
+            }
+            return TSAT_OK;
+        };
+        s = gather(0, keys, (size_t)M, gk);
+        if (s != TSAT_OK) return s;
+        CK(cudaMemcpyAsync(hk.data(), W == 1 ? keys : gk, hk.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->peer) {
+            CK(cudaMemcpyAsync(ctx->h_scal, ctx->ws + ctx->L.scal, sizeof(DevScalars), cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            if (ctx->h_scal->xerr) { ctx->poisoned = TSAT_E_NCCL; return fail(ctx, TSAT_E_NCCL, "peer export exchange timed out"); }
         }
-    }
+        // (3) global top-M: the M smallest keys, ascending (each key is unique: it holds the index)
+        {
+            std::vector<unsigned long long> sel((size_t)M);
+            tsat_merge_keys(reinterpret_cast<const uint64_t*>(hk.data()), hk.size(), M,
+                            reinterpret_cast<uint64_t*>(sel.data()));
+            hk.swap(sel);
+        }
+        if (hk.back() == ~0ull) return fail(ctx, TSAT_E_STATE, "fewer than M evaluated candidates");
+        // (4) the columns this rank owns: k smallest |G| per column (R14, ties -> lower v) + bits
+        std::vector<int> hc, hp;
+        for (int i = 0; i < M; ++i) {
+            const long long g = (long long)(hk[i] & 0xffffffffull);
+            if (g >= ctx->n0 && g < ctx->n0 + N) { hc.push_back((int)(g - ctx->n0)); hp.push_back(i); }
+        }
+        const int Mo = (int)hc.size();
+        CK(cudaMemsetAsync(ent, 0, Mk * 8, ctx->stream));
+        if (Mo > 0) {
+            CK(cudaMemcpyAsync(cols, hc.data(), (size_t)Mo * 4, cudaMemcpyHostToDevice, ctx->stream));
+            CK(cudaMemcpyAsync(pos, hp.data(), (size_t)Mo * 4, cudaMemcpyHostToDevice, ctx->stream));
+            CK(launch_export(a, t_eval, cols, Mo, k, absG, keys, n64, ov, og, ctx->stream, 1));
+            CK(launch_export_pack(a, t_eval, cols, pos, Mo, k, ov, og, ent, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));   // hc / hp stay alive until the copies are done
+        }
+        // (5) every rank receives every selected column's entries (each position has one owner)
+        s = gather(1, ent, Mk, gent);
+        if (s != TSAT_OK) return s;
+        std::vector<unsigned long long> he((size_t)W * Mk);
+        CK(cudaMemcpyAsync(he.data(), W == 1 ? ent : gent, he.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->peer) {
+            CK(cudaMemcpyAsync(ctx->h_scal, ctx->ws + ctx->L.scal, sizeof(DevScalars), cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            if (ctx->h_scal->xerr) { ctx->poisoned = TSAT_E_NCCL; return fail(ctx, TSAT_E_NCCL, "peer export exchange timed out"); }
+        }
+        const long long Nl = N;
+        for (int i = 0; i < M; ++i) {
+            const long long g = (long long)(hk[i] & 0xffffffffull);
+            const int owner = (int)(g / Nl);
+            const unsigned long long* e = he.data() + (size_t)owner * Mk + (size_t)i * k;
+            out[i].candidate = g;
+            out[i].unsat = (int32_t)(hk[i] >> 32);
+            out[i].k = k;
+            for (int j = 0; j < k; ++j) {
+                const uint32_t lo = (uint32_t)(e[j] & 0xffffffffull);
+                const int v = (int)(lo >> 1);
+                if (out[i].lits) out[i].lits[j] = (lo & 1u) ? (v + 1) : -(v + 1);
+                if (out[i].abs_grad) out[i].abs_grad[j] = __uint_as_float_host((uint32_t)(e[j] >> 32));
+            }
+        }
+        return TSAT_OK;
+    });
+}
+
+tsat_status tsat_merge_keys(const uint64_t* keys, size_t n, int32_t M, uint64_t* out) {
+    if (M < 0 || (M > 0 && (!keys || !out)) || (size_t)M > n) return TSAT_E_ARG;
+    return no_throw(nullptr, [&]() -> tsat_status {
+        std::vector<uint64_t> v(keys, keys + n);
+        std::partial_sort(v.begin(), v.begin() + M, v.end());
+        std::copy(v.begin(), v.begin() + M, out);
+        return TSAT_OK;
+    });
+}
+
+tsat_status tsat_export_k(tsat_ctx ctx, int32_t k_req, int32_t* k_out) {
+    GUARD_CTX();
+    if (!k_out) return fail(ctx, TSAT_E_ARG, "null k_out");
+    if (!ctx->have_cnf) return fail(ctx, TSAT_E_STATE, "no CNF loaded");
+    const int64_t V = ctx->cnf.V;
+    int64_t k = k_req > 0 ? k_req : std::max<int64_t>((V + 9999) / 10000, 20);
+    *k_out = (int32_t)std::min<int64_t>(k, V);
     return TSAT_OK;
 }
 
@@ -1164,7 +1312,7 @@ const char* tsat_error_string(tsat_ctx ctx) {
 
 void tsat_destroy(tsat_ctx ctx) {
     if (!ctx) return;
-    cudaSetDevice(ctx->device);
+    DevGuard dev_guard_(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     drop_graphs(ctx);
     for (auto e : ctx->events) cudaEventDestroy(e);

@@ -181,9 +181,16 @@ static void build_batched(HostCnf* hp) {
     h.bat_ptr[V] = (uint32_t)h.bat_rec.size();
 }
 
+// bat_rec offsets are stored as uint32 (bat_ptr, hub super-chunks)
+static bool batched_fits(const HostCnf& h) { return h.bat_rec.size() < ((size_t)1 << 31); }
+
 int build_cnf(int32_t V, int64_t C, const int64_t* ptr, const int32_t* lits, HostCnf* out, std::string* msg) {
     if (V < 0 || C < 0 || (C > 0 && (!ptr || (!lits && ptr[C] > 0)))) { *msg = "bad CNF arrays"; return 1; }
     if (V >= (1 << 29)) { *msg = "V too large (>= 2^29)"; return 3; }
+    if (C > 0 && ptr[0] != 0) { *msg = "clause_ptr[0] must be 0"; return 1; }
+    for (int64_t c = 0; c < C; ++c)
+        if (ptr[c + 1] < ptr[c]) { *msg = "clause_ptr not monotone"; return 1; }
+    if (C > 0 && ptr[C] >= ((int64_t)1 << 32)) { *msg = "too many literals (>= 2^32)"; return 3; }
     HostCnf h;
     h.V = V;
     h.C = C;
@@ -279,7 +286,10 @@ int build_cnf(int32_t V, int64_t C, const int64_t* ptr, const int32_t* lits, Hos
     // k_update stages uniform 3-SAT rows as plain records, every other
     // instance as batched records (build_batched)
     h.batched = !(h.uniform_len && h.K == 3);
-    if (h.batched) build_batched(&h);
+    if (h.batched) {
+        build_batched(&h);
+        if (!batched_fits(h)) { *msg = "batched occurrence records too large (>= 2^31 words)"; return 3; }
+    }
     const std::vector<uint32_t>& sptr = h.batched ? h.bat_ptr : h.occ_ptr;
     h.hub_of.assign((size_t)V, -1);
     for (int32_t v = 0; v < V; ++v) {

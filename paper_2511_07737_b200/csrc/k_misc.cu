@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(256) k_gtable(int* __restrict__ hist, int N, l
     const int lane = threadIdx.x & 31;
     unsigned long long key = ~0ull;
     double gm = 0.0;
-    long long lfx = 0;               // sharded loss: S_n 2^40, exact int64 sum across ranks
+    long long lfx = 0;               // sharded loss: S_n 2^e, exact int64 sum across ranks (mc.loss_scale)
     if (n < N) {
         long long h[KB];
         long long acc = 0;
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(256) k_gtable(int* __restrict__ hist, int N, l
 #pragma unroll
         for (int r = 0; r < KB; ++r) gtab[(size_t)r * N + n] = g[r];
         S[n] = s;
-        lfx = __double2ll_rn(s * 1099511627776.0);
+        lfx = __double2ll_rn(s * mc.loss_scale);
         unsat[n] = (int)h[0];
         key = ((unsigned long long)h[0] << 32) | (unsigned long long)(mc.n0 + n);
     }
@@ -366,6 +366,21 @@ __global__ void __launch_bounds__(1024) k_topk_cols(const double* __restrict__ a
     }
 }
 
+// Export entries of the owned selected columns: entry (pos[i], j) of the
+// M x k table = (|G| fp32 bits << 32) | (v << 1) | b_vn, with b_vn read from
+// the evaluated state's bit plane (only the M columns' bits leave the GPU).
+__global__ void k_export_pack(const uint32_t* __restrict__ Aeval, int NW, const int* __restrict__ cols,
+                              const int* __restrict__ pos, int Mo, int k, const int* __restrict__ out_v,
+                              const double* __restrict__ out_g, unsigned long long* __restrict__ entries) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)Mo * k) return;
+    const int mi = (int)(i / k), j = (int)(i % k);
+    const int n = cols[mi], v = out_v[i];
+    const uint32_t b = (Aeval[(size_t)v * NW + (n >> 5)] >> (n & 31)) & 1u;
+    const float g = (float)out_g[i];                     // |G| is an fp32 value (R27): exact
+    entries[(size_t)pos[mi] * k + j] = ((unsigned long long)__float_as_uint(g) << 32) | ((unsigned long long)v << 1) | b;
+}
+
 // ------------------------------------------------------------------ launchers
 cudaError_t launch_init(float* theta, float* m, float* v, int V, int N, long long n0, unsigned long long seed,
                         cudaStream_t st) {
@@ -390,6 +405,17 @@ cudaError_t launch_gtable(const StepArgs& a, const StepScalars* sc, cudaStream_t
                                 a.unsat, a.ds, a.sharded, a.lossp, sc, a.peer, a.px);
     return launch_maybe_pdl(a.pdl, k_gtable<8>, dim3(blocks), dim3(256), 0, st, a.hist, a.N, a.C, a.mc, a.gtab, a.S,
                             a.unsat, a.ds, a.sharded, a.lossp, sc, a.peer, a.px);
+}
+
+cudaError_t launch_export_pack(const StepArgs& a, long long t_eval, const int* cols_dev, const int* pos_dev, int Mo,
+                               int k, const int* out_v, const double* out_g, unsigned long long* entries,
+                               cudaStream_t st) {
+    const uint32_t* Aeval = (t_eval & 1) ? a.A1 : a.A0;
+    const long long total = (long long)Mo * k;
+    if (total > 0)
+        k_export_pack<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(Aeval, a.N >> 5, cols_dev, pos_dev, Mo, k, out_v,
+                                                                       out_g, entries);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_export(const StepArgs& a, long long t_eval, const int* cols_dev, int M, int k, double* absG,

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(256) k_rows_partial(StepArgs a, const float* _
 // the new state (one warp per row); the global loss from slot V.
 __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a, uint32_t* __restrict__ Anext) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (warp == 0 && lane == 0) a.ds->loss = -((double)a.Qbuf[a.V] * 9.094947017729282e-13);   // * 2^-40
+    if (warp == 0 && lane == 0) a.ds->loss = -((double)a.Qbuf[a.V] * a.mc.loss_unscale);   // * 2^-e
     if (warp >= a.V) return;
     const int v = warp, NW = a.N >> 5;
     double dn = 0.0;
@@ -242,6 +242,52 @@ cudaError_t launch_rows_finish(const StepArgs& a, uint32_t* Anext, cudaStream_t 
 }
 cudaError_t launch_step_end_sharded(const StepArgs& a, const StepScalars* sc, cudaStream_t st) {
     k_step_end_sharded<<<1, 1, 0, st>>>(a.ds, sc);
+    return cudaGetLastError();
+}
+
+// Export all-gather over peer memory (tsat_export_best): every rank stores its
+// n words into its slot of every rank's phase region, then publishes the slot
+// with a release store of the generation; after acquiring the W flags the CTA
+// copies the W slots (rank order) to recv.  Phases 0 (keys) and 1 (entries)
+// use separate regions: a rank writes phase p of call c + 1 only after every
+// rank has sent data that it produces after reading phase p of call c.
+__global__ void __launch_bounds__(256) k_peer_allgather(PeerArgs px, int phase, const unsigned long long* __restrict__ send,
+                                                        int n, unsigned long long* __restrict__ recv, unsigned gen,
+                                                        DevScalars* ds) {
+    __shared__ int ok;
+    const size_t slot_words = (size_t)kExportCap;
+    auto region = [&](int p) {
+        return reinterpret_cast<unsigned long long*>(px.xb[p] + px.L.ex) + (size_t)phase * px.W * slot_words;
+    };
+    for (int p = 0; p < px.W; ++p) {
+        if (p == px.rank) continue;
+        unsigned long long* d = region(p) + (size_t)px.rank * slot_words;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) st_relaxed_sys_u64(d + i, send[i]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int p = 0; p < px.W; ++p)
+            if (p != px.rank)
+                st_release_sys(reinterpret_cast<unsigned*>(px.xb[p] + px.L.ef) + (size_t)phase * px.W + px.rank, gen);
+        int good = 1;
+        const unsigned* fs = reinterpret_cast<const unsigned*>(px.xb[px.rank] + px.L.ef) + (size_t)phase * px.W;
+        for (int r = 0; r < px.W && good; ++r)
+            if (r != px.rank && !peer_wait(fs + r, gen, ds)) good = 0;
+        ok = good;
+    }
+    __syncthreads();
+    if (!ok) return;
+    for (int r = 0; r < px.W; ++r) {
+        const unsigned long long* s = r == px.rank ? send : region(px.rank) + (size_t)r * slot_words;
+        for (int i = threadIdx.x; i < n; i += blockDim.x)
+            recv[(size_t)r * n + i] = r == px.rank ? s[i] : ld_relaxed_sys_u64(s + i);
+    }
+}
+
+cudaError_t launch_peer_allgather(const StepArgs& a, int phase, const unsigned long long* send, int n,
+                                  unsigned long long* recv, unsigned gen, cudaStream_t st) {
+    k_peer_allgather<<<1, 256, 0, st>>>(a.px, phase, send, n, recv, gen, a.ds);
     return cudaGetLastError();
 }
 

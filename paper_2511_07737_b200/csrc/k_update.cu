@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
             const int bu = (int)(pscal[0] >> 32);
             const long long bi = (long long)(pscal[0] & 0xffffffffull);
             if (bu == 0 && a.ds->sol_step < 0) { a.ds->sol_step = t; a.ds->sol_idx = bi; }
-            const double loss = -((double)(long long)x[3] * 9.094947017729282e-13);     // * 2^-40
+            const double loss = -((double)(long long)x[3] * a.mc.loss_unscale);     // * 2^-e
             a.ds->loss = loss;
             a.ds->info_t = t + 1;
             a.ds->info_best_unsat = bu;

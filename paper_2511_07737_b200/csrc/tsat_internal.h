@@ -19,17 +19,19 @@ constexpr int kRecCap = 512;           // occurrence-record words a warp group s
 constexpr int kHubSlab = 1023;         // occurrences per hub super-chunk (11-bit signed counters)
 constexpr int kHubSlabBatches = 127;   // batched records: batches (<= 4 occurrences) per hub super-chunk (k_hub int10)
 constexpr int kMaxPeers = 8;           // peer-exchange path: ranks (GPUs of one NVSwitch node)
+constexpr int kExportCap = 1 << 16;    // export exchange: u64 words per rank and phase (M and M * k)
 
 // Peer-exchange buffer of one rank (cudaMalloc'd, CUDA-IPC shared).
 // Every rank writes its slot [src = its rank] of every rank's buffer:
-//   S: [2][W] x {~best key, gmax bits, thmax bits, loss S 2^40} + flags [2][W]
+//   S: [2][W] x {~best key, gmax bits, thmax bits, loss S 2^e} + flags [2][W]
 //      (once per step, double-buffered by generation parity)
 //   J, Q: [W][V] int64 row partials, each as two self-validating u64 words
 //         (generation << 32 | 32-bit half)                                   (per row, per step)
 // The generation is monotone per context and identical on every rank (the
 // ranks run the same call sequence).
+//   E: export all-gathers (tsat_export_best): flags [2][W] + [2 phases][W][kExportCap] u64
 struct PeerLayout {
-    size_t sx, sf, jx, qx, total;
+    size_t sx, sf, jx, qx, ef, ex, total;
 };
 inline PeerLayout peer_layout(int V, int W) {
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -39,6 +41,8 @@ inline PeerLayout peer_layout(int V, int W) {
     L.sf = o; o = al(o + (size_t)2 * W * 4);
     L.jx = o; o = al(o + (size_t)W * V * 16);
     L.qx = o; o = al(o + (size_t)W * V * 16);
+    L.ef = o; o = al(o + (size_t)2 * W * 4);
+    L.ex = o; o = al(o + (size_t)2 * W * kExportCap * 8);
     L.total = o;
     return L;
 }
@@ -123,7 +127,7 @@ struct DevScalars {
     int pad1;
     long long info_best_idx;
     double info_loss;
-    long long loss_fx;               // sharded: this rank's sum of S_n * 2^40 (exact int64)
+    long long loss_fx;               // sharded: this rank's sum of round(S_n 2^e) (exact int64, MethodConsts)
     unsigned int gt_done;            // k_gtable blocks finished (last block does the step bookkeeping)
     unsigned int xerr;               // peer path: an exchange timed out (step result invalid)
 };
@@ -139,6 +143,8 @@ struct MethodConsts {
     long long n0;       // first global candidate index of this rank
     unsigned long long seed;
     int noise;          // noise_sigma != 0
+    double loss_scale;    // sharded / peer / chunked loss: sum_n round(S_n 2^e) in int64, 2^e with
+    double loss_unscale;  // e = min(40, 61 - ceil(log2(N_global K))) so the sum cannot overflow; 2^-e
 };
 
 // Pointers and sizes one iteration's kernels need (built by capi.cu).
@@ -246,5 +252,12 @@ int comm_async_error(void* comm, std::string* err);
 
 cudaError_t launch_export(const StepArgs& a, long long t_eval, const int* cols_dev, int M, int k, double* absG,
                           unsigned long long* keys, int n64, int* out_v, double* out_g, cudaStream_t st, int phase);
+// export entries of the selected owned columns: (|G| fp32 bits << 32) | (v << 1) | b_vn (evaluated state)
+cudaError_t launch_export_pack(const StepArgs& a, long long t_eval, const int* cols_dev, const int* pos_dev, int Mo,
+                               int k, const int* out_v, const double* out_g, unsigned long long* entries,
+                               cudaStream_t st);
+// peer path: all-gather of n u64 words per rank (phase 0 / 1 regions of PeerLayout E)
+cudaError_t launch_peer_allgather(const StepArgs& a, int phase, const unsigned long long* send, int n,
+                                  unsigned long long* recv, unsigned gen, cudaStream_t st);
 
 }  // namespace tsat

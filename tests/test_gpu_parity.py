@@ -513,3 +513,77 @@ def test_hub_rows_parity_and_export():
         lits, mags = O.export_partial(np.abs(ref.G[:, n]), ref.bits[:, n], k)
         np.testing.assert_array_equal(gi["lits"], lits)
         np.testing.assert_array_equal(gi["abs_grad"], mags.astype(np.float32))
+
+
+# ---------------------------------------------------------------- boundary (round 2)
+def test_load_dimacs_equals_load_clauses():
+    """tsat_load_dimacs on a context (SPEC S:41-49 parsing, dedup) gives the
+    same CNF as tsat_load_clauses: identical steps, bit for bit, also against
+    the oracle; the info block reports the parse (tautology, duplicates)."""
+    from paper_2511_07737_b200 import Solver
+    from tsat_synth import to_dimacs
+    base = industrial_cnf(400, 1500, 12)
+    cls = base.clauses() + [[3, -3, 5], [7, 7, -9]]
+    cnf = Cnf.from_clauses(base.V, cls)
+    text = b"c round-2 boundary test\n" + to_dimacs(cnf)
+    a, b = Solver(0), Solver(0)
+    ia = a.load_dimacs(text)
+    ib = b.load_cnf(cnf)
+    assert (ia.V, ia.C, ia.nnz, ia.K) == (ib.V, ib.C, ib.nnz, ib.K)
+    assert ia.n_tautologies == ib.n_tautologies >= 1 and ia.n_duplicates == ib.n_duplicates == 1
+    assert ia.header_C == cnf.C and ib.header_C == -1
+    N = 96
+    a.init_batch(N, 4)
+    b.init_batch(N, 4)
+    o = O.Oracle(cnf, N, 4)
+    a.set_state(o.theta, o.m, o.v, 0)
+    b.set_state(o.theta, o.m, o.v, 0)
+    for _ in range(4):
+        ia_, ib_ = a.step(1), b.step(1)
+        ref = o.step()
+        np.testing.assert_array_equal(a.query_unsat(), ref.unsat)
+        np.testing.assert_array_equal(b.query_unsat(), ref.unsat)
+        assert (ia_.best_unsat, ia_.best_idx) == (ib_.best_unsat, ib_.best_idx) == (ref.best_unsat, ref.best_idx)
+    np.testing.assert_array_equal(a.get_state()[0], o.theta)
+    np.testing.assert_array_equal(b.get_state()[0], o.theta)
+
+
+def test_abi_size_checks():
+    """host arrays of the wrong size are rejected (TSAT_E_ARG), not
+    read out of bounds; a checkpoint of another batch size cannot be loaded."""
+    from paper_2511_07737_b200 import TsatError
+    from paper_2511_07737_b200.binding import _ptr
+    import ctypes as ct
+    cnf = planted_ksat(50, 210, 3, 2)
+    s, o = make_pair(cnf, 64, 1)
+    s.step(1)
+    with pytest.raises(ValueError):
+        s.set_state(o.theta[:, :32], o.m[:, :32], o.v[:, :32], 0)
+    small = np.zeros(10, np.int32)
+    first = ct.c_int64()
+    assert s.lib.tsat_query_unsat(s.h, _ptr(small), small.size, ct.byref(first)) == 1
+    th = np.zeros((50, 32), np.float32)
+    assert s.lib.tsat_set_state(s.h, _ptr(th), _ptr(th), _ptr(th), th.size, 0) == 1
+    assert s.lib.tsat_get_state(s.h, _ptr(th), None, None, th.size, None) == 1
+    with pytest.raises(TsatError):
+        s.export_best(64 + 1, 0)               # M > N_global
+
+
+def test_export_sharded_path_matches_oracle():
+    """The candidate-sharded (NCCL) path's export on a 1-rank communicator:
+    the all-gather + library merge give the oracle's selection and literals."""
+    cnf = planted_ksat(300, 1260, 3, 15)
+    N = 128
+    s, o = make_pair(cnf, N, 5, sharded=True)
+    s.set_state(o.theta, o.m, o.v, 0)
+    for _ in range(5):
+        s.step(1)
+        ref = o.step()
+    got = s.export_best(4, 0)
+    idx, u = O.select_top(ref.unsat, 4)
+    k = O.compute_k(cnf.V)
+    for gi, n, un in zip(got, idx, u):
+        assert (gi["candidate"], gi["unsat"]) == (n, un)
+        lits, mags = O.export_partial(np.abs(ref.G[:, n]), ref.bits[:, n], k)
+        np.testing.assert_array_equal(gi["lits"], lits)
+        np.testing.assert_array_equal(gi["abs_grad"], mags.astype(np.float32))

@@ -198,3 +198,45 @@ def test_peer_two_processes_ipc(tmp_path):
     for r in range(2):
         bu, bi, t = np.load(tmp_path / f"info{r}.npy")
         assert (bu, bi, t) == (ref.best_unsat, ref.best_idx, 9)
+
+
+def test_peer_export_is_global(monkeypatch):
+    """tsat_export_best over W = 2 peer contexts is one collective: both ranks
+    return the same M best candidates of the WHOLE batch, with the
+    oracle's k most confident literals, although each rank holds
+    only half of the candidates and only the owner reads a candidate's bits."""
+    import torch
+    monkeypatch.setenv("TSAT_UPD_GRID", "70")
+    cnf = planted_ksat(400, 1680, 3, 21)
+    N, W, seed, M = 256, 2, 13, 7
+    streams = [torch.cuda.Stream(0) for _ in range(W)]
+    ss = [_peer_solver(r, W, stream=streams[r]) for r in range(W)]
+    for s in ss:
+        s.load_cnf(cnf)
+    hs = [s.peer_handle() for s in ss]
+    for s in ss:
+        s.peer_open(hs)
+    _run_threads([lambda s=s: s.init_batch(N, seed) for s in ss])
+    _run_threads([lambda s=s: s.step(5) for s in ss])
+    o = O.Oracle(cnf, N, seed)
+    for _ in range(5):
+        ref = o.step()
+    outs = [None] * W
+
+    def ex(r):
+        outs[r] = ss[r].export_best(M, 0)
+    _run_threads([lambda r=r: ex(r) for r in range(W)])
+    idx, u = O.select_top(ref.unsat, M)
+    k = O.compute_k(cnf.V)
+    owners = set()
+    for r in range(W):
+        assert len(outs[r]) == M
+        for gi, n, un in zip(outs[r], idx, u):
+            assert (gi["candidate"], gi["unsat"]) == (n, un)
+            lits, mags = O.export_partial(np.abs(ref.G[:, n]), ref.bits[:, n], k)
+            np.testing.assert_array_equal(gi["lits"], lits)
+            np.testing.assert_array_equal(gi["abs_grad"], mags.astype(np.float32))
+            owners.add(int(n) // (N // W))
+    assert owners == {0, 1}                 # the selection spans both ranks
+    for s in ss:
+        s.close()

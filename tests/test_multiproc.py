@@ -62,7 +62,7 @@ def _worker(rank, world, port, steps, q):
         sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
         from oracle import oracle as O
         from tsat_synth import industrial_cnf, planted_ksat
-        from paper_2511_07737_b200.binding import merge_partials
+        from paper_2511_07737_b200.binding import merge_keys
         out = {}
         for name, cnf, nz in (("planted", planted_ksat(80, 336, 3, 7), 1), ("industrial", industrial_cnf(150, 500, 5), 1),
                               ("planted-mag", planted_ksat(80, 336, 3, 7), 3)):
@@ -77,12 +77,16 @@ def _worker(rank, world, port, steps, q):
                 losses.append(s.loss)
                 best.append((s.best_unsat, s.best_idx))
             out[name] = dict(theta=o.theta, m=o.m, v=o.v, unsat=unsat, losses=losses, best=best)
-            # export merge: each rank's local top-3 by (unsat, index), merged globally
+            # export selection (tsat_export_best's host step): each rank's first
+            # 3 keys (unsat << 32 | global index) all-gathered, merged by the
+            # library's tsat_merge_keys
             idx, u = O.select_top(unsat[-1], 3, n0=rank * Nl)
-            local = [dict(candidate=int(i), unsat=int(x)) for i, x in zip(idx, u)]
-            allp = [None] * world
-            dist.all_gather_object(allp, local)
-            out[name]["merged"] = [(p["candidate"], p["unsat"]) for p in merge_partials(allp, 3)]
+            local = torch.tensor(((u.astype(np.int64) << 32) | idx).astype(np.int64))
+            allk = [torch.zeros_like(local) for _ in range(world)]
+            dist.all_gather(allk, local)
+            keys = torch.cat(allk).numpy().astype(np.uint64)
+            sel = merge_keys(keys, 3)
+            out[name]["merged"] = [(int(k & 0xffffffff), int(k >> 32)) for k in sel]
         # NCCL unique-id broadcast (host logic of Solver.distributed)
         obj = [bytes(range(128)) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
