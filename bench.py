@@ -11,10 +11,15 @@ N=4096 candidates), seeded synthetic input.  The state streamed every step
 (theta, m, v: 492 MB) is larger than L2, so no explicit flush is needed.
 
 Prints ONE JSON line (rank 0).  Under torchrun (N>1) the candidate batch is
-sharded over the ranks (N_global = N_config * world, weak scaling): each rank
-holds N_config candidates, the CNF is replicated, and per iteration the ranks
-exchange Eq. 5's exact integer row / Jacobian sums and three maxima over NCCL
-(DESIGN.md §9).  Timed on the device, max over ranks.
+sharded over the ranks, the CNF is replicated, and per iteration the ranks
+exchange Eq. 5's exact integer row / Jacobian sums and three maxima inside the
+kernels over NVLink peer memory (or NCCL with --nccl).  Timed
+on the device, max over ranks.  Scaling: c2 / c4 weak (N_config candidates
+per GPU: BASELINE quotes them "on 1 B200"); c3 / c5 strong (BASELINE's fixed
+global batch, 1024 / 65536 candidates split over the GPUs); --scaling
+overrides.  At N=1 the line also carries the c3 / c4 sub-results
+(configs_more), the time-to-SAT protocol on c2 (time_to_sat), trajectory
+quality, the e2e pass and the oracle's CPU baseline.
 """
 from __future__ import annotations
 
@@ -47,7 +52,129 @@ def parse():
     ap.add_argument("--nccl", action="store_true",
                     help="N>1: use the NCCL-exchange sharded path instead of the peer-exchange path (default)")
     ap.add_argument("--peer", action="store_true", help="W=1: run the peer-exchange kernels exchanging with themselves")
+    ap.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"],
+                    help="weak: N_config candidates per GPU; strong: N_config candidates in total (BASELINE's "
+                         "fixed global batch; auto = strong for c3 / c5, weak otherwise)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the c3 / c4 sub-results (N=1)")
+    ap.add_argument("--extra", default="c3,c4", help="configs timed as sub-results at N=1")
+    ap.add_argument("--no-tts", action="store_true", help="skip the time-to-SAT block (N=1)")
+    ap.add_argument("--tts-config", default="c2")
+    ap.add_argument("--tts-seeds", default="1,2,3,4,5")
+    ap.add_argument("--tts-max-steps", type=int, default=3600)
+    ap.add_argument("--tts-only", action="store_true", help="run only the time-to-SAT protocol and print it")
     return ap.parse_args()
+
+
+def strong_scaling(args):
+    return args.scaling == "strong" or (args.scaling == "auto" and args.config in ("c3", "c5"))
+
+
+def upd_algorithmic_bytes(cnf, N):
+    """SURVEY §8(d) bytes of k_update per launch: theta, m, v
+    read + write, sign planes write + read, occurrence records, the g table."""
+    V, K = cnf.V, cnf.K
+    occ_words = int(np.sum(np.diff(cnf.clause_ptr) ** 2))
+    return 24.0 * V * N + 2.0 * V * N / 8 + 4.0 * (occ_words + 2 * V + 1) + 8.0 * N * (K + 1)
+
+
+def step_algorithmic_bytes(cnf, N):
+    """SURVEY §8(d) per-step algorithmic bytes (whole step, one GPU)."""
+    V, C, K = cnf.V, cnf.C, cnf.K
+    b = 2 if K <= 3 else 3
+    return 24.0 * V * N + 2.0 * V * N / 8 + 2.0 * C * N * b / 8 + 4.0 * (C + V + 2 * cnf.nnz + 2)
+
+
+def time_config(name, local, stream, hbm, steps=30, warm=10):
+    """Sub-result for another config on this GPU (N=1): device-timed steps and
+    per-kernel CUDA-event times; k_update's fraction of the HBM roofline."""
+    import torch
+    from paper_2511_07737_b200 import Solver
+    from tsat_synth import make_config
+    cnf, cfg = make_config(name)
+    N = cfg["N"]
+    s = Solver(local, stream=stream)
+    s.load_cnf(cnf)
+    s.init_batch(N, cfg["seed"])
+    chunk = 10
+    for _ in range(warm // chunk):
+        s.step(chunk, wait=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps // chunk):
+        s.step(chunk, wait=False)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    s.set_profiling(True)
+    s.kernel_times()
+    for _ in range(steps // chunk):
+        s.step(chunk, wait=False)
+    torch.cuda.synchronize()
+    kms, ks = s.kernel_times()
+    s.close()
+    names = ["k_clause", "k_gtable", "k_hub", "k_update", "k_step_end"]
+    per = {n: float(kms[i] / ks) for i, n in enumerate(names)}
+    ub = upd_algorithmic_bytes(cnf, N)
+    sb = step_algorithmic_bytes(cnf, N)
+    return {"workload": workload_desc(name, cnf, N), "ms_per_step": ms, "value": cnf.C * N / (ms / 1e3),
+            "unit": "evals/s", "steps": steps, "kernel_ms": per,
+            "k_update": {"algorithmic_bytes": ub, "achieved_gbs": ub / (per["k_update"] / 1e3) / 1e9,
+                         "frac": ub / (per["k_update"] / 1e3) / 1e9 / hbm},
+            "step_algorithmic_bytes": sb, "step_frac": sb / (ms / 1e3) / 1e9 / hbm,
+            "traffic_note": "ncu DRAM bytes of these kernels: profiles/ (static, per round)"}
+
+
+def time_to_sat(name, seeds, max_steps, local, stream, chunk=30):
+    """BASELINE.json's time-to-SAT: run each seed until some candidate reaches
+    0 unsat (the library keeps its bits; verified on the host against the CNF)
+    or max_steps; median steps / seconds over seeds, solved count, for the
+    paper-exact reading (R3) and the f2 variants normalize-off and R28."""
+    import torch
+    from paper_2511_07737_b200 import Solver, config_default
+    from tsat_synth import make_config
+    _, cfg = make_config(name)
+    N = cfg["N"]
+    out = {"config": name, "N": N, "max_steps": max_steps, "seeds": seeds,
+           "protocol": "run until a candidate has 0 unsat (model verified on the host) or max_steps; "
+                       "instance seed = init seed = s"}
+    for label, norm in (("paper_exact_R3", 1), ("normalize_off", 0), ("mean_magnitude_R28", 3)):
+        runs = []
+        for sd in seeds:
+            cnf, _ = make_config(name, seed=sd)
+            lits = np.asarray(cnf.lits)
+            q = Solver(local, stream=stream)
+            q.load_cnf(cnf)
+            c = config_default()
+            c.normalize = norm
+            q.init_batch(N, sd, c)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            steps, solved, best = 0, False, None
+            while steps < max_steps:
+                inf = q.step(min(chunk, max_steps - steps))
+                steps = inf.t
+                best = inf.best_unsat if best is None else min(best, inf.best_unsat)
+                if inf.solved:
+                    solved = True
+                    break
+            wall = time.perf_counter() - t0
+            rec = {"seed": sd, "solved": solved, "best_unsat": best, "steps_run": steps, "seconds": wall}
+            if solved:
+                sol = q.get_solution()
+                vals, idx, st = sol
+                var = np.abs(lits) - 1
+                val = np.where(lits > 0, vals[var], 1 - vals[var])
+                ok = bool((np.add.reduceat(val, cnf.clause_ptr[:-1]) > 0).all())
+                rec.update(step_found=int(st), candidate=int(idx), verified=ok)
+            q.close()
+            runs.append(rec)
+        sv = [r for r in runs if r["solved"]]
+        out[label] = {"runs": runs, "solved": len(sv),
+                      "median_steps_to_sat": float(np.median([r["step_found"] + 1 for r in sv])) if len(sv) * 2 > len(runs) else None,
+                      "median_seconds_to_sat": float(np.median([r["seconds"] for r in sv])) if len(sv) * 2 > len(runs) else None,
+                      "median_best_unsat": float(np.median([r["best_unsat"] for r in runs]))}
+    return out
 
 
 def workload_desc(name, cnf, N):
@@ -199,10 +326,19 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    cnf, cfg = make_config(args.config)
-    N = cfg["N"]                       # candidates per GPU
-    seed = cfg["seed"]
     stream = torch.cuda.current_stream()
+    if args.tts_only:
+        if rank == 0:
+            r = time_to_sat(args.tts_config, [int(x) for x in args.tts_seeds.split(",")], args.tts_max_steps, local,
+                            stream)
+            print(json.dumps({"metric": "time-to-SAT", "tts": r}), flush=True)
+        return
+    cnf, cfg = make_config(args.config)
+    strong = strong_scaling(args)
+    if strong and cfg["N"] % (32 * world):
+        raise SystemExit(f"{args.config}: N = {cfg['N']} is not a multiple of 32 x {world}")
+    N = cfg["N"] // world if strong else cfg["N"]       # candidates per GPU
+    seed = cfg["seed"]
 
     use_peer = (world > 1 and not args.nccl) or args.peer
     peer_fallback = None
@@ -295,9 +431,7 @@ def main():
     s.set_profiling(False)
     names = ["k_clause", "k_gtable", "k_hub", "k_update", "k_step_end"]
     per = {n: float(kms[i] / ksteps) for i, n in enumerate(names)}
-    V, C, K = cnf.V, cnf.C, cnf.K
-    occ_words = int(np.sum(np.diff(cnf.clause_ptr) ** 2))
-    upd_bytes = 24.0 * V * N + 2.0 * V * N / 8 + 4.0 * (occ_words + 2 * V + 1) + 8.0 * N * (K + 1)
+    upd_bytes = upd_algorithmic_bytes(cnf, N)
     upd_ms = per["k_update"]
     peaks = {}
     try:
@@ -309,7 +443,9 @@ def main():
     traffic, traffic_src = None, None
     try:      # dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture (profiles/)
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[args.config]["k_update"]
-        traffic, traffic_src = tr["bytes"], "profiles/" + tr["report"]
+        traffic = tr["bytes"]
+        traffic_src = ("profiles/" + tr["report"] + " (static: one ncu --set full capture of this build, "
+                       "refreshed per round with scripts/ncu_summary.py; not measured in this run)")
     except Exception:
         pass
     roofline = {"bound": "hbm", "kernel": "k_update", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -379,6 +515,20 @@ def main():
                "sample": f"{r['steps']} oracle steps on {r['Ns']} of {N} candidates ({r['seconds']:.1f} s, single thread)",
                "cpu": model, "host_cores": cores}
 
+    # ---- sub-results: the other single-GPU BASELINE configs (device-timed)
+    extra = None
+    if world == 1 and not args.no_extra:
+        extra = {}
+        for name in [x for x in args.extra.split(",") if x and x != args.config]:
+            try:
+                extra[name] = time_config(name, local, stream, hbm)
+            except Exception as ex:  # noqa: BLE001
+                extra[name] = {"error": f"{type(ex).__name__}: {ex}"[:200]}
+    tts = None
+    if world == 1 and not args.no_tts:
+        tts = time_to_sat(args.tts_config, [int(x) for x in args.tts_seeds.split(",")], args.tts_max_steps, local,
+                          stream)
+
     # ---- trajectory quality (not a timing): one LR cycle (360 iterations) of
     # the paper-exact Eq. 5 reading (R3) and of the normalize-off variant;
     # best satisfied fraction and whether the 99 % gate fires
@@ -405,7 +555,7 @@ def main():
     line = {
         "metric": "clause-candidate evals/sec", "value": value, "unit": "evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": w, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_desc(args.config, cnf, N * world), "V": cnf.V, "C": cnf.C, "K": cnf.K,
                    "N_per_gpu": N, "N_global": N * world, "seed": seed,
                    "parallelism": (f"candidate-sharded x{world}, exact exchanges inside the kernels over NVLink peer "
@@ -420,7 +570,7 @@ def main():
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": kps * args.steps, "clocks": clk.summary(),
         "last_info": {"t": last.t, "best_unsat": last.best_unsat, "loss": last.loss, "solved": last.solved},
-        "quality": quality,
+        "quality": quality, "configs_more": extra, "time_to_sat": tts,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

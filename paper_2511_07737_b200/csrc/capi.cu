@@ -1153,16 +1153,22 @@ tsat_status tsat_export_best(tsat_ctx ctx, int32_t M, int32_t k, tsat_partial* o
         const long long t_eval = ctx->t - 1;
         int n64 = 1;
         while (n64 < std::max(N, M)) n64 <<= 1;
-        // device scratch (freed on every path)
+        // device scratch, stream-ordered (cudaMallocAsync / cudaFreeAsync never wait for the
+        // device: with several ranks on one GPU a device-synchronising allocation would stall
+        // behind a peer's exchange kernel that waits for this rank); freed on every path
         unsigned long long *keys = nullptr, *gk = nullptr, *ent = nullptr, *gent = nullptr;
         int *cols = nullptr, *pos = nullptr, *ov = nullptr;
         double *absG = nullptr, *og = nullptr;
         struct Free {
+            cudaStream_t st;
             std::vector<void*> p;
-            ~Free() { for (void* x : p) cudaFree(x); }
-        } fr;
+            ~Free() { for (void* x : p) cudaFreeAsync(x, st); }
+        } fr{ctx->stream, {}};
         auto dalloc = [&](void** dst, size_t bytes) -> bool {
-            if (cudaMalloc(dst, std::max<size_t>(bytes, 8)) != cudaSuccess) { cudaGetLastError(); return false; }
+            if (cudaMallocAsync(dst, std::max<size_t>(bytes, 8), ctx->stream) != cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
             fr.p.push_back(*dst);
             return true;
         };
