@@ -62,6 +62,7 @@ def parse():
     ap.add_argument("--tts-seeds", default="1,2,3,4,5")
     ap.add_argument("--tts-max-steps", type=int, default=3600)
     ap.add_argument("--tts-only", action="store_true", help="run only the time-to-SAT protocol and print it")
+    ap.add_argument("--n-per-gpu", type=int, default=0, help="override the config's candidates per GPU (exploration)")
     return ap.parse_args()
 
 
@@ -239,10 +240,12 @@ def cpu_info():
     return model, os.cpu_count()
 
 
-def oracle_timing(cnf, N, seed, budget_s=20.0, min_steps=1, max_steps=None):
-    """Time the plain C oracle (single thread, as it stands) on a bounded
-    sample: a slice of the candidate batch sized so the run takes ~budget_s."""
+def oracle_timing(cnf, N, seed, budget_s=20.0, min_steps=1, max_steps=None, omp=False):
+    """Time the plain C oracle (as it stands; single thread, or its OpenMP
+    build over all host cores) on a bounded sample: a slice of the candidate
+    batch sized so the run takes ~budget_s."""
     from oracle import oracle as O
+    O.use_openmp(omp)
     Ns = min(N, 256)
     o = O.Oracle(cnf, Ns, seed)
     t0 = time.perf_counter()
@@ -266,7 +269,9 @@ def oracle_timing(cnf, N, seed, budget_s=20.0, min_steps=1, max_steps=None):
     for _ in range(steps):
         o.step()
     el = time.perf_counter() - t0
-    return dict(evals_per_s=cnf.C * Ns * steps / el, steps=steps, Ns=Ns, seconds=el)
+    O.use_openmp(False)
+    return dict(evals_per_s=cnf.C * Ns * steps / el, steps=steps, Ns=Ns, seconds=el,
+                threads=O.omp_threads() if omp else 1)
 
 
 def run_reference(args, rank, world):
@@ -281,6 +286,8 @@ def run_reference(args, rank, world):
     total_budget = 120.0
     per_step = total_budget / max(1, args.steps + args.warmup)
     from oracle import oracle as O
+    O.use_openmp(True)                     # the oracle's OpenMP build over all host cores
+    threads = O.omp_threads()
     Ns = 32
     o = O.Oracle(cnf, Ns, cfg["seed"])
     t0 = time.perf_counter()
@@ -302,8 +309,8 @@ def run_reference(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_desc(args.config, cnf, N), "V": cnf.V, "C": cnf.C, "K": cnf.K,
                    "N_per_gpu": cfg["N"], "N_global": N, "seed": cfg["seed"],
-                   "parallelism": "CPU oracle, one host thread, on a bounded candidate sample"},
-        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": 1, "kind": "oracle", "sample": sample,
+                   "parallelism": f"CPU oracle (OpenMP build, {threads} threads) on a bounded candidate sample"},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "oracle", "sample": sample,
                          "cpu": model, "host_cores": cores},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -338,6 +345,8 @@ def main():
     if strong and cfg["N"] % (32 * world):
         raise SystemExit(f"{args.config}: N = {cfg['N']} is not a multiple of 32 x {world}")
     N = cfg["N"] // world if strong else cfg["N"]       # candidates per GPU
+    if args.n_per_gpu:
+        N = args.n_per_gpu
     seed = cfg["seed"]
 
     use_peer = (world > 1 and not args.nccl) or args.peer
@@ -509,10 +518,14 @@ def main():
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        r = oracle_timing(cnf, N, seed, budget_s=15.0)
+        r = oracle_timing(cnf, N, seed, budget_s=12.0, omp=True)
+        r1 = oracle_timing(cnf, N, seed, budget_s=8.0)
         model, cores = cpu_info()
-        cpu = {"value": r["evals_per_s"], "unit": "evals/s", "cores": 1, "kind": "oracle",
-               "sample": f"{r['steps']} oracle steps on {r['Ns']} of {N} candidates ({r['seconds']:.1f} s, single thread)",
+        cpu = {"value": r["evals_per_s"], "unit": "evals/s", "cores": r["threads"], "kind": "oracle",
+               "sample": f"{r['steps']} oracle steps on {r['Ns']} of {N} candidates ({r['seconds']:.1f} s, "
+                         f"OpenMP build over {r['threads']} threads)",
+               "single_thread": {"value": r1["evals_per_s"], "cores": 1,
+                                 "sample": f"{r1['steps']} steps on {r1['Ns']} candidates ({r1['seconds']:.1f} s)"},
                "cpu": model, "host_cores": cores}
 
     # ---- sub-results: the other single-GPU BASELINE configs (device-timed)
