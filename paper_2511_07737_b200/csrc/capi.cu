@@ -78,6 +78,7 @@ struct tsat_ctx_s {
     double prof_ms[kKernelsPerStep] = {0, 0, 0, 0, 0};
     // k_update launch geometry (configure_kernels)
     int upd_mode = 0, upd_GT = 0, upd_NG = 0, upd_grid = 0, num_sms = 0, upd_recbufs = 2;
+    int upd_RB = 1, upd_blk_cap = 0;    // row-block k_update (small shards, k_update_blk.cu)
     int upd_chunk = 0, upd_gs_global = 0;
     bool chunked = false;               // N too large for the fused kernel: split sequence, no collectives at W = 1
     size_t upd_smem = 0;
@@ -275,6 +276,8 @@ StepArgs step_args(tsat_ctx ctx) {
     a.upd_grid = ctx->upd_grid;
     a.upd_smem = ctx->upd_smem;
     a.upd_rec_cap = std::max(64, (ctx->cnf.max_rec_words + 63) / 64 * 64);
+    a.upd_RB = ctx->upd_RB;
+    a.upd_blk_cap = ctx->upd_blk_cap;
     a.sharded = (ctx->sharded || ctx->chunked) ? 1 : 0;     // kernels: the split (phase A / B) sequence
     a.Gbuf = (float*)(w + L.Gbuf);
     a.Jbuf = (long long*)(w + L.Jbuf);
@@ -894,6 +897,25 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
         ctx->t = 0;
         ctx->steps_done = 0;
         CK(cudaSetDevice(ctx->device));
+        // row blocks for small shards (fused W = 1 and peer paths): RB rows per
+        // work item, staging capacity = max over blocks of the non-hub rows' records
+        ctx->upd_RB = 1;
+        ctx->upd_blk_cap = 0;
+        if (!ctx->sharded && !ctx->chunked && !std::getenv("TSAT_NO_BLK")) {
+            const int RB = update_block_rows(ctx->N);
+            if (RB > 1) {
+                const std::vector<uint32_t>& ptr = ctx->cnf.batched ? ctx->cnf.bat_ptr : ctx->cnf.occ_ptr;
+                long long cap = 0;
+                for (int v0 = 0; v0 < ctx->cnf.V; v0 += RB) {
+                    long long w = 0;
+                    for (int v = v0; v < std::min(ctx->cnf.V, v0 + RB); ++v)
+                        if (ctx->cnf.hub_of[v] < 0) w += ptr[v + 1] - ptr[v];
+                    cap = std::max(cap, w);
+                }
+                ctx->upd_RB = RB;
+                ctx->upd_blk_cap = (int)std::max(64LL, (cap + 63) / 64 * 64);
+            }
+        }
         {
             StepArgs g = step_args(ctx);
             CK(configure_kernels(&g));

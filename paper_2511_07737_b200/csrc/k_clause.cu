@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(con
                                                                 const uint32_t* __restrict__ clit, long long C,
                                                                 int* __restrict__ hist, int N, int uniform,
                                                                 DevScalars* __restrict__ ds,
-                                                                const StepScalars* __restrict__ sc) {
+                                                                const StepScalars* __restrict__ sc, int nsub) {
     constexpr int NP = (KB == 4) ? 2 : 3;
     constexpr int CB = 7;
     __shared__ int sh[(KB - 1) * 1024];
@@ -72,8 +72,12 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(con
     __shared__ uint2 soff[kWarps][chunk_clauses(KMAXC) * KMAXC];
     constexpr int kCH = chunk_clauses(KMAXC);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int w = blockIdx.x * 32 + lane;
-    const bool valid = w < NW;
+    // nsub > 1 (fewer than 32 words, N < 1024 per GPU): the warp's lanes are
+    // nsub sub-groups of NW lanes; sub-group `sub` evaluates every nsub-th
+    // carry-save group of the chunk for word w, so no lane idles
+    const int sub = nsub > 1 ? lane / NW : 0;
+    const int w = nsub > 1 ? lane - sub * NW : blockIdx.x * 32 + lane;
+    const bool valid = w < NW && sub < nsub;
     pdl_wait();
     pdl_trigger();
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
@@ -94,6 +98,15 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(con
     const uint32_t* Aw = A + (valid ? w : 0);          // lanes past NW read a valid word, results unused
     const unsigned long long pol = plane_policy(planes_fit_l2(V, NW));
     const long long nchunks = (C + kCH - 1) / kCH;
+    constexpr int kG0 = KMAXC <= 3 ? TSAT_CL_G3 : 1;
+    // with sub-groups a lane sees kCH / nsub clauses per chunk: its counters
+    // (<= 127 per bin) are carried over nsub chunks before one extraction
+    uint32_t cnt[KB - 1][CB];
+#pragma unroll
+    for (int r = 0; r < KB - 1; ++r)
+#pragma unroll
+        for (int b = 0; b < CB; ++b) cnt[r][b] = 0u;
+    int pend = 0;
     // grid-sized: warps stride over the clause chunks of this word block
     for (long long chunk = (long long)blockIdx.y * kWarps + warp; chunk < nchunks;
          chunk += (long long)gridDim.y * kWarps) {
@@ -122,13 +135,8 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(con
             }
         }
         __syncwarp();
-        uint32_t cnt[KB - 1][CB];
-#pragma unroll
-        for (int r = 0; r < KB - 1; ++r)
-#pragma unroll
-            for (int b = 0; b < CB; ++b) cnt[r][b] = 0u;
-        constexpr int kG = KMAXC <= 3 ? TSAT_CL_G3 : 1;  // carry-save groups per iteration (gathers in flight)
-        for (int cb0 = 0; cb0 < nc; cb0 += kUnr * kG) {
+        constexpr int kG = kG0;                         // carry-save groups per iteration (gathers in flight)
+        for (int cb0 = sub * kUnr * kG; cb0 < nc; cb0 += kUnr * kG * nsub) {
             uint32_t xx[kG][kUnr][KMAXC];
 #pragma unroll
             for (int gq = 0; gq < kG; ++gq)
@@ -170,6 +178,10 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(con
             for (int r = 0; r < KB - 1; ++r) csa_add4<CB>(cnt[r], m[0][r], m[1][r], m[2][r], m[3][r]);
           }
         }
+        ++pend;
+        const bool last = chunk + (long long)gridDim.y * kWarps >= nchunks;
+        if (pend < nsub && !last) continue;             // keep counting into the same counters
+        pend = 0;
         if (valid) {
             if (KB == 4) {
                 // one 32x32 transpose packs the three 7-bit counts of each
@@ -186,7 +198,7 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(con
                     if (T[j]) {
                         const unsigned long long pk = T[j];
                         const unsigned long long wide = (pk & 0x3FFull) | ((pk & 0xFFC00ull) << 11) | ((pk & 0x3FF00000ull) << 22);
-                        atomicAdd(&shp[33 * lane + j], wide);             // padded layout
+                        atomicAdd(&shp[33 * w + j], wide);                // padded layout (w = lane without sub-groups)
                     }
             } else {
                 // two 32x32 transposes (bins 0-3, 4-6) give each candidate's
@@ -210,7 +222,7 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(con
                     for (int j = 0; j < 32; ++j) {
                         const unsigned long long x = T[j];
                         if (!x) continue;
-                        const int o = 33 * lane + j;
+                        const int o = 33 * w + j;
                         if (blk == 0) {
                             const unsigned long long w0 = (x & 0xFFull) | ((x & 0xFF00ull) << 13) | ((x & 0xFF0000ull) << 26);
                             if (w0) atomicAdd(&shp[o], w0);
@@ -224,6 +236,10 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(con
                 }
             }
         }
+#pragma unroll
+        for (int r = 0; r < KB - 1; ++r)
+#pragma unroll
+            for (int b = 0; b < CB; ++b) cnt[r][b] = 0u;
     }
     __syncthreads();
     if (KB == 4) {
@@ -272,7 +288,12 @@ cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, const StepSca
     }
     const int NW = a.N >> 5;
     const int nwb = (NW + 31) / 32;
+    // sub-groups of NW lanes when a warp would leave lanes idle (N < 1024 per GPU);
+    // a chunk (kCH clauses) must split evenly into carry-save groups per sub-group
     const int kCH = chunk_clauses(a.mc.K <= 3 ? 3 : 7);
+    const int kGrp = 4 * (a.mc.K <= 3 ? TSAT_CL_G3 : 1);
+    int nsub = NW < 32 ? 32 / NW : 1;
+    while (nsub > 1 && kCH % (kGrp * nsub)) --nsub;
     const long long nchunks = (a.C + kCH - 1) / kCH;
     const long long ctas_needed = (nchunks + kWarps - 1) / kWarps;
     const int K = a.mc.K;
@@ -288,13 +309,13 @@ cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, const StepSca
     const int uni = a.uniform_len;
     if (K <= 2)
         return launch_maybe_pdl(a.pdl, k_clause<4, 2>, grid, dim3(256), 0, st, Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist,
-                                a.N, (int)(uni && K == 2), a.ds, sc);
+                                a.N, (int)(uni && K == 2), a.ds, sc, nsub);
     else if (K == 3)
         return launch_maybe_pdl(a.pdl, k_clause<4, 3>, grid, dim3(256), 0, st, Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist,
-                                a.N, uni, a.ds, sc);
+                                a.N, uni, a.ds, sc, nsub);
     else
         return launch_maybe_pdl(a.pdl, k_clause<8, 7>, grid, dim3(256), 0, st, Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist,
-                                a.N, (int)(uni && K == 7), a.ds, sc);
+                                a.N, (int)(uni && K == 7), a.ds, sc, nsub);
     return cudaGetLastError();
 }
 

@@ -21,207 +21,11 @@
 // Rows whose counts can leave int8 ("hubs", SURVEY §7 hard parts) get their
 // counts from k_hub, which splits a hub's occurrences over many CTAs and adds
 // exact int32 counts (integer atomics: order-free, deterministic).
-#include <cstdio>
-#include <cstdlib>
-
-#include "device_common.cuh"
 #include "peer.cuh"
 
-#ifndef TSAT_UNI3
-#define TSAT_UNI3 2
-#endif
-#ifndef TSAT_3B_UNROLL
-#define TSAT_3B_UNROLL 1
-#endif
-constexpr int kUnroll3b = TSAT_3B_UNROLL;
-#ifndef TSAT_UPD_THREADS8
-#define TSAT_UPD_THREADS8 512        // KB = 8 block size bound
-#endif
-#ifndef TSAT_UPD_THREADS4P
-#define TSAT_UPD_THREADS4P 768      // KB = 4 block size bound of the peer-exchange kernel (MODE 2)
-#endif
-#ifndef TSAT_UPD_THREADS4
-#define TSAT_UPD_THREADS4 768       // KB = 4 block size bound (register budget)
-#endif
-
-#ifndef TSAT_HINTS
-#define TSAT_HINTS 1
-#endif
+#include "upd_common.cuh"
 
 namespace tsat {
-
-// Pass 3b's last reads and writes of theta, m, v: with TSAT_HINTS, streaming
-// (evict-first) so the bit planes and records keep their L2 lines.
-__device__ __forceinline__ float4 ld_last(const float* p) {
-#if TSAT_HINTS
-    return __ldcs(reinterpret_cast<const float4*>(p));
-#else
-    return *reinterpret_cast<const float4*>(p);
-#endif
-}
-__device__ __forceinline__ void st_stream(float* p, float4 x) {
-#if TSAT_HINTS
-    __stcs(reinterpret_cast<float4*>(p), x);
-#else
-    *reinterpret_cast<float4*>(p) = x;
-#endif
-}
-
-namespace {
-constexpr int kCtr = 8;        // counter planes (int8) in the fused kernel
-constexpr int kHubCtrPlain = 11;    // counter planes (int11) in k_hub (kHubSlab = 1023 occurrences)
-constexpr int kHubCtrBatched = 10;  // batched super-chunks: kHubSlabBatches * 4 <= 511 occurrences
-
-__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) / 16 * 16; }
-}  // namespace
-
-// Shared-memory geometry of k_update (host and device agree through this).
-__host__ __device__ inline size_t upd_gs_bytes(int KB, int N) { return align16((size_t)KB * N * 4); }
-__host__ __device__ inline size_t upd_dpk_words(int N) { return (size_t)N + (N >> 5); }
-// nbufs: 2 record buffers (the next row's records land during this row's
-// streams), or 1 (staged after this row's gather) when that buys a warp group:
-// KB = 8 (shared-memory bound), a compile-time choice (a runtime one costs
-// the instruction-cache-bound KB = 8 kernel ~7 %).
-__host__ __device__ constexpr int upd_recbufs(int KB) { return KB == 8 ? 1 : 2; }
-__host__ __device__ inline size_t upd_group_bytes(int KB, int N, int rec_cap, int nbufs) {
-    const int NDW = KB == 4 ? 1 : 2;
-    // dpk | nbufs record buffers | sign planes [2 parities][pos, neg][NW] | 128 B scratch
-    return align16((size_t)NDW * upd_dpk_words(N) * 4) + nbufs * align16((size_t)rec_cap * 4) +
-           align16((size_t)4 * (N >> 5) * 4) + 128;
-}
-
-// x * 2^s, exact (== scalbn) when 2^s is a normal double.
-__device__ __forceinline__ double times_pow2(double x, int s) {
-    if (s >= -1000 && s <= 1000) return x * __longlong_as_double((long long)(1023 + s) << 52);
-    return scalbn(x, s);
-}
-
-// Signed byte r of u (counts stored as int8) -> exact float: the byte, biased
-// by 128, goes into the mantissa of 2^23 (PRMT) and the bias is subtracted.
-__device__ __forceinline__ float sbyte_to_float(uint32_t ub, int r) {
-    return __uint_as_float(__byte_perm(ub, 0x4B000000u, 0x7540u + (unsigned)r)) - 8388736.0f;
-}
-
-// a * b per lane, correctly rounded, never contracted with a following add:
-// ptxas fuses FMUL2 + FADD2 into FFMA2 even with --fmad=false (and folds an
-// FFMA2 with a -0 addend the same way; scripts/micro/fuse_check.cu), so
-// products that feed an add are two scalar __fmul_rn (which ptxas respects).
-__device__ __forceinline__ float2 mul2_unfused(float2 a, float2 b) {
-    return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y));
-}
-
-// Per-bin counts of one candidate as exact floats (bytes + derived last bin).
-template <int KB>
-__device__ __forceinline__ void fold_counts(float (&d)[KB], uint32_t p0, uint32_t p1, float dsumf) {
-    const uint32_t u0 = p0 ^ 0x80808080u, u1 = p1 ^ 0x80808080u;
-#pragma unroll
-    for (int r = 0; r < KB - 1; ++r) d[r] = sbyte_to_float(r < 4 ? u0 : u1, r & 3);
-    float acc = d[0];
-#pragma unroll
-    for (int r = 1; r < KB - 1; ++r) acc = acc + d[r];     // exact: small integers (never -0)
-    d[KB - 1] = dsumf - acc;
-}
-
-template <int KB>
-__device__ __forceinline__ float fold_ints(const int* hubrow, int N, int n, int dsum, const float (&gq)[KB]) {
-    float d[KB];
-    int acc = 0;
-#pragma unroll
-    for (int r = 0; r < KB - 1; ++r) { const int x = hubrow[(size_t)r * N + n]; acc += x; d[r] = (float)x; }
-    d[KB - 1] = (float)(dsum - acc);
-    float G = 0.0f;
-#pragma unroll
-    for (int r = 0; r < KB; ++r) G = __fmaf_rn(d[r], gq[r], G);
-    return G;
-}
-
-// Pass 3a of one row: G for every candidate (stored over its counts in dpk),
-// and the int64 fixed-point partial sum of J_v = sum_n G theta (R13).
-template <int KB, bool HUB>
-__device__ __forceinline__ long long pass_fold(const float* __restrict__ trow, uint32_t* dpk, size_t dpkw,
-                                               const float* gs, int* hubrow, int N, int Nst, int GT, int tg, int dsum,
-                                               bool jvalid, float p2, float* __restrict__ gout) {
-    // N candidates from the pointers' origin; Nst = row stride of gs / hubrow
-    const float dsumf = (float)dsum;
-    long long I = 0;
-    float4 th_nx = (4 * tg < N) ? *reinterpret_cast<const float4*>(trow + 4 * tg) : make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int n = 4 * tg; n < N; n += 4 * GT) {
-        const float4 th4 = th_nx;
-        if (n + 4 * GT < N) th_nx = *reinterpret_cast<const float4*>(trow + n + 4 * GT);
-        const float th[4] = {th4.x, th4.y, th4.z, th4.w};
-        float4 g4[KB];
-#pragma unroll
-        for (int r = 0; r < KB; ++r) g4[r] = *reinterpret_cast<const float4*>(gs + (size_t)r * Nst + n);
-        uint32_t* dp = dpk + n + (n >> 5);
-        float Gq[4];
-        if (HUB) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                float gq[KB];
-#pragma unroll
-                for (int r = 0; r < KB; ++r) gq[r] = q == 0 ? g4[r].x : q == 1 ? g4[r].y : q == 2 ? g4[r].z : g4[r].w;
-                Gq[q] = fold_ints<KB>(hubrow, Nst, n + q, dsum, gq);
-            }
-        } else {
-            // candidate pairs: d_r as floats (exact small integers), then the
-            // r-ascending FMA chain with packed fp32x2 FMAs (per-lane exact FMA)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                float dA[KB], dB[KB];
-                fold_counts<KB>(dA, dp[2 * h], KB == 8 ? dp[dpkw + 2 * h] : 0u, dsumf);
-                fold_counts<KB>(dB, dp[2 * h + 1], KB == 8 ? dp[dpkw + 2 * h + 1] : 0u, dsumf);
-                float2 G2 = make_float2(0.0f, 0.0f);
-#pragma unroll
-                for (int r = 0; r < KB; ++r)
-                    G2 = __ffma2_rn(make_float2(dA[r], dB[r]),
-                                    h == 0 ? make_float2(g4[r].x, g4[r].y) : make_float2(g4[r].z, g4[r].w), G2);
-                Gq[2 * h] = G2.x;
-                Gq[2 * h + 1] = G2.y;
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const float G = Gq[q];
-            dp[q] = __float_as_uint(G);
-            if (jvalid) I += jterm(G, th[q], p2);
-        }
-        if (gout) *reinterpret_cast<float4*>(gout + n) = make_float4(Gq[0], Gq[1], Gq[2], Gq[3]);
-        if (HUB) {
-#pragma unroll
-            for (int r = 0; r < KB - 1; ++r) *reinterpret_cast<int4*>(hubrow + (size_t)r * Nst + n) = make_int4(0, 0, 0, 0);
-        }
-    }
-    return I;
-}
-
-// Bulk prefetch of [p, p + bytes) into L2 (TMA engine; bytes % 16 == 0).
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-// Optional update noise (R17): xi = (x >> 8) 2^-24 - 1/2 with
-// x = Philox(key = seed, ctr = (n>>2, v, 1+t, 0))[n & 3].  Out of line: it is
-// off by default and would otherwise bloat the hot loop's instruction footprint.
-__device__ __noinline__ float noise_xi(unsigned long long seed, long long ng, int v, long long t) {
-    uint32_t xr[4] = {(uint32_t)(ng >> 2), (uint32_t)v, (uint32_t)(1 + t), 0u};
-    philox4x32_10(xr, (uint32_t)seed, (uint32_t)(seed >> 32));
-    return (float)(xr[ng & 3] >> 8) * 5.9604644775390625e-08f - 0.5f;
-}
-
-// 4-byte asynchronous global -> shared copy (LDGSTS) and its group fences.
-__device__ __forceinline__ void cp_async4(uint32_t* smem_dst, const uint32_t* gsrc) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-// Barrier over one warp group: a warp-sized group only needs __syncwarp, so
-// more than 15 groups (the named-barrier limit) can share a CTA.
-__device__ __forceinline__ void gsync(int bar, int GT) {
-    if (GT == 32) __syncwarp();
-    else group_bar(bar, GT);
-}
 
 // MODE 0: fused W = 1 iteration.  MODE 1: phase A of the sharded iteration
 // (G -> Gbuf, int64 J partial -> Jbuf; the AdamW phase runs after the J exchange).

@@ -1,0 +1,494 @@
+// k_update_blk.cu - rows (a7) STE backward, (a8) Eq. 5 Jacobian, (a9) AdamW +
+// re-binarisation for small candidate shards (§3.2 l.189-191, l.226;
+// §4.1 l.255-269; the shard sizes of §8(e)'s strong scaling: N = 128 .. 512
+// candidates per GPU, e.g. BASELINE c3's 1024 candidates over 2-8 B200).
+//
+// The per-row kernel (k_update.cu) maps a warp's lanes to the 32-candidate
+// words of ONE row: with N = 128 only 4 of 32 lanes gather, every row pays
+// its own L2/HBM round trips, barriers and scheduler atomic, and 1M rows
+// cost 13 us each per warp group.  Here a work item is a BLOCK of RB =
+// 32 / (N/32) consecutive rows, one warp per group:
+//   1. gather: lane = (row r = lane / NW, word w = lane % NW), so all lanes
+//      count occurrences at once (same bit-sliced counters and transposes);
+//   2. the block's theta / m / v rows are contiguous ([V][N] layout), so
+//      passes 3a / 3b stream RB * N floats as ONE float4 stream (one-ahead
+//      loads cross row boundaries; one L2 bulk prefetch per array);
+//      per-row values (J_v, Q_v, max |theta|) are warp reductions at the
+//      row's last 128-candidate iteration;
+//   3. peer path (MODE 2): the block's RB J partials are sent together and
+//      awaited together; its Q partials are sent after pass 3b and the block
+//      is finished one block later (as the per-row kernel does per row).
+// Arithmetic is the per-row kernel's, operation for operation, so results
+// are bit-identical to it (and to the oracle).
+#include "peer.cuh"
+#include "upd_common.cuh"
+
+namespace tsat {
+
+namespace {
+// Per-row values of the current block (lane r writes row r); pq / pm2 belong
+// to the pending block of the peer path (finished one block late).
+struct BlkRow {
+    double rho;
+    long long jt, qt, pq;
+    float rhof, ncf, p2, m2, pm2;
+    int hub, dsum, jvalid, s;
+    int guard;
+};
+
+__host__ __device__ inline size_t blk_group_bytes(int KB, int N, int RB, int cap, int nbufs) {
+    const int NDW = KB == 4 ? 1 : 2;
+    return align16((size_t)NDW * RB * upd_dpk_words(N) * 4) + nbufs * align16((size_t)cap * 4) +
+           align16((size_t)4 * RB * (N >> 5) * 4) + align16(sizeof(BlkRow) * RB) + 16;
+}
+}  // namespace
+
+int update_block_rows(int N) {
+    if (N <= 0 || N % 128 != 0) return 1;      // 128-candidate iterations never straddle a row
+    const int NW = N >> 5;
+    if (NW >= 32) return 1;
+    const int rb = 32 / NW;
+    return rb >= 2 ? rb : 1;
+}
+
+template <int KB, int MODE, bool MAG>
+__global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TSAT_UPD_THREADS4) : TSAT_UPD_THREADS8, 1)
+    k_update_blk(StepArgs a, const uint32_t* __restrict__ Acur, uint32_t* __restrict__ Anext,
+                 const StepScalars* __restrict__ sc) {
+    constexpr int NP = (KB == 4) ? 2 : 3;
+    constexpr int NCTR = KB - 1;
+    constexpr int NDW = KB == 4 ? 1 : 2;
+    constexpr int nbufs = upd_recbufs(KB);
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int N = a.N, NW = N >> 5, RB = a.upd_RB;
+    const int ipr = N >> 7;                              // 128-candidate iterations per row
+    const size_t dpkw = upd_dpk_words(N), dplane = (size_t)RB * dpkw;
+    float* gs = reinterpret_cast<float*>(smem);
+    const int grp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cap = a.upd_blk_cap;
+    unsigned char* gb = smem + upd_gs_bytes(KB, N) + (size_t)grp * blk_group_bytes(KB, N, RB, cap, nbufs);
+    uint32_t* dpk = reinterpret_cast<uint32_t*>(gb);
+    uint32_t* rec = reinterpret_cast<uint32_t*>(gb + align16((size_t)NDW * dplane * 4));
+    const size_t recw = align16((size_t)cap * 4) / 4;
+    uint32_t* pl0 = rec + nbufs * recw;                  // [parity][pos | neg][RB * NW]
+    BlkRow* rp = reinterpret_cast<BlkRow*>(reinterpret_cast<unsigned char*>(pl0) + align16((size_t)16 * RB * NW));
+    int* slot = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(rp) + align16(sizeof(BlkRow) * RB));
+    const int nitems = (a.V + RB - 1) / RB;
+    const bool uni3 = a.uniform_len && a.mc.K == 3 && KB == 4;
+    const unsigned long long pol = plane_policy(planes_fit_l2(a.V, NW));
+    const int gr = lane / NW, gw = lane - gr * NW;       // gather lane -> (row of the block, word)
+
+    pdl_wait();
+    pdl_trigger();
+    for (int i = threadIdx.x * 4; i < KB * N; i += blockDim.x * 4)
+        *reinterpret_cast<float4*>(gs + i) = *reinterpret_cast<const float4*>(a.gtab + i);
+    if (lane == 0) slot[1] = atomicAdd(&a.ds->row_counter, 1);
+    const long long t = sc->t;
+    __shared__ unsigned long long pscal[3];
+    if (MODE == 2 && threadIdx.x == 0) {
+        const unsigned long long own[4] = {~a.ds->best_key, a.ds->gmax_bits,
+                                           (unsigned long long)a.ds->thmax_bits[t & 1],
+                                           (unsigned long long)a.ds->loss_fx};
+        unsigned long long x[4];
+        peer_recv_scalars(a.px, sc->xgen, a.ds, own, x);
+        pscal[0] = ~x[0];
+        pscal[1] = a.px.exchange_rows ? x[1] : a.ds->gmax_bits;
+        pscal[2] = a.px.exchange_rows ? x[2] : (unsigned long long)a.ds->thmax_bits[t & 1];
+        if (blockIdx.x == 0) {
+            const int bu = (int)(pscal[0] >> 32);
+            const long long bi = (long long)(pscal[0] & 0xffffffffull);
+            if (bu == 0 && a.ds->sol_step < 0) { a.ds->sol_step = t; a.ds->sol_idx = bi; }
+            const double loss = -((double)(long long)x[3] * a.mc.loss_unscale);
+            a.ds->loss = loss;
+            a.ds->info_t = t + 1;
+            a.ds->info_best_unsat = bu;
+            a.ds->info_best_idx = bi;
+            a.ds->info_loss = loss;
+        }
+    }
+    __syncthreads();
+
+    const double gmax = __longlong_as_double((long long)(MODE == 2 ? pscal[1] : a.ds->gmax_bits));
+    const float thmax = __uint_as_float(MODE == 2 ? (unsigned)pscal[2] : a.ds->thmax_bits[t & 1]);
+    const float wdf = sc->wdf, a1 = sc->a1, b2f = sc->b2f, a2 = sc->a2, nss = sc->nss, rbc2 = sc->rbc2,
+                epsf = sc->epsf, nz = sc->nz, mkeep = sc->mkeep;
+    const MethodConsts& mc = a.mc;
+
+    // records of block v0 .. v0 + nr - 1 (non-hub rows, back to back) -> buf
+    auto stage = [&](int v0, int nr, uint32_t* buf, bool async) {
+        unsigned off = 0;
+        for (int r = 0; r < nr; ++r) {
+            const int v = v0 + r;
+            if (a.hub_of[v] >= 0) continue;
+            const unsigned b = a.upd_ptr[v], e = a.upd_ptr[v + 1];
+            for (unsigned i = lane; i < e - b; i += 32) {
+                if (async) cp_async4(buf + off + i, a.upd_rec + b + i);
+                else buf[off + i] = a.upd_rec[b + i];
+            }
+            off += e - b;
+        }
+    };
+    // Rows of a block are complete once their global Q are known: bit planes
+    // (sign(d) = sign(Q), R3), Eq. 5 statistics, max |theta|, first-model bits.
+    auto finish_block = [&](int v0, int nr, const uint32_t* pl, bool pending) {
+        for (int idx = lane; idx < nr * NW; idx += 32) {
+            const int r = idx / NW;
+            const long long Qg = pending ? rp[r].pq : rp[r].qt;
+            const bool dpos = !mc.normalize || Qg >= 0;
+            Anext[(size_t)v0 * NW + idx] = dpos ? pl[idx] : pl[RB * NW + idx];
+        }
+        float m2 = 0.0f;
+        if (lane < nr) {
+            const int vr = v0 + lane;
+            const long long Qg = pending ? rp[lane].pq : rp[lane].qt;
+            m2 = pending ? rp[lane].pm2 : rp[lane].m2;
+            double dn, rhon;
+            unsigned char gn;
+            row_finish(Qg, mc, &dn, &rhon, &gn);
+            a.rowQ[vr] = Qg; a.rowD[vr] = dn; a.rowRho[vr] = rhon; a.rowGuard[vr] = gn;
+            const unsigned long long bk = MODE == 2 ? pscal[0] : a.ds->best_key;
+            if ((bk >> 32) == 0ull && (a.ds->sol_step < 0 || a.ds->sol_step == t)) {          // first model (A22)
+                const long long idx = (long long)(bk & 0xffffffffull) - mc.n0;
+                if (idx >= 0 && idx < N)
+                    a.sol[vr] = (unsigned char)((Acur[(size_t)vr * NW + (idx >> 5)] >> (idx & 31)) & 1u);
+            }
+        }
+        m2 = warp_maxf(m2);
+        if (lane == 0) atomicMax(&a.ds->thmax_bits[(t + 1) & 1], __float_as_uint(m2));
+    };
+
+    int pend_v0 = -1, pend_nr = 0;
+    int item = slot[1];
+    if (item < nitems) stage(item * RB, min(RB, a.V - item * RB), rec, false);
+    __syncwarp();
+    int it = 0;
+    for (; item < nitems; ++it) {
+        const int v0 = item * RB, nr = min(RB, a.V - v0);
+        uint32_t* rb_cur = rec + (size_t)(nbufs == 2 ? (it & 1) : 0) * recw;
+        uint32_t* rb_nxt = rec + (size_t)(nbufs == 2 ? ((it + 1) & 1) : 0) * recw;
+        uint32_t* pl = pl0 + (MODE == 2 ? (size_t)(it & 1) * 2 * RB * NW : 0);
+        if (lane == 0) {
+            slot[it & 1] = atomicAdd(&a.ds->row_counter, 1);
+            const uint32_t bytes = (uint32_t)nr * (uint32_t)N * 4u;
+            prefetch_l2(a.theta + (size_t)v0 * N, bytes);
+            prefetch_l2(a.m + (size_t)v0 * N, bytes);
+            prefetch_l2(a.v + (size_t)v0 * N, bytes);
+        }
+        if (lane < nr) {                                   // this block's row values
+            const int v = v0 + lane;
+            const int2 pn = a.occ_pn[v];
+            BlkRow& R = rp[lane];
+            R.hub = a.hub_of[v];
+            R.dsum = pn.y - pn.x;
+            R.rho = a.rowRho[v];
+            R.guard = a.rowGuard[v];
+            int s;
+            float p2;
+            R.jvalid = jscale(mc.Nnorm, pn.x + pn.y, gmax, thmax, &s, &p2) ? 1 : 0;
+            R.s = s;
+            R.p2 = p2;
+        }
+
+        // ---- 1+2: gather (lane = row x word), transpose to bytes
+        if (gr < nr) {
+            const int v = v0 + gr;
+            if (a.hub_of[v] < 0) {
+                unsigned roff = 0;
+                for (int r = 0; r < gr; ++r)
+                    if (a.hub_of[v0 + r] < 0) roff += a.upd_ptr[v0 + r + 1] - a.upd_ptr[v0 + r];
+                const uint32_t* rbase = rb_cur + roff;
+                auto recf = [&](unsigned i) { return rbase[i]; };
+                const uint32_t own = __ldg(Acur + (size_t)v * NW + gw);
+                uint32_t cnt[NCTR][kCtr];
+                if (uni3) {
+                    const int2 pn = a.occ_pn[v];
+                    count_uni3<NCTR, kCtr, false>(cnt, recf, (unsigned)pn.y, (unsigned)pn.x, own, Acur, (unsigned)NW,
+                                                  (unsigned)gw, pol);
+                } else {
+                    count_batched<NP, NCTR, kCtr>(cnt, recf, a.upd_ptr[v + 1] - a.upd_ptr[v], own, Acur, (unsigned)NW,
+                                                  (unsigned)gw, pol);
+                }
+#pragma unroll 1
+                for (int blk = 0; blk < (KB == 8 ? 2 : 1); ++blk) {
+                    uint32_t T[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int r = i / kCtr;
+                        const uint32_t lo = (r < NCTR && r < 4) ? cnt[r][i % kCtr] : 0u;
+                        const uint32_t hi = (4 + r < NCTR) ? cnt[4 + r][i % kCtr] : 0u;
+                        T[i] = blk ? hi : lo;
+                    }
+                    transpose32(T);
+                    uint32_t* dst = dpk + blk * dplane + (size_t)gr * dpkw + 33 * gw;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) dst[j] = T[j];
+                }
+            }
+        }
+        if (MODE == 2 && pend_v0 >= 0 && lane < pend_nr)       // previous block's Q, sent a block ago
+            rp[lane].pq = peer_row_recv(a.px, 1, pend_v0 + lane, sc->xgen, a.ds, rp[lane].pq);
+        __syncwarp();
+        const int item_next = slot[it & 1];
+        const int v0n = item_next < nitems ? item_next * RB : a.V;
+        auto stage_next = [&]() {
+            if (v0n < a.V) stage(v0n, min(RB, a.V - v0n), rb_nxt, true);
+            cp_async_commit();
+        };
+        if (nbufs == 1) stage_next();
+        if (MODE == 2 && pend_v0 >= 0) {
+            finish_block(pend_v0, pend_nr, pl0 + (size_t)((it + 1) & 1) * 2 * RB * NW, true);
+            pend_v0 = -1;
+        }
+
+        // ---- 3a: G -> dpk, J partial per row (flat float4 stream over the block)
+        const int total = nr * ipr;
+        {
+            const float* tb = a.theta + (size_t)v0 * N;
+            float4 th_nx = *reinterpret_cast<const float4*>(tb + 4 * lane);
+            long long I = 0;
+            for (int k = 0; k < total; ++k) {
+                const int r = k / ipr, n = (k - r * ipr) * 128 + 4 * lane;
+                const float4 th4 = th_nx;
+                if (k + 1 < total) th_nx = *reinterpret_cast<const float4*>(tb + (size_t)(k + 1) * 128 + 4 * lane);
+                const float th[4] = {th4.x, th4.y, th4.z, th4.w};
+                const int hub = rp[r].hub, dsum = rp[r].dsum;
+                const float p2 = rp[r].p2;
+                const bool jv = rp[r].jvalid != 0;
+                float4 g4[KB];
+#pragma unroll
+                for (int q = 0; q < KB; ++q) g4[q] = *reinterpret_cast<const float4*>(gs + (size_t)q * N + n);
+                uint32_t* dp = dpk + (size_t)r * dpkw + n + (n >> 5);
+                float Gq[4];
+                if (hub >= 0) {
+                    int* hubrow = a.hubD + (size_t)hub * NCTR * N;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        float gq[KB];
+#pragma unroll
+                        for (int b = 0; b < KB; ++b) gq[b] = q == 0 ? g4[b].x : q == 1 ? g4[b].y : q == 2 ? g4[b].z : g4[b].w;
+                        Gq[q] = fold_ints<KB>(hubrow, N, n + q, dsum, gq);
+                    }
+#pragma unroll
+                    for (int b = 0; b < KB - 1; ++b)
+                        *reinterpret_cast<int4*>(hubrow + (size_t)b * N + n) = make_int4(0, 0, 0, 0);
+                } else {
+                    const float dsumf = (float)dsum;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        float dA[KB], dB[KB];
+                        fold_counts<KB>(dA, dp[2 * h], KB == 8 ? dp[dplane + 2 * h] : 0u, dsumf);
+                        fold_counts<KB>(dB, dp[2 * h + 1], KB == 8 ? dp[dplane + 2 * h + 1] : 0u, dsumf);
+                        float2 G2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+                        for (int b = 0; b < KB; ++b)
+                            G2 = __ffma2_rn(make_float2(dA[b], dB[b]),
+                                            h == 0 ? make_float2(g4[b].x, g4[b].y) : make_float2(g4[b].z, g4[b].w), G2);
+                        Gq[2 * h] = G2.x;
+                        Gq[2 * h + 1] = G2.y;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    dp[q] = __float_as_uint(Gq[q]);
+                    if (jv) I += jterm(Gq[q], th[q], p2);
+                }
+                if (k - r * ipr == ipr - 1) {                    // the row's last iteration
+                    I = warp_sum(I);
+                    if (lane == 0) rp[r].jt = I;
+                    I = 0;
+                }
+            }
+        }
+        __syncwarp();
+        if (MODE == 2 && a.px.exchange_rows) {                   // the block's J_v over all ranks
+            if (lane < nr) peer_row_send(a.px, 0, v0 + lane, rp[lane].jt, sc->xgen);
+            if (lane < nr) rp[lane].jt = peer_row_recv(a.px, 0, v0 + lane, sc->xgen, a.ds, rp[lane].jt);
+        }
+        if (nbufs == 2) stage_next();
+        if (lane < nr) {
+            BlkRow& R = rp[lane];
+            double c = 0.0;
+            if (mc.normalize && !R.guard) {
+                const double J = R.jvalid ? times_pow2((double)R.jt, -R.s) : 0.0;
+                c = J / (double)mc.Nnorm;
+                c = c * R.rho;
+                c = c * R.rho;
+            }
+            R.rhof = __double2float_rn(R.rho);
+            R.ncf = -__double2float_rn(c);
+        }
+        __syncwarp();
+
+        // ---- 3b: grad, AdamW, next-state statistics and sign planes (flat stream)
+        {
+            float* tb = a.theta + (size_t)v0 * N;
+            float* mb = a.m + (size_t)v0 * N;
+            float* vb = a.v + (size_t)v0 * N;
+            constexpr bool mag = MAG;
+            float4 thn = ld_last(tb + 4 * lane), mn4 = ld_last(mb + 4 * lane), vn4 = ld_last(vb + 4 * lane);
+            long long Qn = 0;
+            float mx = 0.0f;
+            for (int k = 0; k < total; ++k) {
+                const int r = k / ipr, n = (k - r * ipr) * 128 + 4 * lane;
+                const size_t e = (size_t)k * 128 + 4 * lane;     // flat element of the block
+                const float4 th4 = thn, m4 = mn4, v4 = vn4;
+                if (k + 1 < total) {
+                    thn = ld_last(tb + e + 128);
+                    mn4 = ld_last(mb + e + 128);
+                    vn4 = ld_last(vb + e + 128);
+                }
+                const float rhof = rp[r].rhof, ncf = rp[r].ncf;
+                const int v = v0 + r;
+                float th[4] = {th4.x, th4.y, th4.z, th4.w};
+                float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+                float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+                const uint32_t* dp = dpk + (size_t)r * dpkw + n + (n >> 5);
+                float gg[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) gg[q] = __fmaf_rn(__uint_as_float(dp[q]), rhof, jac_addend(ncf, th[q], mag));
+                unsigned pnib = 0, nnib = 0;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const float2 g2 = make_float2(gg[2 * h], gg[2 * h + 1]);
+                    const float2 m2 = mul2_unfused(make_float2(mm[2 * h], mm[2 * h + 1]), make_float2(mkeep, mkeep));
+                    const float2 v2 = make_float2(vv[2 * h], vv[2 * h + 1]);
+                    float2 x2 = mul2_unfused(make_float2(th[2 * h], th[2 * h + 1]), make_float2(wdf, wdf));
+                    const float2 mn2 = __ffma2_rn(make_float2(a1, a1), __fadd2_rn(g2, make_float2(-m2.x, -m2.y)), m2);
+                    const float2 vb2 = __fmul2_rn(v2, make_float2(b2f, b2f));
+                    const float2 vn2 = __ffma2_rn(__fmul2_rn(make_float2(a2, a2), g2), g2, vb2);
+                    const float2 sq2 = make_float2(__fsqrt_rn(vn2.x), __fsqrt_rn(vn2.y));
+                    const float2 den2 = __fadd2_rn(mul2_unfused(sq2, make_float2(rbc2, rbc2)), make_float2(epsf, epsf));
+                    const float2 num2 = __fmul2_rn(make_float2(nss, nss), mn2);
+                    x2 = __fadd2_rn(x2, make_float2(num2.x / den2.x, num2.y / den2.y));
+                    float xs0 = x2.x, xs1 = x2.y;
+                    if (mc.noise) {
+                        xs0 = xs0 + nz * noise_xi(mc.seed, mc.n0 + n + 2 * h, v, t);
+                        xs1 = xs1 + nz * noise_xi(mc.seed, mc.n0 + n + 2 * h + 1, v, t);
+                    }
+                    const float xs[2] = {xs0, xs1};
+                    const float2 q2 = __fmul2_rn(mag ? make_float2(fabsf(xs0), fabsf(xs1)) : make_float2(xs0, xs1),
+                                                 make_float2(4294967296.0f, 4294967296.0f));
+                    Qn += __float2ll_rn(q2.x) + __float2ll_rn(q2.y);
+#pragma unroll
+                    for (int f = 0; f < 2; ++f) {
+                        const int q = 2 * h + f;
+                        const float x = xs[f];
+                        th[q] = x;
+                        mm[q] = f ? mn2.y : mn2.x;
+                        vv[q] = f ? vn2.y : vn2.x;
+                        mx = fmaxf(mx, fabsf(x));
+                        pnib |= (x > 0.0f ? 1u : 0u) << q;
+                        nnib |= (x < 0.0f ? 1u : 0u) << q;
+                    }
+                }
+                st_stream(tb + e, make_float4(th[0], th[1], th[2], th[3]));
+                st_stream(mb + e, make_float4(mm[0], mm[1], mm[2], mm[3]));
+                st_stream(vb + e, make_float4(vv[0], vv[1], vv[2], vv[3]));
+                unsigned pw = pnib << (4 * (lane & 7)), nw = nnib << (4 * (lane & 7));
+#pragma unroll
+                for (int o = 1; o < 8; o <<= 1) {
+                    pw |= __shfl_xor_sync(0xffffffffu, pw, o);
+                    nw |= __shfl_xor_sync(0xffffffffu, nw, o);
+                }
+                if ((lane & 7) == 0) {
+                    pl[r * NW + (n >> 5)] = pw;
+                    pl[RB * NW + r * NW + (n >> 5)] = nw;
+                }
+                if (k - r * ipr == ipr - 1) {                    // the row's last iteration
+                    Qn = warp_sum(Qn);
+                    mx = warp_maxf(mx);
+                    if (lane == 0) { rp[r].qt = Qn; rp[r].m2 = mx; }
+                    Qn = 0;
+                    mx = 0.0f;
+                }
+            }
+        }
+        cp_async_wait_all();                                     // next block's records visible after this
+        __syncwarp();
+        if (MODE == 2 && a.px.exchange_rows) {
+            // the block's Q_{t+1,v} over all ranks: send now, finish after the next block's gather
+            if (lane < nr) {
+                peer_row_send(a.px, 1, v0 + lane, rp[lane].qt, sc->xgen);
+                rp[lane].pq = rp[lane].qt;
+                rp[lane].pm2 = rp[lane].m2;
+            }
+            pend_v0 = v0;
+            pend_nr = nr;
+        } else {
+            finish_block(v0, nr, pl, false);
+        }
+        __syncwarp();
+        item = item_next;
+    }
+    if (MODE == 2 && pend_v0 >= 0) {
+        if (lane < pend_nr) rp[lane].pq = peer_row_recv(a.px, 1, pend_v0 + lane, sc->xgen, a.ds, rp[lane].pq);
+        __syncwarp();
+        finish_block(pend_v0, pend_nr, pl0 + (size_t)((it + 1) & 1) * 2 * RB * NW, true);
+    }
+}
+
+cudaError_t configure_update_blk(StepArgs* a) {
+    const int N = a->N, KB = a->KB, RB = a->upd_RB;
+    int dev = 0, optin = 0, sms = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    a->num_sms = sms;
+    const int nbufs = upd_recbufs(KB);
+    const size_t gsb = upd_gs_bytes(KB, N), grb = blk_group_bytes(KB, N, RB, a->upd_blk_cap, nbufs);
+    const int max_threads = KB == 4 ? (a->peer ? TSAT_UPD_THREADS4P : TSAT_UPD_THREADS4) : TSAT_UPD_THREADS8;
+    long long ng = optin > (long long)gsb ? ((long long)optin - (long long)gsb) / (long long)grb : 0;
+    if (ng > max_threads / 32) ng = max_threads / 32;
+    if (ng < 1) return cudaErrorInvalidConfiguration;
+    if (std::getenv("TSAT_GEOM_VERBOSE"))
+        std::fprintf(stderr, "k_update_blk geometry: KB %d N %d RB %d groups %lld cap %d smem %zu\n", KB, N, RB, ng,
+                     a->upd_blk_cap, gsb + (size_t)ng * grb);
+    a->upd_mode = 0;
+    a->upd_chunk = N;
+    a->upd_gs_global = 0;
+    a->upd_recbufs = nbufs;
+    a->upd_GT = 32;
+    a->upd_NG = (int)ng;
+    a->upd_smem = gsb + (size_t)ng * grb;
+    a->upd_grid = sms;
+    if (const char* g = std::getenv("TSAT_UPD_GRID")) {
+        const int x = std::atoi(g);
+        if (x > 0 && x < sms) a->upd_grid = x;
+    }
+    const int smem = (int)a->upd_smem;
+    const cudaFuncAttribute attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    if (KB == 4) {
+        if ((e = cudaFuncSetAttribute(k_update_blk<4, 0, false>, attr, smem)) != cudaSuccess) return e;
+        if ((e = cudaFuncSetAttribute(k_update_blk<4, 2, false>, attr, smem)) != cudaSuccess) return e;
+        if ((e = cudaFuncSetAttribute(k_update_blk<4, 0, true>, attr, smem)) != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k_update_blk<4, 2, true>, attr, smem);
+    } else {
+        if ((e = cudaFuncSetAttribute(k_update_blk<8, 0, false>, attr, smem)) != cudaSuccess) return e;
+        if ((e = cudaFuncSetAttribute(k_update_blk<8, 2, false>, attr, smem)) != cudaSuccess) return e;
+        if ((e = cudaFuncSetAttribute(k_update_blk<8, 0, true>, attr, smem)) != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k_update_blk<8, 2, true>, attr, smem);
+    }
+    return e;
+}
+
+cudaError_t launch_update_blk(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
+                              cudaStream_t st) {
+    const bool mag = a.mc.normalize == 3;
+    const dim3 g(a.upd_grid), b(32 * a.upd_NG);
+    const size_t sm = a.upd_smem;
+    if (a.peer) {
+        if (a.KB == 4) mag ? k_update_blk<4, 2, true><<<g, b, sm, st>>>(a, Acur, Anext, sc)
+                           : k_update_blk<4, 2, false><<<g, b, sm, st>>>(a, Acur, Anext, sc);
+        else mag ? k_update_blk<8, 2, true><<<g, b, sm, st>>>(a, Acur, Anext, sc)
+                 : k_update_blk<8, 2, false><<<g, b, sm, st>>>(a, Acur, Anext, sc);
+        return cudaGetLastError();
+    }
+    if (a.KB == 4)
+        return mag ? launch_maybe_pdl(a.pdl, k_update_blk<4, 0, true>, g, b, sm, st, a, Acur, Anext, sc)
+                   : launch_maybe_pdl(a.pdl, k_update_blk<4, 0, false>, g, b, sm, st, a, Acur, Anext, sc);
+    return mag ? launch_maybe_pdl(a.pdl, k_update_blk<8, 0, true>, g, b, sm, st, a, Acur, Anext, sc)
+               : launch_maybe_pdl(a.pdl, k_update_blk<8, 0, false>, g, b, sm, st, a, Acur, Anext, sc);
+}
+
+}  // namespace tsat

@@ -21,12 +21,12 @@ cudaError_t launch_step_kernel(int which, const StepArgs& a, const StepScalars* 
         case 0: return launch_clause(a, Acur, sc_dev, st);
         case 1: return launch_gtable(a, sc_dev, st);
         case 2: return a.upd_mode == 0 ? launch_hub(a, Acur, st) : cudaGetLastError();
-        case 3: return launch_update(a, Acur, Anext, sc_dev, st);
+        case 3: return a.upd_RB > 1 ? launch_update_blk(a, Acur, Anext, sc_dev, st) : launch_update(a, Acur, Anext, sc_dev, st);
         case 4: return cudaGetLastError();
     }
     return cudaErrorInvalidValue;
 }
 
-cudaError_t configure_kernels(StepArgs* a) { return configure_update(a); }
+cudaError_t configure_kernels(StepArgs* a) { return a->upd_RB > 1 ? configure_update_blk(a) : configure_update(a); }
 
 }  // namespace tsat

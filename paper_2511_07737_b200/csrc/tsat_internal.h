@@ -177,6 +177,8 @@ struct StepArgs {
     int upd_GT, upd_NG, upd_grid;    // v2 launch geometry
     int upd_rec_cap;                 // record words a group stages per row (max over non-hub rows)
     int upd_recbufs;                 // record buffers per group (1 or 2, configure_update)
+    int upd_RB;                      // rows per work item: 1, or 32 / (N/32) for small shards (k_update_blk)
+    int upd_blk_cap;                 // record words a group stages per row block (max over blocks, non-hub rows)
     int pdl;                         // launch k_clause / k_gtable / k_update with programmatic
                                      // stream serialisation (PDL; fused W = 1 path without hubs)
     size_t upd_smem;
@@ -235,6 +237,12 @@ cudaError_t launch_update_a(const StepArgs& a, const uint32_t* Acur, const StepS
 cudaError_t launch_update_b(const StepArgs& a, const uint32_t* Acur, const StepScalars* sc, cudaStream_t st);
 cudaError_t launch_rows_partial(const StepArgs& a, const float* theta, unsigned int* thmax_bits, cudaStream_t st);
 cudaError_t launch_rows_finish(const StepArgs& a, uint32_t* Anext, cudaStream_t st);
+// row-block k_update (k_update_blk.cu): rows per work item for a shard of N candidates
+// (1: the per-row kernel), and the block kernel's geometry
+int update_block_rows(int N);
+cudaError_t configure_update_blk(StepArgs* a);
+cudaError_t launch_update_blk(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
+                              cudaStream_t st);
 // whether the fused k_update geometry fits (else: chunked split sequence)
 bool update_fits_fused(int KB, int N, int rec_cap, int optin);
 // peer path: exchange of Qbuf[0..V) row partials (init / set_state), gen = exchange generation

@@ -18,6 +18,6 @@ def test_reference_arm_json_line():
         assert k in line, k
     assert line["impl"] == "reference" and line["metric"] == "clause-candidate evals/sec"
     assert line["value"] > 0 and line["steps"] == 3 and line["higher_is_better"] is True
-    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] == 1
+    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["value"] == line["value"] and line["e2e"]["h2d_bytes_per_step"] == 0
     assert line["config"]["workload"].startswith("c1:")

@@ -178,6 +178,32 @@ def test_degenerate_and_shape_cases(case):
         assert s.get_info().best_unsat >= 1 and s.get_solution() is None
 
 
+@pytest.mark.parametrize("N", [128, 256, 384, 512])
+@pytest.mark.parametrize("kind", ["planted3", "industrial7"])
+def test_row_block_kernel(kind, N):
+    """Small shards (N < 1024, N % 128 == 0) run k_update_blk: a warp covers
+    RB = 32 / (N/32) rows (8, 4, 2, 2 here), gathers all of them at once and
+    streams the block's rows as one float4 stream.  V is not a multiple of RB
+    (ragged last block); industrial7 has hub rows inside blocks and the
+    batched-record layout (KB = 8).  k_clause splits its warps into
+    sub-groups of N/32 lanes at these sizes.  Bit-exact against the oracle."""
+    if kind == "planted3":
+        cnf = planted_ksat(1003, 4213, 3, 21)
+    else:
+        cnf = industrial_cnf(701, 2800, 22)
+    state = random_state(cnf.V, N, seed=17)
+    s, o = make_pair(cnf, N, 9, state=state, t0=0)
+    for _ in range(5):
+        compare_step(s, o, cnf, f"{kind} N={N}")
+    info = s.step(9)
+    for _ in range(9):
+        ref = o.step()
+    th, m, v, _ = s.get_state()
+    np.testing.assert_array_equal(th, o.theta)
+    np.testing.assert_array_equal(v, o.v)
+    assert (info.best_unsat, info.best_idx) == (ref.best_unsat, ref.best_idx)
+
+
 def test_lr_boundaries_and_restart():
     """Cross the t = 29/30 decay and the t = 359/360 restart (R9)."""
     cnf = planted_ksat(200, 840, 3, 6)

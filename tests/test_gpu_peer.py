@@ -38,7 +38,7 @@ def _peer_solver(rank, world, stream=None):
     return Solver(0, stream=stream, rank=rank, world=world, peer=True)
 
 
-@pytest.mark.parametrize("case", ["c1", "industrial7", "ragged3", "c1-per-shard"])
+@pytest.mark.parametrize("case", ["c1", "industrial7", "ragged3", "c1-per-shard", "blk128", "blk256-ind", "blk512"])
 def test_peer_w1_matches_oracle(case):
     """W = 1: the MODE 2 kernels exchanging with themselves reproduce the
     oracle bit for bit, step by step and through a multi-step graph."""
@@ -47,6 +47,12 @@ def test_peer_w1_matches_oracle(case):
         cnf, N = planted_ksat(20, 85, 3, 1), 64
     elif case == "industrial7":
         cnf, N = industrial_cnf(500, 2000, 4), 160
+    elif case == "blk128":           # row-block kernel (MODE 2): 8 rows per warp, ragged tail
+        cnf, N = planted_ksat(1003, 4213, 3, 5), 128
+    elif case == "blk256-ind":
+        cnf, N = industrial_cnf(701, 2800, 6), 256
+    elif case == "blk512":
+        cnf, N = planted_ksat(777, 3263, 3, 8), 512
     else:
         cnf, N = planted_ksat(333, 1400, 3, 3), 96
     s = _peer_solver(0, 1)
@@ -97,15 +103,15 @@ def _run_threads(fns):
         raise errs[0]
 
 
-@pytest.mark.parametrize("normalize", [1, 2, 3])
-def test_peer_two_ranks_one_gpu(normalize, monkeypatch):
+@pytest.mark.parametrize("normalize,N", [(1, 256), (2, 256), (3, 256), (1, 512), (1, 1024)])
+def test_peer_two_ranks_one_gpu(normalize, N, monkeypatch):
     """W = 2 in one process: two contexts on their own streams, stepped from two
     host threads; the rank-concatenated state equals the oracle's (1 shard
     for normalize = 1 and 3; per-shard oracle ranks for normalize = 2)."""
     import torch
     monkeypatch.setenv("TSAT_UPD_GRID", "70")        # both persistent kernels resident on one GPU
     cnf = planted_ksat(400, 1680, 3, 7)
-    N, W, seed = 256, 2, 11
+    W, seed = 2, 11              # N_l = N / 2: 128 and 256 run the row-block kernel, 512 the per-row one
     ocfg = O.Config(normalize=normalize)
     streams = [torch.cuda.Stream(0) for _ in range(W)]
     ss = [_peer_solver(r, W, stream=streams[r]) for r in range(W)]
