@@ -47,7 +47,7 @@ typedef enum {
     TSAT_OK = 0,
     TSAT_E_ARG = 1,          /* invalid argument (null pointer, bad size, N % 32 != 0, k < 1, ...) */
     TSAT_E_PARSE = 2,        /* malformed DIMACS (SPEC S:45 error list) */
-    TSAT_E_RANGE = 3,        /* instance/batch outside the supported range (e.g. clause length > 7) */
+    TSAT_E_RANGE = 3,        /* instance/batch outside the supported range (e.g. clause length > 15) */
     TSAT_E_STATE = 4,        /* call out of order (step before init, export before any step, ...) */
     TSAT_E_OOM = 5,          /* host or device allocation failed / workspace too small */
     TSAT_E_CUDA = 6,         /* CUDA error (context poisoned) */
@@ -78,6 +78,9 @@ typedef struct {
     int32_t reset_moments_on_restart;  /* 1 = re-create AdamW at each LR restart (t > 0, t % restart_every
                                           == 0): m = v = 0 and the bias-correction step restarts at 1
                                           (variant; 0 = paper default, R8) */
+    double  tau_final;       /* SmoothMin temperature annealing (variant f2, reading R29): > 0 -> within each LR
+                                cycle tau_t = tau * (tau_final / tau)^((t mod restart_every) / (restart_every - 1)),
+                                geometric from tau to tau_final; 0 = constant tau (paper default, R1) */
 } tsat_config;
 
 typedef struct {
@@ -165,7 +168,7 @@ tsat_status tsat_nccl_unique_id(void* out, size_t bytes);
  * 'p cnf V C', clauses as signed integers terminated by 0.  Duplicate
  * literals are removed, tautologies kept, empty clauses preserved.
  * Errors: malformed header, '-0', variable > V, non-integer token
- * -> TSAT_E_PARSE; clause length > 7 -> TSAT_E_RANGE.  Replaces any
+ * -> TSAT_E_PARSE; clause length > 15 -> TSAT_E_RANGE.  Replaces any
  * previously loaded CNF and invalidates the batch. */
 tsat_status tsat_load_dimacs(tsat_ctx ctx, const char* text, size_t len, tsat_cnf_info* info);
 
@@ -281,6 +284,44 @@ const char* tsat_error_string(tsat_ctx ctx);
 
 /* Release the context and everything the library owns (not the caller's workspace). */
 void tsat_destroy(tsat_ctx ctx);
+
+/* ---------------------------------------------------------------- CPU hand-off
+ * PAPER.md §4.2 l.277-287: once the best candidate satisfies > 99 % of the
+ * clauses, the k most confident literals of each exported candidate
+ * (tsat_export_best) initialise one CDCL instance per CPU thread; more
+ * candidates than threads: the ones with more satisfied clauses first.
+ * Host-only (no context, no GPU); the confident literals are assumed as the
+ * first decisions, so a seed that excludes every model ends with status 21
+ * (unsatisfiable under its assumptions) and the thread takes the next seed. */
+typedef struct {
+    int32_t status;          /* 10 = SAT (model written), 20 = UNSAT (the formula), 21 = UNSAT under the
+                                assumptions (tsat_cdcl_solve), 0 = unknown (limit reached) */
+    int32_t winner;          /* portfolio: index of the seed whose instance finished, -1 = the unseeded
+                                instance, -2 = none */
+    double  seconds;         /* wall time until the result (portfolio: since the call) */
+    int64_t conflicts, decisions, propagations;   /* of the finishing instance */
+    int32_t failed_seeds;    /* portfolio: seeded instances that were UNSAT under their assumptions */
+    int32_t threads;         /* portfolio: threads used */
+} tsat_cdcl_result;
+
+/* One CDCL run on a CNF (clause_ptr[C+1] int64 offsets into dimacs_lits, signed
+ * 1-based literals) under n_assumptions assumed literals.  conflict_limit <= 0:
+ * none.  seed 0: deterministic default heuristics; otherwise randomised initial
+ * activities and phases.  model_out (V bytes, 0/1, caller-owned, may be NULL)
+ * is written on SAT.  TSAT_E_ARG on malformed arrays (non-monotone offsets,
+ * literal 0 or |lit| > V); TSAT_E_OOM on allocation failure. */
+tsat_status tsat_cdcl_solve(int32_t V, int64_t C, const int64_t* clause_ptr, const int32_t* dimacs_lits,
+                            int32_t n_assumptions, const int32_t* assumptions, int64_t conflict_limit,
+                            uint64_t seed, uint8_t* model_out, tsat_cdcl_result* out);
+
+/* Portfolio of seeded CDCL instances on `threads` host threads: seeds is M x k
+ * signed DIMACS literals (the lits arrays of tsat_export_best, best candidate
+ * first; 0 entries are ignored), unseeded != 0 adds one instance without
+ * assumptions (started first).  Stops at the first SAT (model_out, V bytes)
+ * or UNSAT verdict, or after time_limit_s seconds (status 0). */
+tsat_status tsat_cdcl_portfolio(int32_t V, int64_t C, const int64_t* clause_ptr, const int32_t* dimacs_lits,
+                                int32_t M, int32_t k, const int32_t* seeds, int32_t threads, int32_t unseeded,
+                                double time_limit_s, uint8_t* model_out, tsat_cdcl_result* out);
 
 #ifdef __cplusplus
 }

@@ -178,6 +178,16 @@ def smoothmin(h, tau):
     return S, g, rmin
 
 
+def tau_at(t: int, cfg) -> float:
+    """SmoothMin temperature of iteration t (Eq. 4's tau).  The paper fixes
+    none (R1: constant tau).  Variant R29 (tau_final > 0): geometric from tau
+    at the start of each LR cycle to tau_final at its
+    last iteration: tau (tau_final / tau)^((t mod R) / (R - 1))."""
+    if cfg.tau_final > 0 and cfg.restart_every > 1:
+        return cfg.tau * math.pow(cfg.tau_final / cfg.tau, (t % cfg.restart_every) / (cfg.restart_every - 1))
+    return cfg.tau
+
+
 def smoothmin_direct(col, tau):
     c = np.ascontiguousarray(col, np.int32)
     return lib().or_smoothmin_direct(len(c), _p(c), tau)
@@ -231,6 +241,7 @@ class Config:
     noise_sigma: float = 0.0
     eps_norm: float = 1e-8
     reset_moments_on_restart: int = 0
+    tau_final: float = 0.0      # > 0: SmoothMin temperature annealed within each LR cycle (variant f2, R29)
 
 
 class LocalComm:
@@ -356,7 +367,7 @@ class Oracle:
         h = histogram(R, K)
         unsat = h[:, 0].copy()
         # Eq. 4 / Eq. 3
-        S, g, rmin = smoothmin(h, cfg.tau)
+        S, g, rmin = smoothmin(h, tau_at(t, cfg))
         g32 = g.astype(np.float32)                 # R26: rounded once to fp32
         Sall = self.comm.gather_f64(S)
         loss = -float(sum(float(x) for x in Sall))
@@ -420,7 +431,7 @@ def step_sampled(cnf, theta, m, v, t, rows, cfg: Config | None = None):
     h = np.empty((N, K + 1), np.int32)
     rowbuf = np.empty(N, np.uint8)
     L.or_hist_stream(cnf.C, _p(cnf.clause_ptr), _p(cnf.lits), N, K, _p(b), _p(h), _p(rowbuf))
-    S, g, rmin = smoothmin(h, cfg.tau)
+    S, g, rmin = smoothmin(h, tau_at(t, cfg))
     g32 = g.astype(np.float32)
     loss = -float(sum(float(x) for x in S))
     gmax = L.or_gmax(N, K, _p(g32), _p(rmin))

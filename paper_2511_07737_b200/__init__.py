@@ -16,11 +16,13 @@ from .binding import (  # noqa: F401
     Solver,
     StepInfo,
     TsatError,
+    cdcl_portfolio,
+    cdcl_solve,
     config_default,
     load_library,
     nccl_unique_id,
     parse_dimacs,
 )
 
-__all__ = ["Solver", "StepInfo", "TsatError", "config_default", "load_library", "nccl_unique_id",
+__all__ = ["Solver", "StepInfo", "TsatError", "cdcl_portfolio", "cdcl_solve", "config_default", "load_library", "nccl_unique_id",
            "parse_dimacs", "LIB_PATH"]

@@ -33,7 +33,8 @@ class tsat_config(ct.Structure):
     _fields_ = [("tau", ct.c_double), ("normalize", ct.c_int32), ("beta1", ct.c_double), ("beta2", ct.c_double),
                 ("eps", ct.c_double), ("weight_decay", ct.c_double), ("lr0", ct.c_double), ("lr_min", ct.c_double),
                 ("decay_factor", ct.c_double), ("decay_every", ct.c_int32), ("restart_every", ct.c_int32),
-                ("noise_sigma", ct.c_double), ("eps_norm", ct.c_double), ("reset_moments_on_restart", ct.c_int32)]
+                ("noise_sigma", ct.c_double), ("eps_norm", ct.c_double), ("reset_moments_on_restart", ct.c_int32),
+                ("tau_final", ct.c_double)]
 
 
 class tsat_cnf_info(ct.Structure):
@@ -45,6 +46,12 @@ class tsat_cnf_info(ct.Structure):
 class tsat_step_info(ct.Structure):
     _fields_ = [("t", ct.c_int64), ("best_unsat", ct.c_int32), ("best_idx", ct.c_int64), ("solved", ct.c_int32),
                 ("solved_step", ct.c_int64), ("solved_idx", ct.c_int64), ("loss", ct.c_double)]
+
+
+class tsat_cdcl_result(ct.Structure):
+    _fields_ = [("status", ct.c_int32), ("winner", ct.c_int32), ("seconds", ct.c_double), ("conflicts", ct.c_int64),
+                ("decisions", ct.c_int64), ("propagations", ct.c_int64), ("failed_seeds", ct.c_int32),
+                ("threads", ct.c_int32)]
 
 
 class tsat_partial(ct.Structure):
@@ -74,6 +81,10 @@ _SIGS = {
     "tsat_export_best": (ct.c_int, [P, ct.c_int32, ct.c_int32, ct.POINTER(tsat_partial)]),
     "tsat_export_k": (ct.c_int, [P, ct.c_int32, ct.POINTER(ct.c_int32)]),
     "tsat_merge_keys": (ct.c_int, [P, ct.c_size_t, ct.c_int32, P]),
+    "tsat_cdcl_solve": (ct.c_int, [ct.c_int32, ct.c_int64, P, P, ct.c_int32, P, ct.c_int64, ct.c_uint64, P,
+                                   ct.POINTER(tsat_cdcl_result)]),
+    "tsat_cdcl_portfolio": (ct.c_int, [ct.c_int32, ct.c_int64, P, P, ct.c_int32, ct.c_int32, P, ct.c_int32,
+                                       ct.c_int32, ct.c_double, P, ct.POINTER(tsat_cdcl_result)]),
     "tsat_export_model": (ct.c_int, [P, ct.c_int64, P]),
     "tsat_get_solution": (ct.c_int, [P, P, ct.POINTER(ct.c_int64), ct.POINTER(ct.c_int64)]),
     "tsat_get_state": (ct.c_int, [P, P, P, P, ct.c_size_t, ct.POINTER(ct.c_int64)]),
@@ -124,6 +135,38 @@ def parse_dimacs(text: bytes) -> tsat_cnf_info:
     if s:
         raise TsatError(s, "DIMACS rejected")
     return info
+
+
+def cdcl_solve(cnf, assumptions=(), conflict_limit: int = 0, seed: int = 0):
+    """tsat_cdcl_solve (host only): one CDCL run under assumed DIMACS literals.
+    Returns (result, model or None)."""
+    ptr = np.ascontiguousarray(cnf.clause_ptr, np.int64)
+    lits = np.ascontiguousarray(cnf.lits, np.int32)
+    a = np.ascontiguousarray(np.asarray(assumptions, np.int32).reshape(-1))
+    model = np.zeros(cnf.V, np.uint8)
+    res = tsat_cdcl_result()
+    st = load_library().tsat_cdcl_solve(cnf.V, cnf.C, _ptr(ptr), _ptr(lits), a.size, _ptr(a) if a.size else None,
+                                        int(conflict_limit), int(seed), _ptr(model), ct.byref(res))
+    if st:
+        raise TsatError(st, "tsat_cdcl_solve")
+    return res, (model if res.status == 10 else None)
+
+
+def cdcl_portfolio(cnf, seeds, threads: int, unseeded: bool = True, time_limit_s: float = 60.0):
+    """tsat_cdcl_portfolio (host only): seeds = M x k signed DIMACS literals
+    (tsat_export_best's lits, best candidate first).  Returns (result, model or None)."""
+    ptr = np.ascontiguousarray(cnf.clause_ptr, np.int64)
+    lits = np.ascontiguousarray(cnf.lits, np.int32)
+    sd = np.ascontiguousarray(np.asarray(seeds, np.int32))
+    M, k = (sd.shape if sd.ndim == 2 else (0, 0))
+    model = np.zeros(cnf.V, np.uint8)
+    res = tsat_cdcl_result()
+    st = load_library().tsat_cdcl_portfolio(cnf.V, cnf.C, _ptr(ptr), _ptr(lits), M, k, _ptr(sd) if sd.size else None,
+                                            int(threads), int(bool(unseeded)), float(time_limit_s), _ptr(model),
+                                            ct.byref(res))
+    if st:
+        raise TsatError(st, "tsat_cdcl_portfolio")
+    return res, (model if res.status == 10 else None)
 
 
 def nccl_unique_id() -> bytes:

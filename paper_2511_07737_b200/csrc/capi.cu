@@ -330,6 +330,13 @@ StepScalars step_scalars(const tsat_config& c, int64_t t) {
     s.rbc2 = (float)(1.0 / std::sqrt(bc2));
     s.epsf = (float)c.eps;
     s.nz = (float)(lr * c.noise_sigma);
+    // SmoothMin temperature of this iteration and its table E[d] = exp(-tau d)
+    // (host libm, R11); annealed within each LR cycle when tau_final > 0 (R29)
+    double tau = c.tau;
+    if (c.tau_final > 0 && c.restart_every > 1)
+        tau = c.tau * std::pow(c.tau_final / c.tau, (double)(t % c.restart_every) / (double)(c.restart_every - 1));
+    s.tau = tau;
+    for (int d = 0; d < 16; ++d) s.E[d] = std::exp(-tau * (double)d);
     return s;
 }
 
@@ -640,6 +647,7 @@ tsat_status tsat_config_default(tsat_config* out) {
     out->restart_every = 360;
     out->noise_sigma = 0.0;
     out->reset_moments_on_restart = 0;
+    out->tau_final = 0.0;
     out->eps_norm = 1e-8;
     return TSAT_OK;
 }
@@ -833,7 +841,7 @@ tsat_status tsat_workspace_bytes(tsat_ctx ctx, int64_t N_global, size_t* bytes) 
     if (N_global >= (1LL << 32)) return fail(ctx, TSAT_E_RANGE, "N_global >= 2^32");
     if ((int64_t)ctx->cnf.V * (N / 32) >= (1LL << 31))
         return fail(ctx, TSAT_E_RANGE, "V * N / 32 >= 2^31 (32-bit bit-plane offsets)");
-    int KB = ctx->cnf.K <= 3 ? 4 : 8;
+    int KB = bins_for_K(ctx->cnf.K);
     bool chunked = false;
     tsat_status s = batch_chunked(ctx, (int)N, KB, &chunked);
     if (s != TSAT_OK) return s;
@@ -855,7 +863,7 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
         if (ctx->peer && !ctx->peers_ready) return fail(ctx, TSAT_E_STATE, "peer context: call tsat_peer_open first");
         tsat_config c;
         if (cfg) c = *cfg; else tsat_config_default(&c);
-        if (!(c.tau > 0) || c.decay_every < 1 || c.restart_every < 1 || !(c.decay_factor > 0) || !(c.eps_norm > 0) ||
+        if (!(c.tau > 0) || !(c.tau_final >= 0) || c.decay_every < 1 || c.restart_every < 1 || !(c.decay_factor > 0) || !(c.eps_norm > 0) ||
             c.normalize < 0 || c.normalize > 3 || (c.reset_moments_on_restart & ~1))
             return fail(ctx, TSAT_E_ARG, "invalid config");
         drop_graphs(ctx);
@@ -863,7 +871,7 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
         ctx->N_global = N_global;
         ctx->N = (int)(N_global / ctx->world);
         ctx->n0 = (long long)ctx->rank * ctx->N;
-        ctx->KB = ctx->cnf.K <= 3 ? 4 : 8;
+        ctx->KB = bins_for_K(ctx->cnf.K);
         ctx->seed = seed;
         ctx->ws = (char*)ws;
         ctx->ws_bytes = bytes;
@@ -878,7 +886,7 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
         ctx->L = make_layout(ctx->cnf.V, ctx->N, ctx->KB, ctx->cnf.n_hubs, ctx->sharded || ctx->chunked, ctx->peer);
         MethodConsts& mc = ctx->mc;
         mc = MethodConsts{};
-        for (int d = 0; d < 8; ++d) mc.E[d] = std::exp(-c.tau * (double)d);
+        for (int d = 0; d < 16; ++d) mc.E[d] = std::exp(-c.tau * (double)d);
         mc.tau = c.tau;
         mc.eps_norm = c.eps_norm;
         mc.normalize = c.normalize;                 // 0 off, 1 global, 2 per shard, 3 global mean magnitude (R28)

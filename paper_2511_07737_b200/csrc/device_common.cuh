@@ -14,10 +14,17 @@ namespace tsat {
 // L2 cache policy for the bit-plane gathers (created once per kernel):
 // evict-last when both plane buffers fit comfortably in L2 (they are re-read
 // by every occurrence), evict-normal otherwise.
+#ifndef TSAT_PLANE_FRAC
+#define TSAT_PLANE_FRAC 0            // planes larger than L2: evict-last on this fraction of the lines (0: normal)
+#endif
 __device__ __forceinline__ unsigned long long plane_policy(bool keep) {
     unsigned long long pol;
     if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#if TSAT_PLANE_FRAC
+    else asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, %1;" : "=l"(pol) : "f"((float)TSAT_PLANE_FRAC / 100.0f));
+#else
     else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#endif
     return pol;
 }
 // Eq. 5 gradient addend (R27b): grad = fmaf(G, rho, addend) with addend = -c;
@@ -427,10 +434,12 @@ __device__ __forceinline__ void count_uni3(uint32_t (&cnt)[NCTR][B], RecFn rec, 
 // at a time, absent records start at the all-ones count KB - 1 = 2^NP - 1
 // (the derived bin, never counted), and each bin takes one carry-save sum4
 // and one counter update per batch.
-template <int NP, int NCTR, int B, typename RecFn>
+// R0: the counters hold bins R0 .. R0 + NCTR - 1 (KB = 16 counts its 15 bins
+// in two passes of at most 8, k_hub).
+template <int NP, int NCTR, int B, int R0 = 0, typename RecFn>
 __device__ __forceinline__ void count_batched(uint32_t (&cnt)[NCTR][B], RecFn rec, unsigned nwords, uint32_t own,
                                               const uint32_t* __restrict__ Acur, unsigned NW, unsigned w, unsigned long long pol) {
-    static_assert(NCTR == (1 << NP) - 1, "absent records rely on bin 2^NP - 1 being derived");
+    static_assert(R0 + NCTR <= (1 << NP) - 1, "absent records rely on bin 2^NP - 1 being derived (never counted)");
 #pragma unroll
     for (int r = 0; r < NCTR; ++r)
 #pragma unroll
@@ -469,7 +478,8 @@ __device__ __forceinline__ void count_batched(uint32_t (&cnt)[NCTR][B], RecFn re
 #pragma unroll
         for (int r = 0; r < NCTR; ++r) {
             uint32_t s0, s1, s2;
-            sum4(bs_eq<NP>(sp[0], r), bs_eq<NP>(sp[1], r), bs_eq<NP>(sp[2], r), bs_eq<NP>(sp[3], r), s0, s1, s2);
+            sum4(bs_eq<NP>(sp[0], R0 + r), bs_eq<NP>(sp[1], R0 + r), bs_eq<NP>(sp[2], R0 + r), bs_eq<NP>(sp[3], R0 + r),
+                 s0, s1, s2);
             vc_addc<B>(cnt[r], s0 ^ cm, s1 ^ cm, s2 ^ cm, cm);
         }
         p += 1 + 4 * J;

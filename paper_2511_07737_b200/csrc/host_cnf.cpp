@@ -294,7 +294,8 @@ int build_cnf(int32_t V, int64_t C, const int64_t* ptr, const int32_t* lits, Hos
     h.hub_of.assign((size_t)V, -1);
     for (int32_t v = 0; v < V; ++v) {
         const uint32_t staged = sptr[v + 1] - sptr[v];
-        bool hub = h.occ_pn[2 * v] > 127 || h.occ_pn[2 * v + 1] > 127 || (h.occ_ptr[v + 1] - h.occ_ptr[v]) > (uint32_t)kRecCap ||
+        // K > 7 (KB = 16): every row's 15 bins are counted by k_hub (int32)
+        bool hub = h.K > 7 || h.occ_pn[2 * v] > 127 || h.occ_pn[2 * v + 1] > 127 || (h.occ_ptr[v + 1] - h.occ_ptr[v]) > (uint32_t)kRecCap ||
                    staged > (uint32_t)kRecCap;
         if (!hub) {
             h.max_rec_words = std::max<int32_t>(h.max_rec_words, (int32_t)staged);

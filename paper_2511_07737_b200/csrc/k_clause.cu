@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(con
     const int sub = nsub > 1 ? lane / NW : 0;
     const int w = nsub > 1 ? lane - sub * NW : blockIdx.x * 32 + lane;
     const bool valid = w < NW && sub < nsub;
+    const int wl = nsub > 1 ? w : lane;                 // word within the CTA's 32-word block
     pdl_wait();
     pdl_trigger();
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(con
                     if (T[j]) {
                         const unsigned long long pk = T[j];
                         const unsigned long long wide = (pk & 0x3FFull) | ((pk & 0xFFC00ull) << 11) | ((pk & 0x3FF00000ull) << 22);
-                        atomicAdd(&shp[33 * w + j], wide);                // padded layout (w = lane without sub-groups)
+                        atomicAdd(&shp[33 * wl + j], wide);               // padded layout
                     }
             } else {
                 // two 32x32 transposes (bins 0-3, 4-6) give each candidate's
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(con
                     for (int j = 0; j < 32; ++j) {
                         const unsigned long long x = T[j];
                         if (!x) continue;
-                        const int o = 33 * w + j;
+                        const int o = 33 * wl + j;
                         if (blk == 0) {
                             const unsigned long long w0 = (x & 0xFFull) | ((x & 0xFF00ull) << 13) | ((x & 0xFF0000ull) << 26);
                             if (w0) atomicAdd(&shp[o], w0);
@@ -272,6 +273,78 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(con
     }
 }
 
+// K > 7 (KB = 16: long clauses such as at-least-one constraints):
+// R needs 4 bit-planes and 15 counted bins.  Lane = one 32-candidate word; a
+// warp evaluates chunks of 64 clauses one at a time (literal codes read through
+// L1, broadcast to the lanes), adds the one-hot masks [R = r] to 7-bit
+// vertical counters and, per chunk, extracts per-candidate counts with four
+// 32x32 transposes (4 bins as bytes each) into global int32 atomics.
+// Correctness-first: this layout is not tuned (no long-clause workload in BASELINE).
+__global__ void __launch_bounds__(256, 1) k_clause_wide(const uint32_t* __restrict__ A, int NW, int V,
+                                                      const uint32_t* __restrict__ cptr,
+                                                      const uint32_t* __restrict__ clit, long long C,
+                                                      int* __restrict__ hist, int N, DevScalars* __restrict__ ds,
+                                                      const StepScalars* __restrict__ sc) {
+    constexpr int KB = 16, NP = 4, CB = 7, kCHW = 64;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int w = blockIdx.x * 32 + lane;
+    const bool valid = w < NW;
+    pdl_wait();
+    pdl_trigger();
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+        const long long t = sc->t;
+        ds->best_key = ~0ull;
+        ds->gmax_bits = 0ull;
+        ds->row_counter = 0;
+        ds->thmax_bits[(t + 1) & 1] = 0u;
+        ds->loss_fx = 0;
+    }
+    const uint32_t* Aw = A + (valid ? w : 0);
+    const unsigned long long pol = plane_policy(planes_fit_l2(V, NW));
+    const long long nchunks = (C + kCHW - 1) / kCHW;
+    for (long long chunk = (long long)blockIdx.y * kWarps + warp; chunk < nchunks;
+         chunk += (long long)gridDim.y * kWarps) {
+        const long long c0 = chunk * kCHW, c1 = c0 + kCHW < C ? c0 + kCHW : C;
+        uint32_t cnt[KB - 1][CB];
+#pragma unroll
+        for (int r = 0; r < KB - 1; ++r)
+#pragma unroll
+            for (int b = 0; b < CB; ++b) cnt[r][b] = 0u;
+        for (long long c = c0; c < c1; ++c) {
+            const uint32_t b = __ldg(cptr + c), e = __ldg(cptr + c + 1);
+            uint32_t sp[NP] = {0u, 0u, 0u, 0u};
+            for (uint32_t i = b; i < e; ++i) {
+                const uint32_t code = __ldg(clit + i);
+                bs_add<NP>(sp, ld_plane(Aw + (size_t)(code >> 1) * NW, pol) ^ (0u - (code & 1u)));
+            }
+#pragma unroll
+            for (int r = 0; r < KB - 1; ++r) vc_inc<CB>(cnt[r], bs_eq<NP>(sp, r));
+        }
+        if (!valid) continue;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {                       // bins 4q .. 4q + 3 as bytes
+            uint32_t T[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int r = 4 * q + i / 8, bb = i % 8;
+                T[i] = (r < KB - 1 && bb < CB) ? cnt[r < KB - 1 ? r : 0][bb < CB ? bb : 0] : 0u;
+            }
+            transpose32(T);
+#pragma unroll 4
+            for (int j = 0; j < 32; ++j) {
+                const int n = 32 * w + j;
+                if (n >= N || !T[j]) continue;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int r = 4 * q + k;
+                    const int val = (int)((T[j] >> (8 * k)) & 0xffu);
+                    if (r < KB - 1 && val) atomicAdd(&hist[(size_t)n * KB + r], val);
+                }
+            }
+        }
+    }
+}
+
 __global__ void k_reset_accumulators(DevScalars* __restrict__ ds, const StepScalars* __restrict__ sc) {
     const long long t = sc->t;
     ds->best_key = ~0ull;
@@ -313,9 +386,18 @@ cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, const StepSca
     else if (K == 3)
         return launch_maybe_pdl(a.pdl, k_clause<4, 3>, grid, dim3(256), 0, st, Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist,
                                 a.N, uni, a.ds, sc, nsub);
-    else
+    else if (K <= 7)
         return launch_maybe_pdl(a.pdl, k_clause<8, 7>, grid, dim3(256), 0, st, Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist,
                                 a.N, (int)(uni && K == 7), a.ds, sc, nsub);
+    else {
+        const long long chunks_w = (a.C + 63) / 64;
+        long long gyw = ((long long)a.num_sms * 2 + nwb - 1) / nwb;
+        const long long need = (chunks_w + kWarps - 1) / kWarps;
+        if (gyw > need) gyw = need;
+        if (gyw < 1) gyw = 1;
+        return launch_maybe_pdl(a.pdl, k_clause_wide, dim3(nwb, (unsigned)gyw), dim3(256), 0, st, Acur, NW, a.V, a.cptr,
+                                a.clit, a.C, a.hist, a.N, a.ds, sc);
+    }
     return cudaGetLastError();
 }
 

@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(256) k_gtable(int* __restrict__ hist, int N, l
 #pragma unroll
             for (int r = 0; r < KB; ++r) {
                 if (r >= rmin && r <= K) {
-                    double e = mc.E[r - rmin];
+                    double e = sc->E[r - rmin];
                     den = den + (double)h[r] * e;
                     num = num + (double)((long long)r * h[r]) * e;
                 }
@@ -132,9 +132,9 @@ __global__ void __launch_bounds__(256) k_gtable(int* __restrict__ hist, int N, l
 #pragma unroll
             for (int r = 0; r < KB; ++r) {
                 if (r >= rmin && r <= K) {
-                    double wgt = mc.E[r - rmin] / den;
+                    double wgt = sc->E[r - rmin] / den;
                     double u = (double)r - s;
-                    g[r] = (float)(wgt * (1.0 - mc.tau * u));
+                    g[r] = (float)(wgt * (1.0 - sc->tau * u));
                     gm = fmax(gm, fabs((double)g[r]));
                 }
             }
@@ -403,7 +403,10 @@ cudaError_t launch_gtable(const StepArgs& a, const StepScalars* sc, cudaStream_t
     if (a.KB == 4)
         return launch_maybe_pdl(a.pdl, k_gtable<4>, dim3(blocks), dim3(256), 0, st, a.hist, a.N, a.C, a.mc, a.gtab, a.S,
                                 a.unsat, a.ds, a.sharded, a.lossp, sc, a.peer, a.px);
-    return launch_maybe_pdl(a.pdl, k_gtable<8>, dim3(blocks), dim3(256), 0, st, a.hist, a.N, a.C, a.mc, a.gtab, a.S,
+    if (a.KB == 8)
+        return launch_maybe_pdl(a.pdl, k_gtable<8>, dim3(blocks), dim3(256), 0, st, a.hist, a.N, a.C, a.mc, a.gtab, a.S,
+                                a.unsat, a.ds, a.sharded, a.lossp, sc, a.peer, a.px);
+    return launch_maybe_pdl(a.pdl, k_gtable<16>, dim3(blocks), dim3(256), 0, st, a.hist, a.N, a.C, a.mc, a.gtab, a.S,
                             a.unsat, a.ds, a.sharded, a.lossp, sc, a.peer, a.px);
 }
 
@@ -428,7 +431,8 @@ cudaError_t launch_export(const StepArgs& a, long long t_eval, const int* cols_d
         long long total = (long long)M * a.V;
         unsigned blocks = (unsigned)((total + 255) / 256);
         if (a.KB == 4) k_grad_cols<4><<<blocks, 256, 0, st>>>(a.V, a.N, Aeval, a.occ_ptr, a.occ_rec, a.gtab, cols_dev, M, a.mc.K, absG);
-        else k_grad_cols<8><<<blocks, 256, 0, st>>>(a.V, a.N, Aeval, a.occ_ptr, a.occ_rec, a.gtab, cols_dev, M, a.mc.K, absG);
+        else if (a.KB == 8) k_grad_cols<8><<<blocks, 256, 0, st>>>(a.V, a.N, Aeval, a.occ_ptr, a.occ_rec, a.gtab, cols_dev, M, a.mc.K, absG);
+        else k_grad_cols<16><<<blocks, 256, 0, st>>>(a.V, a.N, Aeval, a.occ_ptr, a.occ_rec, a.gtab, cols_dev, M, a.mc.K, absG);
         k_topk_cols<<<M, 1024, 0, st>>>(absG, a.V, k, out_v, out_g);
     }
     return cudaGetLastError();

@@ -43,7 +43,7 @@ template <int KB, int MODE, bool MAG = false>
 __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TSAT_UPD_THREADS4) : TSAT_UPD_THREADS8, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
                                                                     uint32_t* __restrict__ Anext,
                                                                     const StepScalars* __restrict__ sc) {
-    constexpr int NP = (KB == 4) ? 2 : 3;
+    constexpr int NP = (KB == 4) ? 2 : (KB == 8 ? 3 : 4);
     constexpr int NCTR = KB - 1;
     extern __shared__ __align__(16) unsigned char smem[];
     const int N = a.N, NW = N >> 5, GT = a.upd_GT;
@@ -117,7 +117,13 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
     auto finish_row = [&](int vr, long long Qg, const uint32_t* pw, float m2) {
         const bool dpos = !mc.normalize || Qg >= 0;
         const uint32_t* src = dpos ? pw : pw + NW;
-        for (int w = tg; w < NW; w += GT) Anext[(size_t)vr * NW + w] = src[w];
+        for (int w = tg; w < NW; w += GT) {
+#if TSAT_ANEXT_CS
+            __stcs(Anext + (size_t)vr * NW + w, src[w]);    // streaming: keep L2 for the current planes
+#else
+            Anext[(size_t)vr * NW + w] = src[w];
+#endif
+        }
         if (tg == 0) {
             double dn, rhon;
             unsigned char gn;
@@ -181,7 +187,8 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
         float* vrow = a.v + (size_t)v * N;
 
         // ---- 1+2: bit-sliced gather of the row's occurrences, transpose to bytes
-        if (hub < 0) {
+        // (KB = 16: every row is a hub row, counted by k_hub)
+        if constexpr (KB <= 8) if (hub < 0) {
             const unsigned nrec = re - rb;
             for (int wl = tg; wl < NWc; wl += GT) {
                 const int w = w0 + wl;
@@ -240,9 +247,12 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
         // ---- 3a: G (fp32 FMA chain over exact counts, R27) -> smem; J_v partial
         float* gout = MODE == 1 ? a.Gbuf + (size_t)v * N + n0c : nullptr;
         int* hubc = hubrow ? hubrow + n0c : nullptr;
-        long long I = hub >= 0
-            ? pass_fold<KB, true>(trow + n0c, dpk, dpkw, gs + n0c, hubc, ncand, N, GT, tg, dsum, jvalid, p2, gout)
-            : pass_fold<KB, false>(trow + n0c, dpk, dpkw, gs + n0c, hubc, ncand, N, GT, tg, dsum, jvalid, p2, gout);
+        long long I;
+        if (KB > 8 || hub >= 0)
+            I = pass_fold<KB, true>(trow + n0c, dpk, dpkw, gs + n0c, hubc, ncand, N, GT, tg, dsum, jvalid, p2, gout);
+        else
+            I = pass_fold<KB <= 8 ? KB : 8, false>(trow + n0c, dpk, dpkw, gs + n0c, hubc, ncand, N, GT, tg, dsum, jvalid,
+                                                   p2, gout);
         I = warp_sum(I);
         if (lane == 0) red[gw] = I;
         gsync(bar, GT);
@@ -387,12 +397,13 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
 #ifndef TSAT_HUB_MINB
 #define TSAT_HUB_MINB 16          // k_hub blocks (warps) per SM the kernel is compiled for (<= 128 registers)
 #endif
-template <int KB, bool BATCHED>
-__global__ void __launch_bounds__(32, TSAT_HUB_MINB) k_hub(StepArgs a, const uint32_t* __restrict__ Acur) {
-    constexpr int NP = (KB == 4) ? 2 : 3;
+// Bins R0 .. R0 + NB - 1 of one super-chunk (KB = 16 runs two passes of <= 8
+// bins over the same records so the counters stay within the register budget).
+template <int KB, bool BATCHED, int R0, int NB>
+__device__ __forceinline__ void hub_bins(const StepArgs& a, const uint32_t* __restrict__ Acur, int (&sh)[2][1024 + 32]) {
+    constexpr int NP = (KB == 4) ? 2 : (KB == 8 ? 3 : 4);
     constexpr int NCTR = KB - 1;
     constexpr int kHubCtr = BATCHED ? kHubCtrBatched : kHubCtrPlain;
-    __shared__ int sh[2][1024 + 32];
     const int lane = threadIdx.x;
     const int NW = a.N >> 5;
     const int w = blockIdx.y * 32 + lane;
@@ -401,25 +412,25 @@ __global__ void __launch_bounds__(32, TSAT_HUB_MINB) k_hub(StepArgs a, const uin
     const int v = sc.y;
     const uint32_t own = valid ? __ldg(Acur + (size_t)v * NW + w) : 0u;
     const unsigned long long pol = plane_policy(planes_fit_l2(a.V, NW));
-    uint32_t cnt[NCTR][kHubCtr];
+    uint32_t cnt[NB][kHubCtr];
     const uint32_t* recg = a.upd_rec + sc.z;             // the records k_update stages (plain or batched)
     auto recf = [&](unsigned i) { return __ldg(recg + i); };
-    if (BATCHED)
-        count_batched<NP, NCTR, kHubCtr>(cnt, recf, (unsigned)(sc.w - sc.z), own, Acur, (unsigned)NW,
-                                         valid ? (unsigned)w : 0u, pol);
+    if constexpr (BATCHED)
+        count_batched<NP, NB, kHubCtr, R0>(cnt, recf, (unsigned)(sc.w - sc.z), own, Acur, (unsigned)NW,
+                                           valid ? (unsigned)w : 0u, pol);
     else
-        count_occurrences<NP, NCTR, kHubCtr, false, true>(cnt, recf, (unsigned)(sc.w - sc.z), own, Acur, (unsigned)NW,
-                                                          valid ? (unsigned)w : 0u, pol);
+        count_occurrences<NP, NB, kHubCtr, false, true>(cnt, recf, (unsigned)(sc.w - sc.z), own, Acur, (unsigned)NW,
+                                                        valid ? (unsigned)w : 0u, pol);
     // two counters per transpose (16-bit fields, bits 11..15 = sign extension),
     // staged through shared memory two bins at a time so the atomics coalesce
     int* dst = a.hubD + (size_t)sc.x * NCTR * a.N;
 #pragma unroll
-    for (int r0 = 0; r0 < NCTR; r0 += 2) {
+    for (int r0 = 0; r0 < NB; r0 += 2) {
         uint32_t T[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
             const int r = r0 + i / 16, b = i % 16;
-            T[i] = (r < NCTR) ? cnt[r][b < kHubCtr ? b : kHubCtr - 1] : 0u;
+            T[i] = (r < NB) ? cnt[r][b < kHubCtr ? b : kHubCtr - 1] : 0u;
         }
         transpose32(T);
         __syncwarp();
@@ -429,14 +440,26 @@ __global__ void __launch_bounds__(32, TSAT_HUB_MINB) k_hub(StepArgs a, const uin
             sh[1][33 * lane + j] = (int)(short)(T[j] >> 16);
         }
         __syncwarp();
-        for (int rr = 0; rr < 2 && r0 + rr < NCTR; ++rr)
+        for (int rr = 0; rr < 2 && r0 + rr < NB; ++rr)
 #pragma unroll 4
             for (int k = 0; k < 32; ++k) {
                 const int nl = 32 * k + lane;                  // candidate within the block (coalesced)
                 const int n = blockIdx.y * 1024 + nl;
                 const int val = sh[rr][33 * k + lane];
-                if (n < a.N && val) atomicAdd(dst + (size_t)(r0 + rr) * a.N + n, val);
+                if (n < a.N && val) atomicAdd(dst + (size_t)(R0 + r0 + rr) * a.N + n, val);
             }
+        __syncwarp();
+    }
+}
+
+template <int KB, bool BATCHED>
+__global__ void __launch_bounds__(32, TSAT_HUB_MINB) k_hub(StepArgs a, const uint32_t* __restrict__ Acur) {
+    __shared__ int sh[2][1024 + 32];
+    if constexpr (KB <= 8) {
+        hub_bins<KB, BATCHED, 0, KB - 1>(a, Acur, sh);
+    } else {                          // KB = 16 (batched records only): bins 0-7, then 8-14
+        hub_bins<KB, true, 0, 8>(a, Acur, sh);
+        hub_bins<KB, true, 8, 7>(a, Acur, sh);
     }
 }
 
@@ -452,8 +475,19 @@ bool update_fits_fused(int KB, int N, int rec_cap, int optin) {
 }
 
 int update_chunk(int KB, int N) {
-    const int c = KB == 4 ? 4096 : 2048;
+    const int c = KB == 4 ? 4096 : (KB == 8 ? 2048 : 1024);
     return N < c ? N : c;
+}
+
+template <int KB>
+static cudaError_t set_update_attrs(int smem) {
+    const cudaFuncAttribute attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_update<KB, 0>, attr, smem)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_update<KB, 1>, attr, smem)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_update<KB, 2>, attr, smem)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_update<KB, 0, true>, attr, smem)) != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_update<KB, 2, true>, attr, smem);
 }
 
 cudaError_t configure_update(StepArgs* a) {
@@ -501,21 +535,9 @@ cudaError_t configure_update(StepArgs* a) {
         if (x > 0 && x < sms) a->upd_grid = x;
     }
     const int smem = (int)a->upd_smem;
-    const cudaFuncAttribute attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-    if (KB == 4) {
-        if ((e = cudaFuncSetAttribute(k_update<4, 0>, attr, smem)) != cudaSuccess) return e;
-        if ((e = cudaFuncSetAttribute(k_update<4, 1>, attr, smem)) != cudaSuccess) return e;
-        if ((e = cudaFuncSetAttribute(k_update<4, 2>, attr, smem)) != cudaSuccess) return e;
-        if ((e = cudaFuncSetAttribute(k_update<4, 0, true>, attr, smem)) != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k_update<4, 2, true>, attr, smem);
-    } else {
-        if ((e = cudaFuncSetAttribute(k_update<8, 0>, attr, smem)) != cudaSuccess) return e;
-        if ((e = cudaFuncSetAttribute(k_update<8, 1>, attr, smem)) != cudaSuccess) return e;
-        if ((e = cudaFuncSetAttribute(k_update<8, 2>, attr, smem)) != cudaSuccess) return e;
-        if ((e = cudaFuncSetAttribute(k_update<8, 0, true>, attr, smem)) != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k_update<8, 2, true>, attr, smem);
-    }
-    return e;
+    if (KB == 4) return set_update_attrs<4>(smem);
+    if (KB == 8) return set_update_attrs<8>(smem);
+    return set_update_attrs<16>(smem);
 }
 
 cudaError_t launch_hub(const StepArgs& a, const uint32_t* Acur, cudaStream_t st) {
@@ -526,31 +548,36 @@ cudaError_t launch_hub(const StepArgs& a, const uint32_t* Acur, cudaStream_t st)
     if (a.KB == 4) {
         if (bat) k_hub<4, true><<<grid, 32, 0, st>>>(a, Acur);
         else k_hub<4, false><<<grid, 32, 0, st>>>(a, Acur);
-    } else {
+    } else if (a.KB == 8) {
         if (bat) k_hub<8, true><<<grid, 32, 0, st>>>(a, Acur);
         else k_hub<8, false><<<grid, 32, 0, st>>>(a, Acur);
+    } else {
+        k_hub<16, true><<<grid, 32, 0, st>>>(a, Acur);
     }
     return cudaGetLastError();
+}
+
+template <int KB>
+static cudaError_t launch_update_kb(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
+                                   cudaStream_t st) {
+    const bool mag = a.mc.normalize == 3;
+    const dim3 g(a.upd_grid), b(a.upd_GT * a.upd_NG);
+    const size_t sm = a.upd_smem;
+    if (a.peer) {
+        if (mag) k_update<KB, 2, true><<<g, b, sm, st>>>(a, Acur, Anext, sc);
+        else k_update<KB, 2><<<g, b, sm, st>>>(a, Acur, Anext, sc);
+        return cudaGetLastError();
+    }
+    return mag ? launch_maybe_pdl(a.pdl, k_update<KB, 0, true>, g, b, sm, st, a, Acur, Anext, sc)
+               : launch_maybe_pdl(a.pdl, k_update<KB, 0>, g, b, sm, st, a, Acur, Anext, sc);
 }
 
 cudaError_t launch_update(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
                           cudaStream_t st) {
     if (a.V == 0) return cudaGetLastError();
-    const int threads = a.upd_GT * a.upd_NG;
-    const bool mag = a.mc.normalize == 3;
-    const dim3 g(a.upd_grid), b(threads);
-    const size_t sm = a.upd_smem;
-    if (a.peer) {
-        if (a.KB == 4) mag ? k_update<4, 2, true><<<g, b, sm, st>>>(a, Acur, Anext, sc) : k_update<4, 2><<<g, b, sm, st>>>(a, Acur, Anext, sc);
-        else mag ? k_update<8, 2, true><<<g, b, sm, st>>>(a, Acur, Anext, sc) : k_update<8, 2><<<g, b, sm, st>>>(a, Acur, Anext, sc);
-    } else if (a.KB == 4) {
-        return mag ? launch_maybe_pdl(a.pdl, k_update<4, 0, true>, g, b, sm, st, a, Acur, Anext, sc)
-                   : launch_maybe_pdl(a.pdl, k_update<4, 0>, g, b, sm, st, a, Acur, Anext, sc);
-    } else {
-        return mag ? launch_maybe_pdl(a.pdl, k_update<8, 0, true>, g, b, sm, st, a, Acur, Anext, sc)
-                   : launch_maybe_pdl(a.pdl, k_update<8, 0>, g, b, sm, st, a, Acur, Anext, sc);
-    }
-    return cudaGetLastError();
+    if (a.KB == 4) return launch_update_kb<4>(a, Acur, Anext, sc, st);
+    if (a.KB == 8) return launch_update_kb<8>(a, Acur, Anext, sc, st);
+    return launch_update_kb<16>(a, Acur, Anext, sc, st);
 }
 
 // Phase A of the sharded iteration (always the persistent kernel: the
@@ -559,7 +586,8 @@ cudaError_t launch_update_a(const StepArgs& a, const uint32_t* Acur, const StepS
     if (a.V == 0) return cudaGetLastError();
     const int threads = a.upd_GT * a.upd_NG;
     if (a.KB == 4) k_update<4, 1><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, nullptr, sc);
-    else k_update<8, 1><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, nullptr, sc);
+    else if (a.KB == 8) k_update<8, 1><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, nullptr, sc);
+    else k_update<16, 1><<<a.upd_grid, threads, a.upd_smem, st>>>(a, Acur, nullptr, sc);
     return cudaGetLastError();
 }
 

@@ -55,7 +55,7 @@ template <int KB, int MODE, bool MAG>
 __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TSAT_UPD_THREADS4) : TSAT_UPD_THREADS8, 1)
     k_update_blk(StepArgs a, const uint32_t* __restrict__ Acur, uint32_t* __restrict__ Anext,
                  const StepScalars* __restrict__ sc) {
-    constexpr int NP = (KB == 4) ? 2 : 3;
+    constexpr int NP = (KB == 4) ? 2 : (KB == 8 ? 3 : 4);
     constexpr int NCTR = KB - 1;
     constexpr int NDW = KB == 4 ? 1 : 2;
     constexpr int nbufs = upd_recbufs(KB);
@@ -135,7 +135,11 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
             const int r = idx / NW;
             const long long Qg = pending ? rp[r].pq : rp[r].qt;
             const bool dpos = !mc.normalize || Qg >= 0;
+#if TSAT_ANEXT_CS
+            __stcs(Anext + (size_t)v0 * NW + idx, dpos ? pl[idx] : pl[RB * NW + idx]);
+#else
             Anext[(size_t)v0 * NW + idx] = dpos ? pl[idx] : pl[RB * NW + idx];
+#endif
         }
         float m2 = 0.0f;
         if (lane < nr) {
@@ -189,8 +193,8 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
             R.p2 = p2;
         }
 
-        // ---- 1+2: gather (lane = row x word), transpose to bytes
-        if (gr < nr) {
+        // ---- 1+2: gather (lane = row x word), transpose to bytes (KB = 16: all rows are hubs)
+        if constexpr (KB <= 8) if (gr < nr) {
             const int v = v0 + gr;
             if (a.hub_of[v] < 0) {
                 unsigned roff = 0;
@@ -202,7 +206,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
                 uint32_t cnt[NCTR][kCtr];
                 if (uni3) {
                     const int2 pn = a.occ_pn[v];
-                    count_uni3<NCTR, kCtr, false>(cnt, recf, (unsigned)pn.y, (unsigned)pn.x, own, Acur, (unsigned)NW,
+                    count_uni3<NCTR, kCtr, TSAT_BLK_PIPE != 0>(cnt, recf, (unsigned)pn.y, (unsigned)pn.x, own, Acur, (unsigned)NW,
                                                   (unsigned)gw, pol);
                 } else {
                     count_batched<NP, NCTR, kCtr>(cnt, recf, a.upd_ptr[v + 1] - a.upd_ptr[v], own, Acur, (unsigned)NW,
@@ -259,7 +263,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
                 for (int q = 0; q < KB; ++q) g4[q] = *reinterpret_cast<const float4*>(gs + (size_t)q * N + n);
                 uint32_t* dp = dpk + (size_t)r * dpkw + n + (n >> 5);
                 float Gq[4];
-                if (hub >= 0) {
+                if (KB > 8 || hub >= 0) {
                     int* hubrow = a.hubD + (size_t)hub * NCTR * N;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
 #pragma unroll
                     for (int b = 0; b < KB - 1; ++b)
                         *reinterpret_cast<int4*>(hubrow + (size_t)b * N + n) = make_int4(0, 0, 0, 0);
-                } else {
+                } else if constexpr (KB <= 8) {
                     const float dsumf = (float)dsum;
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
@@ -427,6 +431,16 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
     }
 }
 
+template <int KB>
+static cudaError_t set_blk_attrs(int smem) {
+    const cudaFuncAttribute attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_update_blk<KB, 0, false>, attr, smem)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_update_blk<KB, 2, false>, attr, smem)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_update_blk<KB, 0, true>, attr, smem)) != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_update_blk<KB, 2, true>, attr, smem);
+}
+
 cudaError_t configure_update_blk(StepArgs* a) {
     const int N = a->N, KB = a->KB, RB = a->upd_RB;
     int dev = 0, optin = 0, sms = 0;
@@ -457,38 +471,32 @@ cudaError_t configure_update_blk(StepArgs* a) {
         if (x > 0 && x < sms) a->upd_grid = x;
     }
     const int smem = (int)a->upd_smem;
-    const cudaFuncAttribute attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-    if (KB == 4) {
-        if ((e = cudaFuncSetAttribute(k_update_blk<4, 0, false>, attr, smem)) != cudaSuccess) return e;
-        if ((e = cudaFuncSetAttribute(k_update_blk<4, 2, false>, attr, smem)) != cudaSuccess) return e;
-        if ((e = cudaFuncSetAttribute(k_update_blk<4, 0, true>, attr, smem)) != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k_update_blk<4, 2, true>, attr, smem);
-    } else {
-        if ((e = cudaFuncSetAttribute(k_update_blk<8, 0, false>, attr, smem)) != cudaSuccess) return e;
-        if ((e = cudaFuncSetAttribute(k_update_blk<8, 2, false>, attr, smem)) != cudaSuccess) return e;
-        if ((e = cudaFuncSetAttribute(k_update_blk<8, 0, true>, attr, smem)) != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k_update_blk<8, 2, true>, attr, smem);
-    }
-    return e;
+    if (KB == 4) return set_blk_attrs<4>(smem);
+    if (KB == 8) return set_blk_attrs<8>(smem);
+    return set_blk_attrs<16>(smem);
 }
 
-cudaError_t launch_update_blk(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
-                              cudaStream_t st) {
+template <int KB>
+static cudaError_t launch_blk_kb(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
+                                 cudaStream_t st) {
     const bool mag = a.mc.normalize == 3;
     const dim3 g(a.upd_grid), b(32 * a.upd_NG);
     const size_t sm = a.upd_smem;
     if (a.peer) {
-        if (a.KB == 4) mag ? k_update_blk<4, 2, true><<<g, b, sm, st>>>(a, Acur, Anext, sc)
-                           : k_update_blk<4, 2, false><<<g, b, sm, st>>>(a, Acur, Anext, sc);
-        else mag ? k_update_blk<8, 2, true><<<g, b, sm, st>>>(a, Acur, Anext, sc)
-                 : k_update_blk<8, 2, false><<<g, b, sm, st>>>(a, Acur, Anext, sc);
+        if (mag) k_update_blk<KB, 2, true><<<g, b, sm, st>>>(a, Acur, Anext, sc);
+        else k_update_blk<KB, 2, false><<<g, b, sm, st>>>(a, Acur, Anext, sc);
         return cudaGetLastError();
     }
-    if (a.KB == 4)
-        return mag ? launch_maybe_pdl(a.pdl, k_update_blk<4, 0, true>, g, b, sm, st, a, Acur, Anext, sc)
-                   : launch_maybe_pdl(a.pdl, k_update_blk<4, 0, false>, g, b, sm, st, a, Acur, Anext, sc);
-    return mag ? launch_maybe_pdl(a.pdl, k_update_blk<8, 0, true>, g, b, sm, st, a, Acur, Anext, sc)
-               : launch_maybe_pdl(a.pdl, k_update_blk<8, 0, false>, g, b, sm, st, a, Acur, Anext, sc);
+    return mag ? launch_maybe_pdl(a.pdl, k_update_blk<KB, 0, true>, g, b, sm, st, a, Acur, Anext, sc)
+               : launch_maybe_pdl(a.pdl, k_update_blk<KB, 0, false>, g, b, sm, st, a, Acur, Anext, sc);
+}
+
+cudaError_t launch_update_blk(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
+                              cudaStream_t st) {
+    if (a.V == 0) return cudaGetLastError();
+    if (a.KB == 4) return launch_blk_kb<4>(a, Acur, Anext, sc, st);
+    if (a.KB == 8) return launch_blk_kb<8>(a, Acur, Anext, sc, st);
+    return launch_blk_kb<16>(a, Acur, Anext, sc, st);
 }
 
 }  // namespace tsat

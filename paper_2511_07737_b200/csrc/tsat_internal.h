@@ -12,7 +12,7 @@
 namespace tsat {
 
 // ---------------------------------------------------------------- limits
-constexpr int kMaxK = 7;               // clause length supported by the kernels
+constexpr int kMaxK = 15;              // clause length supported by the kernels (K > 7: KB = 16)
 constexpr int kMaxStepsPerCall = 4096;
 constexpr int kTopkMax = 2048;         // export: k most confident variables per candidate
 constexpr int kRecCap = 512;           // occurrence-record words a warp group stages per row (longer rows: hubs)
@@ -110,6 +110,8 @@ struct StepScalars {
     float mkeep;      // 0 at a moment reset (m *= 0; b2f = 0 zeroes v), else 1
     unsigned xgen;    // peer path: exchange generation of this iteration
     int pad;
+    double tau;       // SmoothMin temperature of this iteration (R1; annealed: R29)
+    double E[16];     // exp(-tau d), d = 0..15 (host libm, R11)
 };
 
 // Device-resident scalars (one struct in the workspace).
@@ -132,9 +134,13 @@ struct DevScalars {
     unsigned int xerr;               // peer path: an exchange timed out (step result invalid)
 };
 
+// Histogram bins per candidate for an instance of max clause length K: R in
+// 0..KB-1 (KB = 4: 2-bit R, K <= 3; 8: 3-bit, K <= 7; 16: 4-bit, K <= 15).
+inline int bins_for_K(int K) { return K <= 3 ? 4 : (K <= 7 ? 8 : 16); }
+
 // Method constants passed by value to kernels.
 struct MethodConsts {
-    double E[8];        // exp(-tau d), d = 0..7 (host libm)
+    double E[16];       // exp(-tau d), d = 0..15 (host libm)
     double tau;
     double eps_norm;
     int normalize;

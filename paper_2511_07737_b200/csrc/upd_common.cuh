@@ -24,6 +24,12 @@ constexpr int kUnroll3b = TSAT_3B_UNROLL;
 #define TSAT_UPD_THREADS4 768       // KB = 4 block size bound (register budget)
 #endif
 
+#ifndef TSAT_ANEXT_CS
+#define TSAT_ANEXT_CS 1            // next-state bit planes stored streaming (c3: k_update -2 %)
+#endif
+#ifndef TSAT_BLK_PIPE
+#define TSAT_BLK_PIPE 0
+#endif
 #ifndef TSAT_HINTS
 #define TSAT_HINTS 1
 #endif

@@ -99,9 +99,12 @@ def test_parse_errors(text):
 
 
 def test_parse_clause_length_limit():
+    """K <= 15 is supported (KB = 16 bins); longer clauses are TSAT_E_RANGE."""
     from paper_2511_07737_b200 import TsatError
+    info = _parse("p cnf 15 1\n" + " ".join(str(i) for i in range(1, 16)) + " 0\n")
+    assert info.K == 15
     with pytest.raises(TsatError) as ei:
-        _parse("p cnf 8 1\n1 2 3 4 5 6 7 8 0\n")
+        _parse("p cnf 16 1\n" + " ".join(str(i) for i in range(1, 17)) + " 0\n")
     assert ei.value.name == "TSAT_E_RANGE"
 
 

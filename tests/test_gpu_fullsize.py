@@ -40,7 +40,7 @@ def test_full_size_sampled_parity(name):
     del th, m, v
     np.testing.assert_array_equal(s.query_unsat(), unsat)
     K = O.binary_problem_matrix(cnf).K
-    KB = 4 if K <= 3 else 8
+    KB = 4 if K <= 3 else (8 if K <= 7 else 16)
     g = s.debug(1, np.float32, (KB, N))
     np.testing.assert_array_equal(g[:K + 1].T, g32)
     np.testing.assert_array_equal(s.debug(2, np.float64, (N,)), S)

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from tsat_synth import Cnf, enumeration_theta, fig1_cnf, industrial_cnf, make_config, planted_ksat, random_state
+from tsat_synth import Cnf, coloring_cnf, enumeration_theta, fig1_cnf, industrial_cnf, make_config, planted_ksat, random_state
 
 pytestmark = pytest.mark.gpu
 
@@ -47,7 +47,7 @@ def make_pair(cnf, N, seed, cfg=None, state=None, t0=0, sharded=False):
     c = config_default()
     ocfg = cfg or O.Config()
     for f in ("tau", "normalize", "beta1", "beta2", "eps", "weight_decay", "lr0", "lr_min", "decay_factor",
-              "decay_every", "restart_every", "noise_sigma", "eps_norm", "reset_moments_on_restart"):
+              "decay_every", "restart_every", "noise_sigma", "eps_norm", "reset_moments_on_restart", "tau_final"):
         setattr(c, f, getattr(ocfg, f))
     s.init_batch(N, seed, c)
     o = O.Oracle(cnf, N, seed, cfg=ocfg)
@@ -61,7 +61,7 @@ def compare_step(s, o, cnf, what=""):
     info = s.step(1)
     ref = o.step()
     K = o.K
-    KB = 4 if K <= 3 else 8
+    KB = 4 if K <= 3 else (8 if K <= 7 else 16)
     N = ref.unsat.shape[0]
     unsat = s.query_unsat()
     np.testing.assert_array_equal(unsat, ref.unsat, err_msg=f"unsat {what} t={ref.t}")
@@ -204,6 +204,41 @@ def test_row_block_kernel(kind, N):
     assert (info.best_unsat, info.best_idx) == (ref.best_unsat, ref.best_idx)
 
 
+@pytest.mark.parametrize("case", ["planted15_blk", "color15", "color9_mixed", "planted12_w1024", "color15_chunked"])
+def test_long_clauses_k_gt_7(case):
+    """clauses longer than 7 (KB = 16: 4-bit R, 15 counted bins,
+    every row counted by k_hub in two 8-bin passes, k_clause_wide).  Planted
+    15-SAT through the row-block kernel (N = 128), graph 15- and 9-colouring
+    (at-least-one clauses of length 15 / 9 plus binary clauses; the shape of
+    PAPER.md Table 1's 6g_6color) through the per-row kernel, a 1024-candidate
+    batch, and the chunked large-batch sequence (g table 16 x 4 B x N > smem)."""
+    if case == "planted15_blk":
+        cnf, N = planted_ksat(301, 260, 15, 3), 128
+    elif case == "color15":
+        cnf, N = coloring_cnf(40, 15, 3, 1), 96
+    elif case == "color9_mixed":
+        base = coloring_cnf(30, 9, 4, 2).clauses() + planted_ksat(270, 300, 3, 4).clauses()
+        cnf, N = Cnf.from_clauses(270, base), 160
+    elif case == "planted12_w1024":
+        cnf, N = planted_ksat(200, 180, 12, 5), 1024
+    else:
+        cnf, N = coloring_cnf(12, 15, 3, 3), 4096
+    assert cnf.K > 7
+    state = random_state(cnf.V, N, seed=19)
+    s, o = make_pair(cnf, N, 3, state=state, t0=0)
+    for _ in range(5):
+        compare_step(s, o, cnf, case)
+    if cnf.sigma is not None:                  # the planted model is a model (zero unsat on both sides)
+        V = cnf.V
+        th = np.where(cnf.sigma[:, None] > 0, 1.0, -1.0).astype(np.float32) * np.ones((V, N), np.float32)
+        th[:, 1::2] *= -1.0                    # mean 0: guard active, d = +eps, bits = sign(theta)
+        z = np.zeros_like(th)
+        s.set_state(th, z, z, 0)
+        o.set_state(th, z, z, 0)
+        info, ref = compare_step(s, o, cnf, case + " planted model")
+        assert ref.unsat[0] == 0 and info.best_unsat == 0
+
+
 def test_lr_boundaries_and_restart():
     """Cross the t = 29/30 decay and the t = 359/360 restart (R9)."""
     cnf = planted_ksat(200, 840, 3, 6)
@@ -218,7 +253,7 @@ def test_lr_boundaries_and_restart():
 @pytest.mark.parametrize("variant", [dict(normalize=0), dict(normalize=3), dict(weight_decay=0.0), dict(tau=5.0), dict(tau=0.5),
                                      dict(noise_sigma=0.3),
                                      dict(reset_moments_on_restart=1, restart_every=3, decay_every=2),
-                                     dict(normalize=2)])
+                                     dict(normalize=2), dict(tau=0.5, tau_final=8.0, restart_every=7, decay_every=3)])
 def test_variants(variant):
     cnf = planted_ksat(150, 630, 3, 8)
     cfg = O.Config(**variant)

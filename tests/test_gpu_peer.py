@@ -22,7 +22,7 @@ def _cfg(ocfg):
     from paper_2511_07737_b200 import config_default
     c = config_default()
     for f in ("tau", "normalize", "beta1", "beta2", "eps", "weight_decay", "lr0", "lr_min", "decay_factor",
-              "decay_every", "restart_every", "noise_sigma", "eps_norm", "reset_moments_on_restart"):
+              "decay_every", "restart_every", "noise_sigma", "eps_norm", "reset_moments_on_restart", "tau_final"):
         setattr(c, f, getattr(ocfg, f))
     return c
 
@@ -38,7 +38,7 @@ def _peer_solver(rank, world, stream=None):
     return Solver(0, stream=stream, rank=rank, world=world, peer=True)
 
 
-@pytest.mark.parametrize("case", ["c1", "industrial7", "ragged3", "c1-per-shard", "blk128", "blk256-ind", "blk512"])
+@pytest.mark.parametrize("case", ["c1", "industrial7", "ragged3", "c1-per-shard", "blk128", "blk256-ind", "blk512", "k15-256"])
 def test_peer_w1_matches_oracle(case):
     """W = 1: the MODE 2 kernels exchanging with themselves reproduce the
     oracle bit for bit, step by step and through a multi-step graph."""
@@ -51,6 +51,9 @@ def test_peer_w1_matches_oracle(case):
         cnf, N = planted_ksat(1003, 4213, 3, 5), 128
     elif case == "blk256-ind":
         cnf, N = industrial_cnf(701, 2800, 6), 256
+    elif case == "k15-256":          # KB = 16 (all rows k_hub) through the peer row-block kernel
+        from tsat_synth import coloring_cnf
+        cnf, N = coloring_cnf(30, 15, 3, 4), 256
     elif case == "blk512":
         cnf, N = planted_ksat(777, 3263, 3, 8), 512
     else:
@@ -63,7 +66,7 @@ def test_peer_w1_matches_oracle(case):
     th, m, v, _ = s.get_state()
     np.testing.assert_array_equal(th, o.theta)
     K = o.K
-    KB = 4 if K <= 3 else 8
+    KB = 4 if K <= 3 else (8 if K <= 7 else 16)
     for _ in range(12):
         info = s.step(1)
         ref = o.step()

@@ -111,6 +111,22 @@ def test_clause_eval_brute_force_small(V, C, seed):
         assert s.unsat[n] == sum(1 for r in _direct_eval(cnf, a) if r == 0)
 
 
+@pytest.mark.parametrize("V,C,k,seed", [(12, 20, 9, 1), (16, 12, 12, 2), (15, 4, 15, 3)])
+def test_clause_eval_brute_force_long_clauses(V, C, k, seed):
+    """SURVEY f3 (K > 7, R in 0..15): every assignment's R and unsat count
+    equal direct clause-by-clause evaluation."""
+    cnf = planted_ksat(V, C, k, seed)
+    th = enumeration_theta(V)
+    o = O.Oracle(cnf, 1 << V, seed=0, init=False)
+    o.set_state(th, np.zeros_like(th), np.zeros_like(th), 0)
+    s = o.step()
+    assert s.h.shape[1] == k + 1
+    for n in range(0, 1 << V, 97):
+        a = [(n >> v) & 1 for v in range(V)]
+        assert s.R[:, n].tolist() == _direct_eval(cnf, a)
+        assert s.unsat[n] == sum(1 for r in _direct_eval(cnf, a) if r == 0)
+
+
 def test_enumeration_batch_v20():
     """north_star: brute-force enumeration of all 2^20 assignments of a planted
     20-variable instance (config c1 shape).  Unsat counts from the oracle equal
@@ -279,13 +295,24 @@ def _G_from_g64(cnf, R, g):
 
 
 @pytest.mark.parametrize("seed,tau,normalize", [(1, 1.0, 1), (2, 0.5, 1), (3, 5.0, 1), (4, 1.0, 0), (5, 2.0, 1),
-                                                (6, 1.0, 3), (7, 2.0, 3)])
+                                                (6, 1.0, 3), (7, 2.0, 3), (8, 1.0, 1), (9, 0.5, 1)])
 def test_gradient_matches_torch_autograd(seed, tau, normalize):
     """STE backward + Eq. 5 Jacobian
-    against torch autograd of the dense formulation, fp64."""
+    against torch autograd of the dense formulation, fp64.  Seeds 8 and 9 use
+    long clauses (K = 12 and a 2..15 mix: SURVEY f3)."""
     rng = np.random.default_rng(seed)
     V, C, N = 10, 40, 24
-    cnf = planted_ksat(V, C, 3, seed) if seed % 2 else industrial_cnf(V, C, seed)
+    if seed == 8:
+        V, C = 16, 30
+        cnf = planted_ksat(V, C, 12, seed)
+    elif seed == 9:
+        V = 24
+        cl = planted_ksat(V, 8, 15, seed).clauses() + planted_ksat(V, 10, 9, seed).clauses()
+        cl += planted_ksat(V, 30, 3, seed).clauses() + planted_ksat(V, 10, 2, seed).clauses()
+        from tsat_synth import Cnf
+        cnf = Cnf.from_clauses(V, cl)
+    else:
+        cnf = planted_ksat(V, C, 3, seed) if seed % 2 else industrial_cnf(V, C, seed)
     theta = (np.round(rng.standard_normal((V, N)) * 2 ** 16) / 2 ** 16).astype(np.float32)
     theta[:, 0] += 0.2                           # keep |mu| away from the guard
     cfg = O.Config(tau=tau, normalize=normalize)

@@ -301,3 +301,29 @@ def test_openmp_build_equals_single_thread():
     b = O.step_sampled(cnf, ref.theta, ref.m, ref.v, 4, rows)
     for x, y in zip(a, b):
         np.testing.assert_array_equal(np.asarray(x), np.asarray(y))
+
+
+def test_tau_annealing_schedule():
+    """Variant R29 (tau annealing): within each LR cycle tau_t goes
+    geometrically from tau (t mod R = 0) to tau_final (t mod R = R - 1), with a
+    constant ratio between consecutive iterations, and restarts with the LR
+    (PAPER.md l.255-258); tau_final = 0 keeps Eq. 4's tau constant (R1)."""
+    cfg = O.Config(tau=0.5, tau_final=8.0, restart_every=360)
+    taus = np.array([O.tau_at(t, cfg) for t in range(720)])
+    assert taus[0] == 0.5 and abs(taus[359] - 8.0) <= 1e-14 * 8.0
+    assert np.array_equal(taus[:360], taus[360:])
+    ratio = taus[1:360] / taus[:359]
+    assert np.allclose(ratio, 16.0 ** (1 / 359), rtol=1e-13, atol=0)
+    assert all(O.tau_at(t, O.Config(tau=2.0)) == 2.0 for t in range(0, 1000, 37))
+    # the step uses the iteration's tau: one annealed step equals a constant-tau
+    # step at that temperature
+    from tsat_synth import planted_ksat
+    cnf = planted_ksat(30, 120, 3, 4)
+    o1 = O.Oracle(cnf, 32, 5, cfg=O.Config(tau=0.5, tau_final=8.0, restart_every=10))
+    for _ in range(4):
+        o1.step()
+    t = o1.t
+    o2 = O.Oracle(cnf, 32, 5, cfg=O.Config(tau=O.tau_at(t, o1.cfg), restart_every=10))
+    o2.set_state(o1.theta, o1.m, o1.v, t)
+    a, b = o1.step(), o2.step()
+    assert np.array_equal(a.g32, b.g32) and np.array_equal(o1.theta, o2.theta)

@@ -17,6 +17,11 @@ Workload recipes:
   proportional to rank^-0.82 (scale-free structure the paper cites for
   industrial instances, PAPER.md §4.2 l.292) under a random id permutation;
   k distinct variables per clause; signs planted as above.
+* ``coloring_cnf``   - planted graph k-colouring (the shape of PAPER.md Table 1's
+  ``6g_6color`` family, l.345): variables x_{u,c}; one at-least-one clause of
+  length k per node (long clauses: k up to 15), at-most-one pairs
+  (-x_{u,c} v -x_{u,d}) and edge conflicts (-x_{u,c} v -x_{w,c}) over a random
+  graph properly coloured by a hidden colouring.
 * ``fig1_cnf``       - the 4-variable / 5-clause example of PAPER.md Fig. 1/2
   (§3.1, l.45-53, l.84-95) in SPEC.md's reconstruction.
 * ``enumeration_theta`` - theta = +-1 from the bits of the candidate index, so
@@ -31,6 +36,7 @@ __all__ = [
     "planted_ksat",
     "industrial_cnf",
     "fig1_cnf",
+    "coloring_cnf",
     "to_dimacs",
     "enumeration_theta",
     "random_state",
@@ -166,6 +172,29 @@ def industrial_cnf(V: int, C: int, seed: int = 1, alpha: float = 0.82,
     ptr = np.zeros(C + 1, dtype=np.int64)
     np.cumsum(lens, out=ptr[1:])
     return Cnf(V, ptr, lits2[mask], sigma, f"industrial-V{V}-C{C}-s{seed}")
+
+
+def coloring_cnf(nodes: int, colors: int, degree: int = 4, seed: int = 1) -> Cnf:
+    """Planted graph colouring CNF: clause lengths 2 and `colors` (K = colors)."""
+    rng = np.random.default_rng([0xC010, int(seed), int(nodes), int(colors), int(degree)])
+    col = rng.integers(0, colors, size=nodes)
+    var = lambda u, c: int(u) * colors + int(c) + 1
+    cl = [[var(u, c) for c in range(colors)] for u in range(nodes)]            # at least one colour
+    for u in range(nodes):                                                      # at most one colour
+        for c in range(colors):
+            for d in range(c + 1, colors):
+                cl.append([-var(u, c), -var(u, d)])
+    m = nodes * degree // 2
+    a, b = rng.integers(0, nodes, size=m), rng.integers(0, nodes, size=m)
+    for u, w in zip(a, b):
+        if u != w and col[u] != col[w]:                                         # edges the hidden colouring respects
+            for c in range(colors):
+                cl.append([-var(u, c), -var(w, c)])
+    sigma = np.zeros(nodes * colors, dtype=np.uint8)
+    sigma[np.arange(nodes) * colors + col] = 1
+    cnf = Cnf.from_clauses(nodes * colors, cl, name=f"color{colors}-n{nodes}-d{degree}-s{seed}")
+    cnf.sigma = sigma
+    return cnf
 
 
 def fig1_cnf() -> Cnf:
