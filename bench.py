@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--tts-max-steps", type=int, default=3600)
     ap.add_argument("--tts-only", action="store_true", help="run only the time-to-SAT protocol and print it")
     ap.add_argument("--n-per-gpu", type=int, default=0, help="override the config's candidates per GPU (exploration)")
+    ap.add_argument("--clause-eval", type=int, default=0, help="1: dense tensor-core clause evaluation (f4 experiment)")
+    ap.add_argument("--hybrid-only", type=str, default="", help="V,seed[,N]: run only the GPU->CDCL hybrid time-to-SAT")
     return ap.parse_args()
 
 
@@ -178,10 +180,84 @@ def time_to_sat(name, seeds, max_steps, local, stream, chunk=30):
     return out
 
 
+def hybrid_tts(cnf, N, seed, local, stream, threads, max_steps=3600, cdcl_limit_s=60.0, norms=(3, 1, 0)):
+    """SURVEY f1 / PAPER.md §4.2 l.277-287: GPU gradient phase until the best
+    candidate satisfies > 99 % of the clauses (or a model appears, or
+    max_steps), then tsat_export_best (the best `threads` candidates, the
+    paper's k = max(ceil(V/10^4), 20) most confident literals each) seeds a
+    portfolio of CDCL instances on the host threads (plus one unseeded).
+    Compared with the same CDCL run unseeded from scratch.  Wall-clock
+    seconds, models verified on the host."""
+    import torch
+    from paper_2511_07737_b200 import Solver, cdcl_portfolio, cdcl_solve, config_default
+    lits = np.asarray(cnf.lits)
+    var = np.abs(lits) - 1
+
+    def verify(m):
+        val = np.where(lits > 0, m[var], 1 - m[var])
+        return bool((np.add.reduceat(val, cnf.clause_ptr[:-1]) > 0).all())
+
+    out = {"instance": f"V={cnf.V} C={cnf.C} (planted 3-SAT, seed {seed})", "N": N, "cdcl_threads": threads,
+           "gate": "best candidate satisfies > 99% of clauses (PAPER.md l.279)"}
+    t0 = time.perf_counter()
+    r, m = cdcl_solve(cnf, conflict_limit=0, seed=0) if cdcl_limit_s <= 0 else \
+        cdcl_portfolio(cnf, np.zeros((0, 0), np.int32), threads=1, unseeded=True, time_limit_s=cdcl_limit_s)
+    out["cdcl_only"] = {"status": {10: "SAT", 20: "UNSAT", 0: "timeout"}[r.status], "seconds": time.perf_counter() - t0,
+                        "conflicts": r.conflicts, "verified": verify(m) if m is not None else None,
+                        "time_limit_s": cdcl_limit_s, "threads": 1}
+    # the same thread count as the hybrid, no GPU seeds: a diversified portfolio
+    # (randomised heuristics per instance, empty assumptions)
+    t0 = time.perf_counter()
+    r, m = cdcl_portfolio(cnf, np.zeros((threads, 1), np.int32), threads=threads, unseeded=True,
+                          time_limit_s=cdcl_limit_s)
+    out["cdcl_portfolio_unseeded"] = {"status": {10: "SAT", 20: "UNSAT", 0: "timeout"}[r.status],
+                                      "seconds": time.perf_counter() - t0, "threads": threads,
+                                      "verified": verify(m) if m is not None else None, "time_limit_s": cdcl_limit_s}
+    labels = {1: "paper_exact_R3", 0: "normalize_off", 3: "mean_magnitude_R28"}
+    for norm in norms:
+        q = Solver(local, stream=stream)
+        q.load_cnf(cnf)
+        c = config_default()
+        c.normalize = norm
+        q.init_batch(N, seed, c)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        steps, gate, solved = 0, None, False
+        while steps < max_steps:
+            inf = q.step(10)
+            steps = inf.t
+            if inf.solved:
+                solved = True
+                break
+            if (cnf.C - inf.best_unsat) / cnf.C > 0.99:
+                gate = steps
+                break
+        t_gpu = time.perf_counter() - t0
+        rec = {"gpu_steps": steps, "gpu_seconds": t_gpu, "gate_at_step": gate, "gpu_solved": solved}
+        if solved:
+            vals, idx, st = q.get_solution()
+            rec.update(status="SAT (GPU)", verified=verify(vals), total_seconds=t_gpu)
+        else:
+            ex = q.export_best(threads)
+            seeds = np.stack([e["lits"] for e in ex]).astype(np.int32)
+            t_ex = time.perf_counter() - t0 - t_gpu
+            r, m = cdcl_portfolio(cnf, seeds, threads=threads, unseeded=True, time_limit_s=cdcl_limit_s)
+            rec.update(export_seconds=t_ex, k=int(seeds.shape[1]), best_unsat_exported=int(ex[0]["unsat"]),
+                       status={10: "SAT", 20: "UNSAT", 0: "timeout"}[r.status], cdcl_seconds=r.seconds,
+                       winner=("unseeded" if r.winner == -1 else int(r.winner)), failed_seeds=r.failed_seeds,
+                       verified=verify(m) if m is not None else None,
+                       total_seconds=time.perf_counter() - t0)
+        q.close()
+        out[labels[norm]] = rec
+    return out
+
+
 def workload_desc(name, cnf, N):
     kinds = {"c1": "planted random 3-SAT", "c2": "planted random 3-SAT", "c3": "planted random 3-SAT",
              "c4": "industrial-shaped CNF (lengths 2-7, power-law occurrences)", "c5": "planted random 3-SAT",
-             "c2h": "2-hidden planted random 3-SAT (SURVEY f2 variant)"}
+             "c2h": "2-hidden planted random 3-SAT (SURVEY f2 variant)",
+             "f4d": "planted random 15-SAT, clause-dense (SURVEY f4 experiment)",
+             "f4s": "planted random 3-SAT, small (SURVEY f4 experiment)"}
     return f"{name}: {kinds[name]} V={cnf.V} C={cnf.C} (ratio {cnf.C / cnf.V:.2f}), N={N} candidates"
 
 
@@ -334,6 +410,17 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     stream = torch.cuda.current_stream()
+    if args.hybrid_only:
+        if rank == 0:
+            from tsat_synth import planted_ksat
+            parts = [int(x) for x in args.hybrid_only.split(",")]
+            V, sd = parts[0], parts[1]
+            Nh = parts[2] if len(parts) > 2 else 4096
+            cnf = planted_ksat(V, int(round(4.2 * V)), 3, sd)
+            print(json.dumps({"metric": "hybrid time-to-SAT",
+                              "hybrid": hybrid_tts(cnf, Nh, sd, local, stream, threads=max(1, (os.cpu_count() or 2) - 1))}),
+                  flush=True)
+        return
     if args.tts_only:
         if rank == 0:
             r = time_to_sat(args.tts_config, [int(x) for x in args.tts_seeds.split(",")], args.tts_max_steps, local,
@@ -376,7 +463,7 @@ def main():
         try:
             s = make_solver()
             info = load(s)
-            s.init_batch(N * world, seed)
+            s.init_batch(N * world, seed, **({'clause_eval': 1} if args.clause_eval else {}))
             s.step(1)
         except Exception as ex:  # noqa: BLE001
             ok, why = 0, f"{type(ex).__name__}: {ex}"[:200]
@@ -391,11 +478,11 @@ def main():
             peer_fallback = why or "another rank failed to set up the peer path"
             s = make_solver()
             info = load(s)
-            s.init_batch(N * world, seed)
+            s.init_batch(N * world, seed, **({'clause_eval': 1} if args.clause_eval else {}))
     else:
         s = make_solver()
         info = load(s)
-        s.init_batch(N * world, seed)
+        s.init_batch(N * world, seed, **({'clause_eval': 1} if args.clause_eval else {}))
     chunk = max(1, min(args.chunk, args.steps))
     assert args.steps % chunk == 0, "--steps must be a multiple of --chunk"
     # warm-up (also instantiates the chunk-sized CUDA graph)
@@ -479,7 +566,7 @@ def main():
         f0 = torch.cuda.Event(enable_timing=True); f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         load(s2)                              # host CSR -> device
-        s2.init_batch(N * world, seed)
+        s2.init_batch(N * world, seed, **({'clause_eval': 1} if args.clause_eval else {}))
         s2.step(1)                            # first call: captures + instantiates the 1-step graph
         s2.query_unsat_async(pins[1].data_ptr())
         torch.cuda.synchronize()
@@ -542,6 +629,14 @@ def main():
         tts = time_to_sat(args.tts_config, [int(x) for x in args.tts_seeds.split(",")], args.tts_max_steps, local,
                           stream)
 
+    # ---- GPU -> CPU CDCL hand-off (f1): hybrid time-to-SAT on a planted
+    # instance small enough for the CDCL arms to be timed (V = 600)
+    hybrid = None
+    if world == 1 and not args.no_tts:
+        from tsat_synth import planted_ksat
+        hybrid = hybrid_tts(planted_ksat(600, 2520, 3, 1), 4096, 1, local, stream,
+                            threads=max(1, (os.cpu_count() or 2) - 1), cdcl_limit_s=20.0)
+
     # ---- trajectory quality (not a timing): one LR cycle (360 iterations) of
     # the paper-exact Eq. 5 reading (R3) and of the normalize-off variant;
     # best satisfied fraction and whether the 99 % gate fires
@@ -583,7 +678,7 @@ def main():
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": kps * args.steps, "clocks": clk.summary(),
         "last_info": {"t": last.t, "best_unsat": last.best_unsat, "loss": last.loss, "solved": last.solved},
-        "quality": quality, "configs_more": extra, "time_to_sat": tts,
+        "quality": quality, "configs_more": extra, "time_to_sat": tts, "hybrid_time_to_sat": hybrid,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -81,6 +81,11 @@ typedef struct {
     double  tau_final;       /* SmoothMin temperature annealing (variant f2, reading R29): > 0 -> within each LR
                                 cycle tau_t = tau * (tau_final / tau)^((t mod restart_every) / (restart_every - 1)),
                                 geometric from tau to tau_final; 0 = constant tau (paper default, R1) */
+    int32_t clause_eval;     /* rows a4/a5 (R = P A, histogram): 0 = bit-sliced sparse gathers (default);
+                                1 = dense tensor-core tiles (tcgen05 uint8 MMA over the C x 2V matrix P and
+                                the 2V x N assignment matrix, SURVEY 8(f) f4 experiment; library-owned
+                                buffers of ceil(C/128)*128 x 2V and ceil(N/256)*256 x 2V bytes, TSAT_E_RANGE
+                                above 2^31 bytes each) */
 } tsat_config;
 
 typedef struct {

@@ -34,7 +34,7 @@ class tsat_config(ct.Structure):
                 ("eps", ct.c_double), ("weight_decay", ct.c_double), ("lr0", ct.c_double), ("lr_min", ct.c_double),
                 ("decay_factor", ct.c_double), ("decay_every", ct.c_int32), ("restart_every", ct.c_int32),
                 ("noise_sigma", ct.c_double), ("eps_norm", ct.c_double), ("reset_moments_on_restart", ct.c_int32),
-                ("tau_final", ct.c_double)]
+                ("tau_final", ct.c_double), ("clause_eval", ct.c_int32)]
 
 
 class tsat_cnf_info(ct.Structure):

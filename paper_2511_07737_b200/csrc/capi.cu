@@ -79,6 +79,10 @@ struct tsat_ctx_s {
     // k_update launch geometry (configure_kernels)
     int upd_mode = 0, upd_GT = 0, upd_NG = 0, upd_grid = 0, num_sms = 0, upd_recbufs = 2;
     int upd_RB = 1, upd_blk_cap = 0;    // row-block k_update (small shards, k_update_blk.cu)
+    // dense tensor-core clause evaluation (config.clause_eval = 1, k_dense.cu): library-owned
+    uint8_t* dP = nullptr;
+    uint8_t* dAL = nullptr;
+    int dKp = 0, dCp = 0;
     int upd_chunk = 0, upd_gs_global = 0;
     bool chunked = false;               // N too large for the fused kernel: split sequence, no collectives at W = 1
     size_t upd_smem = 0;
@@ -278,6 +282,11 @@ StepArgs step_args(tsat_ctx ctx) {
     a.upd_rec_cap = std::max(64, (ctx->cnf.max_rec_words + 63) / 64 * 64);
     a.upd_RB = ctx->upd_RB;
     a.upd_blk_cap = ctx->upd_blk_cap;
+    a.dense = ctx->dP != nullptr;
+    a.dP = ctx->dP;
+    a.dAL = ctx->dAL;
+    a.dKp = ctx->dKp;
+    a.dCp = ctx->dCp;
     a.sharded = (ctx->sharded || ctx->chunked) ? 1 : 0;     // kernels: the split (phase A / B) sequence
     a.Gbuf = (float*)(w + L.Gbuf);
     a.Jbuf = (long long*)(w + L.Jbuf);
@@ -648,6 +657,7 @@ tsat_status tsat_config_default(tsat_config* out) {
     out->noise_sigma = 0.0;
     out->reset_moments_on_restart = 0;
     out->tau_final = 0.0;
+    out->clause_eval = 0;
     out->eps_norm = 1e-8;
     return TSAT_OK;
 }
@@ -905,6 +915,29 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
         ctx->t = 0;
         ctx->steps_done = 0;
         CK(cudaSetDevice(ctx->device));
+        // dense clause evaluation (f4 experiment): P (C x 2V) and A (N x 2V) as uint8, K-major
+        cudaFree(ctx->dP);
+        cudaFree(ctx->dAL);
+        ctx->dP = ctx->dAL = nullptr;
+        if (c.clause_eval == 1 && ctx->cnf.C > 0) {
+            const long long Kp = ((2LL * ctx->cnf.V + 31) / 32) * 32;
+            const long long Cp = (ctx->cnf.C + dense_tile_m() - 1) / dense_tile_m() * dense_tile_m();
+            const long long Np = ((long long)ctx->N + dense_tile_n() - 1) / dense_tile_n() * dense_tile_n();
+            if (Kp * Cp >= (1LL << 31) || Kp * Np >= (1LL << 31))
+                return fail(ctx, TSAT_E_RANGE, "clause_eval = 1: dense P or A above 2^31 bytes");
+            std::vector<uint8_t> hp((size_t)(Kp * Cp), 0);
+            for (int64_t cc = 0; cc < ctx->cnf.C; ++cc)
+                for (uint32_t i = ctx->cnf.clause_ptr[cc]; i < ctx->cnf.clause_ptr[cc + 1]; ++i)
+                    hp[(size_t)cc * Kp + ctx->cnf.clause_lit[i]] = 1;     // column = literal code 2v + neg
+            CK(cudaMalloc(&ctx->dP, hp.size()));
+            CK(cudaMalloc(&ctx->dAL, (size_t)(Kp * Np)));
+            CK(cudaMemcpy(ctx->dP, hp.data(), hp.size(), cudaMemcpyHostToDevice));
+            CK(cudaMemset(ctx->dAL, 0, (size_t)(Kp * Np)));
+            ctx->dKp = (int)Kp;
+            ctx->dCp = (int)Cp;
+        } else if (c.clause_eval != 0 && c.clause_eval != 1) {
+            return fail(ctx, TSAT_E_ARG, "clause_eval must be 0 or 1");
+        }
         // row blocks for small shards (fused W = 1 and peer paths): RB rows per
         // work item, staging capacity = max over blocks of the non-hub rows' records
         ctx->upd_RB = 1;
@@ -1353,6 +1386,8 @@ void tsat_destroy(tsat_ctx ctx) {
     drop_graphs(ctx);
     for (auto e : ctx->events) cudaEventDestroy(e);
     free_cnf(ctx);
+    cudaFree(ctx->dP);
+    cudaFree(ctx->dAL);
     comm_destroy(ctx->comm);
     peer_release(ctx);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);

@@ -105,7 +105,8 @@ private:
     uint64_t rng_;
     bool ok_ = true, stopped_ = false;
     std::vector<Clause> clauses_;
-    std::vector<std::vector<int>> watches_;   // literal -> clauses watching it
+    struct Watch { int ci, blocker; };
+    std::vector<std::vector<Watch>> watches_;   // literal -> clauses watching it (+ a blocker literal)
     std::vector<int8_t> val_, phase_, seen_;
     std::vector<int> level_, reason_, trail_, trail_lim_, assumptions_;
     std::vector<double> act_;
@@ -138,8 +139,8 @@ private:
     }
     void attach(int ci) {
         const Clause& c = clauses_[ci];
-        watches_[c.lits[0]].push_back(ci);
-        watches_[c.lits[1]].push_back(ci);
+        watches_[c.lits[0]].push_back({ci, c.lits[1]});
+        watches_[c.lits[1]].push_back({ci, c.lits[0]});
     }
     void enqueue(int lit, int reason) {
         const int v = lit >> 1;
@@ -205,26 +206,28 @@ private:
         while (qhead_ < trail_.size()) {
             const int p = trail_[qhead_++];
             const int fl = p ^ 1;                                   // the literal that became false
-            std::vector<int>& ws = watches_[fl];
+            std::vector<Watch>& ws = watches_[fl];
             ++propagations;
             size_t i = 0, j = 0;
             while (i < ws.size()) {
-                const int ci = ws[i++];
+                const Watch wch = ws[i++];
+                if (value(wch.blocker) == 1) { ws[j++] = wch; continue; }   // satisfied: clause untouched
+                const int ci = wch.ci;
                 Clause& c = clauses_[ci];
                 if (c.dead) continue;
                 if (c.lits[0] == fl) std::swap(c.lits[0], c.lits[1]);
-                if (value(c.lits[0]) == 1) { ws[j++] = ci; continue; }
+                if (value(c.lits[0]) == 1) { ws[j++] = {ci, c.lits[0]}; continue; }
                 bool moved = false;
                 for (size_t k = 2; k < c.lits.size(); ++k) {
                     if (value(c.lits[k]) != 0) {
                         std::swap(c.lits[1], c.lits[k]);
-                        watches_[c.lits[1]].push_back(ci);
+                        watches_[c.lits[1]].push_back({ci, c.lits[0]});
                         moved = true;
                         break;
                     }
                 }
                 if (moved) continue;
-                ws[j++] = ci;
+                ws[j++] = {ci, c.lits[0]};
                 if (value(c.lits[0]) == 0) {                        // conflict: keep the remaining watches
                     confl = ci;
                     qhead_ = trail_.size();

@@ -18,7 +18,7 @@ cudaError_t launch_step_kernel(int which, const StepArgs& a, const StepScalars* 
     const uint32_t* Acur = (t & 1) ? a.A1 : a.A0;
     uint32_t* Anext = (t & 1) ? a.A0 : a.A1;
     switch (which) {
-        case 0: return launch_clause(a, Acur, sc_dev, st);
+        case 0: return (a.dense && a.C > 0) ? launch_dense_clause(a, Acur, sc_dev, st) : launch_clause(a, Acur, sc_dev, st);
         case 1: return launch_gtable(a, sc_dev, st);
         case 2: return a.upd_mode == 0 ? launch_hub(a, Acur, st) : cudaGetLastError();
         case 3: return a.upd_RB > 1 ? launch_update_blk(a, Acur, Anext, sc_dev, st) : launch_update(a, Acur, Anext, sc_dev, st);
@@ -27,6 +27,12 @@ cudaError_t launch_step_kernel(int which, const StepArgs& a, const StepScalars* 
     return cudaErrorInvalidValue;
 }
 
-cudaError_t configure_kernels(StepArgs* a) { return a->upd_RB > 1 ? configure_update_blk(a) : configure_update(a); }
+cudaError_t configure_kernels(StepArgs* a) {
+    if (a->dense) {
+        cudaError_t e = configure_dense();
+        if (e != cudaSuccess) return e;
+    }
+    return a->upd_RB > 1 ? configure_update_blk(a) : configure_update(a);
+}
 
 }  // namespace tsat

@@ -185,6 +185,11 @@ struct StepArgs {
     int upd_recbufs;                 // record buffers per group (1 or 2, configure_update)
     int upd_RB;                      // rows per work item: 1, or 32 / (N/32) for small shards (k_update_blk)
     int upd_blk_cap;                 // record words a group stages per row block (max over blocks, non-hub rows)
+    // dense tensor-core clause evaluation (k_dense.cu; config.clause_eval = 1)
+    int dense;
+    const uint8_t* dP;               // [dCp][dKp] uint8 0/1 problem matrix (K-major)
+    uint8_t* dAL;                    // [ceil(N/256)*256][dKp] uint8 0/1 assignment matrix (K-major)
+    int dKp, dCp;
     int pdl;                         // launch k_clause / k_gtable / k_update with programmatic
                                      // stream serialisation (PDL; fused W = 1 path without hubs)
     size_t upd_smem;
@@ -249,6 +254,11 @@ int update_block_rows(int N);
 cudaError_t configure_update_blk(StepArgs* a);
 cudaError_t launch_update_blk(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
                               cudaStream_t st);
+// dense clause evaluation (k_dense.cu)
+cudaError_t configure_dense();
+cudaError_t launch_dense_clause(const StepArgs& a, const uint32_t* Acur, const StepScalars* sc, cudaStream_t st);
+int dense_tile_m();
+int dense_tile_n();
 // whether the fused k_update geometry fits (else: chunked split sequence)
 bool update_fits_fused(int KB, int N, int rec_cap, int optin);
 // peer path: exchange of Qbuf[0..V) row partials (init / set_state), gen = exchange generation

@@ -239,6 +239,34 @@ def test_long_clauses_k_gt_7(case):
         assert ref.unsat[0] == 0 and info.best_unsat == 0
 
 
+@pytest.mark.parametrize("case", ["planted3", "ragged", "k15_color", "k7_ind", "blk128"])
+def test_dense_tensor_core_clause_eval(case):
+    """config.clause_eval = 1 evaluates R = P A as a dense uint8
+    tcgen05 product (k_dense.cu) and histograms R from TMEM; the whole step
+    stays bit-exact against the oracle.  C not a multiple of the 128-clause
+    tile, N not a multiple of the 256-candidate tile, 2V not a multiple of
+    the 128-byte K chunk, K = 15 and K = 7 instances."""
+    if case == "planted3":
+        cnf, N = planted_ksat(256, 1075, 3, 2), 512
+    elif case == "ragged":
+        cnf, N = planted_ksat(173, 700, 3, 4), 96
+    elif case == "k15_color":
+        cnf, N = coloring_cnf(20, 15, 3, 5), 320
+    elif case == "k7_ind":
+        cnf, N = industrial_cnf(300, 1100, 6), 256
+    else:
+        cnf, N = planted_ksat(1003, 4213, 3, 21), 128
+    state = random_state(cnf.V, N, seed=23)
+    from paper_2511_07737_b200 import config_default
+    s, o = make_pair(cnf, N, 4, state=state, t0=0)
+    c = config_default()
+    c.clause_eval = 1
+    s.init_batch(N, 4, c)
+    s.set_state(*state, 0)
+    for _ in range(6):
+        compare_step(s, o, cnf, f"dense {case}")
+
+
 def test_lr_boundaries_and_restart():
     """Cross the t = 29/30 decay and the t = 359/360 restart (R9)."""
     cnf = planted_ksat(200, 840, 3, 6)

@@ -258,6 +258,11 @@ CONFIGS = {
     "c3": dict(kind="planted", V=1_000_000, C=4_200_000, k=3, N=1024, steps=360, seed=1),
     "c4": dict(kind="industrial", V=500_000, C=2_000_000, N=2048, steps=360, seed=1),
     "c5": dict(kind="planted", V=100_000, C=425_000, k=3, N=65536, steps=3600, seed=1),
+    # SURVEY f4 (dense tensor-core tiles) experiment: a small clause-DENSE
+    # instance (long clauses over few variables: P is 15/512 = 2.9 % dense) and
+    # a sparse one of the same size (3/512 = 0.6 %); not BASELINE configs
+    "f4d": dict(kind="planted", V=256, C=4096, k=15, N=8192, steps=360, seed=1),
+    "f4s": dict(kind="planted", V=256, C=1075, k=3, N=8192, steps=360, seed=1),
     # c2's shape with 2-hidden planting (not a BASELINE config)
     "c2h": dict(kind="planted", V=10_000, C=42_000, k=3, N=4096, steps=360, seed=1, hidden=2),
 }
