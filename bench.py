@@ -56,7 +56,8 @@ def parse():
                     help="weak: N_config candidates per GPU; strong: N_config candidates in total (BASELINE's "
                          "fixed global batch; auto = strong for c3 / c5, weak otherwise)")
     ap.add_argument("--no-extra", action="store_true", help="skip the c3 / c4 sub-results (N=1)")
-    ap.add_argument("--extra", default="c3,c4", help="configs timed as sub-results at N=1")
+    ap.add_argument("--extra", default="c3,c4,c3@128,c5@8192",
+                    help="configs timed as sub-results at N=1 (cfg@N: N candidates on this GPU)")
     ap.add_argument("--no-tts", action="store_true", help="skip the time-to-SAT block (N=1)")
     ap.add_argument("--tts-config", default="c2")
     ap.add_argument("--tts-seeds", default="1,2,3,4,5")
@@ -89,12 +90,15 @@ def step_algorithmic_bytes(cnf, N):
 
 def time_config(name, local, stream, hbm, steps=30, warm=10):
     """Sub-result for another config on this GPU (N=1): device-timed steps and
-    per-kernel CUDA-event times; k_update's fraction of the HBM roofline."""
+    per-kernel CUDA-event times; k_update's fraction of the HBM roofline.
+    "c3@128" = config c3 with 128 candidates on this GPU (one GPU's share of
+    BASELINE's fixed global batch split over 8 GPUs)."""
     import torch
     from paper_2511_07737_b200 import Solver
     from tsat_synth import make_config
-    cnf, cfg = make_config(name)
-    N = cfg["N"]
+    base, _, nsh = name.partition("@")
+    cnf, cfg = make_config(base)
+    N = int(nsh) if nsh else cfg["N"]
     s = Solver(local, stream=stream)
     s.load_cnf(cnf)
     s.init_batch(N, cfg["seed"])
@@ -120,7 +124,8 @@ def time_config(name, local, stream, hbm, steps=30, warm=10):
     per = {n: float(kms[i] / ks) for i, n in enumerate(names)}
     ub = upd_algorithmic_bytes(cnf, N)
     sb = step_algorithmic_bytes(cnf, N)
-    return {"workload": workload_desc(name, cnf, N), "ms_per_step": ms, "value": cnf.C * N / (ms / 1e3),
+    return {"workload": workload_desc(base, cnf, N) + (f" (one GPU's share of {cfg['N']} over {cfg['N'] // N} GPUs)"
+                                                         if nsh else ""), "ms_per_step": ms, "value": cnf.C * N / (ms / 1e3),
             "unit": "evals/s", "steps": steps, "kernel_ms": per,
             "k_update": {"algorithmic_bytes": ub, "achieved_gbs": ub / (per["k_update"] / 1e3) / 1e9,
                          "frac": ub / (per["k_update"] / 1e3) / 1e9 / hbm},

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
     // too large for shared memory (MODE 1 only), whose g table stays in L2
     const int NCH = MODE == 1 ? a.upd_chunk : N;
     const int nch = MODE == 1 ? (N + NCH - 1) / NCH : 1;  // compile-time 1: fused modes keep smem addressing
-    const bool gs_global = MODE == 1 && a.upd_gs_global != 0;
+    const bool gs_global = a.upd_gs_global != 0;     // g table read through L1/L2 (large N, configure_update)
     const size_t dpkw = upd_dpk_words(NCH);
     float* gs = gs_global ? a.gtab : reinterpret_cast<float*>(smem);
     const int grp = threadIdx.x / GT, tg = threadIdx.x - grp * GT;
@@ -490,6 +490,9 @@ static cudaError_t set_update_attrs(int smem) {
     return cudaFuncSetAttribute(k_update<KB, 2, true>, attr, smem);
 }
 
+#ifndef TSAT_GS_GLOBAL_BELOW
+#define TSAT_GS_GLOBAL_BELOW 4       // fused kernel: g table from L2 when smem would hold fewer groups
+#endif
 cudaError_t configure_update(StepArgs* a) {
     const int N = a->N, KB = a->KB;
     int dev = 0, optin = 0, sms = 0;
@@ -503,7 +506,16 @@ cudaError_t configure_update(StepArgs* a) {
     a->upd_gs_global = fused ? 0 : 1;
     const int NWc = a->upd_chunk >> 5;
     const int GT = NWc >= 128 ? 128 : (NWc > 32 ? 64 : 32);
-    const size_t gsb = fused ? upd_gs_bytes(KB, N) : 0;
+    if (fused) {
+        // the batch's g table in shared memory leaves few warp groups for
+        // large batches (N = 8192: 128 KB of table, 2 groups); read it through
+        // L1 / L2 instead when that buys at least twice the groups
+        const size_t gsb0 = upd_gs_bytes(KB, N), grb0 = upd_group_bytes(KB, N, a->upd_rec_cap, upd_recbufs(KB));
+        const long long ng_s = optin > (long long)gsb0 ? ((long long)optin - (long long)gsb0) / (long long)grb0 : 0;
+        const long long ng_g = (long long)optin / (long long)grb0;
+        if (ng_s < TSAT_GS_GLOBAL_BELOW && ng_g >= 2 * ng_s && !std::getenv("TSAT_NO_GS_GLOBAL")) a->upd_gs_global = 1;
+    }
+    const size_t gsb = (fused && !a->upd_gs_global) ? upd_gs_bytes(KB, N) : 0;
     const int max_threads = KB == 4 ? (a->peer ? TSAT_UPD_THREADS4P : TSAT_UPD_THREADS4)
                                     : TSAT_UPD_THREADS8;   // register budget (launch bounds)
     auto groups = [&](int nbufs) {

@@ -267,6 +267,21 @@ def test_dense_tensor_core_clause_eval(case):
         compare_step(s, o, cnf, f"dense {case}")
 
 
+@pytest.mark.parametrize("kind", ["kb4_n8192", "kb8_n4096"])
+def test_fused_g_table_in_l2(kind):
+    """Large per-GPU batches that still fit the fused kernel (BASELINE c5's
+    8192-candidate share per GPU): the g table is read through L1 / L2 instead
+    of shared memory so more warp groups fit.  Bit-exact against the oracle."""
+    if kind == "kb4_n8192":
+        cnf, N = planted_ksat(90, 380, 3, 3), 8192
+    else:
+        cnf, N = industrial_cnf(70, 260, 5), 4096
+    state = random_state(cnf.V, N, seed=29)
+    s, o = make_pair(cnf, N, 6, state=state, t0=0)
+    for _ in range(4):
+        compare_step(s, o, cnf, kind)
+
+
 def test_lr_boundaries_and_restart():
     """Cross the t = 29/30 decay and the t = 359/360 restart (R9)."""
     cnf = planted_ksat(200, 840, 3, 6)
