@@ -9,10 +9,12 @@
 // 128-clause x 256-candidate tile of R with tcgen05.mma.kind::i8 (uint8 x
 // uint8 -> int32 in TMEM; exact: R <= 15), operands staged in shared memory
 // in the canonical no-swizzle K-major layout (8-row x 16-byte core matrices),
-// K in chunks of 128 bytes (4 MMAs of K = 32).  The epilogue reads R with
+// K in chunks of 64 bytes (2 MMAs of K = 32), double-buffered (the next
+// chunk's cp.async loads overlap the current MMAs).  The epilogue reads R with
 // tcgen05.ld (one clause row per thread), turns each candidate column into
 // 4 bit planes with warp ballots and adds popcount(bin masks) to the
-// histogram (bins 0 .. KB-2; k_gtable derives the top bin).
+// CTA's shared histogram, then one global atomic per (candidate, bin) per CTA
+// (bins 0 .. KB-2; k_gtable derives the top bin).
 //
 // This is an experiment (config.clause_eval = 1): the sparse bit-sliced
 // k_clause moves 1 bit per literal occurrence and candidate; the dense form
@@ -25,7 +27,7 @@
 namespace tsat {
 
 namespace {
-constexpr int kDM = 128, kDN = 256, kDKC = 128;        // tile M (clauses), N (candidates), K chunk (bytes)
+constexpr int kDM = 128, kDN = 256, kDKC = 64;         // tile M (clauses), N (candidates), K chunk (bytes)
 constexpr int kAStep = kDM / 8 * 256, kBStep = kDN / 8 * 256;   // bytes per 32-byte k-step (A, B)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -69,14 +71,14 @@ __global__ void k_dense_pack(const uint32_t* __restrict__ A, int V, int NW, int 
     *reinterpret_cast<uint4*>(AL + (size_t)n * Kp + 16 * g) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-__global__ void __launch_bounds__(128, 1) k_dense_clause(const uint8_t* __restrict__ P, const uint8_t* __restrict__ AL,
+__global__ void __launch_bounds__(128, 2) k_dense_clause(const uint8_t* __restrict__ P, const uint8_t* __restrict__ AL,
                                                           long long C, int Kp, int N, int KB, int* __restrict__ hist,
                                                           DevScalars* __restrict__ ds, const StepScalars* __restrict__ sc) {
     extern __shared__ __align__(1024) uint8_t sm[];
-    uint8_t* sA = sm;
-    uint8_t* sB = sm + (kDKC / 32) * kAStep;
-    __shared__ __align__(8) uint64_t mbar;
+    constexpr int kStage = (kDKC / 32) * (kAStep + kBStep);      // one K chunk of both operands
+    __shared__ __align__(8) uint64_t mbar[2];
     __shared__ uint32_t tmem_base;
+    __shared__ int shist[16 * kDN];                               // the CTA's counts: [bin][column]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const long long m0 = (long long)blockIdx.y * kDM;
     const int n0 = blockIdx.x * kDN;
@@ -90,46 +92,63 @@ __global__ void __launch_bounds__(128, 1) k_dense_clause(const uint8_t* __restri
         ds->thmax_bits[(t + 1) & 1] = 0u;
         ds->loss_fx = 0;
     }
+    for (int i = tid; i < kDN * 16; i += 128) shist[i] = 0;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
                      "r"(kDN) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[1])) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tmem_base;
-    uint32_t phase = 0;
-    for (int kc = 0; kc < Kp; kc += kDKC) {
-        const int kb = Kp - kc < kDKC ? Kp - kc : kDKC;          // bytes in this chunk (multiple of 32)
-        const int nch = kb / 16;
-        // operand tiles -> canonical K-major layout: core matrix (8 rows x 16 B)
-        // at ks * step + (row / 8) * 256 + half * 128 (LBO = 128, SBO = 256)
+    // operand chunk -> canonical K-major layout of stage `st`: core matrix
+    // (8 rows x 16 B) at ks * step + (row / 8) * 256 + half * 128 (LBO 128, SBO 256)
+    auto load_chunk = [&](int kc, int st) {
+        const int kb = Kp - kc < kDKC ? Kp - kc : kDKC, nch = kb / 16;
+        uint8_t* sA = sm + st * kStage;
+        uint8_t* sB = sA + (kDKC / 32) * kAStep;
         for (int idx = tid; idx < kDM * nch; idx += 128) {
             const int row = idx / nch, ch = idx % nch;
             const uint32_t dst = smem_u32(sA) + (ch >> 1) * kAStep + (row >> 3) * 256 + (ch & 1) * 128 + (row & 7) * 16;
-            const uint8_t* src = P + (size_t)(m0 + row) * Kp + kc + ch * 16;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(P + (size_t)(m0 + row) * Kp + kc + ch * 16)
+                         : "memory");
         }
         for (int idx = tid; idx < kDN * nch; idx += 128) {
             const int row = idx / nch, ch = idx % nch;
             const uint32_t dst = smem_u32(sB) + (ch >> 1) * kBStep + (row >> 3) * 256 + (ch & 1) * 128 + (row & 7) * 16;
-            const uint8_t* src = AL + (size_t)(n0 + row) * Kp + kc + ch * 16;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(AL + (size_t)(n0 + row) * Kp + kc + ch * 16)
+                         : "memory");
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_all;" ::: "memory");
+    };
+    // 2-stage pipeline: chunk i+1 loads while the tensor core consumes chunk i
+    const int nk = (Kp + kDKC - 1) / kDKC;
+    uint32_t ph[2] = {0u, 0u};
+    load_chunk(0, 0);
+    for (int i = 0; i < nk; ++i) {
+        const int st = i & 1, kc = i * kDKC;
+        if (i + 1 < nk) {
+            if (i >= 1) { mbar_wait(&mbar[st ^ 1], ph[st ^ 1]); ph[st ^ 1] ^= 1u; }   // MMAs of chunk i-1 done
+            load_chunk(kc + kDKC, st ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");                      // chunk i landed
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy writes -> tensor core
         __syncthreads();
         if (tid == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int kb = Kp - kc < kDKC ? Kp - kc : kDKC;
+            const uint32_t sA = smem_u32(sm + st * kStage), sB = sA + (kDKC / 32) * kAStep;
             for (int ks = 0; ks < kb / 32; ++ks) {
-                const uint64_t ad = sdesc(smem_u32(sA) + ks * kAStep, 128, 256);
-                const uint64_t bd = sdesc(smem_u32(sB) + ks * kBStep, 128, 256);
+                const uint64_t ad = sdesc(sA + ks * kAStep, 128, 256);
+                const uint64_t bd = sdesc(sB + ks * kBStep, 128, 256);
                 const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
                 asm volatile(
                     "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -137,12 +156,15 @@ __global__ void __launch_bounds__(128, 1) k_dense_clause(const uint8_t* __restri
                     ::"r"(tmem), "l"(ad), "l"(bd), "r"(kIdesc), "r"(acc) : "memory");
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                         ::"r"(smem_u32(&mbar)) : "memory");
+                         ::"r"(smem_u32(&mbar[st])) : "memory");
         }
-        mbar_wait(&mbar, phase);          // MMAs done: the tile buffers may be refilled
-        phase ^= 1u;
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
+    {   // the last chunk's MMAs (and, in issue order, all earlier ones) complete
+        const int st = (nk - 1) & 1;
+        mbar_wait(&mbar[st], ph[st]);
+        if (nk >= 2) mbar_wait(&mbar[st ^ 1], ph[st ^ 1]);
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // epilogue: thread = clause row m0 + 32 warp + lane; 32 candidate columns at a time
     const bool vrow = m0 + 32 * warp + lane < C;
     const uint32_t vmask = __ballot_sync(0xffffffffu, vrow);
@@ -166,22 +188,25 @@ __global__ void __launch_bounds__(128, 1) k_dense_clause(const uint8_t* __restri
             const uint32_t b2 = __ballot_sync(0xffffffffu, r[j] & 4u), b3 = __ballot_sync(0xffffffffu, r[j] & 8u);
             if (lane == j) { q0 = b0; q1 = b1; q2 = b2; q3 = b3; }
         }
-        const int n = n0 + c0 + lane;
-        if (n < N) {
-            for (int rr = 0; rr < KB - 1; ++rr) {
-                const uint32_t m = vmask & ((rr & 1) ? q0 : ~q0) & ((rr & 2) ? q1 : ~q1) & ((rr & 4) ? q2 : ~q2) &
-                                   ((rr & 8) ? q3 : ~q3);
-                const int cnt = __popc(m);
-                if (cnt) atomicAdd(&hist[(size_t)n * KB + rr], cnt);
-            }
+        for (int rr = 0; rr < KB - 1; ++rr) {
+            const uint32_t m = vmask & ((rr & 1) ? q0 : ~q0) & ((rr & 2) ? q1 : ~q1) & ((rr & 4) ? q2 : ~q2) &
+                               ((rr & 8) ? q3 : ~q3);
+            const int cnt = __popc(m);
+            if (cnt) atomicAdd(&shist[rr * kDN + c0 + lane], cnt);     // consecutive lanes: no bank conflict
         }
+    }
+    __syncthreads();
+    for (int i = tid; i < kDN * 16; i += 128) {           // one global atomic per (column, bin) per CTA
+        const int col = i % kDN, rr = i / kDN, n = n0 + col;
+        const int x = shist[i];
+        if (x && n < N && rr < KB - 1) atomicAdd(&hist[(size_t)n * KB + rr], x);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kDN) : "memory");
 }
 
-size_t dense_smem_bytes() { return (size_t)(kDKC / 32) * (kAStep + kBStep); }
+size_t dense_smem_bytes() { return 2 * (size_t)(kDKC / 32) * (kAStep + kBStep); }   // 2 stages
 cudaError_t configure_dense() {
     return cudaFuncSetAttribute(k_dense_clause, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dense_smem_bytes());
 }
