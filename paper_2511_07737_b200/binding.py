@@ -110,7 +110,9 @@ def load_library(path: str = LIB_PATH):
                               "(there is no CPU fallback)")
         lib = ct.CDLL(path)
         for name, (res, args) in _SIGS.items():
-            fn = getattr(lib, name)
+            fn = getattr(lib, name, None)
+            if fn is None:          # an older library build (A/B variants): that entry point is absent
+                continue
             fn.restype = res
             fn.argtypes = args
         _lib = lib

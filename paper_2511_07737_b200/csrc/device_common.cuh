@@ -14,6 +14,9 @@ namespace tsat {
 // L2 cache policy for the bit-plane gathers (created once per kernel):
 // evict-last when both plane buffers fit comfortably in L2 (they are re-read
 // by every occurrence), evict-normal otherwise.
+#ifndef TSAT_BIN_SKIP
+#define TSAT_BIN_SKIP 1              // batched records: skip bins above the batch's clause length
+#endif
 #ifndef TSAT_PLANE_FRAC
 #define TSAT_PLANE_FRAC 0            // planes larger than L2: evict-last on this fraction of the lines (0: normal)
 #endif
@@ -477,6 +480,11 @@ __device__ __forceinline__ void count_batched(uint32_t (&cnt)[NCTR][B], RecFn re
         const uint32_t cm = neg ? 0u : 0xffffffffu;
 #pragma unroll
         for (int r = 0; r < NCTR; ++r) {
+#if TSAT_BIN_SKIP
+            // R <= clause length <= J + 1 (records are padded to the batch's
+            // longest): higher bins get nothing from this batch (warp-uniform)
+            if (R0 + r > (int)J + 1) break;
+#endif
             uint32_t s0, s1, s2;
             sum4(bs_eq<NP>(sp[0], R0 + r), bs_eq<NP>(sp[1], R0 + r), bs_eq<NP>(sp[2], R0 + r), bs_eq<NP>(sp[3], R0 + r),
                  s0, s1, s2);

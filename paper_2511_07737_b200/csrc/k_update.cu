@@ -39,7 +39,7 @@ namespace tsat {
 // MAG: normalize 3 (R28, d = mean |theta|): the Jacobian addend carries
 // sign(theta) and the next row sums are of |theta| (a template flag: a
 // run-time one costs the default path ~3 % at c2 / c3).
-template <int KB, int MODE, bool MAG = false>
+template <int KB, int MODE, bool MAG = false, bool GSG = false>
 __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TSAT_UPD_THREADS4) : TSAT_UPD_THREADS8, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
                                                                     uint32_t* __restrict__ Anext,
                                                                     const StepScalars* __restrict__ sc) {
@@ -51,7 +51,10 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
     // too large for shared memory (MODE 1 only), whose g table stays in L2
     const int NCH = MODE == 1 ? a.upd_chunk : N;
     const int nch = MODE == 1 ? (N + NCH - 1) / NCH : 1;  // compile-time 1: fused modes keep smem addressing
-    const bool gs_global = a.upd_gs_global != 0;     // g table read through L1/L2 (large N, configure_update)
+    // g table read through L1/L2: chunked items (MODE 1, run-time flag), or the
+    // fused kernel for large N (GSG: a separate instantiation, so the default
+    // path keeps its shared-memory loads)
+    const bool gs_global = GSG || (MODE == 1 && a.upd_gs_global != 0);
     const size_t dpkw = upd_dpk_words(NCH);
     float* gs = gs_global ? a.gtab : reinterpret_cast<float*>(smem);
     const int grp = threadIdx.x / GT, tg = threadIdx.x - grp * GT;
@@ -487,6 +490,10 @@ static cudaError_t set_update_attrs(int smem) {
     if ((e = cudaFuncSetAttribute(k_update<KB, 1>, attr, smem)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_update<KB, 2>, attr, smem)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_update<KB, 0, true>, attr, smem)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_update<KB, 0, false, true>, attr, smem)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_update<KB, 2, false, true>, attr, smem)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_update<KB, 0, true, true>, attr, smem)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_update<KB, 2, true, true>, attr, smem)) != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_update<KB, 2, true>, attr, smem);
 }
 
@@ -569,19 +576,25 @@ cudaError_t launch_hub(const StepArgs& a, const uint32_t* Acur, cudaStream_t st)
     return cudaGetLastError();
 }
 
-template <int KB>
-static cudaError_t launch_update_kb(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
-                                   cudaStream_t st) {
+template <int KB, bool GSG>
+static cudaError_t launch_update_kbg(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
+                                    cudaStream_t st) {
     const bool mag = a.mc.normalize == 3;
     const dim3 g(a.upd_grid), b(a.upd_GT * a.upd_NG);
     const size_t sm = a.upd_smem;
     if (a.peer) {
-        if (mag) k_update<KB, 2, true><<<g, b, sm, st>>>(a, Acur, Anext, sc);
-        else k_update<KB, 2><<<g, b, sm, st>>>(a, Acur, Anext, sc);
+        if (mag) k_update<KB, 2, true, GSG><<<g, b, sm, st>>>(a, Acur, Anext, sc);
+        else k_update<KB, 2, false, GSG><<<g, b, sm, st>>>(a, Acur, Anext, sc);
         return cudaGetLastError();
     }
-    return mag ? launch_maybe_pdl(a.pdl, k_update<KB, 0, true>, g, b, sm, st, a, Acur, Anext, sc)
-               : launch_maybe_pdl(a.pdl, k_update<KB, 0>, g, b, sm, st, a, Acur, Anext, sc);
+    return mag ? launch_maybe_pdl(a.pdl, k_update<KB, 0, true, GSG>, g, b, sm, st, a, Acur, Anext, sc)
+               : launch_maybe_pdl(a.pdl, k_update<KB, 0, false, GSG>, g, b, sm, st, a, Acur, Anext, sc);
+}
+template <int KB>
+static cudaError_t launch_update_kb(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
+                                   cudaStream_t st) {
+    return a.upd_gs_global ? launch_update_kbg<KB, true>(a, Acur, Anext, sc, st)
+                           : launch_update_kbg<KB, false>(a, Acur, Anext, sc, st);
 }
 
 cudaError_t launch_update(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,

@@ -34,6 +34,14 @@ struct BlkRow {
     float rhof, ncf, p2, m2, pm2;
     int hub, dsum, jvalid, s;
     int guard;
+    int roff, nrec, npos, nneg;      // staged records: offset in the block buffer, words, occurrences by sign
+};
+// A row's values for the next block, prefetched into the registers of lane r
+// while the current block streams (their L2 latency leaves the critical path).
+struct RowPre {
+    int2 pn;
+    int hub, guard, roff, nrec;
+    double rho;
 };
 
 __host__ __device__ inline size_t blk_group_bytes(int KB, int N, int RB, int cap, int nbufs) {
@@ -161,8 +169,26 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
         if (lane == 0) atomicMax(&a.ds->thmax_bits[(t + 1) & 1], __float_as_uint(m2));
     };
 
+    // row values of block v0 .. v0 + nr - 1 for lane r (< nr): occurrence counts,
+    // hub index, Eq. 5 statistics of the evaluated state, and the row's
+    // record offset within the block's staging buffer (non-hub rows back to back)
+    auto fetch_row = [&](int v0, int nr, RowPre& P) {
+        if (lane >= nr) return;
+        const int v = v0 + lane;
+        P.pn = a.occ_pn[v];
+        P.hub = a.hub_of[v];
+        P.rho = a.rowRho[v];
+        P.guard = a.rowGuard[v];
+        unsigned off = 0;
+        for (int r = 0; r < lane; ++r)
+            if (a.hub_of[v0 + r] < 0) off += a.upd_ptr[v0 + r + 1] - a.upd_ptr[v0 + r];
+        P.roff = (int)off;
+        P.nrec = (int)(a.upd_ptr[v + 1] - a.upd_ptr[v]);
+    };
+    RowPre pre{};
     int pend_v0 = -1, pend_nr = 0;
     int item = slot[1];
+    if (item < nitems) fetch_row(item * RB, min(RB, a.V - item * RB), pre);
     if (item < nitems) stage(item * RB, min(RB, a.V - item * RB), rec, false);
     __syncwarp();
     int it = 0;
@@ -178,38 +204,37 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
             prefetch_l2(a.m + (size_t)v0 * N, bytes);
             prefetch_l2(a.v + (size_t)v0 * N, bytes);
         }
-        if (lane < nr) {                                   // this block's row values
-            const int v = v0 + lane;
-            const int2 pn = a.occ_pn[v];
+        if (lane < nr) {                                   // this block's row values (prefetched)
             BlkRow& R = rp[lane];
-            R.hub = a.hub_of[v];
-            R.dsum = pn.y - pn.x;
-            R.rho = a.rowRho[v];
-            R.guard = a.rowGuard[v];
+            R.hub = pre.hub;
+            R.dsum = pre.pn.y - pre.pn.x;
+            R.rho = pre.rho;
+            R.guard = pre.guard;
+            R.roff = pre.roff;
+            R.nrec = pre.nrec;
+            R.npos = pre.pn.x;
+            R.nneg = pre.pn.y;
             int s;
             float p2;
-            R.jvalid = jscale(mc.Nnorm, pn.x + pn.y, gmax, thmax, &s, &p2) ? 1 : 0;
+            R.jvalid = jscale(mc.Nnorm, pre.pn.x + pre.pn.y, gmax, thmax, &s, &p2) ? 1 : 0;
             R.s = s;
             R.p2 = p2;
         }
+        __syncwarp();
 
         // ---- 1+2: gather (lane = row x word), transpose to bytes (KB = 16: all rows are hubs)
         if constexpr (KB <= 8) if (gr < nr) {
             const int v = v0 + gr;
-            if (a.hub_of[v] < 0) {
-                unsigned roff = 0;
-                for (int r = 0; r < gr; ++r)
-                    if (a.hub_of[v0 + r] < 0) roff += a.upd_ptr[v0 + r + 1] - a.upd_ptr[v0 + r];
-                const uint32_t* rbase = rb_cur + roff;
+            if (rp[gr].hub < 0) {
+                const uint32_t* rbase = rb_cur + rp[gr].roff;
                 auto recf = [&](unsigned i) { return rbase[i]; };
                 const uint32_t own = __ldg(Acur + (size_t)v * NW + gw);
                 uint32_t cnt[NCTR][kCtr];
                 if (uni3) {
-                    const int2 pn = a.occ_pn[v];
-                    count_uni3<NCTR, kCtr, TSAT_BLK_PIPE != 0>(cnt, recf, (unsigned)pn.y, (unsigned)pn.x, own, Acur, (unsigned)NW,
-                                                  (unsigned)gw, pol);
+                    count_uni3<NCTR, kCtr, TSAT_BLK_PIPE != 0>(cnt, recf, (unsigned)rp[gr].nneg, (unsigned)rp[gr].npos, own,
+                                                               Acur, (unsigned)NW, (unsigned)gw, pol);
                 } else {
-                    count_batched<NP, NCTR, kCtr>(cnt, recf, a.upd_ptr[v + 1] - a.upd_ptr[v], own, Acur, (unsigned)NW,
+                    count_batched<NP, NCTR, kCtr>(cnt, recf, (unsigned)rp[gr].nrec, own, Acur, (unsigned)NW,
                                                   (unsigned)gw, pol);
                 }
 #pragma unroll 1
@@ -234,6 +259,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
         __syncwarp();
         const int item_next = slot[it & 1];
         const int v0n = item_next < nitems ? item_next * RB : a.V;
+        if (v0n < a.V) fetch_row(v0n, min(RB, a.V - v0n), pre);       // the next block's row values
         auto stage_next = [&]() {
             if (v0n < a.V) stage(v0n, min(RB, a.V - v0n), rb_nxt, true);
             cp_async_commit();
