@@ -40,7 +40,7 @@ struct BlkRow {
 // while the current block streams (their L2 latency leaves the critical path).
 struct RowPre {
     int2 pn;
-    int hub, guard, roff, nrec;
+    int hub, guard, roff, nrec, rbeg;
     double rho;
 };
 
@@ -123,17 +123,17 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
     const MethodConsts& mc = a.mc;
 
     // records of block v0 .. v0 + nr - 1 (non-hub rows, back to back) -> buf
-    auto stage = [&](int v0, int nr, uint32_t* buf, bool async) {
-        unsigned off = 0;
+    // (the rows' record ranges come from the RowPre values lane r holds)
+    auto stage = [&](int nr, uint32_t* buf, bool async, const RowPre& P) {
         for (int r = 0; r < nr; ++r) {
-            const int v = v0 + r;
-            if (a.hub_of[v] >= 0) continue;
-            const unsigned b = a.upd_ptr[v], e = a.upd_ptr[v + 1];
-            for (unsigned i = lane; i < e - b; i += 32) {
+            if (__shfl_sync(0xffffffffu, P.hub, r) >= 0) continue;
+            const unsigned b = (unsigned)__shfl_sync(0xffffffffu, P.rbeg, r);
+            const unsigned len = (unsigned)__shfl_sync(0xffffffffu, P.nrec, r);
+            const unsigned off = (unsigned)__shfl_sync(0xffffffffu, P.roff, r);
+            for (unsigned i = lane; i < len; i += 32) {
                 if (async) cp_async4(buf + off + i, a.upd_rec + b + i);
                 else buf[off + i] = a.upd_rec[b + i];
             }
-            off += e - b;
         }
     };
     // Rows of a block are complete once their global Q are known: bit planes
@@ -183,13 +183,16 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
         for (int r = 0; r < lane; ++r)
             if (a.hub_of[v0 + r] < 0) off += a.upd_ptr[v0 + r + 1] - a.upd_ptr[v0 + r];
         P.roff = (int)off;
+        P.rbeg = (int)a.upd_ptr[v];
         P.nrec = (int)(a.upd_ptr[v + 1] - a.upd_ptr[v]);
     };
     RowPre pre{};
     int pend_v0 = -1, pend_nr = 0;
     int item = slot[1];
-    if (item < nitems) fetch_row(item * RB, min(RB, a.V - item * RB), pre);
-    if (item < nitems) stage(item * RB, min(RB, a.V - item * RB), rec, false);
+    if (item < nitems) {
+        fetch_row(item * RB, min(RB, a.V - item * RB), pre);
+        stage(min(RB, a.V - item * RB), rec, false, pre);
+    }
     __syncwarp();
     int it = 0;
     for (; item < nitems; ++it) {
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
         const int v0n = item_next < nitems ? item_next * RB : a.V;
         if (v0n < a.V) fetch_row(v0n, min(RB, a.V - v0n), pre);       // the next block's row values
         auto stage_next = [&]() {
-            if (v0n < a.V) stage(v0n, min(RB, a.V - v0n), rb_nxt, true);
+            if (v0n < a.V) stage(min(RB, a.V - v0n), rb_nxt, true, pre);
             cp_async_commit();
         };
         if (nbufs == 1) stage_next();
@@ -276,14 +279,16 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
             const float* tb = a.theta + (size_t)v0 * N;
             float4 th_nx = *reinterpret_cast<const float4*>(tb + 4 * lane);
             long long I = 0;
-            for (int k = 0; k < total; ++k) {
-                const int r = k / ipr, n = (k - r * ipr) * 128 + 4 * lane;
+            int k = 0;                                           // flat 128-candidate iteration of the block
+            for (int r = 0; r < nr; ++r) {
+              const int hub = rp[r].hub, dsum = rp[r].dsum;
+              const float p2 = rp[r].p2;
+              const bool jv = rp[r].jvalid != 0;
+              for (int kk = 0; kk < ipr; ++kk, ++k) {
+                const int n = kk * 128 + 4 * lane;
                 const float4 th4 = th_nx;
                 if (k + 1 < total) th_nx = *reinterpret_cast<const float4*>(tb + (size_t)(k + 1) * 128 + 4 * lane);
                 const float th[4] = {th4.x, th4.y, th4.z, th4.w};
-                const int hub = rp[r].hub, dsum = rp[r].dsum;
-                const float p2 = rp[r].p2;
-                const bool jv = rp[r].jvalid != 0;
                 float4 g4[KB];
 #pragma unroll
                 for (int q = 0; q < KB; ++q) g4[q] = *reinterpret_cast<const float4*>(gs + (size_t)q * N + n);
@@ -322,11 +327,10 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
                     dp[q] = __float_as_uint(Gq[q]);
                     if (jv) I += jterm(Gq[q], th[q], p2);
                 }
-                if (k - r * ipr == ipr - 1) {                    // the row's last iteration
-                    I = warp_sum(I);
-                    if (lane == 0) rp[r].jt = I;
-                    I = 0;
-                }
+              }
+              I = warp_sum(I);                                   // the row's J partial
+              if (lane == 0) rp[r].jt = I;
+              I = 0;
             }
         }
         __syncwarp();
@@ -358,8 +362,12 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
             float4 thn = ld_last(tb + 4 * lane), mn4 = ld_last(mb + 4 * lane), vn4 = ld_last(vb + 4 * lane);
             long long Qn = 0;
             float mx = 0.0f;
-            for (int k = 0; k < total; ++k) {
-                const int r = k / ipr, n = (k - r * ipr) * 128 + 4 * lane;
+            int k = 0;
+            for (int r = 0; r < nr; ++r) {
+              const float rhof = rp[r].rhof, ncf = rp[r].ncf;
+              const int v = v0 + r;
+              for (int kk = 0; kk < ipr; ++kk, ++k) {
+                const int n = kk * 128 + 4 * lane;
                 const size_t e = (size_t)k * 128 + 4 * lane;     // flat element of the block
                 const float4 th4 = thn, m4 = mn4, v4 = vn4;
                 if (k + 1 < total) {
@@ -367,8 +375,6 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
                     mn4 = ld_last(mb + e + 128);
                     vn4 = ld_last(vb + e + 128);
                 }
-                const float rhof = rp[r].rhof, ncf = rp[r].ncf;
-                const int v = v0 + r;
                 float th[4] = {th4.x, th4.y, th4.z, th4.w};
                 float mm[4] = {m4.x, m4.y, m4.z, m4.w};
                 float vv[4] = {v4.x, v4.y, v4.z, v4.w};
@@ -424,13 +430,12 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
                     pl[r * NW + (n >> 5)] = pw;
                     pl[RB * NW + r * NW + (n >> 5)] = nw;
                 }
-                if (k - r * ipr == ipr - 1) {                    // the row's last iteration
-                    Qn = warp_sum(Qn);
-                    mx = warp_maxf(mx);
-                    if (lane == 0) { rp[r].qt = Qn; rp[r].m2 = mx; }
-                    Qn = 0;
-                    mx = 0.0f;
-                }
+              }
+              Qn = warp_sum(Qn);                                 // the row's Q partial and max |theta|
+              mx = warp_maxf(mx);
+              if (lane == 0) { rp[r].qt = Qn; rp[r].m2 = mx; }
+              Qn = 0;
+              mx = 0.0f;
             }
         }
         cp_async_wait_all();                                     // next block's records visible after this
