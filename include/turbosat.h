@@ -290,6 +290,40 @@ const char* tsat_error_string(tsat_ctx ctx);
 /* Release the context and everything the library owns (not the caller's workspace). */
 void tsat_destroy(tsat_ctx ctx);
 
+/* ---------------------------------------------------------------- instances (host only)
+ * Native generators of the benchmark instance families, deterministic per
+ * seed (SplitMix64 stream; not bit-compatible with the Python tsat_synth
+ * generators the parity tests use).  Arrays are caller-owned, clause_ptr has
+ * C + 1 int64 offsets, literals are signed 1-based DIMACS, sigma is the
+ * planted model (V bytes, 0/1).  TSAT_E_ARG on invalid sizes. */
+
+/* Planted random k-SAT (k <= 15): k distinct variables per clause, the
+ * clause's truth pattern under sigma uniform over the 2^k - 1 patterns that
+ * satisfy it (hidden = 1) or over 1 .. 2^k - 2 so that the complement of sigma
+ * satisfies it too (hidden = 2).  dimacs_lits holds C * k entries. */
+tsat_status tsat_gen_planted(int32_t V, int64_t C, int32_t k, uint64_t seed, int32_t hidden,
+                             int64_t* clause_ptr, int32_t* dimacs_lits, uint8_t* sigma);
+
+/* Industrial-shaped CNF: clause lengths i.i.d. from len_probs[0..kmax]
+ * (len_probs[0] must be 0; normalised), variables drawn with probability
+ * proportional to rank^-alpha under a random id permutation, signs planted
+ * (hidden = 1).  lits_capacity >= C * kmax. */
+tsat_status tsat_gen_industrial(int32_t V, int64_t C, uint64_t seed, double alpha, int32_t kmax,
+                                const double* len_probs, int64_t* clause_ptr, int32_t* dimacs_lits,
+                                int64_t lits_capacity, uint8_t* sigma);
+
+/* DIMACS text ("c planted ..." comment when sigma != NULL and V <= 64, the
+ * header, one clause per line).  out == NULL: *length = bytes needed;
+ * otherwise writes *length bytes (no terminator; TSAT_E_RANGE if capacity
+ * is too small). */
+tsat_status tsat_write_dimacs(int32_t V, int64_t C, const int64_t* clause_ptr, const int32_t* dimacs_lits,
+                              const uint8_t* sigma, char* out, size_t capacity, size_t* length);
+
+/* Number of clauses the 0/1 assignment model (V bytes) leaves unsatisfied
+ * (0: model is a satisfying assignment; an empty clause is never satisfied). */
+tsat_status tsat_verify_model(int32_t V, int64_t C, const int64_t* clause_ptr, const int32_t* dimacs_lits,
+                              const uint8_t* model, int64_t* n_unsat);
+
 /* ---------------------------------------------------------------- CPU hand-off
  * PAPER.md §4.2 l.277-287: once the best candidate satisfies > 99 % of the
  * clauses, the k most confident literals of each exported candidate

@@ -19,10 +19,15 @@ from .binding import (  # noqa: F401
     cdcl_portfolio,
     cdcl_solve,
     config_default,
+    gen_industrial,
+    gen_planted,
     load_library,
     nccl_unique_id,
     parse_dimacs,
+    verify_model,
+    write_dimacs,
 )
 
 __all__ = ["Solver", "StepInfo", "TsatError", "cdcl_portfolio", "cdcl_solve", "config_default", "load_library", "nccl_unique_id",
-           "parse_dimacs", "LIB_PATH"]
+           "parse_dimacs", "LIB_PATH", "gen_planted", "gen_industrial", "write_dimacs",
+           "verify_model"]

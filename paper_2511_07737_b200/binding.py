@@ -85,6 +85,11 @@ _SIGS = {
                                    ct.POINTER(tsat_cdcl_result)]),
     "tsat_cdcl_portfolio": (ct.c_int, [ct.c_int32, ct.c_int64, P, P, ct.c_int32, ct.c_int32, P, ct.c_int32,
                                        ct.c_int32, ct.c_double, P, ct.POINTER(tsat_cdcl_result)]),
+    "tsat_gen_planted": (ct.c_int, [ct.c_int32, ct.c_int64, ct.c_int32, ct.c_uint64, ct.c_int32, P, P, P]),
+    "tsat_gen_industrial": (ct.c_int, [ct.c_int32, ct.c_int64, ct.c_uint64, ct.c_double, ct.c_int32, P, P, P,
+                                       ct.c_int64, P]),
+    "tsat_write_dimacs": (ct.c_int, [ct.c_int32, ct.c_int64, P, P, P, P, ct.c_size_t, ct.POINTER(ct.c_size_t)]),
+    "tsat_verify_model": (ct.c_int, [ct.c_int32, ct.c_int64, P, P, P, ct.POINTER(ct.c_int64)]),
     "tsat_export_model": (ct.c_int, [P, ct.c_int64, P]),
     "tsat_get_solution": (ct.c_int, [P, P, ct.POINTER(ct.c_int64), ct.POINTER(ct.c_int64)]),
     "tsat_get_state": (ct.c_int, [P, P, P, P, ct.c_size_t, ct.POINTER(ct.c_int64)]),
@@ -137,6 +142,68 @@ def parse_dimacs(text: bytes) -> tsat_cnf_info:
     if s:
         raise TsatError(s, "DIMACS rejected")
     return info
+
+
+def gen_planted(V: int, C: int, k: int = 3, seed: int = 1, hidden: int = 1):
+    """tsat_gen_planted (host only): (clause_ptr int64[C+1], lits int32[C*k], sigma uint8[V])."""
+    ptr = np.zeros(C + 1, np.int64)
+    lits = np.zeros(max(C * k, 1), np.int32)
+    sigma = np.zeros(V, np.uint8)
+    st = load_library().tsat_gen_planted(int(V), int(C), int(k), int(seed) & (2**64 - 1), int(hidden), _ptr(ptr),
+                                         _ptr(lits), _ptr(sigma))
+    if st:
+        raise TsatError(st, "tsat_gen_planted")
+    return ptr, lits[:C * k], sigma
+
+
+def gen_industrial(V: int, C: int, seed: int = 1, alpha: float = 0.82, len_probs=None):
+    """tsat_gen_industrial (host only); len_probs maps clause length -> probability
+    (default SURVEY §8(d): {2:.40, 3:.30, 4:.12, 5:.08, 6:.06, 7:.04})."""
+    lp = len_probs or {2: .40, 3: .30, 4: .12, 5: .08, 6: .06, 7: .04}
+    kmax = max(lp)
+    probs = np.zeros(kmax + 1, np.float64)
+    for k, p in lp.items():
+        probs[k] = p
+    ptr = np.zeros(C + 1, np.int64)
+    lits = np.zeros(max(C * kmax, 1), np.int32)
+    sigma = np.zeros(V, np.uint8)
+    st = load_library().tsat_gen_industrial(int(V), int(C), int(seed) & (2**64 - 1), float(alpha), kmax, _ptr(probs),
+                                            _ptr(ptr), _ptr(lits), lits.size, _ptr(sigma))
+    if st:
+        raise TsatError(st, "tsat_gen_industrial")
+    return ptr, lits[:ptr[-1]].copy(), sigma
+
+
+def write_dimacs(V: int, clause_ptr, lits, sigma=None) -> bytes:
+    """tsat_write_dimacs (host only)."""
+    ptr = np.ascontiguousarray(clause_ptr, np.int64)
+    lt = np.ascontiguousarray(lits, np.int32)
+    sg = None if sigma is None else np.ascontiguousarray(sigma, np.uint8)
+    n = ct.c_size_t()
+    C = len(ptr) - 1
+    L = load_library()
+    args = (int(V), C, _ptr(ptr), _ptr(lt) if lt.size else None, _ptr(sg) if sg is not None else None)
+    st = L.tsat_write_dimacs(*args, None, 0, ct.byref(n))
+    if st:
+        raise TsatError(st, "tsat_write_dimacs")
+    buf = ct.create_string_buffer(n.value)
+    st = L.tsat_write_dimacs(*args, buf, n.value, ct.byref(n))
+    if st:
+        raise TsatError(st, "tsat_write_dimacs")
+    return buf.raw[:n.value]
+
+
+def verify_model(V: int, clause_ptr, lits, model) -> int:
+    """tsat_verify_model (host only): clauses the 0/1 assignment leaves unsatisfied."""
+    ptr = np.ascontiguousarray(clause_ptr, np.int64)
+    lt = np.ascontiguousarray(lits, np.int32)
+    m = np.ascontiguousarray(model, np.uint8)
+    out = ct.c_int64()
+    st = load_library().tsat_verify_model(int(V), len(ptr) - 1, _ptr(ptr), _ptr(lt) if lt.size else None, _ptr(m),
+                                          ct.byref(out))
+    if st:
+        raise TsatError(st, "tsat_verify_model")
+    return int(out.value)
 
 
 def cdcl_solve(cnf, assumptions=(), conflict_limit: int = 0, seed: int = 0):
