@@ -103,6 +103,16 @@ def _bind(L):
         "or_gmax": (f64, [i32, i32, P, P]),
         "or_hist_stream": (None, [i32, P, P, i32, i32, P, P, P]),
         "or_backward_rows": (None, [i32, P, P, i32, i32, P, P, P, i32, P, P, P]),
+        "or_init64": (None, [i32, i64, i32, u64, P, P, P]),
+        "or_row_sums64": (i32, [i32, i32, P, P, P, i32]),
+        "or_row_finish64": (None, [i32, i64, P, P, i32, f64, P, P, P, P]),
+        "or_binarize64": (None, [i32, i32, P, P, P]),
+        "or_backward64": (None, [i32, i32, P, P, i32, i32, P, P, P]),
+        "or_jacobian_partial64": (None, [i32, i32, P, P, P, i64, f64, f64, P, P, P]),
+        "or_grad64": (None, [i32, i32, P, P, P, P, i32, P]),
+        "or_adamw64": (None, [i32, i64, i32, P, P, P, P, i64, i64, f64, f64, f64, f64, f64, f64, u64]),
+        "or_abs_max64": (f64, [ct.c_size_t, P]),
+        "or_gmax64": (f64, [i32, i32, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -242,6 +252,7 @@ class Config:
     eps_norm: float = 1e-8
     reset_moments_on_restart: int = 0
     tau_final: float = 0.0      # > 0: SmoothMin temperature annealed within each LR cycle (variant f2, R29)
+    state_fp64: int = 0         # 1: theta, m, v and every fp32 rounding of R6/R13/R26/R27 in fp64 (variant f2, R30)
 
 
 class LocalComm:
@@ -319,7 +330,14 @@ class Oracle:
         lits = np.abs(cnf.lits.astype(np.int64)) - 1
         self.occ = np.bincount(lits, minlength=cnf.V).astype(np.int32)
         if init:
-            self.theta, self.m, self.v = init_theta(cnf.V, self.N, self.seed, self.n0, self.Nl)
+            if self.cfg.state_fp64:
+                V, Nl = cnf.V, self.Nl
+                self.theta = np.empty((V, Nl), np.float64)
+                self.m = np.empty((V, Nl), np.float64)
+                self.v = np.empty((V, Nl), np.float64)
+                lib().or_init64(V, self.n0, Nl, self.seed, _p(self.theta), _p(self.m), _p(self.v))
+            else:
+                self.theta, self.m, self.v = init_theta(cnf.V, self.N, self.seed, self.n0, self.Nl)
         self.comm = LocalComm()
 
     @property
@@ -335,15 +353,27 @@ class Oracle:
         return self.Nl if self.per_shard else self.N
 
     def set_state(self, theta, m, v, t):
-        self.theta = np.ascontiguousarray(theta, np.float32).copy()
-        self.m = np.ascontiguousarray(m, np.float32).copy()
-        self.v = np.ascontiguousarray(v, np.float32).copy()
+        dt = np.float64 if self.cfg.state_fp64 else np.float32
+        self.theta = np.ascontiguousarray(theta, dt).copy()
+        self.m = np.ascontiguousarray(m, dt).copy()
+        self.v = np.ascontiguousarray(v, dt).copy()
         self.t = int(t)
 
     def row_stats(self):
         V = self.cnf.V
         Q = np.empty(V, np.int64)
         L = lib()
+        if self.cfg.state_fp64:                   # R30: 128-bit row sums at 2^-64 (single shard)
+            assert not isinstance(self.comm, object) or isinstance(self.comm, LocalComm) or self.per_shard, \
+                "fp64 state: one shard (or per-shard normalisation)"
+            Qlo = np.empty(V, np.uint64)
+            bad = L.or_row_sums64(V, self.Nl, _p(self.theta), _p(Q), _p(Qlo), int(self.cfg.normalize == 3))
+            assert bad == 0, "row-sum bound |theta| < 2^14 (R30)"
+            mu = np.empty(V); d = np.empty(V); rho = np.empty(V); guard = np.empty(V, np.uint8)
+            L.or_row_finish64(V, self.Nnorm, _p(Q), _p(Qlo), self.cfg.normalize, self.cfg.eps_norm, _p(mu), _p(d),
+                              _p(rho), _p(guard))
+            self.Qlo = Qlo
+            return Q, mu, d, rho, guard
         (L.or_row_sums_abs if self.cfg.normalize == 3 else L.or_row_sums)(V, self.Nl, _p(self.theta), _p(Q))
         if not self.per_shard:
             Q = self.comm.sum_i64(Q)
@@ -361,7 +391,8 @@ class Oracle:
         # Eq. 5 normalisation statistics and Eq. 2 binarisation
         Q, mu, d, rho, guard = self.row_stats()
         b = np.empty((V, Nl), np.uint8)
-        L.or_binarize(V, Nl, _p(self.theta), _p(d), _p(b))
+        f64 = bool(cfg.state_fp64)
+        (L.or_binarize64 if f64 else L.or_binarize)(V, Nl, _p(self.theta), _p(d), _p(b))
         # Eq. 1 and §3.1.4
         R = clause_eval(cnf, b)
         h = histogram(R, K)
@@ -371,22 +402,35 @@ class Oracle:
         g32 = g.astype(np.float32)                 # R26: rounded once to fp32
         Sall = self.comm.gather_f64(S)
         loss = -float(sum(float(x) for x in Sall))
-        gmax = L.or_gmax(Nl, K, _p(g32), _p(rmin))
-        thmax = L.or_abs_max(self.theta.size, _p(self.theta))
+        if f64:                                    # R30: the g table, G and J terms stay fp64
+            gmax = L.or_gmax64(Nl, K, _p(np.ascontiguousarray(g)), _p(rmin))
+            thmax = L.or_abs_max64(self.theta.size, _p(self.theta))
+        else:
+            gmax = L.or_gmax(Nl, K, _p(g32), _p(rmin))
+            thmax = L.or_abs_max(self.theta.size, _p(self.theta))
         if not self.per_shard:
             gmax, thmax = self.comm.max(gmax), self.comm.max(thmax)
         # STE backward and Eq. 5 Jacobian
-        G = backward(cnf, R, g32)                     # fp32 values (R27)
         I = np.empty(V, np.int64); s = np.empty(V, np.int32); valid = np.empty(V, np.uint8)
-        L.or_jacobian_partial(V, Nl, _p(G), _p(self.theta), _p(self.occ), self.Nnorm, gmax, thmax, _p(I), _p(s),
-                              _p(valid))
+        if f64:
+            G = np.empty((V, Nl), np.float64)
+            L.or_backward64(V, cnf.C, _p(cnf.clause_ptr), _p(cnf.lits), Nl, K, _p(np.ascontiguousarray(R)),
+                            _p(np.ascontiguousarray(g)), _p(G))
+            L.or_jacobian_partial64(V, Nl, _p(G), _p(self.theta), _p(self.occ), self.Nnorm, gmax, thmax, _p(I),
+                                    _p(s), _p(valid))
+        else:
+            G = backward(cnf, R, g32)                     # fp32 values (R27)
+            L.or_jacobian_partial(V, Nl, _p(G), _p(self.theta), _p(self.occ), self.Nnorm, gmax, thmax, _p(I), _p(s),
+                                  _p(valid))
         if not self.per_shard:
             I = self.comm.sum_i64(I)
         J = np.empty(V); cv = np.empty(V)
         L.or_jacobian_finish(V, self.Nnorm, _p(I), _p(s), _p(valid), _p(rho), _p(guard), cfg.normalize, _p(J),
                              _p(cv))
-        grad = np.empty((V, Nl), np.float32)
-        if cfg.normalize == 3:
+        grad = np.empty((V, Nl), np.float64 if f64 else np.float32)
+        if f64:
+            L.or_grad64(V, Nl, _p(G), _p(rho), _p(cv), _p(self.theta), int(cfg.normalize == 3), _p(grad))
+        elif cfg.normalize == 3:
             L.or_grad_mag(V, Nl, _p(G), _p(rho), _p(cv), _p(self.theta), _p(grad))
         else:
             L.or_grad(V, Nl, _p(G), _p(rho), _p(cv), _p(grad))
@@ -400,8 +444,9 @@ class Oracle:
         if reset:
             self.m[:] = 0.0
             self.v[:] = 0.0
-        L.or_adamw(V, self.n0, Nl, _p(self.theta), _p(self.m), _p(self.v), _p(grad), t, bstep, lr,
-                   cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, cfg.noise_sigma, self.seed)
+        (L.or_adamw64 if f64 else L.or_adamw)(V, self.n0, Nl, _p(self.theta), _p(self.m), _p(self.v), _p(grad), t,
+                                               bstep, lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay,
+                                               cfg.noise_sigma, self.seed)
         self.t = t + 1
         return StepOut(t=t, bits=b, R=R, h=h, unsat=unsat, S=S, g=g, g32=g32, loss=loss, G=G, grad=grad,
                        J=J, d=d, gmax=gmax, thmax=thmax, best_unsat=best_unsat, best_idx=best_idx,

@@ -588,3 +588,237 @@ void or_backward_rows(int C, const int64_t* cptr, const int32_t* lits, int Nl, i
         }
     }
 }
+
+/* ------------------------------------------------------------------ fp64 state
+ * Variant f2 "fp64 state" (SPEC S:278 chose double throughout; reading R30):
+ * theta, m, v in fp64 and every rounding R13/R26/R27/R27b/R6 makes to fp32
+ * is made to fp64 instead.  Same definitions, same operation order:
+ *   init: the fp64 Box-Muller value (not rounded to fp32);
+ *   Q_v = sum round_half_even(theta 2^32) (theta 2^32 is exact in fp64);
+ *   g table: Eq. 4's derivative in fp64 (not rounded);
+ *   G_vn = fma chain over r ascending of (cneg - cpos)[r] g_n[r] in fp64;
+ *   J_v: s_v = 61 - ceil(log2(N occ gmax thmax)) clamped to [-1022, 1023],
+ *        terms llrint(G (theta 2^s)) with fp64 products;
+ *   grad = fma(G, rho, -c) in fp64 (normalize 3: -sign(theta) c);
+ *   AdamW in fp64 with the host scalars unrounded (R6b/R6c order).  */
+void or_init64(int V, int64_t n0, int Nl, uint64_t seed, double* theta, double* m, double* vv)
+{
+    const double two_pi = 6.283185307179586;
+    const double two_m32 = 2.3283064365386963e-10; /* 2^-32 */
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    #pragma omp parallel for schedule(static)
+    for (int v = 0; v < V; ++v) {
+        for (int j = 0; j < Nl; ++j) {
+            int64_t n = n0 + j;
+            uint32_t ctr[4] = {(uint32_t)(n >> 2), (uint32_t)v, 0u, 0u};
+            uint32_t x[4];
+            or_philox4x32_10(ctr, key, x);
+            int q = (int)(n & 3);
+            int pair = q >> 1;
+            double u1 = ((double)x[2 * pair] + 1.0) * two_m32;
+            double u2 = (double)x[2 * pair + 1] * two_m32;
+            double r = sqrt(-2.0 * log(u1));
+            double a = two_pi * u2;
+            theta[(size_t)v * Nl + j] = (q & 1) ? r * sin(a) : r * cos(a);
+            m[(size_t)v * Nl + j] = 0.0;
+            vv[(size_t)v * Nl + j] = 0.0;
+        }
+    }
+}
+
+/* R30 row sums: Q_v = sum_n round_half_even(theta_vn 2^64) in a 128-bit
+ * integer (theta 2^64 is exact in fp64; |theta| < 2^14 and N <= 2^30 keep
+ * |Q| < 2^108), returned as hi (signed) and lo (unsigned) 64-bit halves,
+ * Q = hi 2^64 + lo.  The sum is exact and order-free, like R10's, but at
+ * the 2^-64 resolution an fp64 state needs.  magnitude: sum |theta| (R28). */
+static __int128 round64_q(double x)
+{
+    double y = x * 18446744073709551616.0;          /* 2^64, exact */
+    if (fabs(y) < 4503599627370496.0)               /* < 2^52: may have a fraction */
+        return (__int128)llrint(y);                 /* round half even */
+    double hi = floor(y * 5.421010862427522e-20);  /* y 2^-64, exact; an integer-valued double */
+    double lo = y - hi * 18446744073709551616.0;    /* exact, in [0, 2^64) */
+    return (__int128)(int64_t)hi * ((__int128)1 << 64) + (__int128)(uint64_t)lo;
+}
+
+int or_row_sums64(int V, int Nl, const double* theta, int64_t* Qhi, uint64_t* Qlo, int magnitude)
+{
+    int bad = 0;
+    #pragma omp parallel for schedule(static) reduction(|:bad)
+    for (int v = 0; v < V; ++v) {
+        __int128 acc = 0;
+        for (int j = 0; j < Nl; ++j) {
+            double x = theta[(size_t)v * Nl + j];
+            if (magnitude) x = fabs(x);
+            if (!(fabs(x) < 16384.0)) bad = 1;
+            acc += round64_q(x);
+        }
+        Qhi[v] = (int64_t)(acc >> 64);
+        Qlo[v] = (uint64_t)acc;
+    }
+    return bad;
+}
+
+/* R30 row statistics: S = (double)hi 2^64 + (double)lo (two roundings, in
+ * this order), mu = (S 2^-64) / N, then d, rho, guard as or_row_finish. */
+void or_row_finish64(int V, int64_t N, const int64_t* Qhi, const uint64_t* Qlo, int normalize, double eps_norm,
+                     double* mu, double* d, double* rho, uint8_t* guard)
+{
+    for (int v = 0; v < V; ++v) {
+        if (!normalize) { mu[v] = 0.0; d[v] = 1.0; rho[v] = 1.0; guard[v] = 1; continue; }
+        double S = (double)Qhi[v] * 18446744073709551616.0 + (double)Qlo[v];
+        double m = (S * 5.421010862427522e-20) / (double)N;
+        double a = fabs(m);
+        double mag = a > eps_norm ? a : eps_norm;
+        mu[v] = m;
+        d[v] = m >= 0.0 ? mag : -mag;
+        rho[v] = 1.0 / d[v];
+        guard[v] = (uint8_t)(a <= eps_norm);
+    }
+}
+
+void or_binarize64(int V, int Nl, const double* theta, const double* d, uint8_t* b)
+{
+    #pragma omp parallel for schedule(static)
+    for (int v = 0; v < V; ++v)
+        for (int j = 0; j < Nl; ++j) {
+            double x = theta[(size_t)v * Nl + j];
+            b[(size_t)v * Nl + j] = (uint8_t)((x > 0.0 && d[v] > 0.0) || (x < 0.0 && d[v] < 0.0));
+        }
+}
+
+void or_backward64(int V, int C, const int64_t* cptr, const int32_t* lits, int Nl, int K,
+                   const uint8_t* R, const double* g, double* G)
+{
+    int64_t* vptr = (int64_t*)calloc((size_t)V + 1, sizeof(int64_t));
+    int64_t nnz = cptr[C];
+    int32_t* occ_c = (int32_t*)malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(int32_t));
+    int8_t* occ_s = (int8_t*)malloc((size_t)(nnz > 0 ? nnz : 1));
+    for (int64_t l = 0; l < nnz; ++l) vptr[(lits[l] > 0 ? lits[l] : -lits[l])]++;
+    for (int v = 0; v < V; ++v) vptr[v + 1] += vptr[v];
+    int64_t* fill = (int64_t*)malloc(((size_t)V + 1) * sizeof(int64_t));
+    memcpy(fill, vptr, ((size_t)V + 1) * sizeof(int64_t));
+    for (int c = 0; c < C; ++c)
+        for (int64_t l = cptr[c]; l < cptr[c + 1]; ++l) {
+            int v = (lits[l] > 0 ? lits[l] : -lits[l]) - 1;
+            occ_c[fill[v]] = c;
+            occ_s[fill[v]] = lits[l] > 0 ? 1 : -1;
+            fill[v]++;
+        }
+#pragma omp parallel
+    {
+    int32_t* cnt = (int32_t*)malloc((size_t)Nl * (K + 1) * sizeof(int32_t));
+#pragma omp for schedule(dynamic, 16)
+    for (int v = 0; v < V; ++v) {
+        memset(cnt, 0, (size_t)Nl * (K + 1) * sizeof(int32_t));
+        for (int64_t o = vptr[v]; o < vptr[v + 1]; ++o) {
+            const uint8_t* Rrow = R + (size_t)occ_c[o] * Nl;
+            int delta = occ_s[o] < 0 ? +1 : -1;  /* cneg - cpos */
+            for (int j = 0; j < Nl; ++j) cnt[(size_t)j * (K + 1) + Rrow[j]] += delta;
+        }
+        for (int j = 0; j < Nl; ++j) {
+            double acc = 0.0;
+            for (int r = 0; r <= K; ++r)
+                acc = fma((double)cnt[(size_t)j * (K + 1) + r], g[(size_t)j * (K + 1) + r], acc);
+            G[(size_t)v * Nl + j] = acc;
+        }
+    }
+    free(cnt);
+    }
+    free(fill); free(occ_s); free(occ_c); free(vptr);
+}
+
+void or_jacobian_partial64(int V, int Nl, const double* G, const double* theta,
+                           const int32_t* occ, int64_t N, double gmax, double thmax,
+                           int64_t* I, int32_t* s_out, uint8_t* valid)
+{
+    #pragma omp parallel for schedule(static)
+    for (int v = 0; v < V; ++v) {
+        double x = (double)N * (double)occ[v];
+        x = x * gmax;
+        x = x * thmax;
+        I[v] = 0; s_out[v] = 0; valid[v] = 0;
+        if (occ[v] == 0 || !(x > 0.0)) continue;
+        int s = 61 - ceil_log2(x);
+        if (s > 1023) s = 1023;
+        if (s < -1022) s = -1022;
+        const double p2 = ldexp(1.0, s);
+        int64_t acc = 0;
+        for (int j = 0; j < Nl; ++j) {
+            double ts = theta[(size_t)v * Nl + j] * p2;
+            double p = G[(size_t)v * Nl + j] * ts;
+            acc += (int64_t)llrint(p);
+        }
+        I[v] = acc; s_out[v] = s; valid[v] = 1;
+    }
+}
+
+void or_grad64(int V, int Nl, const double* G, const double* rho, const double* cv, const double* theta,
+               int magnitude, double* grad)
+{
+    #pragma omp parallel for schedule(static)
+    for (int v = 0; v < V; ++v)
+        for (int j = 0; j < Nl; ++j) {
+            double c = cv[v];
+            if (magnitude) {
+                const double x = theta[(size_t)v * Nl + j];
+                c = x > 0.0 ? c : (x < 0.0 ? -c : 0.0);
+            }
+            grad[(size_t)v * Nl + j] = fma(G[(size_t)v * Nl + j], rho[v], -c);
+        }
+}
+
+void or_adamw64(int V, int64_t n0, int Nl, double* theta, double* m, double* vv, const double* grad,
+                int64_t t, int64_t bstep, double lr, double beta1, double beta2, double eps, double wd,
+                double noise_sigma, uint64_t seed)
+{
+    double s = (double)bstep;
+    double wdf = 1.0 - lr * wd;
+    double a1 = 1.0 - beta1;
+    double a2 = 1.0 - beta2;
+    double bc1 = 1.0 - pow(beta1, s);
+    double bc2 = 1.0 - pow(beta2, s);
+    double nss = -(lr / bc1);
+    double rbc2 = 1.0 / sqrt(bc2);
+    double nz = lr * noise_sigma;
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+#pragma omp parallel for schedule(static)
+    for (int v = 0; v < V; ++v)
+        for (int j = 0; j < Nl; ++j) {
+            size_t i = (size_t)v * Nl + j;
+            double g = grad[i];
+            double th = theta[i] * wdf;
+            double mm = fma(a1, g - m[i], m[i]);
+            double vb = vv[i] * beta2;
+            double vn = fma(a2 * g, g, vb);
+            double den = sqrt(vn) * rbc2 + eps;
+            th = th + (nss * mm) / den;
+            if (noise_sigma != 0.0) {
+                int64_t n = n0 + j;
+                uint32_t ctr[4] = {(uint32_t)(n >> 2), (uint32_t)v, (uint32_t)(1 + t), 0u};
+                uint32_t x[4];
+                or_philox4x32_10(ctr, key, x);
+                double xi = (double)(x[n & 3] >> 8) * 5.9604644775390625e-08 - 0.5;
+                th = th + nz * xi;
+            }
+            theta[i] = th; m[i] = mm; vv[i] = vn;
+        }
+}
+
+double or_abs_max64(size_t n, const double* x)
+{
+    double mx = 0.0;
+    for (size_t i = 0; i < n; ++i) { double a = fabs(x[i]); if (a > mx) mx = a; }
+    return mx;
+}
+
+double or_gmax64(int Nl, int K, const double* g, const int32_t* rmin)
+{
+    double mx = 0.0;
+    for (int j = 0; j < Nl; ++j)
+        for (int r = rmin[j]; r <= K; ++r) {
+            double a = fabs(g[(size_t)j * (K + 1) + r]);
+            if (a > mx) mx = a;
+        }
+    return mx;
+}
