@@ -86,6 +86,10 @@ typedef struct {
                                 the 2V x N assignment matrix, SURVEY 8(f) f4 experiment; library-owned
                                 buffers of ceil(C/128)*128 x 2V and ceil(N/256)*256 x 2V bytes, TSAT_E_RANGE
                                 above 2^31 bytes each) */
+    int32_t state_fp64;      /* 1 = theta, m, v in fp64 and every fp32 rounding of the step in fp64 (variant
+                                f2, SPEC's choice; reading R30): library-owned state of 48 B per
+                                (variable, candidate); one GPU only (TSAT_E_UNSUPPORTED with world > 1); the
+                                state is read / written with tsat_get_state64 / tsat_set_state64 */
 } tsat_config;
 
 typedef struct {
@@ -256,6 +260,11 @@ tsat_status tsat_get_solution(tsat_ctx ctx, uint8_t* host_values, int64_t* idx, 
 /* elems = elements of each non-NULL array; must equal V * N_local (TSAT_E_ARG
  * otherwise, e.g. a checkpoint of another world size or batch). */
 tsat_status tsat_get_state(tsat_ctx ctx, float* theta, float* m, float* v, size_t elems, int64_t* t);
+/* The same for a batch initialised with config.state_fp64 = 1 (fp64 arrays, V * N_local elements each);
+ * the fp32 calls return TSAT_E_STATE on such a batch and these on an fp32 one. */
+tsat_status tsat_get_state64(tsat_ctx ctx, double* theta, double* m, double* v, size_t elems, int64_t* t);
+tsat_status tsat_set_state64(tsat_ctx ctx, const double* theta, const double* m, const double* v, size_t elems,
+                             int64_t t);
 tsat_status tsat_set_state(tsat_ctx ctx, const float* theta, const float* m, const float* v, size_t elems, int64_t t);
 
 /* Rows rows[0..nrows) (0-based variables) of theta, m, v into host arrays of

@@ -34,7 +34,7 @@ class tsat_config(ct.Structure):
                 ("eps", ct.c_double), ("weight_decay", ct.c_double), ("lr0", ct.c_double), ("lr_min", ct.c_double),
                 ("decay_factor", ct.c_double), ("decay_every", ct.c_int32), ("restart_every", ct.c_int32),
                 ("noise_sigma", ct.c_double), ("eps_norm", ct.c_double), ("reset_moments_on_restart", ct.c_int32),
-                ("tau_final", ct.c_double), ("clause_eval", ct.c_int32)]
+                ("tau_final", ct.c_double), ("clause_eval", ct.c_int32), ("state_fp64", ct.c_int32)]
 
 
 class tsat_cnf_info(ct.Structure):
@@ -94,6 +94,8 @@ _SIGS = {
     "tsat_get_solution": (ct.c_int, [P, P, ct.POINTER(ct.c_int64), ct.POINTER(ct.c_int64)]),
     "tsat_get_state": (ct.c_int, [P, P, P, P, ct.c_size_t, ct.POINTER(ct.c_int64)]),
     "tsat_set_state": (ct.c_int, [P, P, P, P, ct.c_size_t, ct.c_int64]),
+    "tsat_get_state64": (ct.c_int, [P, P, P, P, ct.c_size_t, ct.POINTER(ct.c_int64)]),
+    "tsat_set_state64": (ct.c_int, [P, P, P, P, ct.c_size_t, ct.c_int64]),
     "tsat_debug_copy": (ct.c_int, [P, ct.c_int32, P, ct.c_size_t]),
     "tsat_get_rows": (ct.c_int, [P, P, ct.c_int32, P, P, P, ct.c_size_t]),
     "tsat_set_profiling": (ct.c_int, [P, ct.c_int32]),
@@ -395,6 +397,7 @@ class Solver:
         self._check(self.lib.tsat_init_batch(self.h, int(N_global), int(seed) & (2**64 - 1), ct.byref(cfg),
                                              ct.c_void_p(self.ws.data_ptr()), nbytes))
         self.N = int(N_global)
+        self.fp64 = bool(cfg.state_fp64)
         self.N_local = self.N // self.world
         self.n0 = self.rank * self.N_local
         return self
@@ -471,24 +474,30 @@ class Solver:
         return out, idx.value, st.value
 
     def get_state(self):
+        """(theta, m, v, t): float32 arrays, or float64 for a batch with state_fp64 = 1."""
         n = self.N_local_count()
-        th = np.empty((self.V, n), np.float32)
+        f64 = getattr(self, "fp64", False)
+        th = np.empty((self.V, n), np.float64 if f64 else np.float32)
         m = np.empty_like(th)
         v = np.empty_like(th)
         t = ct.c_int64()
-        self._check(self.lib.tsat_get_state(self.h, _ptr(th), _ptr(m), _ptr(v), th.size, ct.byref(t)))
+        fn = self.lib.tsat_get_state64 if f64 else self.lib.tsat_get_state
+        self._check(fn(self.h, _ptr(th), _ptr(m), _ptr(v), th.size, ct.byref(t)))
         return th, m, v, t.value
 
     def set_state(self, theta, m, v, t: int):
         shape = (self.V, self.N_local_count())
+        f64 = getattr(self, "fp64", False)
+        dt = np.float64 if f64 else np.float32
         arrs = []
         for name, x in (("theta", theta), ("m", m), ("v", v)):
             x = np.asarray(x)
-            if x.dtype != np.float32 or x.shape != shape:
-                raise ValueError(f"{name} must be float32 of shape {shape} (got {x.dtype} {x.shape})")
+            if x.dtype != dt or x.shape != shape:
+                raise ValueError(f"{name} must be {dt.__name__} of shape {shape} (got {x.dtype} {x.shape})")
             arrs.append(np.ascontiguousarray(x))
         th, mm, vv = arrs
-        self._check(self.lib.tsat_set_state(self.h, _ptr(th), _ptr(mm), _ptr(vv), th.size, int(t)))
+        fn = self.lib.tsat_set_state64 if f64 else self.lib.tsat_set_state
+        self._check(fn(self.h, _ptr(th), _ptr(mm), _ptr(vv), th.size, int(t)))
 
     def get_rows(self, rows):
         r = np.ascontiguousarray(rows, np.int32)

@@ -33,7 +33,7 @@ def _nccl_include() -> str:
 
 
 NCCL_INC = _nccl_include()
-SOURCES = ["capi.cu", "launch.cu", "k_clause.cu", "k_misc.cu", "k_update.cu", "k_update_blk.cu", "k_dense.cu", "k_shard.cu", "comm.cpp", "host_cnf.cpp", "host_cdcl.cpp", "host_gen.cpp"]
+SOURCES = ["capi.cu", "launch.cu", "k_clause.cu", "k_misc.cu", "k_update.cu", "k_update_blk.cu", "k_dense.cu", "k_fp64.cu", "k_shard.cu", "comm.cpp", "host_cnf.cpp", "host_cdcl.cpp", "host_gen.cpp"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -83,6 +83,11 @@ struct tsat_ctx_s {
     uint8_t* dP = nullptr;
     uint8_t* dAL = nullptr;
     int dKp = 0, dCp = 0;
+    // fp64 state (config.state_fp64 = 1, k_fp64.cu): library-owned
+    double *th64 = nullptr, *m64 = nullptr, *v64 = nullptr, *G64 = nullptr, *gt64 = nullptr;
+    long long* J64 = nullptr;
+    unsigned long long* Qp64 = nullptr;
+    uint32_t *Pw64 = nullptr, *Nw64 = nullptr;
     int upd_chunk = 0, upd_gs_global = 0;
     bool chunked = false;               // N too large for the fused kernel: split sequence, no collectives at W = 1
     size_t upd_smem = 0;
@@ -275,13 +280,17 @@ StepArgs step_args(tsat_ctx ctx) {
 #define TSAT_PDL 1
 #endif
     // PDL on the fused W = 1 sequence (one stream, no forked k_hub branch)
-    a.pdl = TSAT_PDL && !ctx->profiling && !ctx->sharded && !ctx->chunked && !ctx->peer && ctx->cnf.n_hub_sc == 0;
+    a.pdl = TSAT_PDL && !ctx->profiling && !ctx->sharded && !ctx->chunked && !ctx->peer && ctx->cnf.n_hub_sc == 0 &&
+            ctx->th64 == nullptr;
     a.upd_NG = ctx->upd_NG;
     a.upd_grid = ctx->upd_grid;
     a.upd_smem = ctx->upd_smem;
     a.upd_rec_cap = std::max(64, (ctx->cnf.max_rec_words + 63) / 64 * 64);
     a.upd_RB = ctx->upd_RB;
     a.upd_blk_cap = ctx->upd_blk_cap;
+    a.fp64 = ctx->th64 != nullptr;
+    a.th64 = ctx->th64; a.m64 = ctx->m64; a.v64 = ctx->v64; a.G64 = ctx->G64; a.gt64 = ctx->gt64;
+    a.J64 = ctx->J64; a.Qp64 = ctx->Qp64; a.Pw64 = ctx->Pw64; a.Nw64 = ctx->Nw64;
     a.dense = ctx->dP != nullptr;
     a.dP = ctx->dP;
     a.dAL = ctx->dAL;
@@ -346,7 +355,26 @@ StepScalars step_scalars(const tsat_config& c, int64_t t) {
         tau = c.tau * std::pow(c.tau_final / c.tau, (double)(t % c.restart_every) / (double)(c.restart_every - 1));
     s.tau = tau;
     for (int d = 0; d < 16; ++d) s.E[d] = std::exp(-tau * (double)d);
+    // fp64 state (R30): the same AdamW scalars unrounded
+    s.wdf64 = 1.0 - lr * c.weight_decay;
+    s.a1_64 = 1.0 - c.beta1;
+    s.b2_64 = reset ? 0.0 : c.beta2;
+    s.a2_64 = 1.0 - c.beta2;
+    s.nss64 = -(lr / bc1);
+    s.rbc2_64 = 1.0 / std::sqrt(bc2);
+    s.eps64 = c.eps;
+    s.nz64 = lr * c.noise_sigma;
     return s;
+}
+
+void free_fp64(tsat_ctx ctx) {
+    for (void* p : {(void*)ctx->th64, (void*)ctx->m64, (void*)ctx->v64, (void*)ctx->G64, (void*)ctx->gt64,
+                    (void*)ctx->J64, (void*)ctx->Qp64, (void*)ctx->Pw64, (void*)ctx->Nw64})
+        cudaFree(p);
+    ctx->th64 = ctx->m64 = ctx->v64 = ctx->G64 = ctx->gt64 = nullptr;
+    ctx->J64 = nullptr;
+    ctx->Qp64 = nullptr;
+    ctx->Pw64 = ctx->Nw64 = nullptr;
 }
 
 void free_cnf(tsat_ctx ctx) {
@@ -441,6 +469,11 @@ tsat_status check_batch(tsat_ctx ctx, bool need_step) {
 tsat_status state_stats(tsat_ctx ctx, const StepArgs& a, int64_t t) {
     uint32_t* A = (t & 1) ? a.A1 : a.A0;
     unsigned int* thm = &a.ds->thmax_bits[t & 1];
+    if (a.fp64) {                                  // R30 (one GPU)
+        CK(launch_rowstats64(a, t, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        return TSAT_OK;
+    }
     if (ctx->peer) {
         const unsigned gen = ++ctx->xgen;
         CK(launch_rows_partial(a, a.theta, thm, ctx->stream));
@@ -528,7 +561,7 @@ tsat_status launch_steps(tsat_ctx ctx, int k) {
     // k_hub reads only the evaluated state's bit planes, so (unless every
     // kernel is being timed) it runs on a forked capture branch beside
     // k_clause and k_gtable and joins before k_update
-    const bool fork_hub = !ctx->profiling && ctx->cnf.n_hub_sc > 0;
+    const bool fork_hub = !ctx->profiling && ctx->cnf.n_hub_sc > 0 && ctx->th64 == nullptr;
     if (fork_hub && !ctx->cap_side) {
         CK(cudaStreamCreateWithFlags(&ctx->cap_side, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
@@ -658,6 +691,7 @@ tsat_status tsat_config_default(tsat_config* out) {
     out->reset_moments_on_restart = 0;
     out->tau_final = 0.0;
     out->clause_eval = 0;
+    out->state_fp64 = 0;
     out->eps_norm = 1e-8;
     return TSAT_OK;
 }
@@ -915,6 +949,26 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
         ctx->t = 0;
         ctx->steps_done = 0;
         CK(cudaSetDevice(ctx->device));
+        // fp64 state (f2, R30): library-owned 48 B per (v, n) + G, fp64 g table, row partials
+        free_fp64(ctx);
+        if (c.state_fp64) {
+            if (c.state_fp64 != 1) return fail(ctx, TSAT_E_ARG, "state_fp64 must be 0 or 1");
+            if (ctx->world > 1 || ctx->sharded || ctx->peer || ctx->chunked)
+                return fail(ctx, TSAT_E_UNSUPPORTED, "state_fp64: one GPU, fused path only");
+            const size_t VN = (size_t)ctx->cnf.V * ctx->N, nb = (size_t)fp64_blocks_per_row(ctx->N);
+            const size_t V1 = (size_t)std::max(ctx->cnf.V, 1);
+            CK(cudaMalloc(&ctx->th64, std::max<size_t>(VN, 1) * 8));
+            CK(cudaMalloc(&ctx->m64, std::max<size_t>(VN, 1) * 8));
+            CK(cudaMalloc(&ctx->v64, std::max<size_t>(VN, 1) * 8));
+            CK(cudaMalloc(&ctx->G64, std::max<size_t>(VN, 1) * 8));
+            CK(cudaMalloc(&ctx->gt64, (size_t)ctx->KB * ctx->N * 8));
+            CK(cudaMalloc(&ctx->J64, V1 * 8));
+            CK(cudaMalloc(&ctx->Qp64, V1 * nb * 16));
+            CK(cudaMalloc(&ctx->Pw64, V1 * (ctx->N / 32) * 4));
+            CK(cudaMalloc(&ctx->Nw64, V1 * (ctx->N / 32) * 4));
+            CK(cudaMemset(ctx->J64, 0, V1 * 8));
+            CK(cudaMemset(ctx->G64, 0, std::max<size_t>(VN, 1) * 8));
+        }
         // dense clause evaluation (f4 experiment): P (C x 2V) and A (N x 2V) as uint8, K-major
         cudaFree(ctx->dP);
         cudaFree(ctx->dAL);
@@ -990,7 +1044,8 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
         init.info_best_idx = -1;
         *ctx->h_scal = init;
         CK(cudaMemcpyAsync(a.ds, ctx->h_scal, sizeof(DevScalars), cudaMemcpyHostToDevice, ctx->stream));
-        CK(launch_init(a.theta, a.m, a.v, a.V, a.N, ctx->n0, seed, ctx->stream));
+        if (a.fp64) CK(launch_init64(a, seed, ctx->stream));
+        else CK(launch_init(a.theta, a.m, a.v, a.V, a.N, ctx->n0, seed, ctx->stream));
         s = state_stats(ctx, a, 0);
         if (s != TSAT_OK) return s;
         ctx->have_batch = true;
@@ -1115,10 +1170,58 @@ tsat_status tsat_get_solution(tsat_ctx ctx, uint8_t* host_values, int64_t* idx, 
     });
 }
 
+tsat_status tsat_get_state64(tsat_ctx ctx, double* theta, double* m, double* v, size_t elems, int64_t* t) {
+    GUARD_CTX();
+    tsat_status s = check_batch(ctx, false);
+    if (s != TSAT_OK) return s;
+    if (!ctx->th64) return fail(ctx, TSAT_E_STATE, "the batch has fp32 state: use tsat_get_state");
+    if ((theta || m || v) && elems != (size_t)ctx->cnf.V * ctx->N)
+        return fail(ctx, TSAT_E_ARG, "state arrays must hold exactly V * N_local elements");
+    const size_t bytes = (size_t)ctx->cnf.V * ctx->N * 8;
+    if (theta) CK(cudaMemcpyAsync(theta, ctx->th64, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (m) CK(cudaMemcpyAsync(m, ctx->m64, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (v) CK(cudaMemcpyAsync(v, ctx->v64, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (t) *t = ctx->t;
+    return TSAT_OK;
+}
+
+tsat_status tsat_set_state64(tsat_ctx ctx, const double* theta, const double* m, const double* v, size_t elems,
+                             int64_t t) {
+    GUARD_CTX();
+    tsat_status s = check_batch(ctx, false);
+    if (s != TSAT_OK) return s;
+    if (!ctx->th64) return fail(ctx, TSAT_E_STATE, "the batch has fp32 state: use tsat_set_state");
+    if (!theta || !m || !v || t < 0) return fail(ctx, TSAT_E_ARG, "null state or t < 0");
+    if (elems != (size_t)ctx->cnf.V * ctx->N) return fail(ctx, TSAT_E_ARG, "state arrays must hold exactly V * N_local elements");
+    const size_t bytes = (size_t)ctx->cnf.V * ctx->N * 8;
+    StepArgs a = step_args(ctx);
+    CK(cudaMemcpyAsync(ctx->th64, theta, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->m64, m, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->v64, v, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    DevScalars init{};
+    init.best_key = ~0ull;
+    init.sol_step = -1;
+    init.sol_idx = -1;
+    init.info_best_unsat = -1;
+    init.info_best_idx = -1;
+    CK(cudaStreamSynchronize(ctx->stream));
+    *ctx->h_scal = init;
+    CK(cudaMemcpyAsync(a.ds, ctx->h_scal, sizeof(DevScalars), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(a.hist, 0, (size_t)ctx->N * ctx->KB * 4, ctx->stream));
+    CK(cudaMemsetAsync(ctx->J64, 0, (size_t)std::max(ctx->cnf.V, 1) * 8, ctx->stream));
+    s = state_stats(ctx, a, t);
+    if (s != TSAT_OK) return s;
+    ctx->t = t;
+    ctx->steps_done = 0;
+    return TSAT_OK;
+}
+
 tsat_status tsat_get_state(tsat_ctx ctx, float* theta, float* m, float* v, size_t elems, int64_t* t) {
     GUARD_CTX();
     tsat_status s = check_batch(ctx, false);
     if (s != TSAT_OK) return s;
+    if (ctx->th64) return fail(ctx, TSAT_E_STATE, "the batch has fp64 state: use tsat_get_state64");
     if ((theta || m || v) && elems != (size_t)ctx->cnf.V * ctx->N)
         return fail(ctx, TSAT_E_ARG, "state arrays must hold exactly V * N_local elements");
     size_t bytes = (size_t)ctx->cnf.V * ctx->N * 4;
@@ -1134,6 +1237,7 @@ tsat_status tsat_set_state(tsat_ctx ctx, const float* theta, const float* m, con
     GUARD_CTX();
     tsat_status s = check_batch(ctx, false);
     if (s != TSAT_OK) return s;
+    if (ctx->th64) return fail(ctx, TSAT_E_STATE, "the batch has fp64 state: use tsat_set_state64");
     if (!theta || !m || !v || t < 0) return fail(ctx, TSAT_E_ARG, "null state or t < 0");
     if (elems != (size_t)ctx->cnf.V * ctx->N)
         return fail(ctx, TSAT_E_ARG, "state arrays must hold exactly V * N_local elements (same world size and N)");
@@ -1165,6 +1269,7 @@ tsat_status tsat_get_rows(tsat_ctx ctx, const int32_t* rows, int32_t nrows, floa
     tsat_status s = check_batch(ctx, false);
     if (s != TSAT_OK) return s;
     if (row_elems != (size_t)ctx->N) return fail(ctx, TSAT_E_ARG, "row_elems must equal N_local");
+    if (ctx->th64) return fail(ctx, TSAT_E_STATE, "the batch has fp64 state (use tsat_get_state64)");
     if (nrows < 0 || (nrows > 0 && !rows)) return fail(ctx, TSAT_E_ARG, "bad rows");
     const size_t rb = (size_t)ctx->N * 4;
     for (int32_t i = 0; i < nrows; ++i) {
@@ -1388,6 +1493,7 @@ void tsat_destroy(tsat_ctx ctx) {
     free_cnf(ctx);
     cudaFree(ctx->dP);
     cudaFree(ctx->dAL);
+    free_fp64(ctx);
     comm_destroy(ctx->comm);
     peer_release(ctx);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);

@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) k_gtable(int* __restrict__ hist, int N, l
                                                 float* __restrict__ gtab, double* __restrict__ S,
                                                 int* __restrict__ unsat, DevScalars* __restrict__ ds, int sharded,
                                                 double* __restrict__ lossp, const StepScalars* __restrict__ sc,
-                                                int peer, const PeerArgs px) {
+                                                int peer, const PeerArgs px, double* __restrict__ gt64) {
     __shared__ double shS[8];
     __shared__ bool last;
     pdl_wait();
@@ -115,8 +115,9 @@ __global__ void __launch_bounds__(256) k_gtable(int* __restrict__ hist, int N, l
         for (int r = KB - 1; r >= 0; --r)
             if (r <= K && h[r] != 0) rmin = r;
         float g[KB];
+        double gd[KB];                       // fp64 state (R30): the table before rounding
 #pragma unroll
-        for (int r = 0; r < KB; ++r) g[r] = 0.0f;
+        for (int r = 0; r < KB; ++r) { g[r] = 0.0f; gd[r] = 0.0; }
         double s = 0.0;
         if (rmin <= K) {
             double den = 0.0, num = 0.0;
@@ -134,13 +135,18 @@ __global__ void __launch_bounds__(256) k_gtable(int* __restrict__ hist, int N, l
                 if (r >= rmin && r <= K) {
                     double wgt = sc->E[r - rmin] / den;
                     double u = (double)r - s;
-                    g[r] = (float)(wgt * (1.0 - sc->tau * u));
-                    gm = fmax(gm, fabs((double)g[r]));
+                    gd[r] = wgt * (1.0 - sc->tau * u);
+                    g[r] = (float)gd[r];
+                    gm = fmax(gm, gt64 ? fabs(gd[r]) : fabs((double)g[r]));
                 }
             }
         }
 #pragma unroll
         for (int r = 0; r < KB; ++r) gtab[(size_t)r * N + n] = g[r];
+        if (gt64) {
+#pragma unroll
+            for (int r = 0; r < KB; ++r) gt64[(size_t)r * N + n] = gd[r];
+        }
         S[n] = s;
         lfx = __double2ll_rn(s * mc.loss_scale);
         unsat[n] = (int)h[0];
@@ -402,12 +408,12 @@ cudaError_t launch_gtable(const StepArgs& a, const StepScalars* sc, cudaStream_t
     int blocks = (a.N + 255) / 256;
     if (a.KB == 4)
         return launch_maybe_pdl(a.pdl, k_gtable<4>, dim3(blocks), dim3(256), 0, st, a.hist, a.N, a.C, a.mc, a.gtab, a.S,
-                                a.unsat, a.ds, a.sharded, a.lossp, sc, a.peer, a.px);
+                                a.unsat, a.ds, a.sharded, a.lossp, sc, a.peer, a.px, a.fp64 ? a.gt64 : nullptr);
     if (a.KB == 8)
         return launch_maybe_pdl(a.pdl, k_gtable<8>, dim3(blocks), dim3(256), 0, st, a.hist, a.N, a.C, a.mc, a.gtab, a.S,
-                                a.unsat, a.ds, a.sharded, a.lossp, sc, a.peer, a.px);
+                                a.unsat, a.ds, a.sharded, a.lossp, sc, a.peer, a.px, a.fp64 ? a.gt64 : nullptr);
     return launch_maybe_pdl(a.pdl, k_gtable<16>, dim3(blocks), dim3(256), 0, st, a.hist, a.N, a.C, a.mc, a.gtab, a.S,
-                            a.unsat, a.ds, a.sharded, a.lossp, sc, a.peer, a.px);
+                            a.unsat, a.ds, a.sharded, a.lossp, sc, a.peer, a.px, a.fp64 ? a.gt64 : nullptr);
 }
 
 cudaError_t launch_export_pack(const StepArgs& a, long long t_eval, const int* cols_dev, const int* pos_dev, int Mo,
@@ -430,7 +436,8 @@ cudaError_t launch_export(const StepArgs& a, long long t_eval, const int* cols_d
     } else {
         long long total = (long long)M * a.V;
         unsigned blocks = (unsigned)((total + 255) / 256);
-        if (a.KB == 4) k_grad_cols<4><<<blocks, 256, 0, st>>>(a.V, a.N, Aeval, a.occ_ptr, a.occ_rec, a.gtab, cols_dev, M, a.mc.K, absG);
+        if (a.fp64) launch_absG64(a, cols_dev, M, absG, st);                  // |G| of the evaluated state (R30)
+        else if (a.KB == 4) k_grad_cols<4><<<blocks, 256, 0, st>>>(a.V, a.N, Aeval, a.occ_ptr, a.occ_rec, a.gtab, cols_dev, M, a.mc.K, absG);
         else if (a.KB == 8) k_grad_cols<8><<<blocks, 256, 0, st>>>(a.V, a.N, Aeval, a.occ_ptr, a.occ_rec, a.gtab, cols_dev, M, a.mc.K, absG);
         else k_grad_cols<16><<<blocks, 256, 0, st>>>(a.V, a.N, Aeval, a.occ_ptr, a.occ_rec, a.gtab, cols_dev, M, a.mc.K, absG);
         k_topk_cols<<<M, 1024, 0, st>>>(absG, a.V, k, out_v, out_g);

@@ -20,8 +20,10 @@ cudaError_t launch_step_kernel(int which, const StepArgs& a, const StepScalars* 
     switch (which) {
         case 0: return (a.dense && a.C > 0) ? launch_dense_clause(a, Acur, sc_dev, st) : launch_clause(a, Acur, sc_dev, st);
         case 1: return launch_gtable(a, sc_dev, st);
-        case 2: return a.upd_mode == 0 ? launch_hub(a, Acur, st) : cudaGetLastError();
-        case 3: return a.upd_RB > 1 ? launch_update_blk(a, Acur, Anext, sc_dev, st) : launch_update(a, Acur, Anext, sc_dev, st);
+        case 2: return (a.upd_mode == 0 && !a.fp64) ? launch_hub(a, Acur, st) : cudaGetLastError();
+        case 3:
+            if (a.fp64) return launch_update64(a, Acur, Anext, sc_dev, st);       // f2 fp64 state (R30)
+            return a.upd_RB > 1 ? launch_update_blk(a, Acur, Anext, sc_dev, st) : launch_update(a, Acur, Anext, sc_dev, st);
         case 4: return cudaGetLastError();
     }
     return cudaErrorInvalidValue;

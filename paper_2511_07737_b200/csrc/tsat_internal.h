@@ -112,6 +112,8 @@ struct StepScalars {
     int pad;
     double tau;       // SmoothMin temperature of this iteration (R1; annealed: R29)
     double E[16];     // exp(-tau d), d = 0..15 (host libm, R11)
+    // fp64 state (R30): the AdamW scalars unrounded
+    double wdf64, a1_64, b2_64, a2_64, nss64, rbc2_64, eps64, nz64;
 };
 
 // Device-resident scalars (one struct in the workspace).
@@ -132,6 +134,7 @@ struct DevScalars {
     long long loss_fx;               // sharded: this rank's sum of round(S_n 2^e) (exact int64, MethodConsts)
     unsigned int gt_done;            // k_gtable blocks finished (last block does the step bookkeeping)
     unsigned int xerr;               // peer path: an exchange timed out (step result invalid)
+    unsigned long long thmax64_bits[2];   // fp64 state (R30): max |theta| as fp64 bits, by t & 1
 };
 
 // Histogram bins per candidate for an instance of max clause length K: R in
@@ -190,6 +193,12 @@ struct StepArgs {
     const uint8_t* dP;               // [dCp][dKp] uint8 0/1 problem matrix (K-major)
     uint8_t* dAL;                    // [ceil(N/256)*256][dKp] uint8 0/1 assignment matrix (K-major)
     int dKp, dCp;
+    // fp64 state (config.state_fp64 = 1, k_fp64.cu, reading R30): library-owned buffers
+    int fp64;
+    double *th64, *m64, *v64, *G64, *gt64;   // [V][N] x 4, [KB][N]
+    long long* J64;                  // [V] int64 J partials (exact sums)
+    unsigned long long* Qp64;        // [V][nb][2] 128-bit row-sum partials per 256-candidate block
+    uint32_t *Pw64, *Nw64;           // [V][N/32] sign words of the next state
     int pdl;                         // launch k_clause / k_gtable / k_update with programmatic
                                      // stream serialisation (PDL; fused W = 1 path without hubs)
     size_t upd_smem;
@@ -254,6 +263,13 @@ int update_block_rows(int N);
 cudaError_t configure_update_blk(StepArgs* a);
 cudaError_t launch_update_blk(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
                               cudaStream_t st);
+// fp64 state (k_fp64.cu)
+cudaError_t launch_init64(const StepArgs& a, unsigned long long seed, cudaStream_t st);
+cudaError_t launch_rowstats64(const StepArgs& a, long long t, cudaStream_t st);
+cudaError_t launch_update64(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
+                            cudaStream_t st);
+cudaError_t launch_absG64(const StepArgs& a, const int* cols_dev, int M, double* absG, cudaStream_t st);
+int fp64_blocks_per_row(int N);
 // dense clause evaluation (k_dense.cu)
 cudaError_t configure_dense();
 cudaError_t launch_dense_clause(const StepArgs& a, const uint32_t* Acur, const StepScalars* sc, cudaStream_t st);

@@ -282,6 +282,82 @@ def test_fused_g_table_in_l2(kind):
         compare_step(s, o, cnf, kind)
 
 
+@pytest.mark.parametrize("case", ["planted3", "industrial7_mag", "k15", "reset_noise", "blk128"])
+def test_fp64_state_variant(case):
+    """SURVEY f2 / SPEC S:278: state_fp64 = 1 (reading R30): theta, m, v in
+    fp64, the g table, G, the J terms, the gradient and AdamW in fp64, row
+    sums in 128-bit fixed point at 2^-64 (k_fp64.cu).  Bit-exact against the
+    oracle's fp64 path step by step (theta, m, v, bits, unsat, g32, best)."""
+    from paper_2511_07737_b200 import config_default
+    kw = {}
+    if case == "planted3":
+        cnf, N = planted_ksat(300, 1260, 3, 4), 512
+    elif case == "industrial7_mag":
+        cnf, N, kw = industrial_cnf(400, 1500, 5), 256, dict(normalize=3)
+    elif case == "k15":
+        cnf, N = coloring_cnf(15, 15, 3, 2), 288
+    elif case == "reset_noise":
+        cnf, N, kw = planted_ksat(200, 840, 3, 6), 320, dict(noise_sigma=0.2, reset_moments_on_restart=1,
+                                                              restart_every=4, decay_every=2)
+    else:
+        cnf, N = planted_ksat(600, 2520, 3, 9), 128
+    ocfg = O.Config(state_fp64=1, **kw)
+    o = O.Oracle(cnf, N, 7, cfg=ocfg)
+    c = config_default()
+    for f in ("normalize", "noise_sigma", "reset_moments_on_restart", "restart_every", "decay_every"):
+        setattr(c, f, getattr(ocfg, f))
+    c.state_fp64 = 1
+    from paper_2511_07737_b200 import Solver
+    s = Solver(0)
+    s.load_cnf(cnf)
+    s.init_batch(N, 7, c)
+    th, m, v, t = s.get_state()
+    assert th.dtype == np.float64 and t == 0 and not m.any() and not v.any()
+    d = np.abs(th - o.theta)
+    # CUDA vs glibc fp64 log / sin / cos: a few ulps of the Box-Muller radius (absolute, since cos / sin
+    # near their zeros have large relative error)
+    assert (d <= 8 * np.spacing(1.0) * np.maximum(1.0, np.abs(o.theta))).all()
+    s.set_state(o.theta, o.m, o.v, 0)
+    K = o.K
+    KB = 4 if K <= 3 else (8 if K <= 7 else 16)
+    for step in range(7):
+        info = s.step(1)
+        ref = o.step()
+        np.testing.assert_array_equal(s.query_unsat(), ref.unsat, err_msg=f"unsat {case} {step}")
+        np.testing.assert_array_equal(s.debug(3, np.uint32, (cnf.V, N // 32)), pack_bits(ref.bits))
+        g = s.debug(1, np.float32, (KB, N))
+        np.testing.assert_array_equal(g[:K + 1].T, ref.g32)
+        th, m, v, t = s.get_state()
+        np.testing.assert_array_equal(th, o.theta, err_msg=f"theta {case} {step}")
+        np.testing.assert_array_equal(m, o.m, err_msg=f"m {case} {step}")
+        np.testing.assert_array_equal(v, o.v, err_msg=f"v {case} {step}")
+        assert (info.best_unsat, info.best_idx) == (ref.best_unsat, ref.best_idx)
+        assert abs(info.loss - ref.loss) <= 1e-12 * max(1.0, abs(ref.loss))
+    info = s.step(9)
+    for _ in range(9):
+        ref = o.step()
+    th, _, _, _ = s.get_state()
+    np.testing.assert_array_equal(th, o.theta)
+    ex = s.export_best(2)                       # |G| from the fp64 G of the evaluated state
+    assert len(ex) == 2 and len(ex[0]["lits"]) == min(cnf.V, 20)
+
+
+def test_fp64_state_fig1_solves():
+    from paper_2511_07737_b200 import Solver, config_default
+    c = config_default()
+    c.state_fp64 = 1
+    s = Solver(0)
+    s.load_cnf(fig1_cnf())
+    s.init_batch(32, 1, c)
+    info = s.step(30)
+    assert info.solved
+    vals, idx, st = s.get_solution()
+    assert tuple(vals) in {(1, 0, 0, 1), (1, 1, 0, 1)}
+    import pytest as _p
+    with _p.raises(Exception):
+        s.set_state(np.zeros((4, 32), np.float32), np.zeros((4, 32), np.float32), np.zeros((4, 32), np.float32), 0)
+
+
 def test_lr_boundaries_and_restart():
     """Cross the t = 29/30 decay and the t = 359/360 restart (R9)."""
     cnf = planted_ksat(200, 840, 3, 6)
