@@ -54,6 +54,9 @@ __device__ __forceinline__ void csa_add4(uint32_t (&c)[CB], uint32_t m0, uint32_
     }
 }
 
+#ifndef TSAT_CL_PERSM3
+#define TSAT_CL_PERSM3 3           // K <= 3: CTAs per SM the grid is sized for
+#endif
 #ifndef TSAT_CL_MINB8
 #define TSAT_CL_MINB8 2            // CTAs per SM the K <= 7 kernel is compiled for
 #endif
@@ -371,7 +374,7 @@ cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, const StepSca
     const long long ctas_needed = (nchunks + kWarps - 1) / kWarps;
     const int K = a.mc.K;
     // grid-sized: (CTAs resident per SM) x SMs, split over the word blocks
-    const int per_sm = K <= 3 ? 3 : TSAT_CL_MINB8;
+    const int per_sm = K <= 3 ? TSAT_CL_PERSM3 : TSAT_CL_MINB8;
     long long gy = ((long long)a.num_sms * per_sm + nwb - 1) / nwb;
     if (gy > ctas_needed) gy = ctas_needed;
     // packed 21-bit CTA histogram fields (KB = 4): < 2^21 clauses per CTA

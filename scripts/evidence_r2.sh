@@ -1,7 +1,7 @@
 # Round-2 evidence on one B200: GPU tests, smoke, default bench line, reference arm, f4 timing,
 # ncu launch list of the bench command, ncu --set full per hot kernel/config (summaries + traffic json).
 set -x
-O=gpurun_out/ev2; mkdir -p $O
+O=gpurun_out/${EV_OUT:-ev2}; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv
 python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -3
 timeout 1500 python -m pytest tests -m gpu -q --timeout=900 > $O/pytest_gpu.txt 2>&1; tail -3 $O/pytest_gpu.txt
@@ -23,4 +23,5 @@ python scripts/ncu_lines.py $O/prof_$2_$3.ncu-rep 40 > $O/lines_$2_$3.txt 2>&1
 done
 cp profiles/ncu_traffic.json $O/ncu_traffic.json
 rm -f $O/*.ncu-rep
+SAN_OUT=${EV_OUT:-ev2}/san bash scripts/sanitize.sh
 ls $O
