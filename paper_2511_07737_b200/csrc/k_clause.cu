@@ -27,7 +27,11 @@ namespace {
 constexpr int kWarps = 8;
 // clauses per warp chunk (<= 127: 7-bit counters); K = 7 halves it to keep
 // the staged literals within the 48 KB static shared memory
-__host__ __device__ constexpr int chunk_clauses(int kmaxc) { return kmaxc > 3 ? 32 : TSAT_CL_CH3; }
+__host__ __device__ constexpr int chunk_clauses(int kmaxc, int wide = 0) { return kmaxc > 3 ? 32 : (wide ? 96 : TSAT_CL_CH3); }
+// K <= 3 variants: WIDE = 0 (3 CTAs / SM, 64-clause chunks) for batches of
+// >= 2048 candidates per GPU; WIDE = 1 (4 CTAs / SM at 64 registers, 96-clause
+// chunks) below, where fewer word blocks leave the warps latency-bound (c3
+// N = 1024: k_clause -7 %, N = 128: -21 %; c2 N = 4096: +5 %, so not there)
 constexpr int kUnr = 4;        // clauses evaluated together (carry-save group)
 constexpr uint32_t kNone = 0xffffffffu;
 
@@ -60,8 +64,8 @@ __device__ __forceinline__ void csa_add4(uint32_t (&c)[CB], uint32_t m0, uint32_
 #ifndef TSAT_CL_MINB8
 #define TSAT_CL_MINB8 2            // CTAs per SM the K <= 7 kernel is compiled for
 #endif
-template <int KB, int KMAXC>
-__global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(const uint32_t* __restrict__ A, int NW, int V,
+template <int KB, int KMAXC, int WIDE = 0>
+__global__ void __launch_bounds__(256, KB == 4 ? (WIDE ? 4 : TSAT_CL_PERSM3) : TSAT_CL_MINB8) k_clause(const uint32_t* __restrict__ A, int NW, int V,
                                                                 const uint32_t* __restrict__ cptr,
                                                                 const uint32_t* __restrict__ clit, long long C,
                                                                 int* __restrict__ hist, int N, int uniform,
@@ -72,8 +76,8 @@ __global__ void __launch_bounds__(256, KB == 4 ? 3 : TSAT_CL_MINB8) k_clause(con
     __shared__ int sh[(KB - 1) * 1024];
     // staged literals: {element offset var * NW, sign mask}; empty slots and
     // padding clauses read the all-zero row V with mask 0 (literal false)
-    __shared__ uint2 soff[kWarps][chunk_clauses(KMAXC) * KMAXC];
-    constexpr int kCH = chunk_clauses(KMAXC);
+    __shared__ uint2 soff[kWarps][chunk_clauses(KMAXC, WIDE) * KMAXC];
+    constexpr int kCH = chunk_clauses(KMAXC, WIDE);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // nsub > 1 (fewer than 32 words, N < 1024 per GPU): the warp's lanes are
     // nsub sub-groups of NW lanes; sub-group `sub` evaluates every nsub-th
@@ -366,7 +370,8 @@ cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, const StepSca
     const int nwb = (NW + 31) / 32;
     // sub-groups of NW lanes when a warp would leave lanes idle (N < 1024 per GPU);
     // a chunk (kCH clauses) must split evenly into carry-save groups per sub-group
-    const int kCH = chunk_clauses(a.mc.K <= 3 ? 3 : 7);
+    const int wide = (a.mc.K <= 3 && a.N < 2048) ? 1 : 0;
+    const int kCH = chunk_clauses(a.mc.K <= 3 ? 3 : 7, wide);
     const int kGrp = 4 * (a.mc.K <= 3 ? TSAT_CL_G3 : 1);
     int nsub = NW < 32 ? 32 / NW : 1;
     while (nsub > 1 && kCH % (kGrp * nsub)) --nsub;
@@ -374,7 +379,7 @@ cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, const StepSca
     const long long ctas_needed = (nchunks + kWarps - 1) / kWarps;
     const int K = a.mc.K;
     // grid-sized: (CTAs resident per SM) x SMs, split over the word blocks
-    const int per_sm = K <= 3 ? TSAT_CL_PERSM3 : TSAT_CL_MINB8;
+    const int per_sm = K <= 3 ? (wide ? 4 : TSAT_CL_PERSM3) : TSAT_CL_MINB8;
     long long gy = ((long long)a.num_sms * per_sm + nwb - 1) / nwb;
     if (gy > ctas_needed) gy = ctas_needed;
     // packed 21-bit CTA histogram fields (KB = 4): < 2^21 clauses per CTA
@@ -384,11 +389,15 @@ cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, const StepSca
     dim3 grid(nwb, (unsigned)gy);
     const int uni = a.uniform_len;
     if (K <= 2)
-        return launch_maybe_pdl(a.pdl, k_clause<4, 2>, grid, dim3(256), 0, st, Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist,
-                                a.N, (int)(uni && K == 2), a.ds, sc, nsub);
+        return wide ? launch_maybe_pdl(a.pdl, k_clause<4, 2, 1>, grid, dim3(256), 0, st, Acur, NW, a.V, a.cptr, a.clit,
+                                       a.C, a.hist, a.N, (int)(uni && K == 2), a.ds, sc, nsub)
+                    : launch_maybe_pdl(a.pdl, k_clause<4, 2, 0>, grid, dim3(256), 0, st, Acur, NW, a.V, a.cptr, a.clit,
+                                       a.C, a.hist, a.N, (int)(uni && K == 2), a.ds, sc, nsub);
     else if (K == 3)
-        return launch_maybe_pdl(a.pdl, k_clause<4, 3>, grid, dim3(256), 0, st, Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist,
-                                a.N, uni, a.ds, sc, nsub);
+        return wide ? launch_maybe_pdl(a.pdl, k_clause<4, 3, 1>, grid, dim3(256), 0, st, Acur, NW, a.V, a.cptr, a.clit,
+                                       a.C, a.hist, a.N, uni, a.ds, sc, nsub)
+                    : launch_maybe_pdl(a.pdl, k_clause<4, 3, 0>, grid, dim3(256), 0, st, Acur, NW, a.V, a.cptr, a.clit,
+                                       a.C, a.hist, a.N, uni, a.ds, sc, nsub);
     else if (K <= 7)
         return launch_maybe_pdl(a.pdl, k_clause<8, 7>, grid, dim3(256), 0, st, Acur, NW, a.V, a.cptr, a.clit, a.C, a.hist,
                                 a.N, (int)(uni && K == 7), a.ds, sc, nsub);
