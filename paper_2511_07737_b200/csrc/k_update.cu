@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
     const int grp = threadIdx.x / GT, tg = threadIdx.x - grp * GT;
     const int rec_cap = a.upd_rec_cap;
     constexpr int nbufs = upd_recbufs(KB);
-    const size_t grb = upd_group_bytes(KB, NCH, rec_cap, nbufs);
+    const size_t grb = upd_group_bytes(KB, NCH, rec_cap, nbufs, MODE == 2 ? 2 : 1);
     unsigned char* gb = smem + (gs_global ? 0 : upd_gs_bytes(KB, N)) + (size_t)grp * grb;
     const int nitems = a.V * nch;
     uint32_t* dpk = reinterpret_cast<uint32_t*>(gb);
@@ -517,7 +517,7 @@ cudaError_t configure_update(StepArgs* a) {
         // the batch's g table in shared memory leaves few warp groups for
         // large batches (N = 8192: 128 KB of table, 2 groups); read it through
         // L1 / L2 instead when that buys at least twice the groups
-        const size_t gsb0 = upd_gs_bytes(KB, N), grb0 = upd_group_bytes(KB, N, a->upd_rec_cap, upd_recbufs(KB));
+        const size_t gsb0 = upd_gs_bytes(KB, N), grb0 = upd_group_bytes(KB, N, a->upd_rec_cap, upd_recbufs(KB), a->peer ? 2 : 1);
         const long long ng_s = optin > (long long)gsb0 ? ((long long)optin - (long long)gsb0) / (long long)grb0 : 0;
         const long long ng_g = (long long)optin / (long long)grb0;
         if (ng_s < TSAT_GS_GLOBAL_BELOW && ng_g >= 2 * ng_s && !std::getenv("TSAT_NO_GS_GLOBAL")) a->upd_gs_global = 1;
@@ -526,7 +526,7 @@ cudaError_t configure_update(StepArgs* a) {
     const int max_threads = KB == 4 ? (a->peer ? TSAT_UPD_THREADS4P : TSAT_UPD_THREADS4)
                                     : TSAT_UPD_THREADS8;   // register budget (launch bounds)
     auto groups = [&](int nbufs) {
-        const size_t grb = upd_group_bytes(KB, a->upd_chunk, a->upd_rec_cap, nbufs);
+        const size_t grb = upd_group_bytes(KB, a->upd_chunk, a->upd_rec_cap, nbufs, a->peer ? 2 : 1);
         long long ng = optin > (long long)gsb ? ((long long)optin - (long long)gsb) / (long long)grb : 0;
         ng = ng < max_threads / GT ? ng : max_threads / GT;
         if (GT > 32) ng = ng < 15 ? ng : 15;      // named barriers 1..15 (warp groups use __syncwarp)
@@ -535,8 +535,12 @@ cudaError_t configure_update(StepArgs* a) {
     // (upd_recbufs: measured c4 7 -> 8 groups with one buffer, k_update -11 %;
     // c2 / c3 are register-bound, and two buffers are faster there, c2 +4 %)
     const int nbufs = upd_recbufs(KB);
-    const long long ng = groups(nbufs);
-    const size_t grb = upd_group_bytes(KB, a->upd_chunk, a->upd_rec_cap, nbufs);
+    long long ng = groups(nbufs);
+    if (const char* mg = std::getenv("TSAT_UPD_MAXGROUPS")) {   // A/B hook: cap the warp groups per CTA
+        const long long x = std::atoll(mg);
+        if (x > 0 && x < ng) ng = x;
+    }
+    const size_t grb = upd_group_bytes(KB, a->upd_chunk, a->upd_rec_cap, nbufs, a->peer ? 2 : 1);
     if (ng < 1) return cudaErrorInvalidConfiguration;
     a->upd_recbufs = nbufs;
     if (std::getenv("TSAT_GEOM_VERBOSE"))

@@ -69,11 +69,12 @@ __host__ __device__ inline size_t upd_dpk_words(int N) { return (size_t)N + (N >
 // KB = 8 (shared-memory bound), a compile-time choice (a runtime one costs
 // the instruction-cache-bound KB = 8 kernel ~7 %).
 __host__ __device__ constexpr int upd_recbufs(int KB) { return KB == 8 ? 1 : 2; }
-__host__ __device__ inline size_t upd_group_bytes(int KB, int N, int rec_cap, int nbufs) {
+// parities: 2 for the peer kernel (MODE 2 finishes a row one row late), else 1
+__host__ __device__ inline size_t upd_group_bytes(int KB, int N, int rec_cap, int nbufs, int parities = 2) {
     const int NDW = KB == 4 ? 1 : 2;
-    // dpk | nbufs record buffers | sign planes [2 parities][pos, neg][NW] | 128 B scratch
+    // dpk | nbufs record buffers | sign planes [parities][pos, neg][NW] | 128 B scratch
     return align16((size_t)NDW * upd_dpk_words(N) * 4) + nbufs * align16((size_t)rec_cap * 4) +
-           align16((size_t)4 * (N >> 5) * 4) + 128;
+           align16((size_t)2 * parities * (N >> 5) * 4) + 128;
 }
 
 // x * 2^s, exact (== scalbn) when 2^s is a normal double.
