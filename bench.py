@@ -65,6 +65,10 @@ def parse():
     ap.add_argument("--tts-only", action="store_true", help="run only the time-to-SAT protocol and print it")
     ap.add_argument("--n-per-gpu", type=int, default=0, help="override the config's candidates per GPU (exploration)")
     ap.add_argument("--clause-eval", type=int, default=0, help="1: dense tensor-core clause evaluation (f4 experiment)")
+    ap.add_argument("--trace", type=str, default="",
+                    help="write a per-iteration CSV (iteration, lr, loss, best_unsat, best_fraction) of the first "
+                         "--trace-steps iterations of this config to FILE (SPEC's --trace columns) and exit")
+    ap.add_argument("--trace-steps", type=int, default=360)
     ap.add_argument("--hybrid-only", type=str, default="", help="V,seed[,N]: run only the GPU->CDCL hybrid time-to-SAT")
     return ap.parse_args()
 
@@ -257,6 +261,43 @@ def hybrid_tts(cnf, N, seed, local, stream, threads, max_steps=3600, cdcl_limit_
     return out
 
 
+def quality_2v(cnf, N, seed, local, stream, iters=360):
+    """Trajectory quality of the 2V-literal-row reading (tsat_synth.literal_split,
+    PAPER.md l.191): the paper-exact Eq. 5 (R3) on 2V independent literal rows.
+    Every 30 iterations the positive rows' bits (x_v = b of row v) are
+    evaluated on the ORIGINAL CNF by a second solver (normalisation off, theta
+    = +-1 from those bits, one evaluation step): best satisfied fraction of
+    the original clauses, and the best of the relaxed (2V) problem."""
+    from paper_2511_07737_b200 import Solver, config_default
+    from tsat_synth import literal_split
+    c2v = literal_split(cnf)
+    q = Solver(local, stream=stream)
+    q.load_cnf(c2v)
+    q.init_batch(N, seed, config_default())
+    ev = Solver(local, stream=stream)
+    ev.load_cnf(cnf)
+    ce = config_default()
+    ce.normalize = 0
+    ev.init_batch(N, seed, ce)
+    best_orig, best_relaxed = None, None
+    z = np.zeros((cnf.V, N), np.float32)
+    for _ in range(iters // 30):
+        inf = q.step(30)
+        best_relaxed = inf.best_unsat if best_relaxed is None else min(best_relaxed, inf.best_unsat)
+        words = q.debug(3, np.uint32, (c2v.V, N // 32))[:cnf.V]          # bit planes of the evaluated state
+        bits = ((words[:, :, None] >> np.arange(32, dtype=np.uint32)) & 1).reshape(cnf.V, N)
+        ev.set_state(np.where(bits > 0, 1.0, -1.0).astype(np.float32), z, z, 0)
+        ev.step(1)
+        u = int(ev.query_unsat().min())
+        best_orig = u if best_orig is None else min(best_orig, u)
+    q.close()
+    ev.close()
+    return {"iterations": iters, "best_unsat_original": best_orig,
+            "best_satisfied_frac_original": (cnf.C - best_orig) / cnf.C,
+            "best_unsat_relaxed_2V": best_relaxed,
+            "note": "positive literal rows evaluated on the original CNF (the negative rows are not tied to them)"}
+
+
 def workload_desc(name, cnf, N):
     kinds = {"c1": "planted random 3-SAT", "c2": "planted random 3-SAT", "c3": "planted random 3-SAT",
              "c4": "industrial-shaped CNF (lengths 2-7, power-law occurrences)", "c5": "planted random 3-SAT",
@@ -415,6 +456,25 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     stream = torch.cuda.current_stream()
+    if args.trace:
+        if rank == 0:
+            from paper_2511_07737_b200 import Solver, config_default
+            from paper_2511_07737_b200.binding import lr_at
+            from tsat_synth import make_config
+            cnf, cfg = make_config(args.config)
+            q = Solver(local, stream=stream)
+            q.load_cnf(cnf)
+            c = config_default()
+            q.init_batch(args.n_per_gpu or cfg["N"], cfg["seed"], c)
+            with open(args.trace, "w") as f:
+                f.write("iteration,lr,loss,best_unsat,best_fraction\n")
+                for it in range(args.trace_steps):
+                    inf = q.step(1)                    # evaluates state `it`, then updates it
+                    f.write(f"{it},{lr_at(c, it):.6g},{inf.loss:.10g},{inf.best_unsat},"
+                            f"{(cnf.C - inf.best_unsat) / max(cnf.C, 1):.6f}\n")
+            q.close()
+            print(json.dumps({"trace": args.trace, "iterations": args.trace_steps}), flush=True)
+        return
     if args.hybrid_only:
         if rank == 0:
             from tsat_synth import planted_ksat
@@ -664,6 +724,7 @@ def main():
             quality[label] = {"best_unsat": best, "best_satisfied_frac": (cnf.C - best) / cnf.C,
                               "gate_99_at_iteration": gate, "solved": bool(inf.solved)}
             q.close()
+        quality["literal_rows_2V_R3"] = quality_2v(cnf, N, seed, local, stream)
 
     line = {
         "metric": "clause-candidate evals/sec", "value": value, "unit": "evals/s", "n_gpus": world,

@@ -293,6 +293,10 @@ tsat_status tsat_kernel_times(tsat_ctx ctx, double* ms5, int64_t* steps);
  * hub pre-pass only runs when the instance has hub variables). */
 tsat_status tsat_kernels_per_step(tsat_ctx ctx, int32_t* n);
 
+/* Learning rate of iteration t under cfg (readings R7/R9), host only
+ * (for traces: iteration, lr, loss, best fraction, SPEC's --trace columns). */
+tsat_status tsat_lr_at(const tsat_config* cfg, int64_t t, double* lr);
+
 /* Last error message on ctx (static storage owned by ctx, valid until the next call). */
 const char* tsat_error_string(tsat_ctx ctx);
 

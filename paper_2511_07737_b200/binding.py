@@ -90,6 +90,7 @@ _SIGS = {
                                        ct.c_int64, P]),
     "tsat_write_dimacs": (ct.c_int, [ct.c_int32, ct.c_int64, P, P, P, P, ct.c_size_t, ct.POINTER(ct.c_size_t)]),
     "tsat_verify_model": (ct.c_int, [ct.c_int32, ct.c_int64, P, P, P, ct.POINTER(ct.c_int64)]),
+    "tsat_lr_at": (ct.c_int, [ct.POINTER(tsat_config), ct.c_int64, ct.POINTER(ct.c_double)]),
     "tsat_export_model": (ct.c_int, [P, ct.c_int64, P]),
     "tsat_get_solution": (ct.c_int, [P, P, ct.POINTER(ct.c_int64), ct.POINTER(ct.c_int64)]),
     "tsat_get_state": (ct.c_int, [P, P, P, P, ct.c_size_t, ct.POINTER(ct.c_int64)]),
@@ -238,6 +239,15 @@ def cdcl_portfolio(cnf, seeds, threads: int, unseeded: bool = True, time_limit_s
     if st:
         raise TsatError(st, "tsat_cdcl_portfolio")
     return res, (model if res.status == 10 else None)
+
+
+def lr_at(cfg: tsat_config, t: int) -> float:
+    """tsat_lr_at (host only): the learning rate of iteration t."""
+    out = ct.c_double()
+    st = load_library().tsat_lr_at(ct.byref(cfg), int(t), ct.byref(out))
+    if st:
+        raise TsatError(st, "tsat_lr_at")
+    return out.value
 
 
 def nccl_unique_id() -> bytes:

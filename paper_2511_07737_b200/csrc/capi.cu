@@ -2,6 +2,7 @@
 // the host runtime behind it: context, CNF upload, workspace layout, per-call
 // step-scalar tables, CUDA-graph capture of k-iteration sequences, kernel
 // timing, export.
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges visible to nsys / ncu --nvtx
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -897,6 +898,8 @@ tsat_status tsat_workspace_bytes(tsat_ctx ctx, int64_t N_global, size_t* bytes) 
 
 tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const tsat_config* cfg, void* ws,
                             size_t bytes) {
+    nvtxRangePushA("tsat_init_batch");
+    struct PopOnExit { ~PopOnExit() { nvtxRangePop(); } } pop_;
     return no_throw(ctx, [&]() -> tsat_status {
         GUARD_CTX();
         size_t need;
@@ -1059,6 +1062,10 @@ tsat_status tsat_step(tsat_ctx ctx, int32_t k, tsat_step_info* out) {
         tsat_status s = check_batch(ctx, false);
         if (s != TSAT_OK) return s;
         if (k < 1) return fail(ctx, TSAT_E_ARG, "k < 1");
+        struct NvtxRange {                              // one range per tsat_step call (profiling timelines)
+            explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+            ~NvtxRange() { nvtxRangePop(); }
+        } nvtx_range_("tsat_step");
         int done = 0;
         while (done < k) {
             int kk = std::min(k - done, kMaxStepsPerCall);
@@ -1508,3 +1515,9 @@ void tsat_destroy(tsat_ctx ctx) {
 }
 
 }  // extern "C"
+
+extern "C" tsat_status tsat_lr_at(const tsat_config* cfg, int64_t t, double* lr) {
+    if (!cfg || !lr || t < 0 || cfg->decay_every < 1 || cfg->restart_every < 1) return TSAT_E_ARG;
+    *lr = lr_at(*cfg, t);
+    return TSAT_OK;
+}

@@ -98,3 +98,20 @@ def test_generator_argument_errors():
         P.gen_planted(10, 5, 1, 1, hidden=2)            # 2-hidden needs k >= 2
     with pytest.raises(P.TsatError):
         P.verify_model(3, np.array([0, 1]), np.array([4], np.int32), np.zeros(3, np.uint8))   # |lit| > V
+
+
+def test_literal_split_relabelling():
+    """tsat_synth.literal_split (the 2V-literal-row form of PAPER.md l.191):
+    every literal becomes a positive reference to its own literal row; an
+    assignment a of the original maps to (a, 1 - a) with identical clause
+    truth values, and the planted model maps to a model."""
+    from tsat_synth import literal_split
+    cnf = planted_ksat(30, 120, 3, 4)
+    d = literal_split(cnf)
+    assert d.V == 60 and (d.lits > 0).all() and np.array_equal(d.clause_ptr, cnf.clause_ptr)
+    rng = np.random.default_rng(1)
+    for _ in range(10):
+        a = rng.integers(0, 2, cnf.V).astype(np.uint8)
+        b = np.concatenate([a, 1 - a])
+        assert _direct_unsat(cnf.V, cnf.clause_ptr, cnf.lits, a) == _direct_unsat(d.V, d.clause_ptr, d.lits, b)
+    assert _direct_unsat(d.V, d.clause_ptr, d.lits, d.sigma) == 0

@@ -37,6 +37,7 @@ __all__ = [
     "industrial_cnf",
     "fig1_cnf",
     "coloring_cnf",
+    "literal_split",
     "to_dimacs",
     "enumeration_theta",
     "random_state",
@@ -195,6 +196,19 @@ def coloring_cnf(nodes: int, colors: int, degree: int = 4, seed: int = 1) -> Cnf
     cnf = Cnf.from_clauses(nodes * colors, cl, name=f"color{colors}-n{nodes}-d{degree}-s{seed}")
     cnf.sigma = sigma
     return cnf
+
+
+def literal_split(cnf: Cnf) -> Cnf:
+    """The 2V-literal-row form of PAPER.md l.191 (A_real is 2V x N): literal
+    +v becomes variable v and literal -v becomes variable V + v, both
+    positive, so each literal row has its own parameters and its own Eq. 5
+    normalisation and nothing keeps the two rows of a variable complementary
+    (reading R2 does; this is the alternative the verdict asked to test).
+    sigma extends to (sigma, 1 - sigma).  Pure relabelling: no method arithmetic."""
+    lits = np.asarray(cnf.lits, np.int64)
+    out = np.where(lits > 0, lits, cnf.V - lits).astype(np.int32)        # -v -> V + v (1-based)
+    sigma = None if cnf.sigma is None else np.concatenate([cnf.sigma, 1 - cnf.sigma]).astype(np.uint8)
+    return Cnf(2 * cnf.V, cnf.clause_ptr.copy(), out, sigma, cnf.name + "-2V")
 
 
 def fig1_cnf() -> Cnf:
