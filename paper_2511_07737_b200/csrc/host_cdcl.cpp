@@ -478,7 +478,9 @@ extern "C" tsat_status tsat_cdcl_portfolio(int32_t V, int64_t C, const int64_t* 
         best.status = kUnknown;
         best.winner = -2;
         std::vector<uint8_t> model((size_t)V, 0);
+        std::atomic<int> oom{0};
         auto work = [&](int tid) {
+          try {                                 // no exception may leave a std::thread (terminate)
             for (;;) {
                 const int j = next.fetch_add(1);
                 if (j >= (int)jobs.size() || stop.load()) return;
@@ -510,11 +512,16 @@ extern "C" tsat_status tsat_cdcl_portfolio(int32_t V, int64_t C, const int64_t* 
                 stop.store(1);
                 return;
             }
+          } catch (...) {
+            oom.store(1);
+            stop.store(1);
+          }
         };
         std::vector<std::thread> th;
         const int nt = std::max(1, std::min<int>(threads, (int)jobs.size()));
         for (int i = 0; i < nt; ++i) th.emplace_back(work, i);
         for (auto& x : th) x.join();
+        if (oom.load()) return TSAT_E_OOM;
         *out = best;
         out->failed_seeds = failed.load();
         out->threads = nt;
