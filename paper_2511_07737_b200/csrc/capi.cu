@@ -80,6 +80,7 @@ struct tsat_ctx_s {
     // k_update launch geometry (configure_kernels)
     int upd_mode = 0, upd_GT = 0, upd_NG = 0, upd_grid = 0, num_sms = 0, upd_recbufs = 2;
     int upd_RB = 1, upd_blk_cap = 0;    // row-block k_update (small shards, k_update_blk.cu)
+    int* blk_rows = nullptr;            // device [V]: rows in block order (library-owned)
     // dense tensor-core clause evaluation (config.clause_eval = 1, k_dense.cu): library-owned
     uint8_t* dP = nullptr;
     uint8_t* dAL = nullptr;
@@ -289,6 +290,7 @@ StepArgs step_args(tsat_ctx ctx) {
     a.upd_rec_cap = std::max(64, (ctx->cnf.max_rec_words + 63) / 64 * 64);
     a.upd_RB = ctx->upd_RB;
     a.upd_blk_cap = ctx->upd_blk_cap;
+    a.blk_rows = ctx->blk_rows;
     a.fp64 = ctx->th64 != nullptr;
     a.th64 = ctx->th64; a.m64 = ctx->m64; a.v64 = ctx->v64; a.G64 = ctx->G64; a.gt64 = ctx->gt64;
     a.J64 = ctx->J64; a.Qp64 = ctx->Qp64; a.Pw64 = ctx->Pw64; a.Nw64 = ctx->Nw64;
@@ -1002,14 +1004,35 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
         if (!ctx->sharded && !ctx->chunked && !std::getenv("TSAT_NO_BLK")) {
             const int RB = update_block_rows(ctx->N);
             if (RB > 1) {
-                const std::vector<uint32_t>& ptr = ctx->cnf.batched ? ctx->cnf.bat_ptr : ctx->cnf.occ_ptr;
+                // block order: rows grouped by their gather length (batches of 4
+                // same-sign records, or staged record words), so the RB rows a
+                // warp gathers at once finish together; hub rows (counted by
+                // k_hub) first.  Stable: equal lengths keep the variable order.
+                const HostCnf& h = ctx->cnf;
+                const std::vector<uint32_t>& ptr = h.batched ? h.bat_ptr : h.occ_ptr;
+                const int V = h.V;
+                std::vector<int> order((size_t)V);
+                for (int v = 0; v < V; ++v) order[v] = v;
+                auto glen = [&](int v) -> long long {
+                    if (h.hub_of[v] >= 0) return -1;
+                    if (!h.batched) return (h.occ_pn[2 * v] + 3) / 4 + (h.occ_pn[2 * v + 1] + 3) / 4;
+                    return (long long)(ptr[v + 1] - ptr[v]);
+                };
+                if (!std::getenv("TSAT_BLK_NOSORT"))
+                    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return glen(x) < glen(y); });
                 long long cap = 0;
-                for (int v0 = 0; v0 < ctx->cnf.V; v0 += RB) {
+                for (int b0 = 0; b0 < V; b0 += RB) {
                     long long w = 0;
-                    for (int v = v0; v < std::min(ctx->cnf.V, v0 + RB); ++v)
-                        if (ctx->cnf.hub_of[v] < 0) w += ptr[v + 1] - ptr[v];
+                    for (int i = b0; i < std::min(V, b0 + RB); ++i) {
+                        const int v = order[i];
+                        if (h.hub_of[v] < 0) w += ptr[v + 1] - ptr[v];
+                    }
                     cap = std::max(cap, w);
                 }
+                cudaFree(ctx->blk_rows);
+                ctx->blk_rows = nullptr;
+                CK(cudaMalloc(&ctx->blk_rows, (size_t)std::max(V, 1) * sizeof(int)));
+                CK(cudaMemcpy(ctx->blk_rows, order.data(), (size_t)V * sizeof(int), cudaMemcpyHostToDevice));
                 ctx->upd_RB = RB;
                 ctx->upd_blk_cap = (int)std::max(64LL, (cap + 63) / 64 * 64);
             }
@@ -1500,6 +1523,7 @@ void tsat_destroy(tsat_ctx ctx) {
     free_cnf(ctx);
     cudaFree(ctx->dP);
     cudaFree(ctx->dAL);
+    cudaFree(ctx->blk_rows);
     free_fp64(ctx);
     comm_destroy(ctx->comm);
     peer_release(ctx);

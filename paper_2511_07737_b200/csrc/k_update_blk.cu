@@ -35,12 +35,13 @@ struct BlkRow {
     int hub, dsum, jvalid, s;
     int guard;
     int roff, nrec, npos, nneg;      // staged records: offset in the block buffer, words, occurrences by sign
+    int v, pv;                       // the row (variable) of this block slot; of the pending block's slot
 };
 // A row's values for the next block, prefetched into the registers of lane r
 // while the current block streams (their L2 latency leaves the critical path).
 struct RowPre {
     int2 pn;
-    int hub, guard, roff, nrec, rbeg;
+    int v, hub, guard, roff, nrec, rbeg;
     double rho;
 };
 
@@ -50,6 +51,21 @@ __host__ __device__ inline size_t blk_group_bytes(int KB, int N, int RB, int cap
            align16((size_t)4 * RB * (N >> 5) * 4) + align16(sizeof(BlkRow) * RB) + 16;
 }
 }  // namespace
+
+// Warp sum of an int64 whose magnitude is below 2^57 (J and Q partials of a
+// lane: 4 terms, each below 2^61 / N with N >= 128, resp. 2^46): three 21-bit
+// limbs through the warp-reduce unit (REDUX), exact.
+__device__ __forceinline__ long long warp_sum_redux(long long x) {
+    const unsigned lo = (unsigned)(x & 0x1FFFFF), mid = (unsigned)((x >> 21) & 0x1FFFFF);
+    const int hi = (int)(x >> 42);
+    const unsigned slo = __reduce_add_sync(0xffffffffu, lo), smid = __reduce_add_sync(0xffffffffu, mid);
+    const int shi = __reduce_add_sync(0xffffffffu, hi);
+    return ((long long)shi << 42) + ((long long)smid << 21) + (long long)slo;
+}
+// Warp max of non-negative floats (their bit patterns order like the values).
+__device__ __forceinline__ float warp_max_redux(float x) {
+    return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(x)));
+}
 
 int update_block_rows(int N) {
     if (N <= 0 || N % 128 != 0) return 1;      // 128-candidate iterations never straddle a row
@@ -122,7 +138,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
                 epsf = sc->epsf, nz = sc->nz, mkeep = sc->mkeep;
     const MethodConsts& mc = a.mc;
 
-    // records of block v0 .. v0 + nr - 1 (non-hub rows, back to back) -> buf
+    // records of the block's non-hub rows, back to back -> buf
     // (the rows' record ranges come from the RowPre values lane r holds)
     auto stage = [&](int nr, uint32_t* buf, bool async, const RowPre& P) {
         for (int r = 0; r < nr; ++r) {
@@ -138,20 +154,21 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
     };
     // Rows of a block are complete once their global Q are known: bit planes
     // (sign(d) = sign(Q), R3), Eq. 5 statistics, max |theta|, first-model bits.
-    auto finish_block = [&](int v0, int nr, const uint32_t* pl, bool pending) {
+    auto finish_block = [&](int nr, const uint32_t* pl, bool pending) {
         for (int idx = lane; idx < nr * NW; idx += 32) {
-            const int r = idx / NW;
+            const int r = idx / NW, w = idx - r * NW;
             const long long Qg = pending ? rp[r].pq : rp[r].qt;
+            const int vr = pending ? rp[r].pv : rp[r].v;
             const bool dpos = !mc.normalize || Qg >= 0;
 #if TSAT_ANEXT_CS
-            __stcs(Anext + (size_t)v0 * NW + idx, dpos ? pl[idx] : pl[RB * NW + idx]);
+            __stcs(Anext + (size_t)vr * NW + w, dpos ? pl[idx] : pl[RB * NW + idx]);
 #else
-            Anext[(size_t)v0 * NW + idx] = dpos ? pl[idx] : pl[RB * NW + idx];
+            Anext[(size_t)vr * NW + w] = dpos ? pl[idx] : pl[RB * NW + idx];
 #endif
         }
         float m2 = 0.0f;
         if (lane < nr) {
-            const int vr = v0 + lane;
+            const int vr = pending ? rp[lane].pv : rp[lane].v;
             const long long Qg = pending ? rp[lane].pq : rp[lane].qt;
             m2 = pending ? rp[lane].pm2 : rp[lane].m2;
             double dn, rhon;
@@ -169,46 +186,52 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
         if (lane == 0) atomicMax(&a.ds->thmax_bits[(t + 1) & 1], __float_as_uint(m2));
     };
 
-    // row values of block v0 .. v0 + nr - 1 for lane r (< nr): occurrence counts,
+    // row values of the block's row r for lane r (< nr): occurrence counts,
     // hub index, Eq. 5 statistics of the evaluated state, and the row's
     // record offset within the block's staging buffer (non-hub rows back to back)
-    auto fetch_row = [&](int v0, int nr, RowPre& P) {
+    // (the block's rows are a.blk_rows[item RB ...]: rows grouped by their
+    // gather length on the host, so the lanes of a warp finish together)
+    auto fetch_row = [&](int item, int nr, RowPre& P) {
         if (lane >= nr) return;
-        const int v = v0 + lane;
+        const int* rows = a.blk_rows + (size_t)item * RB;
+        const int v = rows[lane];
+        P.v = v;
         P.pn = a.occ_pn[v];
         P.hub = a.hub_of[v];
         P.rho = a.rowRho[v];
         P.guard = a.rowGuard[v];
         unsigned off = 0;
-        for (int r = 0; r < lane; ++r)
-            if (a.hub_of[v0 + r] < 0) off += a.upd_ptr[v0 + r + 1] - a.upd_ptr[v0 + r];
+        for (int r = 0; r < lane; ++r) {
+            const int u = rows[r];
+            if (a.hub_of[u] < 0) off += a.upd_ptr[u + 1] - a.upd_ptr[u];
+        }
         P.roff = (int)off;
         P.rbeg = (int)a.upd_ptr[v];
         P.nrec = (int)(a.upd_ptr[v + 1] - a.upd_ptr[v]);
     };
     RowPre pre{};
-    int pend_v0 = -1, pend_nr = 0;
+    bool pending = false;
+    int pend_nr = 0;
     int item = slot[1];
     if (item < nitems) {
-        fetch_row(item * RB, min(RB, a.V - item * RB), pre);
+        fetch_row(item, min(RB, a.V - item * RB), pre);
         stage(min(RB, a.V - item * RB), rec, false, pre);
     }
     __syncwarp();
     int it = 0;
     for (; item < nitems; ++it) {
-        const int v0 = item * RB, nr = min(RB, a.V - v0);
+        const int nr = min(RB, a.V - item * RB);
         uint32_t* rb_cur = rec + (size_t)(nbufs == 2 ? (it & 1) : 0) * recw;
         uint32_t* rb_nxt = rec + (size_t)(nbufs == 2 ? ((it + 1) & 1) : 0) * recw;
         uint32_t* pl = pl0 + (MODE == 2 ? (size_t)(it & 1) * 2 * RB * NW : 0);
-        if (lane == 0) {
-            slot[it & 1] = atomicAdd(&a.ds->row_counter, 1);
-            const uint32_t bytes = (uint32_t)nr * (uint32_t)N * 4u;
-            prefetch_l2(a.theta + (size_t)v0 * N, bytes);
-            prefetch_l2(a.m + (size_t)v0 * N, bytes);
-            prefetch_l2(a.v + (size_t)v0 * N, bytes);
-        }
+        if (lane == 0) slot[it & 1] = atomicAdd(&a.ds->row_counter, 1);
         if (lane < nr) {                                   // this block's row values (prefetched)
+            const uint32_t bytes = (uint32_t)N * 4u;
+            prefetch_l2(a.theta + (size_t)pre.v * N, bytes);
+            prefetch_l2(a.m + (size_t)pre.v * N, bytes);
+            prefetch_l2(a.v + (size_t)pre.v * N, bytes);
             BlkRow& R = rp[lane];
+            R.v = pre.v;
             R.hub = pre.hub;
             R.dsum = pre.pn.y - pre.pn.x;
             R.rho = pre.rho;
@@ -227,7 +250,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
 
         // ---- 1+2: gather (lane = row x word), transpose to bytes (KB = 16: all rows are hubs)
         if constexpr (KB <= 8) if (gr < nr) {
-            const int v = v0 + gr;
+            const int v = rp[gr].v;
             if (rp[gr].hub < 0) {
                 const uint32_t* rbase = rb_cur + rp[gr].roff;
                 auto recf = [&](unsigned i) { return rbase[i]; };
@@ -257,37 +280,41 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
                 }
             }
         }
-        if (MODE == 2 && pend_v0 >= 0 && lane < pend_nr)       // previous block's Q, sent a block ago
-            rp[lane].pq = peer_row_recv(a.px, 1, pend_v0 + lane, sc->xgen, a.ds, rp[lane].pq);
+        if (MODE == 2 && pending && lane < pend_nr)          // previous block's Q, sent a block ago
+            rp[lane].pq = peer_row_recv(a.px, 1, rp[lane].pv, sc->xgen, a.ds, rp[lane].pq);
         __syncwarp();
         const int item_next = slot[it & 1];
-        const int v0n = item_next < nitems ? item_next * RB : a.V;
-        if (v0n < a.V) fetch_row(v0n, min(RB, a.V - v0n), pre);       // the next block's row values
+        const int nrn = item_next < nitems ? min(RB, a.V - item_next * RB) : 0;
+        if (nrn > 0) fetch_row(item_next, nrn, pre);                 // the next block's row values
         auto stage_next = [&]() {
-            if (v0n < a.V) stage(min(RB, a.V - v0n), rb_nxt, true, pre);
+            if (nrn > 0) stage(nrn, rb_nxt, true, pre);
             cp_async_commit();
         };
         if (nbufs == 1) stage_next();
-        if (MODE == 2 && pend_v0 >= 0) {
-            finish_block(pend_v0, pend_nr, pl0 + (size_t)((it + 1) & 1) * 2 * RB * NW, true);
-            pend_v0 = -1;
+        if (MODE == 2 && pending) {
+            finish_block(pend_nr, pl0 + (size_t)((it + 1) & 1) * 2 * RB * NW, true);
+            pending = false;
         }
 
         // ---- 3a: G -> dpk, J partial per row (flat float4 stream over the block)
-        const int total = nr * ipr;
         {
-            const float* tb = a.theta + (size_t)v0 * N;
-            float4 th_nx = *reinterpret_cast<const float4*>(tb + 4 * lane);
+            // one float4 stream over the block's rows: the one-ahead load
+            // crosses to the next row of the block
+            auto rowp = [&](const float* base, int r) { return base + (size_t)rp[r].v * N + 4 * lane; };
+            float4 th_nx = *reinterpret_cast<const float4*>(rowp(a.theta, 0));
             long long I = 0;
             int k = 0;                                           // flat 128-candidate iteration of the block
             for (int r = 0; r < nr; ++r) {
               const int hub = rp[r].hub, dsum = rp[r].dsum;
               const float p2 = rp[r].p2;
               const bool jv = rp[r].jvalid != 0;
+              const float* trn = r + 1 < nr ? rowp(a.theta, r + 1) : nullptr;
+              const float* trc = rowp(a.theta, r);
               for (int kk = 0; kk < ipr; ++kk, ++k) {
                 const int n = kk * 128 + 4 * lane;
                 const float4 th4 = th_nx;
-                if (k + 1 < total) th_nx = *reinterpret_cast<const float4*>(tb + (size_t)(k + 1) * 128 + 4 * lane);
+                if (kk + 1 < ipr) th_nx = *reinterpret_cast<const float4*>(trc + (kk + 1) * 128);
+                else if (trn) th_nx = *reinterpret_cast<const float4*>(trn);
                 const float th[4] = {th4.x, th4.y, th4.z, th4.w};
                 float4 g4[KB];
 #pragma unroll
@@ -328,15 +355,15 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
                     if (jv) I += jterm(Gq[q], th[q], p2);
                 }
               }
-              I = warp_sum(I);                                   // the row's J partial
+              I = warp_sum_redux(I);                             // the row's J partial
               if (lane == 0) rp[r].jt = I;
               I = 0;
             }
         }
         __syncwarp();
         if (MODE == 2 && a.px.exchange_rows) {                   // the block's J_v over all ranks
-            if (lane < nr) peer_row_send(a.px, 0, v0 + lane, rp[lane].jt, sc->xgen);
-            if (lane < nr) rp[lane].jt = peer_row_recv(a.px, 0, v0 + lane, sc->xgen, a.ds, rp[lane].jt);
+            if (lane < nr) peer_row_send(a.px, 0, rp[lane].v, rp[lane].jt, sc->xgen);
+            if (lane < nr) rp[lane].jt = peer_row_recv(a.px, 0, rp[lane].v, sc->xgen, a.ds, rp[lane].jt);
         }
         if (nbufs == 2) stage_next();
         if (lane < nr) {
@@ -355,25 +382,26 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
 
         // ---- 3b: grad, AdamW, next-state statistics and sign planes (flat stream)
         {
-            float* tb = a.theta + (size_t)v0 * N;
-            float* mb = a.m + (size_t)v0 * N;
-            float* vb = a.v + (size_t)v0 * N;
             constexpr bool mag = MAG;
-            float4 thn = ld_last(tb + 4 * lane), mn4 = ld_last(mb + 4 * lane), vn4 = ld_last(vb + 4 * lane);
+            size_t o0 = (size_t)rp[0].v * N + 4 * lane;          // element offset of this lane in row 0
+            float4 thn = ld_last(a.theta + o0), mn4 = ld_last(a.m + o0), vn4 = ld_last(a.v + o0);
             long long Qn = 0;
             float mx = 0.0f;
             int k = 0;
             for (int r = 0; r < nr; ++r) {
               const float rhof = rp[r].rhof, ncf = rp[r].ncf;
-              const int v = v0 + r;
+              const int v = rp[r].v;
+              const size_t orow = (size_t)v * N + 4 * lane;
+              const size_t onext = r + 1 < nr ? (size_t)rp[r + 1].v * N + 4 * lane : 0;
               for (int kk = 0; kk < ipr; ++kk, ++k) {
                 const int n = kk * 128 + 4 * lane;
-                const size_t e = (size_t)k * 128 + 4 * lane;     // flat element of the block
+                const size_t e = orow + (size_t)kk * 128;        // this lane's 4 candidates of row v
                 const float4 th4 = thn, m4 = mn4, v4 = vn4;
-                if (k + 1 < total) {
-                    thn = ld_last(tb + e + 128);
-                    mn4 = ld_last(mb + e + 128);
-                    vn4 = ld_last(vb + e + 128);
+                if (kk + 1 < ipr || r + 1 < nr) {               // one ahead, across the block's rows
+                    const size_t en = kk + 1 < ipr ? e + 128 : onext;
+                    thn = ld_last(a.theta + en);
+                    mn4 = ld_last(a.m + en);
+                    vn4 = ld_last(a.v + en);
                 }
                 float th[4] = {th4.x, th4.y, th4.z, th4.w};
                 float mm[4] = {m4.x, m4.y, m4.z, m4.w};
@@ -417,9 +445,9 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
                         nnib |= (x < 0.0f ? 1u : 0u) << q;
                     }
                 }
-                st_stream(tb + e, make_float4(th[0], th[1], th[2], th[3]));
-                st_stream(mb + e, make_float4(mm[0], mm[1], mm[2], mm[3]));
-                st_stream(vb + e, make_float4(vv[0], vv[1], vv[2], vv[3]));
+                st_stream(a.theta + e, make_float4(th[0], th[1], th[2], th[3]));
+                st_stream(a.m + e, make_float4(mm[0], mm[1], mm[2], mm[3]));
+                st_stream(a.v + e, make_float4(vv[0], vv[1], vv[2], vv[3]));
                 unsigned pw = pnib << (4 * (lane & 7)), nw = nnib << (4 * (lane & 7));
 #pragma unroll
                 for (int o = 1; o < 8; o <<= 1) {
@@ -431,8 +459,8 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
                     pl[RB * NW + r * NW + (n >> 5)] = nw;
                 }
               }
-              Qn = warp_sum(Qn);                                 // the row's Q partial and max |theta|
-              mx = warp_maxf(mx);
+              Qn = warp_sum_redux(Qn);                           // the row's Q partial and max |theta|
+              mx = warp_max_redux(mx);
               if (lane == 0) { rp[r].qt = Qn; rp[r].m2 = mx; }
               Qn = 0;
               mx = 0.0f;
@@ -443,22 +471,23 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
         if (MODE == 2 && a.px.exchange_rows) {
             // the block's Q_{t+1,v} over all ranks: send now, finish after the next block's gather
             if (lane < nr) {
-                peer_row_send(a.px, 1, v0 + lane, rp[lane].qt, sc->xgen);
+                peer_row_send(a.px, 1, rp[lane].v, rp[lane].qt, sc->xgen);
                 rp[lane].pq = rp[lane].qt;
                 rp[lane].pm2 = rp[lane].m2;
+                rp[lane].pv = rp[lane].v;
             }
-            pend_v0 = v0;
+            pending = true;
             pend_nr = nr;
         } else {
-            finish_block(v0, nr, pl, false);
+            finish_block(nr, pl, false);
         }
         __syncwarp();
         item = item_next;
     }
-    if (MODE == 2 && pend_v0 >= 0) {
-        if (lane < pend_nr) rp[lane].pq = peer_row_recv(a.px, 1, pend_v0 + lane, sc->xgen, a.ds, rp[lane].pq);
+    if (MODE == 2 && pending) {
+        if (lane < pend_nr) rp[lane].pq = peer_row_recv(a.px, 1, rp[lane].pv, sc->xgen, a.ds, rp[lane].pq);
         __syncwarp();
-        finish_block(pend_v0, pend_nr, pl0 + (size_t)((it + 1) & 1) * 2 * RB * NW, true);
+        finish_block(pend_nr, pl0 + (size_t)((it + 1) & 1) * 2 * RB * NW, true);
     }
 }
 
