@@ -80,6 +80,7 @@ struct tsat_ctx_s {
     // k_update launch geometry (configure_kernels)
     int upd_mode = 0, upd_GT = 0, upd_NG = 0, upd_grid = 0, num_sms = 0, upd_recbufs = 2;
     int upd_RB = 1, upd_blk_cap = 0;    // row-block k_update (small shards, k_update_blk.cu)
+    int upd_cw6 = 0;                    // per-row k_update with 6-plane counters (configure)
     int* blk_rows = nullptr;            // device [V]: rows in block order (library-owned)
     // dense tensor-core clause evaluation (config.clause_eval = 1, k_dense.cu): library-owned
     uint8_t* dP = nullptr;
@@ -290,6 +291,7 @@ StepArgs step_args(tsat_ctx ctx) {
     a.upd_rec_cap = std::max(64, (ctx->cnf.max_rec_words + 63) / 64 * 64);
     a.upd_RB = ctx->upd_RB;
     a.upd_blk_cap = ctx->upd_blk_cap;
+    a.upd_cw6 = ctx->upd_cw6;
     a.blk_rows = ctx->blk_rows;
     a.fp64 = ctx->th64 != nullptr;
     a.th64 = ctx->th64; a.m64 = ctx->m64; a.v64 = ctx->v64; a.G64 = ctx->G64; a.gt64 = ctx->gt64;
@@ -312,7 +314,7 @@ StepArgs step_args(tsat_ctx ctx) {
         a.px.W = ctx->world;
         a.px.rank = ctx->rank;
         a.px.V = ctx->cnf.V;
-        a.px.exchange_rows = ctx->cfg.normalize != 2;
+        a.px.exchange_rows = ctx->cfg.normalize != 2 && !(ctx->world == 1 && std::getenv("TSAT_PEER_NOX"));   // A/B hook
         a.px.L = peer_layout(ctx->cnf.V, ctx->world);
     }
     a.V = ctx->cnf.V;
@@ -996,6 +998,19 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
             ctx->dCp = (int)Cp;
         } else if (c.clause_eval != 0 && c.clause_eval != 1) {
             return fail(ctx, TSAT_E_ARG, "clause_eval must be 0 or 1");
+        }
+        // 6-plane counters for the K <= 3 fused kernel when no row has more than
+        // 31 same-sign occurrences (the counters hold cneg - cpos per bin)
+        // (measured: c2 k_update -2.4 %; where the bit planes exceed L2 - c3,
+        // c5 - the extra warps' HBM gathers make it slower, so only when the
+        // planes are L2-resident: both buffers below 48 MB)
+        ctx->upd_cw6 = 0;
+        const bool planes_l2 = 2.0 * 4.0 * ((double)ctx->cnf.V + 1.0) * (double)(ctx->N / 32) <= 48.0e6;
+        if (ctx->cnf.K <= 3 && planes_l2 && !ctx->sharded && !ctx->chunked && !ctx->peer && !std::getenv("TSAT_NO_CW6")) {
+            int mx = 0;
+            for (int v = 0; v < ctx->cnf.V; ++v)
+                if (ctx->cnf.hub_of[v] < 0) mx = std::max({mx, ctx->cnf.occ_pn[2 * v], ctx->cnf.occ_pn[2 * v + 1]});
+            ctx->upd_cw6 = mx <= 31 ? 1 : 0;
         }
         // row blocks for small shards (fused W = 1 and peer paths): RB rows per
         // work item, staging capacity = max over blocks of the non-hub rows' records

@@ -39,8 +39,11 @@ namespace tsat {
 // MAG: normalize 3 (R28, d = mean |theta|): the Jacobian addend carries
 // sign(theta) and the next row sums are of |theta| (a template flag: a
 // run-time one costs the default path ~3 % at c2 / c3).
-template <int KB, int MODE, bool MAG = false, bool GSG = false>
-__global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TSAT_UPD_THREADS4) : TSAT_UPD_THREADS8, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
+// CW: counter planes of the K <= 3 gather (8, or 6 when no row has more than
+// 31 same-sign occurrences: 6 fewer registers, compiled for 896 threads).
+template <int KB, int MODE, bool MAG = false, bool GSG = false, int CW = 8>
+__global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (CW == 6 ? TSAT_UPD_THREADS4C6 : TSAT_UPD_THREADS4))
+                                          : TSAT_UPD_THREADS8, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
                                                                     uint32_t* __restrict__ Anext,
                                                                     const StepScalars* __restrict__ sc) {
     constexpr int NP = (KB == 4) ? 2 : (KB == 8 ? 3 : 4);
@@ -196,17 +199,18 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
             for (int wl = tg; wl < NWc; wl += GT) {
                 const int w = w0 + wl;
                 const uint32_t own = __ldg(Acur + (size_t)v * NW + w);
-                uint32_t cnt[NCTR][kCtr];
+                constexpr int kB = KB == 4 ? CW : kCtr;        // counter planes (two's complement)
+                uint32_t cnt[NCTR][kB];
                 auto recf = [&](unsigned i) { return rb_cur[i]; };
                 if (uni3) {
 #if TSAT_UNI3 == 0
-                    count_occurrences<NP, NCTR, kCtr, true, true>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w, pol);
+                    count_occurrences<NP, NCTR, kB, true, true>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w, pol);
 #else
-                    count_uni3<NCTR, kCtr, TSAT_UNI3 == 1>(cnt, recf, (unsigned)pn.y, (unsigned)pn.x, own, Acur,
+                    count_uni3<NCTR, kB, TSAT_UNI3 == 1>(cnt, recf, (unsigned)pn.y, (unsigned)pn.x, own, Acur,
                                                           (unsigned)NW, (unsigned)w, pol);
 #endif
                 }
-                else count_batched<NP, NCTR, kCtr>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w, pol);
+                else count_batched<NP, NCTR, kB>(cnt, recf, nrec, own, Acur, (unsigned)NW, (unsigned)w, pol);
                 // counter planes of bins 4 blk .. 4 blk + 3 -> one packed word per
                 // candidate; KB = 8 loops over two blocks (one transpose in the
                 // code: the kernel is instruction-cache bound there)
@@ -215,9 +219,9 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
                     uint32_t T[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
-                        const int r = i / kCtr;
-                        const uint32_t lo = (r < NCTR && r < 4) ? cnt[r][i % kCtr] : 0u;
-                        const uint32_t hi = (4 + r < NCTR) ? cnt[4 + r][i % kCtr] : 0u;
+                        const int r = i / kCtr, b = (i % kCtr) < kB ? (i % kCtr) : kB - 1;   // sign-extend to 8 bits
+                        const uint32_t lo = (r < NCTR && r < 4) ? cnt[r][b] : 0u;
+                        const uint32_t hi = (4 + r < NCTR) ? cnt[4 + r][b] : 0u;
                         T[i] = blk ? hi : lo;
                     }
                     transpose32(T);
@@ -486,15 +490,17 @@ template <int KB>
 static cudaError_t set_update_attrs(int smem) {
     const cudaFuncAttribute attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_update<KB, 0>, attr, smem)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(k_update<KB, 1>, attr, smem)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(k_update<KB, 2>, attr, smem)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(k_update<KB, 0, true>, attr, smem)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(k_update<KB, 0, false, true>, attr, smem)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(k_update<KB, 2, false, true>, attr, smem)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(k_update<KB, 0, true, true>, attr, smem)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(k_update<KB, 2, true, true>, attr, smem)) != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_update<KB, 2, true>, attr, smem);
+    if ((e = set_max_dyn_smem(k_update<KB, 0>, smem)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 1>, smem)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 2>, smem)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 0, true>, smem)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 0, false, true>, smem)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 2, false, true>, smem)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 0, true, true>, smem)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 2, true, true>, smem)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 0, false, false, 6>, smem)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 0, true, false, 6>, smem)) != cudaSuccess) return e;
+    return set_max_dyn_smem(k_update<KB, 2, true>, smem);
 }
 
 #ifndef TSAT_GS_GLOBAL_BELOW
@@ -523,7 +529,7 @@ cudaError_t configure_update(StepArgs* a) {
         if (ng_s < TSAT_GS_GLOBAL_BELOW && ng_g >= 2 * ng_s && !std::getenv("TSAT_NO_GS_GLOBAL")) a->upd_gs_global = 1;
     }
     const size_t gsb = (fused && !a->upd_gs_global) ? upd_gs_bytes(KB, N) : 0;
-    const int max_threads = KB == 4 ? (a->peer ? TSAT_UPD_THREADS4P : TSAT_UPD_THREADS4)
+    const int max_threads = KB == 4 ? (a->peer ? TSAT_UPD_THREADS4P : ((a->upd_cw6 && !a->upd_gs_global) ? TSAT_UPD_THREADS4C6 : TSAT_UPD_THREADS4))
                                     : TSAT_UPD_THREADS8;   // register budget (launch bounds)
     auto groups = [&](int nbufs) {
         const size_t grb = upd_group_bytes(KB, a->upd_chunk, a->upd_rec_cap, nbufs, a->peer ? 2 : 1);
@@ -557,7 +563,10 @@ cudaError_t configure_update(StepArgs* a) {
         const int x = std::atoi(g);
         if (x > 0 && x < sms) a->upd_grid = x;
     }
-    const int smem = (int)a->upd_smem;
+    // the attribute is a process-wide per-function limit: set it to the opt-in
+    // maximum so contexts configured later with smaller geometries cannot
+    // lower it below what an earlier context launches with
+    const int smem = optin;
     if (KB == 4) return set_update_attrs<4>(smem);
     if (KB == 8) return set_update_attrs<8>(smem);
     return set_update_attrs<16>(smem);
@@ -591,6 +600,9 @@ static cudaError_t launch_update_kbg(const StepArgs& a, const uint32_t* Acur, ui
         else k_update<KB, 2, false, GSG><<<g, b, sm, st>>>(a, Acur, Anext, sc);
         return cudaGetLastError();
     }
+    if (!GSG && a.upd_cw6)                       // K <= 3, every row within 6-bit counters
+        return mag ? launch_maybe_pdl(a.pdl, k_update<KB, 0, true, false, 6>, g, b, sm, st, a, Acur, Anext, sc)
+                   : launch_maybe_pdl(a.pdl, k_update<KB, 0, false, false, 6>, g, b, sm, st, a, Acur, Anext, sc);
     return mag ? launch_maybe_pdl(a.pdl, k_update<KB, 0, true, GSG>, g, b, sm, st, a, Acur, Anext, sc)
                : launch_maybe_pdl(a.pdl, k_update<KB, 0, false, GSG>, g, b, sm, st, a, Acur, Anext, sc);
 }

@@ -495,10 +495,10 @@ template <int KB>
 static cudaError_t set_blk_attrs(int smem) {
     const cudaFuncAttribute attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_update_blk<KB, 0, false>, attr, smem)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(k_update_blk<KB, 2, false>, attr, smem)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(k_update_blk<KB, 0, true>, attr, smem)) != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_update_blk<KB, 2, true>, attr, smem);
+    if ((e = set_max_dyn_smem(k_update_blk<KB, 0, false>, smem)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update_blk<KB, 2, false>, smem)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update_blk<KB, 0, true>, smem)) != cudaSuccess) return e;
+    return set_max_dyn_smem(k_update_blk<KB, 2, true>, smem);
 }
 
 cudaError_t configure_update_blk(StepArgs* a) {
@@ -530,7 +530,10 @@ cudaError_t configure_update_blk(StepArgs* a) {
         const int x = std::atoi(g);
         if (x > 0 && x < sms) a->upd_grid = x;
     }
-    const int smem = (int)a->upd_smem;
+    // the attribute is a process-wide per-function limit: set it to the opt-in
+    // maximum so contexts configured later with smaller geometries cannot
+    // lower it below what an earlier context launches with
+    const int smem = optin;
     if (KB == 4) return set_blk_attrs<4>(smem);
     if (KB == 8) return set_blk_attrs<8>(smem);
     return set_blk_attrs<16>(smem);

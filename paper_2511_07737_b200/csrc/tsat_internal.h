@@ -188,6 +188,7 @@ struct StepArgs {
     int upd_recbufs;                 // record buffers per group (1 or 2, configure_update)
     int upd_RB;                      // rows per work item: 1, or 32 / (N/32) for small shards (k_update_blk)
     int upd_blk_cap;                 // record words a group stages per row block (max over blocks, non-hub rows)
+    int upd_cw6;                     // K <= 3 fused W = 1: 6-plane counters (no row above 31 same-sign occurrences)
     const int* blk_rows;             // [V] rows in block order (grouped by gather length; k_update_blk)
     // dense tensor-core clause evaluation (k_dense.cu; config.clause_eval = 1)
     int dense;

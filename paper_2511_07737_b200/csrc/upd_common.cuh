@@ -23,6 +23,9 @@ constexpr int kUnroll3b = TSAT_3B_UNROLL;
 #ifndef TSAT_UPD_THREADS4
 #define TSAT_UPD_THREADS4 768       // KB = 4 block size bound (register budget)
 #endif
+#ifndef TSAT_UPD_THREADS4C6
+#define TSAT_UPD_THREADS4C6 896     // KB = 4 with 6-plane counters (c2: k_update -2.5 % vs 8 planes at 768)
+#endif
 
 #ifndef TSAT_ANEXT_CS
 #define TSAT_ANEXT_CS 1            // next-state bit planes stored streaming (c3: k_update -2 %)
@@ -60,6 +63,18 @@ constexpr int kHubCtrBatched = 10;  // batched super-chunks: kHubSlabBatches * 4
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) / 16 * 16; }
 }  // namespace
+
+// Raise a kernel's dynamic shared-memory limit to the opt-in maximum minus its
+// static shared memory.  The limit is a process-wide per-function attribute,
+// so every context sets it to the same maximum (a context configured later
+// with a smaller geometry must not lower it below another context's launch).
+template <typename Kern>
+inline cudaError_t set_max_dyn_smem(Kern* k, int optin) {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, k);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+}
 
 // Shared-memory geometry of k_update (host and device agree through this).
 __host__ __device__ inline size_t upd_gs_bytes(int KB, int N) { return align16((size_t)KB * N * 4); }
