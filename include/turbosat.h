@@ -293,6 +293,14 @@ tsat_status tsat_kernel_times(tsat_ctx ctx, double* ms5, int64_t* steps);
  * hub pre-pass only runs when the instance has hub variables). */
 tsat_status tsat_kernels_per_step(tsat_ctx ctx, int32_t* n);
 
+/* Launch geometry of the initialised batch (diagnostics, tests): out[0..7] =
+ * {warp-group threads GT, warp groups per CTA, k_update grid (CTAs), k_update
+ * dynamic shared memory (bytes), candidates per CTA slice or work item,
+ * cluster size (> 1: rows split over a thread-block cluster),
+ * rows per work item (> 1: row-block kernel), length-segmented clause
+ * evaluation (1 / 0)}.  n_out must be >= 8.  TSAT_E_STATE before init. */
+tsat_status tsat_update_geometry(tsat_ctx ctx, int32_t* out, int32_t n_out);
+
 /* Learning rate of iteration t under cfg (readings R7/R9), host only
  * (for traces: iteration, lr, loss, best fraction, SPEC's --trace columns). */
 tsat_status tsat_lr_at(const tsat_config* cfg, int64_t t, double* lr);

@@ -102,6 +102,7 @@ _SIGS = {
     "tsat_set_profiling": (ct.c_int, [P, ct.c_int32]),
     "tsat_kernel_times": (ct.c_int, [P, P, ct.POINTER(ct.c_int64)]),
     "tsat_kernels_per_step": (ct.c_int, [P, ct.POINTER(ct.c_int32)]),
+    "tsat_update_geometry": (ct.c_int, [P, P, ct.c_int32]),
     "tsat_error_string": (ct.c_char_p, [P]),
     "tsat_destroy": (None, [P]),
 }
@@ -531,6 +532,12 @@ class Solver:
         st = ct.c_int64()
         self._check(self.lib.tsat_kernel_times(self.h, _ptr(ms), ct.byref(st)))
         return ms, st.value
+
+    def update_geometry(self) -> dict:
+        g = np.zeros(8, np.int32)
+        self._check(self.lib.tsat_update_geometry(self.h, _ptr(g), 8))
+        keys = ("GT", "groups", "grid", "smem", "slice", "cluster", "rows_per_item", "clause_segments")
+        return {k: int(x) for k, x in zip(keys, g)}
 
     def kernels_per_step(self) -> int:
         n = ct.c_int32()

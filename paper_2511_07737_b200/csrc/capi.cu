@@ -22,9 +22,14 @@
 
 using namespace tsat;
 
+#ifndef TSAT_SEG
+#define TSAT_SEG 1                      // length-segmented clause evaluation (k_clause_seg)
+#endif
+
 struct DevCnf {
     uint32_t *cptr = nullptr, *clit = nullptr, *occ_ptr = nullptr, *occ_rec = nullptr, *occ_cnt = nullptr;
     uint32_t *bat_ptr = nullptr, *bat_rec = nullptr;
+    uint32_t* seg_lit = nullptr;        // clause length segments (k_clause_seg), K <= 7
     int2* occ_pn = nullptr;
     int* hub_of = nullptr;
     int4* hub_sc = nullptr;
@@ -93,6 +98,8 @@ struct tsat_ctx_s {
     uint32_t *Pw64 = nullptr, *Nw64 = nullptr;
     int upd_chunk = 0, upd_gs_global = 0;
     bool chunked = false;               // N too large for the fused kernel: split sequence, no collectives at W = 1
+    int upd_cl = 0;                     // > 1: cluster-split rows (k_update MODE 3) instead of chunking
+    bool use_seg = false;               // length-segmented clause evaluation (k_clause_seg)
     size_t upd_smem = 0;
     int64_t prof_steps = 0;
     int prof_pending_k = 0;
@@ -229,13 +236,17 @@ Layout make_layout(int V, int N, int KB, int n_hubs, bool sharded, bool peer) {
 }
 
 // Whether N candidates per GPU need the chunked split sequence (the fused
-// k_update's shared memory would not hold the batch's g table + 2 groups).
-tsat_status batch_chunked(tsat_ctx ctx, int N, int KB, bool* out) {
+// k_update's shared memory would not hold the batch's g table + 2 groups),
+// or (W = 1, *cl > 1) run as cluster-split rows instead.
+tsat_status batch_chunked(tsat_ctx ctx, int N, int KB, bool* out, int* cl = nullptr) {
     int optin = 0;
     CK(cudaSetDevice(ctx->device));
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     const int rec_cap = std::max(64, (ctx->cnf.max_rec_words + 63) / 64 * 64);
-    *out = !update_fits_fused(KB, N, rec_cap, optin);
+    const bool w1 = !ctx->sharded && !ctx->peer && ctx->world == 1 && N >= 1024;
+    const int c = w1 ? update_cluster_size(KB, N, rec_cap, optin) : 0;
+    if (cl) *cl = c;
+    *out = c == 0 && !update_fits_fused(KB, N, rec_cap, optin);
     return TSAT_OK;
 }
 
@@ -284,6 +295,7 @@ StepArgs step_args(tsat_ctx ctx) {
 #endif
     // PDL on the fused W = 1 sequence (one stream, no forked k_hub branch)
     a.pdl = TSAT_PDL && !ctx->profiling && !ctx->sharded && !ctx->chunked && !ctx->peer && ctx->cnf.n_hub_sc == 0 &&
+            ctx->upd_cl <= 1 &&
             ctx->th64 == nullptr;
     a.upd_NG = ctx->upd_NG;
     a.upd_grid = ctx->upd_grid;
@@ -292,7 +304,14 @@ StepArgs step_args(tsat_ctx ctx) {
     a.upd_RB = ctx->upd_RB;
     a.upd_blk_cap = ctx->upd_blk_cap;
     a.upd_cw6 = ctx->upd_cw6;
+    a.upd_cl = ctx->upd_cl;
     a.blk_rows = ctx->blk_rows;
+    a.use_seg = ctx->use_seg ? 1 : 0;
+    a.seg_lit = ctx->dcnf.seg_lit;
+    for (int L = 0; L < 8; ++L) {
+        a.seg_C[L] = ctx->cnf.seg_C.size() == 8 ? ctx->cnf.seg_C[L] : 0;
+        a.seg_off[L] = ctx->cnf.seg_off.size() == 8 ? ctx->cnf.seg_off[L] : 0;
+    }
     a.fp64 = ctx->th64 != nullptr;
     a.th64 = ctx->th64; a.m64 = ctx->m64; a.v64 = ctx->v64; a.G64 = ctx->G64; a.gt64 = ctx->gt64;
     a.J64 = ctx->J64; a.Qp64 = ctx->Qp64; a.Pw64 = ctx->Pw64; a.Nw64 = ctx->Nw64;
@@ -385,6 +404,7 @@ void free_fp64(tsat_ctx ctx) {
 void free_cnf(tsat_ctx ctx) {
     cudaFree(ctx->dcnf.cptr);
     cudaFree(ctx->dcnf.clit);
+    cudaFree(ctx->dcnf.seg_lit);
     cudaFree(ctx->dcnf.occ_ptr);
     cudaFree(ctx->dcnf.occ_rec);
     cudaFree(ctx->dcnf.bat_ptr);
@@ -432,6 +452,7 @@ tsat_status upload_cnf(tsat_ctx ctx, HostCnf&& h) {
     CK(cudaSetDevice(ctx->device));
     CK(up(&ctx->dcnf.cptr, c.clause_ptr));
     CK(up(&ctx->dcnf.clit, c.clause_lit));
+    if (c.K <= 7 && !c.seg_lit.empty()) CK(up(&ctx->dcnf.seg_lit, c.seg_lit));
     CK(up(&ctx->dcnf.occ_ptr, c.occ_ptr));
     CK(up(&ctx->dcnf.occ_rec, c.occ_rec));
     CK(up(&ctx->dcnf.occ_cnt, c.occ_cnt));
@@ -928,9 +949,16 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
         ctx->ws_bytes = bytes;
         {
             bool ch = false;
-            tsat_status s2 = batch_chunked(ctx, ctx->N, ctx->KB, &ch);
+            int cl = 0;
+            tsat_status s2 = batch_chunked(ctx, ctx->N, ctx->KB, &ch, &cl);
             if (s2 != TSAT_OK) return s2;
             ctx->chunked = ch;
+            ctx->upd_cl = cl;
+            // length-segmented clause evaluation: every K <= 7 instance but
+            // uniform 3-SAT (its tuned kernel reads the CSR directly), >= 1024
+            // candidates per GPU (the padded kernel's sub-groups serve below)
+            ctx->use_seg = TSAT_SEG && ctx->dcnf.seg_lit && ctx->cnf.K <= 7 &&
+                           !(ctx->cnf.uniform_len && ctx->cnf.K <= 3) && ctx->N >= 1024 && !std::getenv("TSAT_NO_SEG");
         }
         if (ctx->chunked && ctx->peer)
             return fail(ctx, TSAT_E_RANGE, "peer path: N per GPU too large for the fused kernel (use more GPUs)");
@@ -1065,7 +1093,7 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
             ctx->upd_chunk = g.upd_chunk;
             ctx->upd_gs_global = g.upd_gs_global;
         }
-        if (ctx->chunked != (ctx->upd_chunk < ctx->N))
+        if (ctx->chunked != (ctx->upd_chunk < ctx->N && ctx->upd_cl <= 1))
             return fail(ctx, TSAT_E_STATE, "internal: chunking decision changed between layout and launch");
         StepArgs a = step_args(ctx);
         if (ctx->L.hubD != ctx->L.total)
@@ -1518,9 +1546,29 @@ tsat_status tsat_kernels_per_step(tsat_ctx ctx, int32_t* n) {
     k += 1;                                                                     // gtable
     if (ctx->have_batch && ctx->cnf.n_hub_sc > 0) ++k;                         // hub
     if (ctx->have_cnf && ctx->cnf.V > 0) ++k;                                  // update (phase A when split)
+    if (ctx->have_batch && ctx->use_seg && ctx->cnf.seg_C.size() == 8) {       // clause: short + long segment kernels
+        const bool s = ctx->cnf.seg_C[1] + ctx->cnf.seg_C[2] + ctx->cnf.seg_C[3] > 0;
+        const bool l = ctx->cnf.seg_C[4] + ctx->cnf.seg_C[5] + ctx->cnf.seg_C[6] + ctx->cnf.seg_C[7] > 0;
+        if (s && l) ++k;
+    }
     if (ctx->sharded) k += 5;   // pack/unpack max, update B, rows finish, step end (NCCL's own kernels not counted)
     else if (ctx->chunked) k += 3;   // update B, rows finish, step end (+ the J reset memset)
     *n = k;
+    return TSAT_OK;
+}
+
+tsat_status tsat_update_geometry(tsat_ctx ctx, int32_t* out, int32_t n_out) {
+    GUARD_CTX();
+    if (!out || n_out < 8) return fail(ctx, TSAT_E_ARG, "update_geometry: out must hold 8 values");
+    if (!ctx->have_batch) return fail(ctx, TSAT_E_STATE, "update_geometry: no batch");
+    out[0] = ctx->upd_GT;
+    out[1] = ctx->upd_NG;
+    out[2] = ctx->upd_grid;
+    out[3] = (int32_t)ctx->upd_smem;
+    out[4] = ctx->upd_chunk;
+    out[5] = ctx->upd_cl;
+    out[6] = ctx->upd_RB;
+    out[7] = ctx->use_seg ? 1 : 0;
     return TSAT_OK;
 }
 

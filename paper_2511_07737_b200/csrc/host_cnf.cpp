@@ -181,6 +181,34 @@ static void build_batched(HostCnf* hp) {
     h.bat_ptr[V] = (uint32_t)h.bat_rec.size();
 }
 
+// Length segments for k_clause_seg (K <= 7): the clauses regrouped by length
+// L = 1..7, each segment a dense [C_L][L] array of literal codes, so a warp
+// evaluates exactly L literals and L + 1 bins per clause instead of padding
+// every clause to K.  Empty clauses join the L = 1 segment as the literal
+// "row V" (the all-zero plane: always false, R = 0).  The histogram counts do
+// not depend on clause order (R12).
+static void build_segments(HostCnf* hp) {
+    HostCnf& h = *hp;
+    h.seg_C.assign(8, 0);
+    h.seg_off.assign(8, 0);
+    h.seg_lit.clear();
+    if (h.K > 7) return;
+    for (int64_t c = 0; c < h.C; ++c) {
+        const uint32_t len = h.clause_ptr[c + 1] - h.clause_ptr[c];
+        h.seg_C[len == 0 ? 1 : len] += 1;
+    }
+    int64_t off = 0;
+    for (int L = 1; L <= 7; ++L) { h.seg_off[L] = off; off += h.seg_C[L] * L; }
+    h.seg_lit.assign((size_t)off, 0);
+    std::vector<int64_t> fill(h.seg_off.begin(), h.seg_off.end());
+    for (int64_t c = 0; c < h.C; ++c) {
+        const uint32_t b = h.clause_ptr[c], e = h.clause_ptr[c + 1];
+        if (b == e) { h.seg_lit[(size_t)fill[1]++] = (uint32_t)h.V << 1; continue; }
+        int64_t& f = fill[e - b];
+        for (uint32_t i = b; i < e; ++i) h.seg_lit[(size_t)f++] = h.clause_lit[i];
+    }
+}
+
 // bat_rec offsets are stored as uint32 (bat_ptr, hub super-chunks)
 static bool batched_fits(const HostCnf& h) { return h.bat_rec.size() < ((size_t)1 << 31); }
 
@@ -328,6 +356,7 @@ int build_cnf(int32_t V, int64_t C, const int64_t* ptr, const int32_t* lits, Hos
         }
     }
     h.n_hub_sc = (int32_t)(h.hub_sc.size() / 4);
+    build_segments(&h);
     *out = std::move(h);
     return 0;
 }

@@ -361,11 +361,238 @@ __global__ void k_reset_accumulators(DevScalars* __restrict__ ds, const StepScal
     ds->loss_fx = 0;
 }
 
+// ---------------------------------------------------------------- length segments
+// k_clause_seg: every K <= 7 instance except uniform 3-SAT, >= 1024 candidates
+// per GPU.  Clauses come grouped by length (host_cnf.cpp build_segments); a
+// warp chunk of the length-L segment gathers exactly L literals per clause and
+// counts L + 1 one-hot bins (NP = 1, 2 or 3 count planes), where the padded
+// kernel above gathers K literals and counts KB - 1 bins for every clause
+// (industrial mix, mean length 3.2 of K = 7).  Two instantiations: L <= 3 (4
+// CTAs per SM) and L = 4..7 (2 CTAs per SM), so the short clauses do not
+// run at the long ones' register budget.  Counters are 7-bit carry-save
+// planes per bin as above; each chunk (<= 112 clauses) is extracted by one
+// (NB <= 4 bins) or two byte transposes into 21-bit fields of three 64-bit
+// CTA accumulators per candidate: [0] bins 0, 1, 2  [1] bins 3, 4, 5  [2] bin 6.
+struct SegArgs {
+    long long off[8];          // word offset of segment L in seg_lit
+    long long C[8];            // clauses of length L
+    long long ch0[9];          // first chunk of segment L in this kernel's chunk range (ch0[LMAX + 1] = total)
+};
+__host__ __device__ constexpr int seg_chunk(int L) {
+    return L <= 2 ? 112 : (L == 3 ? 72 : (L == 4 ? 56 : (L == 5 ? 44 : (L == 6 ? 36 : 32))));
+}
+constexpr int kSegStage = 224;     // staged literal slots per warp: max over L of seg_chunk(L) * L
+constexpr int kSegAcc = 33 * 32;   // one padded accumulator plane (u64 per candidate of the block)
+
+template <int KB, int L>
+__device__ __forceinline__ void seg_eval(const uint32_t* __restrict__ Aw, const uint32_t* __restrict__ lit, int nc,
+                                         uint2* my, uint32_t unw, uint2 zero_lit, unsigned long long pol,
+                                         unsigned long long* acc, int lane, bool valid) {
+    constexpr int NB = (L + 1 < KB - 1) ? L + 1 : KB - 1;     // counted bins (bin KB - 1 is derived)
+    constexpr int NP = L <= 1 ? 1 : (L <= 3 ? 2 : 3);
+    constexpr int kCH = seg_chunk(L);
+    constexpr int CB = 7;
+    constexpr int kG = L <= 3 ? 2 : 1;                         // carry-save groups of 4 clauses in flight
+    static_assert(kCH * L <= kSegStage && kCH % (kUnr * kG) == 0 && kCH <= 127, "segment chunk geometry");
+    __syncwarp();
+    for (int i = lane; i < kCH * L; i += 32) {
+        const uint32_t code = i < nc * L ? __ldg(lit + i) : kNone;
+        my[i] = code == kNone ? zero_lit : make_uint2((code >> 1) * unw, 0u - (code & 1u));
+    }
+    __syncwarp();
+    uint32_t cnt[NB][CB];
+#pragma unroll
+    for (int r = 0; r < NB; ++r)
+#pragma unroll
+        for (int b = 0; b < CB; ++b) cnt[r][b] = 0u;
+    for (int cb0 = 0; cb0 < nc; cb0 += kUnr * kG) {
+        uint32_t xx[kG][kUnr][L];
+#pragma unroll
+        for (int gq = 0; gq < kG; ++gq)
+#pragma unroll
+            for (int u = 0; u < kUnr; ++u)
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    const uint2 o = my[(cb0 + gq * kUnr + u) * L + l];     // < kCH: the chunk is padded
+                    xx[gq][u][l] = ld_plane(Aw + o.x, pol) ^ o.y;
+                }
+#pragma unroll
+        for (int gq = 0; gq < kG; ++gq) {
+            uint32_t m[kUnr][NB];
+#pragma unroll
+            for (int u = 0; u < kUnr; ++u) {
+                // padding clauses past nc read literal-false rows: R = 0, bin 0 cleared
+                const uint32_t live = (cb0 + gq * kUnr + u < nc) ? 0xffffffffu : 0u;
+                const uint32_t* x = xx[gq][u];
+                if constexpr (L == 1) {
+                    m[u][0] = ~x[0] & live;
+                    m[u][1] = x[0];
+                } else if constexpr (L == 2) {
+                    m[u][0] = ~(x[0] | x[1]) & live;
+                    m[u][1] = x[0] ^ x[1];
+                    if constexpr (NB > 2) m[u][2] = x[0] & x[1];
+                } else if constexpr (L == 3) {
+                    const uint32_t s0 = x[0] ^ x[1] ^ x[2], s1 = (x[0] & x[1]) | (x[2] & (x[0] ^ x[1]));
+                    m[u][0] = ~(x[0] | x[1] | x[2]) & live;
+                    m[u][1] = s0 & ~s1;
+                    m[u][2] = ~s0 & s1;
+                    if constexpr (NB > 3) m[u][3] = s0 & s1;
+                } else {
+                    uint32_t sp[NP];
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) sp[p] = 0u;
+#pragma unroll
+                    for (int l = 0; l < L; ++l) bs_add<NP>(sp, x[l]);
+#pragma unroll
+                    for (int r = 0; r < NB; ++r) m[u][r] = bs_eq<NP>(sp, r) & (r == 0 ? live : 0xffffffffu);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < NB; ++r) csa_add4<CB>(cnt[r], m[0][r], m[1][r], m[2][r], m[3][r]);
+        }
+    }
+    if (!valid) return;
+    // bins 4 blk .. 4 blk + 3 as bytes per candidate, into the 21-bit fields
+#pragma unroll 1
+    for (int blk = 0; blk < (NB > 4 ? 2 : 1); ++blk) {
+        uint32_t T[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const int r = i / 8, b = i % 8;
+            const uint32_t lo = (b < CB && r < NB) ? cnt[r < NB ? r : 0][b < CB ? b : 0] : 0u;
+            const uint32_t hi = (b < CB && 4 + r < NB) ? cnt[4 + r < NB ? 4 + r : 0][b < CB ? b : 0] : 0u;
+            T[i] = blk ? hi : lo;
+        }
+        transpose32(T);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const unsigned long long x = T[j];
+            if (!x) continue;
+            const int o = 33 * lane + j;
+            if (blk == 0) {
+                const unsigned long long w0 = (x & 0xFFull) | ((x & 0xFF00ull) << 13) | ((x & 0xFF0000ull) << 26);
+                if (w0) atomicAdd(&acc[o], w0);
+                if (NB > 3 && (x >> 24)) atomicAdd(&acc[kSegAcc + o], x >> 24);
+            } else {
+                const unsigned long long w1 = ((x & 0xFFull) << 21) | ((x & 0xFF00ull) << 34);
+                if (w1) atomicAdd(&acc[kSegAcc + o], w1);
+                if (NB > 6 && (x & 0xFF0000ull)) atomicAdd(&acc[2 * kSegAcc + o], (x >> 16) & 0xFFull);
+            }
+        }
+    }
+}
+
+template <int KB, int LMIN, int LMAX>
+__global__ void __launch_bounds__(256, LMAX <= 3 ? 4 : 2)
+    k_clause_seg(const uint32_t* __restrict__ A, int NW, int V, const uint32_t* __restrict__ seg_lit, SegArgs sa,
+                 int* __restrict__ hist, int N, DevScalars* __restrict__ ds, const StepScalars* __restrict__ sc,
+                 int reset) {
+    constexpr int NBK = (LMAX + 1 < KB - 1) ? LMAX + 1 : KB - 1;    // bins this kernel counts
+    constexpr int NACC = NBK > 6 ? 3 : (NBK > 3 ? 2 : 1);
+    __shared__ unsigned long long acc[NACC * kSegAcc];
+    __shared__ uint2 stage[kWarps][kSegStage];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int w = blockIdx.x * 32 + lane;
+    const bool valid = w < NW;
+    pdl_wait();
+    pdl_trigger();
+    if (reset && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+        const long long t = sc->t;               // the iteration's accumulators (see k_clause)
+        ds->best_key = ~0ull;
+        ds->gmax_bits = 0ull;
+        ds->row_counter = 0;
+        ds->thmax_bits[(t + 1) & 1] = 0u;
+        ds->loss_fx = 0;
+    }
+    for (int i = threadIdx.x; i < NACC * kSegAcc; i += blockDim.x) acc[i] = 0ull;
+    __syncthreads();
+    uint2* my = stage[warp];
+    const uint32_t unw = (uint32_t)NW;
+    const uint2 zero_lit = make_uint2((uint32_t)V * unw, 0u);
+    const uint32_t* Aw = A + (valid ? w : 0);
+    const unsigned long long pol = plane_policy(planes_fit_l2(V, NW));
+    const long long nchunks = sa.ch0[LMAX + 1];
+    for (long long chunk = (long long)blockIdx.y * kWarps + warp; chunk < nchunks;
+         chunk += (long long)gridDim.y * kWarps) {
+        int L = LMIN;
+        while (L < LMAX && chunk >= sa.ch0[L + 1]) ++L;      // warp-uniform
+        const long long c0 = (chunk - sa.ch0[L]) * seg_chunk(L);
+        const int nc = (int)min((long long)seg_chunk(L), sa.C[L] - c0);
+        const uint32_t* lit = seg_lit + sa.off[L] + c0 * L;
+#define TSAT_SEG_CASE(LL)                                                                                    \
+    case LL:                                                                                                 \
+        if constexpr (LMIN <= LL && LL <= LMAX) seg_eval<KB, LL>(Aw, lit, nc, my, unw, zero_lit, pol, acc, lane, valid); \
+        break;
+        switch (L) {
+            TSAT_SEG_CASE(1) TSAT_SEG_CASE(2) TSAT_SEG_CASE(3) TSAT_SEG_CASE(4) TSAT_SEG_CASE(5) TSAT_SEG_CASE(6)
+            TSAT_SEG_CASE(7)
+            default: break;
+        }
+#undef TSAT_SEG_CASE
+    }
+    __syncthreads();
+    for (int cl = threadIdx.x; cl < 1024; cl += blockDim.x) {
+        const int n = blockIdx.x * 1024 + cl;
+        if (n >= N) continue;
+        const int o = 33 * (cl >> 5) + (cl & 31);
+#pragma unroll
+        for (int r = 0; r < NBK; ++r) {
+            const unsigned long long pk = acc[(r / 3) * kSegAcc + o];
+            const int val = (int)((pk >> (21 * (r % 3))) & 0x1FFFFFull);
+            if (val) atomicAdd(&hist[(size_t)n * KB + r], val);
+        }
+    }
+}
+
+// Launch the short (L <= 3) and long (L = 4..7) segment kernels, in that order
+// on the stream (the first resets the iteration's accumulators).
+template <int KB>
+static cudaError_t launch_clause_seg(const StepArgs& a, const uint32_t* Acur, const StepScalars* sc, cudaStream_t st) {
+    const int NW = a.N >> 5, nwb = (NW + 31) / 32;
+    bool first = true;
+    for (int part = 0; part < 2; ++part) {
+        const int lmin = part ? 4 : 1, lmax = part ? (KB == 4 ? 3 : 7) : 3;
+        if (lmin > lmax) continue;
+        SegArgs sa{};
+        long long ch = 0, ncl = 0;
+        for (int L = 0; L < 8; ++L) { sa.off[L] = a.seg_off[L]; sa.C[L] = a.seg_C[L]; }
+        for (int L = 0; L <= 8; ++L) {
+            sa.ch0[L] = ch;
+            if (L >= lmin && L <= lmax) { ch += (a.seg_C[L] + seg_chunk(L) - 1) / seg_chunk(L); ncl += a.seg_C[L]; }
+        }
+        if (ch == 0) continue;
+        const int per_sm = part ? 2 : 4;
+        long long gy = ((long long)a.num_sms * per_sm + nwb - 1) / nwb;
+        const long long need = (ch + kWarps - 1) / kWarps;
+        if (gy > need) gy = need;
+        // 21-bit CTA accumulator fields: < 2^20 clauses per CTA and word block (2x margin)
+        const long long gy_min = (ncl + (1LL << 20) - 1) >> 20;
+        if (gy < gy_min) gy = gy_min;
+        if (gy < 1) gy = 1;
+        const dim3 grid(nwb, (unsigned)gy);
+        const int rs = first ? 1 : 0;
+        cudaError_t e;
+        if (part == 0)
+            e = launch_maybe_pdl(a.pdl, k_clause_seg<KB, 1, 3>, grid, dim3(256), 0, st, Acur, NW, a.V, a.seg_lit, sa, a.hist,
+                                 a.N, a.ds, sc, rs);
+        else if constexpr (KB == 8)
+            e = launch_maybe_pdl(a.pdl, k_clause_seg<KB, 4, 7>, grid, dim3(256), 0, st, Acur, NW, a.V, a.seg_lit, sa,
+                                 a.hist, a.N, a.ds, sc, rs);
+        else
+            e = cudaErrorInvalidValue;
+        if (e != cudaSuccess) return e;
+        first = false;
+    }
+    if (first) k_reset_accumulators<<<1, 1, 0, st>>>(a.ds, sc);    // no clause at all
+    return cudaGetLastError();
+}
+
 cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, const StepScalars* sc, cudaStream_t st) {
     if (a.C == 0) {
         k_reset_accumulators<<<1, 1, 0, st>>>(a.ds, sc);
         return cudaGetLastError();
     }
+    if (a.use_seg) return a.KB == 4 ? launch_clause_seg<4>(a, Acur, sc, st) : launch_clause_seg<8>(a, Acur, sc, st);
     const int NW = a.N >> 5;
     const int nwb = (NW + 31) / 32;
     // sub-groups of NW lanes when a warp would leave lanes idle (N < 1024 per GPU);

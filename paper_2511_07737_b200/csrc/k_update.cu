@@ -21,6 +21,7 @@
 // Rows whose counts can leave int8 ("hubs", SURVEY §7 hard parts) get their
 // counts from k_hub, which splits a hub's occurrences over many CTAs and adds
 // exact int32 counts (integer atomics: order-free, deterministic).
+#include "cluster.cuh"
 #include "peer.cuh"
 
 #include "upd_common.cuh"
@@ -41,6 +42,11 @@ namespace tsat {
 // run-time one costs the default path ~3 % at c2 / c3).
 // CW: counter planes of the K <= 3 gather (8, or 6 when no row has more than
 // 31 same-sign occurrences: 6 fewer registers, compiled for 896 threads).
+// MODE 3: cluster-split rows (W = 1, large N): the CL CTAs of a cluster each
+// own N / CL candidates of every row (their slice of the g table in shared
+// memory) and process the same rows in a static order; the row's J and Q
+// partials are summed over DSMEM (cluster.cuh), so no G round trip through
+// HBM and no g table reads from L2.
 template <int KB, int MODE, bool MAG = false, bool GSG = false, int CW = 8>
 __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (CW == 6 ? TSAT_UPD_THREADS4C6 : TSAT_UPD_THREADS4))
                                           : TSAT_UPD_THREADS8, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
@@ -52,8 +58,12 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
     const int N = a.N, NW = N >> 5, GT = a.upd_GT;
     // work item = (row, chunk of NCH candidates); NCH == N except for batches
     // too large for shared memory (MODE 1 only), whose g table stays in L2
-    const int NCH = MODE == 1 ? a.upd_chunk : N;
+    constexpr bool CLU = MODE == 3;
+    const int NCH = (MODE == 1 || CLU) ? a.upd_chunk : N;
     const int nch = MODE == 1 ? (N + NCH - 1) / NCH : 1;  // compile-time 1: fused modes keep smem addressing
+    const unsigned crank = CLU ? cluster_rank() : 0u;      // MODE 3: this CTA's candidate slice
+    const int n0cl = CLU ? (int)crank * NCH : 0;
+    const int NWg = NCH >> 5;                              // words of the group's sign-plane slots
     // g table read through L1/L2: chunked items (MODE 1, run-time flag), or the
     // fused kernel for large N (GSG: a separate instantiation, so the default
     // path keeps its shared-memory loads)
@@ -63,8 +73,9 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
     const int grp = threadIdx.x / GT, tg = threadIdx.x - grp * GT;
     const int rec_cap = a.upd_rec_cap;
     constexpr int nbufs = upd_recbufs(KB);
-    const size_t grb = upd_group_bytes(KB, NCH, rec_cap, nbufs, MODE == 2 ? 2 : 1);
-    unsigned char* gb = smem + (gs_global ? 0 : upd_gs_bytes(KB, N)) + (size_t)grp * grb;
+    constexpr bool DEFER = MODE == 2 || CLU;                 // the row's Q arrives late: finish it one row later
+    const size_t grb = upd_group_bytes(KB, NCH, rec_cap, nbufs, DEFER ? 2 : 1, CLU);
+    unsigned char* gb = smem + (gs_global ? 0 : upd_gs_bytes(KB, CLU ? NCH : N)) + (size_t)grp * grb;
     const int nitems = a.V * nch;
     uint32_t* dpk = reinterpret_cast<uint32_t*>(gb);
     uint32_t* rec = reinterpret_cast<uint32_t*>(gb + align16((size_t)(KB == 4 ? 1 : 2) * dpkw * 4));
@@ -74,6 +85,9 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
     float* redf = reinterpret_cast<float*>(red + 8);                                    // 4 slots
     int* rowslot = reinterpret_cast<int*>(redf + 4);                                    // 2 slots
     long long* pxs = red + 11;                                                          // 2 slots (MODE 2)
+    unsigned long long* xsl = reinterpret_cast<unsigned long long*>(gb + grb - 128 - kClusterSlotBytes);   // MODE 3
+    unsigned long long* xsJ = xsl;                           // [kMaxCluster][2] J partials
+    unsigned long long* xsQ = xsl + 2 * kMaxCluster;         // [kMaxCluster][2] Q partials
     const int bar = 1 + grp;
     const int lane = threadIdx.x & 31, gw = tg >> 5, ngw = GT >> 5;
     const bool uni3 = a.uniform_len && a.mc.K == 3 && KB == 4;
@@ -81,11 +95,18 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
 
     pdl_wait();                                          // k_gtable's table and scalars
     pdl_trigger();
-    // fp32 derivative table of the whole batch -> shared memory
-    if (!gs_global)
+    // fp32 derivative table of the whole batch (MODE 3: of this CTA's slice) -> shared memory
+    if (CLU) {
+        for (int i = threadIdx.x * 4; i < KB * NCH; i += blockDim.x * 4) {
+            const int r = i / NCH, c = i - r * NCH;
+            *reinterpret_cast<float4*>(gs + i) = *reinterpret_cast<const float4*>(a.gtab + (size_t)r * N + n0cl + c);
+        }
+        for (int i = tg; i < 4 * kMaxCluster; i += GT) xsl[i] = 0ull;   // no message seq is 0
+    } else if (!gs_global) {
         for (int i = threadIdx.x * 4; i < KB * N; i += blockDim.x * 4)
             *reinterpret_cast<float4*>(gs + i) = *reinterpret_cast<const float4*>(a.gtab + i);
-    if (tg == 0) rowslot[1] = atomicAdd(&a.ds->row_counter, 1);
+    }
+    if (!CLU && tg == 0) rowslot[1] = atomicAdd(&a.ds->row_counter, 1);
     const long long t = sc->t;
     __shared__ unsigned long long pscal[3];         // MODE 2: global best key, gmax bits, thmax bits
     if (MODE == 2 && threadIdx.x == 0) {
@@ -110,6 +131,12 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
         }
     }
     __syncthreads();
+    // MODE 3: static row schedule (the cluster's CTAs must pair their groups
+    // on the same rows); every CTA's slots are zeroed before any DSMEM write
+    const int cl_slot = CLU ? (int)cluster_id_x() * a.upd_NG + grp : 0;
+    const int cl_stride = CLU ? (int)cluster_count_x() * a.upd_NG : 0;
+    const unsigned CLn = CLU ? (unsigned)a.upd_cl : 1u;
+    if (CLU) cluster_sync_all();
 
     const double gmax = __longlong_as_double((long long)(MODE == 2 ? pscal[1] : a.ds->gmax_bits));
     const float thmax = __uint_as_float(MODE == 2 ? (unsigned)pscal[2] : a.ds->thmax_bits[t & 1]);
@@ -122,24 +149,27 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
     // and the first model's bits.
     auto finish_row = [&](int vr, long long Qg, const uint32_t* pw, float m2) {
         const bool dpos = !mc.normalize || Qg >= 0;
-        const uint32_t* src = dpos ? pw : pw + NW;
-        for (int w = tg; w < NW; w += GT) {
+        const uint32_t* src = dpos ? pw : pw + NWg;
+        uint32_t* dst = Anext + (size_t)vr * NW + (n0cl >> 5);   // MODE 3: this CTA's words of the row
+        for (int w = tg; w < NWg; w += GT) {
 #if TSAT_ANEXT_CS
-            __stcs(Anext + (size_t)vr * NW + w, src[w]);    // streaming: keep L2 for the current planes
+            __stcs(dst + w, src[w]);                            // streaming: keep L2 for the current planes
 #else
-            Anext[(size_t)vr * NW + w] = src[w];
+            dst[w] = src[w];
 #endif
         }
         if (tg == 0) {
-            double dn, rhon;
-            unsigned char gn;
-            row_finish(Qg, mc, &dn, &rhon, &gn);
-            a.rowQ[vr] = Qg; a.rowD[vr] = dn; a.rowRho[vr] = rhon; a.rowGuard[vr] = gn;
+            if (crank == 0) {
+                double dn, rhon;
+                unsigned char gn;
+                row_finish(Qg, mc, &dn, &rhon, &gn);
+                a.rowQ[vr] = Qg; a.rowD[vr] = dn; a.rowRho[vr] = rhon; a.rowGuard[vr] = gn;
+            }
             atomicMax(&a.ds->thmax_bits[(t + 1) & 1], __float_as_uint(m2));
             const unsigned long long bk = MODE == 2 ? pscal[0] : a.ds->best_key;
             if ((bk >> 32) == 0ull && (a.ds->sol_step < 0 || a.ds->sol_step == t)) {          // first model: keep its bits (A22)
                 const long long idx = (long long)(bk & 0xffffffffull) - mc.n0;
-                if (idx >= 0 && idx < N)
+                if (idx >= n0cl && idx < n0cl + NCH)
                     a.sol[vr] = (unsigned char)((Acur[(size_t)vr * NW + (idx >> 5)] >> (idx & 31)) & 1u);
             }
         }
@@ -151,7 +181,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
     long long* pend_q = red + 13;
     float* pend_m2 = reinterpret_cast<float*>(red + 14);
 
-    int item = rowslot[1];
+    int item = CLU ? cl_slot : rowslot[1];
     if (item < nitems && a.hub_of[item / nch] < 0) {      // first row: stage its records now
         const int v0 = item / nch;
         const unsigned rb0 = a.upd_ptr[v0], re0 = a.upd_ptr[v0 + 1];
@@ -161,22 +191,22 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
     int it = 0;
     for (; item < nitems; ++it) {
         const int v = item / nch;
-        const int n0c = (item - v * nch) * NCH;            // first candidate of this chunk
+        const int n0c = CLU ? n0cl : (item - v * nch) * NCH;    // first candidate of this chunk
         const int ncand = min(NCH, N - n0c), w0 = n0c >> 5, NWc = ncand >> 5;
         uint32_t* rb_cur = rec + (size_t)(nbufs == 2 ? (it & 1) : 0) * recw;     // this row's records
         uint32_t* rb_nxt = rec + (size_t)(nbufs == 2 ? ((it + 1) & 1) : 0) * recw;
         // ---- fetch the next row; prefetch this row's streams into L2
         if (tg == 0) {
-            rowslot[it & 1] = atomicAdd(&a.ds->row_counter, 1);
+            if (!CLU) rowslot[it & 1] = atomicAdd(&a.ds->row_counter, 1);
             const uint32_t rowbytes = (uint32_t)ncand * 4u;
             prefetch_l2(a.theta + (size_t)v * N + n0c, rowbytes);
             if (MODE != 1) {
-                prefetch_l2(a.m + (size_t)v * N, rowbytes);
-                prefetch_l2(a.v + (size_t)v * N, rowbytes);
+                prefetch_l2(a.m + (size_t)v * N + n0c, rowbytes);
+                prefetch_l2(a.v + (size_t)v * N + n0c, rowbytes);
             }
         }
-        uint32_t* posw = posw0 + (MODE == 2 ? (size_t)(it & 1) * 2 * NW : 0);
-        uint32_t* negw = posw + NW;
+        uint32_t* posw = posw0 + (DEFER ? (size_t)(it & 1) * 2 * NWg : 0);
+        uint32_t* negw = posw + NWg;
         const int hub = a.hub_of[v];
         const int2 pn = a.occ_pn[v];
         const int dsum = pn.y - pn.x;                       // sum_r (cneg - cpos)[r]
@@ -232,8 +262,10 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
         }
         if (MODE == 2 && pend_v >= 0 && tg == 0)             // previous row's Q, sent a row ago
             pxs[1] = peer_row_recv(a.px, 1, pend_v, sc->xgen, a.ds, *pend_q);
+        if (CLU && pend_v >= 0 && tg == 0)                   // previous row's Q over the cluster (seq = it)
+            pxs[1] = cl_recv_sum(xsQ, CLn, crank, (unsigned)it, *pend_q, a.ds);
         gsync(bar, GT);
-        const int item_next = rowslot[it & 1];              // fetched by tg 0 before the gather
+        const int item_next = CLU ? item + cl_stride : rowslot[it & 1];   // fetched by tg 0 before the gather
         const int vnext = item_next < nitems ? item_next / nch : a.V;
         // stage the next row's records asynchronously (cp.async global -> smem);
         // they land while this row streams and are waited for before the Q
@@ -246,8 +278,8 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
             cp_async_commit();
         };
         if (nbufs == 1) stage_next();
-        if (MODE == 2 && pend_v >= 0) {
-            finish_row(pend_v, pxs[1], posw0 + (size_t)((it + 1) & 1) * 2 * NW, *pend_m2);
+        if (DEFER && pend_v >= 0) {
+            finish_row(pend_v, pxs[1], posw0 + (size_t)((it + 1) & 1) * 2 * NWg, *pend_m2);
             pend_v = -1;
         }
 
@@ -255,11 +287,13 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
         float* gout = MODE == 1 ? a.Gbuf + (size_t)v * N + n0c : nullptr;
         int* hubc = hubrow ? hubrow + n0c : nullptr;
         long long I;
+        const float* gsc = CLU ? gs : gs + n0c;             // MODE 3: the slice table, row stride NCH
+        const int Ngs = CLU ? NCH : N;
         if (KB > 8 || hub >= 0)
-            I = pass_fold<KB, true>(trow + n0c, dpk, dpkw, gs + n0c, hubc, ncand, N, GT, tg, dsum, jvalid, p2, gout);
+            I = pass_fold<KB, true>(trow + n0c, dpk, dpkw, gsc, hubc, ncand, N, GT, tg, dsum, jvalid, p2, gout, Ngs);
         else
-            I = pass_fold<KB <= 8 ? KB : 8, false>(trow + n0c, dpk, dpkw, gs + n0c, hubc, ncand, N, GT, tg, dsum, jvalid,
-                                                   p2, gout);
+            I = pass_fold<KB <= 8 ? KB : 8, false>(trow + n0c, dpk, dpkw, gsc, hubc, ncand, N, GT, tg, dsum, jvalid,
+                                                   p2, gout, Ngs);
         I = warp_sum(I);
         if (lane == 0) red[gw] = I;
         gsync(bar, GT);
@@ -269,6 +303,12 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
             // every thread adds the W - 1 remote partials itself: no broadcast barrier
             if (tg == 0) peer_row_send(a.px, 0, v, Itot, sc->xgen);
             Itot = peer_row_recv(a.px, 0, v, sc->xgen, a.ds, Itot);
+        }
+        if (CLU) {                                           // J_v over the cluster's slices (DSMEM)
+            if (tg == 0) cl_send(xsJ, CLn, crank, (unsigned)it + 1u, Itot);
+            long long Jr = 0;                                // lane 0 of each warp polls, then broadcasts
+            if (lane == 0) Jr = cl_recv_sum(xsJ, CLn, crank, (unsigned)it + 1u, Itot, a.ds);
+            Itot = __shfl_sync(0xffffffffu, Jr, 0);
         }
         if (nbufs == 2) stage_next();
         if (MODE == 1) {                                     // sharded / chunked: J partial out, next item
@@ -296,22 +336,27 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
         float mx = 0.0f;
         const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
         float4 thn = z4, mn4 = z4, vn4 = z4;
-        if (4 * tg < N) {
-            thn = ld_last(trow + 4 * tg);
-            mn4 = ld_last(mrow + 4 * tg);
-            vn4 = ld_last(vrow + 4 * tg);
+        // this CTA's candidates of the row (MODE 3: its slice; otherwise the row)
+        const int NL = CLU ? NCH : N;
+        float* const tr = trow + (CLU ? n0cl : 0);
+        float* const mr = mrow + (CLU ? n0cl : 0);
+        float* const vr3 = vrow + (CLU ? n0cl : 0);
+        if (4 * tg < NL) {
+            thn = ld_last(tr + 4 * tg);
+            mn4 = ld_last(mr + 4 * tg);
+            vn4 = ld_last(vr3 + 4 * tg);
         }
 #pragma unroll kUnroll3b
-        for (int base = 0; base < N; base += 4 * GT) {
+        for (int base = 0; base < NL; base += 4 * GT) {
             const int n = base + 4 * tg;
             unsigned pnib = 0, nnib = 0;
             const float4 th4 = thn, m4 = mn4, v4 = vn4;       // software pipeline: next loads in flight
-            if (n + 4 * GT < N) {
-                thn = ld_last(trow + n + 4 * GT);
-                mn4 = ld_last(mrow + n + 4 * GT);
-                vn4 = ld_last(vrow + n + 4 * GT);
+            if (n + 4 * GT < NL) {
+                thn = ld_last(tr + n + 4 * GT);
+                mn4 = ld_last(mr + n + 4 * GT);
+                vn4 = ld_last(vr3 + n + 4 * GT);
             }
-            if (n < N) {
+            if (n < NL) {
                 float th[4] = {th4.x, th4.y, th4.z, th4.w};
                 float mm[4] = {m4.x, m4.y, m4.z, m4.w};
                 float vv[4] = {v4.x, v4.y, v4.z, v4.w};
@@ -336,8 +381,8 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
                     x2 = __fadd2_rn(x2, make_float2(num2.x / den2.x, num2.y / den2.y));
                     float xs0 = x2.x, xs1 = x2.y;
                     if (mc.noise) {
-                        xs0 = xs0 + nz * noise_xi(mc.seed, mc.n0 + n + 2 * h, v, t);
-                        xs1 = xs1 + nz * noise_xi(mc.seed, mc.n0 + n + 2 * h + 1, v, t);
+                        xs0 = xs0 + nz * noise_xi(mc.seed, mc.n0 + n0cl + n + 2 * h, v, t);
+                        xs1 = xs1 + nz * noise_xi(mc.seed, mc.n0 + n0cl + n + 2 * h + 1, v, t);
                     }
                     const float xs[2] = {xs0, xs1};
                     const float2 q2 = __fmul2_rn(mag ? make_float2(fabsf(xs0), fabsf(xs1)) : make_float2(xs0, xs1),
@@ -355,9 +400,9 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
                         nnib |= (x < 0.0f ? 1u : 0u) << q;
                     }
                 }
-                st_stream(trow + n, make_float4(th[0], th[1], th[2], th[3]));
-                st_stream(mrow + n, make_float4(mm[0], mm[1], mm[2], mm[3]));
-                st_stream(vrow + n, make_float4(vv[0], vv[1], vv[2], vv[3]));
+                st_stream(tr + n, make_float4(th[0], th[1], th[2], th[3]));
+                st_stream(mr + n, make_float4(mm[0], mm[1], mm[2], mm[3]));
+                st_stream(vr3 + n, make_float4(vv[0], vv[1], vv[2], vv[3]));
             }
             // 8 lanes x 4 candidates = one 32-candidate word
             unsigned pw = pnib << (4 * (lane & 7)), nw = nnib << (4 * (lane & 7));
@@ -366,7 +411,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
                 pw |= __shfl_xor_sync(0xffffffffu, pw, o);
                 nw |= __shfl_xor_sync(0xffffffffu, nw, o);
             }
-            if ((lane & 7) == 0 && n < N) { posw[n >> 5] = pw; negw[n >> 5] = nw; }
+            if ((lane & 7) == 0 && n < NL) { posw[n >> 5] = pw; negw[n >> 5] = nw; }
         }
         Qn = warp_sum(Qn);
         mx = warp_maxf(mx);
@@ -378,7 +423,14 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
         float m2 = 0.0f;
         if (tg == 0)
             for (int i = 0; i < ngw; ++i) m2 = fmaxf(m2, redf[i]);
-        if (MODE == 2 && a.px.exchange_rows) {
+        if (CLU) {                                           // Q_{t+1,v} over the cluster: finished after the next gather
+            if (tg == 0) {
+                cl_send(xsQ, CLn, crank, (unsigned)it + 1u, Qtot);
+                *pend_m2 = m2;
+                *pend_q = Qtot;
+            }
+            pend_v = v;
+        } else if (MODE == 2 && a.px.exchange_rows) {
             // Q_{t+1,v} over all ranks: send now, finish the row after the
             // next row's gather (the peers' partials have arrived by then)
             if (tg == 0) peer_row_send(a.px, 1, v, Qtot, sc->xgen);
@@ -390,11 +442,14 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
         item = item_next;
         // (the next row's barriers order these smem reads before any reuse)
     }
-    if (MODE == 2 && pend_v >= 0) {
-        if (tg == 0) pxs[1] = peer_row_recv(a.px, 1, pend_v, sc->xgen, a.ds, *pend_q);
+    if (DEFER && pend_v >= 0) {
+        if (tg == 0)
+            pxs[1] = CLU ? cl_recv_sum(xsQ, CLn, crank, (unsigned)it, *pend_q, a.ds)
+                         : peer_row_recv(a.px, 1, pend_v, sc->xgen, a.ds, *pend_q);
         gsync(bar, GT);
-        finish_row(pend_v, pxs[1], posw0 + (size_t)((it + 1) & 1) * 2 * NW, *pend_m2);
+        finish_row(pend_v, pxs[1], posw0 + (size_t)((it + 1) & 1) * 2 * NWg, *pend_m2);
     }
+    if (CLU) cluster_sync_all();                             // no DSMEM write may target an exited CTA
 }
 
 // ------------------------------------------------------------------ hub pre-pass
@@ -481,31 +536,118 @@ bool update_fits_fused(int KB, int N, int rec_cap, int optin) {
     return ng >= 2 || (ng == 1 && GT == 128);
 }
 
+#ifndef TSAT_GS_GLOBAL_BELOW
+#define TSAT_GS_GLOBAL_BELOW 4       // fused kernel: g table from L2 when smem would hold fewer groups
+#endif
+// Cluster-split rows (MODE 3, W = 1): the smallest cluster size CL = 2, 4, 8,
+// 16 whose slice N / CL (a multiple of 128 candidates) keeps the slice's g
+// table in shared memory beside >= TSAT_GS_GLOBAL_BELOW warp groups; 0 when
+// the fused kernel already holds the whole table with that many groups, or
+// no cluster size fits.
+#ifndef TSAT_CLUSTER_DEFAULT
+#define TSAT_CLUSTER_DEFAULT 0       // measured slower than the L2 g table / split sequence: opt-in
+#endif
+int update_cluster_size(int KB, int N, int rec_cap, int optin) {
+    if (std::getenv("TSAT_NO_CLUSTER")) return 0;
+    if (!TSAT_CLUSTER_DEFAULT && !std::getenv("TSAT_CLUSTER")) return 0;
+    auto groups = [&](int n, bool xs) -> long long {
+        const size_t gsb = upd_gs_bytes(KB, n), grb = upd_group_bytes(KB, n, rec_cap, upd_recbufs(KB), xs ? 2 : 1, xs);
+        return optin > (long long)gsb ? ((long long)optin - (long long)gsb) / (long long)grb : 0;
+    };
+    if (groups(N, false) >= TSAT_GS_GLOBAL_BELOW) return 0;
+    for (int cl = 2; cl <= kMaxCluster; cl *= 2) {
+        if (N % (cl * 128)) return 0;
+        if (groups(N / cl, true) >= TSAT_GS_GLOBAL_BELOW) return cl;
+    }
+    return 0;
+}
+
 int update_chunk(int KB, int N) {
     const int c = KB == 4 ? 4096 : (KB == 8 ? 2048 : 1024);
     return N < c ? N : c;
 }
 
 template <int KB>
-static cudaError_t set_update_attrs(int smem) {
+static cudaError_t set_update_attrs(int need, int optin) {
     const cudaFuncAttribute attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
     cudaError_t e;
-    if ((e = set_max_dyn_smem(k_update<KB, 0>, smem)) != cudaSuccess) return e;
-    if ((e = set_max_dyn_smem(k_update<KB, 1>, smem)) != cudaSuccess) return e;
-    if ((e = set_max_dyn_smem(k_update<KB, 2>, smem)) != cudaSuccess) return e;
-    if ((e = set_max_dyn_smem(k_update<KB, 0, true>, smem)) != cudaSuccess) return e;
-    if ((e = set_max_dyn_smem(k_update<KB, 0, false, true>, smem)) != cudaSuccess) return e;
-    if ((e = set_max_dyn_smem(k_update<KB, 2, false, true>, smem)) != cudaSuccess) return e;
-    if ((e = set_max_dyn_smem(k_update<KB, 0, true, true>, smem)) != cudaSuccess) return e;
-    if ((e = set_max_dyn_smem(k_update<KB, 2, true, true>, smem)) != cudaSuccess) return e;
-    if ((e = set_max_dyn_smem(k_update<KB, 0, false, false, 6>, smem)) != cudaSuccess) return e;
-    if ((e = set_max_dyn_smem(k_update<KB, 0, true, false, 6>, smem)) != cudaSuccess) return e;
-    return set_max_dyn_smem(k_update<KB, 2, true>, smem);
+    if ((e = set_max_dyn_smem(k_update<KB, 0>, need, optin)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 1>, need, optin)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 2>, need, optin)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 0, true>, need, optin)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 0, false, true>, need, optin)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 2, false, true>, need, optin)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 0, true, true>, need, optin)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 2, true, true>, need, optin)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 0, false, false, 6>, need, optin)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 0, true, false, 6>, need, optin)) != cudaSuccess) return e;
+    return set_max_dyn_smem(k_update<KB, 2, true>, need, optin);
 }
 
-#ifndef TSAT_GS_GLOBAL_BELOW
-#define TSAT_GS_GLOBAL_BELOW 4       // fused kernel: g table from L2 when smem would hold fewer groups
-#endif
+template <int KB>
+static cudaError_t cluster_attrs(int need, int optin, int CL, int threads, int* max_clusters) {
+    cudaError_t e;
+    auto k0 = k_update<KB, 3, false>;
+    auto k1 = k_update<KB, 3, true>;
+    if ((e = set_max_dyn_smem(k0, need, optin)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k1, need, optin)) != cudaSuccess) return e;
+    if (CL > 8) {
+        if ((e = cudaFuncSetAttribute(k0, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return e;
+        if ((e = cudaFuncSetAttribute(k1, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = need;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaOccupancyMaxActiveClusters(max_clusters, k0, &cfg);
+}
+
+// MODE 3 geometry: slice NCH = N / CL per CTA, its g table in shared memory,
+// warp groups of the slice, and exactly as many clusters as can be resident
+// at once (the static row schedule needs every CTA running).
+static cudaError_t configure_update_cluster(StepArgs* a, int optin, int sms) {
+    const int KB = a->KB, CL = a->upd_cl, NCH = a->N / CL, NWc = NCH >> 5;
+    const int GT = NWc >= 128 ? 128 : (NWc > 32 ? 64 : 32);
+    const int nbufs = upd_recbufs(KB);
+    const size_t gsb = upd_gs_bytes(KB, NCH), grb = upd_group_bytes(KB, NCH, a->upd_rec_cap, nbufs, 2, true);
+    const int max_threads = KB == 4 ? TSAT_UPD_THREADS4 : TSAT_UPD_THREADS8;
+    long long ng = optin > (long long)gsb ? ((long long)optin - (long long)gsb) / (long long)grb : 0;
+    ng = ng < max_threads / GT ? ng : max_threads / GT;
+    if (GT > 32) ng = ng < 15 ? ng : 15;
+    if (const char* mg = std::getenv("TSAT_UPD_MAXGROUPS")) {
+        const long long x = std::atoll(mg);
+        if (x > 0 && x < ng) ng = x;
+    }
+    if (ng < 1) return cudaErrorInvalidConfiguration;
+    a->upd_mode = 0;                  // (0: k_hub still counts the hub rows)
+    a->upd_chunk = NCH;
+    a->upd_gs_global = 0;
+    a->upd_recbufs = nbufs;
+    a->upd_GT = GT;
+    a->upd_NG = (int)ng;
+    a->upd_smem = gsb + (size_t)ng * grb;
+    int mc = 0;
+    cudaError_t e;
+    const int need = (int)a->upd_smem, threads = GT * (int)ng;
+    if (KB == 4) e = cluster_attrs<4>(need, optin, CL, threads, &mc);
+    else if (KB == 8) e = cluster_attrs<8>(need, optin, CL, threads, &mc);
+    else e = cluster_attrs<16>(need, optin, CL, threads, &mc);
+    if (e != cudaSuccess) return e;
+    if (mc < 1) return cudaErrorInvalidConfiguration;
+    a->upd_grid = mc * CL;
+    if (std::getenv("TSAT_GEOM_VERBOSE"))
+        std::fprintf(stderr, "k_update cluster geometry: KB %d N %d CL %d slice %d GT %d groups %lld clusters %d smem %zu\n",
+                     KB, a->N, CL, NCH, GT, ng, mc, a->upd_smem);
+    return cudaSuccess;
+}
+
 cudaError_t configure_update(StepArgs* a) {
     const int N = a->N, KB = a->KB;
     int dev = 0, optin = 0, sms = 0;
@@ -514,6 +656,7 @@ cudaError_t configure_update(StepArgs* a) {
     if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
     a->num_sms = sms;
+    if (a->upd_cl > 1) return configure_update_cluster(a, optin, sms);
     const bool fused = update_fits_fused(KB, N, a->upd_rec_cap, optin);
     a->upd_chunk = fused ? N : update_chunk(KB, N);
     a->upd_gs_global = fused ? 0 : 1;
@@ -563,13 +706,12 @@ cudaError_t configure_update(StepArgs* a) {
         const int x = std::atoi(g);
         if (x > 0 && x < sms) a->upd_grid = x;
     }
-    // the attribute is a process-wide per-function limit: set it to the opt-in
-    // maximum so contexts configured later with smaller geometries cannot
-    // lower it below what an earlier context launches with
-    const int smem = optin;
-    if (KB == 4) return set_update_attrs<4>(smem);
-    if (KB == 8) return set_update_attrs<8>(smem);
-    return set_update_attrs<16>(smem);
+    // the attribute is a process-wide per-function limit, raised to this
+    // launch's need and never lowered (set_max_dyn_smem)
+    const int smem = (int)a->upd_smem;
+    if (KB == 4) return set_update_attrs<4>(smem, optin);
+    if (KB == 8) return set_update_attrs<8>(smem, optin);
+    return set_update_attrs<16>(smem, optin);
 }
 
 cudaError_t launch_hub(const StepArgs& a, const uint32_t* Acur, cudaStream_t st) {
@@ -595,6 +737,22 @@ static cudaError_t launch_update_kbg(const StepArgs& a, const uint32_t* Acur, ui
     const bool mag = a.mc.normalize == 3;
     const dim3 g(a.upd_grid), b(a.upd_GT * a.upd_NG);
     const size_t sm = a.upd_smem;
+    if (a.upd_cl > 1) {                          // MODE 3: cluster-split rows
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = g;
+        cfg.blockDim = b;
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = a.upd_cl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return a.mc.normalize == 3 ? cudaLaunchKernelEx(&cfg, k_update<KB, 3, true>, a, Acur, Anext, sc)
+                                   : cudaLaunchKernelEx(&cfg, k_update<KB, 3, false>, a, Acur, Anext, sc);
+    }
     if (a.peer) {
         if (mag) k_update<KB, 2, true, GSG><<<g, b, sm, st>>>(a, Acur, Anext, sc);
         else k_update<KB, 2, false, GSG><<<g, b, sm, st>>>(a, Acur, Anext, sc);

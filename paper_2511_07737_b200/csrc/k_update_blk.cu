@@ -334,12 +334,11 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
                     for (int b = 0; b < KB - 1; ++b)
                         *reinterpret_cast<int4*>(hubrow + (size_t)b * N + n) = make_int4(0, 0, 0, 0);
                 } else if constexpr (KB <= 8) {
-                    const float dsumf = (float)dsum;
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         float dA[KB], dB[KB];
-                        fold_counts<KB>(dA, dp[2 * h], KB == 8 ? dp[dplane + 2 * h] : 0u, dsumf);
-                        fold_counts<KB>(dB, dp[2 * h + 1], KB == 8 ? dp[dplane + 2 * h + 1] : 0u, dsumf);
+                        fold_counts<KB>(dA, dp[2 * h], KB == 8 ? dp[dplane + 2 * h] : 0u, dsum);
+                        fold_counts<KB>(dB, dp[2 * h + 1], KB == 8 ? dp[dplane + 2 * h + 1] : 0u, dsum);
                         float2 G2 = make_float2(0.0f, 0.0f);
 #pragma unroll
                         for (int b = 0; b < KB; ++b)
@@ -492,13 +491,13 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
 }
 
 template <int KB>
-static cudaError_t set_blk_attrs(int smem) {
+static cudaError_t set_blk_attrs(int need, int optin) {
     const cudaFuncAttribute attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
     cudaError_t e;
-    if ((e = set_max_dyn_smem(k_update_blk<KB, 0, false>, smem)) != cudaSuccess) return e;
-    if ((e = set_max_dyn_smem(k_update_blk<KB, 2, false>, smem)) != cudaSuccess) return e;
-    if ((e = set_max_dyn_smem(k_update_blk<KB, 0, true>, smem)) != cudaSuccess) return e;
-    return set_max_dyn_smem(k_update_blk<KB, 2, true>, smem);
+    if ((e = set_max_dyn_smem(k_update_blk<KB, 0, false>, need, optin)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update_blk<KB, 2, false>, need, optin)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update_blk<KB, 0, true>, need, optin)) != cudaSuccess) return e;
+    return set_max_dyn_smem(k_update_blk<KB, 2, true>, need, optin);
 }
 
 cudaError_t configure_update_blk(StepArgs* a) {
@@ -530,13 +529,12 @@ cudaError_t configure_update_blk(StepArgs* a) {
         const int x = std::atoi(g);
         if (x > 0 && x < sms) a->upd_grid = x;
     }
-    // the attribute is a process-wide per-function limit: set it to the opt-in
-    // maximum so contexts configured later with smaller geometries cannot
-    // lower it below what an earlier context launches with
-    const int smem = optin;
-    if (KB == 4) return set_blk_attrs<4>(smem);
-    if (KB == 8) return set_blk_attrs<8>(smem);
-    return set_blk_attrs<16>(smem);
+    // the attribute is a process-wide per-function limit, raised to this
+    // launch's need and never lowered (set_max_dyn_smem)
+    const int smem = (int)a->upd_smem;
+    if (KB == 4) return set_blk_attrs<4>(smem, optin);
+    if (KB == 8) return set_blk_attrs<8>(smem, optin);
+    return set_blk_attrs<16>(smem, optin);
 }
 
 template <int KB>

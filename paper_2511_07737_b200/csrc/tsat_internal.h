@@ -85,6 +85,10 @@ struct HostCnf {
     int32_t batched = 0;
     std::vector<uint32_t> bat_ptr;      // V+1
     std::vector<uint32_t> bat_rec;
+    // length segments (build_segments, K <= 7): clauses of length L at
+    // seg_lit[seg_off[L] .. + seg_C[L] * L), L = 1..7 (empty clauses in L = 1)
+    std::vector<int64_t> seg_C, seg_off;
+    std::vector<uint32_t> seg_lit;
 };
 
 // Parse DIMACS.  Returns 0 on success, 2 (TSAT_E_PARSE) with msg.
@@ -189,7 +193,13 @@ struct StepArgs {
     int upd_RB;                      // rows per work item: 1, or 32 / (N/32) for small shards (k_update_blk)
     int upd_blk_cap;                 // record words a group stages per row block (max over blocks, non-hub rows)
     int upd_cw6;                     // K <= 3 fused W = 1: 6-plane counters (no row above 31 same-sign occurrences)
+    int upd_cl;                      // > 1: cluster-split rows (k_update MODE 3), CTAs per cluster
     const int* blk_rows;             // [V] rows in block order (grouped by gather length; k_update_blk)
+    // clause length segments (k_clause_seg; HostCnf::seg_*): use_seg = 1 when
+    // the instance is not uniform 3-SAT, K <= 7 and N >= 1024 per GPU
+    int use_seg;
+    const uint32_t* seg_lit;
+    long long seg_C[8], seg_off[8];
     // dense tensor-core clause evaluation (k_dense.cu; config.clause_eval = 1)
     int dense;
     const uint8_t* dP;               // [dCp][dKp] uint8 0/1 problem matrix (K-major)
@@ -279,6 +289,8 @@ int dense_tile_m();
 int dense_tile_n();
 // whether the fused k_update geometry fits (else: chunked split sequence)
 bool update_fits_fused(int KB, int N, int rec_cap, int optin);
+// MODE 3 cluster size for a W = 1 batch of N candidates (0: not used), k_update.cu
+int update_cluster_size(int KB, int N, int rec_cap, int optin);
 // peer path: exchange of Qbuf[0..V) row partials (init / set_state), gen = exchange generation
 cudaError_t launch_peer_rows_exchange(const StepArgs& a, unsigned gen, cudaStream_t st);
 cudaError_t launch_step_end_sharded(const StepArgs& a, const StepScalars* sc, cudaStream_t st);

@@ -33,6 +33,9 @@ constexpr int kUnroll3b = TSAT_3B_UNROLL;
 #ifndef TSAT_BLK_PIPE
 #define TSAT_BLK_PIPE 0
 #endif
+#ifndef TSAT_FOLD_DP4A
+#define TSAT_FOLD_DP4A 1           // KB = 8: derived bin of the fold by byte dot products (c4 -1.8 %; KB = 4 +3 % at c3, not used)
+#endif
 #ifndef TSAT_HINTS
 #define TSAT_HINTS 1
 #endif
@@ -64,16 +67,21 @@ constexpr int kHubCtrBatched = 10;  // batched super-chunks: kHubSlabBatches * 4
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) / 16 * 16; }
 }  // namespace
 
-// Raise a kernel's dynamic shared-memory limit to the opt-in maximum minus its
-// static shared memory.  The limit is a process-wide per-function attribute,
-// so every context sets it to the same maximum (a context configured later
-// with a smaller geometry must not lower it below another context's launch).
+// Raise a kernel's dynamic shared-memory limit to at least `need` bytes.  The
+// limit is a process-wide per-function attribute: it only ever grows, so a
+// context configured later with a smaller geometry cannot lower it below
+// another context's launch.  (TSAT_ATTR_OPTIN: always the opt-in maximum.)
+#ifndef TSAT_ATTR_OPTIN
+#define TSAT_ATTR_OPTIN 0
+#endif
 template <typename Kern>
-inline cudaError_t set_max_dyn_smem(Kern* k, int optin) {
+inline cudaError_t set_max_dyn_smem(Kern* k, int need, int optin) {
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, k);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+    const int target = TSAT_ATTR_OPTIN ? optin - (int)fa.sharedSizeBytes : need;
+    if (!TSAT_ATTR_OPTIN && fa.maxDynamicSharedSizeBytes >= target) return cudaSuccess;
+    return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, target);
 }
 
 // Shared-memory geometry of k_update (host and device agree through this).
@@ -85,12 +93,16 @@ __host__ __device__ inline size_t upd_dpk_words(int N) { return (size_t)N + (N >
 // the instruction-cache-bound KB = 8 kernel ~7 %).
 __host__ __device__ constexpr int upd_recbufs(int KB) { return KB == 8 ? 1 : 2; }
 // parities: 2 for the peer kernel (MODE 2 finishes a row one row late), else 1
-__host__ __device__ inline size_t upd_group_bytes(int KB, int N, int rec_cap, int nbufs, int parities = 2) {
+// xslots: cluster-split rows (MODE 3) add the group's DSMEM exchange slots
+// [2 kinds][kMaxCluster = 16 ranks][2 words] (cluster.cuh) below the scratch.
+__host__ __device__ inline size_t upd_group_bytes(int KB, int N, int rec_cap, int nbufs, int parities = 2,
+                                                  bool xslots = false) {
     const int NDW = KB == 4 ? 1 : 2;
-    // dpk | nbufs record buffers | sign planes [parities][pos, neg][NW] | 128 B scratch
+    // dpk | nbufs record buffers | sign planes [parities][pos, neg][NW] | (slots) | 128 B scratch
     return align16((size_t)NDW * upd_dpk_words(N) * 4) + nbufs * align16((size_t)rec_cap * 4) +
-           align16((size_t)2 * parities * (N >> 5) * 4) + 128;
+           align16((size_t)2 * parities * (N >> 5) * 4) + (xslots ? 512 : 0) + 128;
 }
+constexpr int kClusterSlotBytes = 512;
 
 // x * 2^s, exact (== scalbn) when 2^s is a normal double.
 __device__ __forceinline__ double times_pow2(double x, int s) {
@@ -114,14 +126,23 @@ __device__ __forceinline__ float2 mul2_unfused(float2 a, float2 b) {
 
 // Per-bin counts of one candidate as exact floats (bytes + derived last bin).
 template <int KB>
-__device__ __forceinline__ void fold_counts(float (&d)[KB], uint32_t p0, uint32_t p1, float dsumf) {
+__device__ __forceinline__ void fold_counts(float (&d)[KB], uint32_t p0, uint32_t p1, int dsum) {
     const uint32_t u0 = p0 ^ 0x80808080u, u1 = p1 ^ 0x80808080u;
 #pragma unroll
     for (int r = 0; r < KB - 1; ++r) d[r] = sbyte_to_float(r < 4 ? u0 : u1, r & 3);
-    float acc = d[0];
+    // derived bin: dsum - sum_r d_r as an integer (byte dot products with -1;
+    // the unused top byte is 0), made an exact float through the mantissa of
+    // 1.5 * 2^23 (|x| < 2^22); +0 for x = 0, as the fp32 subtraction gave
+    if (TSAT_FOLD_DP4A && KB == 8) {
+        int x = __dp4a((int)p0, -1, dsum);
+        x = __dp4a((int)p1, -1, x);
+        d[KB - 1] = __int_as_float(0x4B400000 + x) - 12582912.0f;
+    } else {
+        float acc = d[0];
 #pragma unroll
-    for (int r = 1; r < KB - 1; ++r) acc = acc + d[r];     // exact: small integers (never -0)
-    d[KB - 1] = dsumf - acc;
+        for (int r = 1; r < KB - 1; ++r) acc = acc + d[r];     // exact: small integers (never -0)
+        d[KB - 1] = (float)dsum - acc;
+    }
 }
 
 template <int KB>
@@ -142,9 +163,8 @@ __device__ __forceinline__ float fold_ints(const int* hubrow, int N, int n, int 
 template <int KB, bool HUB>
 __device__ __forceinline__ long long pass_fold(const float* __restrict__ trow, uint32_t* dpk, size_t dpkw,
                                                const float* gs, int* hubrow, int N, int Nst, int GT, int tg, int dsum,
-                                               bool jvalid, float p2, float* __restrict__ gout) {
-    // N candidates from the pointers' origin; Nst = row stride of gs / hubrow
-    const float dsumf = (float)dsum;
+                                               bool jvalid, float p2, float* __restrict__ gout, int Ngs) {
+    // N candidates from the pointers' origin; Nst = row stride of hubrow, Ngs of gs
     long long I = 0;
     float4 th_nx = (4 * tg < N) ? *reinterpret_cast<const float4*>(trow + 4 * tg) : make_float4(0.f, 0.f, 0.f, 0.f);
     for (int n = 4 * tg; n < N; n += 4 * GT) {
@@ -153,7 +173,7 @@ __device__ __forceinline__ long long pass_fold(const float* __restrict__ trow, u
         const float th[4] = {th4.x, th4.y, th4.z, th4.w};
         float4 g4[KB];
 #pragma unroll
-        for (int r = 0; r < KB; ++r) g4[r] = *reinterpret_cast<const float4*>(gs + (size_t)r * Nst + n);
+        for (int r = 0; r < KB; ++r) g4[r] = *reinterpret_cast<const float4*>(gs + (size_t)r * Ngs + n);
         uint32_t* dp = dpk + n + (n >> 5);
         float Gq[4];
         if (HUB) {
@@ -170,8 +190,8 @@ __device__ __forceinline__ long long pass_fold(const float* __restrict__ trow, u
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 float dA[KB], dB[KB];
-                fold_counts<KB>(dA, dp[2 * h], KB == 8 ? dp[dpkw + 2 * h] : 0u, dsumf);
-                fold_counts<KB>(dB, dp[2 * h + 1], KB == 8 ? dp[dpkw + 2 * h + 1] : 0u, dsumf);
+                fold_counts<KB>(dA, dp[2 * h], KB == 8 ? dp[dpkw + 2 * h] : 0u, dsum);
+                fold_counts<KB>(dB, dp[2 * h + 1], KB == 8 ? dp[dpkw + 2 * h + 1] : 0u, dsum);
                 float2 G2 = make_float2(0.0f, 0.0f);
 #pragma unroll
                 for (int r = 0; r < KB; ++r)

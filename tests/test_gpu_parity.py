@@ -178,6 +178,40 @@ def test_degenerate_and_shape_cases(case):
         assert s.get_info().best_unsat >= 1 and s.get_solution() is None
 
 
+@pytest.mark.parametrize("case", ["industrial7", "lengths_1_to_7", "uniform5", "two_three", "many_chunks"])
+def test_length_segment_clause_eval(case):
+    """k_clause_seg (>= 1024 candidates, every K <= 7 instance but uniform
+    3-SAT): clauses regrouped by length, L gathers and L + 1 bins per clause,
+    short (L <= 3) and long (L = 4..7) kernels.  Cases: the industrial mix with
+    hubs; every length 1..7 plus an empty clause, a tautology and a duplicate
+    literal (ragged segments); uniform K = 5 (one long segment); a 2-SAT +
+    3-SAT mix (KB = 4: bin 3 derived, short kernel only); and enough clauses
+    that every warp accumulates several chunks into the CTA fields.  The
+    histograms are checked through unsat / g / S / theta, bit-exact."""
+    if case == "industrial7":
+        cnf, N = industrial_cnf(700, 2800, 22), 1024
+    elif case == "lengths_1_to_7":
+        rng = np.random.default_rng(5)
+        base = []
+        for L in range(1, 8):
+            for _ in range(37 * L + 3):
+                vs = rng.choice(np.arange(1, 241), L, replace=False)
+                base.append([int(v) * (1 if rng.random() < .5 else -1) for v in vs])
+        base += [[], [7, -7, 9], [11, 11, -12]]
+        cnf, N = Cnf.from_clauses(240, base), 1024
+    elif case == "uniform5":
+        cnf, N = planted_ksat(300, 900, 5, 2), 2048
+    elif case == "two_three":
+        base = planted_ksat(400, 900, 3, 3).clauses() + planted_ksat(400, 500, 2, 4).clauses()
+        cnf, N = Cnf.from_clauses(400, base), 1024
+    else:
+        cnf, N = industrial_cnf(3000, 40000, 3), 1024
+    state = random_state(cnf.V, N, seed=19)
+    s, o = make_pair(cnf, N, 3, state=state, t0=0)
+    for _ in range(4):
+        compare_step(s, o, cnf, case)
+
+
 @pytest.mark.parametrize("N", [128, 256, 384, 512])
 @pytest.mark.parametrize("kind", ["planted3", "industrial7"])
 def test_row_block_kernel(kind, N):
@@ -268,10 +302,13 @@ def test_dense_tensor_core_clause_eval(case):
 
 
 @pytest.mark.parametrize("kind", ["kb4_n8192", "kb8_n4096"])
-def test_fused_g_table_in_l2(kind):
+def test_fused_g_table_in_l2(kind, monkeypatch):
     """Large per-GPU batches that still fit the fused kernel (BASELINE c5's
     8192-candidate share per GPU): the g table is read through L1 / L2 instead
-    of shared memory so more warp groups fit.  Bit-exact against the oracle."""
+    of shared memory so more warp groups fit.  Bit-exact against the oracle.
+    (W = 1 runs these as cluster-split rows by default; the peer path, and
+    TSAT_NO_CLUSTER here, keep this geometry.)"""
+    monkeypatch.setenv("TSAT_NO_CLUSTER", "1")
     if kind == "kb4_n8192":
         cnf, N = planted_ksat(90, 380, 3, 3), 8192
     else:
@@ -647,13 +684,57 @@ def test_sharded_equals_fused_c2():
     assert (ia.best_unsat, ia.best_idx) == (ib.best_unsat, ib.best_idx)
 
 
+# ---------------------------------------------------------------- cluster-split rows
+@pytest.mark.parametrize("case", ["kb4_n8192", "kb4_n16384_noise", "kb8_hubs", "kb4_ragged_mag", "kb4_n65536"])
+def test_cluster_split_rows(case, monkeypatch):
+    """Large W = 1 batches (the g table of N candidates would leave fewer than
+    4 warp groups): k_update MODE 3 splits every row's candidates over the CL
+    CTAs of a thread-block cluster, each holding its slice of the g table in
+    shared memory, and sums the row's exact int64 J and Q partials over DSMEM.
+    Cases: CL = 2 (BASELINE c5's 8192 per GPU), CL = 4 with update noise, KB =
+    8 with hub rows (industrial, N = 4096), a slice that is not a power of two
+    (17408 = 4 x 4352) under normalize 3 (R28), and CL = 16 (c5's 65 536 on
+    one GPU, non-portable cluster size).  Bit-exact against the oracle.
+    (Opt-in, TSAT_CLUSTER=1: measured slower than the default geometries.)"""
+    monkeypatch.setenv("TSAT_CLUSTER", "1")
+    cfg = None
+    if case == "kb4_n8192":
+        cnf, N, cl = planted_ksat(90, 380, 3, 3), 8192, 2
+    elif case == "kb4_n16384_noise":
+        cnf, N, cl, cfg = planted_ksat(60, 250, 3, 2), 16384, 4, O.Config(noise_sigma=0.05)
+    elif case == "kb8_hubs":
+        cnf, N, cl = industrial_cnf(300, 1800, 8), 4096, 2
+    elif case == "kb4_ragged_mag":
+        cnf, N, cl, cfg = planted_ksat(70, 290, 3, 5), 17408, 4, O.Config(normalize=3)
+    else:
+        cnf, N, cl = planted_ksat(24, 100, 3, 4), 65536, 16
+    state = random_state(cnf.V, N, seed=31)
+    s, o = make_pair(cnf, N, 8, cfg=cfg, state=state, t0=0)
+    g = s.update_geometry()
+    assert g["cluster"] == cl and g["slice"] == N // cl, g
+    for _ in range(3):
+        compare_step(s, o, cnf, case)
+    if case == "kb8_hubs":
+        assert s.info.n_hub_rows >= 1
+    info = s.step(4)
+    for _ in range(4):
+        ref = o.step()
+    th, m, v, _ = s.get_state()
+    np.testing.assert_array_equal(th, o.theta)
+    np.testing.assert_array_equal(v, o.v)
+    assert (info.best_unsat, info.best_idx) == (ref.best_unsat, ref.best_idx)
+
+
 # ---------------------------------------------------------------- other code paths
 @pytest.mark.parametrize("kind", ["kb4", "kb8", "kb4-ragged"])
-def test_chunked_large_batch_path(kind):
+def test_chunked_large_batch_path(kind, monkeypatch):
     """Batches too large for the fused kernel's shared memory (the g table of
     N candidates) run the split sequence with k_update work items of 4096
     (KB = 8: 2048) candidates, the g table read from L2 and exact int64 J
-    atomics; same canonical results (also with a ragged last chunk)."""
+    atomics; same canonical results (also with a ragged last chunk).  (At W = 1
+    these sizes run cluster-split rows by default; TSAT_NO_CLUSTER keeps the
+    split sequence, which multi-GPU NCCL runs and unsplittable N still use.)"""
+    monkeypatch.setenv("TSAT_NO_CLUSTER", "1")
     if kind == "kb4":
         cnf, N = planted_ksat(60, 250, 3, 2), 16384        # g table 256 KB > smem: 4 chunks
     elif kind == "kb8":
@@ -663,6 +744,7 @@ def test_chunked_large_batch_path(kind):
     s, o = make_pair(cnf, N, 3)
     base = 3 if cnf.V else 0
     assert s.kernels_per_step() >= base + 3               # update B, rows finish, step end
+    assert s.update_geometry()["cluster"] == 0
     s.set_state(o.theta, o.m, o.v, 0)
     for _ in range(4):
         compare_step(s, o, cnf, "chunked-" + kind)
