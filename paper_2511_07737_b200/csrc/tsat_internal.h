@@ -17,7 +17,10 @@ constexpr int kMaxStepsPerCall = 4096;
 constexpr int kTopkMax = 2048;         // export: k most confident variables per candidate
 constexpr int kRecCap = 512;           // occurrence-record words a warp group stages per row (longer rows: hubs)
 constexpr int kHubSlab = 1023;         // occurrences per hub super-chunk (11-bit signed counters)
-constexpr int kHubSlabBatches = 127;   // batched records: batches (<= 4 occurrences) per hub super-chunk (k_hub int10)
+#ifndef TSAT_HUB_SLAB_BATCHES
+#define TSAT_HUB_SLAB_BATCHES 127
+#endif
+constexpr int kHubSlabBatches = TSAT_HUB_SLAB_BATCHES;   // batched records: batches (<= 4 occurrences) per hub super-chunk (k_hub int10)
 constexpr int kMaxPeers = 8;           // peer-exchange path: ranks (GPUs of one NVSwitch node)
 constexpr int kExportCap = 1 << 16;    // export exchange: u64 words per rank and phase (M and M * k)
 
