@@ -191,23 +191,28 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
     // record offset within the block's staging buffer (non-hub rows back to back)
     // (the block's rows are a.blk_rows[item RB ...]: rows grouped by their
     // gather length on the host, so the lanes of a warp finish together)
+    // (called by the whole warp: the offsets are an exclusive warp prefix sum
+    // of the rows' staged lengths, one load chain per lane)
     auto fetch_row = [&](int item, int nr, RowPre& P) {
-        if (lane >= nr) return;
-        const int* rows = a.blk_rows + (size_t)item * RB;
-        const int v = rows[lane];
-        P.v = v;
-        P.pn = a.occ_pn[v];
-        P.hub = a.hub_of[v];
-        P.rho = a.rowRho[v];
-        P.guard = a.rowGuard[v];
-        unsigned off = 0;
-        for (int r = 0; r < lane; ++r) {
-            const int u = rows[r];
-            if (a.hub_of[u] < 0) off += a.upd_ptr[u + 1] - a.upd_ptr[u];
+        unsigned mine = 0;
+        if (lane < nr) {
+            const int v = a.blk_rows[(size_t)item * RB + lane];
+            P.v = v;
+            P.pn = a.occ_pn[v];
+            P.hub = a.hub_of[v];
+            P.rho = a.rowRho[v];
+            P.guard = a.rowGuard[v];
+            P.rbeg = (int)a.upd_ptr[v];
+            P.nrec = (int)(a.upd_ptr[v + 1] - a.upd_ptr[v]);
+            mine = P.hub < 0 ? (unsigned)P.nrec : 0u;
         }
-        P.roff = (int)off;
-        P.rbeg = (int)a.upd_ptr[v];
-        P.nrec = (int)(a.upd_ptr[v + 1] - a.upd_ptr[v]);
+        unsigned incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned x = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += x;
+        }
+        if (lane < nr) P.roff = (int)(incl - mine);
     };
     RowPre pre{};
     bool pending = false;

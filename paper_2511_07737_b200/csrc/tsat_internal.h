@@ -18,7 +18,7 @@ constexpr int kTopkMax = 2048;         // export: k most confident variables per
 constexpr int kRecCap = 512;           // occurrence-record words a warp group stages per row (longer rows: hubs)
 constexpr int kHubSlab = 1023;         // occurrences per hub super-chunk (11-bit signed counters)
 #ifndef TSAT_HUB_SLAB_BATCHES
-#define TSAT_HUB_SLAB_BATCHES 127
+#define TSAT_HUB_SLAB_BATCHES 63      // c4: k_hub 1.53 -> 1.35 ms vs 127 (more, shorter warps; 255: 1.89, 31: 1.39, 15: 1.60)
 #endif
 constexpr int kHubSlabBatches = TSAT_HUB_SLAB_BATCHES;   // batched records: batches (<= 4 occurrences) per hub super-chunk (k_hub int10)
 constexpr int kMaxPeers = 8;           // peer-exchange path: ranks (GPUs of one NVSwitch node)

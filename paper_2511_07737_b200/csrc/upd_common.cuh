@@ -62,7 +62,9 @@ __device__ __forceinline__ void st_stream(float* p, float4 x) {
 namespace {
 constexpr int kCtr = 8;        // counter planes (int8) in the fused kernel
 constexpr int kHubCtrPlain = 11;    // counter planes (int11) in k_hub (kHubSlab = 1023 occurrences)
-constexpr int kHubCtrBatched = kHubSlabBatches * 4 <= 511 ? 10 : 11;  // signed counts of <= kHubSlabBatches * 4 occurrences
+// planes of a signed count of up to x occurrences: the smallest B with 2^(B-1) - 1 >= x
+__host__ __device__ constexpr int signed_planes(int x, int b = 1) { return ((1 << (b - 1)) - 1 >= x) ? b : signed_planes(x, b + 1); }
+constexpr int kHubCtrBatched = signed_planes(kHubSlabBatches * 4);  // batched super-chunks: <= kHubSlabBatches * 4 occurrences
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) / 16 * 16; }
 }  // namespace
