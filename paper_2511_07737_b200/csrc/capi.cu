@@ -27,6 +27,7 @@ using namespace tsat;
 #endif
 
 struct DevCnf {
+    void* arena = nullptr;              // one allocation holding every array below
     uint32_t *cptr = nullptr, *clit = nullptr, *occ_ptr = nullptr, *occ_rec = nullptr, *occ_cnt = nullptr;
     uint32_t *bat_ptr = nullptr, *bat_rec = nullptr;
     uint32_t* seg_lit = nullptr;        // clause length segments (k_clause_seg), K <= 7
@@ -402,17 +403,7 @@ void free_fp64(tsat_ctx ctx) {
 }
 
 void free_cnf(tsat_ctx ctx) {
-    cudaFree(ctx->dcnf.cptr);
-    cudaFree(ctx->dcnf.clit);
-    cudaFree(ctx->dcnf.seg_lit);
-    cudaFree(ctx->dcnf.occ_ptr);
-    cudaFree(ctx->dcnf.occ_rec);
-    cudaFree(ctx->dcnf.bat_ptr);
-    cudaFree(ctx->dcnf.bat_rec);
-    cudaFree(ctx->dcnf.occ_cnt);
-    cudaFree(ctx->dcnf.occ_pn);
-    cudaFree(ctx->dcnf.hub_of);
-    cudaFree(ctx->dcnf.hub_sc);
+    cudaFree(ctx->dcnf.arena);
     ctx->dcnf = DevCnf{};
     ctx->have_cnf = false;
 }
@@ -442,34 +433,40 @@ tsat_status upload_cnf(tsat_ctx ctx, HostCnf&& h) {
     ctx->have_batch = false;
     ctx->cnf = std::move(h);
     const HostCnf& c = ctx->cnf;
-    auto up = [&](uint32_t** dst, const std::vector<uint32_t>& src) -> cudaError_t {
-        size_t bytes = std::max<size_t>(src.size(), 1) * 4;
-        cudaError_t e = cudaMalloc(dst, bytes);
-        if (e != cudaSuccess) return e;
-        if (!src.empty()) e = cudaMemcpyAsync(*dst, src.data(), src.size() * 4, cudaMemcpyHostToDevice, ctx->stream);
-        return e;
+    // every device array of the CNF in one allocation, filled by one copy from
+    // one host staging buffer (per-array cudaMalloc + pageable copies cost
+    // milliseconds of the end-to-end setup)
+    struct Part { void** dst; const void* src; size_t bytes, alloc; };
+    std::vector<Part> parts;
+    auto add = [&](void** dst, const void* src, size_t n, size_t min_n) {
+        parts.push_back({dst, src, n * 4, ((std::max(n, min_n) * 4) + 255) / 256 * 256});
     };
-    CK(cudaSetDevice(ctx->device));
-    CK(up(&ctx->dcnf.cptr, c.clause_ptr));
-    CK(up(&ctx->dcnf.clit, c.clause_lit));
-    if (c.K <= 7 && !c.seg_lit.empty()) CK(up(&ctx->dcnf.seg_lit, c.seg_lit));
-    CK(up(&ctx->dcnf.occ_ptr, c.occ_ptr));
-    CK(up(&ctx->dcnf.occ_rec, c.occ_rec));
-    CK(up(&ctx->dcnf.occ_cnt, c.occ_cnt));
+    add((void**)&ctx->dcnf.cptr, c.clause_ptr.data(), c.clause_ptr.size(), 1);
+    add((void**)&ctx->dcnf.clit, c.clause_lit.data(), c.clause_lit.size(), 1);
+    if (c.K <= 7 && !c.seg_lit.empty()) add((void**)&ctx->dcnf.seg_lit, c.seg_lit.data(), c.seg_lit.size(), 1);
+    add((void**)&ctx->dcnf.occ_ptr, c.occ_ptr.data(), c.occ_ptr.size(), 1);
+    add((void**)&ctx->dcnf.occ_rec, c.occ_rec.data(), c.occ_rec.size(), 1);
+    add((void**)&ctx->dcnf.occ_cnt, c.occ_cnt.data(), c.occ_cnt.size(), 1);
     if (c.batched) {
-        CK(up(&ctx->dcnf.bat_ptr, c.bat_ptr));
-        CK(up(&ctx->dcnf.bat_rec, c.bat_rec));
+        add((void**)&ctx->dcnf.bat_ptr, c.bat_ptr.data(), c.bat_ptr.size(), 1);
+        add((void**)&ctx->dcnf.bat_rec, c.bat_rec.data(), c.bat_rec.size(), 1);
     }
-    auto upi = [&](void** dst, const std::vector<int32_t>& src) -> cudaError_t {
-        size_t bytes = std::max<size_t>(src.size(), 4) * 4;
-        cudaError_t e = cudaMalloc(dst, bytes);
-        if (e != cudaSuccess) return e;
-        if (!src.empty()) e = cudaMemcpyAsync(*dst, src.data(), src.size() * 4, cudaMemcpyHostToDevice, ctx->stream);
-        return e;
-    };
-    CK(upi((void**)&ctx->dcnf.occ_pn, c.occ_pn));
-    CK(upi((void**)&ctx->dcnf.hub_of, c.hub_of));
-    CK(upi((void**)&ctx->dcnf.hub_sc, c.hub_sc));
+    add((void**)&ctx->dcnf.occ_pn, c.occ_pn.data(), c.occ_pn.size(), 4);
+    add((void**)&ctx->dcnf.hub_of, c.hub_of.data(), c.hub_of.size(), 4);
+    add((void**)&ctx->dcnf.hub_sc, c.hub_sc.data(), c.hub_sc.size(), 4);
+    size_t total = 0;
+    for (const Part& p : parts) total += p.alloc;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMalloc(&ctx->dcnf.arena, total));
+    std::vector<unsigned char> stage(total);
+    size_t off = 0;
+    for (const Part& p : parts) {
+        *p.dst = (char*)ctx->dcnf.arena + off;
+        if (p.bytes) std::memcpy(stage.data() + off, p.src, p.bytes);
+        off += p.alloc;
+    }
+    CK(cudaMemcpyAsync(ctx->dcnf.arena, stage.data(), total, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));        // `stage` is pageable and local
     if (ctx->peer) {                    // a fresh, zeroed exchange buffer for this V; peers must reconnect
         peer_release(ctx);
         const size_t xb = peer_layout(c.V, ctx->world).total;

@@ -17,6 +17,9 @@ namespace tsat {
 #ifndef TSAT_BIN_SKIP
 #define TSAT_BIN_SKIP 1              // batched records: skip bins above the batch's clause length
 #endif
+#ifndef TSAT_ODD_STEP
+#define TSAT_ODD_STEP 0              // 1: an odd last literal step skips the absent half (measured c4 k_update +4 %, k_hub +9 %)
+#endif
 #ifndef TSAT_PLANE_FRAC
 #define TSAT_PLANE_FRAC 0            // planes larger than L2: evict-last on this fraction of the lines (0: normal)
 #endif
@@ -513,6 +516,20 @@ __device__ __forceinline__ void count_batched(uint32_t (&cnt)[NCTR][B], RecFn re
             uint32_t x[8];
 #pragma unroll
             for (int k = 0; k < 4; ++k) x[k] = ld(rec(q0 + k));
+#if TSAT_ODD_STEP
+            if (two) {                                   // warp-uniform: an odd last step adds nothing more
+#pragma unroll
+                for (int k = 0; k < 4; ++k) x[4 + k] = ld(rec(q0 + 4 + k));
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    bs_add<NP>(sp[k], x[k]);
+                    bs_add<NP>(sp[k], x[4 + k]);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) bs_add<NP>(sp[k], x[k]);
+            }
+#else
 #pragma unroll
             for (int k = 0; k < 4; ++k) x[4 + k] = two ? ld(rec(q0 + 4 + k)) : 0u;
 #pragma unroll
@@ -520,6 +537,7 @@ __device__ __forceinline__ void count_batched(uint32_t (&cnt)[NCTR][B], RecFn re
                 bs_add<NP>(sp[k], x[k]);
                 bs_add<NP>(sp[k], x[4 + k]);
             }
+#endif
         }
         // one code path for both signs: c - S = c + ~S + 1 (two's complement)
         const uint32_t cm = neg ? 0u : 0xffffffffu;
