@@ -3,15 +3,16 @@ import torch
 from paper_2511_07737_b200 import Solver
 from tsat_synth import make_config
 cnf, cfg = make_config("c2"); N = cfg["N"]
-def run(tag, steps, chunk, close_first=True):
-    s = Solver(0); s.load_cnf(cnf); s.init_batch(N, 1)
+def run(tag, steps, chunk, st=None):
+    kw = {} if st is None else {"stream": st}
+    s = Solver(0, **kw); s.load_cnf(cnf); s.init_batch(N, 1)
     for _ in range(steps // chunk): s.step(chunk)
     torch.cuda.synchronize()
     s.close()
     pins = torch.empty(N, dtype=torch.int32, pin_memory=True)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    s2 = Solver(0); ta = time.perf_counter()
+    s2 = Solver(0, **kw); ta = time.perf_counter()
     s2.load_cnf(cnf); torch.cuda.synchronize(); tl = time.perf_counter()
     s2.init_batch(N, 1); torch.cuda.synchronize(); ti = time.perf_counter()
     s2.step(1); torch.cuda.synchronize(); ts = time.perf_counter()
@@ -22,3 +23,6 @@ def run(tag, steps, chunk, close_first=True):
 run("after 390 steps chunk 30", 390, 30)
 run("again", 390, 30)
 run("after 30 steps chunk 1", 30, 1)
+run("torch current stream", 390, 30, torch.cuda.current_stream())
+run("torch current stream again", 390, 30, torch.cuda.current_stream())
+run("side stream", 390, 30, torch.cuda.Stream())
