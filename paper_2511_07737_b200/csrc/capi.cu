@@ -1039,7 +1039,11 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
         // planes are L2-resident: both buffers below 48 MB)
         ctx->upd_cw6 = 0;
         const bool planes_l2 = 2.0 * 4.0 * ((double)ctx->cnf.V + 1.0) * (double)(ctx->N / 32) <= 48.0e6;
-        if (ctx->cnf.K <= 3 && planes_l2 && !ctx->sharded && !ctx->chunked && !ctx->peer && !std::getenv("TSAT_NO_CW6")) {
+#ifndef TSAT_PEER_CW6
+#define TSAT_PEER_CW6 0                 // 1: the peer kernel with 6-plane counters too (c2 peer k_update 0.278 -> 0.281 ms: not used)
+#endif
+        if (ctx->cnf.K <= 3 && planes_l2 && !ctx->sharded && !ctx->chunked && (TSAT_PEER_CW6 || !ctx->peer) &&
+            !std::getenv("TSAT_NO_CW6")) {
             int mx = 0;
             for (int v = 0; v < ctx->cnf.V; ++v)
                 if (ctx->cnf.hub_of[v] < 0) mx = std::max({mx, ctx->cnf.occ_pn[2 * v], ctx->cnf.occ_pn[2 * v + 1]});
@@ -1052,10 +1056,12 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
         if (!ctx->sharded && !ctx->chunked && !std::getenv("TSAT_NO_BLK")) {
             const int RB = update_block_rows(ctx->N);
             if (RB > 1) {
-                // block order: rows grouped by their gather length (batches of 4
-                // same-sign records, or staged record words), so the RB rows a
-                // warp gathers at once finish together; hub rows (counted by
-                // k_hub) first.  Stable: equal lengths keep the variable order.
+                // block order: consecutive variables (the kernel then needs no
+                // row list).  TSAT_BLK_SORT=1: rows grouped by their gather
+                // length (the RB rows a warp gathers at once finish together)
+                // through a row list - measured slower (c3 N = 128 k_update
+                // 1.16 vs 1.11 ms, N = 256 2.04 vs 1.95 ms): the indirection and
+                // lost row locality cost more than the divergence it removes.
                 const HostCnf& h = ctx->cnf;
                 const std::vector<uint32_t>& ptr = h.batched ? h.bat_ptr : h.occ_ptr;
                 const int V = h.V;
@@ -1066,7 +1072,8 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
                     if (!h.batched) return (h.occ_pn[2 * v] + 3) / 4 + (h.occ_pn[2 * v + 1] + 3) / 4;
                     return (long long)(ptr[v + 1] - ptr[v]);
                 };
-                if (!std::getenv("TSAT_BLK_NOSORT"))
+                const bool sorted = std::getenv("TSAT_BLK_SORT") != nullptr;
+                if (sorted)
                     std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return glen(x) < glen(y); });
                 long long cap = 0;
                 for (int b0 = 0; b0 < V; b0 += RB) {
@@ -1079,8 +1086,10 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
                 }
                 cudaFree(ctx->blk_rows);
                 ctx->blk_rows = nullptr;
-                CK(cudaMalloc(&ctx->blk_rows, (size_t)std::max(V, 1) * sizeof(int)));
-                CK(cudaMemcpy(ctx->blk_rows, order.data(), (size_t)V * sizeof(int), cudaMemcpyHostToDevice));
+                if (sorted) {
+                    CK(cudaMalloc(&ctx->blk_rows, (size_t)std::max(V, 1) * sizeof(int)));
+                    CK(cudaMemcpy(ctx->blk_rows, order.data(), (size_t)V * sizeof(int), cudaMemcpyHostToDevice));
+                }
                 ctx->upd_RB = RB;
                 ctx->upd_blk_cap = (int)std::max(64LL, (cap + 63) / 64 * 64);
             }

@@ -26,6 +26,13 @@
 
 #include "upd_common.cuh"
 
+#ifndef TSAT_ROW_PREFETCH
+#define TSAT_ROW_PREFETCH 1          // L2 bulk prefetch of each row's theta / m / v at the row's start
+#endif
+#ifndef TSAT_PREFETCH_BYTES
+#define TSAT_PREFETCH_BYTES 64.0e6
+#endif
+
 namespace tsat {
 
 // MODE 0: fused W = 1 iteration.  MODE 1: phase A of the sharded iteration
@@ -199,10 +206,17 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
         if (tg == 0) {
             if (!CLU) rowslot[it & 1] = atomicAdd(&a.ds->row_counter, 1);
             const uint32_t rowbytes = (uint32_t)ncand * 4u;
-            prefetch_l2(a.theta + (size_t)v * N + n0c, rowbytes);
-            if (MODE != 1) {
-                prefetch_l2(a.m + (size_t)v * N + n0c, rowbytes);
-                prefetch_l2(a.v + (size_t)v * N + n0c, rowbytes);
+            // TSAT_ROW_PREFETCH: 0 never, 1 always, 2 only while the rows in
+            // flight (groups x SMs x 12 B x N) stay well inside L2
+            const bool pf = TSAT_ROW_PREFETCH == 1 ||
+                            (TSAT_ROW_PREFETCH == 2 && (double)gridDim.x * (double)(blockDim.x / GT) * 12.0 * (double)ncand <
+                                                           TSAT_PREFETCH_BYTES);
+            if (pf) {
+                prefetch_l2(a.theta + (size_t)v * N + n0c, rowbytes);
+                if (MODE != 1) {
+                    prefetch_l2(a.m + (size_t)v * N + n0c, rowbytes);
+                    prefetch_l2(a.v + (size_t)v * N + n0c, rowbytes);
+                }
             }
         }
         uint32_t* posw = posw0 + (DEFER ? (size_t)(it & 1) * 2 * NWg : 0);
@@ -581,6 +595,8 @@ static cudaError_t set_update_attrs(int need, int optin) {
     if ((e = set_max_dyn_smem(k_update<KB, 2, true, true>, need, optin)) != cudaSuccess) return e;
     if ((e = set_max_dyn_smem(k_update<KB, 0, false, false, 6>, need, optin)) != cudaSuccess) return e;
     if ((e = set_max_dyn_smem(k_update<KB, 0, true, false, 6>, need, optin)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 2, false, false, 6>, need, optin)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update<KB, 2, true, false, 6>, need, optin)) != cudaSuccess) return e;
     return set_max_dyn_smem(k_update<KB, 2, true>, need, optin);
 }
 
@@ -754,6 +770,11 @@ static cudaError_t launch_update_kbg(const StepArgs& a, const uint32_t* Acur, ui
                                    : cudaLaunchKernelEx(&cfg, k_update<KB, 3, false>, a, Acur, Anext, sc);
     }
     if (a.peer) {
+        if (!GSG && a.upd_cw6) {                  // 6-plane counters (fewer registers under the exchange state)
+            if (mag) k_update<KB, 2, true, false, 6><<<g, b, sm, st>>>(a, Acur, Anext, sc);
+            else k_update<KB, 2, false, false, 6><<<g, b, sm, st>>>(a, Acur, Anext, sc);
+            return cudaGetLastError();
+        }
         if (mag) k_update<KB, 2, true, GSG><<<g, b, sm, st>>>(a, Acur, Anext, sc);
         else k_update<KB, 2, false, GSG><<<g, b, sm, st>>>(a, Acur, Anext, sc);
         return cudaGetLastError();

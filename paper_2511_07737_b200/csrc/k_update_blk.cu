@@ -189,14 +189,14 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
     // row values of the block's row r for lane r (< nr): occurrence counts,
     // hub index, Eq. 5 statistics of the evaluated state, and the row's
     // record offset within the block's staging buffer (non-hub rows back to back)
-    // (the block's rows are a.blk_rows[item RB ...]: rows grouped by their
+    // (the block's rows are item RB ... item RB + nr - 1, or a.blk_rows[item RB ...]: rows grouped by their
     // gather length on the host, so the lanes of a warp finish together)
     // (called by the whole warp: the offsets are an exclusive warp prefix sum
     // of the rows' staged lengths, one load chain per lane)
     auto fetch_row = [&](int item, int nr, RowPre& P) {
         unsigned mine = 0;
         if (lane < nr) {
-            const int v = a.blk_rows[(size_t)item * RB + lane];
+            const int v = a.blk_rows ? a.blk_rows[(size_t)item * RB + lane] : item * RB + lane;
             P.v = v;
             P.pn = a.occ_pn[v];
             P.hub = a.hub_of[v];
