@@ -100,6 +100,7 @@ struct tsat_ctx_s {
     int upd_chunk = 0, upd_gs_global = 0;
     bool chunked = false;               // N too large for the fused kernel: split sequence, no collectives at W = 1
     int upd_cl = 0;                     // > 1: cluster-split rows (k_update MODE 3) instead of chunking
+    int upd_prefetch = 1;               // k_update L2 row prefetch (configure_update)
     bool use_seg = false;               // length-segmented clause evaluation (k_clause_seg)
     size_t upd_smem = 0;
     int64_t prof_steps = 0;
@@ -306,6 +307,7 @@ StepArgs step_args(tsat_ctx ctx) {
     a.upd_blk_cap = ctx->upd_blk_cap;
     a.upd_cw6 = ctx->upd_cw6;
     a.upd_cl = ctx->upd_cl;
+    a.upd_prefetch = ctx->upd_prefetch;
     a.blk_rows = ctx->blk_rows;
     a.use_seg = ctx->use_seg ? 1 : 0;
     a.seg_lit = ctx->dcnf.seg_lit;
@@ -1102,6 +1104,7 @@ tsat_status tsat_init_batch(tsat_ctx ctx, int64_t N_global, uint64_t seed, const
             ctx->upd_recbufs = g.upd_recbufs;
             ctx->upd_NG = g.upd_NG;
             ctx->upd_grid = g.upd_grid;
+            ctx->upd_prefetch = g.upd_prefetch;
             ctx->upd_smem = g.upd_smem;
             ctx->num_sms = g.num_sms;
             ctx->upd_chunk = g.upd_chunk;

@@ -26,8 +26,13 @@
 
 #include "upd_common.cuh"
 
+// L2 bulk prefetch of each row's theta / m / v at the row's start: 0 never,
+// 1 always, 2 while the rows in flight (CTAs x groups x 12 B x candidates)
+// stay below TSAT_PREFETCH_BYTES - beyond that the prefetched lines are
+// evicted before pass 3b reads them (c5 N = 8192: 87 MB in flight, k_update
+// 5.82 -> 5.26 ms without; c2 49.7 MB: 0.264 -> 0.249 ms with)
 #ifndef TSAT_ROW_PREFETCH
-#define TSAT_ROW_PREFETCH 1          // L2 bulk prefetch of each row's theta / m / v at the row's start
+#define TSAT_ROW_PREFETCH 2
 #endif
 #ifndef TSAT_PREFETCH_BYTES
 #define TSAT_PREFETCH_BYTES 64.0e6
@@ -206,12 +211,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
         if (tg == 0) {
             if (!CLU) rowslot[it & 1] = atomicAdd(&a.ds->row_counter, 1);
             const uint32_t rowbytes = (uint32_t)ncand * 4u;
-            // TSAT_ROW_PREFETCH: 0 never, 1 always, 2 only while the rows in
-            // flight (groups x SMs x 12 B x N) stay well inside L2
-            const bool pf = TSAT_ROW_PREFETCH == 1 ||
-                            (TSAT_ROW_PREFETCH == 2 && (double)gridDim.x * (double)(blockDim.x / GT) * 12.0 * (double)ncand <
-                                                           TSAT_PREFETCH_BYTES);
-            if (pf) {
+            if (a.upd_prefetch) {                            // configure_update: rows in flight fit L2
                 prefetch_l2(a.theta + (size_t)v * N + n0c, rowbytes);
                 if (MODE != 1) {
                     prefetch_l2(a.m + (size_t)v * N + n0c, rowbytes);
@@ -658,6 +658,8 @@ static cudaError_t configure_update_cluster(StepArgs* a, int optin, int sms) {
     if (e != cudaSuccess) return e;
     if (mc < 1) return cudaErrorInvalidConfiguration;
     a->upd_grid = mc * CL;
+    a->upd_prefetch = TSAT_ROW_PREFETCH == 1 ||
+                      (TSAT_ROW_PREFETCH == 2 && (double)a->upd_grid * (double)ng * 12.0 * (double)NCH < TSAT_PREFETCH_BYTES);
     if (std::getenv("TSAT_GEOM_VERBOSE"))
         std::fprintf(stderr, "k_update cluster geometry: KB %d N %d CL %d slice %d GT %d groups %lld clusters %d smem %zu\n",
                      KB, a->N, CL, NCH, GT, ng, mc, a->upd_smem);
@@ -716,6 +718,8 @@ cudaError_t configure_update(StepArgs* a) {
     a->upd_NG = (int)ng;
     a->upd_smem = gsb + (size_t)ng * grb;
     a->upd_grid = sms;
+    a->upd_prefetch = TSAT_ROW_PREFETCH == 1 ||
+                      (TSAT_ROW_PREFETCH == 2 && (double)sms * (double)ng * 12.0 * (double)a->upd_chunk < TSAT_PREFETCH_BYTES);
     // test hook: several ranks' persistent kernels sharing one GPU must be
     // co-resident, so each may be limited to a part of the SMs
     if (const char* g = std::getenv("TSAT_UPD_GRID")) {

@@ -197,6 +197,7 @@ struct StepArgs {
     int upd_blk_cap;                 // record words a group stages per row block (max over blocks, non-hub rows)
     int upd_cw6;                     // K <= 3 fused W = 1: 6-plane counters (no row above 31 same-sign occurrences)
     int upd_cl;                      // > 1: cluster-split rows (k_update MODE 3), CTAs per cluster
+    int upd_prefetch;                // k_update: L2 bulk prefetch of each row's streams (configure_update)
     const int* blk_rows;             // [V] rows in block order (grouped by gather length; k_update_blk)
     // clause length segments (k_clause_seg; HostCnf::seg_*): use_seg = 1 when
     // the instance is not uniform 3-SAT, K <= 7 and N >= 1024 per GPU
