@@ -37,6 +37,9 @@
 #ifndef TSAT_PREFETCH_BYTES
 #define TSAT_PREFETCH_BYTES 64.0e6
 #endif
+#ifndef TSAT_PREFETCH_THETA
+#define TSAT_PREFETCH_THETA 1        // beyond the bound, prefetch theta alone if that fits (c5 N = 8192 step 5.85 -> 5.67 ms)
+#endif
 
 namespace tsat {
 
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
             const uint32_t rowbytes = (uint32_t)ncand * 4u;
             if (a.upd_prefetch) {                            // configure_update: rows in flight fit L2
                 prefetch_l2(a.theta + (size_t)v * N + n0c, rowbytes);
-                if (MODE != 1) {
+                if (MODE != 1 && a.upd_prefetch == 1) {
                     prefetch_l2(a.m + (size_t)v * N + n0c, rowbytes);
                     prefetch_l2(a.v + (size_t)v * N + n0c, rowbytes);
                 }
@@ -718,8 +721,11 @@ cudaError_t configure_update(StepArgs* a) {
     a->upd_NG = (int)ng;
     a->upd_smem = gsb + (size_t)ng * grb;
     a->upd_grid = sms;
-    a->upd_prefetch = TSAT_ROW_PREFETCH == 1 ||
-                      (TSAT_ROW_PREFETCH == 2 && (double)sms * (double)ng * 12.0 * (double)a->upd_chunk < TSAT_PREFETCH_BYTES);
+    {
+        const double fl = (double)sms * (double)ng * 12.0 * (double)a->upd_chunk;   // rows in flight (bytes)
+        a->upd_prefetch = (TSAT_ROW_PREFETCH == 1 || (TSAT_ROW_PREFETCH == 2 && fl < TSAT_PREFETCH_BYTES)) ? 1
+                        : (TSAT_PREFETCH_THETA && fl / 3.0 < TSAT_PREFETCH_BYTES) ? 2 : 0;    // 2: theta only
+    }
     // test hook: several ranks' persistent kernels sharing one GPU must be
     // co-resident, so each may be limited to a part of the SMs
     if (const char* g = std::getenv("TSAT_UPD_GRID")) {
