@@ -15,7 +15,7 @@ for cfg in f4d f4s; do for ce in 0 1; do
 done; done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c2.csv python bench.py --steps 30 --warmup 30 $B > /dev/null 2>&1
 cp profiles/ncu_traffic.json /tmp/ncu_traffic_before.json
-for spec in "c2 k_update c2" "c3 k_update c3" "c4 k_update c4" "c3 k_update_blk c3n128 --n-per-gpu=128" "c5 k_update c5n8192 --n-per-gpu=8192" "c2 k_clause c2" "c4 k_clause_seg c4" "c4 k_hub c4" "f4d k_dense_clause f4d --clause-eval=1"; do
+for spec in "c2 k_update c2" "c3 k_update c3" "c4 k_update c4" "c3 k_update_blk c3n128 --n-per-gpu=128" "c5 k_update c5n8192 --n-per-gpu=8192" "c2 k_clause c2" "c4 k_clause_seg c4" "c4 k_hub c4" ${EXTRA_NCU}; do
 set -- $spec
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"$2[<(]" -s 2 -c 1 -o $O/prof_$2_$3 -f python bench.py --config $1 $4 --no-e2e --no-cpu --no-quality --no-extra --no-tts --steps 10 --warmup 3 > $O/ncu_$2_$3.log 2>&1; tail -1 $O/ncu_$2_$3.log
 python scripts/ncu_summary.py $O $O/prof_$2_$3.ncu-rep > /dev/null 2>&1
@@ -23,5 +23,6 @@ python scripts/ncu_lines.py $O/prof_$2_$3.ncu-rep 40 > $O/lines_$2_$3.txt 2>&1
 done
 cp profiles/ncu_traffic.json $O/ncu_traffic.json
 rm -f $O/*.ncu-rep
-SAN_OUT=${EV_OUT:-ev2}/san bash scripts/sanitize.sh
+[ -n "$SANITIZE" ] && SAN_OUT=${EV_OUT:-ev2}/san bash scripts/sanitize.sh     # (compute-sanitizer is closed on the pool)
+CFG=c2 bash scripts/peer_ab.sh > $O/peer_c2.txt 2>&1; cat $O/peer_c2.txt
 ls $O

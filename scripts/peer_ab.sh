@@ -1,5 +1,5 @@
 # peer kernels at W = 1 (self exchange) vs the fused kernel, and a library variant: bash scripts/peer_ab.sh lib_x
-for r in 1 2; do
+for r in $(seq 1 ${ROUNDS:-2}); do
 for v in base $1; do
   if [ "$v" = base ]; then lib=paper_2511_07737_b200/libturbosat.so; else lib=paper_2511_07737_b200/$v.so; fi
   for p in "" "--peer"; do
