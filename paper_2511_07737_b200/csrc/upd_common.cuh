@@ -144,7 +144,11 @@ __device__ __forceinline__ void fold_counts(float (&d)[KB], uint32_t p0, uint32_
     // derived bin: dsum - sum_r d_r as an integer (byte dot products with -1;
     // the unused top byte is 0), made an exact float through the mantissa of
     // 1.5 * 2^23 (|x| < 2^22); +0 for x = 0, as the fp32 subtraction gave
-    if (TSAT_FOLD_DP4A && KB == 8) {
+    if (TSAT_FOLD_DP4A == 2) {                       // every KB, I2F conversion (exact: |x| < 2^24)
+        int x = __dp4a((int)p0, -1, dsum);
+        if (KB == 8) x = __dp4a((int)p1, -1, x);
+        d[KB - 1] = (float)x;
+    } else if (TSAT_FOLD_DP4A && KB == 8) {
         int x = __dp4a((int)p0, -1, dsum);
         x = __dp4a((int)p1, -1, x);
         d[KB - 1] = __int_as_float(0x4B400000 + x) - 12582912.0f;
