@@ -75,7 +75,11 @@ int update_block_rows(int N) {
     return rb >= 2 ? rb : 1;
 }
 
-template <int KB, int MODE, bool MAG>
+// NT > 0: the shard size as a compile-time constant (N = 128 / 256 / 512, the
+// W = 8 / 4 / 2 shares of c3's fixed batch): the block geometry (words per row,
+// rows per block, iterations per row, lane -> (row, word)) folds into
+// constants instead of living in registers.
+template <int KB, int MODE, bool MAG, int NT = 0>
 __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TSAT_UPD_THREADS4) : TSAT_UPD_THREADS8, 1)
     k_update_blk(StepArgs a, const uint32_t* __restrict__ Acur, uint32_t* __restrict__ Anext,
                  const StepScalars* __restrict__ sc) {
@@ -84,7 +88,7 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
     constexpr int NDW = KB == 4 ? 1 : 2;
     constexpr int nbufs = upd_recbufs(KB);
     extern __shared__ __align__(16) unsigned char smem[];
-    const int N = a.N, NW = N >> 5, RB = a.upd_RB;
+    const int N = NT ? NT : a.N, NW = N >> 5, RB = NT ? 32 / (NT >> 5) : a.upd_RB;
     const int ipr = N >> 7;                              // 128-candidate iterations per row
     const size_t dpkw = upd_dpk_words(N), dplane = (size_t)RB * dpkw;
     float* gs = reinterpret_cast<float*>(smem);
@@ -495,14 +499,26 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : TS
     }
 }
 
+#ifndef TSAT_BLK_NT
+#define TSAT_BLK_NT 1                // compile-time shard sizes 128 / 256 / 512 for KB <= 8 (c3 N = 128: k_update -9 %)
+#endif
+template <int KB, int NT>
+static cudaError_t set_blk_attrs_nt(int need, int optin) {
+    cudaError_t e;
+    if ((e = set_max_dyn_smem(k_update_blk<KB, 0, false, NT>, need, optin)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update_blk<KB, 2, false, NT>, need, optin)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem(k_update_blk<KB, 0, true, NT>, need, optin)) != cudaSuccess) return e;
+    return set_max_dyn_smem(k_update_blk<KB, 2, true, NT>, need, optin);
+}
 template <int KB>
 static cudaError_t set_blk_attrs(int need, int optin) {
-    const cudaFuncAttribute attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
     cudaError_t e;
-    if ((e = set_max_dyn_smem(k_update_blk<KB, 0, false>, need, optin)) != cudaSuccess) return e;
-    if ((e = set_max_dyn_smem(k_update_blk<KB, 2, false>, need, optin)) != cudaSuccess) return e;
-    if ((e = set_max_dyn_smem(k_update_blk<KB, 0, true>, need, optin)) != cudaSuccess) return e;
-    return set_max_dyn_smem(k_update_blk<KB, 2, true>, need, optin);
+    if (TSAT_BLK_NT && KB <= 8) {
+        if ((e = set_blk_attrs_nt<KB, 128>(need, optin)) != cudaSuccess) return e;
+        if ((e = set_blk_attrs_nt<KB, 256>(need, optin)) != cudaSuccess) return e;
+        if ((e = set_blk_attrs_nt<KB, 512>(need, optin)) != cudaSuccess) return e;
+    }
+    return set_blk_attrs_nt<KB, 0>(need, optin);
 }
 
 cudaError_t configure_update_blk(StepArgs* a) {
@@ -542,19 +558,29 @@ cudaError_t configure_update_blk(StepArgs* a) {
     return set_blk_attrs<16>(smem, optin);
 }
 
-template <int KB>
-static cudaError_t launch_blk_kb(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
+template <int KB, int NT>
+static cudaError_t launch_blk_nt(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
                                  cudaStream_t st) {
     const bool mag = a.mc.normalize == 3;
     const dim3 g(a.upd_grid), b(32 * a.upd_NG);
     const size_t sm = a.upd_smem;
     if (a.peer) {
-        if (mag) k_update_blk<KB, 2, true><<<g, b, sm, st>>>(a, Acur, Anext, sc);
-        else k_update_blk<KB, 2, false><<<g, b, sm, st>>>(a, Acur, Anext, sc);
+        if (mag) k_update_blk<KB, 2, true, NT><<<g, b, sm, st>>>(a, Acur, Anext, sc);
+        else k_update_blk<KB, 2, false, NT><<<g, b, sm, st>>>(a, Acur, Anext, sc);
         return cudaGetLastError();
     }
-    return mag ? launch_maybe_pdl(a.pdl, k_update_blk<KB, 0, true>, g, b, sm, st, a, Acur, Anext, sc)
-               : launch_maybe_pdl(a.pdl, k_update_blk<KB, 0, false>, g, b, sm, st, a, Acur, Anext, sc);
+    return mag ? launch_maybe_pdl(a.pdl, k_update_blk<KB, 0, true, NT>, g, b, sm, st, a, Acur, Anext, sc)
+               : launch_maybe_pdl(a.pdl, k_update_blk<KB, 0, false, NT>, g, b, sm, st, a, Acur, Anext, sc);
+}
+template <int KB>
+static cudaError_t launch_blk_kb(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
+                                 cudaStream_t st) {
+    if constexpr (TSAT_BLK_NT && KB <= 8) {
+        if (a.N == 128) return launch_blk_nt<KB, 128>(a, Acur, Anext, sc, st);
+        if (a.N == 256) return launch_blk_nt<KB, 256>(a, Acur, Anext, sc, st);
+        if (a.N == 512) return launch_blk_nt<KB, 512>(a, Acur, Anext, sc, st);
+    }
+    return launch_blk_nt<KB, 0>(a, Acur, Anext, sc, st);
 }
 
 cudaError_t launch_update_blk(const StepArgs& a, const uint32_t* Acur, uint32_t* Anext, const StepScalars* sc,
