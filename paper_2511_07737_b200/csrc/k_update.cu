@@ -31,6 +31,9 @@
 // stay below TSAT_PREFETCH_BYTES - beyond that the prefetched lines are
 // evicted before pass 3b reads them (c5 N = 8192: 87 MB in flight, k_update
 // 5.82 -> 5.26 ms without; c2 49.7 MB: 0.264 -> 0.249 ms with)
+#ifndef TSAT_UPD_NT
+#define TSAT_UPD_NT 1                // compile-time batch size for c4's shape (MODE 0, KB = 8, N = 2048)
+#endif
 #ifndef TSAT_ROW_PREFETCH
 #define TSAT_ROW_PREFETCH 2
 #endif
@@ -62,7 +65,11 @@ namespace tsat {
 // memory) and process the same rows in a static order; the row's J and Q
 // partials are summed over DSMEM (cluster.cuh), so no G round trip through
 // HBM and no g table reads from L2.
-template <int KB, int MODE, bool MAG = false, bool GSG = false, int CW = 8>
+// NT > 0 (MODE 0): the batch size as a compile-time constant, used for c4's
+// shape (KB = 8, N = 2048: k_update -0.9 %); for KB = 4 at c2's 4096, c3's
+// 1024 and c5's 8192 it measured equal or slower (c2 +3 %: more spills), so
+// those keep the run-time geometry.
+template <int KB, int MODE, bool MAG = false, bool GSG = false, int CW = 8, int NT = 0>
 __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (CW == 6 ? TSAT_UPD_THREADS4C6 : TSAT_UPD_THREADS4))
                                           : TSAT_UPD_THREADS8, 1) k_update(StepArgs a, const uint32_t* __restrict__ Acur,
                                                                     uint32_t* __restrict__ Anext,
@@ -70,7 +77,8 @@ __global__ void __launch_bounds__(KB == 4 ? (MODE == 2 ? TSAT_UPD_THREADS4P : (C
     constexpr int NP = (KB == 4) ? 2 : (KB == 8 ? 3 : 4);
     constexpr int NCTR = KB - 1;
     extern __shared__ __align__(16) unsigned char smem[];
-    const int N = a.N, NW = N >> 5, GT = a.upd_GT;
+    const int N = NT ? NT : a.N, NW = N >> 5;
+    const int GT = NT ? ((NT >> 5) >= 128 ? 128 : ((NT >> 5) > 32 ? 64 : 32)) : a.upd_GT;   // as configure_update
     // work item = (row, chunk of NCH candidates); NCH == N except for batches
     // too large for shared memory (MODE 1 only), whose g table stays in L2
     constexpr bool CLU = MODE == 3;
@@ -599,6 +607,8 @@ static cudaError_t set_update_attrs(int need, int optin) {
     if ((e = set_max_dyn_smem(k_update<KB, 0, false, false, 6>, need, optin)) != cudaSuccess) return e;
     if ((e = set_max_dyn_smem(k_update<KB, 0, true, false, 6>, need, optin)) != cudaSuccess) return e;
     if ((e = set_max_dyn_smem(k_update<KB, 2, false, false, 6>, need, optin)) != cudaSuccess) return e;
+    if constexpr (TSAT_UPD_NT && KB == 8)
+        if ((e = set_max_dyn_smem(k_update<8, 0, false, false, 8, 2048>, need, optin)) != cudaSuccess) return e;
     if ((e = set_max_dyn_smem(k_update<KB, 2, true, false, 6>, need, optin)) != cudaSuccess) return e;
     return set_max_dyn_smem(k_update<KB, 2, true>, need, optin);
 }
@@ -788,6 +798,10 @@ static cudaError_t launch_update_kbg(const StepArgs& a, const uint32_t* Acur, ui
         if (mag) k_update<KB, 2, true, GSG><<<g, b, sm, st>>>(a, Acur, Anext, sc);
         else k_update<KB, 2, false, GSG><<<g, b, sm, st>>>(a, Acur, Anext, sc);
         return cudaGetLastError();
+    }
+    if constexpr (TSAT_UPD_NT && KB == 8) {      // compile-time batch size of c4's shape
+        if (!mag && !GSG && a.N == 2048)
+            return launch_maybe_pdl(a.pdl, k_update<8, 0, false, false, 8, 2048>, g, b, sm, st, a, Acur, Anext, sc);
     }
     if (!GSG && a.upd_cw6)                       // K <= 3, every row within 6-bit counters
         return mag ? launch_maybe_pdl(a.pdl, k_update<KB, 0, true, false, 6>, g, b, sm, st, a, Acur, Anext, sc)

@@ -178,7 +178,7 @@ def test_degenerate_and_shape_cases(case):
         assert s.get_info().best_unsat >= 1 and s.get_solution() is None
 
 
-@pytest.mark.parametrize("case", ["industrial7", "lengths_1_to_7", "uniform5", "two_three", "many_chunks"])
+@pytest.mark.parametrize("case", ["industrial7", "lengths_1_to_7", "uniform5", "two_three", "many_chunks", "industrial7_n2048"])
 def test_length_segment_clause_eval(case):
     """k_clause_seg (>= 1024 candidates, every K <= 7 instance but uniform
     3-SAT): clauses regrouped by length, L gathers and L + 1 bins per clause,
@@ -204,12 +204,31 @@ def test_length_segment_clause_eval(case):
     elif case == "two_three":
         base = planted_ksat(400, 900, 3, 3).clauses() + planted_ksat(400, 500, 2, 4).clauses()
         cnf, N = Cnf.from_clauses(400, base), 1024
-    else:
+    elif case == "many_chunks":
         cnf, N = industrial_cnf(3000, 40000, 3), 1024
+    else:                                                   # c4's shape class: the N = 2048 KB = 8 instantiation
+        cnf, N = industrial_cnf(900, 3600, 12), 2048
     state = random_state(cnf.V, N, seed=19)
     s, o = make_pair(cnf, N, 3, state=state, t0=0)
     for _ in range(4):
         compare_step(s, o, cnf, case)
+
+
+def test_uniform3_n1024_eight_plane_counters():
+    """Uniform 3-SAT at N = 1024 with one variable in 40 negated clauses (> 31
+    same-sign occurrences, < 128: not a hub) - the 8-plane counter path with
+    the compile-time N = 1024 instantiation (c3's shape).  Bit-exact."""
+    rng = np.random.default_rng(23)
+    cl = planted_ksat(400, 1600, 3, 23).clauses()
+    for i in range(40):
+        a, b = rng.choice(np.arange(2, 401), 2, replace=False)
+        cl.append([-1, int(a) * (1 if rng.random() < .5 else -1), int(b) * (1 if rng.random() < .5 else -1)])
+    cnf, N = Cnf.from_clauses(400, cl), 1024
+    state = random_state(cnf.V, N, seed=23)
+    s, o = make_pair(cnf, N, 4, state=state, t0=0)
+    assert s.info.n_hub_rows == 0
+    for _ in range(4):
+        compare_step(s, o, cnf, "uni3-n1024-cw8")
 
 
 @pytest.mark.parametrize("N", [128, 256, 384, 512])
