@@ -58,6 +58,9 @@ __device__ __forceinline__ void csa_add4(uint32_t (&c)[CB], uint32_t m0, uint32_
     }
 }
 
+#ifndef TSAT_CL_WIDE_FROM
+#define TSAT_CL_WIDE_FROM 8192     // the wide K <= 3 variant also from this many candidates per GPU (c5 N = 8192: k_clause 0.54 -> 0.35 ms; c2 N = 4096: +5 %)
+#endif
 #ifndef TSAT_CL_PERSM3
 #define TSAT_CL_PERSM3 3           // K <= 3: CTAs per SM the grid is sized for
 #endif
@@ -597,7 +600,7 @@ cudaError_t launch_clause(const StepArgs& a, const uint32_t* Acur, const StepSca
     const int nwb = (NW + 31) / 32;
     // sub-groups of NW lanes when a warp would leave lanes idle (N < 1024 per GPU);
     // a chunk (kCH clauses) must split evenly into carry-save groups per sub-group
-    const int wide = (a.mc.K <= 3 && a.N < 2048) ? 1 : 0;
+    const int wide = (a.mc.K <= 3 && (a.N < 2048 || a.N >= TSAT_CL_WIDE_FROM)) ? 1 : 0;
     const int kCH = chunk_clauses(a.mc.K <= 3 ? 3 : 7, wide);
     const int kGrp = 4 * (a.mc.K <= 3 ? TSAT_CL_G3 : 1);
     int nsub = NW < 32 ? 32 / NW : 1;
