@@ -58,6 +58,12 @@ __device__ __forceinline__ void csa_add4(uint32_t (&c)[CB], uint32_t m0, uint32_
     }
 }
 
+#ifndef TSAT_SEG_SHORT_CTAS
+#define TSAT_SEG_SHORT_CTAS 4        // k_clause_seg L <= 3: CTAs (256 threads) per SM it is compiled and sized for
+#endif
+#ifndef TSAT_SEG_LONG_CTAS
+#define TSAT_SEG_LONG_CTAS 2         // k_clause_seg L = 4..7
+#endif
 #ifndef TSAT_CL_WIDE_FROM
 #define TSAT_CL_WIDE_FROM 8192     // the wide K <= 3 variant also from this many candidates per GPU (c5 N = 8192: k_clause 0.54 -> 0.35 ms; c2 N = 4096: +5 %)
 #endif
@@ -486,7 +492,7 @@ __device__ __forceinline__ void seg_eval(const uint32_t* __restrict__ Aw, const 
 }
 
 template <int KB, int LMIN, int LMAX>
-__global__ void __launch_bounds__(256, LMAX <= 3 ? 4 : 2)
+__global__ void __launch_bounds__(256, LMAX <= 3 ? TSAT_SEG_SHORT_CTAS : TSAT_SEG_LONG_CTAS)
     k_clause_seg(const uint32_t* __restrict__ A, int NW, int V, const uint32_t* __restrict__ seg_lit, SegArgs sa,
                  int* __restrict__ hist, int N, DevScalars* __restrict__ ds, const StepScalars* __restrict__ sc,
                  int reset) {
@@ -564,7 +570,7 @@ static cudaError_t launch_clause_seg(const StepArgs& a, const uint32_t* Acur, co
             if (L >= lmin && L <= lmax) { ch += (a.seg_C[L] + seg_chunk(L) - 1) / seg_chunk(L); ncl += a.seg_C[L]; }
         }
         if (ch == 0) continue;
-        const int per_sm = part ? 2 : 4;
+        const int per_sm = part ? TSAT_SEG_LONG_CTAS : TSAT_SEG_SHORT_CTAS;
         long long gy = ((long long)a.num_sms * per_sm + nwb - 1) / nwb;
         const long long need = (ch + kWarps - 1) / kWarps;
         if (gy > need) gy = need;
